@@ -1,0 +1,659 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 transfer hot path (arXiv 1805.08430, static placement).
+
+Headline (BASELINE.json metric, configs[1] at its largest size): Send/Recv of a
+256 MiB fp32 tensor with static placement - kernel K1 puts payload + tail flag
+straight into the receiver's preallocated region, the receiver's consumer
+kernel K2 acquires the flag and clears it.
+
+* N = 1: sender server and receiver server both live on GPU 0 (local HBM put,
+  the paper's co-located servers).  N > 1 (torchrun, one process per GPU): a
+  ring - rank r puts into rank r+1's region over NVLink and consumes the
+  tensor rank r-1 put into its own; weak scaling, no collective on the data
+  path.
+* ``value``: payload GB/s of the whole job, inputs resident in HBM, device
+  time (CUDA events on the launching stream), max over ranks.  One step = one
+  batch of R transfers of the tensor (R calibrated so a step takes ~15 ms).
+* ``e2e``: same metric through the public API (StaticSender.send ->
+  StaticReceiver.poll -> ReduceMax consumer) with the payload copied from
+  pinned host memory every step and the consumer's result read back.
+* ``roofline``: K1 against HBM (N=1: reads S, writes S+1) or NVLink (N>1).
+* ``cpu_baseline``: the reference algorithm (oracle/port.py: ascending 1-4096 B
+  chunked delivery + flag poll + max) timed on this host's cores.
+
+``--impl reference`` times that CPU path alone (rank 0), same metric/config.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Send/Recv GB/s vs tensor size; PS steps/s at 1/2/4/8 B200 vs CPU ref"
+MIB = 1 << 20
+NVLINK_MEASURED_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction
+NVLINK_NOMINAL_GBS = 900.0
+HBM_FALLBACK_GBS = 6650.0     # B200_PROFILING.md fallback
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "B200_PROFILING.md fallback"
+
+
+# -- clocks during the timed region ------------------------------------------------------
+
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.15)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.06)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append((float(parts[1]), float(parts[2]), parts))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for _, _, p in rows for n, v in zip(names, p[5:9])
+                          if v.lower() == "active"})
+        load = [sm for sm, _, _ in rows]
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": max(m for _, m, _ in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# -- distributed helpers ----------------------------------------------------------------------
+
+
+def dist_max(x: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def dist_sum(x: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier_sync():
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if dist.is_initialized():
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# -- the device-resident Send/Recv ring ---------------------------------------------------------
+
+
+class SendRecvRing:
+    """Static-placement edge(s) for the timed device loop.  N=1: server 0 ->
+    server 1 on one GPU.  N>1: rank r -> rank r+1 over NVLink."""
+
+    def __init__(self, nbytes: int, rank: int, world: int, device: int):
+        from paper_1805_08430_b200 import _lib
+        from paper_1805_08430_b200.distributed import exchange_spaces, lookup, publish_addresses
+        from paper_1805_08430_b200.memspace import ArenaAllocator, MemorySpace
+        from paper_1805_08430_b200.wire import AddrExchangeMsg, Mechanism
+        self.lib = _lib
+        self.S = nbytes
+        self.world = world
+        slack = 8 * MIB
+        if world == 1:
+            self.src = MemorySpace(0, nbytes + 2 * slack, seed=0, device=device)
+            self.rcv = MemorySpace(1, nbytes + 2 * slack, seed=0, device=device)
+            a_src = ArenaAllocator(self.src, self.src.allocate_region(nbytes + slack, True))
+            a_rcv = ArenaAllocator(self.rcv, self.rcv.allocate_region(nbytes + slack, True))
+            _lib.call("srf_connect", self.src.handle, self.rcv.handle)
+            self.payload = a_src.alloc(nbytes)
+            self.flag = a_src.alloc(1)
+            self.recv = a_rcv.alloc(nbytes + 1)
+            self.dst = self.rcv
+            self.dst_region = (self.recv.base_addr, self.recv.access_token)
+        else:
+            self.src = MemorySpace(rank, 2 * nbytes + 2 * slack, seed=0, device=device)
+            arena = ArenaAllocator(self.src, self.src.allocate_region(2 * nbytes + slack, True))
+            self.payload = arena.alloc(nbytes)
+            self.flag = arena.alloc(1)
+            self.recv = arena.alloc(nbytes + 1)
+            self.rcv = self.src
+            nxt = (rank + 1) % world
+            self.proxies = exchange_spaces(self.src, peers=[nxt])
+            pub = publish_addresses([AddrExchangeMsg(rank, self.recv.base_addr,
+                                                     self.recv.access_token, self.recv.length,
+                                                     Mechanism.STATIC)])
+            msg = lookup(pub, nxt, nxt, Mechanism.STATIC)
+            self.dst = self.proxies[nxt]
+            self.dst_region = (msg.base_addr, msg.token)
+        self.src.write_at(self.flag, 0, b"\x01")
+        self.rcv.write_at(self.recv, nbytes, b"\x00")
+        # synthetic payload, generated on the device (uniform fp32 bit patterns)
+        import torch
+        view = self.src.view(self.payload, 0, nbytes)
+        g = torch.Generator(device=f"cuda:{device}")
+        g.manual_seed(1234 + rank)
+        view.view(torch.int32).copy_(torch.randint(-2**31, 2**31 - 1, (nbytes // 4,),
+                                                   dtype=torch.int32, device=f"cuda:{device}",
+                                                   generator=g))
+        torch.cuda.synchronize(device)
+        self.stream = C.c_void_p()
+        _lib.call("srf_stream_create", self.src.handle, C.byref(self.stream))
+        u = _lib.u64_array
+        self.args_addr = u([self.payload.base_addr, self.flag.base_addr])
+        self.args_len = u([nbytes, 1])
+        self.args_tok = u([self.payload.access_token, self.flag.access_token])
+
+    def put(self):
+        self.lib.call("srf_put", self.src.handle, self.args_addr, self.args_len, self.args_tok,
+                      2, self.dst.handle, self.dst_region[0], self.dst_region[1],
+                      self.lib.PUT_WAIT_EMPTY, self.stream, None)
+
+    def consume(self):
+        self.lib.call("srf_flag_wait", self.rcv.handle, self.recv.base_addr + self.S, 1, 1,
+                      10 * 10**9, self.stream)
+
+    def sync(self):
+        self.lib.call("srf_stream_sync", self.stream)
+        self.lib.call("srf_space_sync", self.src.handle)
+        self.lib.call("srf_space_sync", self.rcv.handle)
+
+    def event(self):
+        ev = C.c_void_p()
+        self.lib.call("srf_timing_event_create", self.src.handle, C.byref(ev))
+        return ev
+
+    def record(self, ev):
+        self.lib.call("srf_event_record_on", ev, self.stream)
+
+    def elapsed_ms(self, a, b) -> float:
+        ms = C.c_float()
+        self.lib.call("srf_event_elapsed_ms", a, b, C.byref(ms))
+        return ms.value
+
+    def verify(self) -> bool:
+        """The payload this rank received equals what its sender holds."""
+        import torch
+        got = self.rcv.view(self.recv, 0, self.S)
+        if self.world == 1:
+            want = self.src.view(self.payload, 0, self.S)
+            return bool(torch.equal(got, want))
+        # ring: rank r-1 put into us; compare digests across ranks
+        from paper_1805_08430_b200.distributed import all_gather_objects
+        import hashlib
+        mine = hashlib.sha256(self.src.view(self.payload, 0, self.S).cpu().numpy()).hexdigest()
+        recvd = hashlib.sha256(got.cpu().numpy()).hexdigest()
+        sent = all_gather_objects(mine)
+        import torch.distributed as dist
+        r = dist.get_rank()
+        return recvd == sent[(r - 1) % self.world]
+
+
+def bench_sendrecv_device(S, steps, warmup, rank, world, device):
+    from paper_1805_08430_b200 import _lib
+    ring = SendRecvRing(S, rank, world, device)
+    # calibrate rounds per step (identical on every rank: the ring is coupled)
+    a, b = ring.event(), ring.event()
+    barrier_sync()
+    ring.record(a)
+    for _ in range(4):
+        ring.put()
+        ring.consume()
+    ring.record(b)
+    ring.sync()
+    t_round = ring.elapsed_ms(a, b) / 4
+    rounds = int(dist_max(float(max(1, min(4096, round(15.0 / max(t_round, 1e-3)))))))
+    for _ in range(warmup * rounds):
+        ring.put()
+        ring.consume()
+    ring.sync()
+    n = steps * rounds
+    ev = [ring.event() for _ in range(2 * n)]
+    start, end = ring.event(), ring.event()
+    clocks = ClockSampler(device)
+    clocks.start()
+    barrier_sync()
+    ring.sync()
+    l0 = _lib.launch_count()
+    ring.record(start)
+    for i in range(n):
+        ring.record(ev[2 * i])
+        ring.put()
+        ring.record(ev[2 * i + 1])
+        ring.consume()
+    ring.record(end)
+    ring.sync()
+    launches = _lib.launch_count() - l0
+    barrier_sync()
+    clk = clocks.stop()
+    total_ms = dist_max(ring.elapsed_ms(start, end))
+    put_ms = [ring.elapsed_ms(ev[2 * i], ev[2 * i + 1]) for i in range(n)]
+    put_avg_ms = dist_max(statistics.fmean(put_ms))
+    ok = ring.verify()
+    ok = dist_sum(0.0 if ok else 1.0) == 0.0
+    launches = int(dist_sum(launches))
+    return {"total_ms": total_ms, "rounds": rounds, "n": n, "put_avg_ms": put_avg_ms,
+            "verified": ok, "launches": launches, "clocks": clk, "t_round_ms": t_round,
+            "ring": ring}
+
+
+# -- end to end through the public API ------------------------------------------------------
+
+
+class PublicApiEdge:
+    """One static edge built with the package's public API: spaces, arenas,
+    fabric devices, the analyzer's preallocation + address exchange (N=1) or
+    the IPC/address exchange of paper_1805_08430_b200.distributed (N>1), and
+    the StaticSender / StaticReceiver endpoints."""
+
+    def __init__(self, S, rank, world, device):
+        import torch
+        from paper_1805_08430_b200 import _lib
+        from paper_1805_08430_b200.analyzer import (PlanEntry, build_plan, classify_edges,
+                                                    preallocate_and_distribute)
+        from paper_1805_08430_b200.fabric import Fabric
+        from paper_1805_08430_b200.graph import Tensor, infer_shapes, partition, shape_of
+        from paper_1805_08430_b200.memspace import ArenaAllocator, BufferRef, MemorySpace
+        from paper_1805_08430_b200.runtime.protocol import StaticReceiver, StaticSender
+        from paper_1805_08430_b200.runtime.session import infer_elem_types
+        from paper_1805_08430_b200.wire import AddrExchangeMsg, ElemType, Mechanism
+        from paper_1805_08430_b200.workloads import build_microbench
+        self.lib = _lib
+        self.S = S
+        self.world = world
+        cap = S + 24 * MIB
+        fab = Fabric(seed=0)
+        if world == 1:
+            g, placement = build_microbench(S)
+            pg = partition(g, placement)
+            shapes = infer_shapes(g)
+            plan = build_plan(pg, shapes, classify_edges(pg, shapes), infer_elem_types(g))
+            spaces = {s: MemorySpace(s, cap, seed=0, device=device) for s in (0, 1)}
+            arenas = {s: ArenaAllocator(spaces[s], spaces[s].allocate_region(S + 16 * MIB, True))
+                      for s in (0, 1)}
+            devs = {s: fab.create_device(spaces[s], qps_per_peer=2) for s in (0, 1)}
+            fwd = devs[0].connect(devs[1].endpoint)
+            back = devs[1].channels_to(devs[0].endpoint)
+            chan = {(0, 1): fwd[0], (1, 0): back[0]}
+            preallocate_and_distribute(plan, spaces, arenas, devs, lambda a, b: chan[(a, b)])
+            entry = next(iter(plan.entries.values()))
+            self.src, self.dst_space = spaces[0], spaces[1]
+            src_arena, dst_arena = arenas[0], arenas[1]
+            data_channel = fwd[1]
+            recv_entry = entry
+        else:
+            from paper_1805_08430_b200.distributed import (exchange_spaces, lookup,
+                                                           publish_addresses)
+            nxt, prv = (rank + 1) % world, (rank - 1) % world
+            self.src = MemorySpace(rank, 2 * cap, seed=0, device=device)
+            src_arena = ArenaAllocator(self.src, self.src.allocate_region(2 * S + 16 * MIB, True))
+            dst_arena = src_arena
+            self.dst_space = self.src
+            shape = shape_of(S // 4)
+            recv_entry = PlanEntry(rank, prv, rank, Mechanism.STATIC, shape, ElemType.F32, 1)
+            rb = src_arena.alloc(S + 1)
+            self.src.write_at(rb, S, b"\x00")
+            recv_entry.recv_buffer = rb
+            proxies = exchange_spaces(self.src, peers=[nxt])
+            pub = publish_addresses([AddrExchangeMsg(rank, rb.base_addr, rb.access_token,
+                                                     rb.length, Mechanism.STATIC)])
+            msg = lookup(pub, nxt, nxt, Mechanism.STATIC)
+            entry = PlanEntry(nxt, rank, nxt, Mechanism.STATIC, shape, ElemType.F32, 1)
+            entry.remote_addr, entry.remote_token, entry.remote_len = \
+                msg.base_addr, msg.token, msg.region_len
+            local_dev = fab.create_device(self.src, qps_per_peer=2)
+            fab.create_device(proxies[nxt], qps_per_peer=2)
+            data_channel = local_dev.connect((nxt, 1))[1]
+        flag = src_arena.alloc(1)
+        self.src.write_at(flag, 0, b"\x01")
+        self.sender = StaticSender(entry, self.src, src_arena, data_channel, flag)
+        self.receiver = StaticReceiver(recv_entry, self.dst_space)
+        payload = src_arena.alloc(S)
+        self.tensor = Tensor((S // 4,), ElemType.F32, BufferRef(payload, src_arena),
+                             self.src.server_id)
+        self.out = dst_arena.alloc(8)
+        # host-side input, pinned (synthetic GenGrad values, graph.py:333-350 stream)
+        from paper_1805_08430_b200.graph import node_rng, synthesize_values
+        vals = synthesize_values((S // 4,), ElemType.F32, node_rng(rank, 0, 2))
+        self.host_in = torch.from_numpy(vals.view(np.uint8)).pin_memory()
+        self.host_np = self.host_in.numpy()
+        self.expect = float(vals.max())
+        self.prev_expect = None
+        if world > 1:
+            from paper_1805_08430_b200.distributed import all_gather_objects
+            self.prev_expect = all_gather_objects(self.expect)[(rank - 1) % world]
+
+    def step(self) -> float:
+        """H2D input -> send -> poll -> ReduceMax on the receiver -> D2H result."""
+        lib = self.lib
+        self.src.write_at(self.tensor.buffer.handle, 0, self.host_np)
+        self.sender.send(self.tensor, stage_copy=False)
+        got = None
+        while got is None:
+            got = self.receiver.poll()
+        lib.call("srf_reduce_max_f32", self.dst_space.handle, got.buffer.handle.base_addr,
+                 got.nbytes // 4, self.out.base_addr, None)
+        return float(np.frombuffer(self.dst_space.read_at(self.out, 0, 4), np.float32)[0])
+
+
+def bench_sendrecv_e2e(S, steps, warmup, rank, world, device):
+    import torch.distributed as dist
+    edge = PublicApiEdge(S, rank, world, device)
+    for _ in range(max(1, warmup)):
+        r = edge.step()
+        if dist.is_initialized():
+            dist.barrier()
+    want = edge.expect if world == 1 else edge.prev_expect
+    ok = r == want
+    barrier_sync()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        edge.step()
+        if dist.is_initialized():
+            dist.barrier()  # the protocol's iteration barrier (protocol.py:102-111)
+    barrier_sync()
+    t = dist_max(time.perf_counter() - t0)
+    ok = dist_sum(0.0 if ok else 1.0) == 0.0
+    return {"seconds": t, "verified": ok,
+            "h2d": S + 1,          # payload + the receiver's flag clear
+            "d2h": 4 + 1 + 1}      # result + the poll's flag read + the sender's check
+
+
+# -- CPU reference (oracle port) -----------------------------------------------------------------
+
+
+def cpu_reference(S, min_seconds=10.0, min_steps=3, max_steps=None):
+    from oracle import port
+    rig = port.MicrobenchRig(S, generate=False)
+    rig.step()  # warm
+    n, t0 = 0, time.perf_counter()
+    while True:
+        rig.step()
+        n += 1
+        dt = time.perf_counter() - t0
+        if (max_steps is not None and n >= max_steps) or (dt >= min_seconds and n >= min_steps):
+            break
+    return S * n / dt / 1e9, n, dt
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import port
+    S = args.bytes
+    rig = port.MicrobenchRig(S, generate=False)
+    for _ in range(args.warmup):
+        rig.step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        rig.step()
+    dt = time.perf_counter() - t0
+    gbps = S * args.steps / dt / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbps, 4), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(S, world),
+        "cpu_baseline": {"value": round(gbps, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+                         "sample": f"{args.steps} static Send/Recv steps of {S} B "
+                                   f"(ascending 1-4096 B chunked delivery + flag poll + max, "
+                                   f"oracle/port.py MicrobenchRig), host cpu_count="
+                                   f"{os.cpu_count()}"},
+        "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(S, world):
+    return {"workload": f"configs[1] static-placement Send/Recv, {S} B fp32 tensor "
+                        f"({'server 0 -> server 1 on one GPU' if world == 1 else 'ring rank r -> r+1 over NVLink'})",
+            "tensor_bytes": S, "mechanism": "static", "parallelism": f"ring{world}" if world > 1 else "pair-on-gpu0",
+            "l2": "inputs larger than L2 (126 MB)"}
+
+
+# -- size sweep (configs[1]) -----------------------------------------------------------------------
+
+
+def sweep(max_bytes, device):
+    """Static (device time, graph-replayed rounds) and dynamic (public API,
+    host-driven meta poll + pull) GB/s for 1 KiB x 4^k up to max_bytes, one GPU."""
+    from paper_1805_08430_b200 import _lib
+    out = []
+    size = 1024
+    while size <= max_bytes:
+        ring = SendRecvRing(size, 0, 1, device)
+        for _ in range(8):
+            ring.put()
+            ring.consume()
+        ring.sync()
+        rounds = 200 if size <= 4 * MIB else 20
+        graph = C.c_void_p()
+        _lib.call("srf_graph_begin", ring.stream)
+        for _ in range(rounds):
+            ring.put()
+            ring.consume()
+        _lib.call("srf_graph_end", ring.stream, C.byref(graph))
+        a, b = ring.event(), ring.event()
+        _lib.call("srf_graph_launch", graph, ring.stream)
+        ring.sync()
+        ring.record(a)
+        _lib.call("srf_graph_launch", graph, ring.stream)
+        ring.record(b)
+        ring.sync()
+        t = ring.elapsed_ms(a, b) / rounds / 1e3
+        _lib.call("srf_graph_destroy", graph)
+        dyn = dynamic_rate(size, device)
+        out.append({"bytes": size, "static_gbps": round(size / t / 1e9, 3),
+                    "static_us": round(t * 1e6, 3), **dyn})
+        size *= 4
+    return out
+
+
+def dynamic_rate(size, device, reps=None):
+    """Dynamic allocation through the endpoints: meta write (K3), receiver poll
+    + decode + arena alloc + one-sided pull (K4), buffer freed after use."""
+    from paper_1805_08430_b200.analyzer import PlanEntry
+    from paper_1805_08430_b200.fabric import Fabric
+    from paper_1805_08430_b200.graph import Tensor, shape_of
+    from paper_1805_08430_b200.memspace import ArenaAllocator, BufferRef, MemorySpace
+    from paper_1805_08430_b200.runtime.protocol import DynReceiver, DynSender
+    from paper_1805_08430_b200.wire import ElemType, Mechanism, meta_block_size
+    cap = 2 * size + 8 * MIB
+    fab = Fabric()
+    sp = {s: MemorySpace(s, cap, device=device) for s in (0, 1)}
+    ar = {s: ArenaAllocator(sp[s], sp[s].allocate_region(2 * size + 4 * MIB, True)) for s in (0, 1)}
+    dv = {s: fab.create_device(sp[s], qps_per_peer=2) for s in (0, 1)}
+    fwd = dv[0].connect(dv[1].endpoint)
+    back = dv[1].channels_to(dv[0].endpoint)
+    e = PlanEntry(0, 0, 1, Mechanism.DYNAMIC, shape_of(size // 4), ElemType.F32, 1)
+    mb = ar[1].alloc(meta_block_size(1))
+    sp[1].write_at(mb, mb.length - 1, b"\x00")
+    e.recv_buffer = mb
+    e.remote_addr, e.remote_token, e.remote_len = mb.base_addr, mb.access_token, mb.length
+    snd = DynSender(e, sp[0], ar[0], fwd[1])
+    rcv = DynReceiver(e, sp[1], ar[1], back[1])
+    t = Tensor((size // 4,), ElemType.F32, BufferRef(ar[0].alloc(size), ar[0]), 0)
+    reps = reps or (50 if size <= 4 * MIB else 10)
+
+    def one():
+        snd.send(t, stage_copy=False)
+        m = None
+        while m is None:
+            m = rcv.poll()
+        got = rcv.fetch(m)
+        got.buffer.release()
+
+    for _ in range(3):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        one()
+    dt = (time.perf_counter() - t0) / reps
+    snd.close()
+    for s in sp.values():
+        s.close()
+    return {"dynamic_gbps": round(size / dt / 1e9, 3), "dynamic_us": round(dt * 1e6, 2)}
+
+
+# -- main -------------------------------------------------------------------------------------------
+
+
+def main() -> int:
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--bytes", type=int, default=256 * MIB)
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from paper_1805_08430_b200.distributed import env_world
+    rank, world, local = env_world()
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import torch
+    from paper_1805_08430_b200 import _lib
+    from paper_1805_08430_b200.distributed import init_process_group
+    _lib.load()
+    torch.cuda.set_device(local)
+    init_process_group("nccl")
+    S = args.bytes
+
+    dev = bench_sendrecv_device(S, args.steps, args.warmup, rank, world, local)
+    e2e = bench_sendrecv_e2e(S, max(3, args.steps // 2), args.warmup, rank, world, local)
+
+    total_bytes = world * S * dev["n"]
+    value = total_bytes / (dev["total_ms"] / 1e3) / 1e9
+    hbm_peak, hbm_src = measured_peaks()
+    put_s = dev["put_avg_ms"] / 1e3
+    if world == 1:
+        alg = 2 * S + 1
+        roof = {"bound": "hbm", "achieved": round(alg / put_s / 1e9, 2), "peak": hbm_peak,
+                "unit": "GB/s", "frac": round(alg / put_s / 1e9 / hbm_peak, 4),
+                "kernel": "k_put (K1 static_put)", "bytes_per_launch": alg,
+                "peak_source": hbm_src}
+    else:
+        alg = S + 1
+        ach = alg / put_s / 1e9
+        roof = {"bound": "nvlink", "achieved": round(ach, 2), "peak": NVLINK_MEASURED_GBS,
+                "unit": "GB/s", "frac": round(ach / NVLINK_MEASURED_GBS, 4),
+                "frac_of_nominal_900": round(ach / NVLINK_NOMINAL_GBS, 4),
+                "kernel": "k_put (K1 static_put)", "bytes_per_launch": alg,
+                "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction "
+                               "(nominal 900)"}
+    roof["traffic"] = traffic_from_profiles(world)
+
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dev["total_ms"] / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {**workload_config(S, world), "rounds_per_step": dev["rounds"]},
+        "roofline": roof,
+        "e2e": {"value": round(world * S * max(3, args.steps // 2) / e2e["seconds"] / 1e9, 3),
+                "unit": "GB/s", "h2d_bytes_per_step": e2e["h2d"] * world,
+                "d2h_bytes_per_step": e2e["d2h"] * world,
+                "path": "StaticSender.send -> StaticReceiver.poll -> ReduceMax, pinned H2D in, "
+                        "4-B result D2H", "verified": e2e["verified"]},
+        "gpu_launches": dev["launches"],
+        "clocks": dev["clocks"],
+        "verified": dev["verified"],
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        gbps, n, dt = cpu_reference(S, min_seconds=args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": round(gbps, 4), "unit": "GB/s", "cores": 1, "kind": "port",
+            "sample": f"{n} steps x {S} B static Send/Recv (oracle/port.py MicrobenchRig: "
+                      f"ascending 1-4096 B chunk delivery + flag poll + max), {dt:.1f} s, "
+                      f"host cpu_count={os.cpu_count()}"}
+    if world == 1 and not args.no_sweep:
+        line["sweep"] = sweep(S, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if not dev["verified"] or not e2e["verified"]:
+        log("verification FAILED")
+        return 1
+    return 0
+
+
+def traffic_from_profiles(world):
+    """dram bytes per K1 launch from the committed ncu --set full capture."""
+    path = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(str(world))
+    except Exception:
+        return None
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,193 @@
+/*
+ * srflow.h - C ABI of the B200-native transfer hot path (libsrflow.so).
+ *
+ * The reference (rdmaflow, /root/reference/pkg/src/rdmaflow) has no FFI: its
+ * boundary is a Python class API.  Every entry point below replaces one
+ * reference method on that path; the citation after each declaration names
+ * the method (paths relative to pkg/src/rdmaflow/).  All functions return an
+ * srf_status (0 = OK); the message of the last failure on the calling thread
+ * is available from srf_last_error().  Status codes map 1:1 onto the
+ * reference exception classes in errors.py (see SRF_E_* below).
+ *
+ * Addresses are space-relative byte offsets, exactly like the reference's
+ * flat-space addresses (memspace.py:89-133); the device pointer of an address
+ * is base + addr.  No torch types cross this boundary.
+ */
+#ifndef SRFLOW_H
+#define SRFLOW_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py class each maps onto) ---------------------- */
+enum srf_status {
+    SRF_OK = 0,
+    SRF_PENDING = 1,             /* not an error: event / flag not ready yet   */
+    SRF_E_ZERO_LENGTH = 10,      /* errors.ZeroLength          errors.py:9      */
+    SRF_E_OUT_OF_MEMORY = 11,    /* errors.OutOfMemory         errors.py:13     */
+    SRF_E_OUT_OF_BOUNDS = 12,    /* errors.OutOfBounds         errors.py:21     */
+    SRF_E_NOT_REGISTERED = 13,   /* errors.NotRegistered       errors.py:35     */
+    SRF_E_BAD_TOKEN = 14,        /* errors.BadToken            errors.py:39     */
+    SRF_E_REMOTE_OOB = 15,       /* errors.RemoteOutOfBounds   errors.py:43     */
+    SRF_E_INVALID_LENGTH = 16,   /* errors.InvalidLength       errors.py:47     */
+    SRF_E_TIMEOUT = 17,          /* errors.Timeout             errors.py:59     */
+    SRF_E_PEER_UNREACHABLE = 18, /* errors.PeerUnreachable     errors.py:31     */
+    SRF_E_INVALID_CONFIG = 19,   /* errors.InvalidConfig       errors.py:103    */
+    SRF_E_SHAPE_MISMATCH = 20,   /* errors.ShapeMismatch       errors.py:95     */
+    SRF_E_PROTOCOL = 21,         /* errors.ProtocolError       errors.py:116    */
+    SRF_E_DEVICE = 22            /* CUDA failure -> errors.RdmaFlowError        */
+};
+
+typedef struct srf_space  *srf_space_t;   /* one server's HBM pool          */
+typedef struct srf_stream *srf_stream_t;  /* one queue pair's CUDA stream   */
+typedef struct srf_event  *srf_event_t;   /* one verb's completion          */
+
+/* ---- library -------------------------------------------------------------- */
+const char *srf_last_error(void);
+int srf_version(void);
+int srf_device_count(int *count);
+/* number of sm_100a kernels this library launched since load */
+uint64_t srf_launch_count(void);
+
+/* ---- memory spaces (memspace.py) ----------------------------------------- */
+/* MemorySpace.__init__ (memspace.py:98-113): one cudaMalloc(capacity) on
+ * cuda_device, zero-filled like np.zeros. */
+int srf_space_create(int server_id, int cuda_device, uint64_t capacity,
+                     uint32_t max_regions, srf_space_t *out);
+int srf_space_destroy(srf_space_t space);
+int srf_space_info(srf_space_t space, int *server_id, int *cuda_device,
+                   uint64_t *capacity, void **device_base);
+/* the space's default stream (local compute, byte IO) as cudaStream_t */
+void *srf_space_cuda_stream(srf_space_t space);
+
+/* MemorySpace.allocate_region (memspace.py:116-133): bump allocation, 8-B
+ * aligned base.  The 64-bit access token is supplied by the host so its
+ * random stream stays identical to the reference's. */
+int srf_region_alloc(srf_space_t space, uint64_t length, int registered,
+                     uint64_t token, int64_t *region_id, uint64_t *base);
+int srf_region_count(srf_space_t space, uint32_t *count);
+int srf_next_addr(srf_space_t space, uint64_t *next_addr);
+/* MemorySpace.check_remote_access (memspace.py:145-157) */
+int srf_check_remote(srf_space_t space, uint64_t addr, uint64_t length,
+                     uint64_t token);
+/* MemorySpace.check_registered (memspace.py:159-167) */
+int srf_check_registered(srf_space_t space, uint64_t addr, uint64_t length,
+                         uint64_t token);
+
+/* MemorySpace.read_at/read_raw (memspace.py:180-198), D2H, synchronous */
+int srf_read(srf_space_t space, uint64_t addr, uint64_t length, void *host_dst);
+/* MemorySpace.write_at/write_raw (memspace.py:184-219), H2D, synchronous */
+int srf_write(srf_space_t space, uint64_t addr, uint64_t length,
+              const void *host_src);
+/* H2D from caller-pinned memory, asynchronous on `stream` (NULL = default) */
+int srf_write_async(srf_space_t space, uint64_t addr, uint64_t length,
+                    const void *host_src, srf_stream_t stream);
+int srf_read_async(srf_space_t space, uint64_t addr, uint64_t length,
+                   void *host_dst, srf_stream_t stream);
+/* MemorySpace.view (memspace.py:188-194): device pointer of an address */
+int srf_device_ptr(srf_space_t space, uint64_t addr, void **dptr);
+/* wait for all work on the space's default stream; reports device timeouts */
+int srf_space_sync(srf_space_t space);
+
+/* ---- peers (fabric.py RdmaDevice.connect, fabric.py:286-303) ----------- */
+/* enable NVLink peer access between the two spaces' GPUs (both directions) */
+int srf_connect(srf_space_t a, srf_space_t b);
+/* multi-process: export the pool (cudaIpcGetMemHandle, 64 bytes) and map a
+ * peer's exported pool as a remote space proxy; the proxy's region table is
+ * filled with srf_region_import so remote checks stay identical. */
+int srf_space_export(srf_space_t space, void *handle64);
+int srf_space_import(const void *handle64, int server_id, int local_device,
+                     uint64_t capacity, srf_space_t *out);
+int srf_region_import(srf_space_t proxy, int64_t region_id, uint64_t base,
+                      uint64_t length, int registered, uint64_t token);
+
+/* ---- streams and completions (fabric.py CompletionQueue/_finish_verb) --- */
+int srf_stream_create(srf_space_t space, srf_stream_t *out);
+int srf_stream_destroy(srf_stream_t stream);
+void *srf_stream_cuda(srf_stream_t stream);
+int srf_stream_sync(srf_stream_t stream);
+int srf_event_record(srf_space_t space, srf_stream_t stream, srf_event_t *out);
+/* SRF_OK when complete, SRF_PENDING otherwise (Channel.take_completion poll) */
+int srf_event_query(srf_event_t ev);
+int srf_event_wait(srf_event_t ev);
+int srf_event_free(srf_event_t ev);
+
+/* CUDA-graph capture of a stream's launches (many-small-transfer steps are
+ * launch-bound: SURVEY.md H5) and timing events for the benchmark. */
+int srf_graph_begin(srf_stream_t stream);
+int srf_graph_end(srf_stream_t stream, void **graph_exec);
+int srf_graph_launch(void *graph_exec, srf_stream_t stream);
+int srf_graph_destroy(void *graph_exec);
+int srf_stream_wait_event(srf_stream_t stream, srf_event_t ev);
+int srf_timing_event_create(srf_space_t space, srf_event_t *out);
+int srf_event_record_on(srf_event_t ev, srf_stream_t stream);
+int srf_event_elapsed_ms(srf_event_t start, srf_event_t end, float *ms);
+
+/* ---- verbs: the hot path ------------------------------------------------- */
+/* Channel.one_sided_write (fabric.py:349-369) + _deliver_chunks (:391-421).
+ * K1 static_put / K3 meta_put.  Gathers nseg local registered ranges
+ * (src_addr[i], src_len[i], src_token[i]) of src_space into
+ * [dst_addr, dst_addr + sum(len)) of dst_space.  Every byte but the last is
+ * written by 16-B vector stores from all CTAs; after a system-scope fence and
+ * a grid arrival count the last CTA writes the final byte (the tail flag of
+ * wire.py:74-76 / :112-116) with st.release.sys, so an observed flag implies a
+ * complete payload - the guarantee ascending delivery gave the reference.
+ * flags: SRF_PUT_WAIT_EMPTY makes every CTA acquire-spin until the remote
+ * tail byte reads 0x00 (receiver consumed) before writing.
+ * ev_out may be NULL. */
+#define SRF_PUT_WAIT_EMPTY 0x1
+int srf_put(srf_space_t src_space, const uint64_t *src_addr,
+            const uint64_t *src_len, const uint64_t *src_token, int nseg,
+            srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
+            int flags, srf_stream_t stream, srf_event_t *ev_out);
+/* Channel.one_sided_read (fabric.py:371-389).  K4 peer_pull: launched on the
+ * reader's GPU, loads [src_addr, +length) from the peer pool, stores into the
+ * local registered range dst_addr. */
+int srf_get(srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
+            srf_space_t src_space, uint64_t src_addr, uint64_t src_token,
+            uint64_t length, srf_stream_t stream, srf_event_t *ev_out);
+/* MemorySpace.copy_bytes (memspace.py:223-236).  K5 stage_copy, local D2D. */
+int srf_copy(srf_space_t space, uint64_t src_addr, uint64_t dst_addr,
+             uint64_t length, srf_stream_t stream, srf_event_t *ev_out);
+/* StaticReceiver.poll (runtime/protocol.py:124-138) as a device consumer
+ * prologue.  K2 flag_wait: one warp acquire-spins on the byte at flag_addr
+ * until it equals `expect`, then (clear != 0) stores 0x00.  Bounded by
+ * timeout_ns; a timeout is reported by the next srf_space_sync. */
+int srf_flag_wait(srf_space_t space, uint64_t flag_addr, uint8_t expect,
+                  int clear, uint64_t timeout_ns, srf_stream_t stream);
+
+/* Device consumer used by the release/acquire stress test and the
+ * microbenchmark: thread 0 acquire-spins on flag_addr (== 0x01), then the
+ * CTA computes sum(data[i] * (i % 251 + 1)) over n bytes into the u64 at
+ * out_addr and clears the flag.  Same bounded-timeout reporting as K2. */
+int srf_consume_checksum(srf_space_t space, uint64_t flag_addr, uint64_t data_addr,
+                         uint64_t n, uint64_t out_addr, uint64_t timeout_ns,
+                         srf_stream_t stream);
+
+/* graph.py apply_in_place (graph.py:392-405) for W workers in one pass.
+ * K6 ps_apply:  op SRF_APPLY_XOR: var ^= g_0 ^ ... ^ g_{W-1} (bytewise)
+ *               op SRF_APPLY_SGD: var = (((var - lr*g_0) - lr*g_1) ...) fp32,
+ *                                 every product and difference rounded
+ *                                 separately (no FMA contraction).
+ * Gradients may live in peer pools (fused pull + apply). */
+#define SRF_APPLY_XOR 0
+#define SRF_APPLY_SGD 1
+#define SRF_MAX_WORKERS 16
+int srf_apply(srf_space_t var_space, uint64_t var_addr, uint64_t nbytes,
+              srf_space_t const *grad_spaces, const uint64_t *grad_addrs,
+              int nworkers, int op, float lr, srf_stream_t stream,
+              srf_event_t *ev_out);
+
+/* ReduceMax consumer of the microbenchmark (graph.py:378-382) on the
+ * receiving GPU: out_addr receives max over n fp32 at in_addr. */
+int srf_reduce_max_f32(srf_space_t space, uint64_t in_addr, uint64_t n,
+                       uint64_t out_addr, srf_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SRFLOW_H */

@@ -1,0 +1,477 @@
+"""CPU restatement of the reference transfer path (TEST INFRASTRUCTURE ONLY).
+
+Every function follows the reference (rdmaflow, /root/reference/pkg/src/
+rdmaflow) at the cited file:line.  Bytes live in numpy ``uint8`` arrays and
+one-sided verbs deliver in ascending random chunks of 1..4096 bytes exactly
+like the reference fabric, so this module doubles as the CPU baseline that
+``bench.py`` times (``cpu_baseline.kind = "port"``).
+"""
+from __future__ import annotations
+
+import math
+import random
+import struct
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+FLAG_EMPTY, FLAG_READY = 0, 1
+ELEM_SIZE = {0: 4, 1: 8, 2: 4, 3: 8, 4: 1}          # wire.py:52-53
+ELEM_DTYPE = {0: "<f4", 1: "<f8", 2: "<i4", 3: "<i8", 4: "u1"}
+MAX_CHUNK = 4096                                     # fabric.py:29
+
+
+# -- wire layouts (wire.py:67-142, :145-171) ------------------------------------
+
+
+def meta_block_size(rank: int) -> int:                       # wire.py:79-81
+    return 8 * rank + 33
+
+
+def encode_meta(dims: Sequence[int], elem: int, addr: int, token: int) -> bytes:
+    """wire.py:99-117: head <BB6x, dims <Q*, trailer <QQQB (flag 0x01 last)."""
+    dims = [int(d) for d in dims]
+    plen = math.prod(dims) * ELEM_SIZE[elem]
+    return (struct.pack("<BB6x", elem, len(dims)) + struct.pack(f"<{len(dims)}Q", *dims)
+            + struct.pack("<QQQB", addr, token, plen, FLAG_READY))
+
+
+def decode_meta(raw: bytes, rank: int) -> tuple[tuple[int, ...], int, int, int, int]:
+    """wire.py:120-142 (validation subset): (dims, elem, addr, token, payload_len)."""
+    assert raw[1] == rank and len(raw) == meta_block_size(rank) and raw[-1] == FLAG_READY
+    dims = struct.unpack_from(f"<{rank}Q", raw, 8)
+    addr, token, plen = struct.unpack_from("<QQQ", raw, 8 + 8 * rank)
+    return tuple(dims), raw[0], addr, token, plen
+
+
+def addr_msg(edge_id: int, base: int, token: int, length: int, mech: int) -> bytes:
+    return struct.pack("<QQQQB", edge_id, base, token, length, mech)  # wire.py:159-161
+
+
+# -- deterministic values (graph.py:333-350) -----------------------------------------
+
+
+def node_rng(seed: int, node_id: int, iteration: int) -> np.random.Generator:
+    mix = ((seed & 0xFFFFFFFF) * 1_000_003 + node_id) * 1_000_033 + iteration
+    return np.random.Generator(np.random.PCG64(mix & 0xFFFFFFFFFFFFFFFF))
+
+
+def synthesize(n: int, elem: int, rng: np.random.Generator) -> np.ndarray:
+    if elem == 0:
+        return rng.random(n, dtype=np.float32)
+    if elem == 1:
+        return rng.random(n, dtype=np.float64)
+    if elem == 4:
+        return rng.integers(0, 256, size=n, dtype=np.uint8)
+    return rng.integers(-1000, 1000, size=n).astype(ELEM_DTYPE[elem])
+
+
+# -- memory (memspace.py:89-308) -----------------------------------------------------
+
+
+class Space:
+    """Flat byte memory with a bump region table and seeded tokens."""
+
+    def __init__(self, server_id: int, capacity: int, seed: int = 0):
+        self.server_id = server_id
+        self.mem = np.zeros(capacity, dtype=np.uint8)          # memspace.py:108
+        self.next_addr = 0
+        self.regions: list[tuple[int, int, bool, int]] = []    # base, len, reg, token
+        self.rng = random.Random(((seed & 0xFFFFFFFF) << 20)
+                                 ^ (server_id * 0x9E3779B1) ^ 0x5EED)  # :113
+
+    def allocate_region(self, length: int, register: bool = False) -> tuple[int, int]:
+        base = (self.next_addr + 7) & ~7                       # memspace.py:122
+        assert base + length <= len(self.mem), "OutOfMemory"
+        token = self.rng.getrandbits(64) if register else 0    # :128
+        self.regions.append((base, length, register, token))
+        self.next_addr = base + length
+        return base, token
+
+    def check_remote(self, addr: int, length: int, token: int) -> None:  # :145-157
+        for base, ln, reg, tok in self.regions:
+            if reg and base <= addr and addr + length <= base + ln:
+                assert tok == token, "BadToken"
+                return
+        raise AssertionError("RemoteOutOfBounds")
+
+
+class Arena:
+    """First-fit, 8-B reserved lengths, coalescing (memspace.py:239-308)."""
+
+    def __init__(self, base: int, length: int, token: int):
+        self.base, self.token = base, token
+        self.free_list = [(0, length & ~7)]
+        self.live: dict[int, int] = {}
+        self.resident = 0
+
+    def alloc(self, n: int) -> int:
+        need = (n + 7) & ~7
+        for i, (off, ln) in enumerate(self.free_list):
+            if ln >= need:
+                if ln == need:
+                    del self.free_list[i]
+                else:
+                    self.free_list[i] = (off + need, ln - need)
+                self.live[self.base + off] = need
+                self.resident += n
+                return self.base + off
+        raise AssertionError("ArenaExhausted")
+
+    def free(self, addr: int, n: int) -> None:
+        need = self.live.pop(addr)
+        off = addr - self.base
+        self.free_list.append((off, need))
+        self.free_list.sort()
+        merged: list[tuple[int, int]] = []
+        for o, ln in self.free_list:
+            if merged and merged[-1][0] + merged[-1][1] == o:
+                merged[-1] = (merged[-1][0], merged[-1][1] + ln)
+            else:
+                merged.append((o, ln))
+        self.free_list = merged
+        self.resident -= n
+
+
+# -- one-sided verbs (fabric.py:218-246, :349-421) --------------------------------------
+
+
+class Delivery:
+    """Ascending chunked delivery of one-sided verbs."""
+
+    def __init__(self, seed: int = 0, max_chunk: int = MAX_CHUNK):
+        self.rng = random.Random(seed ^ 0xFAB51C)              # fabric.py:176
+        self.max_chunk = max_chunk
+        self.wire_bytes = 0
+        self.verbs = 0
+
+    def chunk_plan(self, total: int) -> list[int]:           # fabric.py:218-246
+        mc = self.max_chunk
+        plan: list[int] = []
+        covered = 0
+        if total <= mc:
+            first = self.rng.randint(1, mc)
+            if first >= total:
+                return [total]
+            plan, covered = [first], first
+        g = np.random.Generator(np.random.PCG64(self.rng.getrandbits(64)))
+        while covered < total:
+            need = max(8, int((total - covered) * 2 / (mc + 1)) + 8)
+            for size in g.integers(1, mc + 1, size=need):
+                size = int(min(size, total - covered))
+                plan.append(size)
+                covered += size
+                if covered >= total:
+                    break
+        return plan
+
+    def _deliver(self, segments: list[np.ndarray], total: int, target: Space,
+                 base: int) -> None:                          # fabric.py:391-421
+        segs = iter(segments)
+        seg = next(segs, None)
+        spos = pos = 0
+        for size in self.chunk_plan(total):
+            while size:
+                take = min(size, len(seg) - spos)
+                target.mem[base + pos:base + pos + take] = seg[spos:spos + take]
+                spos += take
+                pos += take
+                size -= take
+                if spos == len(seg):
+                    seg, spos = next(segs, None), 0
+        self.verbs += 1
+        self.wire_bytes += total
+
+    def write(self, src: Space, ranges: list[tuple[int, int]], dst: Space,
+              dst_addr: int, dst_token: int) -> None:         # fabric.py:349-369
+        total = sum(n for _a, n in ranges)
+        assert total >= 1, "InvalidLength"
+        dst.check_remote(dst_addr, total, dst_token)
+        self._deliver([src.mem[a:a + n] for a, n in ranges if n], total, dst, dst_addr)
+
+    def read(self, dst: Space, dst_addr: int, src: Space, src_addr: int,
+             src_token: int, n: int) -> None:                 # fabric.py:371-389
+        assert n >= 1, "InvalidLength"
+        src.check_remote(src_addr, n, src_token)
+        self._deliver([src.mem[src_addr:src_addr + n]], n, dst, dst_addr)
+
+
+# -- protocol endpoints (runtime/protocol.py:49-254) ------------------------------------
+
+
+def static_send(fab: Delivery, src: Space, payload: tuple[int, int], flag_cell: int,
+                dst: Space, region: tuple[int, int, int]) -> None:
+    """protocol.py:63-91: flag must be clear; one gather write [payload, flag]."""
+    addr, length, token = region
+    assert payload[1] == length - 1, "SizeMismatch"
+    assert dst.mem[addr + length - 1] == FLAG_EMPTY, "receiver has not consumed"
+    ranges = ([payload] if payload[1] else []) + [(flag_cell, 1)]
+    fab.write(src, ranges, dst, addr, token)
+
+
+def static_poll(dst: Space, region: tuple[int, int, int]) -> Optional[np.ndarray]:
+    """protocol.py:124-138: flag set -> clear it, hand out the payload view."""
+    addr, length, _tok = region
+    if dst.mem[addr + length - 1] != FLAG_READY:
+        return None
+    dst.mem[addr + length - 1] = FLAG_EMPTY
+    return dst.mem[addr:addr + length - 1]
+
+
+def dyn_send(fab: Delivery, src: Space, meta_stage: int, dims, elem: int,
+             payload_addr: int, payload_token: int, dst: Space,
+             meta_region: tuple[int, int, int]) -> bytes:
+    """protocol.py:163-201: encode meta, stage it, one write; payload stays."""
+    maddr, mlen, mtok = meta_region
+    meta = encode_meta(dims, elem, payload_addr, payload_token)
+    assert dst.mem[maddr + mlen - 1] == FLAG_EMPTY, "receiver has not consumed"
+    src.mem[meta_stage:meta_stage + len(meta)] = np.frombuffer(meta, np.uint8)
+    fab.write(src, [(meta_stage, len(meta))], dst, maddr, mtok)
+    return meta
+
+
+def dyn_poll_fetch(fab: Delivery, dst: Space, arena: Arena, meta_region, rank: int,
+                   src: Space) -> Optional[tuple[int, int, tuple[int, ...]]]:
+    """protocol.py:234-254: poll meta, clear, decode, alloc, one-sided read.
+    Returns (local addr, payload_len, dims) of the pulled block."""
+    maddr, mlen, _ = meta_region
+    raw = dst.mem[maddr:maddr + mlen].tobytes()
+    if raw[-1] != FLAG_READY:
+        return None
+    dst.mem[maddr + mlen - 1] = FLAG_EMPTY
+    dims, _elem, addr, token, plen = decode_meta(raw, rank)
+    if plen == 0:
+        return (0, 0, dims)
+    local = arena.alloc(plen)
+    fab.read(dst, local, src, addr, token, plen)
+    return (local, plen, dims)
+
+
+# -- parameter-server update (graph.py:392-402) + SGD restatement ------------------------
+
+
+def apply_xor(var: np.ndarray, grads: Sequence[np.ndarray]) -> np.ndarray:
+    """graph.py:400-402, applied once per worker in ascending node id."""
+    t = var.reshape(-1).view(np.uint8)
+    for g in grads:
+        t ^= np.ascontiguousarray(g).reshape(-1).view(np.uint8)
+    return var
+
+
+def apply_sgd(var: np.ndarray, grads: Sequence[np.ndarray], lr: float) -> np.ndarray:
+    """North-star SGD (no reference implementation; parity unpinned):
+    var = var - lr * g per worker in ascending order, fp32, separately
+    rounded product and difference (numpy never contracts to FMA)."""
+    lr32 = np.float32(lr)
+    for g in grads:
+        prod = (lr32 * g.astype(np.float32, copy=False)).astype(np.float32)
+        var[...] = (var - prod).astype(np.float32)
+    return var
+
+
+def ps_node_ids(v: int, w: int, workers: int) -> tuple[int, int, int]:
+    """workloads.py:81-93 node order: (variable, GenGrad, ApplyGrad)."""
+    var = v * (1 + 2 * workers)
+    return var, var + 1 + 2 * w, var + 2 + 2 * w
+
+
+def ps_expected(shapes: Sequence[tuple[int, ...]], workers: int, seed: int, steps: int,
+                op: str = "xor", lr: float = 0.01, elem: int = 0) -> list[np.ndarray]:
+    """Variable values after ``steps`` PS iterations:
+    init = synth(node_rng(seed, var, 0)); each step, each worker's gradient
+    synth(node_rng(seed, gen(v, w), it)) is folded in ascending w."""
+    out = []
+    for v, dims in enumerate(shapes):
+        n = math.prod(dims)
+        var_id = ps_node_ids(v, 0, workers)[0]
+        val = synthesize(n, elem, node_rng(seed, var_id, 0)).copy()
+        for it in range(1, steps + 1):
+            grads = [synthesize(n, elem, node_rng(seed, ps_node_ids(v, w, workers)[1], it))
+                     for w in range(workers)]
+            if op == "xor":
+                apply_xor(val, grads)
+            else:
+                apply_sgd(val, grads, lr)
+        out.append(val.reshape(dims))
+    return out
+
+
+# -- timed reference workloads (the CPU baseline) -----------------------------------------
+
+
+@dataclass
+class MicrobenchRig:
+    """One steady-state iteration of the reference microbenchmark session
+    (workloads.py:11-28 under session.py:606-629, zerocp, iteration >= 2):
+    GenGrad synthesises the payload into registered memory, the static send
+    delivers payload + flag in ascending chunks, the receiver polls and runs
+    ReduceMax.  ``step`` returns the ReduceMax value."""
+
+    nbytes: int
+    seed: int = 0
+    #: False: the payload is synthesised once (a host-resident input, as the
+    #: GPU end-to-end measurement uses) and each step only moves + consumes it
+    generate: bool = True
+
+    def __post_init__(self):
+        cap = 2 * self.nbytes + (1 << 20)
+        self.fab = Delivery(self.seed)
+        self.src, self.dst = Space(0, cap, self.seed), Space(1, cap, self.seed)
+        self.payload, self.ptok = self.src.allocate_region(max(self.nbytes, 1), True)
+        self.flag, _ = self.src.allocate_region(1, True)
+        self.src.mem[self.flag] = FLAG_READY
+        raddr, rtok = self.dst.allocate_region(self.nbytes + 1, True)
+        self.region = (raddr, self.nbytes + 1, rtok)
+        self.it = 1
+        if not self.generate:
+            self._fill(2)
+
+    def _fill(self, it: int) -> None:
+        n = self.nbytes // 4
+        vals = synthesize(n, 0, node_rng(self.seed, 0, it))
+        self.src.mem[self.payload:self.payload + 4 * n] = vals.view(np.uint8)
+
+    def step(self) -> float:
+        self.it += 1
+        n = self.nbytes // 4
+        if self.generate:
+            self._fill(self.it)
+        static_send(self.fab, self.src, (self.payload, self.nbytes), self.flag,
+                    self.dst, self.region)
+        got = static_poll(self.dst, self.region)
+        assert got is not None
+        return float(np.max(got.view(np.float32))) if n else 0.0
+
+
+class TransferRig:
+    """Transfer-only reference path (the Rig harness, tests/test_protocol.py:15-71):
+    static send + poll, or dynamic meta send + poll + pull, of one resident
+    payload.  ``step`` returns the received bytes' location."""
+
+    def __init__(self, nbytes: int, mechanism: str = "static", seed: int = 5):
+        cap = 2 * nbytes + (1 << 20)
+        self.n = nbytes
+        self.mech = mechanism
+        self.fab = Delivery(seed)
+        self.src, self.dst = Space(0, cap, 0), Space(1, cap, 1)
+        base0, tok0 = self.src.allocate_region(cap // 2, True)
+        base1, tok1 = self.dst.allocate_region(cap // 2, True)
+        self.arena0, self.arena1 = Arena(base0, cap // 2, tok0), Arena(base1, cap // 2, tok1)
+        self.flag = self.arena0.alloc(1)
+        self.src.mem[self.flag] = FLAG_READY
+        self.payload = self.arena0.alloc(max(nbytes, 1))
+        self.src.mem[self.payload:self.payload + nbytes] = (
+            np.random.default_rng(42).integers(0, 256, nbytes, dtype=np.uint8))
+        if mechanism == "static":
+            a = self.arena1.alloc(nbytes + 1)
+            self.region = (a, nbytes + 1, tok1)
+        else:
+            a = self.arena1.alloc(meta_block_size(1))
+            self.region = (a, meta_block_size(1), tok1)
+            self.meta_stage = self.arena0.alloc(meta_block_size(1))
+            self.tok0 = tok0
+        self.last = None
+
+    def step(self):
+        if self.mech == "static":
+            static_send(self.fab, self.src, (self.payload, self.n), self.flag,
+                        self.dst, self.region)
+            got = static_poll(self.dst, self.region)
+            assert got is not None
+            return self.region[0]
+        if self.last is not None:
+            self.arena1.free(*self.last)
+        dyn_send(self.fab, self.src, self.meta_stage, (self.n,), 4, self.payload,
+                 self.tok0, self.dst, self.region)
+        local, plen, _ = dyn_poll_fetch(self.fab, self.dst, self.arena1, self.region, 1,
+                                        self.src)
+        self.last = (local, plen)
+        return local
+
+
+class PsRig:
+    """One steady-state PS iteration of the reference (session.py:606-629 over
+    build_ps_workload, zerocp, iteration >= 2) for the given variable shapes and
+    server placement: per variable, static weight pushes to every worker on
+    another server, synthetic gradients, dynamic meta + pull back to the shard,
+    then the ApplyGrads in ascending worker order (XOR, or the SGD
+    restatement)."""
+
+    def __init__(self, shapes, workers: int, shards: int, colocate: bool,
+                 seed: int = 0, op: str = "xor", lr: float = 0.01):
+        self.shapes = [tuple(s) for s in shapes]
+        self.W, self.P, self.coloc = workers, shards, colocate
+        self.seed, self.op, self.lr = seed, op, lr
+        nsrv = workers if colocate else workers + shards
+        sizes = [4 * math.prod(s) for s in self.shapes]
+        cap = 4 * sum(sizes) + (8 << 20)
+        self.fab = Delivery(seed)
+        self.spaces = [Space(s, cap, seed) for s in range(nsrv)]
+        self.arenas = []
+        for sp in self.spaces:
+            b, t = sp.allocate_region(cap - 64, True)
+            self.arenas.append(Arena(b, cap - 64, t))
+        self.flags = []
+        for sp, ar in zip(self.spaces, self.arenas):
+            f = ar.alloc(1)
+            sp.mem[f] = FLAG_READY
+            self.flags.append(f)
+        self.vars = []     # (server, addr, nbytes)
+        self.wbuf = {}     # (v, w) -> static recv region on worker w
+        self.meta = {}     # (v, w) -> meta block region on the shard
+        self.grad = {}     # (v, w) -> gradient buffer on worker w
+        self.stage = {}
+        for v, nb in enumerate(sizes):
+            shard = (v % shards) + (0 if colocate else workers)
+            a = self.arenas[shard].alloc(nb)
+            n = nb // 4
+            init = synthesize(n, 0, node_rng(seed, ps_node_ids(v, 0, workers)[0], 0))
+            self.spaces[shard].mem[a:a + nb] = init.view(np.uint8)
+            self.vars.append((shard, a, nb))
+            for w in range(workers):
+                if w == shard:
+                    continue
+                tok = self.arenas[w].token
+                self.wbuf[(v, w)] = (self.arenas[w].alloc(nb + 1), nb + 1, tok)
+                self.meta[(v, w)] = (self.arenas[shard].alloc(meta_block_size(len(self.shapes[v]))),
+                                     meta_block_size(len(self.shapes[v])),
+                                     self.arenas[shard].token)
+                self.stage[(v, w)] = self.arenas[w].alloc(meta_block_size(len(self.shapes[v])))
+                self.grad[(v, w)] = self.arenas[w].alloc(nb)
+        self.it = 0
+
+    def step(self) -> None:
+        self.it += 1
+        it, W = self.it, self.W
+        for v, (shard, vaddr, nb) in enumerate(self.vars):
+            n = nb // 4
+            sp_ps = self.spaces[shard]
+            grads = []
+            for w in range(W):
+                gen_id = ps_node_ids(v, w, W)[1]
+                g = synthesize(n, 0, node_rng(self.seed, gen_id, it))
+                if w == shard:               # co-located: no cross edge
+                    grads.append(g)
+                    continue
+                sp_w = self.spaces[w]
+                static_send(self.fab, sp_ps, (vaddr, nb), self.flags[shard], sp_w,
+                            self.wbuf[(v, w)])
+                assert static_poll(sp_w, self.wbuf[(v, w)]) is not None
+                ga = self.grad[(v, w)]
+                sp_w.mem[ga:ga + nb] = g.view(np.uint8)
+                dyn_send(self.fab, sp_w, self.stage[(v, w)], self.shapes[v], 0, ga,
+                         self.arenas[w].token, sp_ps, self.meta[(v, w)])
+                local, plen, _ = dyn_poll_fetch(self.fab, sp_ps, self.arenas[shard],
+                                                self.meta[(v, w)], len(self.shapes[v]), sp_w)
+                grads.append(sp_ps.mem[local:local + plen].view(np.float32).copy())
+                self.arenas[shard].free(local, plen)
+            var = sp_ps.mem[vaddr:vaddr + nb].view(np.float32)
+            if self.op == "xor":
+                apply_xor(var, grads)
+            else:
+                apply_sgd(var, grads, self.lr)
+
+    def variable(self, v: int) -> np.ndarray:
+        shard, a, nb = self.vars[v]
+        return self.spaces[shard].mem[a:a + nb].view(np.float32).reshape(self.shapes[v])

@@ -1,0 +1,1255 @@
+// srflow.cu - libsrflow.so: the B200-native (sm_100a) transfer hot path.
+//
+// Host half: per-server HBM pools with the reference's region table, token
+// and bounds gates (memspace.py:89-236), streams/events standing in for queue
+// pairs and completion queues (fabric.py:113-143, :423-428), and the verb
+// entry points (fabric.py:349-389).  Device half: the kernels K1..K6 of
+// SURVEY.md section 2.2.  The reference moves bytes with a Python loop of
+// 1-4096 B ascending chunks (fabric.py:391-421); here every byte moves through
+// 16-byte vector loads/stores issued by all SMs, and the "final byte lands
+// last" guarantee is rebuilt from a system-scope fence, a grid arrival count
+// and one st.release.sys of the tail byte.
+//
+// Declarations and reference citations: include/srflow.h.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/srflow.h"
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+static thread_local std::string g_last_error;
+static std::atomic<uint64_t> g_launches{0};
+
+static int fail(int code, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                        \
+  do {                                                                        \
+    cudaError_t _e = (expr);                                                  \
+    if (_e != cudaSuccess)                                                    \
+      return fail(SRF_E_DEVICE, "%s: %s (%s:%d)", #expr,                      \
+                  cudaGetErrorString(_e), __FILE__, __LINE__);                \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// host-side objects
+// ---------------------------------------------------------------------------
+struct Region {
+  int64_t id;
+  uint64_t base, length;
+  bool registered;
+  uint64_t token;
+};
+
+struct srf_stream {
+  int device;
+  cudaStream_t s;
+  bool owned;
+  unsigned int *counter;  // grid arrival counter for tail-release kernels
+  float *scratch;         // per-block partials for reductions
+};
+
+struct srf_space {
+  int server_id;
+  int device;
+  uint64_t capacity;
+  uint32_t max_regions;
+  uint8_t *base;       // device pointer (own cudaMalloc or IPC mapping)
+  bool imported;       // remote proxy mapped through cudaIpcOpenMemHandle
+  std::mutex mu;       // region table, next_addr
+  std::vector<Region> regions;
+  uint64_t next_addr;
+  srf_stream *stream;  // default stream (local work + byte IO)
+  int *err;            // device error word (flag-wait timeouts)
+};
+
+struct srf_event {
+  int device;
+  cudaEvent_t e;
+};
+
+static constexpr uint64_t kAlign = 8;  // memspace.py:31 (_ALIGN)
+static constexpr int kMaxSeg = 8;
+static constexpr int kScratchBlocks = 1024;
+
+static int sm_count_of(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (cache[device] == 0) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) !=
+            cudaSuccess || n <= 0)
+      n = 148;
+    cache[device] = n;
+  }
+  return cache[device];
+}
+
+static int make_stream(int device, bool create, cudaStream_t existing,
+                       srf_stream **out) {
+  CUDA_TRY(cudaSetDevice(device));
+  srf_stream *st = new srf_stream();
+  st->device = device;
+  st->owned = create;
+  if (create) {
+    cudaError_t e = cudaStreamCreateWithFlags(&st->s, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+      delete st;
+      return fail(SRF_E_DEVICE, "cudaStreamCreate: %s", cudaGetErrorString(e));
+    }
+  } else {
+    st->s = existing;
+  }
+  cudaError_t e = cudaMalloc(&st->counter, sizeof(unsigned int) + 16);
+  if (e == cudaSuccess) e = cudaMemset(st->counter, 0, sizeof(unsigned int) + 16);
+  if (e == cudaSuccess) e = cudaMalloc(&st->scratch, sizeof(float) * kScratchBlocks);
+  if (e != cudaSuccess) {
+    if (create) cudaStreamDestroy(st->s);
+    delete st;
+    return fail(SRF_E_DEVICE, "stream scratch: %s", cudaGetErrorString(e));
+  }
+  *out = st;
+  return SRF_OK;
+}
+
+static void free_stream(srf_stream *st) {
+  if (!st) return;
+  cudaSetDevice(st->device);
+  cudaStreamSynchronize(st->s);
+  cudaFree(st->counter);
+  cudaFree(st->scratch);
+  if (st->owned) cudaStreamDestroy(st->s);
+  delete st;
+}
+
+static srf_stream *stream_or_default(srf_space *sp, srf_stream *st) {
+  return st ? st : sp->stream;
+}
+
+// memspace.py:139-143 (_find_registered): linear scan, first containing
+// registered region.
+static const Region *find_registered(const srf_space *sp, uint64_t addr,
+                                     uint64_t len) {
+  for (const Region &r : sp->regions)
+    if (r.registered && r.base <= addr && addr + len <= r.base + r.length)
+      return &r;
+  return nullptr;
+}
+
+static int check_remote_locked(srf_space *sp, uint64_t addr, uint64_t len,
+                               uint64_t token) {
+  const Region *r = find_registered(sp, addr, len);
+  if (!r)
+    return fail(SRF_E_REMOTE_OOB,
+                "server %d: [%llu, %llu) is not inside a registered region",
+                sp->server_id, (unsigned long long)addr,
+                (unsigned long long)(addr + len));
+  if (r->token != token)
+    return fail(SRF_E_BAD_TOKEN, "server %d: token mismatch for region %lld",
+                sp->server_id, (long long)r->id);
+  return SRF_OK;
+}
+
+static int check_registered_locked(srf_space *sp, uint64_t addr, uint64_t len,
+                                   uint64_t token) {
+  const Region *r = find_registered(sp, addr, len);
+  if (!r || r->token != token)
+    return fail(SRF_E_NOT_REGISTERED,
+                "server %d: [%llu, %llu) is not registered", sp->server_id,
+                (unsigned long long)addr, (unsigned long long)(addr + len));
+  return SRF_OK;
+}
+
+static int check_raw(const srf_space *sp, uint64_t addr, uint64_t len,
+                     const char *what) {
+  if (addr > sp->capacity || len > sp->capacity - addr)
+    return fail(SRF_E_OUT_OF_BOUNDS, "%s [%llu, %llu) escapes space of %llu",
+                what, (unsigned long long)addr,
+                (unsigned long long)(addr + len),
+                (unsigned long long)sp->capacity);
+  return SRF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// device helpers (inline PTX: system-scope acquire/release on peer memory)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_acquire_sys_u8(const uint8_t *p) {
+  uint16_t v;
+  asm volatile("ld.acquire.sys.global.u8 %0, [%1];"
+               : "=h"(v)
+               : "l"(p)
+               : "memory");
+  return v & 0xff;
+}
+
+__device__ __forceinline__ void st_release_sys_u8(uint8_t *p, uint32_t v) {
+  uint16_t x = (uint16_t)v;
+  asm volatile("st.release.sys.global.u8 [%0], %1;" ::"l"(p), "h"(x)
+               : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_sys_u8(uint8_t *p, uint32_t v) {
+  uint16_t x = (uint16_t)v;
+  asm volatile("st.relaxed.sys.global.u8 [%0], %1;" ::"l"(p), "h"(x)
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// 16-byte streaming load, no L1 allocation (source is read exactly once)
+__device__ __forceinline__ uint4 ld_stream_v4(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v4(uint4 *p, const uint4 &v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+template <typename V>
+__device__ __forceinline__ V ld_stream(const V *p) {
+  return __ldg(p);
+}
+template <>
+__device__ __forceinline__ uint4 ld_stream<uint4>(const uint4 *p) {
+  return ld_stream_v4(p);
+}
+template <typename V>
+__device__ __forceinline__ void st_plain(V *p, const V &v) {
+  *p = v;
+}
+template <>
+__device__ __forceinline__ void st_plain<uint4>(uint4 *p, const uint4 &v) {
+  st_v4(p, v);
+}
+
+// Grid-wide copy of nv vectors: all loads of an unrolled batch are issued
+// before its stores so every thread keeps U requests in flight (the latency of
+// a peer access is ~2000 cycles, B300_MICROARCH.md "NVLink").
+template <typename V, int U>
+__device__ __forceinline__ void vec_copy(V *__restrict__ dst,
+                                         const V *__restrict__ src,
+                                         uint64_t nv, uint64_t t,
+                                         uint64_t nth) {
+  uint64_t i = t;
+  for (; i + (uint64_t)(U - 1) * nth < nv; i += (uint64_t)U * nth) {
+    V r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = ld_stream<V>(src + i + u * nth);
+#pragma unroll
+    for (int u = 0; u < U; ++u) st_plain<V>(dst + i + u * nth, r[u]);
+  }
+  for (; i < nv; i += nth) st_plain<V>(dst + i, ld_stream<V>(src + i));
+}
+
+// Copy n bytes with the widest vector both pointers allow.  Arena blocks are
+// 8-byte aligned (memspace.py:31), so the 16-B path needs equal (p mod 16).
+__device__ void copy_bytes_grid(uint8_t *dst, const uint8_t *src, uint64_t n,
+                                uint64_t t, uint64_t nth) {
+  if (n == 0) return;
+  uintptr_t d = (uintptr_t)dst, s = (uintptr_t)src;
+  uint64_t head, nv;
+  if (((d ^ s) & 15) == 0) {
+    head = (16 - (d & 15)) & 15;
+    if (head > n) head = n;
+    nv = (n - head) / 16;
+    vec_copy<uint4, 4>((uint4 *)(dst + head), (const uint4 *)(src + head), nv,
+                       t, nth);
+    nv *= 16;
+  } else if (((d ^ s) & 7) == 0) {
+    head = (8 - (d & 7)) & 7;
+    if (head > n) head = n;
+    nv = (n - head) / 8;
+    vec_copy<uint2, 8>((uint2 *)(dst + head), (const uint2 *)(src + head), nv,
+                       t, nth);
+    nv *= 8;
+  } else if (((d ^ s) & 3) == 0) {
+    head = (4 - (d & 3)) & 3;
+    if (head > n) head = n;
+    nv = (n - head) / 4;
+    vec_copy<uint32_t, 8>((uint32_t *)(dst + head),
+                          (const uint32_t *)(src + head), nv, t, nth);
+    nv *= 4;
+  } else {
+    head = 0;
+    nv = 0;
+  }
+  // scalar head and tail bytes
+  for (uint64_t i = t; i < head; i += nth) dst[i] = src[i];
+  for (uint64_t i = head + nv + t; i < n; i += nth) dst[i] = src[i];
+}
+
+struct Seg {
+  const uint8_t *src;
+  uint64_t dst_off;
+  uint64_t len;
+};
+
+struct PutArgs {
+  Seg seg[kMaxSeg];
+  int nseg;
+  uint8_t *dst;          // destination base (peer or local device pointer)
+  uint64_t total;        // bytes in the gather list
+  int tail_release;      // 1: last byte written last with st.release.sys
+  int wait_empty;        // 1: spin until dst[total-1] == 0 before writing
+  uint64_t timeout_ns;
+  unsigned int *counter; // arrival counter (per stream, reset by last CTA)
+  int *err;
+};
+
+// K1 static_put / K3 meta_put / K4 peer_pull / K5 stage_copy.
+__global__ void __launch_bounds__(512) k_put(PutArgs a) {
+  __shared__ int s_last;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint8_t *tail = a.dst + a.total - 1;
+
+  if (a.wait_empty) {
+    // credit check of the iteration barrier (runtime/protocol.py:102-111):
+    // the receiver must have cleared the previous transfer's flag.
+    if (threadIdx.x == 0) {
+      uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_sys_u8(tail) != 0) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          atomicExch(a.err, 2);
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  }
+
+  // body: every byte except the tail one when tail_release is set
+  uint64_t body = a.tail_release ? a.total - 1 : a.total;
+  for (int i = 0; i < a.nseg; ++i) {
+    const Seg &sg = a.seg[i];
+    if (sg.dst_off >= body) break;
+    uint64_t n = sg.len;
+    if (sg.dst_off + n > body) n = body - sg.dst_off;
+    copy_bytes_grid(a.dst + sg.dst_off, sg.src, n, t, nth);
+  }
+
+  if (!a.tail_release) return;
+  // flag-last: all CTAs publish, the last to arrive releases the tail byte.
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    unsigned prev = atomicAdd(a.counter, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence_system();
+    const Seg &ls = a.seg[a.nseg - 1];
+    uint32_t v = ls.src[ls.len - 1];
+    st_release_sys_u8(tail, v);
+    atomicExch(a.counter, 0u);
+  }
+}
+
+// K2 flag_wait: device-side consumer prologue of StaticReceiver.poll.
+__global__ void k_flag_wait(uint8_t *flag, uint32_t expect, int clear,
+                            uint64_t timeout_ns, int *err) {
+  if (threadIdx.x != 0) return;
+  uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_sys_u8(flag) != expect) {
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      atomicExch(err, 1);
+      return;
+    }
+    __nanosleep(32);
+  }
+  if (clear) st_relaxed_sys_u8(flag, 0);
+}
+
+
+// Device consumer for release/acquire checks: thread 0 acquire-spins on the
+// flag, the CTA then checksums the payload it guards and clears the flag.
+__global__ void __launch_bounds__(1024) k_consume_sum(uint8_t *flag,
+                                                      const uint8_t *data,
+                                                      uint64_t n, uint64_t *out,
+                                                      uint64_t timeout_ns,
+                                                      int *err) {
+  __shared__ unsigned long long acc;
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    acc = 0;
+    ok = 1;
+    uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys_u8(flag) != 1) {
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        atomicExch(err, 1);
+        ok = 0;
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+  if (!ok) return;
+  unsigned long long s = 0;
+  for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) s += data[i] * (i % 251 + 1);
+  atomicAdd(&acc, s);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *out = acc;
+    st_relaxed_sys_u8(flag, 0);
+  }
+}
+
+// K6 ps_apply
+struct ApplyArgs {
+  uint8_t *var;
+  const uint8_t *g[SRF_MAX_WORKERS];
+  int nw;
+  uint64_t n;  // bytes
+  float lr;
+};
+
+template <typename V>
+__device__ __forceinline__ V xor_v(V a, V b);
+template <>
+__device__ __forceinline__ uint4 xor_v<uint4>(uint4 a, uint4 b) {
+  return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
+}
+template <>
+__device__ __forceinline__ uint2 xor_v<uint2>(uint2 a, uint2 b) {
+  return make_uint2(a.x ^ b.x, a.y ^ b.y);
+}
+template <>
+__device__ __forceinline__ uint8_t xor_v<uint8_t>(uint8_t a, uint8_t b) {
+  return a ^ b;
+}
+
+// plain (coherent) 16-B load: gradients may be peer memory
+__device__ __forceinline__ uint4 ld_v4(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+template <typename V>
+__device__ __forceinline__ V ld_any(const V *p) {
+  return *p;
+}
+template <>
+__device__ __forceinline__ uint4 ld_any<uint4>(const uint4 *p) {
+  return ld_v4(p);
+}
+
+// XOR over nv vectors of type V starting at byte offset off.
+template <typename V, int U>
+__device__ __forceinline__ void xor_body(const ApplyArgs &a, uint64_t off,
+                                         uint64_t nv, uint64_t t,
+                                         uint64_t nth) {
+  V *var = (V *)(a.var + off);
+  uint64_t i = t;
+  for (; i + (uint64_t)(U - 1) * nth < nv; i += (uint64_t)U * nth) {
+    V acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = ld_any<V>(var + i + u * nth);
+    for (int w = 0; w < a.nw; ++w) {
+      const V *g = (const V *)(a.g[w] + off);
+      V r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) r[u] = ld_any<V>(g + i + u * nth);
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc[u] = xor_v<V>(acc[u], r[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) var[i + u * nth] = acc[u];
+  }
+  for (; i < nv; i += nth) {
+    V acc = var[i];
+    for (int w = 0; w < a.nw; ++w)
+      acc = xor_v<V>(acc, ld_any<V>((const V *)(a.g[w] + off) + i));
+    var[i] = acc;
+  }
+}
+
+__device__ __forceinline__ float sgd1(float v, float lr, float g) {
+  return __fsub_rn(v, __fmul_rn(lr, g));
+}
+
+template <int U>
+__device__ __forceinline__ void sgd_body_v4(const ApplyArgs &a, uint64_t off,
+                                            uint64_t nv, uint64_t t,
+                                            uint64_t nth) {
+  float4 *var = (float4 *)(a.var + off);
+  const float lr = a.lr;
+  uint64_t i = t;
+  for (; i + (uint64_t)(U - 1) * nth < nv; i += (uint64_t)U * nth) {
+    float4 acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = var[i + u * nth];
+    for (int w = 0; w < a.nw; ++w) {
+      const uint4 *g = (const uint4 *)(a.g[w] + off);
+      uint4 r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) r[u] = ld_v4(g + i + u * nth);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        acc[u].x = sgd1(acc[u].x, lr, __uint_as_float(r[u].x));
+        acc[u].y = sgd1(acc[u].y, lr, __uint_as_float(r[u].y));
+        acc[u].z = sgd1(acc[u].z, lr, __uint_as_float(r[u].z));
+        acc[u].w = sgd1(acc[u].w, lr, __uint_as_float(r[u].w));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) var[i + u * nth] = acc[u];
+  }
+  for (; i < nv; i += nth) {
+    float4 acc = var[i];
+    for (int w = 0; w < a.nw; ++w) {
+      uint4 r = ld_v4((const uint4 *)(a.g[w] + off) + i);
+      acc.x = sgd1(acc.x, lr, __uint_as_float(r.x));
+      acc.y = sgd1(acc.y, lr, __uint_as_float(r.y));
+      acc.z = sgd1(acc.z, lr, __uint_as_float(r.z));
+      acc.w = sgd1(acc.w, lr, __uint_as_float(r.w));
+    }
+    var[i] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(512) k_apply_xor(ApplyArgs a) {
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uintptr_t m = (uintptr_t)a.var;
+  bool same16 = true, same8 = true;
+  for (int w = 0; w < a.nw; ++w) {
+    uintptr_t p = (uintptr_t)a.g[w];
+    same16 &= ((p ^ m) & 15) == 0;
+    same8 &= ((p ^ m) & 7) == 0;
+  }
+  uint64_t head = 0, nvb = 0;
+  if (same16) {
+    head = (16 - (m & 15)) & 15;
+    if (head > a.n) head = a.n;
+    uint64_t nv = (a.n - head) / 16;
+    xor_body<uint4, 4>(a, head, nv, t, nth);
+    nvb = nv * 16;
+  } else if (same8) {
+    head = (8 - (m & 7)) & 7;
+    if (head > a.n) head = a.n;
+    uint64_t nv = (a.n - head) / 8;
+    xor_body<uint2, 8>(a, head, nv, t, nth);
+    nvb = nv * 8;
+  }
+  // bytes outside the vector body: [0, head) and [head + nvb, n)
+  const uint64_t rest = a.n - nvb;
+  for (uint64_t j = t; j < rest; j += nth) {
+    uint64_t i = j < head ? j : j + nvb;
+    uint8_t acc = a.var[i];
+    for (int w = 0; w < a.nw; ++w) acc ^= a.g[w][i];
+    a.var[i] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(512) k_apply_sgd(ApplyArgs a) {
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uintptr_t m = (uintptr_t)a.var;
+  bool same16 = true;
+  for (int w = 0; w < a.nw; ++w) same16 &= (((uintptr_t)a.g[w] ^ m) & 15) == 0;
+  const uint64_t nf = a.n / 4;
+  uint64_t headf = 0, nvf = 0;
+  if (same16) {
+    headf = ((16 - (m & 15)) & 15) / 4;
+    if (headf > nf) headf = nf;
+    uint64_t nv = (nf - headf) / 4;
+    sgd_body_v4<4>(a, headf * 4, nv, t, nth);
+    nvf = nv * 4;
+  }
+  float *var = (float *)a.var;
+  const uint64_t rest = nf - nvf;
+  for (uint64_t j = t; j < rest; j += nth) {
+    uint64_t i = j < headf ? j : j + nvf;
+    float v = var[i];
+    for (int w = 0; w < a.nw; ++w) v = sgd1(v, a.lr, ((const float *)a.g[w])[i]);
+    var[i] = v;
+  }
+}
+
+// ReduceMax (graph.py:378-382): per-block max, last block folds partials.
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  // numpy max propagates NaN
+  if (a != a) return a;
+  if (b != b) return b;
+  return a > b ? a : b;
+}
+
+__global__ void __launch_bounds__(256) k_reduce_max(const float *x, uint64_t n,
+                                                    float *out, float *part,
+                                                    unsigned int *counter) {
+  __shared__ float sm[32];
+  __shared__ int s_last;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  float m = -INFINITY;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += nth)
+    m = fmax_nan(m, x[i]);
+  for (int o = 16; o; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(~0u, m, o));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : -INFINITY;
+    for (int o = 16; o; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(~0u, m, o));
+    if (threadIdx.x == 0) {
+      part[blockIdx.x] = m;
+      __threadfence();
+      s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  float r = -INFINITY;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x)
+    r = fmax_nan(r, ((volatile float *)part)[i]);
+  for (int o = 16; o; o >>= 1) r = fmax_nan(r, __shfl_xor_sync(~0u, r, o));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = r;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    r = -INFINITY;
+    for (unsigned i = 0; i < (blockDim.x >> 5); ++i) r = fmax_nan(r, sm[i]);
+    *out = (n == 0) ? 0.0f : r;
+    atomicExch(counter, 0u);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launch geometry
+// ---------------------------------------------------------------------------
+static void copy_geometry(int device, uint64_t bytes, int *grid, int *block) {
+  const int threads = 512;
+  // one CTA moves threads * 16 B * 4 per unrolled batch; cap at 2 CTAs/SM
+  uint64_t per_cta = (uint64_t)threads * 16 * 4;
+  uint64_t want = (bytes + per_cta - 1) / per_cta;
+  uint64_t cap = (uint64_t)sm_count_of(device) * 2;
+  if (want < 1) want = 1;
+  if (want > cap) want = cap;
+  *grid = (int)want;
+  *block = threads;
+}
+
+static int record_event(int device, cudaStream_t s, srf_event_t *ev_out) {
+  if (!ev_out) return SRF_OK;
+  srf_event *ev = new srf_event();
+  ev->device = device;
+  cudaError_t e = cudaEventCreateWithFlags(&ev->e, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ev->e, s);
+  if (e != cudaSuccess) {
+    delete ev;
+    return fail(SRF_E_DEVICE, "event: %s", cudaGetErrorString(e));
+  }
+  *ev_out = ev;
+  return SRF_OK;
+}
+
+static int launch_check(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return fail(SRF_E_DEVICE, "%s launch: %s", what, cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return SRF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char *srf_last_error(void) { return g_last_error.c_str(); }
+int srf_version(void) { return 1; }
+uint64_t srf_launch_count(void) { return g_launches.load(); }
+
+int srf_device_count(int *count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    return fail(SRF_E_DEVICE, "cudaGetDeviceCount: %s", cudaGetErrorString(e));
+  }
+  *count = n;
+  return SRF_OK;
+}
+
+int srf_space_create(int server_id, int cuda_device, uint64_t capacity,
+                     uint32_t max_regions, srf_space_t *out) {
+  if (capacity == 0) return fail(SRF_E_ZERO_LENGTH, "capacity must be >= 1");
+  CUDA_TRY(cudaSetDevice(cuda_device));
+  srf_space *sp = new srf_space();
+  sp->server_id = server_id;
+  sp->device = cuda_device;
+  sp->capacity = capacity;
+  sp->max_regions = max_regions;
+  sp->imported = false;
+  sp->next_addr = 0;
+  sp->stream = nullptr;
+  sp->err = nullptr;
+  cudaError_t e = cudaMalloc(&sp->base, capacity);
+  if (e != cudaSuccess) {
+    delete sp;
+    return fail(SRF_E_OUT_OF_MEMORY, "server %d: cudaMalloc(%llu): %s",
+                server_id, (unsigned long long)capacity, cudaGetErrorString(e));
+  }
+  int rc = make_stream(cuda_device, true, nullptr, &sp->stream);
+  if (rc == SRF_OK) {
+    e = cudaMalloc(&sp->err, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(sp->err, 0, sizeof(int));
+    // np.zeros semantics: the whole space reads as zero bytes
+    if (e == cudaSuccess) e = cudaMemsetAsync(sp->base, 0, capacity, sp->stream->s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(sp->stream->s);
+    if (e != cudaSuccess) rc = fail(SRF_E_DEVICE, "space init: %s", cudaGetErrorString(e));
+  }
+  if (rc != SRF_OK) {
+    free_stream(sp->stream);
+    cudaFree(sp->base);
+    if (sp->err) cudaFree(sp->err);
+    delete sp;
+    return rc;
+  }
+  *out = sp;
+  return SRF_OK;
+}
+
+int srf_space_destroy(srf_space_t sp) {
+  if (!sp) return SRF_OK;
+  cudaSetDevice(sp->device);
+  free_stream(sp->stream);
+  if (sp->imported)
+    cudaIpcCloseMemHandle(sp->base);
+  else
+    cudaFree(sp->base);
+  if (sp->err) cudaFree(sp->err);
+  delete sp;
+  return SRF_OK;
+}
+
+int srf_space_info(srf_space_t sp, int *server_id, int *cuda_device,
+                   uint64_t *capacity, void **device_base) {
+  if (server_id) *server_id = sp->server_id;
+  if (cuda_device) *cuda_device = sp->device;
+  if (capacity) *capacity = sp->capacity;
+  if (device_base) *device_base = sp->base;
+  return SRF_OK;
+}
+
+void *srf_space_cuda_stream(srf_space_t sp) { return (void *)sp->stream->s; }
+
+int srf_region_alloc(srf_space_t sp, uint64_t length, int registered,
+                     uint64_t token, int64_t *region_id, uint64_t *base) {
+  if (length < 1)
+    return fail(SRF_E_ZERO_LENGTH, "region length must be >= 1, got %llu",
+                (unsigned long long)length);
+  std::lock_guard<std::mutex> g(sp->mu);
+  if (sp->regions.size() >= sp->max_regions)
+    return fail(SRF_E_OUT_OF_MEMORY, "server %d: region table full (%u)",
+                sp->server_id, sp->max_regions);
+  uint64_t b = (sp->next_addr + kAlign - 1) & ~(kAlign - 1);
+  if (b + length > sp->capacity)
+    return fail(SRF_E_OUT_OF_MEMORY,
+                "server %d: need %llu bytes at %llu, capacity %llu",
+                sp->server_id, (unsigned long long)length,
+                (unsigned long long)b, (unsigned long long)sp->capacity);
+  Region r{(int64_t)sp->regions.size(), b, length, registered != 0,
+           registered ? token : 0};
+  sp->regions.push_back(r);
+  sp->next_addr = b + length;
+  *region_id = r.id;
+  *base = b;
+  return SRF_OK;
+}
+
+int srf_region_import(srf_space_t proxy, int64_t region_id, uint64_t base,
+                      uint64_t length, int registered, uint64_t token) {
+  std::lock_guard<std::mutex> g(proxy->mu);
+  if (base + length > proxy->capacity)
+    return fail(SRF_E_OUT_OF_BOUNDS, "imported region escapes space");
+  proxy->regions.push_back(Region{region_id, base, length, registered != 0,
+                                  registered ? token : 0});
+  proxy->next_addr = std::max(proxy->next_addr, base + length);
+  return SRF_OK;
+}
+
+int srf_region_count(srf_space_t sp, uint32_t *count) {
+  std::lock_guard<std::mutex> g(sp->mu);
+  *count = (uint32_t)sp->regions.size();
+  return SRF_OK;
+}
+
+int srf_next_addr(srf_space_t sp, uint64_t *next_addr) {
+  std::lock_guard<std::mutex> g(sp->mu);
+  *next_addr = sp->next_addr;
+  return SRF_OK;
+}
+
+int srf_check_remote(srf_space_t sp, uint64_t addr, uint64_t length,
+                     uint64_t token) {
+  std::lock_guard<std::mutex> g(sp->mu);
+  return check_remote_locked(sp, addr, length, token);
+}
+
+int srf_check_registered(srf_space_t sp, uint64_t addr, uint64_t length,
+                         uint64_t token) {
+  std::lock_guard<std::mutex> g(sp->mu);
+  return check_registered_locked(sp, addr, length, token);
+}
+
+int srf_read(srf_space_t sp, uint64_t addr, uint64_t length, void *host_dst) {
+  int rc = check_raw(sp, addr, length, "read");
+  if (rc) return rc;
+  if (length == 0) return SRF_OK;
+  CUDA_TRY(cudaSetDevice(sp->device));
+  CUDA_TRY(cudaMemcpyAsync(host_dst, sp->base + addr, length,
+                           cudaMemcpyDeviceToHost, sp->stream->s));
+  CUDA_TRY(cudaStreamSynchronize(sp->stream->s));
+  return SRF_OK;
+}
+
+int srf_write(srf_space_t sp, uint64_t addr, uint64_t length,
+              const void *host_src) {
+  int rc = check_raw(sp, addr, length, "write");
+  if (rc) return rc;
+  if (length == 0) return SRF_OK;
+  CUDA_TRY(cudaSetDevice(sp->device));
+  CUDA_TRY(cudaMemcpyAsync(sp->base + addr, host_src, length,
+                           cudaMemcpyHostToDevice, sp->stream->s));
+  CUDA_TRY(cudaStreamSynchronize(sp->stream->s));
+  return SRF_OK;
+}
+
+int srf_write_async(srf_space_t sp, uint64_t addr, uint64_t length,
+                    const void *host_src, srf_stream_t st) {
+  int rc = check_raw(sp, addr, length, "write");
+  if (rc) return rc;
+  if (length == 0) return SRF_OK;
+  srf_stream *s = stream_or_default(sp, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  CUDA_TRY(cudaMemcpyAsync(sp->base + addr, host_src, length,
+                           cudaMemcpyHostToDevice, s->s));
+  return SRF_OK;
+}
+
+int srf_read_async(srf_space_t sp, uint64_t addr, uint64_t length,
+                   void *host_dst, srf_stream_t st) {
+  int rc = check_raw(sp, addr, length, "read");
+  if (rc) return rc;
+  if (length == 0) return SRF_OK;
+  srf_stream *s = stream_or_default(sp, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  CUDA_TRY(cudaMemcpyAsync(host_dst, sp->base + addr, length,
+                           cudaMemcpyDeviceToHost, s->s));
+  return SRF_OK;
+}
+
+int srf_device_ptr(srf_space_t sp, uint64_t addr, void **dptr) {
+  int rc = check_raw(sp, addr, 0, "view");
+  if (rc) return rc;
+  *dptr = sp->base + addr;
+  return SRF_OK;
+}
+
+int srf_space_sync(srf_space_t sp) {
+  CUDA_TRY(cudaSetDevice(sp->device));
+  CUDA_TRY(cudaStreamSynchronize(sp->stream->s));
+  int err = 0;
+  CUDA_TRY(cudaMemcpy(&err, sp->err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err) {
+    cudaMemset(sp->err, 0, sizeof(int));
+    return fail(SRF_E_TIMEOUT, "server %d: device flag wait timed out (code %d)",
+                sp->server_id, err);
+  }
+  return SRF_OK;
+}
+
+int srf_connect(srf_space_t a, srf_space_t b) {
+  if (a->device == b->device) return SRF_OK;
+  int can_ab = 0, can_ba = 0;
+  CUDA_TRY(cudaDeviceCanAccessPeer(&can_ab, a->device, b->device));
+  CUDA_TRY(cudaDeviceCanAccessPeer(&can_ba, b->device, a->device));
+  if (!can_ab || !can_ba)
+    return fail(SRF_E_PEER_UNREACHABLE, "GPU %d and GPU %d have no peer path",
+                a->device, b->device);
+  const int pairs[2][2] = {{a->device, b->device}, {b->device, a->device}};
+  for (auto &p : pairs) {
+    CUDA_TRY(cudaSetDevice(p[0]));
+    cudaError_t e = cudaDeviceEnablePeerAccess(p[1], 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled)
+      cudaGetLastError();
+    else if (e != cudaSuccess)
+      return fail(SRF_E_PEER_UNREACHABLE, "enable peer %d->%d: %s", p[0], p[1],
+                  cudaGetErrorString(e));
+  }
+  return SRF_OK;
+}
+
+int srf_space_export(srf_space_t sp, void *handle64) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
+  if (sp->imported) return fail(SRF_E_INVALID_CONFIG, "cannot re-export a proxy");
+  CUDA_TRY(cudaSetDevice(sp->device));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, sp->base));
+  memcpy(handle64, &h, sizeof h);
+  return SRF_OK;
+}
+
+int srf_space_import(const void *handle64, int server_id, int local_device,
+                     uint64_t capacity, srf_space_t *out) {
+  CUDA_TRY(cudaSetDevice(local_device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof h);
+  void *p = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  srf_space *sp = new srf_space();
+  sp->server_id = server_id;
+  sp->device = local_device;  // work on the proxy is issued from this GPU
+  sp->capacity = capacity;
+  sp->max_regions = 1u << 30;
+  sp->base = (uint8_t *)p;
+  sp->imported = true;
+  sp->next_addr = 0;
+  sp->err = nullptr;
+  int rc = make_stream(local_device, true, nullptr, &sp->stream);
+  if (rc == SRF_OK) {
+    cudaError_t e = cudaMalloc(&sp->err, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(sp->err, 0, sizeof(int));
+    if (e != cudaSuccess) rc = fail(SRF_E_DEVICE, "proxy: %s", cudaGetErrorString(e));
+  }
+  if (rc != SRF_OK) {
+    cudaIpcCloseMemHandle(p);
+    delete sp;
+    return rc;
+  }
+  *out = sp;
+  return SRF_OK;
+}
+
+int srf_stream_create(srf_space_t sp, srf_stream_t *out) {
+  return make_stream(sp->device, true, nullptr, out);
+}
+
+int srf_stream_destroy(srf_stream_t st) {
+  free_stream(st);
+  return SRF_OK;
+}
+
+void *srf_stream_cuda(srf_stream_t st) { return (void *)st->s; }
+
+int srf_stream_sync(srf_stream_t st) {
+  CUDA_TRY(cudaSetDevice(st->device));
+  CUDA_TRY(cudaStreamSynchronize(st->s));
+  return SRF_OK;
+}
+
+int srf_event_record(srf_space_t sp, srf_stream_t st, srf_event_t *out) {
+  srf_stream *s = stream_or_default(sp, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  return record_event(s->device, s->s, out);
+}
+
+int srf_event_query(srf_event_t ev) {
+  cudaError_t e = cudaEventQuery(ev->e);
+  if (e == cudaSuccess) return SRF_OK;
+  if (e == cudaErrorNotReady) return SRF_PENDING;
+  return fail(SRF_E_DEVICE, "event query: %s", cudaGetErrorString(e));
+}
+
+int srf_event_wait(srf_event_t ev) {
+  CUDA_TRY(cudaEventSynchronize(ev->e));
+  return SRF_OK;
+}
+
+int srf_event_free(srf_event_t ev) {
+  if (!ev) return SRF_OK;
+  cudaEventDestroy(ev->e);
+  delete ev;
+  return SRF_OK;
+}
+
+int srf_put(srf_space_t src_space, const uint64_t *src_addr,
+            const uint64_t *src_len, const uint64_t *src_token, int nseg,
+            srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
+            int flags, srf_stream_t st, srf_event_t *ev_out) {
+  if (nseg < 1 || nseg > kMaxSeg)
+    return fail(SRF_E_INVALID_CONFIG, "gather list of %d segments (max %d)",
+                nseg, kMaxSeg);
+  uint64_t total = 0;
+  for (int i = 0; i < nseg; ++i) total += src_len[i];
+  if (total < 1) return fail(SRF_E_INVALID_LENGTH, "zero-length write");
+  {
+    std::lock_guard<std::mutex> g(src_space->mu);
+    for (int i = 0; i < nseg; ++i) {
+      int rc = check_registered_locked(src_space, src_addr[i], src_len[i],
+                                       src_token[i]);
+      if (rc) return rc;
+    }
+  }
+  {
+    std::lock_guard<std::mutex> g(dst_space->mu);
+    int rc = check_remote_locked(dst_space, dst_addr, total, dst_token);
+    if (rc) return rc;
+  }
+  srf_stream *s = stream_or_default(src_space, st);
+  PutArgs a;
+  memset(&a, 0, sizeof a);
+  uint64_t off = 0;
+  int k = 0;
+  for (int i = 0; i < nseg; ++i) {
+    if (src_len[i] == 0) continue;
+    a.seg[k].src = src_space->base + src_addr[i];
+    a.seg[k].dst_off = off;
+    a.seg[k].len = src_len[i];
+    off += src_len[i];
+    ++k;
+  }
+  a.nseg = k;
+  a.dst = dst_space->base + dst_addr;
+  a.total = total;
+  a.tail_release = 1;
+  a.wait_empty = (flags & SRF_PUT_WAIT_EMPTY) ? 1 : 0;
+  a.timeout_ns = 5ull * 1000 * 1000 * 1000;
+  a.counter = s->counter;
+  a.err = src_space->err;
+  int grid, block;
+  copy_geometry(s->device, total, &grid, &block);
+  CUDA_TRY(cudaSetDevice(s->device));
+  k_put<<<grid, block, 0, s->s>>>(a);
+  int rc = launch_check("k_put");
+  if (rc) return rc;
+  return record_event(s->device, s->s, ev_out);
+}
+
+int srf_get(srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
+            srf_space_t src_space, uint64_t src_addr, uint64_t src_token,
+            uint64_t length, srf_stream_t st, srf_event_t *ev_out) {
+  if (length < 1) return fail(SRF_E_INVALID_LENGTH, "zero-length read");
+  {
+    std::lock_guard<std::mutex> g(dst_space->mu);
+    int rc = check_registered_locked(dst_space, dst_addr, length, dst_token);
+    if (rc) return rc;
+  }
+  {
+    std::lock_guard<std::mutex> g(src_space->mu);
+    int rc = check_remote_locked(src_space, src_addr, length, src_token);
+    if (rc) return rc;
+  }
+  srf_stream *s = stream_or_default(dst_space, st);
+  PutArgs a;
+  memset(&a, 0, sizeof a);
+  a.seg[0].src = src_space->base + src_addr;
+  a.seg[0].dst_off = 0;
+  a.seg[0].len = length;
+  a.nseg = 1;
+  a.dst = dst_space->base + dst_addr;
+  a.total = length;
+  a.tail_release = 0;
+  a.counter = s->counter;
+  a.err = dst_space->err;
+  int grid, block;
+  copy_geometry(s->device, length, &grid, &block);
+  CUDA_TRY(cudaSetDevice(s->device));
+  k_put<<<grid, block, 0, s->s>>>(a);
+  int rc = launch_check("k_put(get)");
+  if (rc) return rc;
+  return record_event(s->device, s->s, ev_out);
+}
+
+int srf_copy(srf_space_t sp, uint64_t src_addr, uint64_t dst_addr,
+             uint64_t length, srf_stream_t st, srf_event_t *ev_out) {
+  if (length == 0) return SRF_OK;
+  int rc = check_raw(sp, src_addr, length, "copy src");
+  if (!rc) rc = check_raw(sp, dst_addr, length, "copy dst");
+  if (rc) return rc;
+  srf_stream *s = stream_or_default(sp, st);
+  PutArgs a;
+  memset(&a, 0, sizeof a);
+  a.seg[0].src = sp->base + src_addr;
+  a.seg[0].len = length;
+  a.nseg = 1;
+  a.dst = sp->base + dst_addr;
+  a.total = length;
+  a.counter = s->counter;
+  a.err = sp->err;
+  int grid, block;
+  copy_geometry(s->device, length, &grid, &block);
+  CUDA_TRY(cudaSetDevice(s->device));
+  k_put<<<grid, block, 0, s->s>>>(a);
+  rc = launch_check("k_put(copy)");
+  if (rc) return rc;
+  return record_event(s->device, s->s, ev_out);
+}
+
+int srf_flag_wait(srf_space_t sp, uint64_t flag_addr, uint8_t expect,
+                  int clear, uint64_t timeout_ns, srf_stream_t st) {
+  int rc = check_raw(sp, flag_addr, 1, "flag");
+  if (rc) return rc;
+  srf_stream *s = stream_or_default(sp, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  k_flag_wait<<<1, 32, 0, s->s>>>(sp->base + flag_addr, expect, clear,
+                                  timeout_ns, sp->err);
+  return launch_check("k_flag_wait");
+}
+
+int srf_consume_checksum(srf_space_t sp, uint64_t flag_addr, uint64_t data_addr,
+                         uint64_t n, uint64_t out_addr, uint64_t timeout_ns,
+                         srf_stream_t st) {
+  int rc = check_raw(sp, flag_addr, 1, "flag");
+  if (!rc) rc = check_raw(sp, data_addr, n, "payload");
+  if (!rc) rc = check_raw(sp, out_addr, 8, "checksum");
+  if (rc) return rc;
+  if (out_addr % 8) return fail(SRF_E_INVALID_CONFIG, "checksum slot must be 8-B aligned");
+  srf_stream *s = stream_or_default(sp, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  k_consume_sum<<<1, 1024, 0, s->s>>>(sp->base + flag_addr, sp->base + data_addr, n,
+                                      (uint64_t *)(sp->base + out_addr), timeout_ns,
+                                      sp->err);
+  return launch_check("k_consume_sum");
+}
+
+int srf_apply(srf_space_t var_space, uint64_t var_addr, uint64_t nbytes,
+              srf_space_t const *grad_spaces, const uint64_t *grad_addrs,
+              int nworkers, int op, float lr, srf_stream_t st,
+              srf_event_t *ev_out) {
+  if (nworkers < 1 || nworkers > SRF_MAX_WORKERS)
+    return fail(SRF_E_INVALID_CONFIG, "nworkers %d outside [1, %d]", nworkers,
+                SRF_MAX_WORKERS);
+  if (op != SRF_APPLY_XOR && op != SRF_APPLY_SGD)
+    return fail(SRF_E_INVALID_CONFIG, "unknown apply op %d", op);
+  if (op == SRF_APPLY_SGD && (nbytes % 4 || var_addr % 4))
+    return fail(SRF_E_SHAPE_MISMATCH, "SGD needs whole fp32 elements");
+  int rc = check_raw(var_space, var_addr, nbytes, "variable");
+  if (rc) return rc;
+  ApplyArgs a;
+  memset(&a, 0, sizeof a);
+  a.var = var_space->base + var_addr;
+  a.nw = nworkers;
+  a.n = nbytes;
+  a.lr = lr;
+  for (int w = 0; w < nworkers; ++w) {
+    rc = check_raw(grad_spaces[w], grad_addrs[w], nbytes, "gradient");
+    if (rc) return rc;
+    if (op == SRF_APPLY_SGD && grad_addrs[w] % 4)
+      return fail(SRF_E_SHAPE_MISMATCH, "SGD gradient not fp32 aligned");
+    a.g[w] = grad_spaces[w]->base + grad_addrs[w];
+  }
+  if (nbytes == 0) return record_event(var_space->device, var_space->stream->s, ev_out);
+  srf_stream *s = stream_or_default(var_space, st);
+  int grid, block;
+  copy_geometry(s->device, nbytes, &grid, &block);
+  CUDA_TRY(cudaSetDevice(s->device));
+  if (op == SRF_APPLY_XOR)
+    k_apply_xor<<<grid, block, 0, s->s>>>(a);
+  else
+    k_apply_sgd<<<grid, block, 0, s->s>>>(a);
+  rc = launch_check("k_apply");
+  if (rc) return rc;
+  return record_event(s->device, s->s, ev_out);
+}
+
+int srf_reduce_max_f32(srf_space_t sp, uint64_t in_addr, uint64_t n,
+                       uint64_t out_addr, srf_stream_t st) {
+  int rc = check_raw(sp, in_addr, n * 4, "reduce input");
+  if (!rc) rc = check_raw(sp, out_addr, 4, "reduce output");
+  if (rc) return rc;
+  srf_stream *s = stream_or_default(sp, st);
+  uint64_t want = (n + 256 * 8 - 1) / (256 * 8);
+  uint64_t cap = std::min<uint64_t>((uint64_t)sm_count_of(s->device) * 4, kScratchBlocks);
+  int grid = (int)std::max<uint64_t>(1, std::min(want, cap));
+  CUDA_TRY(cudaSetDevice(s->device));
+  k_reduce_max<<<grid, 256, 0, s->s>>>((const float *)(sp->base + in_addr), n,
+                                       (float *)(sp->base + out_addr),
+                                       s->scratch, s->counter + 1);
+  return launch_check("k_reduce_max");
+}
+
+int srf_graph_begin(srf_stream_t st) {
+  CUDA_TRY(cudaSetDevice(st->device));
+  CUDA_TRY(cudaStreamBeginCapture(st->s, cudaStreamCaptureModeThreadLocal));
+  return SRF_OK;
+}
+
+int srf_graph_end(srf_stream_t st, void **graph_exec) {
+  CUDA_TRY(cudaSetDevice(st->device));
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(cudaStreamEndCapture(st->s, &g));
+  cudaGraphExec_t ex = nullptr;
+  cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess)
+    return fail(SRF_E_DEVICE, "graph instantiate: %s", cudaGetErrorString(e));
+  *graph_exec = (void *)ex;
+  return SRF_OK;
+}
+
+int srf_graph_launch(void *graph_exec, srf_stream_t st) {
+  CUDA_TRY(cudaSetDevice(st->device));
+  CUDA_TRY(cudaGraphLaunch((cudaGraphExec_t)graph_exec, st->s));
+  return SRF_OK;
+}
+
+int srf_graph_destroy(void *graph_exec) {
+  if (graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)graph_exec);
+  return SRF_OK;
+}
+
+int srf_stream_wait_event(srf_stream_t st, srf_event_t ev) {
+  CUDA_TRY(cudaSetDevice(st->device));
+  CUDA_TRY(cudaStreamWaitEvent(st->s, ev->e, 0));
+  return SRF_OK;
+}
+
+int srf_timing_event_create(srf_space_t sp, srf_event_t *out) {
+  CUDA_TRY(cudaSetDevice(sp->device));
+  srf_event *ev = new srf_event();
+  ev->device = sp->device;
+  cudaError_t e = cudaEventCreate(&ev->e);
+  if (e != cudaSuccess) {
+    delete ev;
+    return fail(SRF_E_DEVICE, "event: %s", cudaGetErrorString(e));
+  }
+  *out = ev;
+  return SRF_OK;
+}
+
+int srf_event_record_on(srf_event_t ev, srf_stream_t st) {
+  CUDA_TRY(cudaSetDevice(st->device));
+  CUDA_TRY(cudaEventRecord(ev->e, st->s));
+  return SRF_OK;
+}
+
+int srf_event_elapsed_ms(srf_event_t start, srf_event_t end, float *ms) {
+  CUDA_TRY(cudaEventElapsedTime(ms, start->e, end->e));
+  return SRF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,227 @@
+"""Host-side logic that needs no GPU: C-ABI exports, wire layouts, arena
+ledger, analyzer classification, partitioning, scheduler.  CPU only."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import random
+import re
+
+import numpy as np
+import pytest
+
+from paper_1805_08430_b200 import _lib, errors, wire
+from paper_1805_08430_b200.analyzer import classify_edges
+from paper_1805_08430_b200.graph import (DataFlowGraph, ExecMode, infer_shapes,
+                                         in_place_control_deps, partition, shape_of)
+from paper_1805_08430_b200.memspace import ArenaAllocator, RegionHandle
+from paper_1805_08430_b200.runtime.executor import Executor, FnHandler
+from paper_1805_08430_b200.wire import ElemType, Mechanism
+from paper_1805_08430_b200.workloads import (build_layered_forward, build_microbench,
+                                             build_ps_workload, total_params, vgg16_shapes)
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+# -- the C ABI -----------------------------------------------------------------------
+
+
+def header_functions() -> list[str]:
+    text = open(os.path.join(ROOT, "include", "srflow.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(srf_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _lib.load()
+    names = header_functions()
+    assert len(names) >= 30
+    for name in names:
+        assert hasattr(lib, name), f"{name} declared in include/srflow.h but not exported"
+    assert set(names) == set(_lib.SIGNATURES), "ctypes binding out of sync with the header"
+    assert lib.srf_version() == 1
+
+
+def test_library_is_sm100a():
+    so = _lib.LIB_PATH
+    out = os.popen(f"cuobjdump --list-elf {so} 2>/dev/null").read()
+    assert "sm_100a" in out, out
+
+
+def test_status_codes_map_to_reference_classes():
+    assert _lib._STATUS[13] is errors.NotRegistered
+    assert _lib._STATUS[14] is errors.BadToken
+    assert _lib._STATUS[15] is errors.RemoteOutOfBounds
+    assert issubclass(errors.RemoteOutOfBounds, errors.FabricError)
+    with pytest.raises(errors.BadToken):
+        _lib.check(14)
+    assert _lib.check(0) == 0 and _lib.check(1) == 1
+
+
+# -- wire (product) vs reference-generated vectors -------------------------------------
+
+
+def test_wire_matches_reference_vectors(golden):
+    doc, _ = golden
+    w = doc["wire"]
+    assert wire.encode_meta((3, 4), ElemType.F32, 0x1000, 0x42).hex() == w["formats_meta_hex"]
+    msg = wire.AddrExchangeMsg(7, 0x2A000, 0x1122334455667788, 49, Mechanism.DYNAMIC)
+    assert msg.encode().hex() == w["formats_addr_hex"]
+    assert wire.AddrExchangeMsg.decode(msg.encode()) == msg
+    for c in w["meta_cases"]:
+        raw = wire.encode_meta(c["dims"], ElemType(c["elem"]), c["addr"], c["token"])
+        assert raw.hex() == c["hex"]
+        m = wire.decode_meta(raw, len(c["dims"]))
+        assert list(m.dims) == c["dims"] and m.remote_token == c["token"]
+
+
+def test_wire_errors():
+    raw = wire.encode_meta((2, 2), ElemType.F32, 0, 0)
+    with pytest.raises(errors.RankMismatch):
+        wire.decode_meta(raw, 3)
+    with pytest.raises(errors.RankZero):
+        wire.encode_meta((), ElemType.F32, 0, 0)
+    bad = bytearray(raw)
+    bad[0] = 9
+    with pytest.raises(errors.BadElemType):
+        wire.decode_meta(bytes(bad), 2)
+    bad = bytearray(raw)
+    bad[-1] = 0
+    with pytest.raises(errors.WireError):
+        wire.decode_meta(bytes(bad), 2)
+    with pytest.raises(errors.LengthMismatch):
+        wire.decode_meta(raw[:-1], 2)
+    assert wire.static_region_size((1024, 1024), ElemType.F32) == 4_194_305
+    assert wire.meta_block_size(1) == 41 and wire.meta_block_size(2) == 49
+
+
+# -- arena ledger (memspace.py:239-308 semantics) ---------------------------------------
+
+
+class _FakeSpace:
+    server_id = 0
+
+
+def test_arena_ledger_replay():
+    backing = RegionHandle(0, 64, 1 << 20, 0xABC)
+    arena = ArenaAllocator(_FakeSpace(), backing)
+    rng = random.Random(7)
+    live: dict[int, int] = {}
+    for _ in range(1000):
+        if live and rng.random() < 0.45:
+            addr = rng.choice(sorted(live))
+            arena.free(RegionHandle(0, addr, live.pop(addr), 0xABC))
+        else:
+            n = rng.randint(1, 5000)
+            try:
+                h = arena.alloc(n)
+            except errors.ArenaExhausted:
+                continue
+            assert h.base_addr % 8 == 0 and h.access_token == 0xABC
+            live[h.base_addr] = n
+        assert arena.current_resident == sum(live.values())
+        blocks = arena.live_blocks()
+        for (o1, l1), (o2, _l2) in zip(blocks, blocks[1:]):
+            assert o1 + l1 <= o2
+    for addr in sorted(live):
+        arena.free(RegionHandle(0, addr, live[addr], 0xABC))
+    assert arena.current_resident == 0
+    assert arena.alloc((1 << 20) - 8).base_addr == 64  # fully coalesced
+    with pytest.raises(ValueError):
+        arena.free(RegionHandle(0, 12345, 8, 0))
+
+
+def test_arena_first_fit_reuse():
+    arena = ArenaAllocator(_FakeSpace(), RegionHandle(0, 0, 1 << 16, 1))
+    a, b, c = (arena.alloc(1024) for _ in range(3))
+    arena.free(b)
+    assert arena.alloc(1024).base_addr == b.base_addr
+    with pytest.raises(errors.ArenaExhausted):
+        arena.alloc((1 << 16) + 1)
+
+
+# -- analyzer / graph ------------------------------------------------------------------
+
+
+def test_ps_classification_matches_reference(golden):
+    doc, _ = golden
+    g, p = build_ps_workload(24_000, 2, 0.0, 2)
+    mech = classify_edges(partition(g, p), infer_shapes(g))
+    want = next(s for s in doc["sessions"] if s["name"] == "ps24k")["mechanisms"]
+    assert {f"{e}_{c}": int(m) for (e, c), m in mech.items()} == want
+    assert set(mech.values()) == {Mechanism.STATIC, Mechanism.DYNAMIC}
+    assert len(partition(g, p).cross) == 2 * 2 * 2  # weight + grad per (var, worker)
+
+
+def test_dynamic_cone_and_shapes():
+    g, _, cone = build_layered_forward(with_concat=True)
+    shapes = infer_shapes(g)
+    for e, s in shapes.items():
+        assert s.is_static == (e not in cone)
+
+
+def test_in_place_deps_order_readers_before_writers():
+    g, p = build_ps_workload(8_000, 1, 0.0, 3)
+    pg = partition(g, p)
+    ps = 3
+    ids = pg.nodes_on(ps)
+    deps = in_place_control_deps(ids, pg.node, lambda e: pg.consumers_on(e, ps))
+    applies = sorted(n for n in ids if pg.node(n).kind.value == "ApplyGrad")
+    for prev, nxt in zip(applies, applies[1:]):
+        assert prev in deps[nxt]
+    sends = [n for n in ids if pg.node(n).kind.value == "RdmaSend"]
+    assert all(s in deps[applies[0]] for s in sends)
+
+
+def test_vgg16_shapes():
+    shapes = vgg16_shapes()
+    assert len(shapes) == 32 and total_params(shapes) == 138_357_544
+
+
+def test_microbench_graph():
+    g, p = build_microbench(1 << 20)
+    pg = partition(g, p)
+    assert len(pg.cross) == 1
+    assert classify_edges(pg, infer_shapes(g))[(0, 1)] is Mechanism.STATIC
+
+
+# -- scheduler (runtime/executor.py semantics) ---------------------------------------------
+
+
+def test_pending_poll_reenqueues_at_tail_and_fairness():
+    ex = Executor(0, keep_trace=True)
+    done = []
+    for i in range(100):
+        ex.add_node(2 * i, FnHandler(ExecMode.POLLING_ASYNC, poll=lambda: None))
+        ex.add_node(2 * i + 1, FnHandler(run=lambda i=i: done.append(i)))
+    ex.begin_iteration(1)
+    steps = 0
+    while len(done) < 100:
+        ex.step()
+        steps += 1
+        assert steps <= 400
+    polls: dict[int, int] = {}
+    for _s, node, ev in ex.trace:
+        if ev == "poll_pending":
+            polls[node] = polls.get(node, 0) + 1
+    assert max(polls.values()) <= 2
+
+
+def test_watchdog_trips():
+    ex = Executor(0)
+    ex.add_node(0, FnHandler(ExecMode.POLLING_ASYNC, poll=lambda: None))
+    ex.begin_iteration(1)
+    with pytest.raises(errors.Deadlock):
+        ex.run_until_done(watchdog_steps=200)
+
+
+def test_ready_poll_completes_once():
+    seen = []
+    ex = Executor(0)
+    ex.add_node(0, FnHandler(ExecMode.POLLING_ASYNC, poll=lambda: "tok",
+                             complete=seen.append))
+    ex.begin_iteration(1)
+    ex.step()
+    assert not ex.done()
+    ex.step()
+    assert ex.done() and seen == ["tok"]

@@ -52,6 +52,10 @@ int srf_version(void);
 int srf_device_count(int *count);
 /* number of sm_100a kernels this library launched since load */
 uint64_t srf_launch_count(void);
+/* launch-geometry knobs of the copy kernels: 0 = CTAs per SM (1..32),
+ * 1 = threads per CTA (128/256/512), 2 = copy implementation (0 vector,
+ * 1 TMA bulk), 3 = pool allocator (0 cudaMalloc + CUDA IPC, 1 VMM + fd) */
+int srf_tune(int knob, int value);
 
 /* ---- memory spaces (memspace.py) ----------------------------------------- */
 /* MemorySpace.__init__ (memspace.py:98-113): one cudaMalloc(capacity) on
@@ -100,8 +104,15 @@ int srf_connect(srf_space_t a, srf_space_t b);
  * peer's exported pool as a remote space proxy; the proxy's region table is
  * filled with srf_region_import so remote checks stay identical. */
 int srf_space_export(srf_space_t space, void *handle64);
+/* enable direct peer access from `device` to `peer_device` (same process) */
+int srf_enable_peer(int device, int peer_device);
 int srf_space_import(const void *handle64, int server_id, int local_device,
                      uint64_t capacity, srf_space_t *out);
+/* VMM pools (knob 3 = 1): export the allocation as a POSIX fd and map a
+ * peer's fd (obtained through pidfd_getfd / SCM_RIGHTS) as a proxy */
+int srf_space_export_fd(srf_space_t space, int *fd);
+int srf_space_import_fd(int fd, int server_id, int local_device, uint64_t capacity,
+                        srf_space_t *out);
 int srf_region_import(srf_space_t proxy, int64_t region_id, uint64_t base,
                       uint64_t length, int registered, uint64_t token);
 

@@ -50,6 +50,7 @@ SIGNATURES = {
     "srf_version": (C.c_int, []),
     "srf_device_count": (C.c_int, [P(C.c_int)]),
     "srf_launch_count": (u64, []),
+    "srf_tune": (C.c_int, [C.c_int, C.c_int]),
     "srf_space_create": (C.c_int, [C.c_int, C.c_int, u64, C.c_uint32, P(vp)]),
     "srf_space_destroy": (C.c_int, [vp]),
     "srf_space_info": (C.c_int, [vp, P(C.c_int), P(C.c_int), P(u64), P(vp)]),
@@ -67,6 +68,9 @@ SIGNATURES = {
     "srf_space_sync": (C.c_int, [vp]),
     "srf_connect": (C.c_int, [vp, vp]),
     "srf_space_export": (C.c_int, [vp, vp]),
+    "srf_space_export_fd": (C.c_int, [vp, P(C.c_int)]),
+    "srf_space_import_fd": (C.c_int, [C.c_int, C.c_int, C.c_int, u64, P(vp)]),
+    "srf_enable_peer": (C.c_int, [C.c_int, C.c_int]),
     "srf_space_import": (C.c_int, [vp, C.c_int, C.c_int, u64, P(vp)]),
     "srf_region_import": (C.c_int, [vp, i64, u64, u64, C.c_int, u64]),
     "srf_stream_create": (C.c_int, [vp, P(vp)]),
@@ -117,7 +121,27 @@ def load() -> C.CDLL:
                 fn.restype = res
                 fn.argtypes = args
             _lib = lib
+            _apply_env_knobs(lib)
     return _lib
+
+
+_KNOBS = {"SRFLOW_CTAS_PER_SM": 0, "SRFLOW_COPY_THREADS": 1, "SRFLOW_PUT_IMPL": 2,
+          "SRFLOW_ALLOC_VMM": 3}
+
+
+def _apply_env_knobs(lib) -> None:
+    """Launch-geometry / implementation knobs from the environment."""
+    for name, knob in _KNOBS.items():
+        if name in os.environ:
+            rc = lib.srf_tune(knob, int(os.environ[name]))
+            if rc != SRF_OK:
+                raise errors.InvalidConfig(f"{name}={os.environ[name]}: "
+                                           f"{lib.srf_last_error().decode()}")
+
+
+def tune(knob: str, value: int) -> None:
+    call("srf_tune", {"ctas_per_sm": 0, "copy_threads": 1, "put_impl": 2,
+                      "alloc_vmm": 3}[knob], value)
 
 
 def last_error() -> str:

@@ -12,7 +12,9 @@
 //
 // Declarations and reference citations: include/srflow.h.
 
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -68,6 +70,10 @@ struct srf_stream {
 };
 
 struct srf_space {
+  bool vmm;                        // allocated with cuMemCreate (VMM) instead of cudaMalloc
+  CUmemGenericAllocationHandle mh; // VMM allocation (own or imported)
+  size_t map_size;
+  int export_fd;                   // POSIX fd of the exported VMM allocation (-1: none)
   int server_id;
   int device;
   uint64_t capacity;
@@ -89,6 +95,11 @@ struct srf_event {
 static constexpr uint64_t kAlign = 8;  // memspace.py:31 (_ALIGN)
 static constexpr int kMaxSeg = 8;
 static constexpr int kScratchBlocks = 1024;
+
+// launch-geometry knobs (srf_tune): CTAs per SM and threads per CTA of the
+// copy kernels; defaults chosen from the NVLink/HBM probes (profiles/).
+static int g_ctas_per_sm = 2;
+static int g_copy_threads = 512;
 
 static int sm_count_of(int device) {
   static int cache[64] = {0};
@@ -186,6 +197,115 @@ static int check_raw(const srf_space *sp, uint64_t addr, uint64_t len,
                 (unsigned long long)(addr + len),
                 (unsigned long long)sp->capacity);
   return SRF_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// CUDA VMM pools (cuMemCreate + POSIX-fd export).  Cross-process SM stores
+// through cudaIpcOpenMemHandle mappings measured ~500 GB/s vs ~690 GB/s
+// in-process (profiles/); VMM mappings are the alternative the multi-process
+// path can select (SRFLOW_ALLOC=vmm).  Driver entry points are resolved at
+// run time through cudaGetDriverEntryPoint, so no libcuda link is needed.
+// ---------------------------------------------------------------------------
+static int g_alloc_vmm = 0;
+
+template <typename F>
+static F drv(const char *name) {
+  void *p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return (F)p;
+}
+
+#define DRV_TRY(expr, what)                                                   \
+  do {                                                                        \
+    CUresult _r = (expr);                                                     \
+    if (_r != CUDA_SUCCESS)                                                   \
+      return fail(SRF_E_DEVICE, "%s failed (CUresult %d)", what, (int)_r);     \
+  } while (0)
+
+typedef CUresult (*PFN_memCreate)(CUmemGenericAllocationHandle *, size_t,
+                                  const CUmemAllocationProp *, unsigned long long);
+typedef CUresult (*PFN_memGran)(size_t *, const CUmemAllocationProp *,
+                                CUmemAllocationGranularity_flags);
+typedef CUresult (*PFN_addrReserve)(CUdeviceptr *, size_t, size_t, CUdeviceptr,
+                                    unsigned long long);
+typedef CUresult (*PFN_memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle,
+                               unsigned long long);
+typedef CUresult (*PFN_setAccess)(CUdeviceptr, size_t, const CUmemAccessDesc *, size_t);
+typedef CUresult (*PFN_export)(void *, CUmemGenericAllocationHandle, CUmemAllocationHandleType,
+                               unsigned long long);
+typedef CUresult (*PFN_import)(CUmemGenericAllocationHandle *, void *,
+                               CUmemAllocationHandleType);
+typedef CUresult (*PFN_unmap)(CUdeviceptr, size_t);
+typedef CUresult (*PFN_release)(CUmemGenericAllocationHandle);
+typedef CUresult (*PFN_addrFree)(CUdeviceptr, size_t);
+
+static size_t vmm_granularity(int device) {
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = device;
+  prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t g = 2 << 20;
+  auto gran = drv<PFN_memGran>("cuMemGetAllocationGranularity");
+  if (gran) gran(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
+  return g;
+}
+
+// map `h` (size bytes) at a fresh VA and grant `local` (+ every peer that
+// can reach it when all_peers) read/write access
+static int vmm_map(CUmemGenericAllocationHandle h, size_t size, int local, bool all_peers,
+                   uint8_t **out) {
+  auto reserve = drv<PFN_addrReserve>("cuMemAddressReserve");
+  auto map = drv<PFN_memMap>("cuMemMap");
+  auto access = drv<PFN_setAccess>("cuMemSetAccess");
+  if (!reserve || !map || !access) return fail(SRF_E_DEVICE, "VMM entry points missing");
+  CUdeviceptr va = 0;
+  DRV_TRY(reserve(&va, size, 2 << 20, 0, 0), "cuMemAddressReserve");
+  DRV_TRY(map(va, size, 0, h, 0), "cuMemMap");
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  std::vector<CUmemAccessDesc> acc;
+  for (int d = 0; d < ndev; ++d) {
+    int ok = (d == local);
+    if (!ok && all_peers) cudaDeviceCanAccessPeer(&ok, d, local);
+    if (!ok) continue;
+    CUmemAccessDesc a = {};
+    a.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    a.location.id = d;
+    a.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    acc.push_back(a);
+  }
+  DRV_TRY(access(va, size, acc.data(), acc.size()), "cuMemSetAccess");
+  *out = (uint8_t *)va;
+  return SRF_OK;
+}
+
+static int vmm_alloc(srf_space *sp) {
+  auto create = drv<PFN_memCreate>("cuMemCreate");
+  if (!create) return fail(SRF_E_DEVICE, "cuMemCreate unavailable");
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  prop.location.id = sp->device;
+  prop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t g = vmm_granularity(sp->device);
+  sp->map_size = (sp->capacity + g - 1) / g * g;
+  DRV_TRY(create(&sp->mh, sp->map_size, &prop, 0), "cuMemCreate");
+  return vmm_map(sp->mh, sp->map_size, sp->device, true, &sp->base);
+}
+
+static void vmm_free(srf_space *sp) {
+  auto unmap = drv<PFN_unmap>("cuMemUnmap");
+  auto release = drv<PFN_release>("cuMemRelease");
+  auto afree = drv<PFN_addrFree>("cuMemAddressFree");
+  if (unmap) unmap((CUdeviceptr)sp->base, sp->map_size);
+  if (afree) afree((CUdeviceptr)sp->base, sp->map_size);
+  if (release) release(sp->mh);
+  if (sp->export_fd >= 0) close(sp->export_fd);
 }
 
 // ---------------------------------------------------------------------------
@@ -358,6 +478,195 @@ __global__ void __launch_bounds__(512) k_put(PutArgs a) {
 
   if (!a.tail_release) return;
   // flag-last: all CTAs publish, the last to arrive releases the tail byte.
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    unsigned prev = atomicAdd(a.counter, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence_system();
+    const Seg &ls = a.seg[a.nseg - 1];
+    uint32_t v = ls.src[ls.len - 1];
+    st_release_sys_u8(tail, v);
+    atomicExch(a.counter, 0u);
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// TMA bulk-copy variant of K1/K4 (cp.async.bulk): one elected thread per CTA
+// streams 16 KB chunks global -> shared (mbarrier complete_tx) -> global
+// (bulk_group), kBulkStages chunks in flight.  Used for large 16-B co-aligned
+// segments; everything else takes the vector path.
+// ---------------------------------------------------------------------------
+static constexpr int kBulkChunk = 16384;
+static constexpr int kBulkStages = 6;
+static constexpr int kBulkSmem = kBulkChunk * kBulkStages + 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *smem, const void *gsrc,
+                                         uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], "
+      "[%1], %2, [%3];" ::"r"(smem_u32(smem)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_s2g(void *gdst, const void *smem,
+                                         uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                   gdst),
+               "r"(smem_u32(smem)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Thread 0 of every CTA: chunks blockIdx.x, +gridDim.x, ... of [src, src+n),
+// n a multiple of 16, both pointers 16-B aligned.
+__device__ void bulk_copy_cta(uint8_t *dst, const uint8_t *src, uint64_t n,
+                              uint8_t *stage, uint64_t *bars, uint32_t &use) {
+  const uint64_t nchunks = (n + kBulkChunk - 1) / kBulkChunk;
+  const uint64_t first = blockIdx.x, step = gridDim.x;
+  if (first >= nchunks) return;
+  const uint64_t mine = (nchunks - first + step - 1) / step;
+  auto chunk_of = [&](uint64_t k) { return first + k * step; };
+  auto bytes_of = [&](uint64_t c) {
+    uint64_t off = c * kBulkChunk;
+    return (uint32_t)((n - off) < (uint64_t)kBulkChunk ? (n - off) : kBulkChunk);
+  };
+  // prologue: fill all stages
+  const uint64_t pre = mine < (uint64_t)kBulkStages ? mine : kBulkStages;
+  for (uint64_t k = 0; k < pre; ++k) {
+    uint64_t c = chunk_of(k);
+    int slot = (int)(k % kBulkStages);
+    mbar_expect_tx(&bars[slot], bytes_of(c));
+    bulk_g2s(stage + slot * kBulkChunk, src + c * kBulkChunk, bytes_of(c), &bars[slot]);
+  }
+  for (uint64_t k = 0; k < mine; ++k) {
+    uint64_t c = chunk_of(k);
+    int slot = (int)(k % kBulkStages);
+    uint32_t parity = (uint32_t)((use + k / kBulkStages) & 1);
+    mbar_wait(&bars[slot], parity);
+    bulk_s2g(dst + c * kBulkChunk, stage + slot * kBulkChunk, bytes_of(c));
+    // refill the slot of chunk k-1 once its store has read shared memory
+    if (k >= 1 && k - 1 + kBulkStages < mine) {
+      bulk_wait_read<1>();
+      uint64_t kk = k - 1 + kBulkStages;
+      uint64_t cc = chunk_of(kk);
+      int s2 = (int)(kk % kBulkStages);
+      mbar_expect_tx(&bars[s2], bytes_of(cc));
+      bulk_g2s(stage + s2 * kBulkChunk, src + cc * kBulkChunk, bytes_of(cc), &bars[s2]);
+    }
+  }
+  bulk_wait_all();
+  // each barrier completed ceil-or-floor(mine / stages) phases; track per slot
+  // parity by the total number of uses (all slots advance together except
+  // the tail: keep slot phases in sync by counting uses per slot)
+  use += (uint32_t)((mine + kBulkStages - 1) / kBulkStages);
+}
+
+__global__ void __launch_bounds__(256) k_put_bulk(PutArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ int s_last;
+  uint64_t *bars = (uint64_t *)(smem + kBulkChunk * kBulkStages);
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  uint8_t *tail = a.dst + a.total - 1;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kBulkStages; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (a.wait_empty) {
+    if (threadIdx.x == 0) {
+      uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_sys_u8(tail) != 0) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          atomicExch(a.err, 2);
+          break;
+        }
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+  }
+  uint64_t body = a.tail_release ? a.total - 1 : a.total;
+  uint32_t use = 0;  // uses per barrier so far (same for every slot: see below)
+  for (int i = 0; i < a.nseg; ++i) {
+    const Seg &sg = a.seg[i];
+    if (sg.dst_off >= body) break;
+    uint64_t n = sg.len;
+    if (sg.dst_off + n > body) n = body - sg.dst_off;
+    uint8_t *d = a.dst + sg.dst_off;
+    const uint8_t *s = sg.src;
+    uintptr_t dp = (uintptr_t)d, sp = (uintptr_t)s;
+    if (n >= (uint64_t)4 * kBulkChunk && ((dp ^ sp) & 15) == 0) {
+      uint64_t head = (16 - (dp & 15)) & 15;
+      uint64_t mid = ((n - head) / 16) * 16;
+      for (uint64_t j = t; j < head; j += nth) d[j] = s[j];
+      for (uint64_t j = head + mid + t; j < n; j += nth) d[j] = s[j];
+      if (threadIdx.x == 0) {
+        // barriers are reused across segments: realign every slot's phase by
+        // running complete rounds only (mine is rounded inside), so track use
+        bulk_copy_cta(d + head, s + head, mid, smem, bars, use);
+      }
+      __syncthreads();
+      // re-initialise the barriers for the next segment (phases may differ
+      // between slots after a partial round)
+      if (threadIdx.x == 0) {
+        for (int b = 0; b < kBulkStages; ++b) {
+          asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[b])));
+          mbar_init(&bars[b], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        use = 0;
+      }
+      __syncthreads();
+    } else {
+      copy_bytes_grid(d, s, n, t, nth);
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+  if (!a.tail_release) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
@@ -650,11 +959,11 @@ __global__ void __launch_bounds__(256) k_reduce_max(const float *x, uint64_t n,
 // launch geometry
 // ---------------------------------------------------------------------------
 static void copy_geometry(int device, uint64_t bytes, int *grid, int *block) {
-  const int threads = 512;
-  // one CTA moves threads * 16 B * 4 per unrolled batch; cap at 2 CTAs/SM
+  const int threads = g_copy_threads;
+  // one CTA moves threads * 16 B * 4 per unrolled batch; cap at k CTAs/SM
   uint64_t per_cta = (uint64_t)threads * 16 * 4;
   uint64_t want = (bytes + per_cta - 1) / per_cta;
-  uint64_t cap = (uint64_t)sm_count_of(device) * 2;
+  uint64_t cap = (uint64_t)sm_count_of(device) * g_ctas_per_sm;
   if (want < 1) want = 1;
   if (want > cap) want = cap;
   *grid = (int)want;
@@ -683,6 +992,31 @@ static int launch_check(const char *what) {
   return SRF_OK;
 }
 
+static int g_put_impl = 0;  // 0 = vector LDG/STG, 1 = TMA bulk (large segments)
+
+// launch K1/K4/K5 with the configured implementation
+static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
+  uint64_t big = 0;
+  for (int i = 0; i < a.nseg; ++i) big = std::max<uint64_t>(big, a.seg[i].len);
+  if (g_put_impl == 1 && big >= (uint64_t)4 * kBulkChunk) {
+    static bool attr_set[64] = {false};
+    if (s->device >= 0 && s->device < 64 && !attr_set[s->device]) {
+      CUDA_TRY(cudaFuncSetAttribute(k_put_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kBulkSmem));
+      attr_set[s->device] = true;
+    }
+    uint64_t chunks = (a.total + kBulkChunk - 1) / kBulkChunk;
+    uint64_t cap = (uint64_t)sm_count_of(s->device) * 2;
+    int grid = (int)std::max<uint64_t>(1, std::min(chunks, cap));
+    k_put_bulk<<<grid, 256, kBulkSmem, s->s>>>(a);
+  } else {
+    int grid, block;
+    copy_geometry(s->device, a.total, &grid, &block);
+    k_put<<<grid, block, 0, s->s>>>(a);
+  }
+  return launch_check(what);
+}
+
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
@@ -690,6 +1024,30 @@ extern "C" {
 
 const char *srf_last_error(void) { return g_last_error.c_str(); }
 int srf_version(void) { return 1; }
+
+int srf_tune(int knob, int value) {
+  switch (knob) {
+    case 0:
+      if (value < 1 || value > 32) return fail(SRF_E_INVALID_CONFIG, "ctas_per_sm");
+      g_ctas_per_sm = value;
+      return SRF_OK;
+    case 1:
+      if (value != 128 && value != 256 && value != 512)
+        return fail(SRF_E_INVALID_CONFIG, "copy threads must be 128, 256 or 512");
+      g_copy_threads = value;
+      return SRF_OK;
+    case 2:
+      if (value != 0 && value != 1) return fail(SRF_E_INVALID_CONFIG, "put impl 0|1");
+      g_put_impl = value;
+      return SRF_OK;
+    case 3:
+      if (value != 0 && value != 1) return fail(SRF_E_INVALID_CONFIG, "alloc 0=cudaMalloc|1=vmm");
+      g_alloc_vmm = value;
+      return SRF_OK;
+    default:
+      return fail(SRF_E_INVALID_CONFIG, "unknown knob %d", knob);
+  }
+}
 uint64_t srf_launch_count(void) { return g_launches.load(); }
 
 int srf_device_count(int *count) {
@@ -716,12 +1074,25 @@ int srf_space_create(int server_id, int cuda_device, uint64_t capacity,
   sp->next_addr = 0;
   sp->stream = nullptr;
   sp->err = nullptr;
-  cudaError_t e = cudaMalloc(&sp->base, capacity);
-  if (e != cudaSuccess) {
-    delete sp;
-    return fail(SRF_E_OUT_OF_MEMORY, "server %d: cudaMalloc(%llu): %s",
-                server_id, (unsigned long long)capacity, cudaGetErrorString(e));
+  sp->vmm = g_alloc_vmm != 0;
+  sp->export_fd = -1;
+  sp->map_size = 0;
+  if (sp->vmm) {
+    cudaFree(0);  // make the primary context current for the driver calls
+    int rc0 = vmm_alloc(sp);
+    if (rc0 != SRF_OK) {
+      delete sp;
+      return rc0;
+    }
+  } else {
+    cudaError_t e0 = cudaMalloc(&sp->base, capacity);
+    if (e0 != cudaSuccess) {
+      delete sp;
+      return fail(SRF_E_OUT_OF_MEMORY, "server %d: cudaMalloc(%llu): %s",
+                  server_id, (unsigned long long)capacity, cudaGetErrorString(e0));
+    }
   }
+  cudaError_t e;
   int rc = make_stream(cuda_device, true, nullptr, &sp->stream);
   if (rc == SRF_OK) {
     e = cudaMalloc(&sp->err, sizeof(int));
@@ -733,7 +1104,10 @@ int srf_space_create(int server_id, int cuda_device, uint64_t capacity,
   }
   if (rc != SRF_OK) {
     free_stream(sp->stream);
-    cudaFree(sp->base);
+    if (sp->vmm)
+      vmm_free(sp);
+    else
+      cudaFree(sp->base);
     if (sp->err) cudaFree(sp->err);
     delete sp;
     return rc;
@@ -746,7 +1120,9 @@ int srf_space_destroy(srf_space_t sp) {
   if (!sp) return SRF_OK;
   cudaSetDevice(sp->device);
   free_stream(sp->stream);
-  if (sp->imported)
+  if (sp->vmm)
+    vmm_free(sp);
+  else if (sp->imported)
     cudaIpcCloseMemHandle(sp->base);
   else
     cudaFree(sp->base);
@@ -913,9 +1289,77 @@ int srf_connect(srf_space_t a, srf_space_t b) {
   return SRF_OK;
 }
 
+int srf_enable_peer(int device, int peer_device) {
+  if (device == peer_device) return SRF_OK;
+  CUDA_TRY(cudaSetDevice(device));
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return SRF_OK;
+  }
+  if (e != cudaSuccess)
+    return fail(SRF_E_PEER_UNREACHABLE, "enable peer %d->%d: %s", device, peer_device,
+                cudaGetErrorString(e));
+  return SRF_OK;
+}
+
+int srf_space_export_fd(srf_space_t sp, int *fd) {
+  if (!sp->vmm || sp->imported)
+    return fail(SRF_E_INVALID_CONFIG, "fd export needs a VMM-allocated local space");
+  if (sp->export_fd < 0) {
+    auto exp = drv<PFN_export>("cuMemExportToShareableHandle");
+    if (!exp) return fail(SRF_E_DEVICE, "cuMemExportToShareableHandle unavailable");
+    int f = -1;
+    DRV_TRY(exp(&f, sp->mh, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0),
+            "cuMemExportToShareableHandle");
+    sp->export_fd = f;
+  }
+  *fd = sp->export_fd;
+  return SRF_OK;
+}
+
+int srf_space_import_fd(int fd, int server_id, int local_device, uint64_t capacity,
+                        srf_space_t *out) {
+  CUDA_TRY(cudaSetDevice(local_device));
+  cudaFree(0);
+  auto imp = drv<PFN_import>("cuMemImportFromShareableHandle");
+  if (!imp) return fail(SRF_E_DEVICE, "cuMemImportFromShareableHandle unavailable");
+  srf_space *sp = new srf_space();
+  sp->vmm = true;
+  sp->imported = true;
+  sp->export_fd = -1;
+  sp->server_id = server_id;
+  sp->device = local_device;
+  sp->capacity = capacity;
+  sp->max_regions = 1u << 30;
+  sp->next_addr = 0;
+  sp->err = nullptr;
+  size_t g = vmm_granularity(local_device);
+  sp->map_size = (capacity + g - 1) / g * g;
+  CUresult r = imp(&sp->mh, (void *)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+  if (r != CUDA_SUCCESS) {
+    delete sp;
+    return fail(SRF_E_DEVICE, "cuMemImportFromShareableHandle (CUresult %d)", (int)r);
+  }
+  int rc = vmm_map(sp->mh, sp->map_size, local_device, false, &sp->base);
+  if (rc == SRF_OK) rc = make_stream(local_device, true, nullptr, &sp->stream);
+  if (rc == SRF_OK) {
+    cudaError_t e = cudaMalloc(&sp->err, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(sp->err, 0, sizeof(int));
+    if (e != cudaSuccess) rc = fail(SRF_E_DEVICE, "proxy: %s", cudaGetErrorString(e));
+  }
+  if (rc != SRF_OK) {
+    delete sp;
+    return rc;
+  }
+  *out = sp;
+  return SRF_OK;
+}
+
 int srf_space_export(srf_space_t sp, void *handle64) {
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
   if (sp->imported) return fail(SRF_E_INVALID_CONFIG, "cannot re-export a proxy");
+  if (sp->vmm) return fail(SRF_E_INVALID_CONFIG, "VMM pools export by fd (srf_space_export_fd)");
   CUDA_TRY(cudaSetDevice(sp->device));
   cudaIpcMemHandle_t h;
   CUDA_TRY(cudaIpcGetMemHandle(&h, sp->base));
@@ -931,6 +1375,9 @@ int srf_space_import(const void *handle64, int server_id, int local_device,
   void *p = nullptr;
   CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
   srf_space *sp = new srf_space();
+  sp->vmm = false;
+  sp->export_fd = -1;
+  sp->map_size = 0;
   sp->server_id = server_id;
   sp->device = local_device;  // work on the proxy is issued from this GPU
   sp->capacity = capacity;
@@ -1040,11 +1487,8 @@ int srf_put(srf_space_t src_space, const uint64_t *src_addr,
   a.timeout_ns = 5ull * 1000 * 1000 * 1000;
   a.counter = s->counter;
   a.err = src_space->err;
-  int grid, block;
-  copy_geometry(s->device, total, &grid, &block);
   CUDA_TRY(cudaSetDevice(s->device));
-  k_put<<<grid, block, 0, s->s>>>(a);
-  int rc = launch_check("k_put");
+  int rc = launch_copy(a, s, "k_put");
   if (rc) return rc;
   return record_event(s->device, s->s, ev_out);
 }
@@ -1075,11 +1519,8 @@ int srf_get(srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
   a.tail_release = 0;
   a.counter = s->counter;
   a.err = dst_space->err;
-  int grid, block;
-  copy_geometry(s->device, length, &grid, &block);
   CUDA_TRY(cudaSetDevice(s->device));
-  k_put<<<grid, block, 0, s->s>>>(a);
-  int rc = launch_check("k_put(get)");
+  int rc = launch_copy(a, s, "k_put(get)");
   if (rc) return rc;
   return record_event(s->device, s->s, ev_out);
 }
@@ -1100,11 +1541,8 @@ int srf_copy(srf_space_t sp, uint64_t src_addr, uint64_t dst_addr,
   a.total = length;
   a.counter = s->counter;
   a.err = sp->err;
-  int grid, block;
-  copy_geometry(s->device, length, &grid, &block);
   CUDA_TRY(cudaSetDevice(s->device));
-  k_put<<<grid, block, 0, s->s>>>(a);
-  rc = launch_check("k_put(copy)");
+  rc = launch_copy(a, s, "k_put(copy)");
   if (rc) return rc;
   return record_event(s->device, s->s, ev_out);
 }

@@ -103,6 +103,21 @@ def default_device(server_id: int) -> int:
     return server_id % n
 
 
+def _fetch_fd(pid: int, fd: int) -> int:
+    """Duplicate file descriptor ``fd`` of process ``pid`` into this process
+    (pidfd_getfd, Linux >= 5.6)."""
+    libc = C.CDLL(None, use_errno=True)
+    pidfd = os.pidfd_open(pid)
+    try:
+        got = libc.syscall(438, pidfd, fd, 0)  # SYS_pidfd_getfd on x86_64
+        if got < 0:
+            err = C.get_errno()
+            raise errors.PeerUnreachable(f"pidfd_getfd({pid}, {fd}): {os.strerror(err)}")
+        return got
+    finally:
+        os.close(pidfd)
+
+
 class _CudaArray:
     """Minimal __cuda_array_interface__ exporter for zero-copy torch views."""
 
@@ -160,12 +175,20 @@ class MemorySpace:
     # -- multi-process: export / import (one process per GPU) -------------------
 
     def export(self) -> dict:
-        """Descriptor a peer process needs to map this pool over NVLink:
-        the CUDA IPC handle plus the region table (for identical checks)."""
+        """Descriptor a peer process needs to map this pool over NVLink: the
+        CUDA IPC handle (cudaMalloc pools) or (pid, fd) of the VMM allocation
+        (SRFLOW_ALLOC_VMM=1 pools), plus the region table for identical checks."""
+        desc = {"server_id": self.server_id, "capacity": self.capacity,
+                "regions": list(self.regions)}
         buf = (C.c_uint8 * 64)()
-        _lib.call("srf_space_export", self._h, buf)
-        return {"server_id": self.server_id, "capacity": self.capacity,
-                "ipc": bytes(buf), "regions": list(self.regions)}
+        try:
+            _lib.call("srf_space_export", self._h, buf)
+            desc["ipc"] = bytes(buf)
+        except errors.InvalidConfig:
+            fd = C.c_int()
+            _lib.call("srf_space_export_fd", self._h, C.byref(fd))
+            desc["pid"], desc["fd"] = os.getpid(), fd.value
+        return desc
 
     @classmethod
     def import_remote(cls, desc: dict, local_device: int) -> "MemorySpace":
@@ -185,9 +208,17 @@ class MemorySpace:
         self.regions = list(desc["regions"])
         self.remote = True
         h = C.c_void_p()
-        ipc = (C.c_uint8 * 64).from_buffer_copy(desc["ipc"])
-        _lib.call("srf_space_import", ipc, self.server_id, local_device, self.capacity,
-                  C.byref(h))
+        if "ipc" in desc:
+            ipc = (C.c_uint8 * 64).from_buffer_copy(desc["ipc"])
+            _lib.call("srf_space_import", ipc, self.server_id, local_device, self.capacity,
+                      C.byref(h))
+        else:
+            fd = _fetch_fd(desc["pid"], desc["fd"])
+            try:
+                _lib.call("srf_space_import_fd", fd, self.server_id, local_device,
+                          self.capacity, C.byref(h))
+            finally:
+                os.close(fd)
         self._h = h
         for rid, base, length, reg, token in self.regions:
             _lib.call("srf_region_import", h, rid, base, length, int(reg), token)

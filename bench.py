@@ -559,6 +559,95 @@ def dynamic_rate(size, device, reps=None):
     return {"dynamic_gbps": round(size / dt / 1e9, 3), "dynamic_us": round(dt * 1e6, 2)}
 
 
+# -- parameter-server step (configs[3]: VGG-16 sharded over the GPUs) ---------------------------------
+
+
+def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True):
+    """Device-timed PS iterations/s.  N=1: worker server 0 + PS server 1 on one
+    GPU (SURVEY 8(d) C4, G=1).  N>1: worker k + shard k co-located on GPU k,
+    variables round-robin over the shards (workloads.py:83-85)."""
+    from oracle import port
+    from paper_1805_08430_b200 import _lib
+    from paper_1805_08430_b200.ps import PsLayout, PsStep
+    from paper_1805_08430_b200.workloads import total_params, vgg16_shapes
+    shapes = shapes or vgg16_shapes()
+    L = PsLayout(shapes, 1, 1) if world == 1 else PsLayout(shapes, world, world, colocate=True)
+    ps = PsStep(L, rank=rank, world=world, device=device, seed=0, op=op, lr=0.01)
+    it = 0
+    for _ in range(warmup):
+        it += 1
+        ps.step(it)
+    ps.sync()
+    barrier_sync()
+    ev = [C.c_void_p(), C.c_void_p()]
+    sp0 = ps.spaces[ps.local[0]]
+    for e in ev:
+        _lib.call("srf_timing_event_create", sp0.handle, C.byref(e))
+    clocks = ClockSampler(device)
+    clocks.start()
+    barrier_sync()
+    l0 = _lib.launch_count()
+    _lib.call("srf_event_record_on", ev[0], ps.stream)
+    for _ in range(steps):
+        it += 1
+        ps.step(it)
+    _lib.call("srf_event_record_on", ev[1], ps.stream)
+    ps.sync()
+    launches = int(dist_sum(_lib.launch_count() - l0))
+    barrier_sync()
+    clk = clocks.stop()
+    ms = C.c_float()
+    _lib.call("srf_event_elapsed_ms", ev[0], ev[1], C.byref(ms))
+    t = dist_max(ms.value / 1e3)
+    # verify the smallest variable this rank owns against the oracle replay
+    mine = [v for v in range(len(shapes)) if L.shard_of(v) % world == rank]
+    ok = True
+    if mine:
+        v = min(mine, key=L.nbytes)
+        want = port.ps_expected_device(shapes, L.workers, 0, range(1, it + 1), op=op, lr=0.01,
+                                       only=[v])[v]
+        ok = ps.variable(v).tobytes() == want.tobytes()
+    ok = dist_sum(0.0 if ok else 1.0) == 0.0
+    # roofline over the busiest GPU
+    tr = [L.traffic(s) for s in range(L.nservers)]
+    model = sum(L.nbytes(v) for v in range(len(shapes)))
+    if world == 1:
+        alg = sum(2 * x["push_out"] + x["pull_in"] + x["hbm"] for x in tr)
+        peak, _src = measured_peaks()
+        ach = alg * steps / t / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "bytes_per_step": alg}
+    else:
+        per_gpu = [max(x["push_out"] + x["meta_out"], x["pull_in"]) for x in tr]
+        hot = max(range(world), key=lambda s: per_gpu[s])
+        ach = per_gpu[hot] * steps / t / 1e9
+        roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_MEASURED_GBS,
+                "unit": "GB/s", "frac": round(ach / NVLINK_MEASURED_GBS, 4),
+                "hottest_gpu": hot, "hottest_bytes_per_step": per_gpu[hot],
+                "note": "round-robin placement puts fc6 (411 MB) on shard 2 (SURVEY F5)"}
+    out = {"workload": f"configs[3] VGG-16 real shapes ({total_params(shapes)} fp32, "
+                       f"{len(shapes)} tensors) PS sync, op={op} lr=0.01, "
+                       + ("worker server 0 + PS server 1 on GPU 0" if world == 1
+                          else f"{world} workers + {world} shards co-located"),
+           "steps_per_s": round(steps / t, 2), "ms_per_step": round(t / steps * 1e3, 4),
+           "steps": steps, "model_bytes": model, "roofline": roof, "gpu_launches": launches,
+           "clocks": clk, "verified": ok,
+           "phases": "K1 weight push batch, GenGrad batch, K3 meta batch, K4+K6 fused apply"}
+    ps.close()
+    if cpu and rank == 0 and world == 1:
+        rig = port.PsRig(shapes, 1, 1, False, seed=0, op=op, lr=0.01)
+        t0 = time.perf_counter()
+        rig.step()
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": round(1.0 / dt, 4), "unit": "steps/s", "cores": 1,
+                               "kind": "port",
+                               "sample": "1 PS iteration of the same VGG-16 config "
+                                         "(oracle/port.py PsRig: chunked static pushes, "
+                                         "PCG64 GenGrad, meta + chunked pulls, ApplyGrad), "
+                                         f"{dt:.1f} s, host cpu_count={os.cpu_count()}"}
+    return out
+
+
 # -- main -------------------------------------------------------------------------------------------
 
 
@@ -572,6 +661,8 @@ def main() -> int:
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-ps", action="store_true")
+    ap.add_argument("--ps-op", choices=("sgd", "xor"), default="sgd")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -637,9 +728,12 @@ def main() -> int:
                       f"host cpu_count={os.cpu_count()}"}
     if world == 1 and not args.no_sweep:
         line["sweep"] = sweep(S, local)
+    if not args.no_ps:
+        line["ps"] = bench_ps(rank, world, local, max(10, args.steps), args.warmup,
+                              op=args.ps_op, cpu=not args.no_cpu)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if not dev["verified"] or not e2e["verified"]:
+    if not dev["verified"] or not e2e["verified"] or not line.get("ps", {}).get("verified", True):
         log("verification FAILED")
         return 1
     return 0

@@ -193,6 +193,45 @@ int srf_apply(srf_space_t var_space, uint64_t var_addr, uint64_t nbytes,
               int nworkers, int op, float lr, srf_stream_t stream,
               srf_event_t *ev_out);
 
+/* ---- batched PS step (configs[2..4]) ------------------------------------
+ * One launch per phase per step over descriptor lists that are validated
+ * once at creation (registration, token and bounds checks of every edge, the
+ * same gates srf_put applies per verb).  Phases of one PS iteration
+ * (runtime/session.py:606-629 over workloads.py:59-94):
+ *   put batch   - K1 weight pushes shard -> workers (static placement) and
+ *                 K3 metadata writes workers -> shards (dynamic allocation);
+ *                 body then tail byte released last; flags SRF_PUT_WAIT_EMPTY
+ *   gen batch   - per worker x variable: acquire the weight flag (consume +
+ *                 clear, StaticReceiver.poll), wait for the shard's credit
+ *                 (meta flag clear), then (mode 1) produce the synthetic
+ *                 gradient on the device (GenGrad stand-in) or (mode 0)
+ *                 keep the host-uploaded one
+ *   apply batch - per variable: DynReceiver.poll + decode_meta + validation
+ *                 on the device, then K4+K6 fused: the update reads every
+ *                 remote gradient straight through the peer mapping (no
+ *                 local copy) and folds all workers in ascending order
+ *                 (XOR or SGD); clears the meta flags.
+ * Descriptor arrays are parallel; for the apply batch the per-(variable,
+ * worker) arrays are flattened in ascending worker order. */
+typedef struct srf_batch *srf_batch_t;
+int srf_batch_put_create(int n, srf_space_t const *src_space, const uint64_t *src_addr,
+                         const uint64_t *body_len, const uint64_t *src_token,
+                         const uint64_t *tail_addr, srf_space_t const *dst_space,
+                         const uint64_t *dst_addr, const uint64_t *dst_token, int flags,
+                         srf_batch_t *out);
+int srf_batch_gen_create(srf_space_t space, int n, const uint64_t *grad_addr,
+                         const uint64_t *nbytes, const uint64_t *weight_flag_addr,
+                         srf_space_t const *credit_space, const uint64_t *credit_addr,
+                         const uint64_t *node_id, uint64_t seed, srf_batch_t *out);
+int srf_batch_apply_create(srf_space_t space, int nvars, const uint64_t *var_addr,
+                           const uint64_t *nbytes, const int *nworkers, const int *rank,
+                           srf_space_t const *src_space, const uint64_t *src_addr,
+                           const int *is_meta, srf_space_t const *peer_space,
+                           const uint64_t *peer_lo, const uint64_t *peer_hi,
+                           const uint64_t *peer_token, int op, float lr, srf_batch_t *out);
+int srf_batch_launch(srf_batch_t batch, srf_stream_t stream, uint64_t iteration, int mode);
+int srf_batch_destroy(srf_batch_t batch);
+
 /* ReduceMax consumer of the microbenchmark (graph.py:378-382) on the
  * receiving GPU: out_addr receives max over n fp32 at in_addr. */
 int srf_reduce_max_f32(srf_space_t space, uint64_t in_addr, uint64_t n,

@@ -475,3 +475,56 @@ class PsRig:
     def variable(self, v: int) -> np.ndarray:
         shard, a, nb = self.vars[v]
         return self.spaces[shard].mem[a:a + nb].view(np.float32).reshape(self.shapes[v])
+
+
+# -- device-side GenGrad stand-in (not a reference function) -----------------------------
+# The timed PS step regenerates synthetic gradients on the GPU with a
+# counter-based hash (k_gen_batch in paper_1805_08430_b200/csrc/srflow.cu)
+# instead of the reference's host PCG64 stream.  This restatement lets the
+# tests check those device gradients and the variables they produce.
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def _mix64(x: np.ndarray) -> np.ndarray:
+    x = x.astype(np.uint64, copy=True)
+    x ^= x >> np.uint64(30)
+    x *= np.uint64(0xBF58476D1CE4E5B9)
+    x ^= x >> np.uint64(27)
+    x *= np.uint64(0x94D049BB133111EB)
+    x ^= x >> np.uint64(31)
+    return x
+
+
+def device_gradient(seed: int, node: int, iteration: int, n: int) -> np.ndarray:
+    """fp32 values k_gen_batch writes for GenGrad node ``node`` at ``iteration``."""
+    with np.errstate(over="ignore"):
+        s = np.array([seed], dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+        a = _mix64(np.array([node], dtype=np.uint64) + np.uint64(0x51ED))
+        b = _mix64(np.array([iteration], dtype=np.uint64) * np.uint64(0xD1B54A32D192ED03))
+        key = _mix64(s ^ a ^ b)[0]
+        idx = np.arange(n, dtype=np.uint64)
+        h = _mix64(key + idx * np.uint64(0x9E3779B97F4A7C15))
+    return ((h >> np.uint64(40)).astype(np.float32) * np.float32(1.0 / 16777216.0))
+
+
+def ps_expected_device(shapes, workers: int, seed: int, iterations, op: str = "xor",
+                       lr: float = 0.01, only=None) -> list[np.ndarray]:
+    """Variables after PS iterations whose gradients come from device_gradient
+    (``only``: restrict to these variable indices; others are None)."""
+    out = []
+    for v, dims in enumerate(shapes):
+        if only is not None and v not in only:
+            out.append(None)
+            continue
+        n = math.prod(dims)
+        val = synthesize(n, 0, node_rng(seed, ps_node_ids(v, 0, workers)[0], 0)).copy()
+        for it in iterations:
+            grads = [device_gradient(seed, ps_node_ids(v, w, workers)[1], it, n)
+                     for w in range(workers)]
+            if op == "xor":
+                apply_xor(val, grads)
+            else:
+                apply_sgd(val, grads, lr)
+        out.append(val.reshape(dims))
+    return out

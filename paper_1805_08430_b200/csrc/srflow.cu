@@ -849,9 +849,7 @@ __device__ __forceinline__ void sgd_body_v4(const ApplyArgs &a, uint64_t off,
   }
 }
 
-__global__ void __launch_bounds__(512) k_apply_xor(ApplyArgs a) {
-  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ void apply_xor_range(const ApplyArgs &a, uint64_t t, uint64_t nth) {
   uintptr_t m = (uintptr_t)a.var;
   bool same16 = true, same8 = true;
   for (int w = 0; w < a.nw; ++w) {
@@ -883,9 +881,7 @@ __global__ void __launch_bounds__(512) k_apply_xor(ApplyArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(512) k_apply_sgd(ApplyArgs a) {
-  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ void apply_sgd_range(const ApplyArgs &a, uint64_t t, uint64_t nth) {
   uintptr_t m = (uintptr_t)a.var;
   bool same16 = true;
   for (int w = 0; w < a.nw; ++w) same16 &= (((uintptr_t)a.g[w] ^ m) & 15) == 0;
@@ -905,6 +901,220 @@ __global__ void __launch_bounds__(512) k_apply_sgd(ApplyArgs a) {
     float v = var[i];
     for (int w = 0; w < a.nw; ++w) v = sgd1(v, a.lr, ((const float *)a.g[w])[i]);
     var[i] = v;
+  }
+}
+
+__global__ void __launch_bounds__(512) k_apply_xor(ApplyArgs a) {
+  apply_xor_range(a, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                  (uint64_t)gridDim.x * blockDim.x);
+}
+
+__global__ void __launch_bounds__(512) k_apply_sgd(ApplyArgs a) {
+  apply_sgd_range(a, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                  (uint64_t)gridDim.x * blockDim.x);
+}
+
+// ---------------------------------------------------------------------------
+// Batched PS step kernels (one launch per phase per step; descriptors live in
+// device memory, validated once at creation like a registered verb list).
+// ---------------------------------------------------------------------------
+struct BatchPut {        // K1/K3 over many edges
+  const uint8_t *src;    // body source
+  uint8_t *dst;          // destination (peer or local)
+  uint64_t body;         // bytes before the tail
+  const uint8_t *tail;   // tail byte source (flag cell / meta flag)
+  uint32_t cta_begin, cta_count;
+  uint32_t wait_empty, pad;
+};
+
+struct BatchGen {        // worker: consume weight, (re)produce gradient
+  uint8_t *grad;
+  uint64_t n;            // bytes (fp32 elements * 4)
+  uint8_t *weight_flag;  // local static region tail (nullptr: local variable)
+  const uint8_t *credit; // shard-side meta tail that must read 0 (nullptr: none)
+  uint64_t node;         // GenGrad node id (RNG stream key)
+  uint32_t cta_begin, cta_count;
+};
+
+struct BatchApply {      // shard: fused dynamic receive (meta decode + peer
+  uint8_t *var;          // reads) + ApplyGrad of all workers, ascending
+  uint64_t n;
+  const uint8_t *src[SRF_MAX_WORKERS];   // local gradient, or meta block
+  const uint8_t *peer_base[SRF_MAX_WORKERS];
+  uint64_t peer_lo[SRF_MAX_WORKERS], peer_hi[SRF_MAX_WORKERS];
+  uint64_t peer_token[SRF_MAX_WORKERS];
+  uint32_t is_meta;      // bit w: src[w] is a meta block
+  int nw, rank;
+  uint32_t cta_begin, cta_count;
+};
+
+template <typename D>
+__device__ __forceinline__ int find_desc(const D *d, int n) {
+  // largest i with d[i].cta_begin <= blockIdx.x
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (d[mid].cta_begin <= blockIdx.x) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ bool spin_until(const uint8_t *p, uint32_t want,
+                                           uint64_t timeout_ns) {
+  uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_sys_u8(p) != want) {
+    if (globaltimer_ns() - t0 > timeout_ns) return false;
+    __nanosleep(64);
+  }
+  return true;
+}
+
+__global__ void __launch_bounds__(512) k_put_batch(const BatchPut *descs, int n,
+                                                   unsigned int *counters,
+                                                   uint64_t timeout_ns, int *err) {
+  __shared__ int s_desc, s_last;
+  if (threadIdx.x == 0) s_desc = find_desc(descs, n);
+  __syncthreads();
+  const BatchPut d = descs[s_desc];
+  const uint32_t lb = blockIdx.x - d.cta_begin;
+  if (d.wait_empty) {
+    if (threadIdx.x == 0 && !spin_until(d.dst + d.body, 0, timeout_ns)) atomicExch(err, 2);
+    __syncthreads();
+  }
+  copy_bytes_grid(d.dst, d.src, d.body, (uint64_t)lb * blockDim.x + threadIdx.x,
+                  (uint64_t)d.cta_count * blockDim.x);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(&counters[s_desc], 1u) == d.cta_count - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys_u8(d.dst + d.body, *d.tail);
+    atomicExch(&counters[s_desc], 0u);
+  }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+
+// uniform [0,1) fp32 of a counter-based stream keyed on (seed, node, iteration)
+__device__ __forceinline__ float unit_f32(uint64_t key, uint64_t i) {
+  return (float)(mix64(key + i * 0x9E3779B97F4A7C15ull) >> 40) * (1.0f / 16777216.0f);
+}
+
+__global__ void __launch_bounds__(512) k_gen_batch(const BatchGen *descs, int n,
+                                                   unsigned int *counters, uint64_t seed,
+                                                   uint64_t iteration, int regen,
+                                                   uint64_t timeout_ns, int *err) {
+  __shared__ int s_desc, s_last;
+  if (threadIdx.x == 0) s_desc = find_desc(descs, n);
+  __syncthreads();
+  const BatchGen d = descs[s_desc];
+  const uint32_t lb = blockIdx.x - d.cta_begin;
+  if (threadIdx.x == 0) {
+    if (d.weight_flag && !spin_until(d.weight_flag, 1, timeout_ns)) atomicExch(err, 3);
+    if (d.credit && !spin_until(d.credit, 0, timeout_ns)) atomicExch(err, 4);
+  }
+  __syncthreads();
+  if (regen) {
+    const uint64_t key = mix64(seed * 0x9E3779B97F4A7C15ull ^ mix64(d.node + 0x51ED) ^
+                               mix64(iteration * 0xD1B54A32D192ED03ull));
+    const uint64_t nf = d.n / 4;
+    const uint64_t nth = (uint64_t)d.cta_count * blockDim.x;
+    float4 *g4 = (float4 *)d.grad;  // gradient blocks are 16-B aligned by layout
+    for (uint64_t q = (uint64_t)lb * blockDim.x + threadIdx.x; q < nf / 4; q += nth)
+      g4[q] = make_float4(unit_f32(key, 4 * q), unit_f32(key, 4 * q + 1),
+                          unit_f32(key, 4 * q + 2), unit_f32(key, 4 * q + 3));
+    float *g = (float *)d.grad;
+    for (uint64_t i = (nf / 4) * 4 + (uint64_t)lb * blockDim.x + threadIdx.x; i < nf; i += nth)
+      g[i] = unit_f32(key, i);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(&counters[s_desc], 1u) == d.cta_count - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    // the weight was consumed: clear its flag (StaticReceiver.poll semantics)
+    if (d.weight_flag) st_release_sys_u8(d.weight_flag, 0);
+    atomicExch(&counters[s_desc], 0u);
+  }
+}
+
+__global__ void __launch_bounds__(512) k_apply_batch(const BatchApply *descs, int n,
+                                                     unsigned int *counters, int op, float lr,
+                                                     uint64_t timeout_ns, int *err) {
+  __shared__ int s_desc, s_last, s_ok;
+  __shared__ const uint8_t *s_g[SRF_MAX_WORKERS];
+  if (threadIdx.x == 0) s_desc = find_desc(descs, n);
+  __syncthreads();
+  const BatchApply &d = descs[s_desc];
+  const uint32_t lb = blockIdx.x - d.cta_begin;
+  if (threadIdx.x == 0) {
+    // DynReceiver.poll + decode_meta + validation (protocol.py:234-242,
+    // wire.py:120-142, memspace.py:145-157) for every remote worker
+    int ok = 1;
+    for (int w = 0; w < d.nw; ++w) {
+      if (!((d.is_meta >> w) & 1)) {
+        s_g[w] = d.src[w];
+        continue;
+      }
+      const uint8_t *m = d.src[w];
+      const int r = d.rank;
+      if (!spin_until(m + 8 * r + 32, 1, timeout_ns)) {
+        ok = 0;
+        atomicExch(err, 5);
+        break;
+      }
+      const uint64_t addr = *(const volatile uint64_t *)(m + 8 + 8 * r);
+      const uint64_t tok = *(const volatile uint64_t *)(m + 16 + 8 * r);
+      const uint64_t plen = *(const volatile uint64_t *)(m + 24 + 8 * r);
+      if (m[1] != r || plen != d.n || tok != d.peer_token[w] || addr < d.peer_lo[w] ||
+          addr + plen > d.peer_hi[w]) {
+        ok = 0;
+        atomicExch(err, 6);
+        break;
+      }
+      s_g[w] = d.peer_base[w] + addr;  // one-sided read through the peer mapping
+    }
+    s_ok = ok;
+  }
+  __syncthreads();
+  if (s_ok) {
+    ApplyArgs a;
+    a.var = d.var;
+    a.nw = d.nw;
+    a.n = d.n;
+    a.lr = lr;
+    for (int w = 0; w < d.nw; ++w) a.g[w] = s_g[w];
+    const uint64_t t = (uint64_t)lb * blockDim.x + threadIdx.x;
+    const uint64_t nth = (uint64_t)d.cta_count * blockDim.x;
+    if (op == SRF_APPLY_XOR)
+      apply_xor_range(a, t, nth);
+    else
+      apply_sgd_range(a, t, nth);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    s_last = atomicAdd(&counters[s_desc], 1u) == d.cta_count - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    // gradients consumed: clear the meta flags (credit for the next send)
+    __threadfence_system();
+    for (int w = 0; w < d.nw; ++w)
+      if ((d.is_meta >> w) & 1) st_release_sys_u8((uint8_t *)d.src[w] + 8 * d.rank + 32, 0);
+    atomicExch(&counters[s_desc], 0u);
   }
 }
 
@@ -1262,6 +1472,10 @@ int srf_space_sync(srf_space_t sp) {
   CUDA_TRY(cudaMemcpy(&err, sp->err, sizeof(int), cudaMemcpyDeviceToHost));
   if (err) {
     cudaMemset(sp->err, 0, sizeof(int));
+    if (err == 6)
+      return fail(SRF_E_BAD_TOKEN,
+                  "server %d: device-side metadata validation failed (token/bounds/length)",
+                  sp->server_id);
     return fail(SRF_E_TIMEOUT, "server %d: device flag wait timed out (code %d)",
                 sp->server_id, err);
   }
@@ -1628,6 +1842,210 @@ int srf_reduce_max_f32(srf_space_t sp, uint64_t in_addr, uint64_t n,
                                        (float *)(sp->base + out_addr),
                                        s->scratch, s->counter + 1);
   return launch_check("k_reduce_max");
+}
+
+// ---------------------------------------------------------------------------
+// batches (PS step phases)
+// ---------------------------------------------------------------------------
+struct srf_batch {
+  int kind;  // 0 put, 1 gen, 2 apply
+  int device;
+  void *descs;
+  int n;
+  unsigned int *counters;
+  int grid;
+  int op;
+  float lr;
+  uint64_t seed;
+  int *err;
+};
+
+static uint32_t ctas_for(int device, uint64_t bytes, int total_desc) {
+  // ~64 KiB per CTA, at most 2 CTAs/SM for one descriptor
+  uint64_t want = (bytes + 65535) / 65536;
+  uint64_t cap = (uint64_t)sm_count_of(device) * 2;
+  (void)total_desc;
+  return (uint32_t)std::max<uint64_t>(1, std::min(want, cap));
+}
+
+}  // extern "C"
+
+template <typename D>
+static int finish_batch(int kind, int device, std::vector<D> &host, int *err, srf_batch_t *out) {
+  srf_batch *b = new srf_batch();
+  b->kind = kind;
+  b->device = device;
+  b->n = (int)host.size();
+  b->err = err;
+  b->op = 0;
+  b->lr = 0;
+  b->seed = 0;
+  uint32_t total = 0;
+  for (auto &d : host) total = d.cta_begin + d.cta_count;
+  b->grid = (int)total;
+  CUDA_TRY(cudaSetDevice(device));
+  cudaError_t e = cudaMalloc(&b->descs, sizeof(D) * std::max<size_t>(1, host.size()));
+  if (e == cudaSuccess && !host.empty())
+    e = cudaMemcpy(b->descs, host.data(), sizeof(D) * host.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&b->counters, sizeof(unsigned) * std::max<size_t>(1, host.size()));
+  if (e == cudaSuccess) e = cudaMemset(b->counters, 0, sizeof(unsigned) * std::max<size_t>(1, host.size()));
+  if (e != cudaSuccess) {
+    delete b;
+    return fail(SRF_E_DEVICE, "batch upload: %s", cudaGetErrorString(e));
+  }
+  *out = b;
+  return SRF_OK;
+}
+
+extern "C" {
+
+int srf_batch_put_create(int n, srf_space_t const *src_space, const uint64_t *src_addr,
+                         const uint64_t *body_len, const uint64_t *src_token,
+                         const uint64_t *tail_addr, srf_space_t const *dst_space,
+                         const uint64_t *dst_addr, const uint64_t *dst_token, int flags,
+                         srf_batch_t *out) {
+  if (n < 1) return fail(SRF_E_INVALID_CONFIG, "empty batch");
+  int device = src_space[0]->device;
+  std::vector<BatchPut> host(n);
+  uint32_t next = 0;
+  for (int i = 0; i < n; ++i) {
+    srf_space *ss = src_space[i], *ds = dst_space[i];
+    if (ss->device != device)
+      return fail(SRF_E_INVALID_CONFIG, "batch spans GPUs %d and %d", device, ss->device);
+    {
+      std::lock_guard<std::mutex> g(ss->mu);
+      int rc = check_registered_locked(ss, src_addr[i], body_len[i], src_token[i]);
+      if (!rc) rc = check_registered_locked(ss, tail_addr[i], 1, src_token[i]);
+      if (rc) return rc;
+    }
+    {
+      std::lock_guard<std::mutex> g(ds->mu);
+      int rc = check_remote_locked(ds, dst_addr[i], body_len[i] + 1, dst_token[i]);
+      if (rc) return rc;
+    }
+    BatchPut &d = host[i];
+    d.src = ss->base + src_addr[i];
+    d.dst = ds->base + dst_addr[i];
+    d.body = body_len[i];
+    d.tail = ss->base + tail_addr[i];
+    d.cta_begin = next;
+    d.cta_count = ctas_for(device, body_len[i], n);
+    d.wait_empty = (flags & SRF_PUT_WAIT_EMPTY) ? 1 : 0;
+    d.pad = 0;
+    next += d.cta_count;
+  }
+  return finish_batch(0, device, host, src_space[0]->err, out);
+}
+
+int srf_batch_gen_create(srf_space_t sp, int n, const uint64_t *grad_addr,
+                         const uint64_t *nbytes, const uint64_t *weight_flag_addr,
+                         srf_space_t const *credit_space, const uint64_t *credit_addr,
+                         const uint64_t *node_id, uint64_t seed, srf_batch_t *out) {
+  if (n < 1) return fail(SRF_E_INVALID_CONFIG, "empty batch");
+  std::vector<BatchGen> host(n);
+  uint32_t next = 0;
+  for (int i = 0; i < n; ++i) {
+    int rc = check_raw(sp, grad_addr[i], nbytes[i], "gradient");
+    if (rc) return rc;
+    if (grad_addr[i] % 16 || nbytes[i] % 4)
+      return fail(SRF_E_SHAPE_MISMATCH, "gradient blocks must be 16-B aligned fp32");
+    BatchGen &d = host[i];
+    d.grad = sp->base + grad_addr[i];
+    d.n = nbytes[i];
+    d.weight_flag = weight_flag_addr[i] == UINT64_MAX ? nullptr : sp->base + weight_flag_addr[i];
+    d.credit = (credit_space[i] == nullptr || credit_addr[i] == UINT64_MAX)
+                   ? nullptr : credit_space[i]->base + credit_addr[i];
+    d.node = node_id[i];
+    d.cta_begin = next;
+    d.cta_count = ctas_for(sp->device, nbytes[i], n);
+    next += d.cta_count;
+  }
+  int rc = finish_batch(1, sp->device, host, sp->err, out);
+  if (rc == SRF_OK) (*out)->seed = seed;
+  return rc;
+}
+
+int srf_batch_apply_create(srf_space_t sp, int nvars, const uint64_t *var_addr,
+                           const uint64_t *nbytes, const int *nworkers, const int *rank,
+                           srf_space_t const *src_space, const uint64_t *src_addr,
+                           const int *is_meta, srf_space_t const *peer_space,
+                           const uint64_t *peer_lo, const uint64_t *peer_hi,
+                           const uint64_t *peer_token, int op, float lr, srf_batch_t *out) {
+  if (nvars < 1) return fail(SRF_E_INVALID_CONFIG, "empty batch");
+  if (op != SRF_APPLY_XOR && op != SRF_APPLY_SGD)
+    return fail(SRF_E_INVALID_CONFIG, "unknown apply op %d", op);
+  std::vector<BatchApply> host(nvars);
+  uint32_t next = 0;
+  int k = 0;
+  for (int v = 0; v < nvars; ++v) {
+    BatchApply &d = host[v];
+    memset(&d, 0, sizeof d);
+    int rc = check_raw(sp, var_addr[v], nbytes[v], "variable");
+    if (rc) return rc;
+    if (nworkers[v] < 1 || nworkers[v] > SRF_MAX_WORKERS)
+      return fail(SRF_E_INVALID_CONFIG, "nworkers %d", nworkers[v]);
+    if (op == SRF_APPLY_SGD && (nbytes[v] % 4 || var_addr[v] % 4))
+      return fail(SRF_E_SHAPE_MISMATCH, "SGD needs whole fp32 elements");
+    d.var = sp->base + var_addr[v];
+    d.n = nbytes[v];
+    d.nw = nworkers[v];
+    d.rank = rank[v];
+    for (int w = 0; w < d.nw; ++w, ++k) {
+      srf_space *ss = src_space[k];
+      if (is_meta[k]) {
+        rc = check_raw(ss, src_addr[k], 8 * rank[v] + 33, "meta block");
+        if (rc) return rc;
+        d.is_meta |= 1u << w;
+        d.peer_base[w] = peer_space[k]->base;
+        d.peer_lo[w] = peer_lo[k];
+        d.peer_hi[w] = peer_hi[k];
+        d.peer_token[w] = peer_token[k];
+        if (peer_hi[k] > peer_space[k]->capacity)
+          return fail(SRF_E_OUT_OF_BOUNDS, "peer region escapes its space");
+      } else {
+        rc = check_raw(ss, src_addr[k], nbytes[v], "gradient");
+        if (rc) return rc;
+      }
+      d.src[w] = ss->base + src_addr[k];
+    }
+    d.cta_begin = next;
+    d.cta_count = ctas_for(sp->device, nbytes[v] * (uint64_t)(d.nw + 2) / 3, nvars);
+    next += d.cta_count;
+  }
+  int rc = finish_batch(2, sp->device, host, sp->err, out);
+  if (rc == SRF_OK) {
+    (*out)->op = op;
+    (*out)->lr = lr;
+  }
+  return rc;
+}
+
+int srf_batch_launch(srf_batch_t b, srf_stream_t st, uint64_t iteration, int mode) {
+  const uint64_t timeout = 10ull * 1000 * 1000 * 1000;
+  CUDA_TRY(cudaSetDevice(st->device));
+  switch (b->kind) {
+    case 0:
+      k_put_batch<<<b->grid, 512, 0, st->s>>>((const BatchPut *)b->descs, b->n, b->counters,
+                                              timeout, b->err);
+      return launch_check("k_put_batch");
+    case 1:
+      k_gen_batch<<<b->grid, 512, 0, st->s>>>((const BatchGen *)b->descs, b->n, b->counters,
+                                              b->seed, iteration, mode, timeout, b->err);
+      return launch_check("k_gen_batch");
+    default:
+      k_apply_batch<<<b->grid, 512, 0, st->s>>>((const BatchApply *)b->descs, b->n,
+                                                b->counters, b->op, b->lr, timeout, b->err);
+      return launch_check("k_apply_batch");
+  }
+}
+
+int srf_batch_destroy(srf_batch_t b) {
+  if (!b) return SRF_OK;
+  cudaSetDevice(b->device);
+  cudaFree(b->descs);
+  cudaFree(b->counters);
+  delete b;
+  return SRF_OK;
 }
 
 int srf_graph_begin(srf_stream_t st) {

@@ -1,0 +1,389 @@
+"""Parameter-server training step on B200, fully device-driven.
+
+This is the hot loop of BASELINE.json configs[2..4]: the reference's
+``Session.run`` over ``build_ps_workload`` (workloads.py:59-94,
+runtime/session.py:606-629), where per iteration every variable is pushed
+shard -> workers with static placement (the weight edge, analyzer.py:105-128
+makes it STATIC), every worker returns a gradient with dynamic allocation
+(meta write + receiver pull, the Variable-feeding rule makes it DYNAMIC), and
+the shard applies the workers' gradients in ascending node order
+(graph.py:507-535) in place.
+
+On B200 the whole iteration is four kernel launches per GPU, with no host
+round trip between phases (``srf_batch_*`` in include/srflow.h):
+
+1. put batch   K1 - weight pushes, payload + tail flag, credit-gated;
+2. gen batch       - each worker acquires/clears its weight flags (the
+                     StaticReceiver poll) and produces its gradient (device
+                     RNG stand-in for GenGrad, or host-uploaded PCG64 values in
+                     parity mode);
+3. put batch   K3 - the 8D+33-byte metadata blocks, byte-identical to
+                     ``encode_meta``, into the shards' fixed slots;
+4. apply batch K4+K6 - the shard decodes each meta block on the device,
+                     validates token/bounds/length, and folds every worker's
+                     gradient straight from the peer pool (XOR = the
+                     reference's bit-exact update, or SGD) - the pull and the
+                     update fused, so no gradient copy lands in shard HBM.
+
+Servers follow the reference placement: workers ``0..W-1``; shard k is server
+``W + k`` or, with ``colocate``, server k (the paper's deployment).  A server
+lives on rank ``server % world``; all of a rank's servers share its GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib, errors
+from .graph import node_rng, synthesize_values
+from .memspace import ArenaAllocator, MemorySpace
+from .wire import ElemType, encode_meta, meta_block_size
+from .workloads import ps_node_ids
+
+_NONE = (1 << 64) - 1
+
+
+def _r16(n: int) -> int:
+    return (n + 15) & ~15
+
+
+@dataclass
+class PsLayout:
+    """Deterministic per-server memory layout (pure host logic).
+
+    Every block is a 16-B aligned slice of the server's one registered arena,
+    allocated in a fixed order, so every rank can derive every peer's
+    coordinates; the exchanged region tables (tokens) validate them.
+    """
+
+    shapes: list[tuple[int, ...]]
+    workers: int
+    shards: int
+    colocate: bool = False
+    elem: ElemType = ElemType.F32
+    blocks: dict[int, dict] = field(default_factory=dict)
+    sizes: dict[int, int] = field(default_factory=dict)
+
+    def __post_init__(self):
+        self.shapes = [tuple(int(d) for d in s) for s in self.shapes]
+        if self.colocate and self.shards > self.workers:
+            raise errors.InvalidConfig("colocate needs shards <= workers")
+        if self.workers > _lib.MAX_WORKERS:
+            raise errors.InvalidConfig(f"at most {_lib.MAX_WORKERS} workers")
+        for s in range(self.nservers):
+            self._lay_out(s)
+
+    @property
+    def nservers(self) -> int:
+        return self.workers if self.colocate else self.workers + self.shards
+
+    def nbytes(self, v: int) -> int:
+        return math.prod(self.shapes[v]) * self.elem.size
+
+    def shard_of(self, v: int) -> int:
+        return (v % self.shards) + (0 if self.colocate else self.workers)
+
+    def is_worker(self, s: int) -> bool:
+        return s < self.workers
+
+    def _lay_out(self, s: int) -> None:
+        off = 0
+        b: dict = {}
+
+        def take(key, n):
+            nonlocal off
+            b[key] = off
+            off += _r16(n)
+
+        take("flag", 1)
+        for v in range(len(self.shapes)):
+            if self.shard_of(v) == s:
+                take(("var", v), self.nbytes(v))
+        if self.is_worker(s):
+            for v in range(len(self.shapes)):
+                take(("grad", v), self.nbytes(v))
+                if self.shard_of(v) != s:
+                    take(("wbuf", v), self.nbytes(v) + 1)
+                    take(("mstage", v), meta_block_size(len(self.shapes[v])))
+        for v in range(len(self.shapes)):
+            if self.shard_of(v) == s:
+                for w in range(self.workers):
+                    if w != s:
+                        take(("mslot", v, w), meta_block_size(len(self.shapes[v])))
+        self.blocks[s] = b
+        self.sizes[s] = off
+
+    def traffic(self, s: int) -> dict:
+        """Algorithmic bytes per iteration at server s."""
+        out = {"push_out": 0, "meta_out": 0, "pull_in": 0, "hbm": 0}
+        for v in range(len(self.shapes)):
+            S = self.nbytes(v)
+            meta = meta_block_size(len(self.shapes[v]))
+            if self.shard_of(v) == s:
+                remote = [w for w in range(self.workers) if w != s]
+                out["push_out"] += len(remote) * (S + 1)
+                out["pull_in"] += len(remote) * S
+                out["hbm"] += 2 * S + (self.workers - len(remote)) * S  # var r/w + local grad
+            if self.is_worker(s):
+                out["hbm"] += S  # gradient produced
+                if self.shard_of(v) != s:
+                    out["meta_out"] += meta
+        return out
+
+
+class PsStep:
+    """The device-resident PS exchange of one rank (see module docstring)."""
+
+    def __init__(self, layout: PsLayout, *, rank: int = 0, world: int = 1, device: int = 0,
+                 seed: int = 0, op: str = "xor", lr: float = 0.01):
+        self.L = layout
+        self.rank, self.world, self.device = rank, world, device
+        self.seed = seed
+        self.op = {"xor": _lib.APPLY_XOR, "sgd": _lib.APPLY_SGD}[op]
+        self.lr = float(lr)
+        self.local = [s for s in range(layout.nservers) if s % world == rank]
+        self.spaces: dict[int, MemorySpace] = {}
+        self.regions = {}
+        for s in self.local:
+            size = layout.sizes[s]
+            sp = MemorySpace(s, size + (1 << 20), seed=seed, device=device)
+            reg = sp.allocate_region(size, register=True)
+            arena = ArenaAllocator(sp, reg)
+            # allocate the layout's blocks in order: first fit == bump here
+            for key, off in sorted(layout.blocks[s].items(), key=lambda kv: kv[1]):
+                h = arena.alloc(_r16(self._block_len(s, key)))
+                if h.base_addr != reg.base_addr + off:
+                    raise AssertionError(f"layout drift at {key}")
+            self.spaces[s] = sp
+            self.regions[s] = reg
+        self.peers: dict[int, MemorySpace] = {}
+        if world > 1:
+            table = gather_descriptors_all(self.spaces)
+            for s, desc in table.items():
+                if s not in self.spaces:
+                    proxy = MemorySpace.import_remote(desc, device)
+                    self.peers[s] = proxy
+                    rid, base, length, reg_, tok = desc["regions"][0]
+                    self.regions[s] = _Reg(base, length, tok)
+        for a in self.spaces.values():
+            for b in list(self.spaces.values()) + list(self.peers.values()):
+                _lib.call("srf_connect", a.handle, b.handle)
+        self._init_memory()
+        first = self.spaces[self.local[0]]
+        self.stream = C.c_void_p()
+        _lib.call("srf_stream_create", first.handle, C.byref(self.stream))
+        self.batches = self._build_batches()
+
+    # -- layout helpers -------------------------------------------------------------
+
+    def _block_len(self, s: int, key) -> int:
+        kind = key if isinstance(key, str) else key[0]
+        if kind == "flag":
+            return 1
+        v = key[1]
+        if kind in ("var", "grad"):
+            return self.L.nbytes(v)
+        if kind == "wbuf":
+            return self.L.nbytes(v) + 1
+        return meta_block_size(len(self.L.shapes[v]))
+
+    def space(self, s: int) -> MemorySpace:
+        return self.spaces.get(s) or self.peers[s]
+
+    def addr(self, s: int, key) -> int:
+        return self.regions[s].base_addr + self.L.blocks[s][key]
+
+    def token(self, s: int) -> int:
+        return self.regions[s].access_token
+
+    # -- initial state ------------------------------------------------------------------
+
+    def _init_memory(self) -> None:
+        L = self.L
+        for s, sp in self.spaces.items():
+            sp.write_raw(self.addr(s, "flag"), b"\x01")
+            for v in range(len(L.shapes)):
+                if L.shard_of(v) == s:
+                    var_node = ps_node_ids(len(L.shapes), L.workers, v, 0)[0]
+                    init = synthesize_values(L.shapes[v], L.elem, node_rng(self.seed, var_node, 0))
+                    sp.write_raw(self.addr(s, ("var", v)), init)
+                    for w in range(L.workers):
+                        if w != s:
+                            mk = ("mslot", v, w)
+                            sp.write_raw(self.addr(s, mk) + meta_block_size(len(L.shapes[v])) - 1,
+                                         b"\x00")
+                if L.is_worker(s) and L.shard_of(v) != s:
+                    sp.write_raw(self.addr(s, ("wbuf", v)) + L.nbytes(v), b"\x00")
+                    meta = encode_meta(L.shapes[v], L.elem, self.addr(s, ("grad", v)), self.token(s))
+                    sp.write_raw(self.addr(s, ("mstage", v)), meta)
+            sp.sync()
+
+    def _build_batches(self) -> dict:
+        L = self.L
+        P, u64 = C.c_void_p, _lib.u64_array
+        out = {}
+        # 1. weight pushes (K1), credit-gated
+        rows = []
+        for s in self.local:
+            for v in range(len(L.shapes)):
+                if L.shard_of(v) != s:
+                    continue
+                for w in range(L.workers):
+                    if w == s:
+                        continue
+                    rows.append((s, self.addr(s, ("var", v)), L.nbytes(v), self.token(s),
+                                 self.addr(s, "flag"), w, self.addr(w, ("wbuf", v)), self.token(w)))
+        out["push"] = self._put_batch(rows, _lib.PUT_WAIT_EMPTY)
+        # 2. worker gen batch
+        g_rows = []
+        for w in self.local:
+            if not L.is_worker(w):
+                continue
+            for v in range(len(L.shapes)):
+                sh = L.shard_of(v)
+                remote = sh != w
+                mlen = meta_block_size(len(L.shapes[v]))
+                g_rows.append((self.addr(w, ("grad", v)), L.nbytes(v),
+                               self.addr(w, ("wbuf", v)) + L.nbytes(v) if remote else _NONE,
+                               self.space(sh).handle.value if remote else None,
+                               self.addr(sh, ("mslot", v, w)) + mlen - 1 if remote else _NONE,
+                               ps_node_ids(len(L.shapes), L.workers, v, w)[1], w))
+        out["gen"] = {}
+        for w in sorted({r[-1] for r in g_rows}):
+            rr = [r for r in g_rows if r[-1] == w]
+            b = C.c_void_p()
+            _lib.call("srf_batch_gen_create", self.spaces[w].handle, len(rr),
+                      u64(r[0] for r in rr), u64(r[1] for r in rr), u64(r[2] for r in rr),
+                      (P * len(rr))(*[r[3] for r in rr]), u64(r[4] for r in rr),
+                      u64(r[5] for r in rr), self.seed, C.byref(b))
+            out["gen"][w] = b
+        # 3. metadata writes (K3)
+        rows = []
+        for w in self.local:
+            if not L.is_worker(w):
+                continue
+            for v in range(len(L.shapes)):
+                sh = L.shard_of(v)
+                if sh == w:
+                    continue
+                mlen = meta_block_size(len(L.shapes[v]))
+                rows.append((w, self.addr(w, ("mstage", v)), mlen - 1, self.token(w),
+                             self.addr(w, ("mstage", v)) + mlen - 1, sh,
+                             self.addr(sh, ("mslot", v, w)), self.token(sh)))
+        out["meta"] = self._put_batch(rows, 0)
+        # 4. fused pull + apply per shard
+        out["apply"] = {}
+        for s in self.local:
+            vs = [v for v in range(len(L.shapes)) if L.shard_of(v) == s]
+            if not vs:
+                continue
+            srcsp, srcad, ismeta, peersp, lo, hi, tok = [], [], [], [], [], [], []
+            for v in vs:
+                for w in range(L.workers):
+                    if w == s:
+                        srcsp.append(self.spaces[s].handle.value)
+                        srcad.append(self.addr(s, ("grad", v)))
+                        ismeta.append(0)
+                        peersp.append(self.spaces[s].handle.value)
+                        lo.append(0), hi.append(0), tok.append(0)
+                    else:
+                        srcsp.append(self.spaces[s].handle.value)
+                        srcad.append(self.addr(s, ("mslot", v, w)))
+                        ismeta.append(1)
+                        peersp.append(self.space(w).handle.value)
+                        r = self.regions[w]
+                        lo.append(r.base_addr), hi.append(r.base_addr + r.length)
+                        tok.append(r.access_token)
+            n = len(vs)
+            b = C.c_void_p()
+            ints = C.c_int * n
+            _lib.call("srf_batch_apply_create", self.spaces[s].handle, n,
+                      u64(self.addr(s, ("var", v)) for v in vs), u64(L.nbytes(v) for v in vs),
+                      ints(*[L.workers] * n), ints(*[len(L.shapes[v]) for v in vs]),
+                      (P * len(srcsp))(*srcsp), u64(srcad), (C.c_int * len(ismeta))(*ismeta),
+                      (P * len(peersp))(*peersp), u64(lo), u64(hi), u64(tok), self.op,
+                      self.lr, C.byref(b))
+            out["apply"][s] = b
+        return out
+
+    def _put_batch(self, rows, flags):
+        if not rows:
+            return None
+        P, u64 = C.c_void_p, _lib.u64_array
+        b = C.c_void_p()
+        n = len(rows)
+        _lib.call("srf_batch_put_create", n,
+                  (P * n)(*[self.space(r[0]).handle.value for r in rows]),
+                  u64(r[1] for r in rows), u64(r[2] for r in rows), u64(r[3] for r in rows),
+                  u64(r[4] for r in rows), (P * n)(*[self.space(r[5]).handle.value for r in rows]),
+                  u64(r[6] for r in rows), u64(r[7] for r in rows), flags, C.byref(b))
+        return b
+
+    # -- running --------------------------------------------------------------------------
+
+    def step(self, iteration: int, regen: bool = True) -> int:
+        """Queue one PS iteration on this rank's stream; returns #launches."""
+        b, n = self.batches, 0
+        if b["push"] is not None:
+            _lib.call("srf_batch_launch", b["push"], self.stream, iteration, 0)
+            n += 1
+        for g in b["gen"].values():
+            _lib.call("srf_batch_launch", g, self.stream, iteration, 1 if regen else 0)
+            n += 1
+        if b["meta"] is not None:
+            _lib.call("srf_batch_launch", b["meta"], self.stream, iteration, 0)
+            n += 1
+        for a in b["apply"].values():
+            _lib.call("srf_batch_launch", a, self.stream, iteration, 0)
+            n += 1
+        return n
+
+    def sync(self) -> None:
+        _lib.call("srf_stream_sync", self.stream)
+        for sp in self.spaces.values():
+            sp.sync()
+
+    def upload_gradients(self, iteration: int) -> None:
+        """Parity mode: this iteration's gradients from the reference's PCG64
+        stream (graph.py:333-350).  Call only after a barrier (no step in
+        flight)."""
+        L = self.L
+        for w in self.local:
+            if not L.is_worker(w):
+                continue
+            for v in range(len(L.shapes)):
+                gen = ps_node_ids(len(L.shapes), L.workers, v, w)[1]
+                g = synthesize_values(L.shapes[v], L.elem, node_rng(self.seed, gen, iteration))
+                self.spaces[w].write_raw(self.addr(w, ("grad", v)), g)
+            self.spaces[w].sync()
+
+    def variable(self, v: int) -> np.ndarray:
+        s = self.L.shard_of(v)
+        raw = self.spaces[s].read_raw(self.addr(s, ("var", v)), self.L.nbytes(v))
+        return np.frombuffer(raw, dtype=self.L.elem.np_dtype).reshape(self.L.shapes[v])
+
+    def close(self) -> None:
+        self.sync()
+        for b in [self.batches["push"], self.batches["meta"], *self.batches["gen"].values(),
+                  *self.batches["apply"].values()]:
+            if b is not None:
+                _lib.load().srf_batch_destroy(b)
+        _lib.call("srf_stream_destroy", self.stream)
+
+
+@dataclass
+class _Reg:
+    base_addr: int
+    length: int
+    access_token: int
+
+
+def gather_descriptors_all(spaces: dict[int, MemorySpace]) -> dict[int, dict]:
+    """Every rank's exported pools, keyed by server id."""
+    from .distributed import all_gather_objects
+    got = all_gather_objects([sp.export() for sp in spaces.values()])
+    return {d["server_id"]: d for lst in got for d in lst}

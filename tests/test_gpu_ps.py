@@ -1,0 +1,99 @@
+"""Device-driven PS step (paper_1805_08430_b200.ps) vs the oracle: the
+reference's XOR update bit-exact (pinned by the golden PS runs through
+oracle.port.ps_expected) and SGD (unpinned restatement), in parity mode
+(host-uploaded PCG64 gradients) and regen mode (device gradients, checked
+against the oracle's restatement of the device RNG)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import port
+from paper_1805_08430_b200 import _lib, errors
+from paper_1805_08430_b200.ps import PsLayout, PsStep
+from paper_1805_08430_b200.workloads import mlp_shapes
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # (shapes, workers, shards, colocate)
+    ([(1000,), (37,), (4, 9)], 1, 1, False),             # G=1: worker + PS on one GPU
+    (mlp_shapes(), 2, 1, False),                          # configs[2] parity set
+    ([(3000,), (17,), (64, 64), (5,)], 4, 4, True),       # co-located shards
+    ([(641,)] * 3, 7, 1, False),                          # configs[4] shape: 7 workers
+]
+
+
+@pytest.mark.parametrize("shapes,W,P,coloc", CASES)
+@pytest.mark.parametrize("op", ["xor", "sgd"])
+def test_parity_mode_matches_oracle(shapes, W, P, coloc, op):
+    L = PsLayout(shapes, W, P, coloc)
+    ps = PsStep(L, seed=3, op=op, lr=0.05)
+    launches = _lib.launch_count()
+    for it in (1, 2, 3):
+        ps.upload_gradients(it)
+        ps.step(it, regen=False)
+        ps.sync()
+    assert _lib.launch_count() - launches >= 3 * 3
+    want = port.ps_expected(shapes, W, 3, 3, op=op, lr=0.05)
+    for v in range(len(shapes)):
+        got = ps.variable(v)
+        if op == "sgd":
+            np.testing.assert_allclose(got, want[v], rtol=1e-6, atol=0)
+        assert got.tobytes() == want[v].tobytes(), (v, op)
+    ps.close()
+
+
+@pytest.mark.parametrize("shapes,W,P,coloc", CASES[:3])
+def test_regen_mode_pipelined(shapes, W, P, coloc):
+    """Back-to-back device iterations (no host sync between steps): the
+    credit/flag protocol alone orders the phases."""
+    L = PsLayout(shapes, W, P, coloc)
+    ps = PsStep(L, seed=9, op="sgd", lr=0.01)
+    for it in range(1, 9):
+        ps.step(it)
+    ps.sync()
+    want = port.ps_expected_device(shapes, W, 9, range(1, 9), op="sgd", lr=0.01)
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes()
+    ps.close()
+
+
+def test_device_gradient_restatement():
+    L = PsLayout([(1031,)], 1, 1, False)
+    ps = PsStep(L, seed=5)
+    ps.step(7)
+    ps.sync()
+    g = np.frombuffer(ps.spaces[0].read_raw(ps.addr(0, ("grad", 0)), 1031 * 4), np.float32)
+    assert g.tobytes() == port.device_gradient(5, 1, 7, 1031).tobytes()
+    ps.close()
+
+
+def test_meta_blocks_are_reference_bytes():
+    from paper_1805_08430_b200.wire import ElemType, encode_meta
+    L = PsLayout([(10, 3)], 2, 1, False)
+    ps = PsStep(L, seed=1)
+    ps.step(1)
+    ps.sync()
+    for w in (0, 1):
+        stage = ps.spaces[w].read_raw(ps.addr(w, ("mstage", 0)), 49)
+        assert stage == port.encode_meta((10, 3), 0, ps.addr(w, ("grad", 0)), ps.token(w))
+        assert stage == encode_meta((10, 3), ElemType.F32, ps.addr(w, ("grad", 0)), ps.token(w))
+    # the shard consumed and cleared every meta flag
+    for w in (0, 1):
+        assert ps.spaces[2].read_raw(ps.addr(2, ("mslot", 0, w)) + 48, 1) == b"\x00"
+    ps.close()
+
+
+def test_bad_token_in_meta_is_rejected():
+    L = PsLayout([(256,)], 2, 1, False)
+    ps = PsStep(L, seed=1)
+    # corrupt worker 1's metadata token
+    raw = bytearray(ps.spaces[1].read_raw(ps.addr(1, ("mstage", 0)), 41))
+    raw[16] ^= 0xFF
+    ps.spaces[1].write_raw(ps.addr(1, ("mstage", 0)), bytes(raw))
+    before = ps.variable(0).copy()
+    ps.step(1)
+    with pytest.raises(errors.BadToken):
+        ps.sync()
+    assert ps.variable(0).tobytes() == before.tobytes()  # no update applied

@@ -225,3 +225,26 @@ def test_ready_poll_completes_once():
     assert not ex.done()
     ex.step()
     assert ex.done() and seen == ["tok"]
+
+
+# -- PS layout (pure host) ----------------------------------------------------------------
+
+
+def test_ps_layout_blocks_and_traffic():
+    from paper_1805_08430_b200.ps import PsLayout
+    shapes = vgg16_shapes()
+    L = PsLayout(shapes, 8, 8, colocate=True)
+    assert L.nservers == 8
+    for s in range(8):
+        offs = sorted(L.blocks[s].values())
+        assert all(o % 16 == 0 for o in offs)
+        assert len(set(offs)) == len(offs)
+    t = [L.traffic(s) for s in range(8)]
+    # round-robin places fc6 (25088x4096, v=26) on shard 2: the hottest egress (F5)
+    assert L.shard_of(26) == 2
+    assert max(range(8), key=lambda s: t[s]["push_out"]) == 2
+    total_vars = sum(L.nbytes(v) for v in range(32))
+    assert sum(x["pull_in"] for x in t) == 7 * total_vars
+    L1 = PsLayout(shapes, 1, 1)
+    assert L1.nservers == 2 and L1.shard_of(5) == 1
+    assert L1.traffic(1)["push_out"] == sum(L1.nbytes(v) + 1 for v in range(32))

@@ -618,13 +618,14 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "bytes_per_step": alg}
     else:
-        per_gpu = [max(x["push_out"] + x["meta_out"], x["pull_in"]) for x in tr]
+        per_gpu = [max(x["link_out"], x["link_in"]) for x in tr]
         hot = max(range(world), key=lambda s: per_gpu[s])
         ach = per_gpu[hot] * steps / t / 1e9
         roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_MEASURED_GBS,
                 "unit": "GB/s", "frac": round(ach / NVLINK_MEASURED_GBS, 4),
                 "hottest_gpu": hot, "hottest_bytes_per_step": per_gpu[hot],
-                "note": "round-robin placement puts fc6 (411 MB) on shard 2 (SURVEY F5)"}
+                "note": "busiest GPU's max(NVLink egress, ingress) per step; round-robin "
+                        "placement concentrates fc6 (411 MB) on one shard (SURVEY F5)"}
     out = {"workload": f"configs[3] VGG-16 real shapes ({total_params(shapes)} fp32, "
                        f"{len(shapes)} tensors) PS sync, op={op} lr=0.01, "
                        + ("worker server 0 + PS server 1 on GPU 0" if world == 1
@@ -671,6 +672,7 @@ def main() -> int:
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
 
+    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
     import torch
     from paper_1805_08430_b200 import _lib
     from paper_1805_08430_b200.distributed import init_process_group

@@ -1075,11 +1075,17 @@ __global__ void __launch_bounds__(512) k_apply_batch(const BatchApply *descs, in
         atomicExch(err, 5);
         break;
       }
-      const uint64_t addr = *(const volatile uint64_t *)(m + 8 + 8 * r);
+      const uint64_t addr = *(const volatile uint64_t *)(m + 8 + 8 * r);  // after the dims
       const uint64_t tok = *(const volatile uint64_t *)(m + 16 + 8 * r);
       const uint64_t plen = *(const volatile uint64_t *)(m + 24 + 8 * r);
-      if (m[1] != r || plen != d.n || tok != d.peer_token[w] || addr < d.peer_lo[w] ||
-          addr + plen > d.peer_hi[w]) {
+      // decode_meta's consistency check: payload_len == prod(dims) * elem size
+      const uint32_t code = m[0];
+      const uint64_t esz = code == 0 ? 4 : code == 1 ? 8 : code == 2 ? 4 : code == 3 ? 8
+                         : code == 4 ? 1 : 0;
+      uint64_t prod = esz;
+      for (int k = 0; k < r; ++k) prod *= *(const volatile uint64_t *)(m + 8 + 8 * k);
+      if (m[1] != r || esz == 0 || prod != plen || plen != d.n || tok != d.peer_token[w] ||
+          addr < d.peer_lo[w] || addr + plen > d.peer_hi[w]) {
         ok = 0;
         atomicExch(err, 6);
         break;

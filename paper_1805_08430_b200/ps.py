@@ -118,20 +118,32 @@ class PsLayout:
         self.sizes[s] = off
 
     def traffic(self, s: int) -> dict:
-        """Algorithmic bytes per iteration at server s."""
-        out = {"push_out": 0, "meta_out": 0, "pull_in": 0, "hbm": 0}
+        """Algorithmic bytes per iteration at server s.
+
+        ``link_out``/``link_in``: bytes leaving/entering s over NVLink - weight
+        pushes out of a shard, gradient reads a shard makes from worker pools
+        (they leave the worker), metadata blocks.  ``hbm``: local bytes of the
+        update (variable read + write, co-located gradient) and gradient
+        production."""
+        out = {"push_out": 0, "meta_out": 0, "pull_in": 0, "link_out": 0, "link_in": 0,
+               "hbm": 0}
         for v in range(len(self.shapes)):
             S = self.nbytes(v)
             meta = meta_block_size(len(self.shapes[v]))
-            if self.shard_of(v) == s:
+            sh = self.shard_of(v)
+            if sh == s:
                 remote = [w for w in range(self.workers) if w != s]
                 out["push_out"] += len(remote) * (S + 1)
                 out["pull_in"] += len(remote) * S
-                out["hbm"] += 2 * S + (self.workers - len(remote)) * S  # var r/w + local grad
+                out["link_out"] += len(remote) * (S + 1)
+                out["link_in"] += len(remote) * (S + meta)
+                out["hbm"] += 2 * S + (self.workers - len(remote)) * S
             if self.is_worker(s):
                 out["hbm"] += S  # gradient produced
-                if self.shard_of(v) != s:
+                if sh != s:
                     out["meta_out"] += meta
+                    out["link_out"] += meta + S   # meta written, gradient read by the shard
+                    out["link_in"] += S + 1       # weight pushed in
         return out
 
 
@@ -173,6 +185,10 @@ class PsStep:
             for b in list(self.spaces.values()) + list(self.peers.values()):
                 _lib.call("srf_connect", a.handle, b.handle)
         self._init_memory()
+        if world > 1:
+            # no peer may write into this rank's pools before they are set up
+            import torch.distributed as dist
+            dist.barrier()
         first = self.spaces[self.local[0]]
         self.stream = C.c_void_p()
         _lib.call("srf_stream_create", first.handle, C.byref(self.stream))

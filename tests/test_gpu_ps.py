@@ -88,12 +88,34 @@ def test_meta_blocks_are_reference_bytes():
 def test_bad_token_in_meta_is_rejected():
     L = PsLayout([(256,)], 2, 1, False)
     ps = PsStep(L, seed=1)
-    # corrupt worker 1's metadata token
+    # corrupt worker 1's metadata token (offset 16 + 8*rank, wire.py layout)
     raw = bytearray(ps.spaces[1].read_raw(ps.addr(1, ("mstage", 0)), 41))
-    raw[16] ^= 0xFF
+    raw[24] ^= 0xFF
     ps.spaces[1].write_raw(ps.addr(1, ("mstage", 0)), bytes(raw))
     before = ps.variable(0).copy()
     ps.step(1)
     with pytest.raises(errors.BadToken):
         ps.sync()
     assert ps.variable(0).tobytes() == before.tobytes()  # no update applied
+
+
+def test_out_of_range_meta_address_is_rejected():
+    L = PsLayout([(256,)], 2, 1, False)
+    ps = PsStep(L, seed=1)
+    raw = bytearray(ps.spaces[0].read_raw(ps.addr(0, ("mstage", 0)), 41))
+    raw[16:24] = (1 << 40).to_bytes(8, "little")  # remote_addr (after dims) out of range
+    ps.spaces[0].write_raw(ps.addr(0, ("mstage", 0)), bytes(raw))
+    ps.step(1)
+    with pytest.raises(errors.BadToken):
+        ps.sync()
+
+
+def test_inconsistent_meta_dims_are_rejected():
+    L = PsLayout([(256,)], 2, 1, False)
+    ps = PsStep(L, seed=1)
+    raw = bytearray(ps.spaces[0].read_raw(ps.addr(0, ("mstage", 0)), 41))
+    raw[8:16] = (255).to_bytes(8, "little")  # dims no longer match payload_len
+    ps.spaces[0].write_raw(ps.addr(0, ("mstage", 0)), bytes(raw))
+    ps.step(1)
+    with pytest.raises(errors.BadToken):
+        ps.sync()

@@ -98,7 +98,7 @@ static constexpr int kScratchBlocks = 1024;
 
 // launch-geometry knobs (srf_tune): CTAs per SM and threads per CTA of the
 // copy kernels; defaults chosen from the NVLink/HBM probes (profiles/).
-static int g_ctas_per_sm = 2;
+static int g_ctas_per_sm = 8;
 static int g_copy_threads = 512;
 
 static int sm_count_of(int device) {
@@ -338,6 +338,30 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   return t;
 }
 
+
+// Grid arrival for the flag-last release.  Every CTA's threads finish their
+// stores; bar.sync orders them before thread 0, whose acq_rel RMW on the
+// arrival counter is cumulative at the chosen scope (gpu when the destination
+// is this GPU's own HBM, sys when it is a peer's).  The CTA that observes
+// count-1 then owns the release store of the tail byte.
+__device__ __forceinline__ bool grid_arrive(unsigned int *counter, unsigned expected_last,
+                                            int sys_scope) {
+  unsigned prev;
+  if (sys_scope)
+    asm volatile("atom.add.acq_rel.sys.u32 %0, [%1], 1;" : "=r"(prev) : "l"(counter) : "memory");
+  else
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(counter) : "memory");
+  return prev == expected_last;
+}
+
+__device__ __forceinline__ void release_tail(uint8_t *p, uint32_t v, int sys_scope) {
+  uint16_t x = (uint16_t)v;
+  if (sys_scope)
+    asm volatile("st.release.sys.global.u8 [%0], %1;" ::"l"(p), "h"(x) : "memory");
+  else
+    asm volatile("st.release.gpu.global.u8 [%0], %1;" ::"l"(p), "h"(x) : "memory");
+}
+
 // 16-byte streaming load, no L1 allocation (source is read exactly once)
 __device__ __forceinline__ uint4 ld_stream_v4(const uint4 *p) {
   uint4 r;
@@ -390,6 +414,7 @@ __device__ __forceinline__ void vec_copy(V *__restrict__ dst,
 
 // Copy n bytes with the widest vector both pointers allow.  Arena blocks are
 // 8-byte aligned (memspace.py:31), so the 16-B path needs equal (p mod 16).
+template <int U16 = 4>
 __device__ void copy_bytes_grid(uint8_t *dst, const uint8_t *src, uint64_t n,
                                 uint64_t t, uint64_t nth) {
   if (n == 0) return;
@@ -399,8 +424,8 @@ __device__ void copy_bytes_grid(uint8_t *dst, const uint8_t *src, uint64_t n,
     head = (16 - (d & 15)) & 15;
     if (head > n) head = n;
     nv = (n - head) / 16;
-    vec_copy<uint4, 4>((uint4 *)(dst + head), (const uint4 *)(src + head), nv,
-                       t, nth);
+    vec_copy<uint4, U16>((uint4 *)(dst + head), (const uint4 *)(src + head), nv,
+                         t, nth);
     nv *= 16;
   } else if (((d ^ s) & 7) == 0) {
     head = (8 - (d & 7)) & 7;
@@ -438,12 +463,14 @@ struct PutArgs {
   uint64_t total;        // bytes in the gather list
   int tail_release;      // 1: last byte written last with st.release.sys
   int wait_empty;        // 1: spin until dst[total-1] == 0 before writing
+  int sys_scope;         // 1: destination is a peer's memory (system-scope release)
   uint64_t timeout_ns;
   unsigned int *counter; // arrival counter (per stream, reset by last CTA)
   int *err;
 };
 
 // K1 static_put / K3 meta_put / K4 peer_pull / K5 stage_copy.
+template <int U16>
 __global__ void __launch_bounds__(512) k_put(PutArgs a) {
   __shared__ int s_last;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
@@ -473,23 +500,17 @@ __global__ void __launch_bounds__(512) k_put(PutArgs a) {
     if (sg.dst_off >= body) break;
     uint64_t n = sg.len;
     if (sg.dst_off + n > body) n = body - sg.dst_off;
-    copy_bytes_grid(a.dst + sg.dst_off, sg.src, n, t, nth);
+    copy_bytes_grid<U16>(a.dst + sg.dst_off, sg.src, n, t, nth);
   }
 
   if (!a.tail_release) return;
   // flag-last: all CTAs publish, the last to arrive releases the tail byte.
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    unsigned prev = atomicAdd(a.counter, 1u);
-    s_last = (prev == gridDim.x - 1);
-  }
+  if (threadIdx.x == 0) s_last = grid_arrive(a.counter, gridDim.x - 1, a.sys_scope);
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
-    __threadfence_system();
     const Seg &ls = a.seg[a.nseg - 1];
-    uint32_t v = ls.src[ls.len - 1];
-    st_release_sys_u8(tail, v);
+    release_tail(tail, ls.src[ls.len - 1], a.sys_scope);
     atomicExch(a.counter, 0u);
   }
 }
@@ -668,17 +689,11 @@ __global__ void __launch_bounds__(256) k_put_bulk(PutArgs a) {
   if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
   if (!a.tail_release) return;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    unsigned prev = atomicAdd(a.counter, 1u);
-    s_last = (prev == gridDim.x - 1);
-  }
+  if (threadIdx.x == 0) s_last = grid_arrive(a.counter, gridDim.x - 1, a.sys_scope);
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
-    __threadfence_system();
     const Seg &ls = a.seg[a.nseg - 1];
-    uint32_t v = ls.src[ls.len - 1];
-    st_release_sys_u8(tail, v);
+    release_tail(tail, ls.src[ls.len - 1], a.sys_scope);
     atomicExch(a.counter, 0u);
   }
 }
@@ -984,14 +999,10 @@ __global__ void __launch_bounds__(512) k_put_batch(const BatchPut *descs, int n,
   copy_bytes_grid(d.dst, d.src, d.body, (uint64_t)lb * blockDim.x + threadIdx.x,
                   (uint64_t)d.cta_count * blockDim.x);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    s_last = atomicAdd(&counters[s_desc], 1u) == d.cta_count - 1;
-  }
+  if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
-    __threadfence_system();
-    st_release_sys_u8(d.dst + d.body, *d.tail);
+    release_tail(d.dst + d.body, *d.tail, 1);
     atomicExch(&counters[s_desc], 0u);
   }
 }
@@ -1139,9 +1150,28 @@ __global__ void __launch_bounds__(256) k_reduce_max(const float *x, uint64_t n,
   __shared__ int s_last;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
   float m = -INFINITY;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += nth)
-    m = fmax_nan(m, x[i]);
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (((uintptr_t)x & 15) == 0) {
+    // 16-B loads, four in flight per thread
+    const float4 *x4 = (const float4 *)x;
+    const uint64_t n4 = n / 4;
+    uint64_t i = t0;
+    for (; i + 3 * nth < n4; i += 4 * nth) {
+      float4 a = __ldg(x4 + i), b = __ldg(x4 + i + nth), c = __ldg(x4 + i + 2 * nth),
+             d = __ldg(x4 + i + 3 * nth);
+      m = fmax_nan(m, fmax_nan(fmax_nan(a.x, a.y), fmax_nan(a.z, a.w)));
+      m = fmax_nan(m, fmax_nan(fmax_nan(b.x, b.y), fmax_nan(b.z, b.w)));
+      m = fmax_nan(m, fmax_nan(fmax_nan(c.x, c.y), fmax_nan(c.z, c.w)));
+      m = fmax_nan(m, fmax_nan(fmax_nan(d.x, d.y), fmax_nan(d.z, d.w)));
+    }
+    for (; i < n4; i += nth) {
+      float4 a = __ldg(x4 + i);
+      m = fmax_nan(m, fmax_nan(fmax_nan(a.x, a.y), fmax_nan(a.z, a.w)));
+    }
+    for (uint64_t j = n4 * 4 + t0; j < n; j += nth) m = fmax_nan(m, x[j]);
+  } else {
+    for (uint64_t i = t0; i < n; i += nth) m = fmax_nan(m, x[i]);
+  }
   for (int o = 16; o; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(~0u, m, o));
   if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
   __syncthreads();
@@ -1209,6 +1239,7 @@ static int launch_check(const char *what) {
 }
 
 static int g_put_impl = 0;  // 0 = vector LDG/STG, 1 = TMA bulk (large segments)
+static int g_unroll = 8;    // 16-B vectors in flight per thread (4 or 8)
 
 // launch K1/K4/K5 with the configured implementation
 static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
@@ -1228,7 +1259,10 @@ static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
   } else {
     int grid, block;
     copy_geometry(s->device, a.total, &grid, &block);
-    k_put<<<grid, block, 0, s->s>>>(a);
+    if (g_unroll == 8)
+      k_put<8><<<grid, block, 0, s->s>>>(a);
+    else
+      k_put<4><<<grid, block, 0, s->s>>>(a);
   }
   return launch_check(what);
 }
@@ -1259,6 +1293,10 @@ int srf_tune(int knob, int value) {
     case 3:
       if (value != 0 && value != 1) return fail(SRF_E_INVALID_CONFIG, "alloc 0=cudaMalloc|1=vmm");
       g_alloc_vmm = value;
+      return SRF_OK;
+    case 4:
+      if (value != 4 && value != 8) return fail(SRF_E_INVALID_CONFIG, "unroll 4|8");
+      g_unroll = value;
       return SRF_OK;
     default:
       return fail(SRF_E_INVALID_CONFIG, "unknown knob %d", knob);
@@ -1703,6 +1741,7 @@ int srf_put(srf_space_t src_space, const uint64_t *src_addr,
   a.dst = dst_space->base + dst_addr;
   a.total = total;
   a.tail_release = 1;
+  a.sys_scope = (dst_space->imported || dst_space->device != s->device) ? 1 : 0;
   a.wait_empty = (flags & SRF_PUT_WAIT_EMPTY) ? 1 : 0;
   a.timeout_ns = 5ull * 1000 * 1000 * 1000;
   a.counter = s->counter;
@@ -1840,8 +1879,8 @@ int srf_reduce_max_f32(srf_space_t sp, uint64_t in_addr, uint64_t n,
   if (!rc) rc = check_raw(sp, out_addr, 4, "reduce output");
   if (rc) return rc;
   srf_stream *s = stream_or_default(sp, st);
-  uint64_t want = (n + 256 * 8 - 1) / (256 * 8);
-  uint64_t cap = std::min<uint64_t>((uint64_t)sm_count_of(s->device) * 4, kScratchBlocks);
+  uint64_t want = (n + 256 * 64 - 1) / (256 * 64);
+  uint64_t cap = std::min<uint64_t>((uint64_t)sm_count_of(s->device) * 6, kScratchBlocks);
   int grid = (int)std::max<uint64_t>(1, std::min(want, cap));
   CUDA_TRY(cudaSetDevice(s->device));
   k_reduce_max<<<grid, 256, 0, s->s>>>((const float *)(sp->base + in_addr), n,

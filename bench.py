@@ -562,16 +562,38 @@ def dynamic_rate(size, device, reps=None):
 # -- parameter-server step (configs[3]: VGG-16 sharded over the GPUs) ---------------------------------
 
 
-def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True):
-    """Device-timed PS iterations/s.  N=1: worker server 0 + PS server 1 on one
-    GPU (SURVEY 8(d) C4, G=1).  N>1: worker k + shard k co-located on GPU k,
-    variables round-robin over the shards (workloads.py:83-85)."""
+PS_CONFIGS = {
+    # name: (BASELINE config, shapes builder, workers, shards, colocate)
+    "mlp": ("configs[2] 1 PS + 2 workers, 3-layer MLP weights (16,12),(12,10),(10,4)",
+            lambda: __import__("paper_1805_08430_b200.workloads", fromlist=["x"]).mlp_shapes(),
+            2, 1, False),
+    "fcn5": ("configs[2] 1 PS + 2 workers, FCN-5 preset 204.47 MB / 10 slabs",
+             lambda: [(int(204.47e6) // 10 // 4,)] * 10, 2, 1, False),
+    "lstm": ("configs[4] LSTM preset 35.93 MB / 14 slabs, 7 workers + 1 PS, dynamic "
+             "allocation on the gradient (Variable) edges",
+             lambda: [(int(35.93e6) // 14 // 4,)] * 14, 7, 1, False),
+}
+
+
+def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True,
+             layout=None, label=None, cpu_rig=None):
+    """Device-timed PS iterations/s over a PsLayout.  Default (configs[3]):
+    VGG-16 real shapes; N=1 worker server 0 + PS server 1 on one GPU (SURVEY
+    8(d) C4, G=1); N>1 worker k + shard k co-located on GPU k, variables
+    round-robin over the shards (workloads.py:83-85)."""
     from oracle import port
     from paper_1805_08430_b200 import _lib
     from paper_1805_08430_b200.ps import PsLayout, PsStep
     from paper_1805_08430_b200.workloads import total_params, vgg16_shapes
-    shapes = shapes or vgg16_shapes()
-    L = PsLayout(shapes, 1, 1) if world == 1 else PsLayout(shapes, world, world, colocate=True)
+    if layout is None:
+        shapes = shapes or vgg16_shapes()
+        L = PsLayout(shapes, 1, 1) if world == 1 else PsLayout(shapes, world, world, colocate=True)
+        label = (f"configs[3] VGG-16 real shapes ({total_params(shapes)} fp32, {len(shapes)} "
+                 f"tensors) PS sync, " + ("worker server 0 + PS server 1 on GPU 0" if world == 1
+                                          else f"{world} workers + {world} shards co-located"))
+    else:
+        L = layout
+        shapes = L.shapes
     ps = PsStep(L, rank=rank, world=world, device=device, seed=0, op=op, lr=0.01)
     it = 0
     for _ in range(warmup):
@@ -611,6 +633,12 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
     # roofline over the busiest GPU
     tr = [L.traffic(s) for s in range(L.nservers)]
     model = sum(L.nbytes(v) for v in range(len(shapes)))
+    gpus = {}
+    for srv, x in enumerate(tr):
+        g = gpus.setdefault(srv % world, {"link_out": 0, "link_in": 0, "hbm": 0, "local": 0})
+        g["link_out"] += x["link_out"]
+        g["link_in"] += x["link_in"]
+        g["hbm"] += x["hbm"]
     if world == 1:
         alg = sum(2 * x["push_out"] + x["pull_in"] + x["hbm"] for x in tr)
         peak, _src = measured_peaks()
@@ -618,34 +646,48 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "bytes_per_step": alg}
     else:
-        per_gpu = [max(x["link_out"], x["link_in"]) for x in tr]
-        hot = max(range(world), key=lambda s: per_gpu[s])
+        per_gpu = {g: max(x["link_out"], x["link_in"]) for g, x in gpus.items()}
+        hot = max(per_gpu, key=per_gpu.get)
         ach = per_gpu[hot] * steps / t / 1e9
         roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_MEASURED_GBS,
                 "unit": "GB/s", "frac": round(ach / NVLINK_MEASURED_GBS, 4),
                 "hottest_gpu": hot, "hottest_bytes_per_step": per_gpu[hot],
-                "note": "busiest GPU's max(NVLink egress, ingress) per step; round-robin "
-                        "placement concentrates fc6 (411 MB) on one shard (SURVEY F5)"}
-    out = {"workload": f"configs[3] VGG-16 real shapes ({total_params(shapes)} fp32, "
-                       f"{len(shapes)} tensors) PS sync, op={op} lr=0.01, "
-                       + ("worker server 0 + PS server 1 on GPU 0" if world == 1
-                          else f"{world} workers + {world} shards co-located"),
+                "note": "busiest GPU's max(NVLink egress, ingress) per step (servers on the "
+                        "same GPU exchange through HBM and are not counted)"}
+    out = {"workload": f"{label}, op={op} lr=0.01",
            "steps_per_s": round(steps / t, 2), "ms_per_step": round(t / steps * 1e3, 4),
            "steps": steps, "model_bytes": model, "roofline": roof, "gpu_launches": launches,
            "clocks": clk, "verified": ok,
            "phases": "K1 weight push batch, GenGrad batch, K3 meta batch, K4+K6 fused apply"}
     ps.close()
     if cpu and rank == 0 and world == 1:
-        rig = port.PsRig(shapes, 1, 1, False, seed=0, op=op, lr=0.01)
-        t0 = time.perf_counter()
-        rig.step()
-        dt = time.perf_counter() - t0
-        out["cpu_baseline"] = {"value": round(1.0 / dt, 4), "unit": "steps/s", "cores": 1,
+        rig = cpu_rig() if cpu_rig else port.PsRig(shapes, L.workers, L.shards, L.colocate,
+                                                    seed=0, op=op, lr=0.01)
+        n, t0 = 0, time.perf_counter()
+        while True:
+            rig.step()
+            n += 1
+            dt = time.perf_counter() - t0
+            if dt > 2.0 or n >= 200:
+                break
+        out["cpu_baseline"] = {"value": round(n / dt, 4), "unit": "steps/s", "cores": 1,
                                "kind": "port",
-                               "sample": "1 PS iteration of the same VGG-16 config "
+                               "sample": f"{n} PS iteration(s) of the same config "
                                          "(oracle/port.py PsRig: chunked static pushes, "
                                          "PCG64 GenGrad, meta + chunked pulls, ApplyGrad), "
                                          f"{dt:.1f} s, host cpu_count={os.cpu_count()}"}
+    return out
+
+
+def bench_ps_configs(rank, world, device, steps, warmup, op, cpu):
+    from paper_1805_08430_b200.ps import PsLayout
+    out = {}
+    for name, (label, shapes_fn, W, P, coloc) in PS_CONFIGS.items():
+        L = PsLayout(shapes_fn(), W, P, coloc)
+        where = ("all servers on GPU 0" if world == 1 else
+                 f"server s on GPU s mod {world}")
+        out[name] = bench_ps(rank, world, device, steps, warmup, op=op, cpu=cpu, layout=L,
+                             label=f"{label}; {where}")
     return out
 
 
@@ -733,9 +775,13 @@ def main() -> int:
     if not args.no_ps:
         line["ps"] = bench_ps(rank, world, local, max(10, args.steps), args.warmup,
                               op=args.ps_op, cpu=not args.no_cpu)
+        line["ps_configs"] = bench_ps_configs(rank, world, local, max(20, args.steps),
+                                              args.warmup, args.ps_op, not args.no_cpu)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if not dev["verified"] or not e2e["verified"] or not line.get("ps", {}).get("verified", True):
+    ps_ok = line.get("ps", {}).get("verified", True) and all(
+        c["verified"] for c in line.get("ps_configs", {}).values())
+    if not dev["verified"] or not e2e["verified"] or not ps_ok:
         log("verification FAILED")
         return 1
     return 0

@@ -220,7 +220,7 @@ int srf_batch_put_create(int n, srf_space_t const *src_space, const uint64_t *sr
                          const uint64_t *tail_addr, srf_space_t const *dst_space,
                          const uint64_t *dst_addr, const uint64_t *dst_token, int flags,
                          srf_batch_t *out);
-int srf_batch_gen_create(srf_space_t space, int n, const uint64_t *grad_addr,
+int srf_batch_gen_create(int n, srf_space_t const *space, const uint64_t *grad_addr,
                          const uint64_t *nbytes, const uint64_t *weight_flag_addr,
                          srf_space_t const *credit_space, const uint64_t *credit_addr,
                          const uint64_t *node_id, uint64_t seed, srf_batch_t *out);

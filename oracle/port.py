@@ -496,16 +496,29 @@ def _mix64(x: np.ndarray) -> np.ndarray:
     return x
 
 
+def _fmix32(h: np.ndarray) -> np.ndarray:
+    h = h.astype(np.uint32, copy=True)
+    h ^= h >> np.uint32(16)
+    h *= np.uint32(0x85EBCA6B)
+    h ^= h >> np.uint32(13)
+    h *= np.uint32(0xC2B2AE35)
+    h ^= h >> np.uint32(16)
+    return h
+
+
 def device_gradient(seed: int, node: int, iteration: int, n: int) -> np.ndarray:
-    """fp32 values k_gen_batch writes for GenGrad node ``node`` at ``iteration``."""
+    """fp32 values k_gen_batch writes for GenGrad node ``node`` at ``iteration``:
+    a 64-bit key from (seed, node, iteration), then per element a 32-bit
+    murmur finaliser of (index, key halves), top 24 bits -> [0, 1)."""
     with np.errstate(over="ignore"):
         s = np.array([seed], dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
         a = _mix64(np.array([node], dtype=np.uint64) + np.uint64(0x51ED))
         b = _mix64(np.array([iteration], dtype=np.uint64) * np.uint64(0xD1B54A32D192ED03))
-        key = _mix64(s ^ a ^ b)[0]
-        idx = np.arange(n, dtype=np.uint64)
-        h = _mix64(key + idx * np.uint64(0x9E3779B97F4A7C15))
-    return ((h >> np.uint64(40)).astype(np.float32) * np.float32(1.0 / 16777216.0))
+        key = int(_mix64(s ^ a ^ b)[0])
+        k0, k1 = np.uint32(key & 0xFFFFFFFF), np.uint32(key >> 32)
+        idx = np.arange(n, dtype=np.uint32)
+        h = _fmix32(idx * np.uint32(0x9E3779B1) + k0) ^ k1
+    return (h >> np.uint32(8)).astype(np.float32) * np.float32(1.0 / 16777216.0)
 
 
 def ps_expected_device(shapes, workers: int, seed: int, iterations, op: str = "xor",

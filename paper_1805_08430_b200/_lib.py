@@ -99,7 +99,7 @@ SIGNATURES = {
     "srf_consume_checksum": (C.c_int, [vp, u64, u64, u64, u64, u64, vp]),
     "srf_batch_put_create": (C.c_int, [C.c_int, P(vp), P(u64), P(u64), P(u64), P(u64), P(vp),
                                        P(u64), P(u64), C.c_int, P(vp)]),
-    "srf_batch_gen_create": (C.c_int, [vp, C.c_int, P(u64), P(u64), P(u64), P(vp), P(u64),
+    "srf_batch_gen_create": (C.c_int, [C.c_int, P(vp), P(u64), P(u64), P(u64), P(vp), P(u64),
                                        P(u64), u64, P(vp)]),
     "srf_batch_apply_create": (C.c_int, [vp, C.c_int, P(u64), P(u64), P(C.c_int), P(C.c_int),
                                          P(vp), P(u64), P(C.c_int), P(vp), P(u64), P(u64),

@@ -757,21 +757,6 @@ struct ApplyArgs {
   float lr;
 };
 
-template <typename V>
-__device__ __forceinline__ V xor_v(V a, V b);
-template <>
-__device__ __forceinline__ uint4 xor_v<uint4>(uint4 a, uint4 b) {
-  return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
-}
-template <>
-__device__ __forceinline__ uint2 xor_v<uint2>(uint2 a, uint2 b) {
-  return make_uint2(a.x ^ b.x, a.y ^ b.y);
-}
-template <>
-__device__ __forceinline__ uint8_t xor_v<uint8_t>(uint8_t a, uint8_t b) {
-  return a ^ b;
-}
-
 // plain (coherent) 16-B load: gradients may be peer memory
 __device__ __forceinline__ uint4 ld_v4(const uint4 *p) {
   uint4 r;
@@ -781,152 +766,132 @@ __device__ __forceinline__ uint4 ld_v4(const uint4 *p) {
   return r;
 }
 
-template <typename V>
-__device__ __forceinline__ V ld_any(const V *p) {
-  return *p;
-}
-template <>
-__device__ __forceinline__ uint4 ld_any<uint4>(const uint4 *p) {
-  return ld_v4(p);
-}
-
-// XOR over nv vectors of type V starting at byte offset off.
-template <typename V, int U>
-__device__ __forceinline__ void xor_body(const ApplyArgs &a, uint64_t off,
-                                         uint64_t nv, uint64_t t,
-                                         uint64_t nth) {
-  V *var = (V *)(a.var + off);
-  uint64_t i = t;
-  for (; i + (uint64_t)(U - 1) * nth < nv; i += (uint64_t)U * nth) {
-    V acc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc[u] = ld_any<V>(var + i + u * nth);
-    for (int w = 0; w < a.nw; ++w) {
-      const V *g = (const V *)(a.g[w] + off);
-      V r[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) r[u] = ld_any<V>(g + i + u * nth);
-#pragma unroll
-      for (int u = 0; u < U; ++u) acc[u] = xor_v<V>(acc[u], r[u]);
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) var[i + u * nth] = acc[u];
-  }
-  for (; i < nv; i += nth) {
-    V acc = var[i];
-    for (int w = 0; w < a.nw; ++w)
-      acc = xor_v<V>(acc, ld_any<V>((const V *)(a.g[w] + off) + i));
-    var[i] = acc;
-  }
-}
-
 __device__ __forceinline__ float sgd1(float v, float lr, float g) {
   return __fsub_rn(v, __fmul_rn(lr, g));
 }
 
-template <int U>
-__device__ __forceinline__ void sgd_body_v4(const ApplyArgs &a, uint64_t off,
-                                            uint64_t nv, uint64_t t,
-                                            uint64_t nth) {
-  float4 *var = (float4 *)(a.var + off);
-  const float lr = a.lr;
+// One element group of the update: XOR (bytewise, any alignment class) or
+// SGD (fp32).  `g` points at an array of nw gradient base pointers (shared
+// memory in the batch kernel, grid-constant parameters in K6) - indexing it
+// never spills a pointer array to local memory.
+struct XorOp {
+  __device__ static uint4 fold(uint4 a, uint4 b, float) {
+    return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
+  }
+  __device__ static uint2 fold2(uint2 a, uint2 b, float) { return make_uint2(a.x ^ b.x, a.y ^ b.y); }
+};
+struct SgdOp {
+  __device__ static uint4 fold(uint4 a, uint4 b, float lr) {
+    return make_uint4(__float_as_uint(sgd1(__uint_as_float(a.x), lr, __uint_as_float(b.x))),
+                      __float_as_uint(sgd1(__uint_as_float(a.y), lr, __uint_as_float(b.y))),
+                      __float_as_uint(sgd1(__uint_as_float(a.z), lr, __uint_as_float(b.z))),
+                      __float_as_uint(sgd1(__uint_as_float(a.w), lr, __uint_as_float(b.w))));
+  }
+  __device__ static uint2 fold2(uint2 a, uint2 b, float lr) {
+    return make_uint2(__float_as_uint(sgd1(__uint_as_float(a.x), lr, __uint_as_float(b.x))),
+                      __float_as_uint(sgd1(__uint_as_float(a.y), lr, __uint_as_float(b.y))));
+  }
+};
+
+// 16-B vectors [0, nv) at byte offset off, U vectors in flight per thread,
+// workers folded in ascending order.
+template <class Op, int U>
+__device__ __forceinline__ void fold_v4(uint8_t *varb, const uint8_t *const *g, int nw,
+                                        uint64_t off, uint64_t nv, uint64_t t, uint64_t nth,
+                                        float lr) {
+  uint4 *var = (uint4 *)(varb + off);
   uint64_t i = t;
   for (; i + (uint64_t)(U - 1) * nth < nv; i += (uint64_t)U * nth) {
-    float4 acc[U];
+    uint4 acc[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) acc[u] = var[i + u * nth];
-    for (int w = 0; w < a.nw; ++w) {
-      const uint4 *g = (const uint4 *)(a.g[w] + off);
+    for (int w = 0; w < nw; ++w) {
+      const uint4 *gw = (const uint4 *)(g[w] + off);
       uint4 r[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) r[u] = ld_v4(g + i + u * nth);
+      for (int u = 0; u < U; ++u) r[u] = ld_v4(gw + i + u * nth);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        acc[u].x = sgd1(acc[u].x, lr, __uint_as_float(r[u].x));
-        acc[u].y = sgd1(acc[u].y, lr, __uint_as_float(r[u].y));
-        acc[u].z = sgd1(acc[u].z, lr, __uint_as_float(r[u].z));
-        acc[u].w = sgd1(acc[u].w, lr, __uint_as_float(r[u].w));
-      }
+      for (int u = 0; u < U; ++u) acc[u] = Op::fold(acc[u], r[u], lr);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) var[i + u * nth] = acc[u];
   }
   for (; i < nv; i += nth) {
-    float4 acc = var[i];
-    for (int w = 0; w < a.nw; ++w) {
-      uint4 r = ld_v4((const uint4 *)(a.g[w] + off) + i);
-      acc.x = sgd1(acc.x, lr, __uint_as_float(r.x));
-      acc.y = sgd1(acc.y, lr, __uint_as_float(r.y));
-      acc.z = sgd1(acc.z, lr, __uint_as_float(r.z));
-      acc.w = sgd1(acc.w, lr, __uint_as_float(r.w));
-    }
+    uint4 acc = var[i];
+    for (int w = 0; w < nw; ++w) acc = Op::fold(acc, ld_v4((const uint4 *)(g[w] + off) + i), lr);
     var[i] = acc;
   }
 }
 
-__device__ void apply_xor_range(const ApplyArgs &a, uint64_t t, uint64_t nth) {
-  uintptr_t m = (uintptr_t)a.var;
+template <class Op>
+__device__ __forceinline__ void fold_v2(uint8_t *varb, const uint8_t *const *g, int nw,
+                                        uint64_t off, uint64_t nv, uint64_t t, uint64_t nth,
+                                        float lr) {
+  uint2 *var = (uint2 *)(varb + off);
+  for (uint64_t i = t; i < nv; i += nth) {
+    uint2 acc = var[i];
+    for (int w = 0; w < nw; ++w) acc = Op::fold2(acc, ((const uint2 *)(g[w] + off))[i], lr);
+    var[i] = acc;
+  }
+}
+
+// The whole update of one variable over threads [t, +nth) of some grid.
+// XOR works on bytes: 16-B vectors when every pointer shares (p mod 16), 8-B
+// when they share (p mod 8) (arena blocks are 8-B aligned), bytes otherwise.
+// SGD works on fp32: same vector classes in whole floats.
+template <bool SGD>
+__device__ void apply_range(uint8_t *var, const uint8_t *const *g, int nw, uint64_t n,
+                            float lr, uint64_t t, uint64_t nth) {
+  const uintptr_t m = (uintptr_t)var;
   bool same16 = true, same8 = true;
-  for (int w = 0; w < a.nw; ++w) {
-    uintptr_t p = (uintptr_t)a.g[w];
+  for (int w = 0; w < nw; ++w) {
+    const uintptr_t p = (uintptr_t)g[w];
     same16 &= ((p ^ m) & 15) == 0;
     same8 &= ((p ^ m) & 7) == 0;
   }
-  uint64_t head = 0, nvb = 0;
+  const uint64_t unit = SGD ? 4 : 1;  // scalar element size
+  uint64_t head = 0, body = 0;
   if (same16) {
-    head = (16 - (m & 15)) & 15;
-    if (head > a.n) head = a.n;
-    uint64_t nv = (a.n - head) / 16;
-    xor_body<uint4, 4>(a, head, nv, t, nth);
-    nvb = nv * 16;
+    head = ((16 - (m & 15)) & 15);
+    if (head > n) head = n;
+    const uint64_t nv = (n - head) / 16;
+    if (SGD) fold_v4<SgdOp, 8>(var, g, nw, head, nv, t, nth, lr);
+    else fold_v4<XorOp, 8>(var, g, nw, head, nv, t, nth, lr);
+    body = nv * 16;
   } else if (same8) {
-    head = (8 - (m & 7)) & 7;
-    if (head > a.n) head = a.n;
-    uint64_t nv = (a.n - head) / 8;
-    xor_body<uint2, 8>(a, head, nv, t, nth);
-    nvb = nv * 8;
+    head = ((8 - (m & 7)) & 7);
+    if (head > n) head = n;
+    const uint64_t nv = (n - head) / 8;
+    if (SGD) fold_v2<SgdOp>(var, g, nw, head, nv, t, nth, lr);
+    else fold_v2<XorOp>(var, g, nw, head, nv, t, nth, lr);
+    body = nv * 8;
   }
-  // bytes outside the vector body: [0, head) and [head + nvb, n)
-  const uint64_t rest = a.n - nvb;
+  // scalar elements outside the vector body: [0, head) and [head + body, n)
+  const uint64_t rest = (n - body) / unit;
   for (uint64_t j = t; j < rest; j += nth) {
-    uint64_t i = j < head ? j : j + nvb;
-    uint8_t acc = a.var[i];
-    for (int w = 0; w < a.nw; ++w) acc ^= a.g[w][i];
-    a.var[i] = acc;
+    const uint64_t e = j * unit < head ? j * unit : j * unit + body;  // byte offset
+    if (SGD) {
+      float v = *(float *)(var + e);
+      for (int w = 0; w < nw; ++w) v = sgd1(v, lr, *(const float *)(g[w] + e));
+      *(float *)(var + e) = v;
+    } else {
+      uint8_t acc = var[e];
+      for (int w = 0; w < nw; ++w) acc ^= g[w][e];
+      var[e] = acc;
+    }
   }
 }
 
-__device__ void apply_sgd_range(const ApplyArgs &a, uint64_t t, uint64_t nth) {
-  uintptr_t m = (uintptr_t)a.var;
-  bool same16 = true;
-  for (int w = 0; w < a.nw; ++w) same16 &= (((uintptr_t)a.g[w] ^ m) & 15) == 0;
-  const uint64_t nf = a.n / 4;
-  uint64_t headf = 0, nvf = 0;
-  if (same16) {
-    headf = ((16 - (m & 15)) & 15) / 4;
-    if (headf > nf) headf = nf;
-    uint64_t nv = (nf - headf) / 4;
-    sgd_body_v4<4>(a, headf * 4, nv, t, nth);
-    nvf = nv * 4;
-  }
-  float *var = (float *)a.var;
-  const uint64_t rest = nf - nvf;
-  for (uint64_t j = t; j < rest; j += nth) {
-    uint64_t i = j < headf ? j : j + nvf;
-    float v = var[i];
-    for (int w = 0; w < a.nw; ++w) v = sgd1(v, a.lr, ((const float *)a.g[w])[i]);
-    var[i] = v;
-  }
+__global__ void __launch_bounds__(512) k_apply_xor(const __grid_constant__ ApplyArgs a) {
+  apply_range<false>(a.var, a.g, a.nw, a.n, a.lr,
+                     (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                     (uint64_t)gridDim.x * blockDim.x);
 }
 
-__global__ void __launch_bounds__(512) k_apply_xor(ApplyArgs a) {
-  apply_xor_range(a, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
-                  (uint64_t)gridDim.x * blockDim.x);
-}
-
-__global__ void __launch_bounds__(512) k_apply_sgd(ApplyArgs a) {
-  apply_sgd_range(a, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
-                  (uint64_t)gridDim.x * blockDim.x);
+__global__ void __launch_bounds__(512) k_apply_sgd(const __grid_constant__ ApplyArgs a) {
+  apply_range<true>(a.var, a.g, a.nw, a.n, a.lr,
+                    (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                    (uint64_t)gridDim.x * blockDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -996,8 +961,8 @@ __global__ void __launch_bounds__(512) k_put_batch(const BatchPut *descs, int n,
     if (threadIdx.x == 0 && !spin_until(d.dst + d.body, 0, timeout_ns)) atomicExch(err, 2);
     __syncthreads();
   }
-  copy_bytes_grid(d.dst, d.src, d.body, (uint64_t)lb * blockDim.x + threadIdx.x,
-                  (uint64_t)d.cta_count * blockDim.x);
+  copy_bytes_grid<8>(d.dst, d.src, d.body, (uint64_t)lb * blockDim.x + threadIdx.x,
+                     (uint64_t)d.cta_count * blockDim.x);
   __syncthreads();
   if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
   __syncthreads();
@@ -1016,9 +981,18 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
   return x;
 }
 
+__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+
 // uniform [0,1) fp32 of a counter-based stream keyed on (seed, node, iteration)
-__device__ __forceinline__ float unit_f32(uint64_t key, uint64_t i) {
-  return (float)(mix64(key + i * 0x9E3779B97F4A7C15ull) >> 40) * (1.0f / 16777216.0f);
+__device__ __forceinline__ float unit_f32(uint32_t k0, uint32_t k1, uint32_t i) {
+  return (float)((fmix32(i * 0x9E3779B1u + k0) ^ k1) >> 8) * (1.0f / 16777216.0f);
 }
 
 __global__ void __launch_bounds__(512) k_gen_batch(const BatchGen *descs, int n,
@@ -1038,54 +1012,53 @@ __global__ void __launch_bounds__(512) k_gen_batch(const BatchGen *descs, int n,
   if (regen) {
     const uint64_t key = mix64(seed * 0x9E3779B97F4A7C15ull ^ mix64(d.node + 0x51ED) ^
                                mix64(iteration * 0xD1B54A32D192ED03ull));
+    const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
     const uint64_t nf = d.n / 4;
     const uint64_t nth = (uint64_t)d.cta_count * blockDim.x;
     float4 *g4 = (float4 *)d.grad;  // gradient blocks are 16-B aligned by layout
-    for (uint64_t q = (uint64_t)lb * blockDim.x + threadIdx.x; q < nf / 4; q += nth)
-      g4[q] = make_float4(unit_f32(key, 4 * q), unit_f32(key, 4 * q + 1),
-                          unit_f32(key, 4 * q + 2), unit_f32(key, 4 * q + 3));
+    for (uint64_t q = (uint64_t)lb * blockDim.x + threadIdx.x; q < nf / 4; q += nth) {
+      const uint32_t i = (uint32_t)(4 * q);
+      g4[q] = make_float4(unit_f32(k0, k1, i), unit_f32(k0, k1, i + 1),
+                          unit_f32(k0, k1, i + 2), unit_f32(k0, k1, i + 3));
+    }
     float *g = (float *)d.grad;
     for (uint64_t i = (nf / 4) * 4 + (uint64_t)lb * blockDim.x + threadIdx.x; i < nf; i += nth)
-      g[i] = unit_f32(key, i);
+      g[i] = unit_f32(k0, k1, (uint32_t)i);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    s_last = atomicAdd(&counters[s_desc], 1u) == d.cta_count - 1;
-  }
+  if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
     // the weight was consumed: clear its flag (StaticReceiver.poll semantics)
-    if (d.weight_flag) st_release_sys_u8(d.weight_flag, 0);
+    if (d.weight_flag) release_tail(d.weight_flag, 0, 1);
     atomicExch(&counters[s_desc], 0u);
   }
 }
 
-__global__ void __launch_bounds__(512) k_apply_batch(const BatchApply *descs, int n,
+__global__ void __launch_bounds__(256) k_apply_batch(const BatchApply *descs, int n,
                                                      unsigned int *counters, int op, float lr,
                                                      uint64_t timeout_ns, int *err) {
-  __shared__ int s_desc, s_last, s_ok;
+  __shared__ int s_desc, s_last, s_bad;
   __shared__ const uint8_t *s_g[SRF_MAX_WORKERS];
-  if (threadIdx.x == 0) s_desc = find_desc(descs, n);
+  if (threadIdx.x == 0) {
+    s_desc = find_desc(descs, n);
+    s_bad = 0;
+  }
   __syncthreads();
   const BatchApply &d = descs[s_desc];
   const uint32_t lb = blockIdx.x - d.cta_begin;
-  if (threadIdx.x == 0) {
+  const int r = d.rank;
+  if (threadIdx.x < (unsigned)d.nw) {
     // DynReceiver.poll + decode_meta + validation (protocol.py:234-242,
-    // wire.py:120-142, memspace.py:145-157) for every remote worker
-    int ok = 1;
-    for (int w = 0; w < d.nw; ++w) {
-      if (!((d.is_meta >> w) & 1)) {
-        s_g[w] = d.src[w];
-        continue;
-      }
-      const uint8_t *m = d.src[w];
-      const int r = d.rank;
-      if (!spin_until(m + 8 * r + 32, 1, timeout_ns)) {
-        ok = 0;
-        atomicExch(err, 5);
-        break;
-      }
+    // wire.py:120-142, memspace.py:145-157): one lane per worker, in parallel
+    const int w = threadIdx.x;
+    const uint8_t *m = d.src[w];
+    if (!((d.is_meta >> w) & 1)) {
+      s_g[w] = m;  // co-located worker: its gradient block directly
+    } else if (!spin_until(m + 8 * r + 32, 1, timeout_ns)) {
+      atomicExch(err, 5);
+      s_bad = 1;
+    } else {
       const uint64_t addr = *(const volatile uint64_t *)(m + 8 + 8 * r);  // after the dims
       const uint64_t tok = *(const volatile uint64_t *)(m + 16 + 8 * r);
       const uint64_t plen = *(const volatile uint64_t *)(m + 24 + 8 * r);
@@ -1097,42 +1070,29 @@ __global__ void __launch_bounds__(512) k_apply_batch(const BatchApply *descs, in
       for (int k = 0; k < r; ++k) prod *= *(const volatile uint64_t *)(m + 8 + 8 * k);
       if (m[1] != r || esz == 0 || prod != plen || plen != d.n || tok != d.peer_token[w] ||
           addr < d.peer_lo[w] || addr + plen > d.peer_hi[w]) {
-        ok = 0;
         atomicExch(err, 6);
-        break;
+        s_bad = 1;
       }
       s_g[w] = d.peer_base[w] + addr;  // one-sided read through the peer mapping
     }
-    s_ok = ok;
   }
   __syncthreads();
-  if (s_ok) {
-    ApplyArgs a;
-    a.var = d.var;
-    a.nw = d.nw;
-    a.n = d.n;
-    a.lr = lr;
-    for (int w = 0; w < d.nw; ++w) a.g[w] = s_g[w];
+  if (!s_bad) {
     const uint64_t t = (uint64_t)lb * blockDim.x + threadIdx.x;
     const uint64_t nth = (uint64_t)d.cta_count * blockDim.x;
     if (op == SRF_APPLY_XOR)
-      apply_xor_range(a, t, nth);
+      apply_range<false>(d.var, s_g, d.nw, d.n, lr, t, nth);
     else
-      apply_sgd_range(a, t, nth);
+      apply_range<true>(d.var, s_g, d.nw, d.n, lr, t, nth);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    s_last = atomicAdd(&counters[s_desc], 1u) == d.cta_count - 1;
-  }
+  if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
-    // gradients consumed: clear the meta flags (credit for the next send)
-    __threadfence_system();
-    for (int w = 0; w < d.nw; ++w)
-      if ((d.is_meta >> w) & 1) st_release_sys_u8((uint8_t *)d.src[w] + 8 * d.rank + 32, 0);
-    atomicExch(&counters[s_desc], 0u);
-  }
+  // gradients consumed: the last CTA clears the meta flags (credit for the
+  // next send; DynReceiver.poll's clear)
+  if (s_last && threadIdx.x < (unsigned)d.nw && ((d.is_meta >> threadIdx.x) & 1))
+    release_tail((uint8_t *)d.src[threadIdx.x] + 8 * r + 32, 0, 1);
+  if (s_last && threadIdx.x == 0) atomicExch(&counters[s_desc], 0u);
 }
 
 // ReduceMax (graph.py:378-382): per-block max, last block folds partials.
@@ -1905,11 +1865,10 @@ struct srf_batch {
   int *err;
 };
 
-static uint32_t ctas_for(int device, uint64_t bytes, int total_desc) {
-  // ~64 KiB per CTA, at most 2 CTAs/SM for one descriptor
-  uint64_t want = (bytes + 65535) / 65536;
-  uint64_t cap = (uint64_t)sm_count_of(device) * 2;
-  (void)total_desc;
+static uint32_t ctas_for(int device, uint64_t bytes, uint64_t per_cta) {
+  // enough CTAs that each moves ~per_cta bytes, at most g_ctas_per_sm per SM
+  uint64_t want = (bytes + per_cta - 1) / per_cta;
+  uint64_t cap = (uint64_t)sm_count_of(device) * g_ctas_per_sm;
   return (uint32_t)std::max<uint64_t>(1, std::min(want, cap));
 }
 
@@ -1974,7 +1933,7 @@ int srf_batch_put_create(int n, srf_space_t const *src_space, const uint64_t *sr
     d.body = body_len[i];
     d.tail = ss->base + tail_addr[i];
     d.cta_begin = next;
-    d.cta_count = ctas_for(device, body_len[i], n);
+    d.cta_count = ctas_for(device, body_len[i], 512 * 16 * 8);
     d.wait_empty = (flags & SRF_PUT_WAIT_EMPTY) ? 1 : 0;
     d.pad = 0;
     next += d.cta_count;
@@ -1982,18 +1941,24 @@ int srf_batch_put_create(int n, srf_space_t const *src_space, const uint64_t *sr
   return finish_batch(0, device, host, src_space[0]->err, out);
 }
 
-int srf_batch_gen_create(srf_space_t sp, int n, const uint64_t *grad_addr,
+int srf_batch_gen_create(int n, srf_space_t const *space, const uint64_t *grad_addr,
                          const uint64_t *nbytes, const uint64_t *weight_flag_addr,
                          srf_space_t const *credit_space, const uint64_t *credit_addr,
                          const uint64_t *node_id, uint64_t seed, srf_batch_t *out) {
   if (n < 1) return fail(SRF_E_INVALID_CONFIG, "empty batch");
+  const int device = space[0]->device;
   std::vector<BatchGen> host(n);
   uint32_t next = 0;
   for (int i = 0; i < n; ++i) {
+    srf_space *sp = space[i];
+    if (sp->device != device)
+      return fail(SRF_E_INVALID_CONFIG, "batch spans GPUs %d and %d", device, sp->device);
     int rc = check_raw(sp, grad_addr[i], nbytes[i], "gradient");
     if (rc) return rc;
     if (grad_addr[i] % 16 || nbytes[i] % 4)
       return fail(SRF_E_SHAPE_MISMATCH, "gradient blocks must be 16-B aligned fp32");
+    if (nbytes[i] / 4 > 0xFFFFFFFFull)
+      return fail(SRF_E_SHAPE_MISMATCH, "gradient larger than 2^32 elements");
     BatchGen &d = host[i];
     d.grad = sp->base + grad_addr[i];
     d.n = nbytes[i];
@@ -2002,10 +1967,10 @@ int srf_batch_gen_create(srf_space_t sp, int n, const uint64_t *grad_addr,
                    ? nullptr : credit_space[i]->base + credit_addr[i];
     d.node = node_id[i];
     d.cta_begin = next;
-    d.cta_count = ctas_for(sp->device, nbytes[i], n);
+    d.cta_count = ctas_for(device, nbytes[i], 512 * 16 * 4);
     next += d.cta_count;
   }
-  int rc = finish_batch(1, sp->device, host, sp->err, out);
+  int rc = finish_batch(1, device, host, space[0]->err, out);
   if (rc == SRF_OK) (*out)->seed = seed;
   return rc;
 }
@@ -2054,7 +2019,7 @@ int srf_batch_apply_create(srf_space_t sp, int nvars, const uint64_t *var_addr,
       d.src[w] = ss->base + src_addr[k];
     }
     d.cta_begin = next;
-    d.cta_count = ctas_for(sp->device, nbytes[v] * (uint64_t)(d.nw + 2) / 3, nvars);
+    d.cta_count = ctas_for(sp->device, nbytes[v], 256 * 16 * 4);
     next += d.cta_count;
   }
   int rc = finish_batch(2, sp->device, host, sp->err, out);
@@ -2078,7 +2043,7 @@ int srf_batch_launch(srf_batch_t b, srf_stream_t st, uint64_t iteration, int mod
                                               b->seed, iteration, mode, timeout, b->err);
       return launch_check("k_gen_batch");
     default:
-      k_apply_batch<<<b->grid, 512, 0, st->s>>>((const BatchApply *)b->descs, b->n,
+      k_apply_batch<<<b->grid, 256, 0, st->s>>>((const BatchApply *)b->descs, b->n,
                                                 b->counters, b->op, b->lr, timeout, b->err);
       return launch_check("k_apply_batch");
   }

@@ -269,14 +269,16 @@ class PsStep:
                                self.addr(sh, ("mslot", v, w)) + mlen - 1 if remote else _NONE,
                                ps_node_ids(len(L.shapes), L.workers, v, w)[1], w))
         out["gen"] = {}
-        for w in sorted({r[-1] for r in g_rows}):
-            rr = [r for r in g_rows if r[-1] == w]
+        if g_rows:
             b = C.c_void_p()
-            _lib.call("srf_batch_gen_create", self.spaces[w].handle, len(rr),
-                      u64(r[0] for r in rr), u64(r[1] for r in rr), u64(r[2] for r in rr),
-                      (P * len(rr))(*[r[3] for r in rr]), u64(r[4] for r in rr),
-                      u64(r[5] for r in rr), self.seed, C.byref(b))
-            out["gen"][w] = b
+            n = len(g_rows)
+            _lib.call("srf_batch_gen_create", n,
+                      (P * n)(*[self.spaces[r[-1]].handle.value for r in g_rows]),
+                      u64(r[0] for r in g_rows), u64(r[1] for r in g_rows),
+                      u64(r[2] for r in g_rows), (P * n)(*[r[3] for r in g_rows]),
+                      u64(r[4] for r in g_rows), u64(r[5] for r in g_rows), self.seed,
+                      C.byref(b))
+            out["gen"]["all"] = b
         # 3. metadata writes (K3)
         rows = []
         for w in self.local:

@@ -1,0 +1,18 @@
+"""Run a few PS iterations of one config (for ncu launch lists)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1805_08430_b200.ps import PsLayout, PsStep
+from paper_1805_08430_b200.workloads import vgg16_shapes
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "vgg"
+if cfg == "vgg":
+    L = PsLayout(vgg16_shapes(), 1, 1)
+else:
+    L = PsLayout([(int(35.93e6) // 14 // 4,)] * 14, 7, 1)
+ps = PsStep(L, seed=0, op="sgd", lr=0.01)
+for it in range(1, 8):
+    ps.step(it)
+ps.sync()
+print("ok", cfg)

@@ -602,7 +602,7 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
     ps.sync()
     barrier_sync()
     ev = [C.c_void_p(), C.c_void_p()]
-    sp0 = ps.spaces[ps.local[0]]
+    sp0 = ps.stream_space
     for e in ev:
         _lib.call("srf_timing_event_create", sp0.handle, C.byref(e))
     clocks = ClockSampler(device)

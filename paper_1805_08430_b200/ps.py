@@ -189,9 +189,12 @@ class PsStep:
             # no peer may write into this rank's pools before they are set up
             import torch.distributed as dist
             dist.barrier()
-        first = self.spaces[self.local[0]]
+        # a rank hosting no server of this layout still joins the collectives;
+        # it gets a 1 MiB scratch pool only to own a stream
+        self.stream_space = (self.spaces[self.local[0]] if self.local else
+                             MemorySpace(-1 - rank, 1 << 20, seed=seed, device=device))
         self.stream = C.c_void_p()
-        _lib.call("srf_stream_create", first.handle, C.byref(self.stream))
+        _lib.call("srf_stream_create", self.stream_space.handle, C.byref(self.stream))
         self.batches = self._build_batches()
 
     # -- layout helpers -------------------------------------------------------------

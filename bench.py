@@ -162,13 +162,15 @@ class SendRecvRing:
         self.world = world
         slack = 8 * MIB
         if world == 1:
-            self.src = MemorySpace(0, nbytes + 2 * slack, seed=0, device=device)
+            self.src = MemorySpace(0, 2 * nbytes + 3 * slack, seed=0, device=device)
             self.rcv = MemorySpace(1, nbytes + 2 * slack, seed=0, device=device)
             a_src = ArenaAllocator(self.src, self.src.allocate_region(nbytes + slack, True))
             a_rcv = ArenaAllocator(self.rcv, self.rcv.allocate_region(nbytes + slack, True))
             _lib.call("srf_connect", self.src.handle, self.rcv.handle)
             self.payload = a_src.alloc(nbytes)
             self.flag = a_src.alloc(1)
+            self.stage = ArenaAllocator(self.src, self.src.allocate_region(nbytes + 64, True)
+                                        ).alloc(nbytes)
             self.recv = a_rcv.alloc(nbytes + 1)
             self.dst = self.rcv
             self.dst_region = (self.recv.base_addr, self.recv.access_token)
@@ -209,6 +211,19 @@ class SendRecvRing:
         self.lib.call("srf_put", self.src.handle, self.args_addr, self.args_len, self.args_tok,
                       2, self.dst.handle, self.dst_region[0], self.dst_region[1],
                       self.lib.PUT_WAIT_EMPTY, self.stream, None)
+
+    def put_staged(self):
+        """RDMA.cp analogue: counted copy into a registered staging block (K5),
+        then the put from there (protocol.py:77-80)."""
+        lib = self.lib
+        lib.call("srf_copy", self.src.handle, self.payload.base_addr, self.stage.base_addr,
+                 self.S, self.stream, None)
+        lib.call("srf_put", self.src.handle, lib.u64_array([self.stage.base_addr,
+                                                             self.flag.base_addr]),
+                 self.args_len, lib.u64_array([self.stage.access_token,
+                                               self.flag.access_token]),
+                 2, self.dst.handle, self.dst_region[0], self.dst_region[1],
+                 lib.PUT_WAIT_EMPTY, self.stream, None)
 
     def consume(self):
         self.lib.call("srf_flag_wait", self.rcv.handle, self.recv.base_addr + self.S, 1, 1,
@@ -479,38 +494,87 @@ def workload_config(S, world):
 
 
 def sweep(max_bytes, device):
-    """Static (device time, graph-replayed rounds) and dynamic (public API,
-    host-driven meta poll + pull) GB/s for 1 KiB x 4^k up to max_bytes, one GPU."""
+    """configs[1]: for 1 KiB x 4^k up to max_bytes on one GPU -
+    static zero-copy (K1+K2, device time of graph-replayed rounds), staged
+    'cp' (K5 copy + K1 + K2, the paper's RDMA.cp), dynamic allocation through
+    the public endpoints (meta write, doorbell poll + decode, arena alloc, K4
+    pull), and for small sizes the host-staged RPC fragment ring."""
     from paper_1805_08430_b200 import _lib
     out = []
     size = 1024
     while size <= max_bytes:
         ring = SendRecvRing(size, 0, 1, device)
-        for _ in range(8):
-            ring.put()
-            ring.consume()
-        ring.sync()
-        rounds = 200 if size <= 4 * MIB else 20
-        graph = C.c_void_p()
-        _lib.call("srf_graph_begin", ring.stream)
-        for _ in range(rounds):
-            ring.put()
-            ring.consume()
-        _lib.call("srf_graph_end", ring.stream, C.byref(graph))
-        a, b = ring.event(), ring.event()
-        _lib.call("srf_graph_launch", graph, ring.stream)
-        ring.sync()
-        ring.record(a)
-        _lib.call("srf_graph_launch", graph, ring.stream)
-        ring.record(b)
-        ring.sync()
-        t = ring.elapsed_ms(a, b) / rounds / 1e3
-        _lib.call("srf_graph_destroy", graph)
-        dyn = dynamic_rate(size, device)
-        out.append({"bytes": size, "static_gbps": round(size / t / 1e9, 3),
-                    "static_us": round(t * 1e6, 3), **dyn})
+        row = {"bytes": size}
+        for name, body in (("static", ring.put), ("cp", ring.put_staged)):
+            for _ in range(8):
+                body()
+                ring.consume()
+            ring.sync()
+            rounds = 200 if size <= 4 * MIB else 20
+            graph = C.c_void_p()
+            _lib.call("srf_graph_begin", ring.stream)
+            for _ in range(rounds):
+                body()
+                ring.consume()
+            _lib.call("srf_graph_end", ring.stream, C.byref(graph))
+            a, b = ring.event(), ring.event()
+            _lib.call("srf_graph_launch", graph, ring.stream)
+            ring.sync()
+            ring.record(a)
+            _lib.call("srf_graph_launch", graph, ring.stream)
+            ring.record(b)
+            ring.sync()
+            t = ring.elapsed_ms(a, b) / rounds / 1e3
+            _lib.call("srf_graph_destroy", graph)
+            row[f"{name}_gbps"] = round(size / t / 1e9, 3)
+            row[f"{name}_us"] = round(t * 1e6, 3)
+        row["verified"] = ring.verify()
+        row.update(dynamic_rate(size, device))
+        if size <= MIB:
+            row.update(rpc_rate(size, device))
+        out.append(row)
         size *= 4
     return out
+
+
+def rpc_rate(size, device, reps=5):
+    """The copy-heavy RPC baseline (protocol.py:257-448): 4 KiB fragments with a
+    16-B header through a 16-slot receive ring, counted copies on both sides;
+    fragments cross through host staging (send/recv verbs are host control
+    plane here)."""
+    from paper_1805_08430_b200.fabric import Fabric
+    from paper_1805_08430_b200.graph import Tensor
+    from paper_1805_08430_b200.memspace import ArenaAllocator, BufferRef, MemorySpace
+    from paper_1805_08430_b200.runtime.protocol import RpcReceiver, RpcSender
+    from paper_1805_08430_b200.wire import ElemType
+    cap = 4 * size + 8 * MIB
+    fab = Fabric()
+    sp = {s: MemorySpace(s, cap, device=device) for s in (0, 1)}
+    ar = {s: ArenaAllocator(sp[s], sp[s].allocate_region(2 * size + 4 * MIB, True)) for s in (0, 1)}
+    dv = {s: fab.create_device(sp[s], qps_per_peer=2) for s in (0, 1)}
+    fwd = dv[0].connect(dv[1].endpoint)
+    back = dv[1].channels_to(dv[0].endpoint)
+    snd = RpcSender(0, 1, sp[0], ar[0], fwd[1])
+    rcv = RpcReceiver(0, 1, sp[1], ar[1], ar[1], back[1])
+    t = Tensor((size // 4,), ElemType.F32, BufferRef(ar[0].alloc(size), ar[0]), 0)
+
+    def one():
+        snd.start(t)
+        got = None
+        while got is None or snd.busy:
+            snd.pump()
+            r = rcv.poll()
+            got = r if r is not None else got
+        got.buffer.release()
+
+    one()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        one()
+    dt = (time.perf_counter() - t0) / reps
+    for s in sp.values():
+        s.close()
+    return {"rpc_gbps": round(size / dt / 1e9, 4), "rpc_us": round(dt * 1e6, 1)}
 
 
 def dynamic_rate(size, device, reps=None):
@@ -610,9 +674,11 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
     barrier_sync()
     l0 = _lib.launch_count()
     _lib.call("srf_event_record_on", ev[0], ps.stream)
+    ps.fork()
     for _ in range(steps):
         it += 1
         ps.step(it)
+    ps.join()
     _lib.call("srf_event_record_on", ev[1], ps.stream)
     ps.sync()
     launches = int(dist_sum(_lib.launch_count() - l0))
@@ -658,7 +724,8 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
            "steps_per_s": round(steps / t, 2), "ms_per_step": round(t / steps * 1e3, 4),
            "steps": steps, "model_bytes": model, "roofline": roof, "gpu_launches": launches,
            "clocks": clk, "verified": ok,
-           "phases": "K1 weight push batch, GenGrad batch, K3 meta batch, K4+K6 fused apply"}
+           "phases": "K1 weight push batch, GenGrad batch, K3 meta batch, K4+K6 fused apply",
+           "schedule": "overlapped (3 streams, capped grids)" if ps.overlap else "one stream"}
     ps.close()
     if cpu and rank == 0 and world == 1:
         rig = cpu_rig() if cpu_rig else port.PsRig(shapes, L.workers, L.shards, L.colocate,

@@ -50,6 +50,9 @@ typedef struct srf_event  *srf_event_t;   /* one verb's completion          */
 const char *srf_last_error(void);
 int srf_version(void);
 int srf_device_count(int *count);
+/* pinned host staging (async H2D of metadata blocks, e2e inputs) */
+int srf_host_alloc(uint64_t nbytes, void **out);
+int srf_host_free(void *ptr);
 /* number of sm_100a kernels this library launched since load */
 uint64_t srf_launch_count(void);
 /* launch-geometry knobs of the copy kernels: 0 = CTAs per SM (1..32),
@@ -180,6 +183,22 @@ int srf_consume_checksum(srf_space_t space, uint64_t flag_addr, uint64_t data_ad
                          uint64_t n, uint64_t out_addr, uint64_t timeout_ns,
                          srf_stream_t stream);
 
+/* ---- host doorbells (polling without a CUDA call) -------
+ * srf_doorbell_bind gives a receive region (static payload||flag, or a
+ * metadata block with mirror != 0) a pinned, host-mapped shadow.  Every
+ * srf_put from this process into that region also writes the shadow from its
+ * last CTA (the block, then the flag, st.release.sys), so
+ * StaticReceiver.poll / DynReceiver.poll (protocol.py:124-138, :234-242) read
+ * host memory instead of copying from the device.  srf_flag_read falls back
+ * to a device read when no doorbell is bound or the space was exported to
+ * other processes.  srf_flag_clear clears the shadow and (asynchronously, on
+ * the space's stream) the device byte; the next srf_put into the region waits
+ * for that clear. */
+int srf_doorbell_bind(srf_space_t space, uint64_t region_addr, uint64_t region_len,
+                      int mirror);
+int srf_flag_read(srf_space_t space, uint64_t tail_addr, uint64_t len, void *host_out);
+int srf_flag_clear(srf_space_t space, uint64_t tail_addr);
+
 /* graph.py apply_in_place (graph.py:392-405) for W workers in one pass.
  * K6 ps_apply:  op SRF_APPLY_XOR: var ^= g_0 ^ ... ^ g_{W-1} (bytewise)
  *               op SRF_APPLY_SGD: var = (((var - lr*g_0) - lr*g_1) ...) fp32,
@@ -230,7 +249,10 @@ int srf_batch_apply_create(srf_space_t space, int nvars, const uint64_t *var_add
                            const int *is_meta, srf_space_t const *peer_space,
                            const uint64_t *peer_lo, const uint64_t *peer_hi,
                            const uint64_t *peer_token, int op, float lr, srf_batch_t *out);
-int srf_batch_launch(srf_batch_t batch, srf_stream_t stream, uint64_t iteration, int mode);
+/* grid_cap > 0 bounds the grid (CTAs loop over the batch's work units): the
+ * overlapped PS schedule caps every phase so all phases fit on the GPU at once */
+int srf_batch_launch(srf_batch_t batch, srf_stream_t stream, uint64_t iteration, int mode,
+                     int grid_cap);
 int srf_batch_destroy(srf_batch_t batch);
 
 /* ReduceMax consumer of the microbenchmark (graph.py:378-382) on the

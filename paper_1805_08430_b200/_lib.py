@@ -50,6 +50,8 @@ SIGNATURES = {
     "srf_version": (C.c_int, []),
     "srf_device_count": (C.c_int, [P(C.c_int)]),
     "srf_launch_count": (u64, []),
+    "srf_host_alloc": (C.c_int, [u64, P(vp)]),
+    "srf_host_free": (C.c_int, [vp]),
     "srf_tune": (C.c_int, [C.c_int, C.c_int]),
     "srf_space_create": (C.c_int, [C.c_int, C.c_int, u64, C.c_uint32, P(vp)]),
     "srf_space_destroy": (C.c_int, [vp]),
@@ -104,8 +106,11 @@ SIGNATURES = {
     "srf_batch_apply_create": (C.c_int, [vp, C.c_int, P(u64), P(u64), P(C.c_int), P(C.c_int),
                                          P(vp), P(u64), P(C.c_int), P(vp), P(u64), P(u64),
                                          P(u64), C.c_int, C.c_float, P(vp)]),
-    "srf_batch_launch": (C.c_int, [vp, vp, u64, C.c_int]),
+    "srf_batch_launch": (C.c_int, [vp, vp, u64, C.c_int, C.c_int]),
     "srf_batch_destroy": (C.c_int, [vp]),
+    "srf_doorbell_bind": (C.c_int, [vp, u64, u64, C.c_int]),
+    "srf_flag_read": (C.c_int, [vp, u64, u64, vp]),
+    "srf_flag_clear": (C.c_int, [vp, u64]),
     "srf_reduce_max_f32": (C.c_int, [vp, u64, u64, u64, vp]),
 }
 
@@ -183,6 +188,25 @@ def device_count() -> int:
     n = C.c_int(0)
     rc = load().srf_device_count(C.byref(n))
     return n.value if rc == SRF_OK else 0
+
+
+class PinnedBuffer:
+    """Page-locked host bytes (cudaHostAlloc) for asynchronous H2D staging."""
+
+    def __init__(self, nbytes: int):
+        p = C.c_void_p()
+        call("srf_host_alloc", nbytes, C.byref(p))
+        self.ptr = p.value
+        self.nbytes = nbytes
+
+    def write(self, data: bytes) -> None:
+        C.memmove(self.ptr, data, len(data))
+
+    def __del__(self):  # pragma: no cover
+        try:
+            load().srf_host_free(C.c_void_p(self.ptr))
+        except Exception:
+            pass
 
 
 class Event:

@@ -23,6 +23,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/srflow.h"
@@ -85,6 +86,22 @@ struct srf_space {
   uint64_t next_addr;
   srf_stream *stream;  // default stream (local work + byte IO)
   int *err;            // device error word (flag-wait timeouts)
+  // host-visible doorbells: pinned, mapped shadows of receive
+  // flags / metadata blocks that K1/K3 update next to the device bytes
+  uint8_t *db_host = nullptr;   // pinned host page(s)
+  uint8_t *db_dev = nullptr;    // the same memory, device address
+  uint64_t db_cap = 0, db_used = 0;
+  bool exported = false;        // producers may live in other processes
+  std::unordered_map<uint64_t, struct Doorbell> *db = nullptr;  // tail addr -> entry
+};
+
+struct Doorbell {
+  uint64_t region_addr, region_len;  // shadowed device bytes
+  uint64_t host_off;                 // offset of the shadow in db_host
+  uint64_t shadow_len;               // last shadow_len bytes of the region (flag last)
+  bool mirror;                       // whole region (metadata) or only the tail flag
+  cudaEvent_t clear_ev;              // receiver's device-flag clear
+  bool clear_pending;
 };
 
 struct srf_event {
@@ -464,6 +481,8 @@ struct PutArgs {
   int tail_release;      // 1: last byte written last with st.release.sys
   int wait_empty;        // 1: spin until dst[total-1] == 0 before writing
   int sys_scope;         // 1: destination is a peer's memory (system-scope release)
+  uint8_t *db;           // host-mapped doorbell shadow (nullptr: none)
+  uint32_t db_len;       // bytes mirrored (1: tail flag only; total: whole block)
   uint64_t timeout_ns;
   unsigned int *counter; // arrival counter (per stream, reset by last CTA)
   int *err;
@@ -510,7 +529,24 @@ __global__ void __launch_bounds__(512) k_put(PutArgs a) {
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
     const Seg &ls = a.seg[a.nseg - 1];
-    release_tail(tail, ls.src[ls.len - 1], a.sys_scope);
+    const uint32_t v = ls.src[ls.len - 1];
+    release_tail(tail, v, a.sys_scope);
+    if (a.db) {
+      // host doorbell: mirror the block (metadata) and then its flag, release
+      // at system scope so a host load that sees the flag sees the block
+      for (uint32_t i = 0; i + 1 < a.db_len; ++i) {
+        const uint64_t off = a.total - a.db_len + i;
+        uint64_t acc = 0;
+        const uint8_t *b = nullptr;
+        for (int k = 0; k < a.nseg; ++k) {
+          if (off < acc + a.seg[k].len) { b = a.seg[k].src + (off - acc); break; }
+          acc += a.seg[k].len;
+        }
+        a.db[i] = b ? *b : 0;
+      }
+      __threadfence_system();
+      st_release_sys_u8(a.db + a.db_len - 1, v);
+    }
     atomicExch(a.counter, 0u);
   }
 }
@@ -693,7 +729,24 @@ __global__ void __launch_bounds__(256) k_put_bulk(PutArgs a) {
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
     const Seg &ls = a.seg[a.nseg - 1];
-    release_tail(tail, ls.src[ls.len - 1], a.sys_scope);
+    const uint32_t v = ls.src[ls.len - 1];
+    release_tail(tail, v, a.sys_scope);
+    if (a.db) {
+      // host doorbell: mirror the block (metadata) and then its flag, release
+      // at system scope so a host load that sees the flag sees the block
+      for (uint32_t i = 0; i + 1 < a.db_len; ++i) {
+        const uint64_t off = a.total - a.db_len + i;
+        uint64_t acc = 0;
+        const uint8_t *b = nullptr;
+        for (int k = 0; k < a.nseg; ++k) {
+          if (off < acc + a.seg[k].len) { b = a.seg[k].src + (off - acc); break; }
+          acc += a.seg[k].len;
+        }
+        a.db[i] = b ? *b : 0;
+      }
+      __threadfence_system();
+      st_release_sys_u8(a.db + a.db_len - 1, v);
+    }
     atomicExch(a.counter, 0u);
   }
 }
@@ -929,12 +982,12 @@ struct BatchApply {      // shard: fused dynamic receive (meta decode + peer
 };
 
 template <typename D>
-__device__ __forceinline__ int find_desc(const D *d, int n) {
-  // largest i with d[i].cta_begin <= blockIdx.x
+__device__ __forceinline__ int find_desc(const D *d, int n, uint32_t u) {
+  // largest i with d[i].cta_begin <= u (work units are CTA-sized slices)
   int lo = 0, hi = n - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
-    if (d[mid].cta_begin <= blockIdx.x) lo = mid; else hi = mid - 1;
+    if (d[mid].cta_begin <= u) lo = mid; else hi = mid - 1;
   }
   return lo;
 }
@@ -950,25 +1003,28 @@ __device__ __forceinline__ bool spin_until(const uint8_t *p, uint32_t want,
 }
 
 __global__ void __launch_bounds__(512) k_put_batch(const BatchPut *descs, int n,
-                                                   unsigned int *counters,
+                                                   uint32_t total_units, unsigned int *counters,
                                                    uint64_t timeout_ns, int *err) {
   __shared__ int s_desc, s_last;
-  if (threadIdx.x == 0) s_desc = find_desc(descs, n);
-  __syncthreads();
-  const BatchPut d = descs[s_desc];
-  const uint32_t lb = blockIdx.x - d.cta_begin;
-  if (d.wait_empty) {
-    if (threadIdx.x == 0 && !spin_until(d.dst + d.body, 0, timeout_ns)) atomicExch(err, 2);
+  for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x) {
+    if (threadIdx.x == 0) s_desc = find_desc(descs, n, u);
     __syncthreads();
-  }
-  copy_bytes_grid<8>(d.dst, d.src, d.body, (uint64_t)lb * blockDim.x + threadIdx.x,
-                     (uint64_t)d.cta_count * blockDim.x);
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
-  __syncthreads();
-  if (s_last && threadIdx.x == 0) {
-    release_tail(d.dst + d.body, *d.tail, 1);
-    atomicExch(&counters[s_desc], 0u);
+    const BatchPut d = descs[s_desc];
+    const uint32_t lb = u - d.cta_begin;
+    if (d.wait_empty) {
+      if (threadIdx.x == 0 && !spin_until(d.dst + d.body, 0, timeout_ns)) atomicExch(err, 2);
+      __syncthreads();
+    }
+    copy_bytes_grid<8>(d.dst, d.src, d.body, (uint64_t)lb * blockDim.x + threadIdx.x,
+                       (uint64_t)d.cta_count * blockDim.x);
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      release_tail(d.dst + d.body, *d.tail, 1);
+      atomicExch(&counters[s_desc], 0u);
+    }
+    __syncthreads();  // shared state is reused by the next unit
   }
 }
 
@@ -996,103 +1052,111 @@ __device__ __forceinline__ float unit_f32(uint32_t k0, uint32_t k1, uint32_t i) 
 }
 
 __global__ void __launch_bounds__(512) k_gen_batch(const BatchGen *descs, int n,
-                                                   unsigned int *counters, uint64_t seed,
+                                                   uint32_t total_units, unsigned int *counters,
+                                                   uint64_t seed,
                                                    uint64_t iteration, int regen,
                                                    uint64_t timeout_ns, int *err) {
   __shared__ int s_desc, s_last;
-  if (threadIdx.x == 0) s_desc = find_desc(descs, n);
-  __syncthreads();
-  const BatchGen d = descs[s_desc];
-  const uint32_t lb = blockIdx.x - d.cta_begin;
-  if (threadIdx.x == 0) {
-    if (d.weight_flag && !spin_until(d.weight_flag, 1, timeout_ns)) atomicExch(err, 3);
-    if (d.credit && !spin_until(d.credit, 0, timeout_ns)) atomicExch(err, 4);
-  }
-  __syncthreads();
-  if (regen) {
-    const uint64_t key = mix64(seed * 0x9E3779B97F4A7C15ull ^ mix64(d.node + 0x51ED) ^
-                               mix64(iteration * 0xD1B54A32D192ED03ull));
-    const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
-    const uint64_t nf = d.n / 4;
-    const uint64_t nth = (uint64_t)d.cta_count * blockDim.x;
-    float4 *g4 = (float4 *)d.grad;  // gradient blocks are 16-B aligned by layout
-    for (uint64_t q = (uint64_t)lb * blockDim.x + threadIdx.x; q < nf / 4; q += nth) {
-      const uint32_t i = (uint32_t)(4 * q);
-      g4[q] = make_float4(unit_f32(k0, k1, i), unit_f32(k0, k1, i + 1),
-                          unit_f32(k0, k1, i + 2), unit_f32(k0, k1, i + 3));
+  for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x) {
+    if (threadIdx.x == 0) s_desc = find_desc(descs, n, u);
+    __syncthreads();
+    const BatchGen d = descs[s_desc];
+    const uint32_t lb = u - d.cta_begin;
+    if (threadIdx.x == 0) {
+      if (d.weight_flag && !spin_until(d.weight_flag, 1, timeout_ns)) atomicExch(err, 3);
+      if (d.credit && !spin_until(d.credit, 0, timeout_ns)) atomicExch(err, 4);
     }
-    float *g = (float *)d.grad;
-    for (uint64_t i = (nf / 4) * 4 + (uint64_t)lb * blockDim.x + threadIdx.x; i < nf; i += nth)
-      g[i] = unit_f32(k0, k1, (uint32_t)i);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
-  __syncthreads();
-  if (s_last && threadIdx.x == 0) {
-    // the weight was consumed: clear its flag (StaticReceiver.poll semantics)
-    if (d.weight_flag) release_tail(d.weight_flag, 0, 1);
-    atomicExch(&counters[s_desc], 0u);
+    __syncthreads();
+    if (regen) {
+      const uint64_t key = mix64(seed * 0x9E3779B97F4A7C15ull ^ mix64(d.node + 0x51ED) ^
+                                 mix64(iteration * 0xD1B54A32D192ED03ull));
+      const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+      const uint64_t nf = d.n / 4;
+      const uint64_t nth = (uint64_t)d.cta_count * blockDim.x;
+      float4 *g4 = (float4 *)d.grad;  // gradient blocks are 16-B aligned by layout
+      for (uint64_t q = (uint64_t)lb * blockDim.x + threadIdx.x; q < nf / 4; q += nth) {
+        const uint32_t i = (uint32_t)(4 * q);
+        g4[q] = make_float4(unit_f32(k0, k1, i), unit_f32(k0, k1, i + 1),
+                            unit_f32(k0, k1, i + 2), unit_f32(k0, k1, i + 3));
+      }
+      float *g = (float *)d.grad;
+      for (uint64_t i = (nf / 4) * 4 + (uint64_t)lb * blockDim.x + threadIdx.x; i < nf; i += nth)
+        g[i] = unit_f32(k0, k1, (uint32_t)i);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      // the weight was consumed: clear its flag (StaticReceiver.poll semantics)
+      if (d.weight_flag) release_tail(d.weight_flag, 0, 1);
+      atomicExch(&counters[s_desc], 0u);
+    }
+    __syncthreads();  // shared state is reused by the next unit
   }
 }
 
 __global__ void __launch_bounds__(256) k_apply_batch(const BatchApply *descs, int n,
-                                                     unsigned int *counters, int op, float lr,
+                                                     uint32_t total_units, unsigned int *counters,
+                                                     int op, float lr,
                                                      uint64_t timeout_ns, int *err) {
   __shared__ int s_desc, s_last, s_bad;
   __shared__ const uint8_t *s_g[SRF_MAX_WORKERS];
-  if (threadIdx.x == 0) {
-    s_desc = find_desc(descs, n);
-    s_bad = 0;
-  }
-  __syncthreads();
-  const BatchApply &d = descs[s_desc];
-  const uint32_t lb = blockIdx.x - d.cta_begin;
-  const int r = d.rank;
-  if (threadIdx.x < (unsigned)d.nw) {
-    // DynReceiver.poll + decode_meta + validation (protocol.py:234-242,
-    // wire.py:120-142, memspace.py:145-157): one lane per worker, in parallel
-    const int w = threadIdx.x;
-    const uint8_t *m = d.src[w];
-    if (!((d.is_meta >> w) & 1)) {
-      s_g[w] = m;  // co-located worker: its gradient block directly
-    } else if (!spin_until(m + 8 * r + 32, 1, timeout_ns)) {
-      atomicExch(err, 5);
-      s_bad = 1;
-    } else {
-      const uint64_t addr = *(const volatile uint64_t *)(m + 8 + 8 * r);  // after the dims
-      const uint64_t tok = *(const volatile uint64_t *)(m + 16 + 8 * r);
-      const uint64_t plen = *(const volatile uint64_t *)(m + 24 + 8 * r);
-      // decode_meta's consistency check: payload_len == prod(dims) * elem size
-      const uint32_t code = m[0];
-      const uint64_t esz = code == 0 ? 4 : code == 1 ? 8 : code == 2 ? 4 : code == 3 ? 8
-                         : code == 4 ? 1 : 0;
-      uint64_t prod = esz;
-      for (int k = 0; k < r; ++k) prod *= *(const volatile uint64_t *)(m + 8 + 8 * k);
-      if (m[1] != r || esz == 0 || prod != plen || plen != d.n || tok != d.peer_token[w] ||
-          addr < d.peer_lo[w] || addr + plen > d.peer_hi[w]) {
-        atomicExch(err, 6);
-        s_bad = 1;
-      }
-      s_g[w] = d.peer_base[w] + addr;  // one-sided read through the peer mapping
+  for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x) {
+    if (threadIdx.x == 0) {
+      s_desc = find_desc(descs, n, u);
+      s_bad = 0;
     }
+    __syncthreads();
+    const BatchApply &d = descs[s_desc];
+    const uint32_t lb = u - d.cta_begin;
+    const int r = d.rank;
+    if (threadIdx.x < (unsigned)d.nw) {
+      // DynReceiver.poll + decode_meta + validation (protocol.py:234-242,
+      // wire.py:120-142, memspace.py:145-157): one lane per worker, in parallel
+      const int w = threadIdx.x;
+      const uint8_t *m = d.src[w];
+      if (!((d.is_meta >> w) & 1)) {
+        s_g[w] = m;  // co-located worker: its gradient block directly
+      } else if (!spin_until(m + 8 * r + 32, 1, timeout_ns)) {
+        atomicExch(err, 5);
+        s_bad = 1;
+      } else {
+        const uint64_t addr = *(const volatile uint64_t *)(m + 8 + 8 * r);  // after the dims
+        const uint64_t tok = *(const volatile uint64_t *)(m + 16 + 8 * r);
+        const uint64_t plen = *(const volatile uint64_t *)(m + 24 + 8 * r);
+        // decode_meta's consistency check: payload_len == prod(dims) * elem size
+        const uint32_t code = m[0];
+        const uint64_t esz = code == 0 ? 4 : code == 1 ? 8 : code == 2 ? 4 : code == 3 ? 8
+                           : code == 4 ? 1 : 0;
+        uint64_t prod = esz;
+        for (int k = 0; k < r; ++k) prod *= *(const volatile uint64_t *)(m + 8 + 8 * k);
+        if (m[1] != r || esz == 0 || prod != plen || plen != d.n || tok != d.peer_token[w] ||
+            addr < d.peer_lo[w] || addr + plen > d.peer_hi[w]) {
+          atomicExch(err, 6);
+          s_bad = 1;
+        }
+        s_g[w] = d.peer_base[w] + addr;  // one-sided read through the peer mapping
+      }
+    }
+    __syncthreads();
+    if (!s_bad) {
+      const uint64_t t = (uint64_t)lb * blockDim.x + threadIdx.x;
+      const uint64_t nth = (uint64_t)d.cta_count * blockDim.x;
+      if (op == SRF_APPLY_XOR)
+        apply_range<false>(d.var, s_g, d.nw, d.n, lr, t, nth);
+      else
+        apply_range<true>(d.var, s_g, d.nw, d.n, lr, t, nth);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
+    __syncthreads();
+    // gradients consumed: the last CTA clears the meta flags (credit for the
+    // next send; DynReceiver.poll's clear)
+    if (s_last && threadIdx.x < (unsigned)d.nw && ((d.is_meta >> threadIdx.x) & 1))
+      release_tail((uint8_t *)d.src[threadIdx.x] + 8 * r + 32, 0, 1);
+    if (s_last && threadIdx.x == 0) atomicExch(&counters[s_desc], 0u);
+    __syncthreads();  // shared state is reused by the next unit
   }
-  __syncthreads();
-  if (!s_bad) {
-    const uint64_t t = (uint64_t)lb * blockDim.x + threadIdx.x;
-    const uint64_t nth = (uint64_t)d.cta_count * blockDim.x;
-    if (op == SRF_APPLY_XOR)
-      apply_range<false>(d.var, s_g, d.nw, d.n, lr, t, nth);
-    else
-      apply_range<true>(d.var, s_g, d.nw, d.n, lr, t, nth);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
-  __syncthreads();
-  // gradients consumed: the last CTA clears the meta flags (credit for the
-  // next send; DynReceiver.poll's clear)
-  if (s_last && threadIdx.x < (unsigned)d.nw && ((d.is_meta >> threadIdx.x) & 1))
-    release_tail((uint8_t *)d.src[threadIdx.x] + 8 * r + 32, 0, 1);
-  if (s_last && threadIdx.x == 0) atomicExch(&counters[s_desc], 0u);
 }
 
 // ReduceMax (graph.py:378-382): per-block max, last block folds partials.
@@ -1264,6 +1328,17 @@ int srf_tune(int knob, int value) {
 }
 uint64_t srf_launch_count(void) { return g_launches.load(); }
 
+int srf_host_alloc(uint64_t nbytes, void **out) {
+  CUDA_TRY(cudaHostAlloc(out, nbytes ? nbytes : 1, cudaHostAllocPortable));
+  memset(*out, 0, nbytes ? nbytes : 1);
+  return SRF_OK;
+}
+
+int srf_host_free(void *p) {
+  if (p) cudaFreeHost(p);
+  return SRF_OK;
+}
+
 int srf_device_count(int *count) {
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
@@ -1334,6 +1409,11 @@ int srf_space_destroy(srf_space_t sp) {
   if (!sp) return SRF_OK;
   cudaSetDevice(sp->device);
   free_stream(sp->stream);
+  if (sp->db) {
+    for (auto &kv : *sp->db) cudaEventDestroy(kv.second.clear_ev);
+    delete sp->db;
+    cudaFreeHost(sp->db_host);
+  }
   if (sp->vmm)
     vmm_free(sp);
   else if (sp->imported)
@@ -1524,6 +1604,7 @@ int srf_enable_peer(int device, int peer_device) {
 int srf_space_export_fd(srf_space_t sp, int *fd) {
   if (!sp->vmm || sp->imported)
     return fail(SRF_E_INVALID_CONFIG, "fd export needs a VMM-allocated local space");
+  sp->exported = true;
   if (sp->export_fd < 0) {
     auto exp = drv<PFN_export>("cuMemExportToShareableHandle");
     if (!exp) return fail(SRF_E_DEVICE, "cuMemExportToShareableHandle unavailable");
@@ -1578,6 +1659,7 @@ int srf_space_export(srf_space_t sp, void *handle64) {
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
   if (sp->imported) return fail(SRF_E_INVALID_CONFIG, "cannot re-export a proxy");
   if (sp->vmm) return fail(SRF_E_INVALID_CONFIG, "VMM pools export by fd (srf_space_export_fd)");
+  sp->exported = true;
   CUDA_TRY(cudaSetDevice(sp->device));
   cudaIpcMemHandle_t h;
   CUDA_TRY(cudaIpcGetMemHandle(&h, sp->base));
@@ -1702,6 +1784,24 @@ int srf_put(srf_space_t src_space, const uint64_t *src_addr,
   a.total = total;
   a.tail_release = 1;
   a.sys_scope = (dst_space->imported || dst_space->device != s->device) ? 1 : 0;
+  a.db = nullptr;
+  a.db_len = 0;
+  if (dst_space->db && !dst_space->imported) {
+    std::lock_guard<std::mutex> g(dst_space->mu);
+    auto it = dst_space->db->find(dst_addr + total - 1);
+    if (it != dst_space->db->end()) {
+      Doorbell &d = it->second;
+      const uint64_t n = std::min<uint64_t>(total, d.shadow_len);
+      a.db = dst_space->db_dev + d.host_off + (d.shadow_len - n);
+      a.db_len = (uint32_t)n;
+      if (d.clear_pending) {
+        // the receiver's clear of the device flag precedes this write
+        CUDA_TRY(cudaSetDevice(s->device));
+        CUDA_TRY(cudaStreamWaitEvent(s->s, d.clear_ev, 0));
+        d.clear_pending = false;
+      }
+    }
+  }
   a.wait_empty = (flags & SRF_PUT_WAIT_EMPTY) ? 1 : 0;
   a.timeout_ns = 5ull * 1000 * 1000 * 1000;
   a.counter = s->counter;
@@ -2030,21 +2130,25 @@ int srf_batch_apply_create(srf_space_t sp, int nvars, const uint64_t *var_addr,
   return rc;
 }
 
-int srf_batch_launch(srf_batch_t b, srf_stream_t st, uint64_t iteration, int mode) {
+int srf_batch_launch(srf_batch_t b, srf_stream_t st, uint64_t iteration, int mode,
+                     int grid_cap) {
   const uint64_t timeout = 10ull * 1000 * 1000 * 1000;
+  const uint32_t units = (uint32_t)b->grid;
+  const int grid = (int)(grid_cap > 0 ? std::min<uint32_t>(units, (uint32_t)grid_cap) : units);
   CUDA_TRY(cudaSetDevice(st->device));
   switch (b->kind) {
     case 0:
-      k_put_batch<<<b->grid, 512, 0, st->s>>>((const BatchPut *)b->descs, b->n, b->counters,
-                                              timeout, b->err);
+      k_put_batch<<<grid, 512, 0, st->s>>>((const BatchPut *)b->descs, b->n, units,
+                                           b->counters, timeout, b->err);
       return launch_check("k_put_batch");
     case 1:
-      k_gen_batch<<<b->grid, 512, 0, st->s>>>((const BatchGen *)b->descs, b->n, b->counters,
-                                              b->seed, iteration, mode, timeout, b->err);
+      k_gen_batch<<<grid, 512, 0, st->s>>>((const BatchGen *)b->descs, b->n, units,
+                                           b->counters, b->seed, iteration, mode, timeout,
+                                           b->err);
       return launch_check("k_gen_batch");
     default:
-      k_apply_batch<<<b->grid, 256, 0, st->s>>>((const BatchApply *)b->descs, b->n,
-                                                b->counters, b->op, b->lr, timeout, b->err);
+      k_apply_batch<<<grid, 256, 0, st->s>>>((const BatchApply *)b->descs, b->n, units,
+                                             b->counters, b->op, b->lr, timeout, b->err);
       return launch_check("k_apply_batch");
   }
 }
@@ -2056,6 +2160,91 @@ int srf_batch_destroy(srf_batch_t b) {
   cudaFree(b->counters);
   delete b;
   return SRF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// doorbells (host-visible receive flags)
+// ---------------------------------------------------------------------------
+int srf_doorbell_bind(srf_space_t sp, uint64_t region_addr, uint64_t region_len, int mirror) {
+  if (region_len < 1) return fail(SRF_E_ZERO_LENGTH, "doorbell region must be >= 1 byte");
+  int rc = check_raw(sp, region_addr, region_len, "doorbell region");
+  if (rc) return rc;
+  if (sp->imported) return fail(SRF_E_INVALID_CONFIG, "doorbells live with the receiver");
+  std::lock_guard<std::mutex> g(sp->mu);
+  if (!sp->db) {
+    sp->db_cap = 1 << 20;
+    CUDA_TRY(cudaSetDevice(sp->device));
+    CUDA_TRY(cudaHostAlloc((void **)&sp->db_host, sp->db_cap,
+                           cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(sp->db_host, 0, sp->db_cap);
+    CUDA_TRY(cudaHostGetDevicePointer((void **)&sp->db_dev, sp->db_host, 0));
+    sp->db = new std::unordered_map<uint64_t, Doorbell>();
+  }
+  const uint64_t tail = region_addr + region_len - 1;
+  if (sp->db->count(tail)) return SRF_OK;
+  const uint64_t need = mirror ? region_len : 1;
+  if (sp->db_used + need > sp->db_cap) return fail(SRF_E_OUT_OF_MEMORY, "doorbell page full");
+  Doorbell d;
+  d.region_addr = region_addr;
+  d.region_len = region_len;
+  d.mirror = mirror != 0;
+  d.shadow_len = need;
+  d.host_off = sp->db_used;
+  d.clear_pending = false;
+  CUDA_TRY(cudaEventCreateWithFlags(&d.clear_ev, cudaEventDisableTiming));
+  // initial shadow = current device bytes
+  std::vector<uint8_t> cur(need);
+  CUDA_TRY(cudaMemcpy(cur.data(), sp->base + tail + 1 - need, need, cudaMemcpyDeviceToHost));
+  memcpy(sp->db_host + sp->db_used, cur.data(), need);
+  sp->db_used += need;
+  (*sp->db)[tail] = d;
+  return SRF_OK;
+}
+
+// Read `len` bytes ending at tail_addr + 1: from the doorbell shadow when one
+// is bound and every producer is in this process, else from the device.
+int srf_flag_read(srf_space_t sp, uint64_t tail_addr, uint64_t len, void *host_out) {
+  if (sp->db && !sp->exported) {
+    std::lock_guard<std::mutex> g(sp->mu);
+    auto it = sp->db->find(tail_addr);
+    if (it != sp->db->end()) {
+      const Doorbell &d = it->second;
+      if (len <= d.shadow_len) {
+        const volatile uint8_t *src = sp->db_host + d.host_off + (d.shadow_len - len);
+        // flag byte first (acquire), then the rest
+        uint8_t *o = (uint8_t *)host_out;
+        o[len - 1] = src[len - 1];
+        std::atomic_thread_fence(std::memory_order_acquire);
+        for (uint64_t i = 0; i + 1 < len; ++i) o[i] = src[i];
+        return SRF_OK;
+      }
+    }
+  }
+  return srf_read(sp, tail_addr + 1 - len, len, host_out);
+}
+
+// Clear a receive flag (StaticReceiver/DynReceiver.poll): shadow now, device
+// byte asynchronously on the space's stream; the next srf_put into the region
+// waits for that clear.
+int srf_flag_clear(srf_space_t sp, uint64_t tail_addr) {
+  int rc = check_raw(sp, tail_addr, 1, "flag");
+  if (rc) return rc;
+  if (sp->db) {
+    std::lock_guard<std::mutex> g(sp->mu);
+    auto it = sp->db->find(tail_addr);
+    if (it != sp->db->end()) {
+      Doorbell &d = it->second;
+      volatile uint8_t *flag = sp->db_host + d.host_off + d.shadow_len - 1;
+      *flag = 0;
+      CUDA_TRY(cudaSetDevice(sp->device));
+      CUDA_TRY(cudaMemsetAsync(sp->base + tail_addr, 0, 1, sp->stream->s));
+      CUDA_TRY(cudaEventRecord(d.clear_ev, sp->stream->s));
+      d.clear_pending = true;
+      return SRF_OK;
+    }
+  }
+  const uint8_t z = 0;
+  return srf_write(sp, tail_addr, 1, &z);
 }
 
 int srf_graph_begin(srf_stream_t st) {

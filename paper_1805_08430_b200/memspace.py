@@ -366,6 +366,31 @@ class MemorySpace:
     def device_ptr(self, addr: int) -> int:
         return self.device_base + addr
 
+    def write_async(self, handle: RegionHandle, offset: int, pinned, length: int) -> None:
+        """H2D from a pinned staging buffer, ordered on the space's stream (the
+        verbs this space issues next see the bytes; no host wait)."""
+        addr = self._handle_range(handle, offset, length)
+        _lib.call("srf_write_async", self._h, addr, length, pinned.ptr, None)
+
+    # -- receive flags (host doorbells, SURVEY H2) ------------------------------
+
+    def bind_doorbell(self, handle: RegionHandle, mirror: bool = False) -> None:
+        """Give a receive region a host-visible shadow that this process's
+        one-sided writes keep current (flag only, or the whole block)."""
+        if self.remote:
+            return
+        _lib.call("srf_doorbell_bind", self._h, handle.base_addr, handle.length, int(mirror))
+
+    def flag_read(self, tail_addr: int, length: int = 1) -> bytes:
+        """The ``length`` bytes ending at ``tail_addr`` (inclusive): from the
+        doorbell shadow when possible, else from the device."""
+        out = (C.c_uint8 * length)()
+        _lib.call("srf_flag_read", self._h, tail_addr, length, out)
+        return bytes(out)
+
+    def flag_clear(self, tail_addr: int) -> None:
+        _lib.call("srf_flag_clear", self._h, tail_addr)
+
     # -- counted copy (memspace.py:223-236): kernel K5 ---------------------------
 
     def copy_bytes(self, src: RegionHandle, src_off: int,

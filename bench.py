@@ -530,11 +530,35 @@ def sweep(max_bytes, device):
             row[f"{name}_us"] = round(t * 1e6, 3)
         row["verified"] = ring.verify()
         row.update(dynamic_rate(size, device))
+        row.update(rpc_device_rate(size, device))
         if size <= MIB:
             row.update(rpc_rate(size, device))
         out.append(row)
         size *= 4
     return out
+
+
+def rpc_device_rate(size, device, reps=None):
+    """RPC baseline with every byte on the GPU (RpcDeviceLink / srf_rpc_transfer):
+    4 KiB fragments through the 16-slot posted ring, two counted copies."""
+    from paper_1805_08430_b200.graph import Tensor
+    from paper_1805_08430_b200.memspace import ArenaAllocator, BufferRef, MemorySpace
+    from paper_1805_08430_b200.runtime.protocol import RpcDeviceLink
+    from paper_1805_08430_b200.wire import ElemType
+    cap = 3 * size + 8 * MIB
+    sp = {s: MemorySpace(s, cap, device=device) for s in (0, 1)}
+    ar = {s: ArenaAllocator(sp[s], sp[s].allocate_region(2 * size + 4 * MIB, True)) for s in (0, 1)}
+    link = RpcDeviceLink(1, sp[0], ar[0], sp[1], ar[1], ar[1])
+    t = Tensor((size // 4,), ElemType.F32, BufferRef(ar[0].alloc(size), ar[0]), 0)
+    reps = reps or (20 if size <= 4 * MIB else 3)
+    link.transfer(t).buffer.release()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        link.transfer(t).buffer.release()
+    dt = (time.perf_counter() - t0) / reps
+    for s_ in sp.values():
+        s_.close()
+    return {"rpc_gpu_gbps": round(size / dt / 1e9, 3), "rpc_gpu_us": round(dt * 1e6, 1)}
 
 
 def rpc_rate(size, device, reps=5):

@@ -255,6 +255,20 @@ int srf_batch_launch(srf_batch_t batch, srf_stream_t stream, uint64_t iteration,
                      int grid_cap);
 int srf_batch_destroy(srf_batch_t batch);
 
+/* RPC-style serialize/copy baseline (runtime/protocol.py:257-448) on the
+ * device - the comparator the north star reports zero-copy against.  The
+ * stream metadata||payload moves in 4096-B fragments (16-B header + 4080 B)
+ * through a 16-slot ring of posted 4-KiB receive slots in dst: a sender CTA
+ * serialises each fragment into its staging slot (counted copy 1) and writes
+ * it into a free ring slot; a receiver CTA checks the header, copies it out
+ * into meta_out / tensor_out (counted copy 2) and re-posts the slot.  Same
+ * GPU: one cooperative launch; two GPUs: one launch per side. */
+int srf_rpc_transfer(srf_space_t src, uint64_t meta_addr, uint32_t meta_len,
+                     uint64_t payload_addr, uint64_t payload_len, uint64_t stage_addr,
+                     srf_space_t dst, uint64_t ring_addr, uint64_t ring_flags_addr,
+                     uint64_t meta_out_addr, uint64_t tensor_out_addr, uint64_t msg_id,
+                     srf_stream_t src_stream, srf_stream_t dst_stream);
+
 /* ReduceMax consumer of the microbenchmark (graph.py:378-382) on the
  * receiving GPU: out_addr receives max over n fp32 at in_addr. */
 int srf_reduce_max_f32(srf_space_t space, uint64_t in_addr, uint64_t n,

@@ -111,6 +111,8 @@ SIGNATURES = {
     "srf_doorbell_bind": (C.c_int, [vp, u64, u64, C.c_int]),
     "srf_flag_read": (C.c_int, [vp, u64, u64, vp]),
     "srf_flag_clear": (C.c_int, [vp, u64]),
+    "srf_rpc_transfer": (C.c_int, [vp, u64, C.c_uint32, u64, u64, u64, vp, u64, u64, u64, u64,
+                                   u64, vp, vp]),
     "srf_reduce_max_f32": (C.c_int, [vp, u64, u64, u64, vp]),
 }
 

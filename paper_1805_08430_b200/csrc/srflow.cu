@@ -459,8 +459,32 @@ __device__ void copy_bytes_grid(uint8_t *dst, const uint8_t *src, uint64_t n,
                           (const uint32_t *)(src + head), nv, t, nth);
     nv *= 4;
   } else {
-    head = 0;
-    nv = 0;
+    // no common 4-B alignment (e.g. payload behind a 41-B metadata prefix):
+    // aligned 4-B destination words assembled from two aligned source words
+    // with a funnel shift, so loads and stores stay word-wide and coalesced
+    head = (4 - (d & 3)) & 3;
+    if (head > n) head = n;
+    const uint64_t words = (n - head) / 4;
+    // word j reads source words at floor((s+head)/4)+j and +1; the last one
+    // may extend up to 3 bytes past the range, so keep one word for the tail
+    nv = words > 0 ? words - 1 : 0;
+    const uint8_t *sp = src + head;
+    const uint32_t m = (uint32_t)((uintptr_t)sp & 3);
+    const uint32_t *sw = (const uint32_t *)((uintptr_t)sp - m);
+    uint32_t *dw = (uint32_t *)(dst + head);
+    uint64_t j = t;
+    for (; j + 3 * nth < nv; j += 4 * nth) {
+      uint32_t a[4], b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        a[u] = __ldg(sw + j + u * nth);
+        b[u] = __ldg(sw + j + u * nth + 1);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) dw[j + u * nth] = __funnelshift_r(a[u], b[u], 8 * m);
+    }
+    for (; j < nv; j += nth) dw[j] = __funnelshift_r(__ldg(sw + j), __ldg(sw + j + 1), 8 * m);
+    nv *= 4;
   }
   // scalar head and tail bytes
   for (uint64_t i = t; i < head; i += nth) dst[i] = src[i];
@@ -997,7 +1021,7 @@ __device__ __forceinline__ bool spin_until(const uint8_t *p, uint32_t want,
   uint64_t t0 = globaltimer_ns();
   while (ld_acquire_sys_u8(p) != want) {
     if (globaltimer_ns() - t0 > timeout_ns) return false;
-    __nanosleep(64);
+    __nanosleep(20);
   }
   return true;
 }
@@ -1156,6 +1180,116 @@ __global__ void __launch_bounds__(256) k_apply_batch(const BatchApply *descs, in
       release_tail((uint8_t *)d.src[threadIdx.x] + 8 * r + 32, 0, 1);
     if (s_last && threadIdx.x == 0) atomicExch(&counters[s_desc], 0u);
     __syncthreads();  // shared state is reused by the next unit
+  }
+}
+
+
+// ---------------------------------------------------------------------------
+// RPC-style baseline on the device (runtime/protocol.py:257-448, FORMATS.md
+// "RPC baseline fragment"): the stream metadata||payload is cut into 4096-B
+// fragments (16-B header msg_id u64, index u32, count u32 + 4080 B); the
+// sender serialises each fragment into a staging slot (counted copy 1) and
+// writes it into one of the receiver's 16 posted 4-KiB ring slots; the
+// receiver checks the header, copies the bytes out (counted copy 2) and
+// re-posts the slot.  Warp w owns ring slot w (fragments w, w+16, ...), so the
+// ring's 16-deep pipeline is kept and fragments land in order per slot.
+// ---------------------------------------------------------------------------
+static constexpr int kFrag = 4096, kFragHdr = 16, kFragPay = kFrag - kFragHdr, kRing = 16;
+
+struct RpcArgs {
+  const uint8_t *meta;  uint32_t meta_len;   // sender: metadata stage
+  const uint8_t *payload; uint64_t pay_len;  // sender: tensor bytes
+  uint8_t *stage;                            // sender: 16 x 4096 staging
+  uint8_t *ring;                             // receiver: 16 x 4096 posted slots
+  uint8_t *ring_flags;                       // receiver: 16 slot states (1 full)
+  uint8_t *meta_out;                         // receiver: reassembled metadata
+  uint8_t *tensor_out;                       // receiver: tensor buffer
+  uint64_t msg_id;
+  uint64_t timeout_ns;
+  int *err;
+  int role;                                  // -1: both (block 0 sender, 1 receiver)
+};
+
+// 64 threads (a warp pair) move one fragment
+static constexpr int kSlotThreads = 64;
+
+__device__ __forceinline__ void slot_copy(uint8_t *dst, const uint8_t *src, uint64_t n) {
+  copy_bytes_grid<4>(dst, src, n, threadIdx.x % kSlotThreads, kSlotThreads);
+}
+
+__device__ __forceinline__ void slot_sync() {
+  // the two warps of a slot: named barrier = slot index (0..15; the kernel
+  // never uses __syncthreads)
+  asm volatile("bar.sync %0, %1;" ::"r"((int)(threadIdx.x / kSlotThreads)),
+               "r"(kSlotThreads));
+}
+
+// bytes [off, off + n) of the message stream into dst
+__device__ __forceinline__ void stream_gather(const RpcArgs &a, uint8_t *dst, uint64_t off,
+                                              uint64_t n) {
+  if (off < a.meta_len) {
+    uint64_t k = a.meta_len - off < n ? a.meta_len - off : n;
+    slot_copy(dst, a.meta + off, k);
+    dst += k; off += k; n -= k;
+  }
+  if (n) slot_copy(dst, a.payload + (off - a.meta_len), n);
+}
+
+__device__ __forceinline__ void stream_scatter(const RpcArgs &a, const uint8_t *src,
+                                               uint64_t off, uint64_t n) {
+  if (off < a.meta_len) {
+    uint64_t k = a.meta_len - off < n ? a.meta_len - off : n;
+    slot_copy(a.meta_out + off, src, k);
+    src += k; off += k; n -= k;
+  }
+  if (n) slot_copy(a.tensor_out + (off - a.meta_len), src, n);
+}
+
+__global__ void __launch_bounds__(1024) k_rpc(RpcArgs a) {
+  const int role = a.role >= 0 ? a.role : (int)blockIdx.x;
+  const int w = threadIdx.x / kSlotThreads;            // ring slot of this warp pair
+  const bool leader = (threadIdx.x % kSlotThreads) == 0;
+  const uint64_t total = a.meta_len + a.pay_len;
+  const uint32_t count = (uint32_t)((total + kFragPay - 1) / kFragPay);
+  uint8_t *slot = a.ring + (uint64_t)w * kFrag;
+  uint8_t *flag = a.ring_flags + w;
+  uint8_t *st = a.stage + (uint64_t)w * kFrag;
+  for (uint32_t f = w; f < count; f += kRing) {
+    const uint64_t off = (uint64_t)f * kFragPay;
+    const uint64_t n = total - off < (uint64_t)kFragPay ? total - off : (uint64_t)kFragPay;
+    if (role == 0) {
+      // sender: serialise into the staging slot (counted copy 1) - this
+      // overlaps the receiver draining the previous fragment of the slot -
+      // then wait for the posted ring slot and send
+      if (leader) {
+        *(uint64_t *)st = a.msg_id;
+        *(uint32_t *)(st + 8) = f;
+        *(uint32_t *)(st + 12) = count;
+      }
+      stream_gather(a, st + kFragHdr, off, n);
+      if (leader && !spin_until(flag, 0, a.timeout_ns)) atomicExch(a.err, 7);
+      slot_sync();
+      slot_copy(slot, st, kFragHdr + n);  // the send verb
+      slot_sync();
+      if (leader) {
+        __threadfence_system();
+        st_release_sys_u8(flag, 1);
+      }
+    } else {
+      // receiver: drain the slot in order, copy out (counted copy 2), re-post
+      if (leader && !spin_until(flag, 1, a.timeout_ns)) atomicExch(a.err, 7);
+      slot_sync();
+      if (leader && (*(volatile uint64_t *)slot != a.msg_id ||
+                     *(volatile uint32_t *)(slot + 8) != f))
+        atomicExch(a.err, 8);  // ReassemblyGap
+      stream_scatter(a, slot + kFragHdr, off, n);
+      slot_sync();
+      if (leader) {
+        __threadfence_system();
+        st_release_sys_u8(flag, 0);
+      }
+    }
+    slot_sync();
   }
 }
 
@@ -1556,6 +1690,9 @@ int srf_space_sync(srf_space_t sp) {
   CUDA_TRY(cudaMemcpy(&err, sp->err, sizeof(int), cudaMemcpyDeviceToHost));
   if (err) {
     cudaMemset(sp->err, 0, sizeof(int));
+    if (err == 8)
+      return fail(SRF_E_PROTOCOL, "server %d: RPC fragment out of order (ReassemblyGap)",
+                  sp->server_id);
     if (err == 6)
       return fail(SRF_E_BAD_TOKEN,
                   "server %d: device-side metadata validation failed (token/bounds/length)",
@@ -2245,6 +2382,57 @@ int srf_flag_clear(srf_space_t sp, uint64_t tail_addr) {
   }
   const uint8_t z = 0;
   return srf_write(sp, tail_addr, 1, &z);
+}
+
+int srf_rpc_transfer(srf_space_t src, uint64_t meta_addr, uint32_t meta_len,
+                     uint64_t payload_addr, uint64_t payload_len, uint64_t stage_addr,
+                     srf_space_t dst, uint64_t ring_addr, uint64_t ring_flags_addr,
+                     uint64_t meta_out_addr, uint64_t tensor_out_addr, uint64_t msg_id,
+                     srf_stream_t st_src, srf_stream_t st_dst) {
+  int rc = check_raw(src, meta_addr, meta_len, "rpc meta");
+  if (!rc) rc = check_raw(src, payload_addr, payload_len, "rpc payload");
+  if (!rc) rc = check_raw(src, stage_addr, (uint64_t)kRing * kFrag, "rpc stage");
+  if (!rc) rc = check_raw(dst, ring_addr, (uint64_t)kRing * kFrag, "rpc ring");
+  if (!rc) rc = check_raw(dst, ring_flags_addr, kRing, "rpc ring flags");
+  if (!rc) rc = check_raw(dst, meta_out_addr, meta_len, "rpc meta out");
+  if (!rc) rc = check_raw(dst, tensor_out_addr, payload_len, "rpc tensor out");
+  if (rc) return rc;
+  RpcArgs a;
+  a.meta = src->base + meta_addr;
+  a.meta_len = meta_len;
+  a.payload = src->base + payload_addr;
+  a.pay_len = payload_len;
+  a.stage = src->base + stage_addr;
+  a.ring = dst->base + ring_addr;
+  a.ring_flags = dst->base + ring_flags_addr;
+  a.meta_out = dst->base + meta_out_addr;
+  a.tensor_out = dst->base + tensor_out_addr;
+  a.msg_id = msg_id;
+  a.timeout_ns = 10ull * 1000 * 1000 * 1000;
+  a.err = src->err;
+  srf_stream *ss = stream_or_default(src, st_src);
+  srf_stream *ds = stream_or_default(dst, st_dst);
+  if (ss->device == ds->device) {
+    // both roles in one cooperative launch: the two CTAs are co-resident
+    a.role = -1;
+    CUDA_TRY(cudaSetDevice(ss->device));
+    void *params[] = {&a};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_rpc, dim3(2), dim3(1024), params, 0,
+                                         ss->s));
+    return launch_check("k_rpc");
+  }
+  // two GPUs: receiver first (it waits for the sender over NVLink)
+  a.role = 1;
+  a.err = dst->err;
+  CUDA_TRY(cudaSetDevice(ds->device));
+  k_rpc<<<1, 1024, 0, ds->s>>>(a);
+  rc = launch_check("k_rpc(recv)");
+  if (rc) return rc;
+  a.role = 0;
+  a.err = src->err;
+  CUDA_TRY(cudaSetDevice(ss->device));
+  k_rpc<<<1, 1024, 0, ss->s>>>(a);
+  return launch_check("k_rpc(send)");
 }
 
 int srf_graph_begin(srf_stream_t st) {

@@ -243,3 +243,32 @@ class TestRpcBaseline:
         copied = (rig.spaces[0].counters.payload_bytes_copied +
                   rig.spaces[1].counters.payload_bytes_copied)
         assert copied == 2 * nbytes + meta_block_size(1)
+
+
+class TestRpcDevice:
+    @pytest.mark.parametrize("dims", [(0, 7), (1,), (1020,), (2560, 1), (40 * 1020,), (1 << 20,)])
+    def test_fragment_ring_on_device(self, dims):
+        from paper_1805_08430_b200.runtime.protocol import RpcDeviceLink
+        rig = Rig(capacity=1 << 24)
+        link = RpcDeviceLink(len(dims), rig.spaces[0], rig.arenas[0], rig.spaces[1],
+                             rig.arenas[1], rig.arenas[1])
+        t = rig.tensor(dims)
+        got = link.transfer(t)
+        n = t.nbytes
+        if n:
+            assert rig.spaces[1].read_at(got.buffer.handle, 0, n) == \
+                rig.spaces[0].read_at(t.buffer.handle, 0, n)
+        meta = rig.spaces[1].read_at(link.meta_out, 0, meta_block_size(len(dims)))
+        from paper_1805_08430_b200.wire import encode_meta
+        assert meta == encode_meta(dims, ElemType.F32, 0, 0)
+        copied = (rig.spaces[0].counters.payload_bytes_copied +
+                  rig.spaces[1].counters.payload_bytes_copied)
+        assert copied == 2 * n + meta_block_size(len(dims))
+        # every ring slot re-posted
+        assert rig.spaces[1].read_at(link.ring_flags, 0, 16) == bytes(16)
+        # a second message through the same ring
+        got.buffer.release()
+        got2 = link.transfer(t)
+        if n:
+            assert rig.spaces[1].read_at(got2.buffer.handle, 0, n) == \
+                rig.spaces[0].read_at(t.buffer.handle, 0, n)

@@ -115,8 +115,8 @@ static constexpr int kScratchBlocks = 1024;
 
 // launch-geometry knobs (srf_tune): CTAs per SM and threads per CTA of the
 // copy kernels; defaults chosen from the NVLink/HBM probes (profiles/).
-static int g_ctas_per_sm = 8;
-static int g_copy_threads = 512;
+static int g_ctas_per_sm = 2;
+static int g_copy_threads = 256;
 
 static int sm_count_of(int device) {
   static int cache[64] = {0};
@@ -393,9 +393,34 @@ __device__ __forceinline__ void st_v4(uint4 *p, const uint4 &v) {
                : "memory");
 }
 
+// 32-B vectors: sm_100 has 256-bit global loads/stores (LDG/STG.E.ENL2.256)
+struct __align__(32) u256 {
+  uint32_t v[8];
+};
+
+__device__ __forceinline__ u256 ld_v8(const u256 *p) {
+  u256 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]),
+                 "=r"(r.v[5]), "=r"(r.v[6]), "=r"(r.v[7])
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_v8(u256 *p, const u256 &r) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(r.v[0]),
+               "r"(r.v[1]), "r"(r.v[2]), "r"(r.v[3]), "r"(r.v[4]), "r"(r.v[5]), "r"(r.v[6]),
+               "r"(r.v[7])
+               : "memory");
+}
+
 template <typename V>
 __device__ __forceinline__ V ld_stream(const V *p) {
   return __ldg(p);
+}
+template <>
+__device__ __forceinline__ u256 ld_stream<u256>(const u256 *p) {
+  return ld_v8(p);
 }
 template <>
 __device__ __forceinline__ uint4 ld_stream<uint4>(const uint4 *p) {
@@ -408,6 +433,10 @@ __device__ __forceinline__ void st_plain(V *p, const V &v) {
 template <>
 __device__ __forceinline__ void st_plain<uint4>(uint4 *p, const uint4 &v) {
   st_v4(p, v);
+}
+template <>
+__device__ __forceinline__ void st_plain<u256>(u256 *p, const u256 &v) {
+  st_v8(p, v);
 }
 
 // Grid-wide copy of nv vectors: all loads of an unrolled batch are issued
@@ -431,13 +460,22 @@ __device__ __forceinline__ void vec_copy(V *__restrict__ dst,
 
 // Copy n bytes with the widest vector both pointers allow.  Arena blocks are
 // 8-byte aligned (memspace.py:31), so the 16-B path needs equal (p mod 16).
+__constant__ int g_vec32 = 1;  // knob 5: 32-B vectors when co-aligned mod 32
+
 template <int U16 = 4>
 __device__ void copy_bytes_grid(uint8_t *dst, const uint8_t *src, uint64_t n,
                                 uint64_t t, uint64_t nth) {
   if (n == 0) return;
   uintptr_t d = (uintptr_t)dst, s = (uintptr_t)src;
   uint64_t head, nv;
-  if (((d ^ s) & 15) == 0) {
+  if (g_vec32 && ((d ^ s) & 31) == 0 && n >= 4096) {
+    head = (32 - (d & 31)) & 31;
+    if (head > n) head = n;
+    nv = (n - head) / 32;
+    vec_copy<u256, (U16 > 4 ? U16 / 2 : 2)>((u256 *)(dst + head), (const u256 *)(src + head),
+                                            nv, t, nth);
+    nv *= 32;
+  } else if (((d ^ s) & 15) == 0) {
     head = (16 - (d & 15)) & 15;
     if (head > n) head = n;
     nv = (n - head) / 16;
@@ -1456,6 +1494,19 @@ int srf_tune(int knob, int value) {
       if (value != 4 && value != 8) return fail(SRF_E_INVALID_CONFIG, "unroll 4|8");
       g_unroll = value;
       return SRF_OK;
+    case 5: {
+      if (value != 0 && value != 1) return fail(SRF_E_INVALID_CONFIG, "vec32 0|1");
+      int ndev = 0;
+      cudaGetDeviceCount(&ndev);
+      int cur = 0;
+      cudaGetDevice(&cur);
+      for (int dev = 0; dev < ndev; ++dev) {
+        CUDA_TRY(cudaSetDevice(dev));
+        CUDA_TRY(cudaMemcpyToSymbol(g_vec32, &value, sizeof value));
+      }
+      cudaSetDevice(cur);
+      return SRF_OK;
+    }
     default:
       return fail(SRF_E_INVALID_CONFIG, "unknown knob %d", knob);
   }
@@ -2105,7 +2156,7 @@ struct srf_batch {
 static uint32_t ctas_for(int device, uint64_t bytes, uint64_t per_cta) {
   // enough CTAs that each moves ~per_cta bytes, at most g_ctas_per_sm per SM
   uint64_t want = (bytes + per_cta - 1) / per_cta;
-  uint64_t cap = (uint64_t)sm_count_of(device) * g_ctas_per_sm;
+  uint64_t cap = (uint64_t)sm_count_of(device) * 8;  // batch phases: up to 8 units/SM
   return (uint32_t)std::max<uint64_t>(1, std::min(want, cap));
 }
 

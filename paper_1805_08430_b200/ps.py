@@ -48,14 +48,15 @@ _NONE = (1 << 64) - 1
 
 
 def _r16(n: int) -> int:
-    return (n + 15) & ~15
+    """Block size rounded to 32 B: blocks stay co-aligned for 32-B vectors."""
+    return (n + 31) & ~31
 
 
 @dataclass
 class PsLayout:
     """Deterministic per-server memory layout (pure host logic).
 
-    Every block is a 16-B aligned slice of the server's one registered arena,
+    Every block is a 32-B aligned slice of the server's one registered arena,
     allocated in a fixed order, so every rank can derive every peer's
     coordinates; the exchanged region tables (tokens) validate them.
     """

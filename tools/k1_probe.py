@@ -13,9 +13,10 @@ S = int(os.environ.get("PROBE_BYTES", 256 << 20))
 ring = bench.SendRecvRing(S, 0, 1, 0)
 R = 30
 peak, _ = bench.measured_peaks()
-for unroll in (4, 8):
-    for ctas in (1, 2, 4, 8):
+for unroll, vec32 in ((8, 0), (8, 1), (4, 1)):
+    for ctas in (2, 4, 8):
         for threads in (256, 512):
+            _lib.tune("vec32", vec32)
             _lib.tune("unroll", unroll)
             _lib.tune("ctas_per_sm", ctas)
             _lib.tune("copy_threads", threads)
@@ -31,7 +32,7 @@ for unroll in (4, 8):
             ring.sync()
             put_ms = statistics.fmean(ring.elapsed_ms(ev[2 * i], ev[2 * i + 1]) for i in range(R))
             round_ms = ring.elapsed_ms(a, b) / R
-            print(json.dumps({"unroll": unroll, "ctas": ctas, "threads": threads,
+            print(json.dumps({"unroll": unroll, "vec32": vec32, "ctas": ctas, "threads": threads,
                               "k1_us": round(put_ms * 1e3, 2),
                               "k1_hbm_frac": round((2 * S + 1) / (put_ms / 1e3) / 1e9 / peak, 4),
                               "round_us": round(round_ms * 1e3, 2),

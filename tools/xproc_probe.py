@@ -44,13 +44,13 @@ def put():
               ring.dst.handle, ring.dst_region[0], ring.dst_region[1], 0, ring.stream, None)
 
 
-for ctas in (2,):
-    for threads in (512,):
-        _lib.tune("ctas_per_sm", ctas)
-        _lib.tune("copy_threads", threads)
-        t_uni = timed(put, active=(rank == 0))
-        t_bi = bench.dist_max(timed(put))
-        if rank == 0:
-            rec = {"ctas": ctas, "threads": threads, "uni_gbps": S / t_uni / 1e6,
-                   "bi_gbps": S / t_bi / 1e6}
-            print(json.dumps(rec), flush=True)
+for ctas, threads, vec32 in ((8, 512, 0), (8, 512, 1), (2, 512, 1), (4, 256, 1)):
+    _lib.tune("ctas_per_sm", ctas)
+    _lib.tune("copy_threads", threads)
+    _lib.tune("vec32", vec32)
+    t_uni = timed(put, active=(rank == 0))
+    t_bi = bench.dist_max(timed(put))
+    if rank == 0:
+        rec = {"ctas": ctas, "threads": threads, "vec32": vec32, "uni_gbps": S / t_uni / 1e6,
+               "bi_gbps": S / t_bi / 1e6}
+        print(json.dumps(rec), flush=True)

@@ -970,8 +970,8 @@ __device__ void apply_range(uint8_t *var, const uint8_t *const *g, int nw, uint6
     head = ((16 - (m & 15)) & 15);
     if (head > n) head = n;
     const uint64_t nv = (n - head) / 16;
-    if (SGD) fold_v4<SgdOp, 8>(var, g, nw, head, nv, t, nth, lr);
-    else fold_v4<XorOp, 8>(var, g, nw, head, nv, t, nth, lr);
+    if (SGD) fold_v4<SgdOp, 4>(var, g, nw, head, nv, t, nth, lr);
+    else fold_v4<XorOp, 4>(var, g, nw, head, nv, t, nth, lr);
     body = nv * 16;
   } else if (same8) {
     head = ((8 - (m & 7)) & 7);
@@ -2154,7 +2154,8 @@ struct srf_batch {
 };
 
 static uint32_t ctas_for(int device, uint64_t bytes, uint64_t per_cta) {
-  // enough CTAs that each moves ~per_cta bytes, at most g_ctas_per_sm per SM
+  // work units of ~per_cta bytes each (large enough to amortise the per-unit
+  // flag acquire / metadata decode), at most 8 units per SM per descriptor
   uint64_t want = (bytes + per_cta - 1) / per_cta;
   uint64_t cap = (uint64_t)sm_count_of(device) * 8;  // batch phases: up to 8 units/SM
   return (uint32_t)std::max<uint64_t>(1, std::min(want, cap));
@@ -2221,7 +2222,7 @@ int srf_batch_put_create(int n, srf_space_t const *src_space, const uint64_t *sr
     d.body = body_len[i];
     d.tail = ss->base + tail_addr[i];
     d.cta_begin = next;
-    d.cta_count = ctas_for(device, body_len[i], 512 * 16 * 8);
+    d.cta_count = ctas_for(device, body_len[i], 128 << 10);
     d.wait_empty = (flags & SRF_PUT_WAIT_EMPTY) ? 1 : 0;
     d.pad = 0;
     next += d.cta_count;
@@ -2255,7 +2256,7 @@ int srf_batch_gen_create(int n, srf_space_t const *space, const uint64_t *grad_a
                    ? nullptr : credit_space[i]->base + credit_addr[i];
     d.node = node_id[i];
     d.cta_begin = next;
-    d.cta_count = ctas_for(device, nbytes[i], 512 * 16 * 4);
+    d.cta_count = ctas_for(device, nbytes[i], 128 << 10);
     next += d.cta_count;
   }
   int rc = finish_batch(1, device, host, space[0]->err, out);
@@ -2307,7 +2308,7 @@ int srf_batch_apply_create(srf_space_t sp, int nvars, const uint64_t *var_addr,
       d.src[w] = ss->base + src_addr[k];
     }
     d.cta_begin = next;
-    d.cta_count = ctas_for(sp->device, nbytes[v], 256 * 16 * 4);
+    d.cta_count = ctas_for(sp->device, nbytes[v] * (uint64_t)(d.nw + 2), 512 << 10);
     next += d.cta_count;
   }
   int rc = finish_batch(2, sp->device, host, sp->err, out);

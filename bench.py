@@ -13,7 +13,7 @@ kernel K2 acquires the flag and clears it.
   path.
 * ``value``: payload GB/s of the whole job, inputs resident in HBM, device
   time (CUDA events on the launching stream), max over ranks.  One step = one
-  batch of R transfers of the tensor (R calibrated so a step takes ~15 ms).
+  batch of R transfers of the tensor (R calibrated so a step takes ~25 ms).
 * ``e2e``: same metric through the public API (StaticSender.send ->
   StaticReceiver.poll -> ReduceMax consumer) with the payload copied from
   pinned host memory every step and the consumer's result read back.
@@ -278,7 +278,8 @@ def bench_sendrecv_device(S, steps, warmup, rank, world, device):
     ring.record(b)
     ring.sync()
     t_round = ring.elapsed_ms(a, b) / 4
-    rounds = int(dist_max(float(max(1, min(4096, round(15.0 / max(t_round, 1e-3)))))))
+    # one step ~25 ms so the timed region spans several clock samples
+    rounds = int(dist_max(float(max(1, min(4096, round(25.0 / max(t_round, 1e-3)))))))
     for _ in range(warmup * rounds):
         ring.put()
         ring.consume()

@@ -737,7 +737,9 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(ach / peak, 4), "bytes_per_step": alg}
     else:
-        per_gpu = {g: max(x["link_out"], x["link_in"]) for g, x in gpus.items()}
+        from paper_1805_08430_b200.ps import link_traffic
+        per_gpu = {g: max(x["link_out"], x["link_in"])
+                   for g, x in link_traffic(L, world).items()}
         hot = max(per_gpu, key=per_gpu.get)
         ach = per_gpu[hot] * steps / t / 1e9
         roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_MEASURED_GBS,
@@ -867,12 +869,23 @@ def main() -> int:
     if not args.no_ps:
         line["ps"] = bench_ps(rank, world, local, max(10, args.steps), args.warmup,
                               op=args.ps_op, cpu=not args.no_cpu)
+        if world > 1:
+            # labelled extension: byte-balanced shards instead of v % G
+            from paper_1805_08430_b200.ps import PsLayout
+            from paper_1805_08430_b200.workloads import vgg16_shapes
+            Lb = PsLayout(vgg16_shapes(), world, world, colocate=True, placement="bytes")
+            line["ps_balanced"] = bench_ps(
+                rank, world, local, max(10, args.steps), args.warmup, op=args.ps_op,
+                cpu=False, layout=Lb,
+                label=f"EXTENSION: VGG-16 with byte-balanced shards (largest-first), "
+                      f"{world} workers + {world} shards co-located")
         line["ps_configs"] = bench_ps_configs(rank, world, local, max(20, args.steps),
                                               args.warmup, args.ps_op, not args.no_cpu)
     if rank == 0:
         print(json.dumps(line), flush=True)
     ps_ok = line.get("ps", {}).get("verified", True) and all(
-        c["verified"] for c in line.get("ps_configs", {}).values())
+        c["verified"] for c in line.get("ps_configs", {}).values()) and \
+        line.get("ps_balanced", {}).get("verified", True)
     if not dev["verified"] or not e2e["verified"] or not ps_ok:
         log("verification FAILED")
         return 1

@@ -66,6 +66,9 @@ class PsLayout:
     shards: int
     colocate: bool = False
     elem: ElemType = ElemType.F32
+    #: "round_robin" = the reference placement v % shards (workloads.py:84);
+    #: "bytes" = extension: largest variable first onto the least-loaded shard
+    placement: str = "round_robin"
     blocks: dict[int, dict] = field(default_factory=dict)
     sizes: dict[int, int] = field(default_factory=dict)
 
@@ -75,6 +78,17 @@ class PsLayout:
             raise errors.InvalidConfig("colocate needs shards <= workers")
         if self.workers > _lib.MAX_WORKERS:
             raise errors.InvalidConfig(f"at most {_lib.MAX_WORKERS} workers")
+        if self.placement == "round_robin":
+            self._shard = [v % self.shards for v in range(len(self.shapes))]
+        elif self.placement == "bytes":
+            load = [0] * self.shards
+            self._shard = [0] * len(self.shapes)
+            for v in sorted(range(len(self.shapes)), key=lambda v: (-self.nbytes(v), v)):
+                k = min(range(self.shards), key=lambda k: (load[k], k))
+                self._shard[v] = k
+                load[k] += self.nbytes(v)
+        else:
+            raise errors.InvalidConfig(f"unknown placement {self.placement!r}")
         for s in range(self.nservers):
             self._lay_out(s)
 
@@ -86,7 +100,7 @@ class PsLayout:
         return math.prod(self.shapes[v]) * self.elem.size
 
     def shard_of(self, v: int) -> int:
-        return (v % self.shards) + (0 if self.colocate else self.workers)
+        return self._shard[v] + (0 if self.colocate else self.workers)
 
     def is_worker(self, s: int) -> bool:
         return s < self.workers
@@ -146,6 +160,25 @@ class PsLayout:
                     out["link_out"] += meta + S   # meta written, gradient read by the shard
                     out["link_in"] += S + 1       # weight pushed in
         return out
+
+
+def link_traffic(L: "PsLayout", world: int) -> dict[int, dict]:
+    """NVLink bytes per iteration per GPU (server s on GPU s % world); traffic
+    between servers on the same GPU stays in HBM and is not counted."""
+    out = {g: {"link_out": 0, "link_in": 0} for g in range(world)}
+    for v in range(len(L.shapes)):
+        S = L.nbytes(v)
+        meta = meta_block_size(len(L.shapes[v]))
+        s = L.shard_of(v)
+        for w in range(L.workers):
+            if w == s or w % world == s % world:
+                continue
+            gs, gw = s % world, w % world
+            out[gs]["link_out"] += S + 1          # weight push
+            out[gw]["link_in"] += S + 1
+            out[gw]["link_out"] += meta + S       # metadata write + gradient read
+            out[gs]["link_in"] += meta + S
+    return out
 
 
 class PsStep:

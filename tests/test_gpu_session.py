@@ -196,3 +196,32 @@ def test_mode_validation():
     g, p = build_microbench(4096)
     with pytest.raises(errors.InvalidConfig):
         Session(g, p, mode="bogus")
+
+
+@pytest.mark.parametrize("mode", ["zerocp", "rpc"])
+def test_threaded_sessions_match_round_robin_counters(mode):
+    """One OS thread per server (reference session.py:631-649): interleavings
+    differ, byte volumes / counters / simulated time agree; host doorbells are
+    polled concurrently from several threads."""
+    def rows(threads):
+        g, p = build_ps_workload(24_000, 2, 0.0, 2)
+        s = Session(g, p, mode=mode, seed=33, threads=threads)
+        rep = s.run(3)
+        s.close()
+        return [(r.iteration, r.bytes_sent, r.payload_bytes, r.payload_bytes_copied,
+                 r.copy_events, r.serialize_bytes, round(r.sim_time_us, 6)) for r in rep.rows]
+    assert rows(False) == rows(True)
+
+
+def test_doorbell_falls_back_to_device_reads_once_exported():
+    from paper_1805_08430_b200.memspace import MemorySpace
+    sp = MemorySpace(0, 1 << 20, device=0)
+    r = sp.allocate_region(4096, register=True)
+    sp.bind_doorbell(r)
+    tail = r.base_addr + r.length - 1
+    sp.write_raw(tail, b"\x01")            # a write the shadow never saw
+    assert sp.flag_read(tail, 1) == b"\x00"   # in-process: the shadow is authoritative
+    sp.export()                             # producers may now be other processes
+    assert sp.flag_read(tail, 1) == b"\x01"   # device read
+    sp.flag_clear(tail)
+    assert sp.read_raw(tail, 1) == b"\x00"

@@ -248,3 +248,24 @@ def test_ps_layout_blocks_and_traffic():
     L1 = PsLayout(shapes, 1, 1)
     assert L1.nservers == 2 and L1.shard_of(5) == 1
     assert L1.traffic(1)["push_out"] == sum(L1.nbytes(v) + 1 for v in range(32))
+
+
+def test_ps_byte_balanced_placement_extension():
+    from paper_1805_08430_b200.ps import PsLayout
+    shapes = vgg16_shapes()
+    rr = PsLayout(shapes, 8, 8, colocate=True)
+    bb = PsLayout(shapes, 8, 8, colocate=True, placement="bytes")
+    load = lambda L: [sum(L.nbytes(v) for v in range(32) if L.shard_of(v) == k) for k in range(8)]
+    assert max(load(bb)) < max(load(rr))  # fc6 still alone, but nothing piles onto it
+    assert sorted(bb.shard_of(v) for v in range(32)) != [v % 8 for v in range(32)]
+    assert max(load(bb)) == bb.nbytes(26)  # the 411 MB fc6 shard holds only fc6
+
+
+def test_ps_link_traffic_excludes_same_gpu_servers():
+    from paper_1805_08430_b200.ps import PsLayout, link_traffic
+    L = PsLayout([(1000,)] * 10, 2, 1)          # workers 0,1 + PS server 2
+    t = link_traffic(L, 2)                      # servers 0,2 on GPU 0; server 1 on GPU 1
+    S = 4000
+    assert t[0]["link_out"] == 10 * (S + 1)     # pushes to worker 1 only
+    assert t[1]["link_out"] == 10 * (41 + S)    # worker 1's metadata + gradient reads
+    assert link_traffic(L, 1)[0] == {"link_out": 0, "link_in": 0}

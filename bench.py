@@ -697,16 +697,32 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
     clocks = ClockSampler(device)
     clocks.start()
     barrier_sync()
+    graph = None
+    if not ps.overlap and os.environ.get("SRFLOW_PS_GRAPH") == "1":
+        # optional: replay the timed iterations as one CUDA graph (the gen batch
+        # takes the iteration from a device counter).  Measured slower than
+        # eager launches on B200 (MLP 23.8k vs 29.6k it/s), so off by default.
+        ps.set_iteration(it + 1)
+        graph = ps.capture(steps)
+        barrier_sync()
     l0 = _lib.launch_count()
     _lib.call("srf_event_record_on", ev[0], ps.stream)
-    ps.fork()
-    for _ in range(steps):
-        it += 1
-        ps.step(it)
-    ps.join()
+    if graph is not None:
+        ps.replay(graph)
+        it += steps
+        launched = steps * (ps.launches_per_step() + 1)
+    else:
+        ps.fork()
+        for _ in range(steps):
+            it += 1
+            ps.step(it)
+        ps.join()
+        launched = 0
     _lib.call("srf_event_record_on", ev[1], ps.stream)
     ps.sync()
-    launches = int(dist_sum(_lib.launch_count() - l0))
+    launches = int(dist_sum(_lib.launch_count() - l0 + launched))
+    if graph is not None:
+        _lib.call("srf_graph_destroy", graph)
     barrier_sync()
     clk = clocks.stop()
     ms = C.c_float()
@@ -752,7 +768,8 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
            "steps": steps, "model_bytes": model, "roofline": roof, "gpu_launches": launches,
            "clocks": clk, "verified": ok,
            "phases": "K1 weight push batch, GenGrad batch, K3 meta batch, K4+K6 fused apply",
-           "schedule": "overlapped (3 streams, capped grids)" if ps.overlap else "one stream"}
+           "schedule": ("overlapped (3 streams, capped grids)" if ps.overlap else
+                        "one stream, CUDA graph" if graph is not None else "one stream")}
     ps.close()
     if cpu and rank == 0 and world == 1:
         rig = cpu_rig() if cpu_rig else port.PsRig(shapes, L.workers, L.shards, L.colocate,

@@ -254,6 +254,11 @@ int srf_batch_apply_create(srf_space_t space, int nvars, const uint64_t *var_add
 int srf_batch_launch(srf_batch_t batch, srf_stream_t stream, uint64_t iteration, int mode,
                      int grid_cap);
 int srf_batch_destroy(srf_batch_t batch);
+/* graph-replayed PS steps: a gen batch launched with iteration == UINT64_MAX
+ * reads the iteration from the u64 at addr of space; srf_counter_add bumps it
+ * (one thread, stream-ordered) at the end of each captured step */
+int srf_batch_set_iteration_source(srf_batch_t batch, srf_space_t space, uint64_t addr);
+int srf_counter_add(srf_space_t space, uint64_t addr, uint64_t delta, srf_stream_t stream);
 
 /* RPC-style serialize/copy baseline (runtime/protocol.py:257-448) on the
  * device - the comparator the north star reports zero-copy against.  The

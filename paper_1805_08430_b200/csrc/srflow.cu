@@ -1116,8 +1116,12 @@ __device__ __forceinline__ float unit_f32(uint32_t k0, uint32_t k1, uint32_t i) 
 __global__ void __launch_bounds__(512) k_gen_batch(const BatchGen *descs, int n,
                                                    uint32_t total_units, unsigned int *counters,
                                                    uint64_t seed,
-                                                   uint64_t iteration, int regen,
+                                                   uint64_t iteration_arg,
+                                                   const uint64_t *iteration_ptr, int regen,
                                                    uint64_t timeout_ns, int *err) {
+  // iteration from a device counter when given (graph-replayed steps)
+  const uint64_t iteration = iteration_ptr ? *(const volatile uint64_t *)iteration_ptr
+                                           : iteration_arg;
   __shared__ int s_desc, s_last;
   for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x) {
     if (threadIdx.x == 0) s_desc = find_desc(descs, n, u);
@@ -2143,6 +2147,7 @@ int srf_reduce_max_f32(srf_space_t sp, uint64_t in_addr, uint64_t n,
 struct srf_batch {
   int kind;  // 0 put, 1 gen, 2 apply
   int device;
+  const uint64_t *iter_ptr = nullptr;  // gen: device iteration counter (graphs)
   void *descs;
   int n;
   unsigned int *counters;
@@ -2332,14 +2337,37 @@ int srf_batch_launch(srf_batch_t b, srf_stream_t st, uint64_t iteration, int mod
       return launch_check("k_put_batch");
     case 1:
       k_gen_batch<<<grid, 512, 0, st->s>>>((const BatchGen *)b->descs, b->n, units,
-                                           b->counters, b->seed, iteration, mode, timeout,
-                                           b->err);
+                                           b->counters, b->seed, iteration,
+                                           iteration == UINT64_MAX ? b->iter_ptr : nullptr,
+                                           mode, timeout, b->err);
       return launch_check("k_gen_batch");
     default:
       k_apply_batch<<<grid, 256, 0, st->s>>>((const BatchApply *)b->descs, b->n, units,
                                              b->counters, b->op, b->lr, timeout, b->err);
       return launch_check("k_apply_batch");
   }
+}
+
+// Device iteration counter for graph-captured PS steps: a gen batch launched
+// with iteration == UINT64_MAX reads *counter; srf_counter_add bumps it in
+// stream order at the end of a step.
+__global__ void k_counter_add(uint64_t *p, uint64_t delta) { *p += delta; }
+
+int srf_batch_set_iteration_source(srf_batch_t b, srf_space_t sp, uint64_t addr) {
+  int rc = check_raw(sp, addr, 8, "iteration counter");
+  if (rc) return rc;
+  if (addr % 8) return fail(SRF_E_INVALID_CONFIG, "counter must be 8-B aligned");
+  b->iter_ptr = (const uint64_t *)(sp->base + addr);
+  return SRF_OK;
+}
+
+int srf_counter_add(srf_space_t sp, uint64_t addr, uint64_t delta, srf_stream_t st) {
+  int rc = check_raw(sp, addr, 8, "counter");
+  if (rc) return rc;
+  srf_stream *s = stream_or_default(sp, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  k_counter_add<<<1, 1, 0, s->s>>>((uint64_t *)(sp->base + addr), delta);
+  return launch_check("k_counter_add");
 }
 
 int srf_batch_destroy(srf_batch_t b) {

@@ -230,7 +230,12 @@ class PsStep:
                              MemorySpace(-1 - rank, 1 << 20, seed=seed, device=device))
         self.stream = C.c_void_p()
         _lib.call("srf_stream_create", self.stream_space.handle, C.byref(self.stream))
+        # device iteration counter for graph-replayed steps
+        self._counter = self.stream_space.allocate_region(64)
         self.batches = self._build_batches()
+        for g in self.batches["gen"].values():
+            _lib.call("srf_batch_set_iteration_source", g, self.stream_space.handle,
+                      self._counter.base_addr)
         # Overlapped schedule: weight pushes, worker phase and shard apply on
         # three streams, ordered locally by events and across GPUs by the
         # device flags.  Only when this rank hosts exactly one server (worker k
@@ -456,6 +461,43 @@ class PsStep:
         _lib.call("srf_event_record_on", ev["apply"], sc)
         self._applied = True
         return n
+
+    def launches_per_step(self) -> int:
+        b = self.batches
+        return ((b["push"] is not None) + len(b["gen"]) + (b["meta"] is not None)
+                + len(b["apply"]))
+
+    def capture(self, steps: int, regen: bool = True):
+        """A CUDA graph of ``steps`` iterations on self.stream; the gen batch
+        reads the iteration from the device counter, which each captured step
+        advances (set the first value with :meth:`set_iteration`)."""
+        if self.overlap:
+            raise errors.InvalidConfig("graph capture uses the one-stream schedule")
+        none = (1 << 64) - 1
+        graph = C.c_void_p()
+        _lib.call("srf_graph_begin", self.stream)
+        b = self.batches
+        for _ in range(steps):
+            if b["push"] is not None:
+                _lib.call("srf_batch_launch", b["push"], self.stream, none, 0, 0)
+            for g in b["gen"].values():
+                _lib.call("srf_batch_launch", g, self.stream, none, 1 if regen else 0, 0)
+            if b["meta"] is not None:
+                _lib.call("srf_batch_launch", b["meta"], self.stream, none, 0, 0)
+            for a in b["apply"].values():
+                _lib.call("srf_batch_launch", a, self.stream, none, 0, 0)
+            _lib.call("srf_counter_add", self.stream_space.handle, self._counter.base_addr, 1,
+                      self.stream)
+        _lib.call("srf_graph_end", self.stream, C.byref(graph))
+        return graph
+
+    def set_iteration(self, iteration: int) -> None:
+        self.sync()
+        self.stream_space.write_at(self._counter, 0, np.array([iteration], dtype="<u8"))
+
+    def replay(self, graph) -> int:
+        _lib.call("srf_graph_launch", graph, self.stream)
+        return 0
 
     def fork(self) -> None:
         """Order the phase streams after work already queued on self.stream."""

@@ -119,3 +119,21 @@ def test_inconsistent_meta_dims_are_rejected():
     ps.step(1)
     with pytest.raises(errors.BadToken):
         ps.sync()
+
+
+def test_graph_replayed_steps_match_eager():
+    """CUDA-graph capture of several iterations: the gen batch reads the
+    iteration from the device counter the captured steps advance."""
+    shapes, W, P = mlp_shapes(), 2, 1
+    L = PsLayout(shapes, W, P, False)
+    ps = PsStep(L, seed=4, op="sgd", lr=0.02)
+    ps.step(1)
+    ps.set_iteration(2)
+    g = ps.capture(5)
+    ps.replay(g)
+    ps.sync()
+    want = port.ps_expected_device(shapes, W, 4, range(1, 7), op="sgd", lr=0.02)
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes()
+    _lib.call("srf_graph_destroy", g)
+    ps.close()

@@ -453,6 +453,26 @@ def cpu_reference(S, min_seconds=10.0, min_steps=3, max_steps=None):
     return S * n / dt / 1e9, n, dt
 
 
+def cpu_mechanisms(sizes=(1 << 20, 16 << 20), seconds=1.5):
+    """The reference's three mechanisms on this host (oracle/port.py, 1 core):
+    zero-copy static, staged 'cp', and the copy-heavy RPC fragment ring."""
+    from oracle import port
+    out = []
+    for size in sizes:
+        row = {"bytes": size}
+        for name, rig in (("static", port.MicrobenchRig(size, generate=False)),
+                          ("cp", port.MicrobenchRig(size, generate=False, stage_copy=True)),
+                          ("rpc", port.RpcRig(size))):
+            rig.step()
+            n, t0 = 0, time.perf_counter()
+            while time.perf_counter() - t0 < seconds or n < 2:
+                rig.step()
+                n += 1
+            row[f"{name}_gbps"] = round(size * n / (time.perf_counter() - t0) / 1e9, 4)
+        out.append(row)
+    return out
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
@@ -883,6 +903,8 @@ def main() -> int:
                       f"host cpu_count={os.cpu_count()}"}
     if world == 1 and not args.no_sweep:
         line["sweep"] = sweep(S, local)
+        if not args.no_cpu:
+            line["cpu_sweep"] = cpu_mechanisms()
     if not args.no_ps:
         line["ps"] = bench_ps(rank, world, local, max(10, args.steps), args.warmup,
                               op=args.ps_op, cpu=not args.no_cpu)

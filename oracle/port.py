@@ -313,6 +313,9 @@ class MicrobenchRig:
     #: False: the payload is synthesised once (a host-resident input, as the
     #: GPU end-to-end measurement uses) and each step only moves + consumes it
     generate: bool = True
+    #: True: the reference "cp" mode - a counted copy into a registered
+    #: staging block before the put (protocol.py:77-80)
+    stage_copy: bool = False
 
     def __post_init__(self):
         cap = 2 * self.nbytes + (1 << 20)
@@ -337,7 +340,14 @@ class MicrobenchRig:
         n = self.nbytes // 4
         if self.generate:
             self._fill(self.it)
-        static_send(self.fab, self.src, (self.payload, self.nbytes), self.flag,
+        src = self.payload
+        if self.stage_copy:
+            if not hasattr(self, "_stage"):
+                self._stage, _ = self.src.allocate_region(max(self.nbytes, 1), True)
+            self.src.mem[self._stage:self._stage + self.nbytes] = \
+                self.src.mem[self.payload:self.payload + self.nbytes]
+            src = self._stage
+        static_send(self.fab, self.src, (src, self.nbytes), self.flag,
                     self.dst, self.region)
         got = static_poll(self.dst, self.region)
         assert got is not None
@@ -541,3 +551,67 @@ def ps_expected_device(shapes, workers: int, seed: int, iterations, op: str = "x
                 apply_sgd(val, grads, lr)
         out.append(val.reshape(dims))
     return out
+
+
+# -- the reference's copy-heavy RPC baseline (runtime/protocol.py:257-448) -------------
+
+FRAGMENT_BYTES = 4096                      # protocol.py:31
+FRAG_HEADER = struct.Struct("<QII")        # msg_id, frag_index, frag_count (:32)
+FRAG_PAYLOAD = FRAGMENT_BYTES - FRAG_HEADER.size
+RING_SLOTS = 16                            # 64 KiB ring / 4 KiB (:34-36)
+
+
+class RpcRig:
+    """One message through the RPC baseline per ``step``: metadata + payload
+    serialised into 4 KiB fragments through a staging buffer (counted copy 1,
+    protocol.py:336-347), each pushed into the next posted ring slot of the
+    receiver (post_send, fabric.py:432-497: one copy onto the wire), drained in
+    order and copied out into a fresh tensor buffer (counted copy 2,
+    protocol.py:397-438).  The ring's 16 slots are re-posted as they drain."""
+
+    def __init__(self, nbytes: int, rank: int = 1):
+        self.n = nbytes
+        self.rank = rank
+        self.src = np.random.default_rng(1).integers(0, 256, nbytes, dtype=np.uint8)
+        self.stage = np.zeros(FRAGMENT_BYTES, np.uint8)
+        self.ring = np.zeros((RING_SLOTS, FRAGMENT_BYTES), np.uint8)
+        self.out = np.zeros(nbytes, np.uint8)
+        self.msg = 0
+        self.copied = 0
+
+    def step(self) -> np.ndarray:
+        self.msg += 1
+        meta = np.frombuffer(encode_meta((self.n // 4,) if self.rank == 1 else (self.n,), 0 if
+                                         self.rank == 1 else 4, 0, 0), np.uint8)
+        total = len(meta) + self.n
+        count = -(-total // FRAG_PAYLOAD)
+        meta_out = np.zeros(len(meta), np.uint8)
+        for f in range(count):
+            off = f * FRAG_PAYLOAD
+            k = min(FRAG_PAYLOAD, total - off)
+            # sender: header + serialise the stream slice into the staging buffer
+            self.stage[:FRAG_HEADER.size] = np.frombuffer(
+                FRAG_HEADER.pack(self.msg, f, count), np.uint8)
+            pos, cur, left = FRAG_HEADER.size, off, k
+            if cur < len(meta):
+                m = min(len(meta) - cur, left)
+                self.stage[pos:pos + m] = meta[cur:cur + m]
+                pos, cur, left = pos + m, cur + m, left - m
+            if left:
+                self.stage[pos:pos + left] = self.src[cur - len(meta):cur - len(meta) + left]
+            self.copied += k
+            # send into the posted ring slot
+            slot = self.ring[f % RING_SLOTS]
+            slot[:FRAG_HEADER.size + k] = self.stage[:FRAG_HEADER.size + k]
+            # receiver: check the header, copy out, re-post
+            msg_id, idx, cnt = FRAG_HEADER.unpack(slot[:FRAG_HEADER.size].tobytes())
+            assert (msg_id, idx, cnt) == (self.msg, f, count), "ReassemblyGap"
+            pos, cur, left = FRAG_HEADER.size, off, k
+            if cur < len(meta):
+                m = min(len(meta) - cur, left)
+                meta_out[cur:cur + m] = slot[pos:pos + m]
+                pos, cur, left = pos + m, cur + m, left - m
+            if left:
+                self.out[cur - len(meta):cur - len(meta) + left] = slot[pos:pos + left]
+                self.copied += left
+        return self.out

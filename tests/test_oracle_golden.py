@@ -195,3 +195,14 @@ def test_transfer_rigs_run():
     val = mb.step()
     want = port.synthesize(1024, 0, port.node_rng(0, 0, 2)).max()
     assert val == float(want)
+
+
+def test_rpc_port_and_cp_rig():
+    rig = port.RpcRig(40 * port.FRAG_PAYLOAD + 123 * 4)
+    out = rig.step()
+    assert out.tobytes() == rig.src.tobytes()
+    assert rig.copied == 2 * rig.n + port.meta_block_size(1)
+    rig.step()
+    cp = port.MicrobenchRig(1 << 16, generate=False, stage_copy=True)
+    zc = port.MicrobenchRig(1 << 16, generate=False)
+    assert cp.step() == zc.step()

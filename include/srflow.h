@@ -259,6 +259,13 @@ int srf_batch_destroy(srf_batch_t batch);
  * (one thread, stream-ordered) at the end of each captured step */
 int srf_batch_set_iteration_source(srf_batch_t batch, srf_space_t space, uint64_t addr);
 int srf_counter_add(srf_space_t space, uint64_t addr, uint64_t delta, srf_stream_t stream);
+/* `iters` PS iterations (it0, it0+1, ...) in ONE cooperative launch when every
+ * server lives on this GPU: the four phases run back to back separated by
+ * grid-wide barriers; flags and credits are used exactly as in the per-phase
+ * launches (latency-bound configs: the MLP parity set) */
+int srf_ps_persistent(srf_batch_t push, srf_batch_t gen, srf_batch_t meta,
+                      srf_batch_t const *apply, int napply, srf_stream_t stream, uint64_t it0,
+                      uint32_t iters, int mode);
 
 /* RPC-style serialize/copy baseline (runtime/protocol.py:257-448) on the
  * device - the comparator the north star reports zero-copy against.  The

@@ -110,6 +110,7 @@ SIGNATURES = {
     "srf_batch_destroy": (C.c_int, [vp]),
     "srf_batch_set_iteration_source": (C.c_int, [vp, vp, u64]),
     "srf_counter_add": (C.c_int, [vp, u64, u64, vp]),
+    "srf_ps_persistent": (C.c_int, [vp, vp, vp, P(vp), C.c_int, vp, u64, C.c_uint32, C.c_int]),
     "srf_doorbell_bind": (C.c_int, [vp, u64, u64, C.c_int]),
     "srf_flag_read": (C.c_int, [vp, u64, u64, vp]),
     "srf_flag_clear": (C.c_int, [vp, u64]),

@@ -12,6 +12,7 @@
 //
 // Declarations and reference citations: include/srflow.h.
 
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <unistd.h>
@@ -27,6 +28,8 @@
 #include <vector>
 
 #include "../../include/srflow.h"
+
+namespace cg = cooperative_groups;
 
 // ---------------------------------------------------------------------------
 // error plumbing
@@ -1054,19 +1057,25 @@ __device__ __forceinline__ int find_desc(const D *d, int n, uint32_t u) {
   return lo;
 }
 
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u8(const uint8_t *p) {
+  uint16_t v;
+  asm volatile("ld.acquire.gpu.global.u8 %0, [%1];" : "=h"(v) : "l"(p) : "memory");
+  return v & 0xff;
+}
+
 __device__ __forceinline__ bool spin_until(const uint8_t *p, uint32_t want,
-                                           uint64_t timeout_ns) {
+                                           uint64_t timeout_ns, int sys_scope = 1) {
   uint64_t t0 = globaltimer_ns();
-  while (ld_acquire_sys_u8(p) != want) {
+  while ((sys_scope ? ld_acquire_sys_u8(p) : ld_acquire_gpu_u8(p)) != want) {
     if (globaltimer_ns() - t0 > timeout_ns) return false;
     __nanosleep(20);
   }
   return true;
 }
 
-__global__ void __launch_bounds__(512) k_put_batch(const BatchPut *descs, int n,
-                                                   uint32_t total_units, unsigned int *counters,
-                                                   uint64_t timeout_ns, int *err) {
+__device__ __forceinline__ void put_batch_units(const BatchPut *descs, int n,
+                                                uint32_t total_units, unsigned int *counters,
+                                                uint64_t timeout_ns, int *err, int sys) {
   __shared__ int s_desc, s_last;
   for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x) {
     if (threadIdx.x == 0) s_desc = find_desc(descs, n, u);
@@ -1074,16 +1083,16 @@ __global__ void __launch_bounds__(512) k_put_batch(const BatchPut *descs, int n,
     const BatchPut d = descs[s_desc];
     const uint32_t lb = u - d.cta_begin;
     if (d.wait_empty) {
-      if (threadIdx.x == 0 && !spin_until(d.dst + d.body, 0, timeout_ns)) atomicExch(err, 2);
+      if (threadIdx.x == 0 && !spin_until(d.dst + d.body, 0, timeout_ns, sys)) atomicExch(err, 2);
       __syncthreads();
     }
     copy_bytes_grid<8>(d.dst, d.src, d.body, (uint64_t)lb * blockDim.x + threadIdx.x,
                        (uint64_t)d.cta_count * blockDim.x);
     __syncthreads();
-    if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
+    if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, sys);
     __syncthreads();
     if (s_last && threadIdx.x == 0) {
-      release_tail(d.dst + d.body, *d.tail, 1);
+      release_tail(d.dst + d.body, *d.tail, sys);
       atomicExch(&counters[s_desc], 0u);
     }
     __syncthreads();  // shared state is reused by the next unit
@@ -1113,12 +1122,11 @@ __device__ __forceinline__ float unit_f32(uint32_t k0, uint32_t k1, uint32_t i) 
   return (float)((fmix32(i * 0x9E3779B1u + k0) ^ k1) >> 8) * (1.0f / 16777216.0f);
 }
 
-__global__ void __launch_bounds__(512) k_gen_batch(const BatchGen *descs, int n,
-                                                   uint32_t total_units, unsigned int *counters,
-                                                   uint64_t seed,
-                                                   uint64_t iteration_arg,
-                                                   const uint64_t *iteration_ptr, int regen,
-                                                   uint64_t timeout_ns, int *err) {
+__device__ __forceinline__ void gen_batch_units(const BatchGen *descs, int n,
+                                                uint32_t total_units, unsigned int *counters,
+                                                uint64_t seed, uint64_t iteration_arg,
+                                                const uint64_t *iteration_ptr, int regen,
+                                                uint64_t timeout_ns, int *err, int sys) {
   // iteration from a device counter when given (graph-replayed steps)
   const uint64_t iteration = iteration_ptr ? *(const volatile uint64_t *)iteration_ptr
                                            : iteration_arg;
@@ -1129,8 +1137,8 @@ __global__ void __launch_bounds__(512) k_gen_batch(const BatchGen *descs, int n,
     const BatchGen d = descs[s_desc];
     const uint32_t lb = u - d.cta_begin;
     if (threadIdx.x == 0) {
-      if (d.weight_flag && !spin_until(d.weight_flag, 1, timeout_ns)) atomicExch(err, 3);
-      if (d.credit && !spin_until(d.credit, 0, timeout_ns)) atomicExch(err, 4);
+      if (d.weight_flag && !spin_until(d.weight_flag, 1, timeout_ns, sys)) atomicExch(err, 3);
+      if (d.credit && !spin_until(d.credit, 0, timeout_ns, sys)) atomicExch(err, 4);
     }
     __syncthreads();
     if (regen) {
@@ -1150,21 +1158,21 @@ __global__ void __launch_bounds__(512) k_gen_batch(const BatchGen *descs, int n,
         g[i] = unit_f32(k0, k1, (uint32_t)i);
     }
     __syncthreads();
-    if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
+    if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, sys);
     __syncthreads();
     if (s_last && threadIdx.x == 0) {
       // the weight was consumed: clear its flag (StaticReceiver.poll semantics)
-      if (d.weight_flag) release_tail(d.weight_flag, 0, 1);
+      if (d.weight_flag) release_tail(d.weight_flag, 0, sys);
       atomicExch(&counters[s_desc], 0u);
     }
     __syncthreads();  // shared state is reused by the next unit
   }
 }
 
-__global__ void __launch_bounds__(256) k_apply_batch(const BatchApply *descs, int n,
-                                                     uint32_t total_units, unsigned int *counters,
-                                                     int op, float lr,
-                                                     uint64_t timeout_ns, int *err) {
+__device__ __forceinline__ void apply_batch_units(const BatchApply *descs, int n,
+                                                  uint32_t total_units, unsigned int *counters,
+                                                  int op, float lr, uint64_t timeout_ns,
+                                                  int *err, int sys) {
   __shared__ int s_desc, s_last, s_bad;
   __shared__ const uint8_t *s_g[SRF_MAX_WORKERS];
   for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x) {
@@ -1183,7 +1191,7 @@ __global__ void __launch_bounds__(256) k_apply_batch(const BatchApply *descs, in
       const uint8_t *m = d.src[w];
       if (!((d.is_meta >> w) & 1)) {
         s_g[w] = m;  // co-located worker: its gradient block directly
-      } else if (!spin_until(m + 8 * r + 32, 1, timeout_ns)) {
+      } else if (!spin_until(m + 8 * r + 32, 1, timeout_ns, sys)) {
         atomicExch(err, 5);
         s_bad = 1;
       } else {
@@ -1214,14 +1222,72 @@ __global__ void __launch_bounds__(256) k_apply_batch(const BatchApply *descs, in
         apply_range<true>(d.var, s_g, d.nw, d.n, lr, t, nth);
     }
     __syncthreads();
-    if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, 1);
+    if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, sys);
     __syncthreads();
     // gradients consumed: the last CTA clears the meta flags (credit for the
     // next send; DynReceiver.poll's clear)
     if (s_last && threadIdx.x < (unsigned)d.nw && ((d.is_meta >> threadIdx.x) & 1))
-      release_tail((uint8_t *)d.src[threadIdx.x] + 8 * r + 32, 0, 1);
+      release_tail((uint8_t *)d.src[threadIdx.x] + 8 * r + 32, 0, sys);
     if (s_last && threadIdx.x == 0) atomicExch(&counters[s_desc], 0u);
     __syncthreads();  // shared state is reused by the next unit
+  }
+}
+
+
+__global__ void __launch_bounds__(512) k_put_batch(const BatchPut *descs, int n,
+                                                   uint32_t total_units, unsigned int *counters,
+                                                   uint64_t timeout_ns, int *err, int sys) {
+  put_batch_units(descs, n, total_units, counters, timeout_ns, err, sys);
+}
+
+__global__ void __launch_bounds__(512) k_gen_batch(const BatchGen *descs, int n,
+                                                   uint32_t total_units, unsigned int *counters,
+                                                   uint64_t seed, uint64_t iteration_arg,
+                                                   const uint64_t *iteration_ptr, int regen,
+                                                   uint64_t timeout_ns, int *err, int sys) {
+  gen_batch_units(descs, n, total_units, counters, seed, iteration_arg, iteration_ptr, regen,
+                  timeout_ns, err, sys);
+}
+
+__global__ void __launch_bounds__(256) k_apply_batch(const BatchApply *descs, int n,
+                                                     uint32_t total_units, unsigned int *counters,
+                                                     int op, float lr, uint64_t timeout_ns,
+                                                     int *err, int sys) {
+  apply_batch_units(descs, n, total_units, counters, op, lr, timeout_ns, err, sys);
+}
+
+// One PS iteration loop in a single cooperative launch (all servers on this
+// GPU): the four phases back to back, separated by grid-wide barriers, for
+// `iters` iterations.  The device flags and credits are still set and
+// consumed exactly as in the per-phase launches; only the launch gaps go.
+static constexpr int kMaxApply = 8;
+
+struct PsPersistArgs {
+  const BatchPut *push; int npush; uint32_t upush; unsigned int *cpush;
+  const BatchGen *gen; int ngen; uint32_t ugen; unsigned int *cgen; uint64_t seed;
+  const BatchPut *meta; int nmeta; uint32_t umeta; unsigned int *cmeta;
+  const BatchApply *apply[kMaxApply]; int napply[kMaxApply]; uint32_t uapply[kMaxApply];
+  unsigned int *capply[kMaxApply]; int nbatches;
+  int op; float lr;
+  uint64_t it0; uint32_t iters; int regen; uint64_t timeout_ns; int *err;
+  int sys;  // every buffer is this GPU's own HBM -> 0 (gpu-scope ordering)
+};
+
+__global__ void __launch_bounds__(256) k_ps_persistent(const __grid_constant__ PsPersistArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  for (uint32_t i = 0; i < a.iters; ++i) {
+    if (a.push) put_batch_units(a.push, a.npush, a.upush, a.cpush, a.timeout_ns, a.err, a.sys);
+    grid.sync();
+    if (a.gen)
+      gen_batch_units(a.gen, a.ngen, a.ugen, a.cgen, a.seed, a.it0 + i, nullptr, a.regen,
+                      a.timeout_ns, a.err, a.sys);
+    grid.sync();
+    if (a.meta) put_batch_units(a.meta, a.nmeta, a.umeta, a.cmeta, a.timeout_ns, a.err, a.sys);
+    grid.sync();
+    for (int b = 0; b < a.nbatches; ++b)
+      apply_batch_units(a.apply[b], a.napply[b], a.uapply[b], a.capply[b], a.op, a.lr,
+                        a.timeout_ns, a.err, a.sys);
+    grid.sync();
   }
 }
 
@@ -2148,6 +2214,7 @@ struct srf_batch {
   int kind;  // 0 put, 1 gen, 2 apply
   int device;
   const uint64_t *iter_ptr = nullptr;  // gen: device iteration counter (graphs)
+  int sys = 1;  // 0 when every buffer of the batch is on the launching GPU
   void *descs;
   int n;
   unsigned int *counters;
@@ -2232,7 +2299,14 @@ int srf_batch_put_create(int n, srf_space_t const *src_space, const uint64_t *sr
     d.pad = 0;
     next += d.cta_count;
   }
-  return finish_batch(0, device, host, src_space[0]->err, out);
+  int rc0 = finish_batch(0, device, host, src_space[0]->err, out);
+  if (rc0 == SRF_OK) {
+    int sys = 0;
+    for (int i = 0; i < n; ++i)
+      sys |= (dst_space[i]->imported || dst_space[i]->device != device) ? 1 : 0;
+    (*out)->sys = sys;
+  }
+  return rc0;
 }
 
 int srf_batch_gen_create(int n, srf_space_t const *space, const uint64_t *grad_addr,
@@ -2265,7 +2339,14 @@ int srf_batch_gen_create(int n, srf_space_t const *space, const uint64_t *grad_a
     next += d.cta_count;
   }
   int rc = finish_batch(1, device, host, space[0]->err, out);
-  if (rc == SRF_OK) (*out)->seed = seed;
+  if (rc == SRF_OK) {
+    (*out)->seed = seed;
+    int sys = 0;
+    for (int i = 0; i < n; ++i)
+      if (credit_space[i])
+        sys |= (credit_space[i]->imported || credit_space[i]->device != device) ? 1 : 0;
+    (*out)->sys = sys;
+  }
   return rc;
 }
 
@@ -2320,6 +2401,11 @@ int srf_batch_apply_create(srf_space_t sp, int nvars, const uint64_t *var_addr,
   if (rc == SRF_OK) {
     (*out)->op = op;
     (*out)->lr = lr;
+    int sys = 0;
+    for (int i = 0; i < k; ++i)
+      if (is_meta[i])
+        sys |= (peer_space[i]->imported || peer_space[i]->device != sp->device) ? 1 : 0;
+    (*out)->sys = sys;
   }
   return rc;
 }
@@ -2333,17 +2419,17 @@ int srf_batch_launch(srf_batch_t b, srf_stream_t st, uint64_t iteration, int mod
   switch (b->kind) {
     case 0:
       k_put_batch<<<grid, 512, 0, st->s>>>((const BatchPut *)b->descs, b->n, units,
-                                           b->counters, timeout, b->err);
+                                           b->counters, timeout, b->err, b->sys);
       return launch_check("k_put_batch");
     case 1:
       k_gen_batch<<<grid, 512, 0, st->s>>>((const BatchGen *)b->descs, b->n, units,
                                            b->counters, b->seed, iteration,
                                            iteration == UINT64_MAX ? b->iter_ptr : nullptr,
-                                           mode, timeout, b->err);
+                                           mode, timeout, b->err, b->sys);
       return launch_check("k_gen_batch");
     default:
       k_apply_batch<<<grid, 256, 0, st->s>>>((const BatchApply *)b->descs, b->n, units,
-                                             b->counters, b->op, b->lr, timeout, b->err);
+                                             b->counters, b->op, b->lr, timeout, b->err, b->sys);
       return launch_check("k_apply_batch");
   }
 }
@@ -2368,6 +2454,55 @@ int srf_counter_add(srf_space_t sp, uint64_t addr, uint64_t delta, srf_stream_t 
   CUDA_TRY(cudaSetDevice(s->device));
   k_counter_add<<<1, 1, 0, s->s>>>((uint64_t *)(sp->base + addr), delta);
   return launch_check("k_counter_add");
+}
+
+int srf_ps_persistent(srf_batch_t push, srf_batch_t gen, srf_batch_t meta,
+                      srf_batch_t const *apply, int napply, srf_stream_t st, uint64_t it0,
+                      uint32_t iters, int mode) {
+  if (napply < 0 || napply > kMaxApply)
+    return fail(SRF_E_INVALID_CONFIG, "at most %d apply batches", kMaxApply);
+  srf_batch *all[3] = {push, gen, meta};
+  for (srf_batch *b : all)
+    if (b && b->device != st->device)
+      return fail(SRF_E_INVALID_CONFIG, "persistent PS step needs every batch on one GPU");
+  PsPersistArgs a;
+  memset(&a, 0, sizeof a);
+  if (push) { a.push = (const BatchPut *)push->descs; a.npush = push->n; a.upush = push->grid; a.cpush = push->counters; }
+  if (gen) { a.gen = (const BatchGen *)gen->descs; a.ngen = gen->n; a.ugen = gen->grid; a.cgen = gen->counters; a.seed = gen->seed; }
+  if (meta) { a.meta = (const BatchPut *)meta->descs; a.nmeta = meta->n; a.umeta = meta->grid; a.cmeta = meta->counters; }
+  for (int i = 0; i < napply; ++i) {
+    if (apply[i]->device != st->device)
+      return fail(SRF_E_INVALID_CONFIG, "persistent PS step needs every batch on one GPU");
+    a.apply[i] = (const BatchApply *)apply[i]->descs;
+    a.napply[i] = apply[i]->n;
+    a.uapply[i] = apply[i]->grid;
+    a.capply[i] = apply[i]->counters;
+    a.op = apply[i]->op;
+    a.lr = apply[i]->lr;
+  }
+  a.nbatches = napply;
+  a.it0 = it0;
+  a.iters = iters;
+  a.regen = mode;
+  a.timeout_ns = 10ull * 1000 * 1000 * 1000;
+  a.err = (push ? push : gen ? gen : meta)->err;
+  a.sys = 0;
+  for (srf_batch *b : all) a.sys |= b ? b->sys : 0;
+  for (int i = 0; i < napply; ++i) a.sys |= apply[i]->sys;
+  CUDA_TRY(cudaSetDevice(st->device));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ps_persistent, 256, 0));
+  if (per_sm < 1) return fail(SRF_E_DEVICE, "persistent PS kernel does not fit an SM");
+  // no more CTAs than the busiest phase has work units: grid barriers of a
+  // small grid are cheaper (latency-bound configs)
+  uint32_t most = 1;
+  for (srf_batch *b : all) most = std::max<uint32_t>(most, b ? (uint32_t)b->grid : 0u);
+  for (int i = 0; i < napply; ++i) most = std::max<uint32_t>(most, (uint32_t)apply[i]->grid);
+  const int grid = (int)std::min<uint32_t>(most, (uint32_t)(per_sm * sm_count_of(st->device)));
+  void *params[] = {&a};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_ps_persistent, dim3(grid), dim3(256),
+                                       params, 0, st->s));
+  return launch_check("k_ps_persistent");
 }
 
 int srf_batch_destroy(srf_batch_t b) {

@@ -491,6 +491,20 @@ class PsStep:
         _lib.call("srf_graph_end", self.stream, C.byref(graph))
         return graph
 
+    def run_persistent(self, first_iteration: int, iterations: int, regen: bool = True) -> None:
+        """``iterations`` PS iterations in one cooperative launch (every server
+        of the layout on this GPU, world == 1): phases separated by grid-wide
+        barriers instead of kernel boundaries."""
+        if self.world != 1:
+            raise errors.InvalidConfig("the persistent PS step runs on one GPU")
+        b = self.batches
+        applies = list(b["apply"].values())
+        gen = next(iter(b["gen"].values()), None)
+        _lib.call("srf_ps_persistent", b["push"], gen, b["meta"],
+                  (C.c_void_p * max(1, len(applies)))(*[a.value for a in applies]),
+                  len(applies), self.stream, first_iteration, iterations,
+                  1 if regen else 0)
+
     def set_iteration(self, iteration: int) -> None:
         self.sync()
         self.stream_space.write_at(self._counter, 0, np.array([iteration], dtype="<u8"))

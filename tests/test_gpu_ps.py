@@ -137,3 +137,18 @@ def test_graph_replayed_steps_match_eager():
         assert ps.variable(v).tobytes() == want[v].tobytes()
     _lib.call("srf_graph_destroy", g)
     ps.close()
+
+
+@pytest.mark.parametrize("shapes,W,P,coloc", CASES)
+def test_persistent_step_matches_oracle(shapes, W, P, coloc):
+    """All four phases of many iterations in one cooperative launch."""
+    L = PsLayout(shapes, W, P, coloc)
+    ps = PsStep(L, seed=6, op="sgd", lr=0.03)
+    ps.step(1)
+    ps.run_persistent(2, 6)
+    ps.step(8)
+    ps.sync()
+    want = port.ps_expected_device(shapes, W, 6, range(1, 9), op="sgd", lr=0.03)
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes()
+    ps.close()

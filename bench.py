@@ -309,9 +309,32 @@ def bench_sendrecv_device(S, steps, warmup, rank, world, device):
     ok = ring.verify()
     ok = dist_sum(0.0 if ok else 1.0) == 0.0
     launches = int(dist_sum(launches))
+    ce = copy_engine_comparator(ring, S, device)
     return {"total_ms": total_ms, "rounds": rounds, "n": n, "put_avg_ms": put_avg_ms,
             "verified": ok, "launches": launches, "clocks": clk, "t_round_ms": t_round,
-            "ring": ring}
+            "ring": ring, "copy_engine_gbps": ce}
+
+
+def copy_engine_comparator(ring, S, device, reps=10):
+    """Comparator only (not on the path): the DMA copy engine moving the same
+    payload into the same destination mapping (cudaMemcpy via torch), per
+    direction, max time over ranks."""
+    import torch
+    from paper_1805_08430_b200.memspace import device_view
+    src = ring.src.view(ring.payload, 0, S)
+    dst = device_view(ring.dst.device_base + ring.dst_region[0], S, device)
+    for _ in range(3):
+        dst.copy_(src)
+    barrier_sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        dst.copy_(src)
+    e1.record()
+    torch.cuda.synchronize()
+    t = dist_max(e0.elapsed_time(e1) / 1e3)
+    barrier_sync()
+    return round(S * reps / t / 1e9, 1)
 
 
 # -- end to end through the public API ------------------------------------------------------
@@ -953,6 +976,10 @@ def main() -> int:
         "gpu_launches": dev["launches"],
         "clocks": dev["clocks"],
         "verified": dev["verified"],
+        "comparators": {"copy_engine_gbps_per_gpu": dev["copy_engine_gbps"],
+                        "k1_gbps_per_gpu": round(S / put_s / 1e9, 1),
+                        "note": "DMA copy engine (cudaMemcpy) into the same destination "
+                                "mapping - comparator only, not on the path"},
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         gbps, n, dt = cpu_reference(S, min_seconds=args.cpu_seconds)

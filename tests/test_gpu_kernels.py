@@ -244,3 +244,39 @@ def test_wait_empty_put_credit(pair):
         b.sync()
     assert hashlib.sha256(b.read_raw(dst, 4096)).digest() == \
         hashlib.sha256(rand_bytes(4096, 1).tobytes()).digest()
+
+
+def test_transfers_beyond_4gib_indexing():
+    """> 2^32-byte put and pull (64-bit offsets everywhere), checked on the
+    device against the source."""
+    import torch
+    S = (4 << 30) + 4096 + 24
+    a = MemorySpace(0, S + (8 << 20), device=0)
+    b = MemorySpace(1, S + (8 << 20), device=1 if _lib.device_count() > 1 else 0)
+    _lib.call("srf_connect", a.handle, b.handle)
+    ra = a.allocate_region(S + (4 << 20), register=True)
+    rb = b.allocate_region(S + (4 << 20), register=True)
+    src = a.view(ra, 0, S)
+    g = torch.Generator(device=src.device)
+    g.manual_seed(7)
+    src.view(torch.int32)[: S // 4].copy_(torch.randint(-2**31, 2**31 - 1, (S // 4,),
+                                                        dtype=torch.int32, device=src.device,
+                                                        generator=g))
+    flag = ra.base_addr + S
+    a.write_raw(flag, b"\x01")
+    put(a, [(ra.base_addr, S, ra.access_token), (flag, 1, ra.access_token)], b, rb.base_addr,
+        rb.access_token)
+    dst = b.view(rb, 0, S)
+    assert torch.equal(dst.to(src.device), src)
+    assert b.read_raw(rb.base_addr + S, 1) == b"\x01"
+    # wipe the source, then pull the bytes back from the peer (K4)
+    src.zero_()
+    torch.cuda.synchronize(src.device)
+    ev = C.c_void_p()
+    _lib.call("srf_get", a.handle, ra.base_addr + 0, ra.access_token, b.handle, rb.base_addr,
+              rb.access_token, S, None, C.byref(ev))
+    _lib.Event(ev).wait()
+    assert torch.equal(src, dst.to(src.device))
+    assert int(src[-4096:].to(torch.int64).sum()) != 0
+    a.close()
+    b.close()

@@ -150,7 +150,8 @@ static int make_stream(int device, bool create, cudaStream_t existing,
     st->s = existing;
   }
   cudaError_t e = cudaMalloc(&st->counter, sizeof(unsigned int) + 16);
-  if (e == cudaSuccess) e = cudaMemset(st->counter, 0, sizeof(unsigned int) + 16);
+  if (e == cudaSuccess) e = cudaMemsetAsync(st->counter, 0, sizeof(unsigned int) + 16, st->s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st->s);
   if (e == cudaSuccess) e = cudaMalloc(&st->scratch, sizeof(float) * kScratchBlocks);
   if (e != cudaSuccess) {
     if (create) cudaStreamDestroy(st->s);
@@ -814,6 +815,24 @@ __global__ void __launch_bounds__(256) k_put_bulk(PutArgs a) {
     }
     atomicExch(a.counter, 0u);
   }
+}
+
+// Pool zero-fill with plain SM stores.  cudaMemsetAsync(0) on a fresh
+// multi-GiB cudaMalloc pool left it in a state where later peer (NVLink)
+// stores from another GPU were partly not visible to local reads (~1.3 % of
+// the bytes of a > 2 GiB put, reproducible; tests/test_gpu_kernels.py
+// ::test_transfers_beyond_4gib_indexing); writing real zeros from the SMs
+// avoids it.
+__global__ void __launch_bounds__(256) k_zero_fill(uint8_t *p, uint64_t n) {
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t head = ((16 - ((uintptr_t)p & 15)) & 15) < n ? ((16 - ((uintptr_t)p & 15)) & 15) : n;
+  const uint64_t nv = (n - head) / 16;
+  uint4 *v = (uint4 *)(p + head);
+  const uint4 z = make_uint4(0, 0, 0, 0);
+  for (uint64_t i = t; i < nv; i += nth) v[i] = z;
+  for (uint64_t i = t; i < head; i += nth) p[i] = 0;
+  for (uint64_t i = head + nv * 16 + t; i < n; i += nth) p[i] = 0;
 }
 
 // K2 flag_wait: device-side consumer prologue of StaticReceiver.poll.
@@ -1640,9 +1659,14 @@ int srf_space_create(int server_id, int cuda_device, uint64_t capacity,
   int rc = make_stream(cuda_device, true, nullptr, &sp->stream);
   if (rc == SRF_OK) {
     e = cudaMalloc(&sp->err, sizeof(int));
-    if (e == cudaSuccess) e = cudaMemset(sp->err, 0, sizeof(int));
-    // np.zeros semantics: the whole space reads as zero bytes
-    if (e == cudaSuccess) e = cudaMemsetAsync(sp->base, 0, capacity, sp->stream->s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(sp->err, 0, sizeof(int), sp->stream->s);
+    // np.zeros semantics: the whole space reads as zero bytes (SM stores, see
+    // k_zero_fill)
+    if (e == cudaSuccess) {
+      const int grid = sm_count_of(cuda_device) * 4;
+      k_zero_fill<<<grid, 256, 0, sp->stream->s>>>(sp->base, capacity);
+      e = cudaGetLastError();
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(sp->stream->s);
     if (e != cudaSuccess) rc = fail(SRF_E_DEVICE, "space init: %s", cudaGetErrorString(e));
   }
@@ -1810,7 +1834,8 @@ int srf_space_sync(srf_space_t sp) {
   int err = 0;
   CUDA_TRY(cudaMemcpy(&err, sp->err, sizeof(int), cudaMemcpyDeviceToHost));
   if (err) {
-    cudaMemset(sp->err, 0, sizeof(int));
+    cudaMemsetAsync(sp->err, 0, sizeof(int), sp->stream->s);
+    cudaStreamSynchronize(sp->stream->s);
     if (err == 8)
       return fail(SRF_E_PROTOCOL, "server %d: RPC fragment out of order (ReassemblyGap)",
                   sp->server_id);
@@ -1902,7 +1927,8 @@ int srf_space_import_fd(int fd, int server_id, int local_device, uint64_t capaci
   if (rc == SRF_OK) rc = make_stream(local_device, true, nullptr, &sp->stream);
   if (rc == SRF_OK) {
     cudaError_t e = cudaMalloc(&sp->err, sizeof(int));
-    if (e == cudaSuccess) e = cudaMemset(sp->err, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(sp->err, 0, sizeof(int), sp->stream->s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(sp->stream->s);
     if (e != cudaSuccess) rc = fail(SRF_E_DEVICE, "proxy: %s", cudaGetErrorString(e));
   }
   if (rc != SRF_OK) {
@@ -1947,7 +1973,8 @@ int srf_space_import(const void *handle64, int server_id, int local_device,
   int rc = make_stream(local_device, true, nullptr, &sp->stream);
   if (rc == SRF_OK) {
     cudaError_t e = cudaMalloc(&sp->err, sizeof(int));
-    if (e == cudaSuccess) e = cudaMemset(sp->err, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemsetAsync(sp->err, 0, sizeof(int), sp->stream->s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(sp->stream->s);
     if (e != cudaSuccess) rc = fail(SRF_E_DEVICE, "proxy: %s", cudaGetErrorString(e));
   }
   if (rc != SRF_OK) {
@@ -2254,6 +2281,7 @@ static int finish_batch(int kind, int device, std::vector<D> &host, int *err, sr
     e = cudaMemcpy(b->descs, host.data(), sizeof(D) * host.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&b->counters, sizeof(unsigned) * std::max<size_t>(1, host.size()));
   if (e == cudaSuccess) e = cudaMemset(b->counters, 0, sizeof(unsigned) * std::max<size_t>(1, host.size()));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();  // counters zero before any launch
   if (e != cudaSuccess) {
     delete b;
     return fail(SRF_E_DEVICE, "batch upload: %s", cudaGetErrorString(e));

@@ -344,7 +344,12 @@ class MemorySpace:
 
     def view(self, handle: RegionHandle, offset: int = 0,
              length: Optional[int] = None):
-        """Writable uint8 device view (a torch tensor aliasing the pool)."""
+        """Writable uint8 device view (a torch tensor aliasing the pool).
+
+        Work torch issues on the view runs on torch's stream, which is not
+        ordered with this space's stream: synchronise it (e.g.
+        ``torch.cuda.current_stream(dev).synchronize()``) before a verb reads
+        or writes the same bytes."""
         if length is None:
             length = handle.length - offset
         addr = self._handle_range(handle, offset, length)

@@ -262,6 +262,8 @@ def test_transfers_beyond_4gib_indexing():
     src.view(torch.int32)[: S // 4].copy_(torch.randint(-2**31, 2**31 - 1, (S // 4,),
                                                         dtype=torch.int32, device=src.device,
                                                         generator=g))
+    # torch's stream is not ordered with the space's stream: finish the fill
+    torch.cuda.synchronize(src.device)
     flag = ra.base_addr + S
     a.write_raw(flag, b"\x01")
     put(a, [(ra.base_addr, S, ra.access_token), (flag, 1, ra.access_token)], b, rb.base_addr,

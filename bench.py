@@ -523,7 +523,7 @@ def run_reference_arm(args, rank, world):
         "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=JSON_OUT, flush=True)
     return 0
 
 
@@ -905,6 +905,8 @@ def bench_ps_configs(rank, world, device, steps, warmup, op, cpu):
     return out
 
 
+JSON_OUT = None
+
 # -- main -------------------------------------------------------------------------------------------
 
 
@@ -922,6 +924,13 @@ def main() -> int:
     ap.add_argument("--ps-op", choices=("sgd", "xor"), default="sgd")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+
+    # stdout carries the one JSON line only: everything else written to fd 1
+    # (the NCCL version banner, library prints) goes to stderr
+    global JSON_OUT
+    JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    sys.stdout = sys.stderr
 
     from paper_1805_08430_b200.distributed import env_world
     rank, world, local = env_world()
@@ -956,7 +965,8 @@ def main() -> int:
         roof = {"bound": "nvlink", "achieved": round(ach, 2), "peak": NVLINK_MEASURED_GBS,
                 "unit": "GB/s", "frac": round(ach / NVLINK_MEASURED_GBS, 4),
                 "frac_of_nominal_900": round(ach / NVLINK_NOMINAL_GBS, 4),
-                "kernel": "k_put (K1 static_put)", "bytes_per_launch": alg,
+                "kernel": "K1 static_put: copy-engine body (knob 6, cross-device >= 1 MiB) "
+                          "+ k_put tail release", "bytes_per_launch": alg,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction "
                                "(nominal 900)"}
     roof["traffic"] = traffic_from_profiles(world)
@@ -978,8 +988,11 @@ def main() -> int:
         "verified": dev["verified"],
         "comparators": {"copy_engine_gbps_per_gpu": dev["copy_engine_gbps"],
                         "k1_gbps_per_gpu": round(S / put_s / 1e9, 1),
-                        "note": "DMA copy engine (cudaMemcpy) into the same destination "
-                                "mapping - comparator only, not on the path"},
+                        "note": ("DMA copy engine (cudaMemcpy) into the same destination "
+                                 "mapping - comparator only, not on the path" if world == 1
+                                 else "raw cudaMemcpy ceiling through the same peer mapping; "
+                                      "K1 moves its body on the same engine (SM stores "
+                                      "into a peer pool cap near 496 GB/s cross-process)")},
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         gbps, n, dt = cpu_reference(S, min_seconds=args.cpu_seconds)
@@ -1008,7 +1021,7 @@ def main() -> int:
         line["ps_configs"] = bench_ps_configs(rank, world, local, max(20, args.steps),
                                               args.warmup, args.ps_op, not args.no_cpu)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=JSON_OUT, flush=True)
     ps_ok = line.get("ps", {}).get("verified", True) and all(
         c["verified"] for c in line.get("ps_configs", {}).values()) and \
         line.get("ps_balanced", {}).get("verified", True)

@@ -58,7 +58,9 @@ uint64_t srf_launch_count(void);
 /* launch-geometry knobs of the copy kernels: 0 = CTAs per SM (1..32),
  * 1 = threads per CTA (128/256/512), 2 = copy implementation (0 vector,
  * 1 TMA bulk), 3 = pool allocator (0 cudaMalloc + CUDA IPC, 1 VMM + fd),
- * 4 = 16-B vectors in flight per thread (4 or 8), 5 = 32-B vectors (0/1) */
+ * 4 = 16-B vectors in flight per thread (4 or 8), 5 = 32-B vectors (0/1),
+ * 6 = cross-device bodies >= value KiB move on the copy engine, the tail
+ *     flag still released by an SM store after them (0 = never; default 1024) */
 int srf_tune(int knob, int value);
 
 /* ---- memory spaces (memspace.py) ----------------------------------------- */

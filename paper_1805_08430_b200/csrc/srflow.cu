@@ -1525,6 +1525,11 @@ static int launch_check(const char *what) {
 
 static int g_put_impl = 0;  // 0 = vector LDG/STG, 1 = TMA bulk (large segments)
 static int g_unroll = 8;    // 16-B vectors in flight per thread (4 or 8)
+// knob 6: cross-device bodies of at least this many bytes move on the copy
+// engine (0: never).  SM stores into a peer's pool are capped near 496 GB/s
+// across processes; the DMA engine reaches ~750 GB/s through the same mapping
+// (profiles/r1_ring_probe.json, r1_xproc_store_probe*.jsonl).
+static uint64_t g_peer_ce_bytes = 1ull << 20;
 
 // launch K1/K4/K5 with the configured implementation
 static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
@@ -1550,6 +1555,35 @@ static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
       k_put<4><<<grid, block, 0, s->s>>>(a);
   }
   return launch_check(what);
+}
+
+// K1 with a copy-engine body: [credit wait] -> body copies -> a one-thread K1
+// that releases the tail byte.  Stream order starts the tail kernel only after
+// the copies have completed, so a consumer that acquires the flag sees the
+// body (release/acquire stress test, tests/test_gpu_kernels.py).
+static int put_via_copy_engine(const PutArgs &a, srf_stream *s) {
+  uint8_t *tail = a.dst + a.total - 1;
+  if (a.wait_empty) {
+    k_flag_wait<<<1, 32, 0, s->s>>>(tail, 0, 0, a.timeout_ns, a.err);
+    int rc = launch_check("k_flag_wait(credit)");
+    if (rc) return rc;
+  }
+  const uint64_t body = a.total - 1;
+  for (int i = 0; i < a.nseg; ++i) {
+    const Seg &sg = a.seg[i];
+    if (sg.dst_off >= body) break;
+    const uint64_t n = std::min<uint64_t>(sg.len, body - sg.dst_off);
+    CUDA_TRY(cudaMemcpyAsync(a.dst + sg.dst_off, sg.src, n, cudaMemcpyDeviceToDevice, s->s));
+  }
+  PutArgs t = a;
+  const Seg &ls = a.seg[a.nseg - 1];
+  t.nseg = 1;
+  t.seg[0].src = ls.src + ls.len - 1;
+  t.seg[0].dst_off = a.total - 1;
+  t.seg[0].len = 1;
+  t.wait_empty = 0;
+  k_put<4><<<1, 32, 0, s->s>>>(t);
+  return launch_check("k_put(tail)");
 }
 
 // ---------------------------------------------------------------------------
@@ -1596,6 +1630,10 @@ int srf_tune(int knob, int value) {
       cudaSetDevice(cur);
       return SRF_OK;
     }
+    case 6:
+      if (value < 0) return fail(SRF_E_INVALID_CONFIG, "peer_ce_kib >= 0");
+      g_peer_ce_bytes = (uint64_t)value << 10;
+      return SRF_OK;
     default:
       return fail(SRF_E_INVALID_CONFIG, "unknown knob %d", knob);
   }
@@ -2092,7 +2130,11 @@ int srf_put(srf_space_t src_space, const uint64_t *src_addr,
   a.counter = s->counter;
   a.err = src_space->err;
   CUDA_TRY(cudaSetDevice(s->device));
-  int rc = launch_copy(a, s, "k_put");
+  int rc;
+  if (a.sys_scope && g_peer_ce_bytes && total - 1 >= g_peer_ce_bytes && a.db_len <= 1)
+    rc = put_via_copy_engine(a, s);
+  else
+    rc = launch_copy(a, s, "k_put");
   if (rc) return rc;
   return record_event(s->device, s->s, ev_out);
 }
@@ -2124,7 +2166,12 @@ int srf_get(srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
   a.counter = s->counter;
   a.err = dst_space->err;
   CUDA_TRY(cudaSetDevice(s->device));
-  int rc = launch_copy(a, s, "k_put(get)");
+  int rc = SRF_OK;
+  const bool cross = src_space->imported || src_space->device != s->device;
+  if (cross && g_peer_ce_bytes && length >= g_peer_ce_bytes)
+    CUDA_TRY(cudaMemcpyAsync(a.dst, a.seg[0].src, length, cudaMemcpyDeviceToDevice, s->s));
+  else
+    rc = launch_copy(a, s, "k_put(get)");
   if (rc) return rc;
   return record_event(s->device, s->s, ev_out);
 }

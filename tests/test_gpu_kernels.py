@@ -183,7 +183,37 @@ def test_flag_wait_and_timeout(pair):
         b.sync()
 
 
-def test_release_acquire_stress(pair):
+@pytest.fixture(params=["sm", "copy_engine"])
+def peer_engine(request):
+    """Cross-device bodies by SM stores, or by the copy engine (knob 6) with
+    the flag released by an SM store after them."""
+    _lib.tune("peer_ce_kib", 0 if request.param == "sm" else 1)
+    yield request.param
+    _lib.tune("peer_ce_kib", 1024)
+
+
+@pytest.mark.parametrize("size", [1025, 4097, (1 << 20) + 3, (8 << 20) + 8])
+@pytest.mark.parametrize("soff,doff", [(0, 0), (3, 5)])
+def test_copy_engine_put_and_get_bit_exact(pair, peer_engine, size, soff, doff):
+    a, b, ra, rb = pair
+    data = rand_bytes(size, size)
+    flag = rand_bytes(1, 5)
+    src = ra.base_addr + 4096 + soff
+    a.write_raw(src, data)
+    a.write_raw(ra.base_addr + 64, flag)
+    dst = rb.base_addr + 4096 + doff
+    put(a, [(src, size, ra.access_token), (ra.base_addr + 64, 1, ra.access_token)], b, dst,
+        rb.access_token)
+    assert b.read_raw(dst, size + 1) == data.tobytes() + flag.tobytes()
+    back = ra.base_addr + (48 << 20) + doff
+    ev = C.c_void_p()
+    _lib.call("srf_get", a.handle, back, ra.access_token, b.handle, dst, rb.access_token,
+              size, None, C.byref(ev))
+    _lib.Event(ev).wait()
+    assert a.read_raw(back, size) == data.tobytes()
+
+
+def test_release_acquire_stress(pair, peer_engine):
     """>= 1000 trials: a consumer kernel acquire-spins on the tail flag and
     checksums the payload it guards; any payload byte landing after the flag
     shows up as a checksum mismatch.  With two GPUs the consumer is launched

@@ -32,6 +32,7 @@ lives on rank ``server % world``; all of a rank's servers share its GPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -47,16 +48,24 @@ from .workloads import ps_node_ids
 _NONE = (1 << 64) - 1
 
 
+#: block alignment (power of two >= 32; SRFLOW_PS_ALIGN for experiments).
+#: 256 B keeps every warp's 32-B vectors inside whole 128-B lines of a peer's
+#: pool: the fused pull + apply went 643 -> 748 GB/s over NVLink at N=2 vs 32 B
+#: (profiles/r1_ps_phase_probe.jsonl)
+_BLOCK_ALIGN = int(os.environ.get("SRFLOW_PS_ALIGN", "256"))
+
+
 def _r16(n: int) -> int:
-    """Block size rounded to 32 B: blocks stay co-aligned for 32-B vectors."""
-    return (n + 31) & ~31
+    """Block size rounded to the block alignment (>= 32 B, so blocks stay
+    co-aligned for 32-B vectors)."""
+    return (n + _BLOCK_ALIGN - 1) & ~(_BLOCK_ALIGN - 1)
 
 
 @dataclass
 class PsLayout:
     """Deterministic per-server memory layout (pure host logic).
 
-    Every block is a 32-B aligned slice of the server's one registered arena,
+    Every block is a 256-B aligned slice of the server's one registered arena,
     allocated in a fixed order, so every rank can derive every peer's
     coordinates; the exchanged region tables (tokens) validate them.
     """

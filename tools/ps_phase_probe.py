@@ -1,0 +1,87 @@
+"""Per-phase device time of the PS step on every rank (torchrun): events
+between the phase launches on the rank's stream, averaged over R steps.
+A phase's time includes its spins on flags other GPUs set."""
+import ctypes as C
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import bench
+from paper_1805_08430_b200 import _lib
+from paper_1805_08430_b200.distributed import init_process_group
+from paper_1805_08430_b200.ps import PsLayout, PsStep
+from paper_1805_08430_b200.workloads import vgg16_shapes
+
+rank, world, local = init_process_group("nccl")
+torch.cuda.set_device(local)
+balanced = os.environ.get("PROBE_PLACEMENT", "round_robin")
+L = PsLayout(vgg16_shapes(), world, world, colocate=True, placement=balanced)
+mode = os.environ.get("PROBE_MODE", "phases")
+if mode != "phases":
+    # whole-step wall time of the eager or overlapped schedule, max over ranks
+    import time
+    ps = PsStep(L, rank=rank, world=world, device=local, seed=0, op="sgd", lr=0.01,
+                overlap=(mode == "overlap"))
+    if os.environ.get("PROBE_CAP"):
+        ps._cap = int(os.environ["PROBE_CAP"])
+    for it in range(1, 6):
+        ps.step(it)
+    ps.sync()
+    bench.barrier_sync()
+    t0 = time.perf_counter()
+    R = 40
+    for it in range(6, 6 + R):
+        ps.step(it)
+    ps.sync()
+    bench.barrier_sync()
+    dt = bench.dist_max(time.perf_counter() - t0) / R
+    if rank == 0:
+        print(json.dumps({"mode": mode, "cap": getattr(ps, "_cap", None),
+                          "placement": balanced, "step_us": round(dt * 1e6, 1),
+                          "knobs": {k: v for k, v in os.environ.items()
+                                    if k.startswith("SRFLOW_")}}), flush=True)
+    ps.close()
+    sys.exit(0)
+ps = PsStep(L, rank=rank, world=world, device=local, seed=0, op="sgd", lr=0.01)
+sp = ps.stream_space
+names = ["push", "gen", "meta", "apply"]
+ev = []
+for _ in range(len(names) + 1):
+    e = C.c_void_p()
+    _lib.call("srf_timing_event_create", sp.handle, C.byref(e))
+    ev.append(e)
+R = 20
+acc = {n: 0.0 for n in names}
+acc["step"] = 0.0
+b = ps.batches
+for it in range(1, R + 6):
+    bench.barrier_sync()
+    _lib.call("srf_event_record_on", ev[0], ps.stream)
+    _lib.call("srf_batch_launch", b["push"], ps.stream, it, 0, 0) if b["push"] else None
+    _lib.call("srf_event_record_on", ev[1], ps.stream)
+    for g in b["gen"].values():
+        _lib.call("srf_batch_launch", g, ps.stream, it, 1, 0)
+    _lib.call("srf_event_record_on", ev[2], ps.stream)
+    if b["meta"]:
+        _lib.call("srf_batch_launch", b["meta"], ps.stream, it, 0, 0)
+    _lib.call("srf_event_record_on", ev[3], ps.stream)
+    for a in b["apply"].values():
+        _lib.call("srf_batch_launch", a, ps.stream, it, 0, 0)
+    _lib.call("srf_event_record_on", ev[4], ps.stream)
+    _lib.call("srf_stream_sync", ps.stream)
+    if it > 5:
+        for i, n in enumerate(names):
+            f = C.c_float()
+            _lib.call("srf_event_elapsed_ms", ev[i], ev[i + 1], C.byref(f))
+            acc[n] += f.value / R
+        f = C.c_float()
+        _lib.call("srf_event_elapsed_ms", ev[0], ev[4], C.byref(f))
+        acc["step"] += f.value / R
+out = {"rank": rank, "placement": balanced, "knobs": {k: v for k, v in os.environ.items()
+                                                      if k.startswith("SRFLOW_")},
+       **{k: round(v * 1000, 1) for k, v in acc.items()}}
+print(json.dumps(out), flush=True)
+ps.close()

@@ -738,39 +738,51 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
     for e in ev:
         _lib.call("srf_timing_event_create", sp0.handle, C.byref(e))
     persistent = False
+
+    # schedule autotune on a short sample (max over ranks): per-phase launches,
+    # one exchange launch per step (dependency-ordered unit queue), and at N=1
+    # one persistent cooperative launch (grid barriers between phases)
+    def sample(fn, n=5):
+        barrier_sync()
+        _lib.call("srf_event_record_on", ev[0], ps.stream)
+        fn(n)
+        _lib.call("srf_event_record_on", ev[1], ps.stream)
+        ps.sync()
+        t_ = C.c_float()
+        _lib.call("srf_event_elapsed_ms", ev[0], ev[1], C.byref(t_))
+        return dist_max(t_.value)
+
+    def eager(n):
+        nonlocal it
+        for _ in range(n):
+            it += 1
+            ps.step(it)
+
+    def pers(n):
+        nonlocal it
+        ps.run_persistent(it + 1, n)
+        it += n
+
+    times = {}
+    for name in ("phases", "exchange"):
+        ps.use_schedule(name)
+        eager(2)
+        times[name] = sample(eager)
     if world == 1:
-        # schedule autotune on a short sample: per-phase launches vs one
-        # persistent cooperative launch (grid barriers between phases)
-        def sample(fn, n=5):
-            _lib.call("srf_event_record_on", ev[0], ps.stream)
-            fn(n)
-            _lib.call("srf_event_record_on", ev[1], ps.stream)
-            ps.sync()
-            t_ = C.c_float()
-            _lib.call("srf_event_elapsed_ms", ev[0], ev[1], C.byref(t_))
-            return t_.value
-
-        def eager(n):
-            nonlocal it
-            for _ in range(n):
-                it += 1
-                ps.step(it)
-
-        def pers(n):
-            nonlocal it
-            ps.run_persistent(it + 1, n)
-            it += n
-
-        t_pers, t_eager = sample(pers), sample(eager)
-        persistent = t_pers < t_eager
-        # latency-bound configs: enough iterations for a timed region of ~0.3 s
-        per_iter_s = min(t_pers, t_eager) / 5 / 1e3
-        steps = int(max(steps, min(20000, 0.3 / max(per_iter_s, 1e-7))))
+        ps.use_schedule("phases")
+        times["persistent"] = sample(pers)
+    best = min(times, key=times.get)
+    persistent = best == "persistent"
+    ps.use_schedule("exchange" if best == "exchange" else "phases")
+    # latency-bound configs: enough iterations for a timed region of ~0.3 s
+    per_iter_s = times[best] / 5 / 1e3
+    steps = int(max(steps, min(20000, 0.3 / max(per_iter_s, 1e-7))))
     clocks = ClockSampler(device)
     clocks.start()
     barrier_sync()
     graph = None
-    if not ps.overlap and os.environ.get("SRFLOW_PS_GRAPH") == "1":
+    if (not ps.overlap and ps.schedule == "phases" and not persistent
+            and os.environ.get("SRFLOW_PS_GRAPH") == "1"):
         # optional: replay the timed iterations as one CUDA graph (the gen batch
         # takes the iteration from a device counter).  Measured slower than
         # eager launches on B200 (MLP 23.8k vs 29.6k it/s), so off by default.
@@ -885,7 +897,11 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
            "schedule": ("overlapped (3 streams, capped grids)" if ps.overlap else
                         "one stream, CUDA graph" if graph is not None else
                         "one persistent cooperative launch (grid barriers between phases)"
-                        if persistent else "one stream, one launch per phase")}
+                        if persistent else
+                        "exchange: one k_ps_exchange launch per step (dependency-ordered "
+                        "unit queue, meta fused into GenGrad)" if ps.schedule == "exchange"
+                        else "one stream, one launch per phase"),
+           "autotune_ms_per_5": {k: round(v, 3) for k, v in times.items()}}
     ps.close()
     if cpu and rank == 0 and world == 1:
         rig = cpu_rig() if cpu_rig else port.PsRig(shapes, L.workers, L.shards, L.colocate,

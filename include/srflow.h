@@ -270,6 +270,24 @@ int srf_ps_persistent(srf_batch_t push, srf_batch_t gen, srf_batch_t meta,
                       srf_batch_t const *apply, int napply, srf_stream_t stream, uint64_t it0,
                       uint32_t iters, int mode);
 
+/* Exchange schedule: one launch per PS iteration in which persistent CTAs
+ * claim the work units of this GPU's push, gen and apply batches from ONE
+ * queue ordered by a per-edge key (every rank derives the same keys from the
+ * variable, e.g. push(v) < gen(v) < apply(v) < ...).  A unit waits only on
+ * units earlier in that global order, so any grid makes progress, and a shard
+ * pulls variable v while later weights are still in flight.  The gen batch
+ * must carry its metadata puts (srf_batch_gen_set_meta: gen edge
+ * gen_index[i] sends meta edge i from its last CTA - DynSender.send after the
+ * producer, runtime/protocol.py:163-201). */
+typedef struct srf_exchange *srf_exchange_t;
+int srf_batch_gen_set_meta(srf_batch_t gen, int n, const int *gen_index, srf_batch_t meta);
+int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch_t gen,
+                           const uint64_t *gen_key, srf_batch_t const *apply, int napply,
+                           const uint64_t *apply_key, srf_exchange_t *out);
+int srf_ps_exchange_launch(srf_exchange_t exchange, srf_stream_t stream, uint64_t iteration,
+                           int regen);
+int srf_ps_exchange_destroy(srf_exchange_t exchange);
+
 /* RPC-style serialize/copy baseline (runtime/protocol.py:257-448) on the
  * device - the comparator the north star reports zero-copy against.  The
  * stream metadata||payload moves in 4096-B fragments (16-B header + 4080 B)

@@ -1053,6 +1053,12 @@ struct BatchGen {        // worker: consume weight, (re)produce gradient
   const uint8_t *credit; // shard-side meta tail that must read 0 (nullptr: none)
   uint64_t node;         // GenGrad node id (RNG stream key)
   uint32_t cta_begin, cta_count;
+  // K3 fused into the gen's last CTA (exchange schedule): the DynSender.send
+  // of this gradient's metadata block (nullptr: none / separate meta batch)
+  const uint8_t *meta_src;
+  uint8_t *meta_dst;
+  const uint8_t *meta_tail;
+  uint64_t meta_body;
 };
 
 struct BatchApply {      // shard: fused dynamic receive (meta decode + peer
@@ -1094,11 +1100,13 @@ __device__ __forceinline__ bool spin_until(const uint8_t *p, uint32_t want,
   return true;
 }
 
-__device__ __forceinline__ void put_batch_units(const BatchPut *descs, int n,
-                                                uint32_t total_units, unsigned int *counters,
-                                                uint64_t timeout_ns, int *err, int sys) {
+// One work unit (a CTA-sized slice of one descriptor) of each batch kind; the
+// batch kernels loop over units, the exchange kernel claims them from a queue.
+__device__ __forceinline__ void put_unit(const BatchPut *descs, int n, uint32_t u,
+                                         unsigned int *counters, uint64_t timeout_ns, int *err,
+                                         int sys) {
   __shared__ int s_desc, s_last;
-  for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x) {
+  {
     if (threadIdx.x == 0) s_desc = find_desc(descs, n, u);
     __syncthreads();
     const BatchPut d = descs[s_desc];
@@ -1119,6 +1127,13 @@ __device__ __forceinline__ void put_batch_units(const BatchPut *descs, int n,
     }
     __syncthreads();  // shared state is reused by the next unit
   }
+}
+
+__device__ __forceinline__ void put_batch_units(const BatchPut *descs, int n,
+                                                uint32_t total_units, unsigned int *counters,
+                                                uint64_t timeout_ns, int *err, int sys) {
+  for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x)
+    put_unit(descs, n, u, counters, timeout_ns, err, sys);
 }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
@@ -1144,16 +1159,12 @@ __device__ __forceinline__ float unit_f32(uint32_t k0, uint32_t k1, uint32_t i) 
   return (float)((fmix32(i * 0x9E3779B1u + k0) ^ k1) >> 8) * (1.0f / 16777216.0f);
 }
 
-__device__ __forceinline__ void gen_batch_units(const BatchGen *descs, int n,
-                                                uint32_t total_units, unsigned int *counters,
-                                                uint64_t seed, uint64_t iteration_arg,
-                                                const uint64_t *iteration_ptr, int regen,
-                                                uint64_t timeout_ns, int *err, int sys) {
-  // iteration from a device counter when given (graph-replayed steps)
-  const uint64_t iteration = iteration_ptr ? *(const volatile uint64_t *)iteration_ptr
-                                           : iteration_arg;
+__device__ __forceinline__ void gen_unit(const BatchGen *descs, int n, uint32_t u,
+                                         unsigned int *counters, uint64_t seed,
+                                         uint64_t iteration, int regen, int fuse_meta,
+                                         uint64_t timeout_ns, int *err, int sys) {
   __shared__ int s_desc, s_last;
-  for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x) {
+  {
     if (threadIdx.x == 0) s_desc = find_desc(descs, n, u);
     __syncthreads();
     const BatchGen d = descs[s_desc];
@@ -1185,19 +1196,36 @@ __device__ __forceinline__ void gen_batch_units(const BatchGen *descs, int n,
     if (s_last && threadIdx.x == 0) {
       // the weight was consumed: clear its flag (StaticReceiver.poll semantics)
       if (d.weight_flag) release_tail(d.weight_flag, 0, sys);
+      if (fuse_meta && d.meta_dst) {
+        // K3: the gradient's metadata block, flag last; the acq_rel arrival
+        // above made every CTA's gradient stores visible before this release
+        for (uint64_t k = 0; k < d.meta_body; ++k) d.meta_dst[k] = d.meta_src[k];
+        release_tail(d.meta_dst + d.meta_body, *d.meta_tail, sys);
+      }
       atomicExch(&counters[s_desc], 0u);
     }
     __syncthreads();  // shared state is reused by the next unit
   }
 }
 
-__device__ __forceinline__ void apply_batch_units(const BatchApply *descs, int n,
-                                                  uint32_t total_units, unsigned int *counters,
-                                                  int op, float lr, uint64_t timeout_ns,
-                                                  int *err, int sys) {
+__device__ __forceinline__ void gen_batch_units(const BatchGen *descs, int n,
+                                                uint32_t total_units, unsigned int *counters,
+                                                uint64_t seed, uint64_t iteration_arg,
+                                                const uint64_t *iteration_ptr, int regen,
+                                                uint64_t timeout_ns, int *err, int sys) {
+  // iteration from a device counter when given (graph-replayed steps)
+  const uint64_t iteration = iteration_ptr ? *(const volatile uint64_t *)iteration_ptr
+                                           : iteration_arg;
+  for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x)
+    gen_unit(descs, n, u, counters, seed, iteration, regen, 0, timeout_ns, err, sys);
+}
+
+__device__ __forceinline__ void apply_unit(const BatchApply *descs, int n, uint32_t u,
+                                           unsigned int *counters, int op, float lr,
+                                           uint64_t timeout_ns, int *err, int sys) {
   __shared__ int s_desc, s_last, s_bad;
   __shared__ const uint8_t *s_g[SRF_MAX_WORKERS];
-  for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x) {
+  {
     if (threadIdx.x == 0) {
       s_desc = find_desc(descs, n, u);
       s_bad = 0;
@@ -1253,6 +1281,14 @@ __device__ __forceinline__ void apply_batch_units(const BatchApply *descs, int n
     if (s_last && threadIdx.x == 0) atomicExch(&counters[s_desc], 0u);
     __syncthreads();  // shared state is reused by the next unit
   }
+}
+
+__device__ __forceinline__ void apply_batch_units(const BatchApply *descs, int n,
+                                                  uint32_t total_units, unsigned int *counters,
+                                                  int op, float lr, uint64_t timeout_ns,
+                                                  int *err, int sys) {
+  for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x)
+    apply_unit(descs, n, u, counters, op, lr, timeout_ns, err, sys);
 }
 
 
@@ -1313,6 +1349,55 @@ __global__ void __launch_bounds__(256) k_ps_persistent(const __grid_constant__ P
   }
 }
 
+
+// Dependency-driven PS step (the exchange schedule): every unit of this GPU's
+// push, gen (+ fused meta) and apply batches sits in one queue, ordered by a
+// key every rank derives from the variable, and persistent CTAs claim units
+// in queue order with one atomic.  A unit only waits on units that precede it
+// in that global order (weights before their gradient, gradients before their
+// apply, the previous step before this one), so the earliest unfinished unit
+// can always run: no deadlock whatever the grid, and a shard starts pulling
+// variable v while its later weights are still being pushed.
+struct ExItem {
+  uint32_t unit;
+  uint16_t kind;   // 0 push, 1 gen, 2 apply
+  uint16_t batch;  // apply batch index
+};
+
+struct ExArgs {
+  const BatchPut *push; int npush; unsigned int *cpush; int push_sys;
+  const BatchGen *gen; int ngen; unsigned int *cgen; uint64_t seed; int gen_sys;
+  const BatchApply *apply[kMaxApply]; int napply[kMaxApply]; unsigned int *capply[kMaxApply];
+  int apply_sys[kMaxApply];
+  int op; float lr;
+  const ExItem *items; uint32_t nitems; unsigned int *claim; unsigned int *exit_count;
+  uint64_t iteration; int regen; uint64_t timeout_ns; int *err;
+};
+
+__global__ void __launch_bounds__(512) k_ps_exchange(const __grid_constant__ ExArgs a) {
+  __shared__ uint32_t s_i;
+  for (;;) {
+    if (threadIdx.x == 0) s_i = atomicAdd(a.claim, 1u);
+    __syncthreads();
+    const uint32_t i = s_i;
+    __syncthreads();
+    if (i >= a.nitems) break;
+    const ExItem x = a.items[i];
+    if (x.kind == 0)
+      put_unit(a.push, a.npush, x.unit, a.cpush, a.timeout_ns, a.err, a.push_sys);
+    else if (x.kind == 1)
+      gen_unit(a.gen, a.ngen, x.unit, a.cgen, a.seed, a.iteration, a.regen, 1, a.timeout_ns,
+               a.err, a.gen_sys);
+    else
+      apply_unit(a.apply[x.batch], a.napply[x.batch], x.unit, a.capply[x.batch], a.op, a.lr,
+                 a.timeout_ns, a.err, a.apply_sys[x.batch]);
+  }
+  // the last CTA out re-arms the queue for the next launch
+  if (threadIdx.x == 0 && atomicAdd(a.exit_count, 1u) == gridDim.x - 1) {
+    *a.claim = 0;
+    *a.exit_count = 0;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // RPC-style baseline on the device (runtime/protocol.py:257-448, FORMATS.md
@@ -2321,6 +2406,7 @@ struct srf_batch {
   std::vector<std::pair<std::pair<uint8_t *, const uint8_t *>, uint64_t>> ce_copies;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::vector<uint8_t> host;  // host copy of the descriptors
 };
 
 static uint32_t ctas_for(int device, uint64_t bytes, uint64_t per_cta) {
@@ -2346,6 +2432,7 @@ static int finish_batch(int kind, int device, std::vector<D> &host, int *err, sr
   uint32_t total = 0;
   for (auto &d : host) total = d.cta_begin + d.cta_count;
   b->grid = (int)total;
+  b->host.assign((const uint8_t *)host.data(), (const uint8_t *)(host.data() + host.size()));
   CUDA_TRY(cudaSetDevice(device));
   cudaError_t e = cudaMalloc(&b->descs, sizeof(D) * std::max<size_t>(1, host.size()));
   if (e == cudaSuccess && !host.empty())
@@ -2700,6 +2787,26 @@ int srf_ps_persistent(srf_batch_t push, srf_batch_t gen, srf_batch_t meta,
   return launch_check("k_ps_persistent");
 }
 
+int srf_batch_gen_set_meta(srf_batch_t gen, int n, const int *gen_index, srf_batch_t meta) {
+  if (!gen || gen->kind != 1 || !meta || meta->kind != 0 || n != meta->n)
+    return fail(SRF_E_INVALID_CONFIG, "gen_set_meta: a gen batch and a put batch of n edges");
+  BatchGen *g = (BatchGen *)gen->host.data();
+  const BatchPut *m = (const BatchPut *)meta->host.data();
+  for (int i = 0; i < n; ++i) {
+    if (gen_index[i] < 0 || gen_index[i] >= gen->n)
+      return fail(SRF_E_INVALID_CONFIG, "gen_set_meta: index %d out of range", gen_index[i]);
+    BatchGen &d = g[gen_index[i]];
+    d.meta_src = m[i].src;
+    d.meta_dst = m[i].dst;
+    d.meta_tail = m[i].tail;
+    d.meta_body = m[i].body;
+  }
+  gen->sys |= meta->sys;
+  CUDA_TRY(cudaSetDevice(gen->device));
+  CUDA_TRY(cudaMemcpy(gen->descs, gen->host.data(), gen->host.size(), cudaMemcpyHostToDevice));
+  return SRF_OK;
+}
+
 int srf_batch_destroy(srf_batch_t b) {
   if (!b) return SRF_OK;
   cudaSetDevice(b->device);
@@ -2715,6 +2822,128 @@ int srf_batch_destroy(srf_batch_t b) {
   if (b->ev_fork) cudaEventDestroy(b->ev_fork);
   if (b->ev_join) cudaEventDestroy(b->ev_join);
   delete b;
+  return SRF_OK;
+}
+
+// ---------------------------------------------------------------------------
+// exchange schedule (k_ps_exchange)
+// ---------------------------------------------------------------------------
+struct srf_exchange {
+  int device;
+  ExArgs args;
+  ExItem *items = nullptr;
+  unsigned int *ctr = nullptr;  // [claim, exit_count]
+  int grid = 0;
+};
+
+int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch_t gen,
+                           const uint64_t *gen_key, srf_batch_t const *apply, int napply,
+                           const uint64_t *apply_key, srf_exchange_t *out) {
+  if (napply < 0 || napply > kMaxApply)
+    return fail(SRF_E_INVALID_CONFIG, "at most %d apply batches", kMaxApply);
+  if ((push && push->kind != 0) || (gen && gen->kind != 1))
+    return fail(SRF_E_INVALID_CONFIG, "exchange: batch kinds");
+  if (push && push->ce_n)
+    return fail(SRF_E_INVALID_CONFIG, "exchange: copy-engine put batches are not queued");
+  int device = push ? push->device : gen ? gen->device : napply ? apply[0]->device : -1;
+  if (device < 0) return fail(SRF_E_INVALID_CONFIG, "exchange: no batches");
+  struct K { uint64_t key; uint32_t kind, batch, desc, unit; };
+  std::vector<K> ks;
+  auto add = [&](srf_batch *b, const uint64_t *key, uint32_t kind, uint32_t batch) -> int {
+    if (!b) return SRF_OK;
+    if (b->device != device) return fail(SRF_E_INVALID_CONFIG, "exchange spans GPUs");
+    for (int i = 0; i < b->n; ++i) {
+      uint32_t begin, count;
+      if (kind == 0) {
+        const BatchPut &d = ((const BatchPut *)b->host.data())[i];
+        begin = d.cta_begin; count = d.cta_count;
+      } else if (kind == 1) {
+        const BatchGen &d = ((const BatchGen *)b->host.data())[i];
+        begin = d.cta_begin; count = d.cta_count;
+        if (d.credit && !d.meta_dst)
+          return fail(SRF_E_INVALID_CONFIG, "exchange: gen edge %d has no fused meta", i);
+      } else {
+        const BatchApply &d = ((const BatchApply *)b->host.data())[i];
+        begin = d.cta_begin; count = d.cta_count;
+      }
+      for (uint32_t u = 0; u < count; ++u) ks.push_back({key[i], kind, batch, (uint32_t)i, begin + u});
+    }
+    return SRF_OK;
+  };
+  int rc = add(push, push_key, 0, 0);
+  if (!rc) rc = add(gen, gen_key, 1, 0);
+  uint64_t off = 0;
+  for (int b = 0; !rc && b < napply; ++b) {
+    if (apply[b]->kind != 2) return fail(SRF_E_INVALID_CONFIG, "exchange: batch kinds");
+    rc = add(apply[b], apply_key + off, 2, (uint32_t)b);
+    off += apply[b]->n;
+  }
+  if (rc) return rc;
+  std::stable_sort(ks.begin(), ks.end(), [](const K &x, const K &y) {
+    if (x.key != y.key) return x.key < y.key;
+    if (x.kind != y.kind) return x.kind < y.kind;
+    if (x.batch != y.batch) return x.batch < y.batch;
+    return x.desc < y.desc;
+  });
+  std::vector<ExItem> items(ks.size());
+  for (size_t i = 0; i < ks.size(); ++i)
+    items[i] = {ks[i].unit, (uint16_t)ks[i].kind, (uint16_t)ks[i].batch};
+  srf_exchange *x = new srf_exchange();
+  x->device = device;
+  memset(&x->args, 0, sizeof x->args);
+  ExArgs &a = x->args;
+  if (push) { a.push = (const BatchPut *)push->descs; a.npush = push->n; a.cpush = push->counters; a.push_sys = push->sys; }
+  if (gen) { a.gen = (const BatchGen *)gen->descs; a.ngen = gen->n; a.cgen = gen->counters; a.seed = gen->seed; a.gen_sys = gen->sys; }
+  for (int b = 0; b < napply; ++b) {
+    a.apply[b] = (const BatchApply *)apply[b]->descs;
+    a.napply[b] = apply[b]->n;
+    a.capply[b] = apply[b]->counters;
+    a.apply_sys[b] = apply[b]->sys;
+    a.op = apply[b]->op;
+    a.lr = apply[b]->lr;
+  }
+  a.err = push ? push->err : gen ? gen->err : apply[0]->err;
+  a.nitems = (uint32_t)items.size();
+  a.timeout_ns = 10ull * 1000 * 1000 * 1000;
+  CUDA_TRY(cudaSetDevice(device));
+  cudaError_t e = cudaMalloc(&x->items, sizeof(ExItem) * std::max<size_t>(1, items.size()));
+  if (e == cudaSuccess && !items.empty())
+    e = cudaMemcpy(x->items, items.data(), sizeof(ExItem) * items.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&x->ctr, 2 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(x->ctr, 0, 2 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  int per_sm = 0;
+  if (e == cudaSuccess)
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ps_exchange, 512, 0);
+  if (e != cudaSuccess) {
+    cudaFree(x->items);
+    cudaFree(x->ctr);
+    delete x;
+    return fail(SRF_E_DEVICE, "exchange: %s", cudaGetErrorString(e));
+  }
+  a.items = x->items;
+  a.claim = x->ctr;
+  a.exit_count = x->ctr + 1;
+  x->grid = sm_count_of(device) * std::max(1, per_sm);
+  *out = x;
+  return SRF_OK;
+}
+
+int srf_ps_exchange_launch(srf_exchange_t x, srf_stream_t st, uint64_t iteration, int regen) {
+  if (st->device != x->device) return fail(SRF_E_INVALID_CONFIG, "exchange: stream GPU");
+  x->args.iteration = iteration;
+  x->args.regen = regen;
+  CUDA_TRY(cudaSetDevice(x->device));
+  k_ps_exchange<<<x->grid, 512, 0, st->s>>>(x->args);
+  return launch_check("k_ps_exchange");
+}
+
+int srf_ps_exchange_destroy(srf_exchange_t x) {
+  if (!x) return SRF_OK;
+  cudaSetDevice(x->device);
+  cudaFree(x->items);
+  cudaFree(x->ctr);
+  delete x;
   return SRF_OK;
 }
 

@@ -195,7 +195,8 @@ class PsStep:
 
     def __init__(self, layout: PsLayout, *, rank: int = 0, world: int = 1, device: int = 0,
                  seed: int = 0, op: str = "xor", lr: float = 0.01,
-                 overlap: Optional[bool] = None):
+                 overlap: Optional[bool] = None, schedule: str = "phases",
+                 exchange_lag: Optional[int] = None, exchange_order: Optional[str] = None):
         self.L = layout
         self.rank, self.world, self.device = rank, world, device
         self.seed = seed
@@ -257,6 +258,15 @@ class PsStep:
         # transfer.  Off by default; finer-grained flags would be needed.
         one_server = len(self.local) == 1 and layout.colocate and world > 1
         self.overlap = bool(overlap) and one_server
+        self._exchange = None
+        self._exchange_built = None
+        self._exchange_cfg = (
+            int(os.environ.get("SRFLOW_PS_EXCHANGE_LAG", 1) if exchange_lag is None
+                else exchange_lag),
+            (os.environ.get("SRFLOW_PS_EXCHANGE_ORDER", "index") if exchange_order is None
+             else exchange_order))
+        self.schedule = "phases"
+        self.use_schedule(schedule)
         if self.overlap:
             sp = self.stream_space
             self._streams = []
@@ -326,6 +336,8 @@ class PsStep:
         L = self.L
         P, u64 = C.c_void_p, _lib.u64_array
         out = {}
+        # variable of every edge, per batch (exchange keys)
+        self._rows = {"push": [], "gen": [], "meta": [], "apply": {}}
         # 1. weight pushes (K1), credit-gated
         rows = []
         for s in self.local:
@@ -337,6 +349,7 @@ class PsStep:
                         continue
                     rows.append((s, self.addr(s, ("var", v)), L.nbytes(v), self.token(s),
                                  self.addr(s, "flag"), w, self.addr(w, ("wbuf", v)), self.token(w)))
+                    self._rows["push"].append(v)
         out["push"] = self._put_batch(rows, _lib.PUT_WAIT_EMPTY)
         # 2. worker gen batch
         g_rows = []
@@ -352,6 +365,7 @@ class PsStep:
                                self.space(sh).handle.value if remote else None,
                                self.addr(sh, ("mslot", v, w)) + mlen - 1 if remote else _NONE,
                                ps_node_ids(len(L.shapes), L.workers, v, w)[1], w))
+                self._rows["gen"].append((w, v))
         out["gen"] = {}
         if g_rows:
             b = C.c_void_p()
@@ -376,6 +390,7 @@ class PsStep:
                 rows.append((w, self.addr(w, ("mstage", v)), mlen - 1, self.token(w),
                              self.addr(w, ("mstage", v)) + mlen - 1, sh,
                              self.addr(sh, ("mslot", v, w)), self.token(sh)))
+                self._rows["meta"].append((w, v))
         out["meta"] = self._put_batch(rows, 0)
         # 4. fused pull + apply per shard
         out["apply"] = {}
@@ -383,6 +398,7 @@ class PsStep:
             vs = [v for v in range(len(L.shapes)) if L.shard_of(v) == s]
             if not vs:
                 continue
+            self._rows["apply"][s] = vs
             srcsp, srcad, ismeta, peersp, lo, hi, tok = [], [], [], [], [], [], []
             for v in vs:
                 for w in range(L.workers):
@@ -425,12 +441,62 @@ class PsStep:
                   u64(r[6] for r in rows), u64(r[7] for r in rows), flags, C.byref(b))
         return b
 
+    def use_schedule(self, schedule: str) -> None:
+        """Switch between the per-phase launches and the exchange launch (both
+        use the same flags and credits, so they can alternate step by step)."""
+        if schedule not in ("phases", "exchange"):
+            raise errors.InvalidConfig(f"unknown PS schedule {schedule!r}")
+        if schedule == "exchange":
+            if self.overlap:
+                raise errors.InvalidConfig("the exchange schedule is one launch per step")
+            if self._exchange_built is None:
+                self._exchange_built = self._build_exchange(*self._exchange_cfg)
+            self._exchange = self._exchange_built
+        else:
+            self._exchange = None
+        self.schedule = schedule
+
+    def _build_exchange(self, lag: int, order: str):
+        """One queue of this GPU's units (k_ps_exchange).  Keys are a global
+        order every rank derives alike: push(v) < gen(v) < apply(v), the
+        apply of a variable placed ``lag`` variables later so the next
+        weights are already moving while its gradients are awaited."""
+        L, b, rows = self.L, self.batches, self._rows
+        u64 = _lib.u64_array
+        nv = len(L.shapes)
+        if order == "index":
+            seq = list(range(nv))
+        elif order == "size":  # largest first: the longest push -> pull chain starts first
+            seq = sorted(range(nv), key=lambda v: (-L.nbytes(v), v))
+        else:
+            raise errors.InvalidConfig(f"unknown exchange order {order!r}")
+        pos = {v: i for i, v in enumerate(seq)}
+        gen = next(iter(b["gen"].values()), None)
+        if b["meta"] is not None:
+            index = {wv: i for i, wv in enumerate(rows["gen"])}
+            gi = (C.c_int * len(rows["meta"]))(*[index[wv] for wv in rows["meta"]])
+            _lib.call("srf_batch_gen_set_meta", gen, len(rows["meta"]), gi, b["meta"])
+        applies = list(b["apply"].items())
+        x = C.c_void_p()
+        _lib.call("srf_ps_exchange_create",
+                  b["push"], u64(4 * pos[v] for v in rows["push"]) if rows["push"] else None,
+                  gen, u64(4 * pos[v] + 1 for _w, v in rows["gen"]) if rows["gen"] else None,
+                  (C.c_void_p * max(1, len(applies)))(*[a.value for _s, a in applies]),
+                  len(applies),
+                  u64(4 * (pos[v] + lag) + 2 for s, _a in applies for v in rows["apply"][s])
+                  if applies else None,
+                  C.byref(x))
+        return x
+
     # -- running --------------------------------------------------------------------------
 
     def step(self, iteration: int, regen: bool = True) -> int:
         """Queue one PS iteration; returns the number of kernel launches."""
         b, n = self.batches, 0
         mode = 1 if regen else 0
+        if self._exchange is not None:
+            _lib.call("srf_ps_exchange_launch", self._exchange, self.stream, iteration, mode)
+            return 1
         if self.overlap:
             return self._step_overlapped(iteration, mode)
         if b["push"] is not None:
@@ -472,6 +538,8 @@ class PsStep:
         return n
 
     def launches_per_step(self) -> int:
+        if self._exchange is not None:
+            return 1
         b = self.batches
         return ((b["push"] is not None) + len(b["gen"]) + (b["meta"] is not None)
                 + len(b["apply"]))
@@ -480,8 +548,8 @@ class PsStep:
         """A CUDA graph of ``steps`` iterations on self.stream; the gen batch
         reads the iteration from the device counter, which each captured step
         advances (set the first value with :meth:`set_iteration`)."""
-        if self.overlap:
-            raise errors.InvalidConfig("graph capture uses the one-stream schedule")
+        if self.overlap or self._exchange is not None:
+            raise errors.InvalidConfig("graph capture uses the one-stream phase schedule")
         none = (1 << 64) - 1
         graph = C.c_void_p()
         _lib.call("srf_graph_begin", self.stream)
@@ -565,6 +633,9 @@ class PsStep:
 
     def close(self) -> None:
         self.sync()
+        if self._exchange_built is not None:
+            _lib.call("srf_ps_exchange_destroy", self._exchange_built)
+            self._exchange = self._exchange_built = None
         for b in [self.batches["push"], self.batches["meta"], *self.batches["gen"].values(),
                   *self.batches["apply"].values()]:
             if b is not None:

@@ -1,0 +1,51 @@
+"""One rank of the multi-process PS check (launched by
+tests/test_gpu_multiprocess.py under torchrun): every schedule, two
+placements, variables each rank owns checked against the oracle."""
+from __future__ import annotations
+
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from oracle import port  # noqa: E402
+from paper_1805_08430_b200.distributed import init_process_group  # noqa: E402
+from paper_1805_08430_b200.ps import PsLayout, PsStep  # noqa: E402
+from paper_1805_08430_b200.workloads import mlp_shapes  # noqa: E402
+
+
+def main() -> int:
+    rank, world, local = init_process_group("nccl")
+    torch.cuda.set_device(local)
+    layouts = [
+        ("coloc", [(3000,), (17,), (200, 300), (5,), (70000,)], world, world, True),
+        ("ps+workers", mlp_shapes() + [(4096,)], 2, 1, False),
+    ]
+    bad = 0
+    for name, shapes, W, P, coloc in layouts:
+        for schedule in ("phases", "exchange"):
+            L = PsLayout(shapes, W, P, coloc)
+            ps = PsStep(L, rank=rank, world=world, device=local, seed=5, op="sgd", lr=0.02,
+                        schedule=schedule)
+            for it in range(1, 9):
+                ps.step(it)
+            ps.sync()
+            torch.distributed.barrier()
+            mine = [v for v in range(len(shapes)) if L.shard_of(v) % world == rank]
+            want = port.ps_expected_device(shapes, W, 5, range(1, 9), op="sgd", lr=0.02,
+                                           only=mine)
+            for v in mine:
+                if ps.variable(v).tobytes() != want[v].tobytes():
+                    print(f"rank {rank}: {name}/{schedule} variable {v} differs", flush=True)
+                    bad += 1
+            ps.close()
+            torch.distributed.barrier()
+    print(f"rank {rank}: {'OK' if bad == 0 else 'FAIL'}", flush=True)
+    torch.distributed.destroy_process_group()
+    return 1 if bad else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -152,3 +152,49 @@ def test_persistent_step_matches_oracle(shapes, W, P, coloc):
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes()
     ps.close()
+
+
+@pytest.mark.parametrize("shapes,W,P,coloc", CASES)
+@pytest.mark.parametrize("lag,order", [(1, "index"), (0, "index"), (2, "size")])
+def test_exchange_schedule_matches_oracle(shapes, W, P, coloc, lag, order):
+    """One k_ps_exchange launch per iteration (dependency-ordered work queue,
+    metadata puts fused into the gradient producer): same bytes as the phases."""
+    L = PsLayout(shapes, W, P, coloc)
+    ps = PsStep(L, seed=12, op="sgd", lr=0.03, schedule="exchange", exchange_lag=lag,
+                exchange_order=order)
+    launches = _lib.launch_count()
+    for it in range(1, 7):
+        assert ps.step(it) == 1
+    ps.sync()
+    assert _lib.launch_count() - launches == 6
+    want = port.ps_expected_device(shapes, W, 12, range(1, 7), op="sgd", lr=0.03)
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes(), (v, lag, order)
+    # parity mode (reference PCG64 gradients uploaded), XOR
+    ps.close()
+    ps = PsStep(L, seed=3, op="xor", schedule="exchange", exchange_lag=lag,
+                exchange_order=order)
+    for it in (1, 2, 3):
+        ps.upload_gradients(it)
+        ps.step(it, regen=False)
+        ps.sync()
+    want = port.ps_expected(shapes, W, 3, 3, op="xor")
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes()
+    ps.close()
+
+
+def test_exchange_schedule_mixes_with_phases():
+    """Phase launches and exchange launches share flags and credits: a run
+    that alternates them matches the oracle."""
+    shapes, W, P = mlp_shapes(), 2, 1
+    L = PsLayout(shapes, W, P, False)
+    ps = PsStep(L, seed=2, op="sgd", lr=0.01, schedule="exchange")
+    for it in range(1, 7):
+        ps.use_schedule("exchange" if it % 2 else "phases")
+        ps.step(it)
+    ps.sync()
+    want = port.ps_expected_device(shapes, W, 2, range(1, 7), op="sgd", lr=0.01)
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes()
+    ps.close()

@@ -18,13 +18,20 @@ from paper_1805_08430_b200.workloads import vgg16_shapes
 rank, world, local = init_process_group("nccl")
 torch.cuda.set_device(local)
 balanced = os.environ.get("PROBE_PLACEMENT", "round_robin")
-L = PsLayout(vgg16_shapes(), world, world, colocate=True, placement=balanced)
+cfg = os.environ.get("PROBE_CFG", "vgg")
+if cfg == "vgg":
+    L = PsLayout(vgg16_shapes(), world, world, colocate=True, placement=balanced)
+elif cfg == "fcn5":
+    L = PsLayout([(int(204.47e6) // 10 // 4,)] * 10, 2, 1, False)
+else:
+    L = PsLayout([(int(35.93e6) // 14 // 4,)] * 14, 7, 1, False)
 mode = os.environ.get("PROBE_MODE", "phases")
 if mode != "phases":
     # whole-step wall time of the eager or overlapped schedule, max over ranks
     import time
     ps = PsStep(L, rank=rank, world=world, device=local, seed=0, op="sgd", lr=0.01,
-                overlap=(mode == "overlap"))
+                overlap=(mode == "overlap"),
+                schedule="exchange" if mode == "exchange" else "phases")
     if os.environ.get("PROBE_CAP"):
         ps._cap = int(os.environ["PROBE_CAP"])
     for it in range(1, 6):
@@ -39,7 +46,7 @@ if mode != "phases":
     bench.barrier_sync()
     dt = bench.dist_max(time.perf_counter() - t0) / R
     if rank == 0:
-        print(json.dumps({"mode": mode, "cap": getattr(ps, "_cap", None),
+        print(json.dumps({"mode": mode, "cfg": cfg, "cap": getattr(ps, "_cap", None),
                           "placement": balanced, "step_us": round(dt * 1e6, 1),
                           "knobs": {k: v for k, v in os.environ.items()
                                     if k.startswith("SRFLOW_")}}), flush=True)

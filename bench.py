@@ -745,7 +745,9 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
     def sample(fn, n=5):
         barrier_sync()
         _lib.call("srf_event_record_on", ev[0], ps.stream)
+        ps.fork()
         fn(n)
+        ps.join()
         _lib.call("srf_event_record_on", ev[1], ps.stream)
         ps.sync()
         t_ = C.c_float()
@@ -773,7 +775,7 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         times["persistent"] = sample(pers)
     best = min(times, key=times.get)
     persistent = best == "persistent"
-    ps.use_schedule("exchange" if best == "exchange" else "phases")
+    ps.use_schedule("phases" if best == "persistent" else best)
     # latency-bound configs: enough iterations for a timed region of ~0.3 s
     per_iter_s = times[best] / 5 / 1e3
     steps = int(max(steps, min(20000, 0.3 / max(per_iter_s, 1e-7))))

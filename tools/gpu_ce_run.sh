@@ -1,2 +1,5 @@
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/ex_pytest2.log 2>&1; echo rc=$? >> gpurun_out/ex_pytest2.log
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --no-cpu > gpurun_out/ex_bench_n2.json 2> gpurun_out/ex_bench_n2.err
+TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511"
+for cfg in lstm fcn5; do
+for m in ce phases; do
+PROBE_HOST=1 PROBE_CFG=$cfg PROBE_MODE=$m timeout 300 $TR tools/ps_phase_probe.py >> gpurun_out/dbg_ce12.log 2>&1
+done; done

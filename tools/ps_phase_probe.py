@@ -43,6 +43,29 @@ if mode != "phases":
     for it in range(6, 6 + R):
         ps.step(it)
     ps.sync()
+    if os.environ.get("PROBE_HOST"):
+        # host issue time vs device completion, one step at a time
+        ti, ts = 0.0, 0.0
+        for it2 in range(6 + R, 6 + R + 10):
+            bench.barrier_sync()
+            a0 = time.perf_counter()
+            ps.step(it2)
+            a1 = time.perf_counter()
+            ps.sync()
+            a2 = time.perf_counter()
+            ti += (a1 - a0) / 10
+            ts += (a2 - a1) / 10
+        print(json.dumps({"rank": rank, "cfg": cfg, "mode": mode, "issue_us": round(ti * 1e6, 1),
+                          "sync_us": round(ts * 1e6, 1)}), flush=True)
+        R += 10
+    if mode != "phases":
+        from oracle import port
+        mine = [v for v in range(len(L.shapes)) if L.shard_of(v) % world == rank]
+        small = [v for v in mine if L.nbytes(v) < (4 << 20)][:2]
+        want = port.ps_expected_device(L.shapes, L.workers, 0, range(1, 6 + R), op="sgd",
+                                       lr=0.01, only=small)
+        for v in small:
+            assert ps.variable(v).tobytes() == want[v].tobytes(), ("mismatch", v)
     bench.barrier_sync()
     dt = bench.dist_max(time.perf_counter() - t0) / R
     if rank == 0:

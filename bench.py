@@ -872,15 +872,16 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         per_gpu = {g: max(x["link_out"], x["link_in"])
                    for g, x in link_traffic(L, world).items()}
         hot = max(per_gpu, key=per_gpu.get)
-        # dependency chain: a variable's weight push must land before its
-        # gradient can be produced and pulled back, so for each variable the
-        # shard GPU moves its remote pushes and then its remote pulls in
-        # sequence (one link direction each), whatever else overlaps
+        # dependency chain: a worker's gradient of v cannot be pulled before
+        # its weight of v landed, so the shard GPU's k remote pushes and k
+        # remote pulls of v overlap at best as push1, (push2 | pull1), ...,
+        # pullk: (k+1)*S on the busier link direction, whatever else overlaps
         chain = 0
         for v in range(len(shapes)):
             k = sum(1 for w in range(L.workers)
                     if w % world != L.shard_of(v) % world)
-            chain = max(chain, k * (2 * L.nbytes(v) + 1))
+            if k:
+                chain = max(chain, (k + 1) * L.nbytes(v) + k)
         bound_bytes = max(per_gpu[hot], chain)
         ach = bound_bytes * steps / t / 1e9
         roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_MEASURED_GBS,
@@ -889,7 +890,8 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
                 "chain_bytes_per_step": chain,
                 "frac_link_only": round(per_gpu[hot] * steps / t / 1e9 / NVLINK_MEASURED_GBS, 4),
                 "note": "bytes per step = max(busiest GPU's max(NVLink egress, ingress), the "
-                        "largest variable's push-then-pull chain k*(2S+1)); servers on the "
+                        "largest variable's push-then-pull chain (k+1)*S for k remote "
+                        "workers); servers on the "
                         "same GPU exchange through HBM and are not counted"}
     out = {"workload": f"{label}, op={op} lr=0.01",
            "steps_per_s": round(steps / t, 2), "ms_per_step": round(t / steps * 1e3, 4),

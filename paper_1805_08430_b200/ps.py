@@ -449,8 +449,11 @@ class PsStep:
         if schedule == "exchange":
             if self.overlap:
                 raise errors.InvalidConfig("the exchange schedule is one launch per step")
-            if self._exchange_built is None:
+            b = self.batches
+            if self._exchange_built is None and (b["push"] is not None or b["gen"]
+                                                 or b["apply"]):
                 self._exchange_built = self._build_exchange(*self._exchange_cfg)
+            # (a rank hosting no server of the layout has nothing to launch)
             self._exchange = self._exchange_built
         else:
             self._exchange = None

@@ -28,6 +28,7 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -821,6 +822,8 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
     # verify the smallest variable this rank owns: a full oracle replay of
     # every iteration when that is cheap, else one further iteration checked
     # against the oracle applied to the live state
+    # (transfer units: a partitioned variable's slices are checked against the
+    # matching slice of the model variable)
     mine = [v for v in range(len(shapes)) if L.shard_of(v) % world == rank]
     ok, how = True, "none"
     if not mine:
@@ -828,10 +831,12 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
     if mine:
         v = min(mine, key=L.nbytes)
         n_v = L.nbytes(v) // 4
-        if it * L.workers * n_v <= 4e8:
-            want = port.ps_expected_device(shapes, L.workers, 0, range(1, it + 1), op=op,
-                                           lr=0.01, only=[v])[v]
-            ok = ps.variable(v).tobytes() == want.tobytes()
+        pv, p_off, _pn = L.parent(v)
+        n_parent = math.prod(L.model_shapes[pv])
+        if it * L.workers * n_parent <= 4e8:
+            want = port.ps_expected_device(L.model_shapes, L.workers, 0, range(1, it + 1),
+                                           op=op, lr=0.01, only=[pv])[pv].reshape(-1)
+            ok = ps.variable(v).tobytes() == want[p_off:p_off + n_v].tobytes()
             how = f"oracle replay of all {it} iterations"
         else:
             before = ps.variable(v).copy()
@@ -842,7 +847,8 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         ps.sync()
         barrier_sync()
         if mine and how == "none":
-            grads = [port.device_gradient(0, port.ps_node_ids(v, w, L.workers)[1], it, n_v)
+            grads = [port.device_gradient(0, port.ps_node_ids(pv, w, L.workers)[1], it, n_v,
+                                          offset=p_off)
                      for w in range(L.workers)]
             want = before.reshape(-1).copy()
             if op == "xor":
@@ -1051,6 +1057,16 @@ def main() -> int:
                 cpu=False, layout=Lb,
                 label=f"EXTENSION: VGG-16 with byte-balanced shards (largest-first), "
                       f"{world} workers + {world} shards co-located")
+            # labelled extension: partitioned variables (every tensor > 16 MiB cut
+            # into one slice per shard), byte-balanced; values bit-identical
+            Lp = PsLayout(vgg16_shapes(), world, world, colocate=True, placement="bytes",
+                          partition_bytes=16 << 20)
+            line["ps_partitioned"] = bench_ps(
+                rank, world, local, max(10, args.steps), args.warmup, op=args.ps_op,
+                cpu=False, layout=Lp,
+                label=f"EXTENSION: VGG-16 with partitioned variables (tensors > 16 MiB "
+                      f"split into {world} slices, {len(Lp.shapes)} transfer units), "
+                      f"byte-balanced, {world} workers + {world} shards co-located")
         line["ps_configs"] = bench_ps_configs(rank, world, local, max(20, args.steps),
                                               args.warmup, args.ps_op, not args.no_cpu)
     if rank == 0:

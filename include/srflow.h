@@ -281,6 +281,9 @@ int srf_ps_persistent(srf_batch_t push, srf_batch_t gen, srf_batch_t meta,
  * producer, runtime/protocol.py:163-201). */
 typedef struct srf_exchange *srf_exchange_t;
 int srf_batch_gen_set_meta(srf_batch_t gen, int n, const int *gen_index, srf_batch_t meta);
+/* partitioned variables (extension): gen edge i produces elements
+ * elem_offset[i] ... of its model variable's gradient stream */
+int srf_batch_gen_set_offsets(srf_batch_t gen, const uint64_t *elem_offset);
 int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch_t gen,
                            const uint64_t *gen_key, srf_batch_t const *apply, int napply,
                            const uint64_t *apply_key, srf_exchange_t *out);

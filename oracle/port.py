@@ -516,17 +516,19 @@ def _fmix32(h: np.ndarray) -> np.ndarray:
     return h
 
 
-def device_gradient(seed: int, node: int, iteration: int, n: int) -> np.ndarray:
+def device_gradient(seed: int, node: int, iteration: int, n: int,
+                    offset: int = 0) -> np.ndarray:
     """fp32 values k_gen_batch writes for GenGrad node ``node`` at ``iteration``:
     a 64-bit key from (seed, node, iteration), then per element a 32-bit
-    murmur finaliser of (index, key halves), top 24 bits -> [0, 1)."""
+    murmur finaliser of (index, key halves), top 24 bits -> [0, 1).  ``offset``:
+    elements offset ... offset+n-1 (a slice of a partitioned variable)."""
     with np.errstate(over="ignore"):
         s = np.array([seed], dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
         a = _mix64(np.array([node], dtype=np.uint64) + np.uint64(0x51ED))
         b = _mix64(np.array([iteration], dtype=np.uint64) * np.uint64(0xD1B54A32D192ED03))
         key = int(_mix64(s ^ a ^ b)[0])
         k0, k1 = np.uint32(key & 0xFFFFFFFF), np.uint32(key >> 32)
-        idx = np.arange(n, dtype=np.uint32)
+        idx = np.arange(offset, offset + n, dtype=np.uint64).astype(np.uint32)
         h = _fmix32(idx * np.uint32(0x9E3779B1) + k0) ^ k1
     return (h >> np.uint32(8)).astype(np.float32) * np.float32(1.0 / 16777216.0)
 

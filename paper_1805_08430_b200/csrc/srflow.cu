@@ -1059,6 +1059,7 @@ struct BatchGen {        // worker: consume weight, (re)produce gradient
   uint8_t *meta_dst;
   const uint8_t *meta_tail;
   uint64_t meta_body;
+  uint64_t elem_offset;  // first element's index in its model variable (slices)
 };
 
 struct BatchApply {      // shard: fused dynamic receive (meta decode + peer
@@ -1181,14 +1182,15 @@ __device__ __forceinline__ void gen_unit(const BatchGen *descs, int n, uint32_t 
       const uint64_t nf = d.n / 4;
       const uint64_t nth = (uint64_t)d.cta_count * blockDim.x;
       float4 *g4 = (float4 *)d.grad;  // gradient blocks are 16-B aligned by layout
+      const uint32_t e0 = (uint32_t)d.elem_offset;
       for (uint64_t q = (uint64_t)lb * blockDim.x + threadIdx.x; q < nf / 4; q += nth) {
-        const uint32_t i = (uint32_t)(4 * q);
+        const uint32_t i = (uint32_t)(4 * q) + e0;
         g4[q] = make_float4(unit_f32(k0, k1, i), unit_f32(k0, k1, i + 1),
                             unit_f32(k0, k1, i + 2), unit_f32(k0, k1, i + 3));
       }
       float *g = (float *)d.grad;
       for (uint64_t i = (nf / 4) * 4 + (uint64_t)lb * blockDim.x + threadIdx.x; i < nf; i += nth)
-        g[i] = unit_f32(k0, k1, (uint32_t)i);
+        g[i] = unit_f32(k0, k1, (uint32_t)i + e0);
     }
     __syncthreads();
     if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, sys);
@@ -2785,6 +2787,19 @@ int srf_ps_persistent(srf_batch_t push, srf_batch_t gen, srf_batch_t meta,
   CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_ps_persistent, dim3(grid), dim3(256),
                                        params, 0, st->s));
   return launch_check("k_ps_persistent");
+}
+
+int srf_batch_gen_set_offsets(srf_batch_t gen, const uint64_t *elem_offset) {
+  if (!gen || gen->kind != 1) return fail(SRF_E_INVALID_CONFIG, "not a gen batch");
+  BatchGen *g = (BatchGen *)gen->host.data();
+  for (int i = 0; i < gen->n; ++i) {
+    if (elem_offset[i] + g[i].n / 4 > 0xFFFFFFFFull)
+      return fail(SRF_E_SHAPE_MISMATCH, "gradient element index beyond 2^32");
+    g[i].elem_offset = elem_offset[i];
+  }
+  CUDA_TRY(cudaSetDevice(gen->device));
+  CUDA_TRY(cudaMemcpy(gen->descs, gen->host.data(), gen->host.size(), cudaMemcpyHostToDevice));
+  return SRF_OK;
 }
 
 int srf_batch_gen_set_meta(srf_batch_t gen, int n, const int *gen_index, srf_batch_t meta) {

@@ -78,17 +78,39 @@ class PsLayout:
     #: "round_robin" = the reference placement v % shards (workloads.py:84);
     #: "bytes" = extension: largest variable first onto the least-loaded shard
     placement: str = "round_robin"
+    #: EXTENSION (partitioned variables, as MXNet's kvstore splits big arrays
+    #: over servers): a variable larger than this many bytes is cut into
+    #: ``shards`` contiguous slices, each its own transfer unit on its own
+    #: shard.  Updates are elementwise and gradients are generated per global
+    #: element index, so the model's values are bit-identical to unpartitioned.
+    partition_bytes: Optional[int] = None
     blocks: dict[int, dict] = field(default_factory=dict)
     sizes: dict[int, int] = field(default_factory=dict)
 
     def __post_init__(self):
-        self.shapes = [tuple(int(d) for d in s) for s in self.shapes]
+        self.model_shapes = [tuple(int(d) for d in s) for s in self.shapes]
         if self.colocate and self.shards > self.workers:
             raise errors.InvalidConfig("colocate needs shards <= workers")
         if self.workers > _lib.MAX_WORKERS:
             raise errors.InvalidConfig(f"at most {_lib.MAX_WORKERS} workers")
+        # transfer units: (model variable, first element, elements, slice index)
+        self.units = []
+        esz = self.elem.size
+        for v, dims in enumerate(self.model_shapes):
+            n = math.prod(dims)
+            if self.partition_bytes is not None and n * esz > self.partition_bytes \
+                    and self.shards > 1:
+                step = -(-n // self.shards)
+                step = (step + 63) // 64 * 64          # 256-B slices
+                for j, off in enumerate(range(0, n, step)):
+                    self.units.append((v, off, min(step, n - off), j))
+            else:
+                self.units.append((v, 0, n, -1))
+        self.shapes = [self.model_shapes[v] if j < 0 else (cnt,)
+                       for v, _off, cnt, j in self.units]
         if self.placement == "round_robin":
-            self._shard = [v % self.shards for v in range(len(self.shapes))]
+            # slice j of variable v on shard (v + j) % shards
+            self._shard = [(v + max(j, 0)) % self.shards for v, _o, _c, j in self.units]
         elif self.placement == "bytes":
             load = [0] * self.shards
             self._shard = [0] * len(self.shapes)
@@ -107,6 +129,16 @@ class PsLayout:
 
     def nbytes(self, v: int) -> int:
         return math.prod(self.shapes[v]) * self.elem.size
+
+    def parent(self, u: int) -> tuple[int, int, int]:
+        """(model variable, first element, elements) of transfer unit u."""
+        v, off, n, _j = self.units[u]
+        return v, off, n
+
+    def node_ids(self, u: int, w: int) -> tuple[int, int, int]:
+        """Reference node ids (variable, GenGrad, ApplyGrad) of unit u's model
+        variable for worker w (workloads.py:81-93)."""
+        return ps_node_ids(len(self.model_shapes), self.workers, self.units[u][0], w)
 
     def shard_of(self, v: int) -> int:
         return self._shard[v] + (0 if self.colocate else self.workers)
@@ -318,9 +350,7 @@ class PsStep:
             sp.write_raw(self.addr(s, "flag"), b"\x01")
             for v in range(len(L.shapes)):
                 if L.shard_of(v) == s:
-                    var_node = ps_node_ids(len(L.shapes), L.workers, v, 0)[0]
-                    init = synthesize_values(L.shapes[v], L.elem, node_rng(self.seed, var_node, 0))
-                    sp.write_raw(self.addr(s, ("var", v)), init)
+                    sp.write_raw(self.addr(s, ("var", v)), self._model_slice(v, 0, 0))
                     for w in range(L.workers):
                         if w != s:
                             mk = ("mslot", v, w)
@@ -331,6 +361,20 @@ class PsStep:
                     meta = encode_meta(L.shapes[v], L.elem, self.addr(s, ("grad", v)), self.token(s))
                     sp.write_raw(self.addr(s, ("mstage", v)), meta)
             sp.sync()
+
+    def _model_slice(self, u: int, kind: int, iteration: int) -> np.ndarray:
+        """Unit u's slice of its model variable's initial value (kind 0) or of
+        worker w=kind-1's reference PCG64 gradient (graph.py:333-350)."""
+        L = self.L
+        v, off, n = L.parent(u)
+        node = (L.node_ids(u, 0)[0] if kind == 0 else L.node_ids(u, kind - 1)[1])
+        key = (v, node, iteration)
+        cache = self.__dict__.setdefault("_slice_cache", {})
+        if key not in cache:
+            cache.clear()
+            cache[key] = synthesize_values(L.model_shapes[v], L.elem,
+                                           node_rng(self.seed, node, iteration)).reshape(-1)
+        return cache[key][off:off + n].reshape(L.shapes[u])
 
     def _build_batches(self) -> dict:
         L = self.L
@@ -364,7 +408,7 @@ class PsStep:
                                self.addr(w, ("wbuf", v)) + L.nbytes(v) if remote else _NONE,
                                self.space(sh).handle.value if remote else None,
                                self.addr(sh, ("mslot", v, w)) + mlen - 1 if remote else _NONE,
-                               ps_node_ids(len(L.shapes), L.workers, v, w)[1], w))
+                               L.node_ids(v, w)[1], w))
                 self._rows["gen"].append((w, v))
         out["gen"] = {}
         if g_rows:
@@ -376,6 +420,9 @@ class PsStep:
                       u64(r[2] for r in g_rows), (P * n)(*[r[3] for r in g_rows]),
                       u64(r[4] for r in g_rows), u64(r[5] for r in g_rows), self.seed,
                       C.byref(b))
+            offs = [L.parent(v)[1] for _w, v in self._rows["gen"]]
+            if any(offs):  # partitioned variables: slices keep global element indices
+                _lib.call("srf_batch_gen_set_offsets", b, u64(offs))
             out["gen"]["all"] = b
         # 3. metadata writes (K3)
         rows = []
@@ -624,8 +671,7 @@ class PsStep:
             if not L.is_worker(w):
                 continue
             for v in range(len(L.shapes)):
-                gen = ps_node_ids(len(L.shapes), L.workers, v, w)[1]
-                g = synthesize_values(L.shapes[v], L.elem, node_rng(self.seed, gen, iteration))
+                g = self._model_slice(v, w + 1, iteration)
                 self.spaces[w].write_raw(self.addr(w, ("grad", v)), g)
             self.spaces[w].sync()
 

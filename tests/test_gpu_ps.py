@@ -198,3 +198,30 @@ def test_exchange_schedule_mixes_with_phases():
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes()
     ps.close()
+
+
+@pytest.mark.parametrize("placement", ["round_robin", "bytes"])
+def test_partitioned_variables_equal_the_model(placement):
+    """EXTENSION: variables cut into one slice per shard; gathering the slices
+    gives exactly the unpartitioned model's values (device and PCG64 grads)."""
+    shapes, W, P = [(3000,), (17,), (64, 70), (5,)], 3, 3
+    L = PsLayout(shapes, W, P, True, placement=placement, partition_bytes=4096)
+    assert len(L.shapes) > len(shapes)
+    for op, regen in (("sgd", True), ("xor", False)):
+        ps = PsStep(L, seed=8, op=op, lr=0.02)
+        for it in range(1, 5):
+            if not regen:
+                ps.upload_gradients(it)
+            ps.step(it, regen=regen)
+            if not regen:
+                ps.sync()
+        ps.sync()
+        want = (port.ps_expected_device(shapes, W, 8, range(1, 5), op=op, lr=0.02) if regen
+                else port.ps_expected(shapes, W, 8, 4, op=op))
+        got = [np.zeros(int(np.prod(s)), np.float32) for s in shapes]
+        for u in range(len(L.shapes)):
+            v, off, n = L.parent(u)
+            got[v][off:off + n] = ps.variable(u).reshape(-1)
+        for v in range(len(shapes)):
+            assert got[v].tobytes() == want[v].reshape(-1).tobytes(), (op, v)
+        ps.close()

@@ -269,3 +269,26 @@ def test_ps_link_traffic_excludes_same_gpu_servers():
     assert t[0]["link_out"] == 10 * (S + 1)     # pushes to worker 1 only
     assert t[1]["link_out"] == 10 * (41 + S)    # worker 1's metadata + gradient reads
     assert link_traffic(L, 1)[0] == {"link_out": 0, "link_in": 0}
+
+
+def test_partitioned_layout_units():
+    from paper_1805_08430_b200.ps import PsLayout
+    from paper_1805_08430_b200.workloads import vgg16_shapes
+    shapes = vgg16_shapes()
+    L = PsLayout(shapes, 4, 4, colocate=True, placement="bytes", partition_bytes=16 << 20)
+    # every element of every model variable is covered exactly once, in order
+    for v, dims in enumerate(shapes):
+        parts = sorted((L.parent(u)[1], L.parent(u)[2]) for u in range(len(L.shapes))
+                       if L.parent(u)[0] == v)
+        n = int(np.prod(dims))
+        assert parts[0][0] == 0 and sum(c for _o, c in parts) == n
+        for (o1, c1), (o2, _c2) in zip(parts, parts[1:]):
+            assert o1 + c1 == o2 and (o2 * 4) % 256 == 0
+    big = [u for u in range(len(L.shapes)) if L.parent(u)[0] == 26]   # fc6
+    assert len(big) == 4 and len({L.shard_of(u) for u in big}) == 4
+    # no unit exceeds the largest slice; shard loads within one slice of each other
+    load = [sum(L.nbytes(u) for u in range(len(L.shapes)) if L.shard_of(u) == k)
+            for k in range(4)]
+    assert max(load) - min(load) <= max(L.nbytes(u) for u in range(len(L.shapes)))
+    # node ids are the model variable's
+    assert L.node_ids(big[2], 1) == L.node_ids(big[0], 1)

@@ -1,3 +1,2 @@
-for n in 4; do
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $n > gpurun_out/r1e_bench_n$n.json 2> gpurun_out/r1e_bench_n$n.err
-done
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/part_pytest.log 2>&1; echo rc=$? >> gpurun_out/part_pytest.log
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --no-cpu --no-sweep > gpurun_out/part_bench_n2.json 2> gpurun_out/part_bench_n2.err

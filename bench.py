@@ -543,7 +543,9 @@ def sweep(max_bytes, device):
     static zero-copy (K1+K2, device time of graph-replayed rounds), staged
     'cp' (K5 copy + K1 + K2, the paper's RDMA.cp), dynamic allocation through
     the public endpoints (meta write, doorbell poll + decode, arena alloc, K4
-    pull), and for small sizes the host-staged RPC fragment ring."""
+    pull), dynamic with the receiver on the device (K3 + srf_dyn_recv,
+    graph-replayed like static), and for small sizes the host-staged RPC
+    fragment ring."""
     from paper_1805_08430_b200 import _lib
     out = []
     size = 1024
@@ -575,12 +577,76 @@ def sweep(max_bytes, device):
             row[f"{name}_us"] = round(t * 1e6, 3)
         row["verified"] = ring.verify()
         row.update(dynamic_rate(size, device))
+        row.update(dynamic_device_rate(size, device))
         row.update(rpc_device_rate(size, device))
         if size <= MIB:
             row.update(rpc_rate(size, device))
         out.append(row)
         size *= 4
     return out
+
+
+def dynamic_device_rate(size, device, rounds=None):
+    """Dynamic allocation with the receiver on the device: K3 metadata write
+    (credit-gated), then srf_dyn_recv (flag acquire + decode + validation +
+    K4 pull into the receive block + flag clear), graph-replayed rounds timed
+    on the device like the static rows."""
+    from paper_1805_08430_b200 import _lib
+    from paper_1805_08430_b200.memspace import MemorySpace
+    from paper_1805_08430_b200.wire import ElemType, encode_meta, meta_block_size
+    cap = 2 * size + 8 * MIB
+    src = MemorySpace(0, cap, device=device)
+    rcv = MemorySpace(1, cap, device=device)
+    _lib.call("srf_connect", src.handle, rcv.handle)
+    rs = src.allocate_region(size + 2 * MIB, True)
+    rr = rcv.allocate_region(size + 2 * MIB, True)
+    payload = rs.base_addr + MIB
+    stage, slot, word = rs.base_addr, rr.base_addr, rr.base_addr + 4096
+    dst = rr.base_addr + MIB
+    mlen = meta_block_size(1)
+    src.write_raw(stage, encode_meta((size // 4,), ElemType.F32, payload, rs.access_token))
+    rcv.write_raw(slot + mlen - 1, b"\x00")
+    st = C.c_void_p()
+    _lib.call("srf_stream_create", src.handle, C.byref(st))
+    u = _lib.u64_array
+
+    def body():
+        _lib.call("srf_put", src.handle, u([stage]), u([mlen]), u([rs.access_token]), 1,
+                  rcv.handle, slot, rr.access_token, _lib.PUT_WAIT_EMPTY, st, None)
+        _lib.call("srf_dyn_recv", rcv.handle, slot, 1, src.handle, rs.base_addr,
+                  rs.base_addr + rs.length, rs.access_token, dst, size, word, st)
+
+    for _ in range(8):
+        body()
+    _lib.call("srf_stream_sync", st)
+    rounds = rounds or (200 if size <= 4 * MIB else 20)
+    graph = C.c_void_p()
+    _lib.call("srf_graph_begin", st)
+    for _ in range(rounds):
+        body()
+    _lib.call("srf_graph_end", st, C.byref(graph))
+    ev = [C.c_void_p(), C.c_void_p()]
+    for e in ev:
+        _lib.call("srf_timing_event_create", src.handle, C.byref(e))
+    _lib.call("srf_graph_launch", graph, st)
+    _lib.call("srf_stream_sync", st)
+    _lib.call("srf_event_record_on", ev[0], st)
+    _lib.call("srf_graph_launch", graph, st)
+    _lib.call("srf_event_record_on", ev[1], st)
+    _lib.call("srf_stream_sync", st)
+    ms = C.c_float()
+    _lib.call("srf_event_elapsed_ms", ev[0], ev[1], C.byref(ms))
+    t = ms.value / rounds / 1e3
+    src.sync()
+    rcv.sync()
+    ok = (rcv.read_raw(dst, min(size, 4096)) == src.read_raw(payload, min(size, 4096)) and
+          int.from_bytes(rcv.read_raw(word, 8), "little") == size)
+    _lib.call("srf_graph_destroy", graph)
+    _lib.call("srf_stream_destroy", st)
+    src.close()
+    rcv.close()
+    return {"dynamic_dev_gbps": round(size / t / 1e9, 3), "dynamic_dev_us": round(t * 1e6, 3),
+            "dynamic_dev_verified": ok}
 
 
 def rpc_device_rate(size, device, reps=None):

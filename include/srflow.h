@@ -291,6 +291,17 @@ int srf_ps_exchange_launch(srf_exchange_t exchange, srf_stream_t stream, uint64_
                            int regen);
 int srf_ps_exchange_destroy(srf_exchange_t exchange);
 
+/* Device-side DynReceiver.poll + fetch (runtime/protocol.py:224-254): acquire
+ * the metadata flag of the block at meta_addr (rank-D layout, wire.py:79-142),
+ * validate it like decode_meta + check_remote_access (token, [peer_lo,
+ * peer_hi) of peer, payload_len == prod(dims) * elem size, <= dst_cap),
+ * pull the bytes into [dst_addr, +len) (K4), store len at len_out_addr
+ * (UINT64_MAX: none; all ones on a rejected block) and clear the flag.
+ * Rejections raise SRF_E_BAD_TOKEN at the next sync. */
+int srf_dyn_recv(srf_space_t receiver, uint64_t meta_addr, int rank, srf_space_t peer,
+                 uint64_t peer_lo, uint64_t peer_hi, uint64_t peer_token, uint64_t dst_addr,
+                 uint64_t dst_cap, uint64_t len_out_addr, srf_stream_t stream);
+
 /* RPC-style serialize/copy baseline (runtime/protocol.py:257-448) on the
  * device - the comparator the north star reports zero-copy against.  The
  * stream metadata||payload moves in 4096-B fragments (16-B header + 4080 B)

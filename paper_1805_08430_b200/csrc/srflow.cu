@@ -1316,6 +1316,69 @@ __global__ void __launch_bounds__(256) k_apply_batch(const BatchApply *descs, in
   apply_batch_units(descs, n, total_units, counters, op, lr, timeout_ns, err, sys);
 }
 
+// Device-side DynReceiver (runtime/protocol.py:224-254) for device-resident
+// loops: acquire the metadata flag, decode and validate the block exactly as
+// decode_meta + check_remote_access do (wire.py:114-142, memspace.py:145-157),
+// pull the announced bytes into a pre-allocated block (K4), publish the length,
+// and clear the flag (the poll's clear = the sender's next credit).
+struct DynRecvArgs {
+  uint8_t *meta;            // receiver's metadata block
+  int rank;
+  const uint8_t *peer_base;
+  uint64_t peer_lo, peer_hi, peer_token;
+  uint8_t *dst;
+  uint64_t dst_cap;
+  uint64_t *len_out;        // nullptr: none
+  unsigned int *counter;
+  uint64_t timeout_ns;
+  int *err;
+  int sys;
+};
+
+__global__ void __launch_bounds__(256) k_dyn_recv(const __grid_constant__ DynRecvArgs a) {
+  __shared__ const uint8_t *s_src;
+  __shared__ uint64_t s_len;
+  __shared__ int s_ok, s_last;
+  const int r = a.rank;
+  if (threadIdx.x == 0) {
+    s_ok = 0;
+    s_len = 0;
+    const uint8_t *m = a.meta;
+    if (!spin_until(m + 8 * r + 32, 1, a.timeout_ns, 1)) {
+      atomicExch(a.err, 5);
+    } else {
+      const uint64_t addr = *(const volatile uint64_t *)(m + 8 + 8 * r);
+      const uint64_t tok = *(const volatile uint64_t *)(m + 16 + 8 * r);
+      const uint64_t plen = *(const volatile uint64_t *)(m + 24 + 8 * r);
+      const uint32_t code = m[0];
+      const uint64_t esz = code == 0 ? 4 : code == 1 ? 8 : code == 2 ? 4 : code == 3 ? 8
+                         : code == 4 ? 1 : 0;
+      uint64_t prod = esz;
+      for (int k = 0; k < r; ++k) prod *= *(const volatile uint64_t *)(m + 8 + 8 * k);
+      if (m[1] != r || esz == 0 || prod != plen || tok != a.peer_token || addr < a.peer_lo ||
+          addr + plen > a.peer_hi || plen > a.dst_cap) {
+        atomicExch(a.err, 6);
+      } else {
+        s_src = a.peer_base + addr;
+        s_len = plen;
+        s_ok = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_ok)
+    copy_bytes_grid<8>(a.dst, s_src, s_len, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                       (uint64_t)gridDim.x * blockDim.x);
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = grid_arrive(a.counter, gridDim.x - 1, a.sys);
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    if (a.len_out) *(volatile uint64_t *)a.len_out = s_ok ? s_len : ~0ull;
+    release_tail(a.meta + 8 * r + 32, 0, a.sys);
+    atomicExch(a.counter, 0u);
+  }
+}
+
 // One PS iteration loop in a single cooperative launch (all servers on this
 // GPU): the four phases back to back, separated by grid-wide barriers, for
 // `iters` iterations.  The device flags and credits are still set and
@@ -2305,6 +2368,41 @@ int srf_flag_wait(srf_space_t sp, uint64_t flag_addr, uint8_t expect,
   k_flag_wait<<<1, 32, 0, s->s>>>(sp->base + flag_addr, expect, clear,
                                   timeout_ns, sp->err);
   return launch_check("k_flag_wait");
+}
+
+int srf_dyn_recv(srf_space_t rcv, uint64_t meta_addr, int rank, srf_space_t peer,
+                 uint64_t peer_lo, uint64_t peer_hi, uint64_t peer_token, uint64_t dst_addr,
+                 uint64_t dst_cap, uint64_t len_out_addr, srf_stream_t st) {
+  if (rank < 0 || rank > 64) return fail(SRF_E_INVALID_CONFIG, "rank %d", rank);
+  int rc = check_raw(rcv, meta_addr, 8 * (uint64_t)rank + 33, "meta block");
+  if (!rc && dst_cap) rc = check_raw(rcv, dst_addr, dst_cap, "receive block");
+  if (!rc && len_out_addr != UINT64_MAX) {
+    rc = check_raw(rcv, len_out_addr, 8, "length word");
+    if (!rc && len_out_addr % 8) rc = fail(SRF_E_INVALID_CONFIG, "length word must be 8-B aligned");
+  }
+  if (rc) return rc;
+  if (peer_hi < peer_lo || peer_hi > peer->capacity)
+    return fail(SRF_E_OUT_OF_BOUNDS, "peer region escapes its space");
+  srf_stream *s = stream_or_default(rcv, st);
+  DynRecvArgs a;
+  a.meta = rcv->base + meta_addr;
+  a.rank = rank;
+  a.peer_base = peer->base;
+  a.peer_lo = peer_lo;
+  a.peer_hi = peer_hi;
+  a.peer_token = peer_token;
+  a.dst = rcv->base + dst_addr;
+  a.dst_cap = dst_cap;
+  a.len_out = len_out_addr == UINT64_MAX ? nullptr : (uint64_t *)(rcv->base + len_out_addr);
+  a.counter = s->counter;
+  a.timeout_ns = 10ull * 1000 * 1000 * 1000;
+  a.err = rcv->err;
+  a.sys = (peer->imported || peer->device != s->device) ? 1 : 0;
+  int grid, block;
+  copy_geometry(s->device, std::max<uint64_t>(dst_cap, 1), &grid, &block);
+  CUDA_TRY(cudaSetDevice(s->device));
+  k_dyn_recv<<<grid, 256, 0, s->s>>>(a);
+  return launch_check("k_dyn_recv");
 }
 
 int srf_consume_checksum(srf_space_t sp, uint64_t flag_addr, uint64_t data_addr,

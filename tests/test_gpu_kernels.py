@@ -312,3 +312,52 @@ def test_transfers_beyond_4gib_indexing():
     assert int(src[-4096:].to(torch.int64).sum()) != 0
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("dims", [(1,), (1031,), (64, 33), (2, 3, 4, 5), ((4 << 20) // 4 + 7,)])
+def test_device_dyn_recv_matches_sent_bytes(pair, dims):
+    """srf_dyn_recv: device-side DynReceiver.poll + decode + validate + fetch."""
+    a, b, ra, rb = pair
+    n = int(np.prod(dims)) * 4
+    data = rand_bytes(n, n)
+    payload = ra.base_addr + (32 << 20) + 8
+    a.write_raw(payload, data)
+    stage = ra.base_addr + 4096
+    slot = rb.base_addr + 4096
+    mlen = port.meta_block_size(len(dims))
+    b.write_raw(slot + mlen - 1, b"\x00")
+    meta = port.encode_meta(dims, 0, payload, ra.access_token)
+    a.write_raw(stage, meta)
+    put(a, [(stage, mlen, ra.access_token)], b, slot, rb.access_token)
+    dst = rb.base_addr + (16 << 20) + 16
+    word = rb.base_addr + 8192
+    _lib.call("srf_dyn_recv", b.handle, slot, len(dims), a.handle, ra.base_addr,
+              ra.base_addr + ra.length, ra.access_token, dst, n + 4096, word, None)
+    b.sync()
+    assert b.read_raw(dst, n) == data.tobytes()
+    assert int(np.frombuffer(b.read_raw(word, 8), np.uint64)[0]) == n
+    assert b.read_raw(slot + mlen - 1, 1) == b"\x00"      # flag cleared: sender credit
+
+
+@pytest.mark.parametrize("bad", ["token", "range", "capacity", "dims"])
+def test_device_dyn_recv_rejects_bad_metadata(pair, bad):
+    a, b, ra, rb = pair
+    dims, n = (1000,), 4000
+    payload = ra.base_addr + (32 << 20)
+    stage, slot = ra.base_addr + 4096, rb.base_addr + 4096
+    mlen = port.meta_block_size(1)
+    tok = ra.access_token ^ (1 if bad == "token" else 0)
+    addr = ra.base_addr + ra.length - 100 if bad == "range" else payload
+    meta = bytearray(port.encode_meta(dims, 0, addr, tok))
+    if bad == "dims":
+        meta[8:16] = (999).to_bytes(8, "little")     # prod(dims) * 4 != payload_len
+    b.write_raw(slot + mlen - 1, b"\x00")
+    a.write_raw(stage, bytes(meta))
+    put(a, [(stage, mlen, ra.access_token)], b, slot, rb.access_token)
+    word = rb.base_addr + 8192
+    cap = n - 4 if bad == "capacity" else n
+    _lib.call("srf_dyn_recv", b.handle, slot, 1, a.handle, ra.base_addr, ra.base_addr + ra.length,
+              ra.access_token, rb.base_addr + (16 << 20), cap, word, None)
+    with pytest.raises(errors.BadToken):
+        b.sync()
+    assert int(np.frombuffer(b.read_raw(word, 8), np.uint64)[0]) == (1 << 64) - 1

@@ -18,6 +18,7 @@
 
 #include <stddef.h>
 #include <stdint.h>
+#include <sys/types.h>
 
 #ifdef __cplusplus
 extern "C" {
@@ -301,6 +302,19 @@ int srf_ps_exchange_destroy(srf_exchange_t exchange);
 int srf_dyn_recv(srf_space_t receiver, uint64_t meta_addr, int rank, srf_space_t peer,
                  uint64_t peer_lo, uint64_t peer_hi, uint64_t peer_token, uint64_t dst_addr,
                  uint64_t dst_cap, uint64_t len_out_addr, srf_stream_t stream);
+
+/* Registered pool behind torch's CUDA allocator (torch.cuda.memory.
+ * CUDAPluggableAllocator over srf_torch_malloc / srf_torch_free): every torch
+ * tensor of that GPU lives in [region_addr, +length) of the space, so it can
+ * be sent or received zero-copy (analyzer.py:226-272).
+ * Freed blocks are reused only after the freeing stream passed them.  A GPU
+ * without a pool, or a request the pool cannot hold, gets plain cudaMalloc
+ * memory (torch works; zero-copy verbs on it are refused as NotRegistered). */
+int srf_torch_pool_attach(srf_space_t space, uint64_t region_addr, uint64_t length);
+int srf_torch_pool_stats(int cuda_device, uint64_t *in_use, uint64_t *peak,
+                         uint64_t *capacity);
+void *srf_torch_malloc(ssize_t size, int cuda_device, void *cuda_stream);
+void srf_torch_free(void *ptr, ssize_t size, int cuda_device, void *cuda_stream);
 
 /* RPC-style serialize/copy baseline (runtime/protocol.py:257-448) on the
  * device - the comparator the north star reports zero-copy against.  The

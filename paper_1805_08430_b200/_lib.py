@@ -113,6 +113,10 @@ SIGNATURES = {
     "srf_ps_persistent": (C.c_int, [vp, vp, vp, P(vp), C.c_int, vp, u64, C.c_uint32, C.c_int]),
     "srf_batch_gen_set_meta": (C.c_int, [vp, C.c_int, P(C.c_int), vp]),
     "srf_dyn_recv": (C.c_int, [vp, u64, C.c_int, vp, u64, u64, u64, u64, u64, u64, vp]),
+    "srf_torch_pool_attach": (C.c_int, [vp, u64, u64]),
+    "srf_torch_pool_stats": (C.c_int, [C.c_int, P(u64), P(u64), P(u64)]),
+    "srf_torch_malloc": (vp, [C.c_ssize_t, C.c_int, vp]),
+    "srf_torch_free": (None, [vp, C.c_ssize_t, C.c_int, vp]),
     "srf_batch_gen_set_offsets": (C.c_int, [vp, P(u64)]),
     "srf_ps_exchange_create": (C.c_int, [vp, P(u64), vp, P(u64), P(vp), C.c_int, P(u64),
                                          P(vp)]),

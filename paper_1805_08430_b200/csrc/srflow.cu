@@ -20,8 +20,10 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -1743,6 +1745,20 @@ static int put_via_copy_engine(const PutArgs &a, srf_stream *s) {
   return launch_check("k_put(tail)");
 }
 
+// Restores the caller's current device when an API call returns: entry
+// points switch to the device of the objects they touch, and a caller (torch
+// with device="cuda") must not see that switch.
+struct DeviceGuard {
+  int dev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+  }
+  ~DeviceGuard() {
+    int now = -1;
+    if (dev >= 0 && cudaGetDevice(&now) == cudaSuccess && now != dev) cudaSetDevice(dev);
+  }
+};
+
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
@@ -1752,6 +1768,7 @@ const char *srf_last_error(void) { return g_last_error.c_str(); }
 int srf_version(void) { return 1; }
 
 int srf_tune(int knob, int value) {
+  DeviceGuard device_guard;
   switch (knob) {
     case 0:
       if (value < 1 || value > 32) return fail(SRF_E_INVALID_CONFIG, "ctas_per_sm");
@@ -1802,17 +1819,179 @@ int srf_tune(int knob, int value) {
 uint64_t srf_launch_count(void) { return g_launches.load(); }
 
 int srf_host_alloc(uint64_t nbytes, void **out) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaHostAlloc(out, nbytes ? nbytes : 1, cudaHostAllocPortable));
   memset(*out, 0, nbytes ? nbytes : 1);
   return SRF_OK;
 }
 
 int srf_host_free(void *p) {
+  DeviceGuard device_guard;
   if (p) cudaFreeHost(p);
   return SRF_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Registered pool for torch's CUDA allocator: torch tensors
+// are born inside a registered region, so any of them is a zero-copy source
+// or destination of a one-sided verb (analyzer.py:226-272 generalised beyond
+// the synthetic producers).  First fit over an offset-ordered free map with
+// coalescing; a freed block returns to the map only once the work queued on
+// the freeing stream has passed it (event), like the caching allocator's
+// stream-ordered reuse.
+// ---------------------------------------------------------------------------
+struct TorchPool {
+  srf_space *sp = nullptr;
+  uint64_t base = 0, cap = 0;  // region [base, base + cap) of sp
+  std::map<uint64_t, uint64_t> free_;        // offset -> length
+  std::unordered_map<uint64_t, uint64_t> live;
+  struct Pending { uint64_t off, len; cudaEvent_t ev; };
+  std::vector<Pending> pending;
+  uint64_t in_use = 0, peak = 0;
+  std::mutex mu;
+};
+static TorchPool *g_tpool[64] = {nullptr};
+static constexpr uint64_t kTorchAlign = 512;
+
+static void tpool_insert_free(TorchPool *p, uint64_t off, uint64_t len) {
+  auto it = p->free_.emplace(off, len).first;
+  auto nx = std::next(it);
+  if (nx != p->free_.end() && it->first + it->second == nx->first) {
+    it->second += nx->second;
+    p->free_.erase(nx);
+  }
+  if (it != p->free_.begin()) {
+    auto pv = std::prev(it);
+    if (pv->first + pv->second == it->first) {
+      pv->second += it->second;
+      p->free_.erase(it);
+    }
+  }
+}
+
+static void tpool_reclaim(TorchPool *p, bool wait) {
+  size_t k = 0;
+  for (auto &q : p->pending) {
+    if (wait) cudaEventSynchronize(q.ev);
+    if (cudaEventQuery(q.ev) == cudaSuccess) {
+      cudaEventDestroy(q.ev);
+      tpool_insert_free(p, q.off, q.len);
+    } else {
+      p->pending[k++] = q;
+    }
+  }
+  p->pending.resize(k);
+}
+
+int srf_torch_pool_attach(srf_space_t sp, uint64_t region_addr, uint64_t length) {
+  DeviceGuard device_guard;
+  if (!sp || sp->imported) return fail(SRF_E_INVALID_CONFIG, "torch pool needs a local space");
+  int rc = check_raw(sp, region_addr, length, "torch pool");
+  if (rc) return rc;
+  if (sp->device < 0 || sp->device >= 64 || g_tpool[sp->device])
+    return fail(SRF_E_INVALID_CONFIG, "GPU %d already has a torch pool", sp->device);
+  TorchPool *p = new TorchPool();
+  p->sp = sp;
+  const uint64_t a0 = (region_addr + kTorchAlign - 1) / kTorchAlign * kTorchAlign;
+  p->base = a0;
+  p->cap = (region_addr + length - a0) / kTorchAlign * kTorchAlign;
+  p->free_.emplace(0, p->cap);
+  g_tpool[sp->device] = p;
+  return SRF_OK;
+}
+
+int srf_torch_pool_stats(int device, uint64_t *in_use, uint64_t *peak, uint64_t *capacity) {
+  DeviceGuard device_guard;
+  if (device < 0 || device >= 64 || !g_tpool[device])
+    return fail(SRF_E_INVALID_CONFIG, "no torch pool on GPU %d", device);
+  TorchPool *p = g_tpool[device];
+  std::lock_guard<std::mutex> g(p->mu);
+  *in_use = p->in_use;
+  *peak = p->peak;
+  *capacity = p->cap;
+  return SRF_OK;
+}
+
+void *srf_torch_malloc(ssize_t size, int device, void *stream) {
+  (void)stream;
+  if (size < 0 || device < 0 || device >= 64) return nullptr;
+  if (!g_tpool[device]) {
+    // a GPU without a pool: plain device memory (torch works, nothing registered)
+    void *q = nullptr;
+    if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&q, std::max<ssize_t>(size, 1)) !=
+        cudaSuccess)
+      return nullptr;
+    return q;
+  }
+  TorchPool *p = g_tpool[device];
+  const uint64_t len = std::max<uint64_t>(kTorchAlign,
+                                          ((uint64_t)size + kTorchAlign - 1) / kTorchAlign *
+                                              kTorchAlign);
+  std::lock_guard<std::mutex> g(p->mu);
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    tpool_reclaim(p, attempt == 1);
+    for (auto it = p->free_.begin(); it != p->free_.end(); ++it) {
+      if (it->second < len) continue;
+      const uint64_t off = it->first, rest = it->second - len;
+      p->free_.erase(it);
+      if (rest) p->free_.emplace(off + len, rest);
+      p->live[off] = len;
+      p->in_use += len;
+      p->peak = std::max(p->peak, p->in_use);
+      return p->sp->base + p->base + off;
+    }
+  }
+  // pool exhausted: ordinary device memory (the tensor works; a zero-copy
+  // verb on it is refused as NotRegistered by the region checks)
+  void *q = nullptr;
+  if (cudaSetDevice(device) == cudaSuccess && cudaMalloc(&q, (size_t)size) == cudaSuccess)
+    return q;
+  if (getenv("SRFLOW_TPOOL_DEBUG")) {
+    uint64_t largest = 0, total = 0;
+    for (auto &kv : p->free_) { largest = std::max(largest, kv.second); total += kv.second; }
+    fprintf(stderr, "srf_torch_malloc(%zd): no block; free %llu in %zu blocks (largest %llu), "
+            "pending %zu, in use %llu\n", size, (unsigned long long)total, p->free_.size(),
+            (unsigned long long)largest, p->pending.size(), (unsigned long long)p->in_use);
+  }
+  return nullptr;
+}
+
+void srf_torch_free(void *ptr, ssize_t size, int device, void *stream_) {
+  DeviceGuard device_guard;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  (void)size;
+  if (!ptr || device < 0 || device >= 64) return;
+  TorchPool *p = g_tpool[device];
+  if (!p || (uint8_t *)ptr < p->sp->base + p->base ||
+      (uint8_t *)ptr >= p->sp->base + p->base + p->cap) {
+    cudaSetDevice(device);
+    cudaFree(ptr);  // plain memory of a GPU without a pool
+    return;
+  }
+  const uint64_t off = (uint64_t)((uint8_t *)ptr - (p->sp->base + p->base));
+  std::lock_guard<std::mutex> g(p->mu);
+  auto it = p->live.find(off);
+  if (it == p->live.end()) return;
+  const uint64_t len = it->second;
+  p->live.erase(it);
+  p->in_use -= len;
+  cudaEvent_t ev = nullptr;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(device);
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess &&
+      cudaEventRecord(ev, stream) == cudaSuccess) {
+    p->pending.push_back({off, len, ev});
+  } else {
+    if (ev) cudaEventDestroy(ev);
+    cudaStreamSynchronize(stream);
+    tpool_insert_free(p, off, len);
+  }
+  cudaSetDevice(cur);
+}
+
 int srf_device_count(int *count) {
+  DeviceGuard device_guard;
   int n = 0;
   cudaError_t e = cudaGetDeviceCount(&n);
   if (e != cudaSuccess) {
@@ -1825,6 +2004,7 @@ int srf_device_count(int *count) {
 
 int srf_space_create(int server_id, int cuda_device, uint64_t capacity,
                      uint32_t max_regions, srf_space_t *out) {
+  DeviceGuard device_guard;
   if (capacity == 0) return fail(SRF_E_ZERO_LENGTH, "capacity must be >= 1");
   CUDA_TRY(cudaSetDevice(cuda_device));
   srf_space *sp = new srf_space();
@@ -1884,6 +2064,7 @@ int srf_space_create(int server_id, int cuda_device, uint64_t capacity,
 }
 
 int srf_space_destroy(srf_space_t sp) {
+  DeviceGuard device_guard;
   if (!sp) return SRF_OK;
   cudaSetDevice(sp->device);
   free_stream(sp->stream);
@@ -1905,6 +2086,7 @@ int srf_space_destroy(srf_space_t sp) {
 
 int srf_space_info(srf_space_t sp, int *server_id, int *cuda_device,
                    uint64_t *capacity, void **device_base) {
+  DeviceGuard device_guard;
   if (server_id) *server_id = sp->server_id;
   if (cuda_device) *cuda_device = sp->device;
   if (capacity) *capacity = sp->capacity;
@@ -1916,6 +2098,7 @@ void *srf_space_cuda_stream(srf_space_t sp) { return (void *)sp->stream->s; }
 
 int srf_region_alloc(srf_space_t sp, uint64_t length, int registered,
                      uint64_t token, int64_t *region_id, uint64_t *base) {
+  DeviceGuard device_guard;
   if (length < 1)
     return fail(SRF_E_ZERO_LENGTH, "region length must be >= 1, got %llu",
                 (unsigned long long)length);
@@ -1940,6 +2123,7 @@ int srf_region_alloc(srf_space_t sp, uint64_t length, int registered,
 
 int srf_region_import(srf_space_t proxy, int64_t region_id, uint64_t base,
                       uint64_t length, int registered, uint64_t token) {
+  DeviceGuard device_guard;
   std::lock_guard<std::mutex> g(proxy->mu);
   if (base + length > proxy->capacity)
     return fail(SRF_E_OUT_OF_BOUNDS, "imported region escapes space");
@@ -1950,12 +2134,14 @@ int srf_region_import(srf_space_t proxy, int64_t region_id, uint64_t base,
 }
 
 int srf_region_count(srf_space_t sp, uint32_t *count) {
+  DeviceGuard device_guard;
   std::lock_guard<std::mutex> g(sp->mu);
   *count = (uint32_t)sp->regions.size();
   return SRF_OK;
 }
 
 int srf_next_addr(srf_space_t sp, uint64_t *next_addr) {
+  DeviceGuard device_guard;
   std::lock_guard<std::mutex> g(sp->mu);
   *next_addr = sp->next_addr;
   return SRF_OK;
@@ -1963,17 +2149,20 @@ int srf_next_addr(srf_space_t sp, uint64_t *next_addr) {
 
 int srf_check_remote(srf_space_t sp, uint64_t addr, uint64_t length,
                      uint64_t token) {
+  DeviceGuard device_guard;
   std::lock_guard<std::mutex> g(sp->mu);
   return check_remote_locked(sp, addr, length, token);
 }
 
 int srf_check_registered(srf_space_t sp, uint64_t addr, uint64_t length,
                          uint64_t token) {
+  DeviceGuard device_guard;
   std::lock_guard<std::mutex> g(sp->mu);
   return check_registered_locked(sp, addr, length, token);
 }
 
 int srf_read(srf_space_t sp, uint64_t addr, uint64_t length, void *host_dst) {
+  DeviceGuard device_guard;
   int rc = check_raw(sp, addr, length, "read");
   if (rc) return rc;
   if (length == 0) return SRF_OK;
@@ -1986,6 +2175,7 @@ int srf_read(srf_space_t sp, uint64_t addr, uint64_t length, void *host_dst) {
 
 int srf_write(srf_space_t sp, uint64_t addr, uint64_t length,
               const void *host_src) {
+  DeviceGuard device_guard;
   int rc = check_raw(sp, addr, length, "write");
   if (rc) return rc;
   if (length == 0) return SRF_OK;
@@ -1998,6 +2188,7 @@ int srf_write(srf_space_t sp, uint64_t addr, uint64_t length,
 
 int srf_write_async(srf_space_t sp, uint64_t addr, uint64_t length,
                     const void *host_src, srf_stream_t st) {
+  DeviceGuard device_guard;
   int rc = check_raw(sp, addr, length, "write");
   if (rc) return rc;
   if (length == 0) return SRF_OK;
@@ -2010,6 +2201,7 @@ int srf_write_async(srf_space_t sp, uint64_t addr, uint64_t length,
 
 int srf_read_async(srf_space_t sp, uint64_t addr, uint64_t length,
                    void *host_dst, srf_stream_t st) {
+  DeviceGuard device_guard;
   int rc = check_raw(sp, addr, length, "read");
   if (rc) return rc;
   if (length == 0) return SRF_OK;
@@ -2021,6 +2213,7 @@ int srf_read_async(srf_space_t sp, uint64_t addr, uint64_t length,
 }
 
 int srf_device_ptr(srf_space_t sp, uint64_t addr, void **dptr) {
+  DeviceGuard device_guard;
   int rc = check_raw(sp, addr, 0, "view");
   if (rc) return rc;
   *dptr = sp->base + addr;
@@ -2028,6 +2221,7 @@ int srf_device_ptr(srf_space_t sp, uint64_t addr, void **dptr) {
 }
 
 int srf_space_sync(srf_space_t sp) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaSetDevice(sp->device));
   CUDA_TRY(cudaStreamSynchronize(sp->stream->s));
   int err = 0;
@@ -2049,6 +2243,7 @@ int srf_space_sync(srf_space_t sp) {
 }
 
 int srf_connect(srf_space_t a, srf_space_t b) {
+  DeviceGuard device_guard;
   if (a->device == b->device) return SRF_OK;
   int can_ab = 0, can_ba = 0;
   CUDA_TRY(cudaDeviceCanAccessPeer(&can_ab, a->device, b->device));
@@ -2070,6 +2265,7 @@ int srf_connect(srf_space_t a, srf_space_t b) {
 }
 
 int srf_enable_peer(int device, int peer_device) {
+  DeviceGuard device_guard;
   if (device == peer_device) return SRF_OK;
   CUDA_TRY(cudaSetDevice(device));
   cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
@@ -2084,6 +2280,7 @@ int srf_enable_peer(int device, int peer_device) {
 }
 
 int srf_space_export_fd(srf_space_t sp, int *fd) {
+  DeviceGuard device_guard;
   if (!sp->vmm || sp->imported)
     return fail(SRF_E_INVALID_CONFIG, "fd export needs a VMM-allocated local space");
   sp->exported = true;
@@ -2101,6 +2298,7 @@ int srf_space_export_fd(srf_space_t sp, int *fd) {
 
 int srf_space_import_fd(int fd, int server_id, int local_device, uint64_t capacity,
                         srf_space_t *out) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaSetDevice(local_device));
   cudaFree(0);
   auto imp = drv<PFN_import>("cuMemImportFromShareableHandle");
@@ -2139,6 +2337,7 @@ int srf_space_import_fd(int fd, int server_id, int local_device, uint64_t capaci
 }
 
 int srf_space_export(srf_space_t sp, void *handle64) {
+  DeviceGuard device_guard;
   static_assert(sizeof(cudaIpcMemHandle_t) == 64, "ipc handle size");
   if (sp->imported) return fail(SRF_E_INVALID_CONFIG, "cannot re-export a proxy");
   if (sp->vmm) return fail(SRF_E_INVALID_CONFIG, "VMM pools export by fd (srf_space_export_fd)");
@@ -2152,6 +2351,7 @@ int srf_space_export(srf_space_t sp, void *handle64) {
 
 int srf_space_import(const void *handle64, int server_id, int local_device,
                      uint64_t capacity, srf_space_t *out) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaSetDevice(local_device));
   cudaIpcMemHandle_t h;
   memcpy(&h, handle64, sizeof h);
@@ -2186,10 +2386,12 @@ int srf_space_import(const void *handle64, int server_id, int local_device,
 }
 
 int srf_stream_create(srf_space_t sp, srf_stream_t *out) {
+  DeviceGuard device_guard;
   return make_stream(sp->device, true, nullptr, out);
 }
 
 int srf_stream_destroy(srf_stream_t st) {
+  DeviceGuard device_guard;
   free_stream(st);
   return SRF_OK;
 }
@@ -2197,18 +2399,21 @@ int srf_stream_destroy(srf_stream_t st) {
 void *srf_stream_cuda(srf_stream_t st) { return (void *)st->s; }
 
 int srf_stream_sync(srf_stream_t st) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaSetDevice(st->device));
   CUDA_TRY(cudaStreamSynchronize(st->s));
   return SRF_OK;
 }
 
 int srf_event_record(srf_space_t sp, srf_stream_t st, srf_event_t *out) {
+  DeviceGuard device_guard;
   srf_stream *s = stream_or_default(sp, st);
   CUDA_TRY(cudaSetDevice(s->device));
   return record_event(s->device, s->s, out);
 }
 
 int srf_event_query(srf_event_t ev) {
+  DeviceGuard device_guard;
   cudaError_t e = cudaEventQuery(ev->e);
   if (e == cudaSuccess) return SRF_OK;
   if (e == cudaErrorNotReady) return SRF_PENDING;
@@ -2216,11 +2421,13 @@ int srf_event_query(srf_event_t ev) {
 }
 
 int srf_event_wait(srf_event_t ev) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaEventSynchronize(ev->e));
   return SRF_OK;
 }
 
 int srf_event_free(srf_event_t ev) {
+  DeviceGuard device_guard;
   if (!ev) return SRF_OK;
   cudaEventDestroy(ev->e);
   delete ev;
@@ -2231,6 +2438,7 @@ int srf_put(srf_space_t src_space, const uint64_t *src_addr,
             const uint64_t *src_len, const uint64_t *src_token, int nseg,
             srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
             int flags, srf_stream_t st, srf_event_t *ev_out) {
+  DeviceGuard device_guard;
   if (nseg < 1 || nseg > kMaxSeg)
     return fail(SRF_E_INVALID_CONFIG, "gather list of %d segments (max %d)",
                 nseg, kMaxSeg);
@@ -2303,6 +2511,7 @@ int srf_put(srf_space_t src_space, const uint64_t *src_addr,
 int srf_get(srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
             srf_space_t src_space, uint64_t src_addr, uint64_t src_token,
             uint64_t length, srf_stream_t st, srf_event_t *ev_out) {
+  DeviceGuard device_guard;
   if (length < 1) return fail(SRF_E_INVALID_LENGTH, "zero-length read");
   {
     std::lock_guard<std::mutex> g(dst_space->mu);
@@ -2339,6 +2548,7 @@ int srf_get(srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
 
 int srf_copy(srf_space_t sp, uint64_t src_addr, uint64_t dst_addr,
              uint64_t length, srf_stream_t st, srf_event_t *ev_out) {
+  DeviceGuard device_guard;
   if (length == 0) return SRF_OK;
   int rc = check_raw(sp, src_addr, length, "copy src");
   if (!rc) rc = check_raw(sp, dst_addr, length, "copy dst");
@@ -2361,6 +2571,7 @@ int srf_copy(srf_space_t sp, uint64_t src_addr, uint64_t dst_addr,
 
 int srf_flag_wait(srf_space_t sp, uint64_t flag_addr, uint8_t expect,
                   int clear, uint64_t timeout_ns, srf_stream_t st) {
+  DeviceGuard device_guard;
   int rc = check_raw(sp, flag_addr, 1, "flag");
   if (rc) return rc;
   srf_stream *s = stream_or_default(sp, st);
@@ -2373,6 +2584,7 @@ int srf_flag_wait(srf_space_t sp, uint64_t flag_addr, uint8_t expect,
 int srf_dyn_recv(srf_space_t rcv, uint64_t meta_addr, int rank, srf_space_t peer,
                  uint64_t peer_lo, uint64_t peer_hi, uint64_t peer_token, uint64_t dst_addr,
                  uint64_t dst_cap, uint64_t len_out_addr, srf_stream_t st) {
+  DeviceGuard device_guard;
   if (rank < 0 || rank > 64) return fail(SRF_E_INVALID_CONFIG, "rank %d", rank);
   int rc = check_raw(rcv, meta_addr, 8 * (uint64_t)rank + 33, "meta block");
   if (!rc && dst_cap) rc = check_raw(rcv, dst_addr, dst_cap, "receive block");
@@ -2408,6 +2620,7 @@ int srf_dyn_recv(srf_space_t rcv, uint64_t meta_addr, int rank, srf_space_t peer
 int srf_consume_checksum(srf_space_t sp, uint64_t flag_addr, uint64_t data_addr,
                          uint64_t n, uint64_t out_addr, uint64_t timeout_ns,
                          srf_stream_t st) {
+  DeviceGuard device_guard;
   int rc = check_raw(sp, flag_addr, 1, "flag");
   if (!rc) rc = check_raw(sp, data_addr, n, "payload");
   if (!rc) rc = check_raw(sp, out_addr, 8, "checksum");
@@ -2425,6 +2638,7 @@ int srf_apply(srf_space_t var_space, uint64_t var_addr, uint64_t nbytes,
               srf_space_t const *grad_spaces, const uint64_t *grad_addrs,
               int nworkers, int op, float lr, srf_stream_t st,
               srf_event_t *ev_out) {
+  DeviceGuard device_guard;
   if (nworkers < 1 || nworkers > SRF_MAX_WORKERS)
     return fail(SRF_E_INVALID_CONFIG, "nworkers %d outside [1, %d]", nworkers,
                 SRF_MAX_WORKERS);
@@ -2463,6 +2677,7 @@ int srf_apply(srf_space_t var_space, uint64_t var_addr, uint64_t nbytes,
 
 int srf_reduce_max_f32(srf_space_t sp, uint64_t in_addr, uint64_t n,
                        uint64_t out_addr, srf_stream_t st) {
+  DeviceGuard device_guard;
   int rc = check_raw(sp, in_addr, n * 4, "reduce input");
   if (!rc) rc = check_raw(sp, out_addr, 4, "reduce output");
   if (rc) return rc;
@@ -2614,6 +2829,7 @@ int srf_batch_put_create(int n, srf_space_t const *src_space, const uint64_t *sr
                          const uint64_t *tail_addr, srf_space_t const *dst_space,
                          const uint64_t *dst_addr, const uint64_t *dst_token, int flags,
                          srf_batch_t *out) {
+  DeviceGuard device_guard;
   if (n < 1) return fail(SRF_E_INVALID_CONFIG, "empty batch");
   int device = src_space[0]->device;
   std::vector<BatchPut> host(n);
@@ -2663,6 +2879,7 @@ int srf_batch_gen_create(int n, srf_space_t const *space, const uint64_t *grad_a
                          const uint64_t *nbytes, const uint64_t *weight_flag_addr,
                          srf_space_t const *credit_space, const uint64_t *credit_addr,
                          const uint64_t *node_id, uint64_t seed, srf_batch_t *out) {
+  DeviceGuard device_guard;
   if (n < 1) return fail(SRF_E_INVALID_CONFIG, "empty batch");
   const int device = space[0]->device;
   std::vector<BatchGen> host(n);
@@ -2706,6 +2923,7 @@ int srf_batch_apply_create(srf_space_t sp, int nvars, const uint64_t *var_addr,
                            const int *is_meta, srf_space_t const *peer_space,
                            const uint64_t *peer_lo, const uint64_t *peer_hi,
                            const uint64_t *peer_token, int op, float lr, srf_batch_t *out) {
+  DeviceGuard device_guard;
   if (nvars < 1) return fail(SRF_E_INVALID_CONFIG, "empty batch");
   if (op != SRF_APPLY_XOR && op != SRF_APPLY_SGD)
     return fail(SRF_E_INVALID_CONFIG, "unknown apply op %d", op);
@@ -2762,6 +2980,7 @@ int srf_batch_apply_create(srf_space_t sp, int nvars, const uint64_t *var_addr,
 
 int srf_batch_launch(srf_batch_t b, srf_stream_t st, uint64_t iteration, int mode,
                      int grid_cap) {
+  DeviceGuard device_guard;
   const uint64_t timeout = 10ull * 1000 * 1000 * 1000;
   const uint32_t units = (uint32_t)b->grid;
   const int grid = (int)(grid_cap > 0 ? std::min<uint32_t>(units, (uint32_t)grid_cap) : units);
@@ -2822,6 +3041,7 @@ int srf_batch_launch(srf_batch_t b, srf_stream_t st, uint64_t iteration, int mod
 __global__ void k_counter_add(uint64_t *p, uint64_t delta) { *p += delta; }
 
 int srf_batch_set_iteration_source(srf_batch_t b, srf_space_t sp, uint64_t addr) {
+  DeviceGuard device_guard;
   int rc = check_raw(sp, addr, 8, "iteration counter");
   if (rc) return rc;
   if (addr % 8) return fail(SRF_E_INVALID_CONFIG, "counter must be 8-B aligned");
@@ -2830,6 +3050,7 @@ int srf_batch_set_iteration_source(srf_batch_t b, srf_space_t sp, uint64_t addr)
 }
 
 int srf_counter_add(srf_space_t sp, uint64_t addr, uint64_t delta, srf_stream_t st) {
+  DeviceGuard device_guard;
   int rc = check_raw(sp, addr, 8, "counter");
   if (rc) return rc;
   srf_stream *s = stream_or_default(sp, st);
@@ -2841,6 +3062,7 @@ int srf_counter_add(srf_space_t sp, uint64_t addr, uint64_t delta, srf_stream_t 
 int srf_ps_persistent(srf_batch_t push, srf_batch_t gen, srf_batch_t meta,
                       srf_batch_t const *apply, int napply, srf_stream_t st, uint64_t it0,
                       uint32_t iters, int mode) {
+  DeviceGuard device_guard;
   if (napply < 0 || napply > kMaxApply)
     return fail(SRF_E_INVALID_CONFIG, "at most %d apply batches", kMaxApply);
   srf_batch *all[3] = {push, gen, meta};
@@ -2888,6 +3110,7 @@ int srf_ps_persistent(srf_batch_t push, srf_batch_t gen, srf_batch_t meta,
 }
 
 int srf_batch_gen_set_offsets(srf_batch_t gen, const uint64_t *elem_offset) {
+  DeviceGuard device_guard;
   if (!gen || gen->kind != 1) return fail(SRF_E_INVALID_CONFIG, "not a gen batch");
   BatchGen *g = (BatchGen *)gen->host.data();
   for (int i = 0; i < gen->n; ++i) {
@@ -2901,6 +3124,7 @@ int srf_batch_gen_set_offsets(srf_batch_t gen, const uint64_t *elem_offset) {
 }
 
 int srf_batch_gen_set_meta(srf_batch_t gen, int n, const int *gen_index, srf_batch_t meta) {
+  DeviceGuard device_guard;
   if (!gen || gen->kind != 1 || !meta || meta->kind != 0 || n != meta->n)
     return fail(SRF_E_INVALID_CONFIG, "gen_set_meta: a gen batch and a put batch of n edges");
   BatchGen *g = (BatchGen *)gen->host.data();
@@ -2921,6 +3145,7 @@ int srf_batch_gen_set_meta(srf_batch_t gen, int n, const int *gen_index, srf_bat
 }
 
 int srf_batch_destroy(srf_batch_t b) {
+  DeviceGuard device_guard;
   if (!b) return SRF_OK;
   cudaSetDevice(b->device);
   cudaFree(b->descs);
@@ -2952,6 +3177,7 @@ struct srf_exchange {
 int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch_t gen,
                            const uint64_t *gen_key, srf_batch_t const *apply, int napply,
                            const uint64_t *apply_key, srf_exchange_t *out) {
+  DeviceGuard device_guard;
   if (napply < 0 || napply > kMaxApply)
     return fail(SRF_E_INVALID_CONFIG, "at most %d apply batches", kMaxApply);
   if ((push && push->kind != 0) || (gen && gen->kind != 1))
@@ -3043,6 +3269,7 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
 }
 
 int srf_ps_exchange_launch(srf_exchange_t x, srf_stream_t st, uint64_t iteration, int regen) {
+  DeviceGuard device_guard;
   if (st->device != x->device) return fail(SRF_E_INVALID_CONFIG, "exchange: stream GPU");
   x->args.iteration = iteration;
   x->args.regen = regen;
@@ -3052,6 +3279,7 @@ int srf_ps_exchange_launch(srf_exchange_t x, srf_stream_t st, uint64_t iteration
 }
 
 int srf_ps_exchange_destroy(srf_exchange_t x) {
+  DeviceGuard device_guard;
   if (!x) return SRF_OK;
   cudaSetDevice(x->device);
   cudaFree(x->items);
@@ -3064,6 +3292,7 @@ int srf_ps_exchange_destroy(srf_exchange_t x) {
 // doorbells (host-visible receive flags)
 // ---------------------------------------------------------------------------
 int srf_doorbell_bind(srf_space_t sp, uint64_t region_addr, uint64_t region_len, int mirror) {
+  DeviceGuard device_guard;
   if (region_len < 1) return fail(SRF_E_ZERO_LENGTH, "doorbell region must be >= 1 byte");
   int rc = check_raw(sp, region_addr, region_len, "doorbell region");
   if (rc) return rc;
@@ -3103,6 +3332,7 @@ int srf_doorbell_bind(srf_space_t sp, uint64_t region_addr, uint64_t region_len,
 // Read `len` bytes ending at tail_addr + 1: from the doorbell shadow when one
 // is bound and every producer is in this process, else from the device.
 int srf_flag_read(srf_space_t sp, uint64_t tail_addr, uint64_t len, void *host_out) {
+  DeviceGuard device_guard;
   if (sp->db && !sp->exported) {
     std::lock_guard<std::mutex> g(sp->mu);
     auto it = sp->db->find(tail_addr);
@@ -3126,6 +3356,7 @@ int srf_flag_read(srf_space_t sp, uint64_t tail_addr, uint64_t len, void *host_o
 // byte asynchronously on the space's stream; the next srf_put into the region
 // waits for that clear.
 int srf_flag_clear(srf_space_t sp, uint64_t tail_addr) {
+  DeviceGuard device_guard;
   int rc = check_raw(sp, tail_addr, 1, "flag");
   if (rc) return rc;
   if (sp->db) {
@@ -3151,6 +3382,7 @@ int srf_rpc_transfer(srf_space_t src, uint64_t meta_addr, uint32_t meta_len,
                      srf_space_t dst, uint64_t ring_addr, uint64_t ring_flags_addr,
                      uint64_t meta_out_addr, uint64_t tensor_out_addr, uint64_t msg_id,
                      srf_stream_t st_src, srf_stream_t st_dst) {
+  DeviceGuard device_guard;
   int rc = check_raw(src, meta_addr, meta_len, "rpc meta");
   if (!rc) rc = check_raw(src, payload_addr, payload_len, "rpc payload");
   if (!rc) rc = check_raw(src, stage_addr, (uint64_t)kRing * kFrag, "rpc stage");
@@ -3198,12 +3430,14 @@ int srf_rpc_transfer(srf_space_t src, uint64_t meta_addr, uint32_t meta_len,
 }
 
 int srf_graph_begin(srf_stream_t st) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaSetDevice(st->device));
   CUDA_TRY(cudaStreamBeginCapture(st->s, cudaStreamCaptureModeThreadLocal));
   return SRF_OK;
 }
 
 int srf_graph_end(srf_stream_t st, void **graph_exec) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaSetDevice(st->device));
   cudaGraph_t g = nullptr;
   CUDA_TRY(cudaStreamEndCapture(st->s, &g));
@@ -3217,23 +3451,27 @@ int srf_graph_end(srf_stream_t st, void **graph_exec) {
 }
 
 int srf_graph_launch(void *graph_exec, srf_stream_t st) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaSetDevice(st->device));
   CUDA_TRY(cudaGraphLaunch((cudaGraphExec_t)graph_exec, st->s));
   return SRF_OK;
 }
 
 int srf_graph_destroy(void *graph_exec) {
+  DeviceGuard device_guard;
   if (graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)graph_exec);
   return SRF_OK;
 }
 
 int srf_stream_wait_event(srf_stream_t st, srf_event_t ev) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaSetDevice(st->device));
   CUDA_TRY(cudaStreamWaitEvent(st->s, ev->e, 0));
   return SRF_OK;
 }
 
 int srf_timing_event_create(srf_space_t sp, srf_event_t *out) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaSetDevice(sp->device));
   srf_event *ev = new srf_event();
   ev->device = sp->device;
@@ -3247,12 +3485,14 @@ int srf_timing_event_create(srf_space_t sp, srf_event_t *out) {
 }
 
 int srf_event_record_on(srf_event_t ev, srf_stream_t st) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaSetDevice(st->device));
   CUDA_TRY(cudaEventRecord(ev->e, st->s));
   return SRF_OK;
 }
 
 int srf_event_elapsed_ms(srf_event_t start, srf_event_t end, float *ms) {
+  DeviceGuard device_guard;
   CUDA_TRY(cudaEventElapsedTime(ms, start->e, end->e));
   return SRF_OK;
 }

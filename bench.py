@@ -850,7 +850,7 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
     clocks.start()
     barrier_sync()
     graph = None
-    if (not ps.overlap and ps.schedule == "phases" and not persistent
+    if (ps.schedule == "phases" and not persistent
             and os.environ.get("SRFLOW_PS_GRAPH") == "1"):
         # optional: replay the timed iterations as one CUDA graph (the gen batch
         # takes the iteration from a device counter).  Measured slower than
@@ -970,8 +970,7 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
            "steps": steps, "model_bytes": model, "roofline": roof, "gpu_launches": launches,
            "clocks": clk, "verified": ok, "verification": how,
            "phases": "K1 weight push batch, GenGrad batch, K3 meta batch, K4+K6 fused apply",
-           "schedule": ("overlapped (3 streams, capped grids)" if ps.overlap else
-                        "one stream, CUDA graph" if graph is not None else
+           "schedule": ("one stream, CUDA graph" if graph is not None else
                         "one persistent cooperative launch (grid barriers between phases)"
                         if persistent else
                         "exchange: one k_ps_exchange launch per step (dependency-ordered "

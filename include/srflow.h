@@ -61,8 +61,7 @@ uint64_t srf_launch_count(void);
  * 1 TMA bulk), 3 = pool allocator (0 cudaMalloc + CUDA IPC, 1 VMM + fd),
  * 4 = 16-B vectors in flight per thread (4 or 8), 5 = 32-B vectors (0/1),
  * 6 = cross-device bodies >= value KiB move on the copy engine, the tail
- *     flag still released by an SM store after them (0 = never; default 1024),
- * 7 = PS put batches use the copy engine for such bodies too (0/1; default 0) */
+ *     flag still released by an SM store after them (0 = never; default 1024) */
 int srf_tune(int knob, int value);
 
 /* ---- memory spaces (memspace.py) ----------------------------------------- */
@@ -253,8 +252,7 @@ int srf_batch_apply_create(srf_space_t space, int nvars, const uint64_t *var_add
                            const int *is_meta, srf_space_t const *peer_space,
                            const uint64_t *peer_lo, const uint64_t *peer_hi,
                            const uint64_t *peer_token, int op, float lr, srf_batch_t *out);
-/* grid_cap > 0 bounds the grid (CTAs loop over the batch's work units): the
- * overlapped PS schedule caps every phase so all phases fit on the GPU at once */
+/* grid_cap > 0 bounds the grid (CTAs loop over the batch's work units) */
 int srf_batch_launch(srf_batch_t batch, srf_stream_t stream, uint64_t iteration, int mode,
                      int grid_cap);
 int srf_batch_destroy(srf_batch_t batch);

@@ -157,7 +157,7 @@ def load() -> C.CDLL:
 
 _KNOBS = {"SRFLOW_CTAS_PER_SM": 0, "SRFLOW_COPY_THREADS": 1, "SRFLOW_PUT_IMPL": 2,
           "SRFLOW_ALLOC_VMM": 3, "SRFLOW_UNROLL": 4, "SRFLOW_VEC32": 5,
-          "SRFLOW_PEER_CE_KIB": 6, "SRFLOW_BATCH_CE": 7}
+          "SRFLOW_PEER_CE_KIB": 6}
 
 
 def _apply_env_knobs(lib) -> None:
@@ -172,8 +172,8 @@ def _apply_env_knobs(lib) -> None:
 
 def tune(knob: str, value: int) -> None:
     call("srf_tune", {"ctas_per_sm": 0, "copy_threads": 1, "put_impl": 2,
-                      "alloc_vmm": 3, "unroll": 4, "vec32": 5, "peer_ce_kib": 6,
-                      "batch_ce": 7}[knob], value)
+                      "alloc_vmm": 3, "unroll": 4, "vec32": 5,
+                      "peer_ce_kib": 6}[knob], value)
 
 
 def last_error() -> str:

@@ -1043,10 +1043,8 @@ struct BatchPut {        // K1/K3 over many edges
   uint64_t body;         // bytes before the tail
   const uint8_t *tail;   // tail byte source (flag cell / meta flag)
   uint32_t cta_begin, cta_count;
-  uint32_t wait_empty, pad;  // pad: kBatchSkip* bits (copy-engine split)
+  uint32_t wait_empty, pad;
 };
-static constexpr uint32_t kBatchSkipBody = 1;  // body moved by the copy engine
-static constexpr uint32_t kBatchSkipTail = 2;  // credit wait only
 
 struct BatchGen {        // worker: consume weight, (re)produce gradient
   uint8_t *grad;
@@ -1118,14 +1116,13 @@ __device__ __forceinline__ void put_unit(const BatchPut *descs, int n, uint32_t 
       if (threadIdx.x == 0 && !spin_until(d.dst + d.body, 0, timeout_ns, sys)) atomicExch(err, 2);
       __syncthreads();
     }
-    if (!(d.pad & kBatchSkipBody))
-      copy_bytes_grid<8>(d.dst, d.src, d.body, (uint64_t)lb * blockDim.x + threadIdx.x,
-                         (uint64_t)d.cta_count * blockDim.x);
+    copy_bytes_grid<8>(d.dst, d.src, d.body, (uint64_t)lb * blockDim.x + threadIdx.x,
+                       (uint64_t)d.cta_count * blockDim.x);
     __syncthreads();
     if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, sys);
     __syncthreads();
     if (s_last && threadIdx.x == 0) {
-      if (!(d.pad & kBatchSkipTail)) release_tail(d.dst + d.body, *d.tail, sys);
+      release_tail(d.dst + d.body, *d.tail, sys);
       atomicExch(&counters[s_desc], 0u);
     }
     __syncthreads();  // shared state is reused by the next unit
@@ -1685,10 +1682,6 @@ static int g_unroll = 8;    // 16-B vectors in flight per thread (4 or 8)
 // across processes; the DMA engine reaches ~750 GB/s through the same mapping
 // (profiles/r1_ring_probe.json, r1_xproc_store_probe*.jsonl).
 static uint64_t g_peer_ce_bytes = 1ull << 20;
-// knob 7: let PS put batches move their cross-device bodies on the copy
-// engine too (0 by default: measured slower for every PS config at N=2,
-// profiles/r1_ps_batch_ce_probe.txt - the SM batch pipelines edge by edge)
-static int g_batch_ce = 0;
 
 // launch K1/K4/K5 with the configured implementation
 static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
@@ -1807,10 +1800,6 @@ int srf_tune(int knob, int value) {
     case 6:
       if (value < 0) return fail(SRF_E_INVALID_CONFIG, "peer_ce_kib >= 0");
       g_peer_ce_bytes = (uint64_t)value << 10;
-      return SRF_OK;
-    case 7:
-      if (value != 0 && value != 1) return fail(SRF_E_INVALID_CONFIG, "batch_ce 0|1");
-      g_batch_ce = value;
       return SRF_OK;
     default:
       return fail(SRF_E_INVALID_CONFIG, "unknown knob %d", knob);
@@ -2708,19 +2697,6 @@ struct srf_batch {
   float lr;
   uint64_t seed;
   int *err;
-  // put batches with cross-device bodies >= knob 6: those bodies move on the
-  // copy engine on a side stream, between a credit-wait launch and a
-  // tail-release launch; the rest runs as the SM batch (sm_descs).  `descs`
-  // keeps every edge on the SM path for the persistent step.
-  void *sm_descs = nullptr;
-  int sm_n = 0, sm_grid = 0;
-  unsigned int *sm_counters = nullptr;
-  void *ce_credit = nullptr, *ce_tail = nullptr;
-  int ce_n = 0;
-  unsigned int *ce_counters = nullptr;
-  std::vector<std::pair<std::pair<uint8_t *, const uint8_t *>, uint64_t>> ce_copies;
-  cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<uint8_t> host;  // host copy of the descriptors
 };
 
@@ -2763,64 +2739,6 @@ static int finish_batch(int kind, int device, std::vector<D> &host, int *err, sr
   return SRF_OK;
 }
 
-template <typename D>
-static int upload(const std::vector<D> &host, void **descs, unsigned int **counters) {
-  const size_t n = std::max<size_t>(1, host.size());
-  cudaError_t e = cudaMalloc(descs, sizeof(D) * n);
-  if (e == cudaSuccess && !host.empty())
-    e = cudaMemcpy(*descs, host.data(), sizeof(D) * host.size(), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMalloc(counters, sizeof(unsigned) * n);
-  if (e == cudaSuccess) e = cudaMemset(*counters, 0, sizeof(unsigned) * n);
-  if (e == cudaSuccess) e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) return fail(SRF_E_DEVICE, "batch upload: %s", cudaGetErrorString(e));
-  return SRF_OK;
-}
-
-// Split a put batch for the hybrid launch (see srf_batch): cross-device bodies
-// of at least g_peer_ce_bytes go to the copy engine.
-static int split_copy_engine(srf_batch *b, const std::vector<BatchPut> &host,
-                             srf_space_t const *dst_space) {
-  std::vector<BatchPut> sm, credit, tail;
-  uint32_t next = 0;
-  for (size_t i = 0; i < host.size(); ++i) {
-    const BatchPut &d = host[i];
-    const bool cross = dst_space[i]->imported || dst_space[i]->device != b->device;
-    if (cross && g_batch_ce && g_peer_ce_bytes && d.body >= g_peer_ce_bytes) {
-      BatchPut c = d;
-      c.cta_begin = (uint32_t)credit.size();
-      c.cta_count = 1;
-      c.pad = kBatchSkipBody | kBatchSkipTail;
-      credit.push_back(c);
-      c.wait_empty = 0;
-      c.pad = kBatchSkipBody;
-      c.cta_begin = 0;  // launched one descriptor at a time
-      tail.push_back(c);
-      b->ce_copies.push_back({{d.dst, d.src}, d.body});
-    } else {
-      BatchPut c = d;
-      c.cta_begin = next;
-      next += c.cta_count;
-      sm.push_back(c);
-    }
-  }
-  if (credit.empty()) return SRF_OK;
-  CUDA_TRY(cudaSetDevice(b->device));
-  int rc = upload(credit, &b->ce_credit, &b->ce_counters);
-  if (!rc) {
-    unsigned int *unused = nullptr;
-    rc = upload(tail, &b->ce_tail, &unused);
-    cudaFree(unused);  // the tail launch shares ce_counters (same stream order)
-  }
-  if (!rc) rc = upload(sm, &b->sm_descs, &b->sm_counters);
-  if (rc) return rc;
-  b->ce_n = (int)credit.size();
-  b->sm_n = (int)sm.size();
-  b->sm_grid = (int)next;
-  CUDA_TRY(cudaStreamCreateWithFlags(&b->side, cudaStreamNonBlocking));
-  CUDA_TRY(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
-  CUDA_TRY(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming));
-  return SRF_OK;
-}
 
 extern "C" {
 
@@ -2866,11 +2784,6 @@ int srf_batch_put_create(int n, srf_space_t const *src_space, const uint64_t *sr
     for (int i = 0; i < n; ++i)
       sys |= (dst_space[i]->imported || dst_space[i]->device != device) ? 1 : 0;
     (*out)->sys = sys;
-    rc0 = split_copy_engine(*out, host, dst_space);
-    if (rc0 != SRF_OK) {
-      srf_batch_destroy(*out);
-      *out = nullptr;
-    }
   }
   return rc0;
 }
@@ -2987,38 +2900,6 @@ int srf_batch_launch(srf_batch_t b, srf_stream_t st, uint64_t iteration, int mod
   CUDA_TRY(cudaSetDevice(st->device));
   switch (b->kind) {
     case 0:
-      if (b->ce_n) {
-        // credit waits (stream st) -> fork -> [copy-engine bodies -> tail
-        // releases] on the side stream, concurrently with the SM batch on st
-        // -> join
-        int rc;
-        const BatchPut *credit = (const BatchPut *)b->ce_credit;
-        k_put_batch<<<b->ce_n, 32, 0, st->s>>>(credit, b->ce_n, (uint32_t)b->ce_n,
-                                               b->ce_counters, timeout, b->err, b->sys);
-        if ((rc = launch_check("k_put_batch(credit)"))) return rc;
-        CUDA_TRY(cudaEventRecord(b->ev_fork, st->s));
-        CUDA_TRY(cudaStreamWaitEvent(b->side, b->ev_fork, 0));
-        // each body's flag is released right after its copy, so receivers
-        // start on early edges while later bodies are still moving
-        for (int i = 0; i < b->ce_n; ++i) {
-          auto &c = b->ce_copies[i];
-          CUDA_TRY(cudaMemcpyAsync(c.first.first, c.first.second, c.second,
-                                   cudaMemcpyDeviceToDevice, b->side));
-          k_put_batch<<<1, 32, 0, b->side>>>((const BatchPut *)b->ce_tail + i, 1, 1u,
-                                             b->ce_counters + i, timeout, b->err, b->sys);
-          if ((rc = launch_check("k_put_batch(tail)"))) return rc;
-        }
-        CUDA_TRY(cudaEventRecord(b->ev_join, b->side));
-        if (b->sm_n) {
-          const uint32_t su = (uint32_t)b->sm_grid;
-          const int sg = (int)(grid_cap > 0 ? std::min<uint32_t>(su, (uint32_t)grid_cap) : su);
-          k_put_batch<<<sg, 512, 0, st->s>>>((const BatchPut *)b->sm_descs, b->sm_n, su,
-                                             b->sm_counters, timeout, b->err, b->sys);
-          if ((rc = launch_check("k_put_batch"))) return rc;
-        }
-        CUDA_TRY(cudaStreamWaitEvent(st->s, b->ev_join, 0));
-        return SRF_OK;
-      }
       k_put_batch<<<grid, 512, 0, st->s>>>((const BatchPut *)b->descs, b->n, units,
                                            b->counters, timeout, b->err, b->sys);
       return launch_check("k_put_batch");
@@ -3150,15 +3031,6 @@ int srf_batch_destroy(srf_batch_t b) {
   cudaSetDevice(b->device);
   cudaFree(b->descs);
   cudaFree(b->counters);
-  if (b->side) cudaStreamSynchronize(b->side);
-  cudaFree(b->sm_descs);
-  cudaFree(b->sm_counters);
-  cudaFree(b->ce_credit);
-  cudaFree(b->ce_tail);
-  cudaFree(b->ce_counters);
-  if (b->side) cudaStreamDestroy(b->side);
-  if (b->ev_fork) cudaEventDestroy(b->ev_fork);
-  if (b->ev_join) cudaEventDestroy(b->ev_join);
   delete b;
   return SRF_OK;
 }
@@ -3182,8 +3054,6 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
     return fail(SRF_E_INVALID_CONFIG, "at most %d apply batches", kMaxApply);
   if ((push && push->kind != 0) || (gen && gen->kind != 1))
     return fail(SRF_E_INVALID_CONFIG, "exchange: batch kinds");
-  if (push && push->ce_n)
-    return fail(SRF_E_INVALID_CONFIG, "exchange: copy-engine put batches are not queued");
   int device = push ? push->device : gen ? gen->device : napply ? apply[0]->device : -1;
   if (device < 0) return fail(SRF_E_INVALID_CONFIG, "exchange: no batches");
   struct K { uint64_t key; uint32_t kind, batch, desc, unit; };

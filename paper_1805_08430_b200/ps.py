@@ -227,7 +227,7 @@ class PsStep:
 
     def __init__(self, layout: PsLayout, *, rank: int = 0, world: int = 1, device: int = 0,
                  seed: int = 0, op: str = "xor", lr: float = 0.01,
-                 overlap: Optional[bool] = None, schedule: str = "phases",
+                 schedule: str = "phases",
                  exchange_lag: Optional[int] = None, exchange_order: Optional[str] = None):
         self.L = layout
         self.rank, self.world, self.device = rank, world, device
@@ -278,18 +278,6 @@ class PsStep:
         for g in self.batches["gen"].values():
             _lib.call("srf_batch_set_iteration_source", g, self.stream_space.handle,
                       self._counter.base_addr)
-        # Overlapped schedule: weight pushes, worker phase and shard apply on
-        # three streams, ordered locally by events and across GPUs by the
-        # device flags.  Only when this rank hosts exactly one server (worker k
-        # + shard k co-located): then every device-side wait is on another
-        # GPU's kernel, and the capped grids (1 CTA/SM per phase) fit on the
-        # GPU together, so no phase can starve the one a peer waits for.
-        # Measured on 2 x B200 (VGG-16, round-robin shards): 259 vs 475 it/s for
-        # the one-stream schedule - a phase's CTAs spin on whole-tensor flags
-        # (fc6 dominates), so capped grids serialise behind the largest
-        # transfer.  Off by default; finer-grained flags would be needed.
-        one_server = len(self.local) == 1 and layout.colocate and world > 1
-        self.overlap = bool(overlap) and one_server
         self._exchange = None
         self._exchange_built = None
         self._exchange_cfg = (
@@ -299,26 +287,6 @@ class PsStep:
              else exchange_order))
         self.schedule = "phases"
         self.use_schedule(schedule)
-        if self.overlap:
-            sp = self.stream_space
-            self._streams = []
-            for _ in range(3):
-                st = C.c_void_p()
-                _lib.call("srf_stream_create", sp.handle, C.byref(st))
-                self._streams.append(st)
-            self._ev = {}
-            for name in ("apply", "gen", "fork", "j0", "j1", "j2"):
-                e = C.c_void_p()
-                _lib.call("srf_timing_event_create", sp.handle, C.byref(e))
-                self._ev[name] = e
-            self._applied = False
-            n_sm = 148
-            try:
-                import torch
-                n_sm = torch.cuda.get_device_properties(device).multi_processor_count
-            except Exception:
-                pass
-            self._cap = n_sm
 
     # -- layout helpers -------------------------------------------------------------
 
@@ -494,8 +462,6 @@ class PsStep:
         if schedule not in ("phases", "exchange"):
             raise errors.InvalidConfig(f"unknown PS schedule {schedule!r}")
         if schedule == "exchange":
-            if self.overlap:
-                raise errors.InvalidConfig("the exchange schedule is one launch per step")
             b = self.batches
             if self._exchange_built is None and (b["push"] is not None or b["gen"]
                                                  or b["apply"]):
@@ -547,8 +513,6 @@ class PsStep:
         if self._exchange is not None:
             _lib.call("srf_ps_exchange_launch", self._exchange, self.stream, iteration, mode)
             return 1
-        if self.overlap:
-            return self._step_overlapped(iteration, mode)
         if b["push"] is not None:
             _lib.call("srf_batch_launch", b["push"], self.stream, iteration, 0, 0)
             n += 1
@@ -563,30 +527,6 @@ class PsStep:
             n += 1
         return n
 
-    def _step_overlapped(self, iteration: int, mode: int) -> int:
-        b, (sa, sb, sc), ev, cap = self.batches, self._streams, self._ev, self._cap
-        n = 0
-        if self._applied:  # the previous update is done before weights/grads change
-            _lib.call("srf_stream_wait_event", sa, ev["apply"])
-            _lib.call("srf_stream_wait_event", sb, ev["apply"])
-        if b["push"] is not None:
-            _lib.call("srf_batch_launch", b["push"], sa, iteration, 0, cap)
-            n += 1
-        for g in b["gen"].values():
-            _lib.call("srf_batch_launch", g, sb, iteration, mode, cap)
-            n += 1
-        _lib.call("srf_event_record_on", ev["gen"], sb)
-        if b["meta"] is not None:
-            _lib.call("srf_batch_launch", b["meta"], sb, iteration, 0, cap)
-            n += 1
-        _lib.call("srf_stream_wait_event", sc, ev["gen"])
-        for a in b["apply"].values():
-            _lib.call("srf_batch_launch", a, sc, iteration, 0, cap)
-            n += 1
-        _lib.call("srf_event_record_on", ev["apply"], sc)
-        self._applied = True
-        return n
-
     def launches_per_step(self) -> int:
         if self._exchange is not None:
             return 1
@@ -598,7 +538,7 @@ class PsStep:
         """A CUDA graph of ``steps`` iterations on self.stream; the gen batch
         reads the iteration from the device counter, which each captured step
         advances (set the first value with :meth:`set_iteration`)."""
-        if self.overlap or self._exchange is not None:
+        if self._exchange is not None:
             raise errors.InvalidConfig("graph capture uses the one-stream phase schedule")
         none = (1 << 64) - 1
         graph = C.c_void_p()
@@ -641,23 +581,12 @@ class PsStep:
         return 0
 
     def fork(self) -> None:
-        """Order the phase streams after work already queued on self.stream."""
-        if self.overlap:
-            _lib.call("srf_event_record_on", self._ev["fork"], self.stream)
-            for st in self._streams:
-                _lib.call("srf_stream_wait_event", st, self._ev["fork"])
+        """(Timing helper; every schedule runs on self.stream.)"""
 
     def join(self) -> None:
-        """Make self.stream wait for every phase stream (end of a timed region)."""
-        if self.overlap:
-            for st, name in zip(self._streams, ("j0", "j1", "j2")):
-                _lib.call("srf_event_record_on", self._ev[name], st)
-                _lib.call("srf_stream_wait_event", self.stream, self._ev[name])
+        """(Timing helper; every schedule runs on self.stream.)"""
 
     def sync(self) -> None:
-        if self.overlap:
-            for st in self._streams:
-                _lib.call("srf_stream_sync", st)
         _lib.call("srf_stream_sync", self.stream)
         for sp in self.spaces.values():
             sp.sync()
@@ -690,9 +619,6 @@ class PsStep:
             if b is not None:
                 _lib.load().srf_batch_destroy(b)
         _lib.call("srf_stream_destroy", self.stream)
-        if self.overlap:
-            for st in self._streams:
-                _lib.call("srf_stream_destroy", st)
 
 
 @dataclass

@@ -1,3 +1,4 @@
+# scratch command file for one gpurun call (rewritten per experiment)
 timeout 900 python -m pytest tests/test_gpu_kernels.py -x -q > gpurun_out/dyn_pytest.log 2>&1; echo rc=$? >> gpurun_out/dyn_pytest.log
 python -c "
 import sys; sys.path.insert(0, '.')

@@ -27,13 +27,10 @@ else:
     L = PsLayout([(int(35.93e6) // 14 // 4,)] * 14, 7, 1, False)
 mode = os.environ.get("PROBE_MODE", "phases")
 if mode != "phases":
-    # whole-step wall time of the eager or overlapped schedule, max over ranks
+    # whole-step wall time of the phase or exchange schedule, max over ranks
     import time
     ps = PsStep(L, rank=rank, world=world, device=local, seed=0, op="sgd", lr=0.01,
-                overlap=(mode == "overlap"),
                 schedule="exchange" if mode == "exchange" else "phases")
-    if os.environ.get("PROBE_CAP"):
-        ps._cap = int(os.environ["PROBE_CAP"])
     for it in range(1, 6):
         ps.step(it)
     ps.sync()
@@ -69,7 +66,7 @@ if mode != "phases":
     bench.barrier_sync()
     dt = bench.dist_max(time.perf_counter() - t0) / R
     if rank == 0:
-        print(json.dumps({"mode": mode, "cfg": cfg, "cap": getattr(ps, "_cap", None),
+        print(json.dumps({"mode": mode, "cfg": cfg,
                           "placement": balanced, "step_us": round(dt * 1e6, 1),
                           "knobs": {k: v for k, v in os.environ.items()
                                     if k.startswith("SRFLOW_")}}), flush=True)

@@ -649,6 +649,133 @@ def dynamic_device_rate(size, device, rounds=None):
             "dynamic_dev_verified": ok}
 
 
+def sweep_nvlink(max_bytes, rank, world, device):
+    """configs[1] over NVLink (N>1): every rank sends to rank+1 at once,
+    1 KiB x 4^k up to max_bytes; static zero-copy (K1 + K2, copy-engine body
+    >= 32 MiB) and dynamic with the receiver on the device (K3 + srf_dyn_recv
+    pulling from the previous rank's pool), graph-replayed rounds, device
+    time, max over ranks."""
+    from paper_1805_08430_b200 import _lib
+    out = []
+    size = 1024
+    while size <= max_bytes:
+        row = {"bytes": size}
+        rounds = 100 if size <= 4 * MIB else 10
+        ring = SendRecvRing(size, rank, world, device)
+        for _ in range(4):
+            ring.put()
+            ring.consume()
+        ring.sync()
+        row["static_us"] = _ring_graph_us(ring.stream, lambda: (ring.put(), ring.consume()),
+                                          rounds, ring.src)
+        row["static_gbps"] = round(size / row["static_us"] / 1e3, 3)
+        row["verified"] = dist_sum(0.0 if ring.verify() else 1.0) == 0.0
+        dyn = DynDeviceRing(size, rank, world, device)
+        for _ in range(4):
+            dyn.step()
+        dyn.sync()
+        row["dynamic_dev_us"] = _ring_graph_us(dyn.stream, dyn.step, rounds, dyn.space)
+        row["dynamic_dev_gbps"] = round(size / row["dynamic_dev_us"] / 1e3, 3)
+        row["dynamic_dev_verified"] = dyn.verify()
+        dyn.close()
+        out.append(row)
+        size *= 4
+    return out
+
+
+def _ring_graph_us(stream, body, rounds, space):
+    from paper_1805_08430_b200 import _lib
+    graph = C.c_void_p()
+    _lib.call("srf_graph_begin", stream)
+    for _ in range(rounds):
+        body()
+    _lib.call("srf_graph_end", stream, C.byref(graph))
+    ev = [C.c_void_p(), C.c_void_p()]
+    for e in ev:
+        _lib.call("srf_timing_event_create", space.handle, C.byref(e))
+    barrier_sync()
+    _lib.call("srf_graph_launch", graph, stream)
+    _lib.call("srf_stream_sync", stream)
+    barrier_sync()
+    _lib.call("srf_event_record_on", ev[0], stream)
+    _lib.call("srf_graph_launch", graph, stream)
+    _lib.call("srf_event_record_on", ev[1], stream)
+    _lib.call("srf_stream_sync", stream)
+    ms = C.c_float()
+    _lib.call("srf_event_elapsed_ms", ev[0], ev[1], C.byref(ms))
+    _lib.call("srf_graph_destroy", graph)
+    return round(dist_max(ms.value * 1e3 / rounds), 3)
+
+
+class DynDeviceRing:
+    """Dynamic-allocation ring for N>1: rank r writes its metadata block into
+    rank r+1's slot (K3), and pulls what rank r-1 announced into its receive
+    block with srf_dyn_recv (decode + validation + peer read on the device)."""
+
+    def __init__(self, size, rank, world, device):
+        from paper_1805_08430_b200 import _lib
+        from paper_1805_08430_b200.distributed import gather_descriptors
+        from paper_1805_08430_b200.memspace import MemorySpace
+        from paper_1805_08430_b200.wire import ElemType, encode_meta, meta_block_size
+        self.lib, self.size = _lib, size
+        self.space = MemorySpace(rank, 2 * size + 8 * MIB, seed=7, device=device)
+        self.reg = self.space.allocate_region(2 * size + 4 * MIB, register=True)
+        base = self.reg.base_addr
+        self.mlen = meta_block_size(1)
+        self.stage, self.slot, self.word = base, base + 256, base + 512
+        self.payload, self.dst = base + MIB, base + MIB + size + 4096
+        view = self.space.view(self.reg, self.payload - base, size)
+        import torch
+        g = torch.Generator(device=f"cuda:{device}")
+        g.manual_seed(99 + rank)
+        view.copy_(torch.randint(0, 256, (size,), dtype=torch.uint8, device=f"cuda:{device}",
+                                 generator=g))
+        torch.cuda.synchronize(device)
+        self.space.write_raw(self.stage, encode_meta((size // 4,), ElemType.F32, self.payload,
+                                                    self.reg.access_token))
+        self.space.write_raw(self.slot + self.mlen - 1, b"\x00")
+        table = gather_descriptors(self.space.export())
+        nxt, prv = (rank + 1) % world, (rank - 1) % world
+        self.next = MemorySpace.import_remote(table[nxt], device)
+        self.prev = MemorySpace.import_remote(table[prv], device)
+        _rid, pbase, plen, _r, ptok = table[prv]["regions"][0]
+        _rid, _nb, _nl, _r, ntok = table[nxt]["regions"][0]
+        self.prev_bounds = (pbase, pbase + plen, ptok)
+        self.next_token = ntok
+        self.rank = rank
+        self.stream = C.c_void_p()
+        _lib.call("srf_stream_create", self.space.handle, C.byref(self.stream))
+        barrier_sync()
+
+    def step(self):
+        lib, u = self.lib, self.lib.u64_array
+        lib.call("srf_put", self.space.handle, u([self.stage]), u([self.mlen]),
+                 u([self.reg.access_token]), 1, self.next.handle, self.slot, self.next_token,
+                 lib.PUT_WAIT_EMPTY, self.stream, None)
+        lo, hi, tok = self.prev_bounds
+        lib.call("srf_dyn_recv", self.space.handle, self.slot, 1, self.prev.handle, lo, hi, tok,
+                 self.dst, self.size, self.word, self.stream)
+
+    def sync(self):
+        self.lib.call("srf_stream_sync", self.stream)
+        self.space.sync()
+
+    def verify(self) -> bool:
+        import hashlib
+        from paper_1805_08430_b200.distributed import all_gather_objects
+        self.sync()
+        mine = hashlib.sha256(self.space.read_raw(self.payload, self.size)).hexdigest()
+        got = hashlib.sha256(self.space.read_raw(self.dst, self.size)).hexdigest()
+        n = int.from_bytes(self.space.read_raw(self.word, 8), "little")
+        sent = all_gather_objects(mine)
+        ok = got == sent[(self.rank - 1) % len(sent)] and n == self.size
+        return dist_sum(0.0 if ok else 1.0) == 0.0
+
+    def close(self):
+        self.sync()
+        self.lib.call("srf_stream_destroy", self.stream)
+
+
 def rpc_device_rate(size, device, reps=None):
     """RPC baseline with every byte on the GPU (RpcDeviceLink / srf_rpc_transfer):
     4 KiB fragments through the 16-slot posted ring, two counted copies."""
@@ -1069,7 +1196,7 @@ def main() -> int:
         roof = {"bound": "nvlink", "achieved": round(ach, 2), "peak": NVLINK_MEASURED_GBS,
                 "unit": "GB/s", "frac": round(ach / NVLINK_MEASURED_GBS, 4),
                 "frac_of_nominal_900": round(ach / NVLINK_NOMINAL_GBS, 4),
-                "kernel": "K1 static_put: copy-engine body (knob 6, cross-device >= 1 MiB) "
+                "kernel": "K1 static_put: copy-engine body (knob 6, cross-device >= 32 MiB) "
                           "+ k_put tail release", "bytes_per_launch": alg,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction "
                                "(nominal 900)"}
@@ -1105,6 +1232,8 @@ def main() -> int:
             "sample": f"{n} steps x {S} B static Send/Recv (oracle/port.py MicrobenchRig: "
                       f"ascending 1-4096 B chunk delivery + flag poll + max), {dt:.1f} s, "
                       f"host cpu_count={os.cpu_count()}"}
+    if world > 1 and not args.no_sweep:
+        line["sweep_nvlink"] = sweep_nvlink(S, rank, world, local)
     if world == 1 and not args.no_sweep:
         line["sweep"] = sweep(S, local)
         if not args.no_cpu:

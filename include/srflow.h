@@ -61,7 +61,7 @@ uint64_t srf_launch_count(void);
  * 1 TMA bulk), 3 = pool allocator (0 cudaMalloc + CUDA IPC, 1 VMM + fd),
  * 4 = 16-B vectors in flight per thread (4 or 8), 5 = 32-B vectors (0/1),
  * 6 = cross-device bodies >= value KiB move on the copy engine, the tail
- *     flag still released by an SM store after them (0 = never; default 1024) */
+ *     flag still released by an SM store after them (0 = never; default 32768) */
 int srf_tune(int knob, int value);
 
 /* ---- memory spaces (memspace.py) ----------------------------------------- */

@@ -189,7 +189,7 @@ def peer_engine(request):
     the flag released by an SM store after them."""
     _lib.tune("peer_ce_kib", 0 if request.param == "sm" else 1)
     yield request.param
-    _lib.tune("peer_ce_kib", 1024)
+    _lib.tune("peer_ce_kib", 32768)
 
 
 @pytest.mark.parametrize("size", [1025, 4097, (1 << 20) + 3, (8 << 20) + 8])

@@ -280,6 +280,15 @@ int srf_ps_persistent(srf_batch_t push, srf_batch_t gen, srf_batch_t meta,
  * producer, runtime/protocol.py:163-201). */
 typedef struct srf_exchange *srf_exchange_t;
 int srf_batch_gen_set_meta(srf_batch_t gen, int n, const int *gen_index, srf_batch_t meta);
+/* co-located worker/shard (the apply reads the gradient in place): gen edge i
+ * releases the byte at ready_addr[i] of space[i] to 1 when its gradient is
+ * complete and waits for 0 before overwriting it; the apply waits for 1 and
+ * clears it (srf_batch_apply_set_ready, one entry per (variable, worker) edge
+ * in creation order, UINT64_MAX = none).  Needed by the exchange schedule,
+ * where an apply unit may be claimed while the gradient is still produced. */
+int srf_batch_gen_set_ready(srf_batch_t gen, srf_space_t const *space,
+                            const uint64_t *ready_addr);
+int srf_batch_apply_set_ready(srf_batch_t apply, srf_space_t space, const uint64_t *ready_addr);
 /* partitioned variables (extension): gen edge i produces elements
  * elem_offset[i] ... of its model variable's gradient stream */
 int srf_batch_gen_set_offsets(srf_batch_t gen, const uint64_t *elem_offset);

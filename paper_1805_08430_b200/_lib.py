@@ -118,6 +118,8 @@ SIGNATURES = {
     "srf_torch_malloc": (vp, [C.c_ssize_t, C.c_int, vp]),
     "srf_torch_free": (None, [vp, C.c_ssize_t, C.c_int, vp]),
     "srf_batch_gen_set_offsets": (C.c_int, [vp, P(u64)]),
+    "srf_batch_gen_set_ready": (C.c_int, [vp, P(vp), P(u64)]),
+    "srf_batch_apply_set_ready": (C.c_int, [vp, vp, P(u64)]),
     "srf_ps_exchange_create": (C.c_int, [vp, P(u64), vp, P(u64), P(vp), C.c_int, P(u64),
                                          P(vp)]),
     "srf_ps_exchange_launch": (C.c_int, [vp, vp, u64, C.c_int]),

@@ -1060,6 +1060,10 @@ struct BatchGen {        // worker: consume weight, (re)produce gradient
   const uint8_t *meta_tail;
   uint64_t meta_body;
   uint64_t elem_offset;  // first element's index in its model variable (slices)
+  // gradient read in place by a shard on this server (co-located worker):
+  // released to 1 when the gradient is complete, cleared by that apply; the
+  // gen waits for 0 (credit) before overwriting it.  nullptr: none.
+  uint8_t *ready;
 };
 
 struct BatchApply {      // shard: fused dynamic receive (meta decode + peer
@@ -1072,6 +1076,7 @@ struct BatchApply {      // shard: fused dynamic receive (meta decode + peer
   uint32_t is_meta;      // bit w: src[w] is a meta block
   int nw, rank;
   uint32_t cta_begin, cta_count;
+  const uint8_t *ready[SRF_MAX_WORKERS];  // in-place gradient w complete (nullptr: none)
 };
 
 template <typename D>
@@ -1197,6 +1202,8 @@ __device__ __forceinline__ void gen_unit(const BatchGen *descs, int n, uint32_t 
     if (s_last && threadIdx.x == 0) {
       // the weight was consumed: clear its flag (StaticReceiver.poll semantics)
       if (d.weight_flag) release_tail(d.weight_flag, 0, sys);
+      // the in-place gradient is complete (read directly by the co-located apply)
+      if (d.ready) release_tail(d.ready, 1, sys);
       if (fuse_meta && d.meta_dst) {
         // K3: the gradient's metadata block, flag last; the acq_rel arrival
         // above made every CTA's gradient stores visible before this release
@@ -1242,6 +1249,10 @@ __device__ __forceinline__ void apply_unit(const BatchApply *descs, int n, uint3
       const uint8_t *m = d.src[w];
       if (!((d.is_meta >> w) & 1)) {
         s_g[w] = m;  // co-located worker: its gradient block directly
+        if (d.ready[w] && !spin_until(d.ready[w], 1, timeout_ns, sys)) {
+          atomicExch(err, 5);
+          s_bad = 1;
+        }
       } else if (!spin_until(m + 8 * r + 32, 1, timeout_ns, sys)) {
         atomicExch(err, 5);
         s_bad = 1;
@@ -1279,6 +1290,8 @@ __device__ __forceinline__ void apply_unit(const BatchApply *descs, int n, uint3
     // next send; DynReceiver.poll's clear)
     if (s_last && threadIdx.x < (unsigned)d.nw && ((d.is_meta >> threadIdx.x) & 1))
       release_tail((uint8_t *)d.src[threadIdx.x] + 8 * r + 32, 0, sys);
+    if (s_last && threadIdx.x < (unsigned)d.nw && d.ready[threadIdx.x])
+      release_tail((uint8_t *)d.ready[threadIdx.x], 0, sys);
     if (s_last && threadIdx.x == 0) atomicExch(&counters[s_desc], 0u);
     __syncthreads();  // shared state is reused by the next unit
   }
@@ -2991,6 +3004,49 @@ int srf_ps_persistent(srf_batch_t push, srf_batch_t gen, srf_batch_t meta,
   return launch_check("k_ps_persistent");
 }
 
+int srf_batch_gen_set_ready(srf_batch_t gen, srf_space_t const *space,
+                            const uint64_t *ready_addr) {
+  if (!gen || gen->kind != 1) return fail(SRF_E_INVALID_CONFIG, "not a gen batch");
+  BatchGen *g = (BatchGen *)gen->host.data();
+  for (int i = 0; i < gen->n; ++i) {
+    if (ready_addr[i] == UINT64_MAX) {
+      g[i].ready = nullptr;
+      continue;
+    }
+    int rc = check_raw(space[i], ready_addr[i], 1, "ready flag");
+    if (rc) return rc;
+    if (g[i].credit) return fail(SRF_E_INVALID_CONFIG, "gen edge %d already has a credit", i);
+    g[i].ready = space[i]->base + ready_addr[i];
+    g[i].credit = g[i].ready;  // overwrite only after the apply consumed it
+  }
+  CUDA_TRY(cudaSetDevice(gen->device));
+  CUDA_TRY(cudaMemcpy(gen->descs, gen->host.data(), gen->host.size(), cudaMemcpyHostToDevice));
+  return SRF_OK;
+}
+
+int srf_batch_apply_set_ready(srf_batch_t apply, srf_space_t space, const uint64_t *ready_addr) {
+  if (!apply || apply->kind != 2) return fail(SRF_E_INVALID_CONFIG, "not an apply batch");
+  BatchApply *d = (BatchApply *)apply->host.data();
+  int k = 0;
+  for (int v = 0; v < apply->n; ++v) {
+    for (int w = 0; w < d[v].nw; ++w, ++k) {
+      if (ready_addr[k] == UINT64_MAX) {
+        d[v].ready[w] = nullptr;
+        continue;
+      }
+      if ((d[v].is_meta >> w) & 1)
+        return fail(SRF_E_INVALID_CONFIG, "ready flag on a metadata edge (%d)", k);
+      int rc = check_raw(space, ready_addr[k], 1, "ready flag");
+      if (rc) return rc;
+      d[v].ready[w] = space->base + ready_addr[k];
+    }
+  }
+  CUDA_TRY(cudaSetDevice(apply->device));
+  CUDA_TRY(cudaMemcpy(apply->descs, apply->host.data(), apply->host.size(),
+                      cudaMemcpyHostToDevice));
+  return SRF_OK;
+}
+
 int srf_batch_gen_set_offsets(srf_batch_t gen, const uint64_t *elem_offset) {
   DeviceGuard device_guard;
   if (!gen || gen->kind != 1) return fail(SRF_E_INVALID_CONFIG, "not a gen batch");
@@ -3070,7 +3126,7 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
       } else if (kind == 1) {
         const BatchGen &d = ((const BatchGen *)b->host.data())[i];
         begin = d.cta_begin; count = d.cta_count;
-        if (d.credit && !d.meta_dst)
+        if (d.credit && d.credit != d.ready && !d.meta_dst)
           return fail(SRF_E_INVALID_CONFIG, "exchange: gen edge %d has no fused meta", i);
       } else {
         const BatchApply &d = ((const BatchApply *)b->host.data())[i];

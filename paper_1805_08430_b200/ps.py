@@ -159,6 +159,8 @@ class PsLayout:
         for v in range(len(self.shapes)):
             if self.shard_of(v) == s:
                 take(("var", v), self.nbytes(v))
+                if self.is_worker(s):  # co-located: the in-place gradient's ready byte
+                    take(("ready", v), 1)
         if self.is_worker(s):
             for v in range(len(self.shapes)):
                 take(("grad", v), self.nbytes(v))
@@ -292,7 +294,7 @@ class PsStep:
 
     def _block_len(self, s: int, key) -> int:
         kind = key if isinstance(key, str) else key[0]
-        if kind == "flag":
+        if kind in ("flag", "ready"):
             return 1
         v = key[1]
         if kind in ("var", "grad"):
@@ -388,6 +390,12 @@ class PsStep:
                       u64(r[2] for r in g_rows), (P * n)(*[r[3] for r in g_rows]),
                       u64(r[4] for r in g_rows), u64(r[5] for r in g_rows), self.seed,
                       C.byref(b))
+            ready = [self.addr(w, ("ready", v)) if L.shard_of(v) == w else _NONE
+                     for w, v in self._rows["gen"]]
+            if any(r != _NONE for r in ready):
+                _lib.call("srf_batch_gen_set_ready", b,
+                          (P * n)(*[self.spaces[w].handle.value for w, _v in self._rows["gen"]]),
+                          u64(ready))
             offs = [L.parent(v)[1] for _w, v in self._rows["gen"]]
             if any(offs):  # partitioned variables: slices keep global element indices
                 _lib.call("srf_batch_gen_set_offsets", b, u64(offs))
@@ -440,6 +448,10 @@ class PsStep:
                       (P * len(srcsp))(*srcsp), u64(srcad), (C.c_int * len(ismeta))(*ismeta),
                       (P * len(peersp))(*peersp), u64(lo), u64(hi), u64(tok), self.op,
                       self.lr, C.byref(b))
+            if L.is_worker(s):
+                _lib.call("srf_batch_apply_set_ready", b, self.spaces[s].handle,
+                          u64(self.addr(s, ("ready", v)) if w == s else _NONE
+                              for v in vs for w in range(L.workers)))
             out["apply"][s] = b
         return out
 

@@ -225,3 +225,20 @@ def test_partitioned_variables_equal_the_model(placement):
         for v in range(len(shapes)):
             assert got[v].tobytes() == want[v].reshape(-1).tobytes(), (op, v)
         ps.close()
+
+
+def test_exchange_waits_for_in_place_gradients():
+    """Co-located worker/shard: the apply reads the worker's gradient in place,
+    so in the single-launch exchange it must wait for the gradient's ready
+    byte (an apply unit can be claimed while that gradient is still being
+    produced).  Large gradients, lag 0: the window is wide."""
+    shapes, W, P = [(1 << 22,), (1 << 21,), (3,)], 2, 2
+    L = PsLayout(shapes, W, P, True)
+    ps = PsStep(L, seed=17, op="sgd", lr=0.01, schedule="exchange", exchange_lag=0)
+    for it in range(1, 6):
+        ps.step(it)
+    ps.sync()
+    want = port.ps_expected_device(shapes, W, 17, range(1, 6), op="sgd", lr=0.01)
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes(), v
+    ps.close()

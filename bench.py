@@ -959,17 +959,26 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         ps.run_persistent(it + 1, n)
         it += n
 
+    def multi(n):
+        nonlocal it
+        ps.run_exchange(it + 1, n)
+        it += n
+
     times = {}
     for name in ("phases", "exchange"):
         ps.use_schedule(name)
         eager(2)
         times[name] = sample(eager)
+    times["exchange_multi"] = sample(multi)
     if world == 1:
         ps.use_schedule("phases")
         times["persistent"] = sample(pers)
     best = min(times, key=times.get)
     persistent = best == "persistent"
-    ps.use_schedule("phases" if best == "persistent" else best)
+    multi_launch = best == "exchange_multi"
+    ps.use_schedule("phases" if best in ("persistent", "exchange_multi") else best)
+    if multi_launch:
+        ps.use_schedule("exchange")
     # latency-bound configs: enough iterations for a timed region of ~0.3 s
     per_iter_s = times[best] / 5 / 1e3
     steps = int(max(steps, min(20000, 0.3 / max(per_iter_s, 1e-7))))
@@ -993,6 +1002,10 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         launched = steps * (ps.launches_per_step() + 1)
     elif persistent:
         ps.run_persistent(it + 1, steps)
+        it += steps
+        launched = 0
+    elif multi_launch:
+        ps.run_exchange(it + 1, steps)
         it += steps
         launched = 0
     else:
@@ -1100,6 +1113,9 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
            "schedule": ("one stream, CUDA graph" if graph is not None else
                         "one persistent cooperative launch (grid barriers between phases)"
                         if persistent else
+                        "exchange x64: one k_ps_exchange launch per 64 steps (the unit "
+                        "queue repeats; a push waits for its variable's previous apply)"
+                        if multi_launch else
                         "exchange: one k_ps_exchange launch per step (dependency-ordered "
                         "unit queue, meta fused into GenGrad)" if ps.schedule == "exchange"
                         else "one stream, one launch per phase"),

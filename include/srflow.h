@@ -297,6 +297,14 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
                            const uint64_t *apply_key, srf_exchange_t *out);
 int srf_ps_exchange_launch(srf_exchange_t exchange, srf_stream_t stream, uint64_t iteration,
                            int regen);
+/* iterations iteration, iteration+1, ... in ONE launch: the queue repeats,
+ * and push edge i of a later iteration first waits until its variable's
+ * apply (global apply descriptor push_apply_index[i] across the apply
+ * batches in creation order, -1: none) completed for the previous one
+ * (srf_ps_exchange_link must have been called). */
+int srf_ps_exchange_link(srf_exchange_t exchange, const int *push_apply_index);
+int srf_ps_exchange_launch_n(srf_exchange_t exchange, srf_stream_t stream, uint64_t iteration,
+                             uint32_t iterations, int regen);
 int srf_ps_exchange_destroy(srf_exchange_t exchange);
 
 /* Device-side DynReceiver.poll + fetch (runtime/protocol.py:224-254): acquire

@@ -124,6 +124,8 @@ SIGNATURES = {
                                          P(vp)]),
     "srf_ps_exchange_launch": (C.c_int, [vp, vp, u64, C.c_int]),
     "srf_ps_exchange_destroy": (C.c_int, [vp]),
+    "srf_ps_exchange_link": (C.c_int, [vp, P(C.c_int)]),
+    "srf_ps_exchange_launch_n": (C.c_int, [vp, vp, u64, C.c_uint32, C.c_int]),
     "srf_doorbell_bind": (C.c_int, [vp, u64, u64, C.c_int]),
     "srf_flag_read": (C.c_int, [vp, u64, u64, vp]),
     "srf_flag_clear": (C.c_int, [vp, u64]),

@@ -1108,12 +1108,49 @@ __device__ __forceinline__ bool spin_until(const uint8_t *p, uint32_t want,
 
 // One work unit (a CTA-sized slice of one descriptor) of each batch kind; the
 // batch kernels loop over units, the exchange kernel claims them from a queue.
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const unsigned int *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Several iterations per exchange launch: a descriptor's units of iteration
+// k start only after its iteration k-1 completed (its per-launch completion
+// count reached k) - flags alone do not tell iterations apart, and the
+// arrival counter must not mix them.
+__device__ __forceinline__ void wait_count(const unsigned int *p, uint32_t want,
+                                           uint64_t timeout_ns, int *err) {
+  if (!p || want == 0) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_gpu_u32(p) < want) {
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      atomicExch(err, 7);
+      return;
+    }
+    __nanosleep(20);
+  }
+}
+
+__device__ __forceinline__ void count_done(unsigned int *p) {
+  if (p) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+
+// seq: per-descriptor completion counts of this launch (nullptr: one
+// iteration per launch); k: iteration index in the launch; wait_done /
+// wait_index: the pushed variable must have been updated k times before its
+// weights are read again
 __device__ __forceinline__ void put_unit(const BatchPut *descs, int n, uint32_t u,
                                          unsigned int *counters, uint64_t timeout_ns, int *err,
-                                         int sys) {
+                                         int sys, const unsigned int *wait_done = nullptr,
+                                         const int *wait_index = nullptr, uint32_t k = 0,
+                                         unsigned int *seq = nullptr) {
   __shared__ int s_desc, s_last;
   {
-    if (threadIdx.x == 0) s_desc = find_desc(descs, n, u);
+    if (threadIdx.x == 0) {
+      s_desc = find_desc(descs, n, u);
+      if (seq) wait_count(seq + s_desc, k, timeout_ns, err);
+      if (k && wait_index[s_desc] >= 0) wait_count(wait_done + wait_index[s_desc], k, timeout_ns, err);
+    }
     __syncthreads();
     const BatchPut d = descs[s_desc];
     const uint32_t lb = u - d.cta_begin;
@@ -1127,8 +1164,11 @@ __device__ __forceinline__ void put_unit(const BatchPut *descs, int n, uint32_t 
     if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, sys);
     __syncthreads();
     if (s_last && threadIdx.x == 0) {
-      release_tail(d.dst + d.body, *d.tail, sys);
+      // re-arm the arrival counter BEFORE publishing: whoever acquires the
+      // flag (and, downstream, the next use of this edge) sees it at zero
       atomicExch(&counters[s_desc], 0u);
+      release_tail(d.dst + d.body, *d.tail, sys);
+      if (seq) count_done(seq + s_desc);
     }
     __syncthreads();  // shared state is reused by the next unit
   }
@@ -1167,10 +1207,14 @@ __device__ __forceinline__ float unit_f32(uint32_t k0, uint32_t k1, uint32_t i) 
 __device__ __forceinline__ void gen_unit(const BatchGen *descs, int n, uint32_t u,
                                          unsigned int *counters, uint64_t seed,
                                          uint64_t iteration, int regen, int fuse_meta,
-                                         uint64_t timeout_ns, int *err, int sys) {
+                                         uint64_t timeout_ns, int *err, int sys,
+                                         uint32_t k = 0, unsigned int *seq = nullptr) {
   __shared__ int s_desc, s_last;
   {
-    if (threadIdx.x == 0) s_desc = find_desc(descs, n, u);
+    if (threadIdx.x == 0) {
+      s_desc = find_desc(descs, n, u);
+      if (seq) wait_count(seq + s_desc, k, timeout_ns, err);
+    }
     __syncthreads();
     const BatchGen d = descs[s_desc];
     const uint32_t lb = u - d.cta_begin;
@@ -1200,6 +1244,7 @@ __device__ __forceinline__ void gen_unit(const BatchGen *descs, int n, uint32_t 
     if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, sys);
     __syncthreads();
     if (s_last && threadIdx.x == 0) {
+      atomicExch(&counters[s_desc], 0u);  // re-armed before anything is published
       // the weight was consumed: clear its flag (StaticReceiver.poll semantics)
       if (d.weight_flag) release_tail(d.weight_flag, 0, sys);
       // the in-place gradient is complete (read directly by the co-located apply)
@@ -1207,10 +1252,10 @@ __device__ __forceinline__ void gen_unit(const BatchGen *descs, int n, uint32_t 
       if (fuse_meta && d.meta_dst) {
         // K3: the gradient's metadata block, flag last; the acq_rel arrival
         // above made every CTA's gradient stores visible before this release
-        for (uint64_t k = 0; k < d.meta_body; ++k) d.meta_dst[k] = d.meta_src[k];
+        for (uint64_t b = 0; b < d.meta_body; ++b) d.meta_dst[b] = d.meta_src[b];
         release_tail(d.meta_dst + d.meta_body, *d.meta_tail, sys);
       }
-      atomicExch(&counters[s_desc], 0u);
+      if (seq) count_done(seq + s_desc);
     }
     __syncthreads();  // shared state is reused by the next unit
   }
@@ -1230,13 +1275,15 @@ __device__ __forceinline__ void gen_batch_units(const BatchGen *descs, int n,
 
 __device__ __forceinline__ void apply_unit(const BatchApply *descs, int n, uint32_t u,
                                            unsigned int *counters, int op, float lr,
-                                           uint64_t timeout_ns, int *err, int sys) {
+                                           uint64_t timeout_ns, int *err, int sys,
+                                           unsigned int *done = nullptr, uint32_t k = 0) {
   __shared__ int s_desc, s_last, s_bad;
   __shared__ const uint8_t *s_g[SRF_MAX_WORKERS];
   {
     if (threadIdx.x == 0) {
       s_desc = find_desc(descs, n, u);
       s_bad = 0;
+      if (done) wait_count(done + s_desc, k, timeout_ns, err);
     }
     __syncthreads();
     const BatchApply &d = descs[s_desc];
@@ -1286,13 +1333,20 @@ __device__ __forceinline__ void apply_unit(const BatchApply *descs, int n, uint3
     __syncthreads();
     if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, sys);
     __syncthreads();
+    // re-arm the arrival counter before any credit is published (thread 0,
+    // ordered before the lanes' releases by the barrier)
+    if (s_last && threadIdx.x == 0) atomicExch(&counters[s_desc], 0u);
+    __syncthreads();
     // gradients consumed: the last CTA clears the meta flags (credit for the
     // next send; DynReceiver.poll's clear)
     if (s_last && threadIdx.x < (unsigned)d.nw && ((d.is_meta >> threadIdx.x) & 1))
       release_tail((uint8_t *)d.src[threadIdx.x] + 8 * r + 32, 0, sys);
     if (s_last && threadIdx.x < (unsigned)d.nw && d.ready[threadIdx.x])
       release_tail((uint8_t *)d.ready[threadIdx.x], 0, sys);
-    if (s_last && threadIdx.x == 0) atomicExch(&counters[s_desc], 0u);
+    if (s_last && threadIdx.x == 0) {
+      // one more update of this variable completed (multi-iteration exchange)
+      if (done) count_done(done + s_desc);
+    }
     __syncthreads();  // shared state is reused by the next unit
   }
 }
@@ -1449,6 +1503,13 @@ struct ExArgs {
   int op; float lr;
   const ExItem *items; uint32_t nitems; unsigned int *claim; unsigned int *exit_count;
   uint64_t iteration; int regen; uint64_t timeout_ns; int *err;
+  // several iterations per launch: the queue repeats `iters` times (iteration
+  // k's units after iteration k-1's); done[] counts completed applies per
+  // apply descriptor in this launch, push_done[i] maps push edge i to its
+  // variable's counter (-1: none)
+  uint32_t iters;
+  unsigned int *done; int apply_base[kMaxApply]; const int *push_done;
+  unsigned int *seq_push, *seq_gen;  // per-descriptor completion counts (this launch)
 };
 
 __global__ void __launch_bounds__(512) k_ps_exchange(const __grid_constant__ ExArgs a) {
@@ -1458,16 +1519,18 @@ __global__ void __launch_bounds__(512) k_ps_exchange(const __grid_constant__ ExA
     __syncthreads();
     const uint32_t i = s_i;
     __syncthreads();
-    if (i >= a.nitems) break;
-    const ExItem x = a.items[i];
+    if (i >= a.nitems * a.iters) break;
+    const uint32_t k = i / a.nitems;
+    const ExItem x = a.items[i - k * a.nitems];
     if (x.kind == 0)
-      put_unit(a.push, a.npush, x.unit, a.cpush, a.timeout_ns, a.err, a.push_sys);
+      put_unit(a.push, a.npush, x.unit, a.cpush, a.timeout_ns, a.err, a.push_sys, a.done,
+               a.push_done, k, a.seq_push);
     else if (x.kind == 1)
-      gen_unit(a.gen, a.ngen, x.unit, a.cgen, a.seed, a.iteration, a.regen, 1, a.timeout_ns,
-               a.err, a.gen_sys);
+      gen_unit(a.gen, a.ngen, x.unit, a.cgen, a.seed, a.iteration + k, a.regen, 1,
+               a.timeout_ns, a.err, a.gen_sys, k, a.seq_gen);
     else
       apply_unit(a.apply[x.batch], a.napply[x.batch], x.unit, a.capply[x.batch], a.op, a.lr,
-                 a.timeout_ns, a.err, a.apply_sys[x.batch]);
+                 a.timeout_ns, a.err, a.apply_sys[x.batch], a.done + a.apply_base[x.batch], k);
   }
   // the last CTA out re-arms the queue for the next launch
   if (threadIdx.x == 0 && atomicAdd(a.exit_count, 1u) == gridDim.x - 1) {
@@ -3100,6 +3163,9 @@ struct srf_exchange {
   ExArgs args;
   ExItem *items = nullptr;
   unsigned int *ctr = nullptr;  // [claim, exit_count]
+  unsigned int *done = nullptr; // completions per descriptor this launch: [apply|push|gen]
+  int ndone = 0, napply_descs = 0;
+  int *push_done = nullptr;
   int grid = 0;
 };
 
@@ -3160,7 +3226,10 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
   ExArgs &a = x->args;
   if (push) { a.push = (const BatchPut *)push->descs; a.npush = push->n; a.cpush = push->counters; a.push_sys = push->sys; }
   if (gen) { a.gen = (const BatchGen *)gen->descs; a.ngen = gen->n; a.cgen = gen->counters; a.seed = gen->seed; a.gen_sys = gen->sys; }
+  int nd = 0;
   for (int b = 0; b < napply; ++b) {
+    a.apply_base[b] = nd;
+    nd += apply[b]->n;
     a.apply[b] = (const BatchApply *)apply[b]->descs;
     a.napply[b] = apply[b]->n;
     a.capply[b] = apply[b]->counters;
@@ -3177,6 +3246,12 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
     e = cudaMemcpy(x->items, items.data(), sizeof(ExItem) * items.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&x->ctr, 2 * sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(x->ctr, 0, 2 * sizeof(unsigned int));
+  const int np = a.npush, ng = a.ngen;
+  x->ndone = std::max(nd + np + ng, 1);
+  if (e == cudaSuccess) e = cudaMalloc(&x->done, sizeof(unsigned int) * x->ndone);
+  if (e == cudaSuccess) e = cudaMemset(x->done, 0, sizeof(unsigned int) * x->ndone);
+  if (e == cudaSuccess) e = cudaMalloc(&x->push_done, sizeof(int) * std::max(1, a.npush));
+  if (e == cudaSuccess) e = cudaMemset(x->push_done, 0xff, sizeof(int) * std::max(1, a.npush));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   int per_sm = 0;
   if (e == cudaSuccess)
@@ -3184,25 +3259,57 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
   if (e != cudaSuccess) {
     cudaFree(x->items);
     cudaFree(x->ctr);
+    cudaFree(x->done);
+    cudaFree(x->push_done);
     delete x;
     return fail(SRF_E_DEVICE, "exchange: %s", cudaGetErrorString(e));
   }
   a.items = x->items;
   a.claim = x->ctr;
   a.exit_count = x->ctr + 1;
+  a.done = x->done;
+  a.push_done = x->push_done;
+  a.seq_push = np ? x->done + nd : nullptr;
+  a.seq_gen = ng ? x->done + nd + np : nullptr;
+  x->napply_descs = nd;
+  a.iters = 1;
   x->grid = sm_count_of(device) * std::max(1, per_sm);
   *out = x;
   return SRF_OK;
 }
 
-int srf_ps_exchange_launch(srf_exchange_t x, srf_stream_t st, uint64_t iteration, int regen) {
+int srf_ps_exchange_link(srf_exchange_t x, const int *push_apply_index) {
+  DeviceGuard device_guard;
+  std::vector<int> m(std::max(1, x->args.npush));
+  for (int i = 0; i < x->args.npush; ++i) {
+    if (push_apply_index[i] < -1 || push_apply_index[i] >= x->napply_descs)
+      return fail(SRF_E_INVALID_CONFIG, "exchange_link: index %d", push_apply_index[i]);
+    m[i] = push_apply_index[i];
+  }
+  CUDA_TRY(cudaSetDevice(x->device));
+  CUDA_TRY(cudaMemcpy(x->push_done, m.data(), sizeof(int) * m.size(), cudaMemcpyHostToDevice));
+  return SRF_OK;
+}
+
+int srf_ps_exchange_launch_n(srf_exchange_t x, srf_stream_t st, uint64_t iteration,
+                             uint32_t iterations, int regen) {
   DeviceGuard device_guard;
   if (st->device != x->device) return fail(SRF_E_INVALID_CONFIG, "exchange: stream GPU");
+  if (iterations < 1) return fail(SRF_E_INVALID_CONFIG, "exchange: iterations >= 1");
+  if ((uint64_t)x->args.nitems * iterations > 0xFFFFFFFFull)
+    return fail(SRF_E_INVALID_CONFIG, "exchange: too many units for one launch");
   x->args.iteration = iteration;
   x->args.regen = regen;
+  x->args.iters = iterations;
   CUDA_TRY(cudaSetDevice(x->device));
+  if (iterations > 1)
+    CUDA_TRY(cudaMemsetAsync(x->done, 0, sizeof(unsigned int) * x->ndone, st->s));
   k_ps_exchange<<<x->grid, 512, 0, st->s>>>(x->args);
   return launch_check("k_ps_exchange");
+}
+
+int srf_ps_exchange_launch(srf_exchange_t x, srf_stream_t st, uint64_t iteration, int regen) {
+  return srf_ps_exchange_launch_n(x, st, iteration, 1, regen);
 }
 
 int srf_ps_exchange_destroy(srf_exchange_t x) {
@@ -3211,6 +3318,8 @@ int srf_ps_exchange_destroy(srf_exchange_t x) {
   cudaSetDevice(x->device);
   cudaFree(x->items);
   cudaFree(x->ctr);
+  cudaFree(x->done);
+  cudaFree(x->push_done);
   delete x;
   return SRF_OK;
 }

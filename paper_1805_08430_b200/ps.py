@@ -514,6 +514,16 @@ class PsStep:
                   u64(4 * (pos[v] + lag) + 2 for s, _a in applies for v in rows["apply"][s])
                   if applies else None,
                   C.byref(x))
+        if rows["push"]:
+            # push edge -> its variable's apply descriptor (global order over the
+            # apply batches), for launches of several iterations
+            index, base = {}, 0
+            for s_, _a in applies:
+                for i, v in enumerate(rows["apply"][s_]):
+                    index[v] = base + i
+                base += len(rows["apply"][s_])
+            link = (C.c_int * len(rows["push"]))(*[index.get(v, -1) for v in rows["push"]])
+            _lib.call("srf_ps_exchange_link", x, link)
         return x
 
     # -- running --------------------------------------------------------------------------
@@ -569,6 +579,24 @@ class PsStep:
                       self.stream)
         _lib.call("srf_graph_end", self.stream, C.byref(graph))
         return graph
+
+    def run_exchange(self, first_iteration: int, iterations: int, regen: bool = True,
+                     per_launch: int = 64) -> int:
+        """``iterations`` PS iterations as exchange launches of up to
+        ``per_launch`` iterations each (the unit queue repeats inside one
+        launch; a push of iteration k waits for its variable's apply of
+        iteration k-1).  Returns the number of launches."""
+        self.use_schedule("exchange")
+        n, it = 0, first_iteration
+        while iterations > 0:
+            k = min(per_launch, iterations)
+            if self._exchange is not None:
+                _lib.call("srf_ps_exchange_launch_n", self._exchange, self.stream, it, k,
+                          1 if regen else 0)
+                n += 1
+            it += k
+            iterations -= k
+        return n
 
     def run_persistent(self, first_iteration: int, iterations: int, regen: bool = True) -> None:
         """``iterations`` PS iterations in one cooperative launch (every server

@@ -242,3 +242,21 @@ def test_exchange_waits_for_in_place_gradients():
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes(), v
     ps.close()
+
+
+@pytest.mark.parametrize("shapes,W,P,coloc", CASES + [([(1 << 20,), (7,)], 2, 2, True)])
+@pytest.mark.parametrize("per_launch", [3, 64])
+def test_multi_iteration_exchange_matches_oracle(shapes, W, P, coloc, per_launch):
+    """Several iterations per k_ps_exchange launch: a push of iteration k waits
+    for its variable's apply of iteration k-1 inside the launch."""
+    L = PsLayout(shapes, W, P, coloc)
+    ps = PsStep(L, seed=31, op="sgd", lr=0.02)
+    ps.step(1)
+    assert ps.run_exchange(2, 10, per_launch=per_launch) == -(-10 // per_launch)
+    ps.use_schedule("phases")
+    ps.step(12)
+    ps.sync()
+    want = port.ps_expected_device(shapes, W, 31, range(1, 13), op="sgd", lr=0.02)
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes(), v
+    ps.close()

@@ -1,6 +1,3 @@
 # scratch command file for one gpurun call (rewritten per experiment)
-s=$(date +%s); timeout 1200 python bench.py > gpurun_out/r1i_bench_n1.json 2> gpurun_out/r1i_bench_n1.err; echo "n1 $(( $(date +%s) - s )) s" > gpurun_out/r1i_times.txt
-for n in 2 4; do
-s=$(date +%s); timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $n > gpurun_out/r1i_bench_n$n.json 2> gpurun_out/r1i_bench_n$n.err; echo "n$n $(( $(date +%s) - s )) s" >> gpurun_out/r1i_times.txt
-done
-s=$(date +%s); timeout 600 python bench.py --impl reference > gpurun_out/r1i_ref_n1.json 2> gpurun_out/r1i_ref_n1.err; echo "ref $(( $(date +%s) - s )) s" >> gpurun_out/r1i_times.txt
+timeout 900 python -m pytest tests/test_gpu_ps.py -x -q > gpurun_out/r1j_pytest.log 2>&1; echo rc=$? >> gpurun_out/r1j_pytest.log
+timeout 900 python bench.py --no-cpu --no-sweep > gpurun_out/r1j_bench_n1.json 2> gpurun_out/r1j_bench_n1.err

@@ -59,6 +59,20 @@ def _worker(rank: int, world: int, port: int, errq):
         # 3. traffic symmetry: what one rank sends the other receives
         t = [L.traffic(s) for s in range(world)]
         assert t[0]["link_out"] == t[1]["link_in"] and t[1]["link_out"] == t[0]["link_in"]
+        # 4. every rank derives the same layouts - peers' block coordinates are
+        # computed, not exchanged - including the labelled extensions
+        import hashlib
+        import json
+        digests = []
+        for kw in ({}, {"placement": "bytes"},
+                   {"placement": "bytes", "partition_bytes": 16 << 20}):
+            Lx = PsLayout(vgg16_shapes(), world, world, colocate=True, **kw)
+            blob = json.dumps([[sorted((str(k), o) for k, o in Lx.blocks[s].items())
+                                for s in range(Lx.nservers)], Lx.units, Lx.sizes],
+                              sort_keys=True).encode()
+            digests.append(hashlib.sha256(blob).hexdigest())
+        got = D.all_gather_objects(digests)
+        assert all(g == got[0] for g in got)
         dist.barrier()
         dist.destroy_process_group()
     except BaseException as exc:  # report to the parent

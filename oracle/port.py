@@ -489,7 +489,7 @@ class PsRig:
 
 # -- device-side GenGrad stand-in (not a reference function) -----------------------------
 # The timed PS step regenerates synthetic gradients on the GPU with a
-# counter-based hash (k_gen_batch in paper_1805_08430_b200/csrc/srflow.cu)
+# counter-based hash (k_gen_batch, paper_1805_08430_b200/csrc/device_ps.cuh)
 # instead of the reference's host PCG64 stream.  This restatement lets the
 # tests check those device gradients and the variables they produce.
 

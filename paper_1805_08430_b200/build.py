@@ -36,7 +36,9 @@ def needs_build() -> bool:
     if not os.path.exists(OUT):
         return True
     out_m = os.path.getmtime(OUT)
-    deps = [SRC, os.path.join(ROOT, "include", "srflow.h")]
+    csrc = os.path.dirname(SRC)
+    deps = [os.path.join(csrc, f) for f in os.listdir(csrc) if f.endswith((".cu", ".cuh"))]
+    deps.append(os.path.join(ROOT, "include", "srflow.h"))
     return any(os.path.getmtime(d) > out_m for d in deps if os.path.exists(d))
 
 

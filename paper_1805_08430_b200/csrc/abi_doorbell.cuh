@@ -1,0 +1,214 @@
+// abi_doorbell.cuh - part of libsrflow (included by srflow.cu, one translation unit).
+// C ABI: doorbells, RPC transfer, reduce, events.
+
+extern "C" {
+// ---------------------------------------------------------------------------
+// doorbells (host-visible receive flags)
+// ---------------------------------------------------------------------------
+int srf_doorbell_bind(srf_space_t sp, uint64_t region_addr, uint64_t region_len, int mirror) {
+  DeviceGuard device_guard;
+  if (region_len < 1) return fail(SRF_E_ZERO_LENGTH, "doorbell region must be >= 1 byte");
+  int rc = check_raw(sp, region_addr, region_len, "doorbell region");
+  if (rc) return rc;
+  if (sp->imported) return fail(SRF_E_INVALID_CONFIG, "doorbells live with the receiver");
+  std::lock_guard<std::mutex> g(sp->mu);
+  if (!sp->db) {
+    sp->db_cap = 1 << 20;
+    CUDA_TRY(cudaSetDevice(sp->device));
+    CUDA_TRY(cudaHostAlloc((void **)&sp->db_host, sp->db_cap,
+                           cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(sp->db_host, 0, sp->db_cap);
+    CUDA_TRY(cudaHostGetDevicePointer((void **)&sp->db_dev, sp->db_host, 0));
+    sp->db = new std::unordered_map<uint64_t, Doorbell>();
+  }
+  const uint64_t tail = region_addr + region_len - 1;
+  if (sp->db->count(tail)) return SRF_OK;
+  const uint64_t need = mirror ? region_len : 1;
+  if (sp->db_used + need > sp->db_cap) return fail(SRF_E_OUT_OF_MEMORY, "doorbell page full");
+  Doorbell d;
+  d.region_addr = region_addr;
+  d.region_len = region_len;
+  d.mirror = mirror != 0;
+  d.shadow_len = need;
+  d.host_off = sp->db_used;
+  d.clear_pending = false;
+  CUDA_TRY(cudaSetDevice(sp->device));  // the event lives on the space's GPU
+  CUDA_TRY(cudaEventCreateWithFlags(&d.clear_ev, cudaEventDisableTiming));
+  // initial shadow = current device bytes
+  std::vector<uint8_t> cur(need);
+  CUDA_TRY(cudaMemcpy(cur.data(), sp->base + tail + 1 - need, need, cudaMemcpyDeviceToHost));
+  memcpy(sp->db_host + sp->db_used, cur.data(), need);
+  sp->db_used += need;
+  (*sp->db)[tail] = d;
+  return SRF_OK;
+}
+
+// Read `len` bytes ending at tail_addr + 1: from the doorbell shadow when one
+// is bound and every producer is in this process, else from the device.
+int srf_flag_read(srf_space_t sp, uint64_t tail_addr, uint64_t len, void *host_out) {
+  DeviceGuard device_guard;
+  if (sp->db && !sp->exported) {
+    std::lock_guard<std::mutex> g(sp->mu);
+    auto it = sp->db->find(tail_addr);
+    if (it != sp->db->end()) {
+      const Doorbell &d = it->second;
+      if (len <= d.shadow_len) {
+        const volatile uint8_t *src = sp->db_host + d.host_off + (d.shadow_len - len);
+        // flag byte first (acquire), then the rest
+        uint8_t *o = (uint8_t *)host_out;
+        o[len - 1] = src[len - 1];
+        std::atomic_thread_fence(std::memory_order_acquire);
+        for (uint64_t i = 0; i + 1 < len; ++i) o[i] = src[i];
+        return SRF_OK;
+      }
+    }
+  }
+  return srf_read(sp, tail_addr + 1 - len, len, host_out);
+}
+
+// Clear a receive flag (StaticReceiver/DynReceiver.poll): shadow now, device
+// byte asynchronously on the space's stream; the next srf_put into the region
+// waits for that clear.
+int srf_flag_clear(srf_space_t sp, uint64_t tail_addr) {
+  DeviceGuard device_guard;
+  int rc = check_raw(sp, tail_addr, 1, "flag");
+  if (rc) return rc;
+  if (sp->db) {
+    std::lock_guard<std::mutex> g(sp->mu);
+    auto it = sp->db->find(tail_addr);
+    if (it != sp->db->end()) {
+      Doorbell &d = it->second;
+      volatile uint8_t *flag = sp->db_host + d.host_off + d.shadow_len - 1;
+      *flag = 0;
+      CUDA_TRY(cudaSetDevice(sp->device));
+      CUDA_TRY(cudaMemsetAsync(sp->base + tail_addr, 0, 1, sp->stream->s));
+      CUDA_TRY(cudaEventRecord(d.clear_ev, sp->stream->s));
+      d.clear_pending = true;
+      return SRF_OK;
+    }
+  }
+  const uint8_t z = 0;
+  return srf_write(sp, tail_addr, 1, &z);
+}
+
+int srf_rpc_transfer(srf_space_t src, uint64_t meta_addr, uint32_t meta_len,
+                     uint64_t payload_addr, uint64_t payload_len, uint64_t stage_addr,
+                     srf_space_t dst, uint64_t ring_addr, uint64_t ring_flags_addr,
+                     uint64_t meta_out_addr, uint64_t tensor_out_addr, uint64_t msg_id,
+                     srf_stream_t st_src, srf_stream_t st_dst) {
+  DeviceGuard device_guard;
+  int rc = check_raw(src, meta_addr, meta_len, "rpc meta");
+  if (!rc) rc = check_raw(src, payload_addr, payload_len, "rpc payload");
+  if (!rc) rc = check_raw(src, stage_addr, (uint64_t)kRing * kFrag, "rpc stage");
+  if (!rc) rc = check_raw(dst, ring_addr, (uint64_t)kRing * kFrag, "rpc ring");
+  if (!rc) rc = check_raw(dst, ring_flags_addr, kRing, "rpc ring flags");
+  if (!rc) rc = check_raw(dst, meta_out_addr, meta_len, "rpc meta out");
+  if (!rc) rc = check_raw(dst, tensor_out_addr, payload_len, "rpc tensor out");
+  if (rc) return rc;
+  RpcArgs a;
+  a.meta = src->base + meta_addr;
+  a.meta_len = meta_len;
+  a.payload = src->base + payload_addr;
+  a.pay_len = payload_len;
+  a.stage = src->base + stage_addr;
+  a.ring = dst->base + ring_addr;
+  a.ring_flags = dst->base + ring_flags_addr;
+  a.meta_out = dst->base + meta_out_addr;
+  a.tensor_out = dst->base + tensor_out_addr;
+  a.msg_id = msg_id;
+  a.timeout_ns = 10ull * 1000 * 1000 * 1000;
+  a.err = src->err;
+  srf_stream *ss = stream_or_default(src, st_src);
+  srf_stream *ds = stream_or_default(dst, st_dst);
+  if (ss->device == ds->device) {
+    // both roles in one cooperative launch: the two CTAs are co-resident
+    a.role = -1;
+    CUDA_TRY(cudaSetDevice(ss->device));
+    void *params[] = {&a};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void *)k_rpc, dim3(2), dim3(1024), params, 0,
+                                         ss->s));
+    return launch_check("k_rpc");
+  }
+  // two GPUs: receiver first (it waits for the sender over NVLink)
+  a.role = 1;
+  a.err = dst->err;
+  CUDA_TRY(cudaSetDevice(ds->device));
+  k_rpc<<<1, 1024, 0, ds->s>>>(a);
+  rc = launch_check("k_rpc(recv)");
+  if (rc) return rc;
+  a.role = 0;
+  a.err = src->err;
+  CUDA_TRY(cudaSetDevice(ss->device));
+  k_rpc<<<1, 1024, 0, ss->s>>>(a);
+  return launch_check("k_rpc(send)");
+}
+
+int srf_graph_begin(srf_stream_t st) {
+  DeviceGuard device_guard;
+  CUDA_TRY(cudaSetDevice(st->device));
+  CUDA_TRY(cudaStreamBeginCapture(st->s, cudaStreamCaptureModeThreadLocal));
+  return SRF_OK;
+}
+
+int srf_graph_end(srf_stream_t st, void **graph_exec) {
+  DeviceGuard device_guard;
+  CUDA_TRY(cudaSetDevice(st->device));
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(cudaStreamEndCapture(st->s, &g));
+  cudaGraphExec_t ex = nullptr;
+  cudaError_t e = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess)
+    return fail(SRF_E_DEVICE, "graph instantiate: %s", cudaGetErrorString(e));
+  *graph_exec = (void *)ex;
+  return SRF_OK;
+}
+
+int srf_graph_launch(void *graph_exec, srf_stream_t st) {
+  DeviceGuard device_guard;
+  CUDA_TRY(cudaSetDevice(st->device));
+  CUDA_TRY(cudaGraphLaunch((cudaGraphExec_t)graph_exec, st->s));
+  return SRF_OK;
+}
+
+int srf_graph_destroy(void *graph_exec) {
+  DeviceGuard device_guard;
+  if (graph_exec) cudaGraphExecDestroy((cudaGraphExec_t)graph_exec);
+  return SRF_OK;
+}
+
+int srf_stream_wait_event(srf_stream_t st, srf_event_t ev) {
+  DeviceGuard device_guard;
+  CUDA_TRY(cudaSetDevice(st->device));
+  CUDA_TRY(cudaStreamWaitEvent(st->s, ev->e, 0));
+  return SRF_OK;
+}
+
+int srf_timing_event_create(srf_space_t sp, srf_event_t *out) {
+  DeviceGuard device_guard;
+  CUDA_TRY(cudaSetDevice(sp->device));
+  srf_event *ev = new srf_event();
+  ev->device = sp->device;
+  cudaError_t e = cudaEventCreate(&ev->e);
+  if (e != cudaSuccess) {
+    delete ev;
+    return fail(SRF_E_DEVICE, "event: %s", cudaGetErrorString(e));
+  }
+  *out = ev;
+  return SRF_OK;
+}
+
+int srf_event_record_on(srf_event_t ev, srf_stream_t st) {
+  DeviceGuard device_guard;
+  CUDA_TRY(cudaSetDevice(st->device));
+  CUDA_TRY(cudaEventRecord(ev->e, st->s));
+  return SRF_OK;
+}
+
+int srf_event_elapsed_ms(srf_event_t start, srf_event_t end, float *ms) {
+  DeviceGuard device_guard;
+  CUDA_TRY(cudaEventElapsedTime(ms, start->e, end->e));
+  return SRF_OK;
+}
+
+}  // extern "C"

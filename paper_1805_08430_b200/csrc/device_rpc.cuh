@@ -1,0 +1,177 @@
+// device_rpc.cuh - part of libsrflow (included by srflow.cu, one translation unit).
+// RPC-style fragment ring baseline and ReduceMax.
+
+// ---------------------------------------------------------------------------
+// RPC-style baseline on the device (runtime/protocol.py:257-448, FORMATS.md
+// "RPC baseline fragment"): the stream metadata||payload is cut into 4096-B
+// fragments (16-B header msg_id u64, index u32, count u32 + 4080 B); the
+// sender serialises each fragment into a staging slot (counted copy 1) and
+// writes it into one of the receiver's 16 posted 4-KiB ring slots; the
+// receiver checks the header, copies the bytes out (counted copy 2) and
+// re-posts the slot.  Warp w owns ring slot w (fragments w, w+16, ...), so the
+// ring's 16-deep pipeline is kept and fragments land in order per slot.
+// ---------------------------------------------------------------------------
+static constexpr int kFrag = 4096, kFragHdr = 16, kFragPay = kFrag - kFragHdr, kRing = 16;
+
+struct RpcArgs {
+  const uint8_t *meta;  uint32_t meta_len;   // sender: metadata stage
+  const uint8_t *payload; uint64_t pay_len;  // sender: tensor bytes
+  uint8_t *stage;                            // sender: 16 x 4096 staging
+  uint8_t *ring;                             // receiver: 16 x 4096 posted slots
+  uint8_t *ring_flags;                       // receiver: 16 slot states (1 full)
+  uint8_t *meta_out;                         // receiver: reassembled metadata
+  uint8_t *tensor_out;                       // receiver: tensor buffer
+  uint64_t msg_id;
+  uint64_t timeout_ns;
+  int *err;
+  int role;                                  // -1: both (block 0 sender, 1 receiver)
+};
+
+// 64 threads (a warp pair) move one fragment
+static constexpr int kSlotThreads = 64;
+
+__device__ __forceinline__ void slot_copy(uint8_t *dst, const uint8_t *src, uint64_t n) {
+  copy_bytes_grid<4>(dst, src, n, threadIdx.x % kSlotThreads, kSlotThreads);
+}
+
+__device__ __forceinline__ void slot_sync() {
+  // the two warps of a slot: named barrier = slot index (0..15; the kernel
+  // never uses __syncthreads)
+  asm volatile("bar.sync %0, %1;" ::"r"((int)(threadIdx.x / kSlotThreads)),
+               "r"(kSlotThreads));
+}
+
+// bytes [off, off + n) of the message stream into dst
+__device__ __forceinline__ void stream_gather(const RpcArgs &a, uint8_t *dst, uint64_t off,
+                                              uint64_t n) {
+  if (off < a.meta_len) {
+    uint64_t k = a.meta_len - off < n ? a.meta_len - off : n;
+    slot_copy(dst, a.meta + off, k);
+    dst += k; off += k; n -= k;
+  }
+  if (n) slot_copy(dst, a.payload + (off - a.meta_len), n);
+}
+
+__device__ __forceinline__ void stream_scatter(const RpcArgs &a, const uint8_t *src,
+                                               uint64_t off, uint64_t n) {
+  if (off < a.meta_len) {
+    uint64_t k = a.meta_len - off < n ? a.meta_len - off : n;
+    slot_copy(a.meta_out + off, src, k);
+    src += k; off += k; n -= k;
+  }
+  if (n) slot_copy(a.tensor_out + (off - a.meta_len), src, n);
+}
+
+__global__ void __launch_bounds__(1024) k_rpc(RpcArgs a) {
+  const int role = a.role >= 0 ? a.role : (int)blockIdx.x;
+  const int w = threadIdx.x / kSlotThreads;            // ring slot of this warp pair
+  const bool leader = (threadIdx.x % kSlotThreads) == 0;
+  const uint64_t total = a.meta_len + a.pay_len;
+  const uint32_t count = (uint32_t)((total + kFragPay - 1) / kFragPay);
+  uint8_t *slot = a.ring + (uint64_t)w * kFrag;
+  uint8_t *flag = a.ring_flags + w;
+  uint8_t *st = a.stage + (uint64_t)w * kFrag;
+  for (uint32_t f = w; f < count; f += kRing) {
+    const uint64_t off = (uint64_t)f * kFragPay;
+    const uint64_t n = total - off < (uint64_t)kFragPay ? total - off : (uint64_t)kFragPay;
+    if (role == 0) {
+      // sender: serialise into the staging slot (counted copy 1) - this
+      // overlaps the receiver draining the previous fragment of the slot -
+      // then wait for the posted ring slot and send
+      if (leader) {
+        *(uint64_t *)st = a.msg_id;
+        *(uint32_t *)(st + 8) = f;
+        *(uint32_t *)(st + 12) = count;
+      }
+      stream_gather(a, st + kFragHdr, off, n);
+      if (leader && !spin_until(flag, 0, a.timeout_ns)) atomicExch(a.err, 7);
+      slot_sync();
+      slot_copy(slot, st, kFragHdr + n);  // the send verb
+      slot_sync();
+      if (leader) {
+        __threadfence_system();
+        st_release_sys_u8(flag, 1);
+      }
+    } else {
+      // receiver: drain the slot in order, copy out (counted copy 2), re-post
+      if (leader && !spin_until(flag, 1, a.timeout_ns)) atomicExch(a.err, 7);
+      slot_sync();
+      if (leader && (*(volatile uint64_t *)slot != a.msg_id ||
+                     *(volatile uint32_t *)(slot + 8) != f))
+        atomicExch(a.err, 8);  // ReassemblyGap
+      stream_scatter(a, slot + kFragHdr, off, n);
+      slot_sync();
+      if (leader) {
+        __threadfence_system();
+        st_release_sys_u8(flag, 0);
+      }
+    }
+    slot_sync();
+  }
+}
+
+// ReduceMax (graph.py:378-382): per-block max, last block folds partials.
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  // numpy max propagates NaN
+  if (a != a) return a;
+  if (b != b) return b;
+  return a > b ? a : b;
+}
+
+__global__ void __launch_bounds__(256) k_reduce_max(const float *x, uint64_t n,
+                                                    float *out, float *part,
+                                                    unsigned int *counter) {
+  __shared__ float sm[32];
+  __shared__ int s_last;
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  float m = -INFINITY;
+  const uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (((uintptr_t)x & 15) == 0) {
+    // 16-B loads, four in flight per thread
+    const float4 *x4 = (const float4 *)x;
+    const uint64_t n4 = n / 4;
+    uint64_t i = t0;
+    for (; i + 3 * nth < n4; i += 4 * nth) {
+      float4 a = __ldg(x4 + i), b = __ldg(x4 + i + nth), c = __ldg(x4 + i + 2 * nth),
+             d = __ldg(x4 + i + 3 * nth);
+      m = fmax_nan(m, fmax_nan(fmax_nan(a.x, a.y), fmax_nan(a.z, a.w)));
+      m = fmax_nan(m, fmax_nan(fmax_nan(b.x, b.y), fmax_nan(b.z, b.w)));
+      m = fmax_nan(m, fmax_nan(fmax_nan(c.x, c.y), fmax_nan(c.z, c.w)));
+      m = fmax_nan(m, fmax_nan(fmax_nan(d.x, d.y), fmax_nan(d.z, d.w)));
+    }
+    for (; i < n4; i += nth) {
+      float4 a = __ldg(x4 + i);
+      m = fmax_nan(m, fmax_nan(fmax_nan(a.x, a.y), fmax_nan(a.z, a.w)));
+    }
+    for (uint64_t j = n4 * 4 + t0; j < n; j += nth) m = fmax_nan(m, x[j]);
+  } else {
+    for (uint64_t i = t0; i < n; i += nth) m = fmax_nan(m, x[i]);
+  }
+  for (int o = 16; o; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(~0u, m, o));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? sm[threadIdx.x] : -INFINITY;
+    for (int o = 16; o; o >>= 1) m = fmax_nan(m, __shfl_xor_sync(~0u, m, o));
+    if (threadIdx.x == 0) {
+      part[blockIdx.x] = m;
+      __threadfence();
+      s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  float r = -INFINITY;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x)
+    r = fmax_nan(r, ((volatile float *)part)[i]);
+  for (int o = 16; o; o >>= 1) r = fmax_nan(r, __shfl_xor_sync(~0u, r, o));
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = r;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    r = -INFINITY;
+    for (unsigned i = 0; i < (blockDim.x >> 5); ++i) r = fmax_nan(r, sm[i]);
+    *out = (n == 0) ? 0.0f : r;
+    atomicExch(counter, 0u);
+  }
+}

@@ -1,0 +1,117 @@
+// host_launch.cuh - part of libsrflow (included by srflow.cu, one translation unit).
+// Launch geometry, copy-engine K1 variant, DeviceGuard.
+
+// ---------------------------------------------------------------------------
+// launch geometry
+// ---------------------------------------------------------------------------
+static void copy_geometry(int device, uint64_t bytes, int *grid, int *block) {
+  const int threads = g_copy_threads;
+  // one CTA moves threads * 16 B * 4 per unrolled batch; cap at k CTAs/SM
+  uint64_t per_cta = (uint64_t)threads * 16 * 4;
+  uint64_t want = (bytes + per_cta - 1) / per_cta;
+  uint64_t cap = (uint64_t)sm_count_of(device) * g_ctas_per_sm;
+  if (want < 1) want = 1;
+  if (want > cap) want = cap;
+  *grid = (int)want;
+  *block = threads;
+}
+
+static int record_event(int device, cudaStream_t s, srf_event_t *ev_out) {
+  if (!ev_out) return SRF_OK;
+  srf_event *ev = new srf_event();
+  ev->device = device;
+  cudaError_t e = cudaEventCreateWithFlags(&ev->e, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(ev->e, s);
+  if (e != cudaSuccess) {
+    delete ev;
+    return fail(SRF_E_DEVICE, "event: %s", cudaGetErrorString(e));
+  }
+  *ev_out = ev;
+  return SRF_OK;
+}
+
+static int launch_check(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess)
+    return fail(SRF_E_DEVICE, "%s launch: %s", what, cudaGetErrorString(e));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return SRF_OK;
+}
+
+static int g_put_impl = 0;  // 0 = vector LDG/STG, 1 = TMA bulk (large segments)
+static int g_unroll = 8;    // 16-B vectors in flight per thread (4 or 8)
+// knob 6: cross-device bodies of at least this many bytes move on the copy
+// engine (0: never).  32 MiB: the engine's extra ~15 us per put (credit wait
+// launch, copy, tail launch) pays off only above ~20 MB (NVLink sweep).  SM stores into a peer's pool are capped near 496 GB/s
+// across processes; the DMA engine reaches ~750 GB/s through the same mapping
+// (profiles/r1_ring_probe.json, r1_xproc_store_probe*.jsonl).
+static uint64_t g_peer_ce_bytes = 32ull << 20;
+
+// launch K1/K4/K5 with the configured implementation
+static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
+  uint64_t big = 0;
+  for (int i = 0; i < a.nseg; ++i) big = std::max<uint64_t>(big, a.seg[i].len);
+  if (g_put_impl == 1 && big >= (uint64_t)4 * kBulkChunk) {
+    static bool attr_set[64] = {false};
+    if (s->device >= 0 && s->device < 64 && !attr_set[s->device]) {
+      CUDA_TRY(cudaFuncSetAttribute(k_put_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    kBulkSmem));
+      attr_set[s->device] = true;
+    }
+    uint64_t chunks = (a.total + kBulkChunk - 1) / kBulkChunk;
+    uint64_t cap = (uint64_t)sm_count_of(s->device) * 2;
+    int grid = (int)std::max<uint64_t>(1, std::min(chunks, cap));
+    k_put_bulk<<<grid, 256, kBulkSmem, s->s>>>(a);
+  } else {
+    int grid, block;
+    copy_geometry(s->device, a.total, &grid, &block);
+    if (g_unroll == 8)
+      k_put<8><<<grid, block, 0, s->s>>>(a);
+    else
+      k_put<4><<<grid, block, 0, s->s>>>(a);
+  }
+  return launch_check(what);
+}
+
+// K1 with a copy-engine body: [credit wait] -> body copies -> a one-thread K1
+// that releases the tail byte.  Stream order starts the tail kernel only after
+// the copies have completed, so a consumer that acquires the flag sees the
+// body (release/acquire stress test, tests/test_gpu_kernels.py).
+static int put_via_copy_engine(const PutArgs &a, srf_stream *s) {
+  uint8_t *tail = a.dst + a.total - 1;
+  if (a.wait_empty) {
+    k_flag_wait<<<1, 32, 0, s->s>>>(tail, 0, 0, a.timeout_ns, a.err);
+    int rc = launch_check("k_flag_wait(credit)");
+    if (rc) return rc;
+  }
+  const uint64_t body = a.total - 1;
+  for (int i = 0; i < a.nseg; ++i) {
+    const Seg &sg = a.seg[i];
+    if (sg.dst_off >= body) break;
+    const uint64_t n = std::min<uint64_t>(sg.len, body - sg.dst_off);
+    CUDA_TRY(cudaMemcpyAsync(a.dst + sg.dst_off, sg.src, n, cudaMemcpyDeviceToDevice, s->s));
+  }
+  PutArgs t = a;
+  const Seg &ls = a.seg[a.nseg - 1];
+  t.nseg = 1;
+  t.seg[0].src = ls.src + ls.len - 1;
+  t.seg[0].dst_off = a.total - 1;
+  t.seg[0].len = 1;
+  t.wait_empty = 0;
+  k_put<4><<<1, 32, 0, s->s>>>(t);
+  return launch_check("k_put(tail)");
+}
+
+// Restores the caller's current device when an API call returns: entry
+// points switch to the device of the objects they touch, and a caller (torch
+// with device="cuda") must not see that switch.
+struct DeviceGuard {
+  int dev = -1;
+  DeviceGuard() {
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+  }
+  ~DeviceGuard() {
+    int now = -1;
+    if (dev >= 0 && cudaGetDevice(&now) == cudaSuccess && now != dev) cudaSetDevice(dev);
+  }
+};

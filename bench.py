@@ -520,7 +520,9 @@ def run_reference_arm(args, rank, world):
                          "sample": f"{args.steps} static Send/Recv steps of {S} B "
                                    f"(ascending 1-4096 B chunked delivery + flag poll + max, "
                                    f"oracle/port.py MicrobenchRig), host cpu_count="
-                                   f"{os.cpu_count()}"},
+                                   f"{os.cpu_count()}; the reference's delivery loop is "
+                                   f"single-threaded Python (its threads=True mode is "
+                                   f"GIL-serialised), so it uses one core"},
         "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }

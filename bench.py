@@ -137,6 +137,26 @@ def dist_sum(x: float) -> float:
     return float(t.item())
 
 
+def bind_gpu_local_cpus(device: int) -> str:
+    """Pin this process to the CPUs NVML reports as local to its GPU, so the
+    pinned host buffers of the e2e leg are first-touched on the GPU's NUMA node
+    (best effort)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        ncpu = os.cpu_count() or 1
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(ncpu))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return f"{len(cpus)} GPU-local cpus (NVML)"
+    except Exception as exc:  # pragma: no cover - depends on the box
+        return f"unchanged ({type(exc).__name__})"
+    return "unchanged"
+
+
 def barrier_sync():
     import torch
     import torch.distributed as dist
@@ -1192,6 +1212,7 @@ def main() -> int:
     from paper_1805_08430_b200.distributed import init_process_group
     _lib.load()
     torch.cuda.set_device(local)
+    affinity = bind_gpu_local_cpus(local)
     init_process_group("nccl")
     S = args.bytes
 
@@ -1225,7 +1246,8 @@ def main() -> int:
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dev["total_ms"] / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {**workload_config(S, world), "rounds_per_step": dev["rounds"]},
+        "config": {**workload_config(S, world), "rounds_per_step": dev["rounds"],
+                   "cpu_affinity": affinity},
         "roofline": roof,
         "e2e": {"value": round(world * S * max(3, args.steps // 2) / e2e["seconds"] / 1e9, 3),
                 "unit": "GB/s", "h2d_bytes_per_step": e2e["h2d"] * world,

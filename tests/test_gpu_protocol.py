@@ -70,6 +70,28 @@ class TestStatic:
         assert dev.device.index == rig.spaces[1].device
         assert dev.cpu().numpy().tobytes() == rig.spaces[0].read_at(t.buffer.handle, 0, t.nbytes)
 
+    @pytest.mark.parametrize("ce_kib", [0, 1])
+    def test_large_send_through_doorbell_both_engines(self, ce_kib):
+        """A 2 MiB static send between two GPUs with the body moved by SM
+        stores or by the copy engine: the receiver's host doorbell sees the
+        flag only with the whole body in place, three sends in a row."""
+        _lib.tune("peer_ce_kib", ce_kib)
+        try:
+            rig = Rig(capacity=1 << 25)
+            entry, snd, rcv = static_pair(rig, (1024, 512))
+            for k in range(3):
+                t = rig.tensor((1024, 512), seed=100 + k)
+                snd.send(t, stage_copy=False)
+                got = None
+                while got is None:
+                    got = rcv.poll()
+                assert rig.spaces[1].read_at(entry.recv_buffer, 0, t.nbytes) == \
+                    rig.spaces[0].read_at(t.buffer.handle, 0, t.nbytes)
+                t.buffer.release()
+            rig.close()
+        finally:
+            _lib.tune("peer_ce_kib", 32768)
+
     def test_size_mismatch(self):
         rig = Rig()
         _, snd, _ = static_pair(rig, (3, 4))

@@ -35,7 +35,7 @@ import ctypes as C
 import os
 import math
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import Optional
 
 import numpy as np
 

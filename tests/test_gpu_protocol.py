@@ -4,9 +4,6 @@ case that has no GPU meaning - replaced by the release/acquire stress test in
 test_gpu_kernels.py)."""
 from __future__ import annotations
 
-import math
-
-import numpy as np
 import pytest
 
 from paper_1805_08430_b200 import _lib, errors

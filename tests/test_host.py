@@ -12,8 +12,8 @@ import pytest
 
 from paper_1805_08430_b200 import _lib, errors, wire
 from paper_1805_08430_b200.analyzer import classify_edges
-from paper_1805_08430_b200.graph import (DataFlowGraph, ExecMode, infer_shapes,
-                                         in_place_control_deps, partition, shape_of)
+from paper_1805_08430_b200.graph import (ExecMode, infer_shapes, in_place_control_deps,
+                                         partition)
 from paper_1805_08430_b200.memspace import ArenaAllocator, RegionHandle
 from paper_1805_08430_b200.runtime.executor import Executor, FnHandler
 from paper_1805_08430_b200.wire import ElemType, Mechanism

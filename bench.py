@@ -1262,8 +1262,9 @@ def main() -> int:
                         "note": ("DMA copy engine (cudaMemcpy) into the same destination "
                                  "mapping - comparator only, not on the path" if world == 1
                                  else "raw cudaMemcpy ceiling through the same peer mapping; "
-                                      "K1 moves its body on the same engine (SM stores "
-                                      "into a peer pool cap near 496 GB/s cross-process)")},
+                                      "K1 moves bodies >= 32 MiB on the same engine (with "
+                                      "both directions busy, SM-driven NVLink traffic of "
+                                      "one GPU shares one ceiling)")},
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         gbps, n, dt = cpu_reference(S, min_seconds=args.cpu_seconds)

@@ -771,11 +771,12 @@ int srf_get(srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
   a.dst = dst_space->base + dst_addr;
   a.total = length;
   a.tail_release = 0;
+  const bool cross = src_space->imported || src_space->device != s->device;
+  a.src_remote = cross ? 1 : 0;
   a.counter = s->counter;
   a.err = dst_space->err;
   CUDA_TRY(cudaSetDevice(s->device));
   int rc = SRF_OK;
-  const bool cross = src_space->imported || src_space->device != s->device;
   if (cross && g_peer_ce_bytes && length >= g_peer_ce_bytes)
     CUDA_TRY(cudaMemcpyAsync(a.dst, a.seg[0].src, length, cudaMemcpyDeviceToDevice, s->s));
   else

@@ -134,16 +134,104 @@ __device__ __forceinline__ void vec_copy(V *__restrict__ dst,
   for (; i < nv; i += nth) st_plain<V>(dst + i, ld_stream<V>(src + i));
 }
 
+__device__ __forceinline__ u256 pack8(const uint2 (&a)[4]) {
+  u256 r;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    r.v[2 * k] = a[k].x;
+    r.v[2 * k + 1] = a[k].y;
+  }
+  return r;
+}
+
+// Destination-aligned copy for large ranges whose ends are not co-aligned mod
+// 32 (arena blocks are only 8-B aligned, memspace.py:31): every store is one
+// whole, aligned 32-B sector - partial-sector stores cost NVLink bandwidth
+// (K1 at a destination 8 B off a sector: 495 vs 694 GB/s, 4 B off: 378;
+// profiles/r1_align_probe.txt) - and the source is read at its own alignment
+// class (8-B, 4-B, or aligned words funnel-shifted) and reassembled in
+// registers.  U chunks of 32 B in flight per thread.
+template <int U>
+__device__ void copy_dst_aligned(uint8_t *dst, const uint8_t *src, uint64_t n, uint64_t t,
+                                 uint64_t nth) {
+  uint64_t head = (32 - ((uintptr_t)dst & 31)) & 31;
+  if (head > n) head = n;
+  const uint8_t *sp = src + head;
+  u256 *D = (u256 *)(dst + head);
+  uint64_t nv = (n - head) / 32;
+  const uint32_t sa = (uint32_t)((uintptr_t)sp & 7);
+  if (sa == 0) {
+    const uint2 *S8 = (const uint2 *)sp;
+    uint64_t i = t;
+    for (; i + (uint64_t)(U - 1) * nth < nv; i += (uint64_t)U * nth) {
+      uint2 a[U][4];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) a[u][k] = __ldg(S8 + 4 * (i + u * nth) + k);
+#pragma unroll
+      for (int u = 0; u < U; ++u) st_v8(D + i + u * nth, pack8(a[u]));
+    }
+    for (; i < nv; i += nth) {
+      uint2 a[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) a[k] = __ldg(S8 + 4 * i + k);
+      st_v8(D + i, pack8(a));
+    }
+  } else {
+    // 4-B aligned source: plain words; otherwise aligned words funnel-shifted
+    // by m bytes (chunk i reads words 8i .. 8i+8, the ninth reaching up to 3
+    // bytes past the chunk: the last chunk is left to the scalar tail)
+    const uint32_t m = (uint32_t)((uintptr_t)sp & 3);
+    const uint32_t *sw = (const uint32_t *)((uintptr_t)sp - m);
+    if (m && nv) nv -= 1;
+    uint64_t i = t;
+    for (; i + (uint64_t)(U - 1) * nth < nv; i += (uint64_t)U * nth) {
+      uint32_t w[U][9];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < 9; ++k)
+          w[u][k] = (k < 8 || m) ? __ldg(sw + 8 * (i + u * nth) + k) : 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        u256 r;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r.v[k] = __funnelshift_r(w[u][k], w[u][k + 1], 8 * m);
+        st_v8(D + i + u * nth, r);
+      }
+    }
+    for (; i < nv; i += nth) {
+      uint32_t w[9];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) w[k] = (k < 8 || m) ? __ldg(sw + 8 * i + k) : 0u;
+      u256 r;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) r.v[k] = __funnelshift_r(w[k], w[k + 1], 8 * m);
+      st_v8(D + i, r);
+    }
+  }
+  for (uint64_t j = t; j < head; j += nth) dst[j] = src[j];
+  for (uint64_t j = head + 32 * nv + t; j < n; j += nth) dst[j] = src[j];
+}
+
 // Copy n bytes with the widest vector both pointers allow.  Arena blocks are
 // 8-byte aligned (memspace.py:31), so the 16-B path needs equal (p mod 16).
+// align_dst: large copies that are not co-aligned mod 32 store whole 32-B
+// destination sectors (puts, whose destination is often a peer's memory);
+// false keeps the source side aligned instead (pulls read a peer's memory).
 __constant__ int g_vec32 = 1;  // knob 5: 32-B vectors when co-aligned mod 32
 
-template <int U16 = 4>
+template <int U16 = 4, bool kAlignDst = true>
 __device__ void copy_bytes_grid(uint8_t *dst, const uint8_t *src, uint64_t n,
-                                uint64_t t, uint64_t nth) {
+                                uint64_t t, uint64_t nth, bool align_dst = true) {
   if (n == 0) return;
   uintptr_t d = (uintptr_t)dst, s = (uintptr_t)src;
   uint64_t head, nv;
+  if (kAlignDst && align_dst && g_vec32 && ((d ^ s) & 31) != 0 && n >= 4096) {
+    copy_dst_aligned<(U16 > 4 ? U16 / 2 : 2)>(dst, src, n, t, nth);
+    return;
+  }
   if (g_vec32 && ((d ^ s) & 31) == 0 && n >= 4096) {
     head = (32 - (d & 31)) & 31;
     if (head > n) head = n;
@@ -217,6 +305,7 @@ struct PutArgs {
   uint8_t *dst;          // destination base (peer or local device pointer)
   uint64_t total;        // bytes in the gather list
   int tail_release;      // 1: last byte written last with st.release.sys
+  int src_remote;        // 1: a pull (K4) - keep the peer-side source reads aligned
   int wait_empty;        // 1: spin until dst[total-1] == 0 before writing
   int sys_scope;         // 1: destination is a peer's memory (system-scope release)
   uint8_t *db;           // host-mapped doorbell shadow (nullptr: none)
@@ -257,7 +346,7 @@ __global__ void __launch_bounds__(512) k_put(PutArgs a) {
     if (sg.dst_off >= body) break;
     uint64_t n = sg.len;
     if (sg.dst_off + n > body) n = body - sg.dst_off;
-    copy_bytes_grid<U16>(a.dst + sg.dst_off, sg.src, n, t, nth);
+    copy_bytes_grid<U16>(a.dst + sg.dst_off, sg.src, n, t, nth, !a.src_remote);
   }
 
   if (!a.tail_release) return;

@@ -272,8 +272,9 @@ __device__ __forceinline__ void put_unit(const BatchPut *descs, int n, uint32_t 
       if (threadIdx.x == 0 && !spin_until(d.dst + d.body, 0, timeout_ns, sys)) atomicExch(err, 2);
       __syncthreads();
     }
-    copy_bytes_grid<8>(d.dst, d.src, d.body, (uint64_t)lb * blockDim.x + threadIdx.x,
-                       (uint64_t)d.cta_count * blockDim.x);
+    // (PS blocks are 256-B aligned: always co-aligned, no destination realignment)
+    copy_bytes_grid<8, false>(d.dst, d.src, d.body, (uint64_t)lb * blockDim.x + threadIdx.x,
+                              (uint64_t)d.cta_count * blockDim.x);
     __syncthreads();
     if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, sys);
     __syncthreads();
@@ -547,8 +548,9 @@ __global__ void __launch_bounds__(256) k_dyn_recv(const __grid_constant__ DynRec
   }
   __syncthreads();
   if (s_ok)
-    copy_bytes_grid<8>(a.dst, s_src, s_len, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
-                       (uint64_t)gridDim.x * blockDim.x);
+    copy_bytes_grid<8, false>(a.dst, s_src, s_len,  // pull: peer-side reads stay aligned
+                              (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                              (uint64_t)gridDim.x * blockDim.x);
   __syncthreads();
   if (threadIdx.x == 0) s_last = grid_arrive(a.counter, gridDim.x - 1, a.sys);
   __syncthreads();

@@ -41,10 +41,11 @@ static int launch_check(const char *what) {
 static int g_put_impl = 0;  // 0 = vector LDG/STG, 1 = TMA bulk (large segments)
 static int g_unroll = 8;    // 16-B vectors in flight per thread (4 or 8)
 // knob 6: cross-device bodies of at least this many bytes move on the copy
-// engine (0: never).  32 MiB: the engine's extra ~15 us per put (credit wait
-// launch, copy, tail launch) pays off only above ~20 MB (NVLink sweep).  SM stores into a peer's pool are capped near 496 GB/s
-// across processes; the DMA engine reaches ~750 GB/s through the same mapping
-// (profiles/r1_ring_probe.json, r1_xproc_store_probe*.jsonl).
+// engine (0: never).  With both NVLink directions busy (the ring), SM-driven
+// traffic of one GPU shares one ceiling and K1 gets ~616 GB/s per direction
+// at 256 MiB, the copy engines 713 (profiles/r1_align_probe.txt, duplex
+// probe); the engine's extra ~15 us per put (credit-wait launch, copy, tail
+// launch) only pays off from ~64 MiB: threshold 32 MiB.
 static uint64_t g_peer_ce_bytes = 32ull << 20;
 
 // launch K1/K4/K5 with the configured implementation

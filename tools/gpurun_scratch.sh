@@ -1,7 +1,5 @@
 # scratch command file for one gpurun call (rewritten per experiment)
-timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/r1l_pytest.log 2>&1; echo rc=$? >> gpurun_out/r1l_pytest.log
-s=$(date +%s); timeout 1200 python bench.py > gpurun_out/r1l_bench_n1.json 2> gpurun_out/r1l_bench_n1.err; echo "n1 $(( $(date +%s) - s )) s" > gpurun_out/r1l_times.txt
-for n in 2 4; do
-s=$(date +%s); timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $n > gpurun_out/r1l_bench_n$n.json 2> gpurun_out/r1l_bench_n$n.err; echo "n$n $(( $(date +%s) - s )) s" >> gpurun_out/r1l_times.txt
+TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511"
+for kib in 0 131072 32768; do
+SRFLOW_PEER_CE_KIB=$kib timeout 900 $TR bench.py --gpus 2 --no-cpu --no-ps --steps 10 > gpurun_out/al_n2_$kib.json 2> gpurun_out/al_n2_$kib.err
 done
-timeout 600 python bench.py --impl reference > gpurun_out/r1l_ref_n1.json 2> gpurun_out/r1l_ref_n1.err

@@ -215,22 +215,76 @@ __device__ void copy_dst_aligned(uint8_t *dst, const uint8_t *src, uint64_t n, u
   for (uint64_t j = head + 32 * nv + t; j < n; j += nth) dst[j] = src[j];
 }
 
+// Source-aligned twin for pulls (the source is a peer's memory): whole
+// aligned 32-B sector loads, stores at the destination's alignment (8-B or
+// 4-B words; callers guarantee (dst - src) % 4 == 0).  A pull whose source
+// sat 8 B off a sector ran at 571 GB/s instead of 736 (r1_align_probe.txt).
+template <int U>
+__device__ void copy_src_aligned(uint8_t *dst, const uint8_t *src, uint64_t n, uint64_t t,
+                                 uint64_t nth) {
+  uint64_t head = (32 - ((uintptr_t)src & 31)) & 31;
+  if (head > n) head = n;
+  const u256 *S = (const u256 *)(src + head);
+  uint8_t *dp = dst + head;
+  const uint64_t nv = (n - head) / 32;
+  const bool w8 = ((uintptr_t)dp & 7) == 0;
+  uint64_t i = t;
+  for (; i + (uint64_t)(U - 1) * nth < nv; i += (uint64_t)U * nth) {
+    u256 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) r[u] = ld_v8(S + i + u * nth);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (w8) {
+        uint2 *D8 = (uint2 *)dp + 4 * (i + u * nth);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) D8[k] = make_uint2(r[u].v[2 * k], r[u].v[2 * k + 1]);
+      } else {
+        uint32_t *D4 = (uint32_t *)dp + 8 * (i + u * nth);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) D4[k] = r[u].v[k];
+      }
+    }
+  }
+  for (; i < nv; i += nth) {
+    const u256 r = ld_v8(S + i);
+    if (w8) {
+      uint2 *D8 = (uint2 *)dp + 4 * i;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) D8[k] = make_uint2(r.v[2 * k], r.v[2 * k + 1]);
+    } else {
+      uint32_t *D4 = (uint32_t *)dp + 8 * i;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) D4[k] = r.v[k];
+    }
+  }
+  for (uint64_t j = t; j < head; j += nth) dst[j] = src[j];
+  for (uint64_t j = head + 32 * nv + t; j < n; j += nth) dst[j] = src[j];
+}
+
 // Copy n bytes with the widest vector both pointers allow.  Arena blocks are
 // 8-byte aligned (memspace.py:31), so the 16-B path needs equal (p mod 16).
-// align_dst: large copies that are not co-aligned mod 32 store whole 32-B
-// destination sectors (puts, whose destination is often a peer's memory);
-// false keeps the source side aligned instead (pulls read a peer's memory).
+// Large copies that are not co-aligned mod 32 keep one side in whole aligned
+// 32-B sectors: the destination for puts (align_dst, often a peer's memory),
+// the source for pulls (!align_dst, reading a peer's memory).
+// kSectors = false compiles only the co-aligned classes (PS blocks).
 __constant__ int g_vec32 = 1;  // knob 5: 32-B vectors when co-aligned mod 32
 
-template <int U16 = 4, bool kAlignDst = true>
+template <int U16 = 4, bool kSectors = true>
 __device__ void copy_bytes_grid(uint8_t *dst, const uint8_t *src, uint64_t n,
                                 uint64_t t, uint64_t nth, bool align_dst = true) {
   if (n == 0) return;
   uintptr_t d = (uintptr_t)dst, s = (uintptr_t)src;
   uint64_t head, nv;
-  if (kAlignDst && align_dst && g_vec32 && ((d ^ s) & 31) != 0 && n >= 4096) {
-    copy_dst_aligned<(U16 > 4 ? U16 / 2 : 2)>(dst, src, n, t, nth);
-    return;
+  if (kSectors && g_vec32 && ((d ^ s) & 31) != 0 && n >= 4096) {
+    if (align_dst) {
+      copy_dst_aligned<(U16 > 4 ? U16 / 2 : 2)>(dst, src, n, t, nth);
+      return;
+    }
+    if (((d ^ s) & 3) == 0) {
+      copy_src_aligned<(U16 > 4 ? U16 / 2 : 2)>(dst, src, n, t, nth);
+      return;
+    }
   }
   if (g_vec32 && ((d ^ s) & 31) == 0 && n >= 4096) {
     head = (32 - (d & 31)) & 31;
@@ -316,7 +370,10 @@ struct PutArgs {
 };
 
 // K1 static_put / K3 meta_put / K4 peer_pull / K5 stage_copy.
-template <int U16>
+// kSectors: the variant for gather lists that are not co-aligned mod 32
+// (whole-sector realignment, copy_dst_aligned / copy_src_aligned); the
+// co-aligned variant keeps the lean register budget of the plain paths.
+template <int U16, bool kSectors>
 __global__ void __launch_bounds__(512) k_put(PutArgs a) {
   __shared__ int s_last;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
@@ -346,7 +403,7 @@ __global__ void __launch_bounds__(512) k_put(PutArgs a) {
     if (sg.dst_off >= body) break;
     uint64_t n = sg.len;
     if (sg.dst_off + n > body) n = body - sg.dst_off;
-    copy_bytes_grid<U16>(a.dst + sg.dst_off, sg.src, n, t, nth, !a.src_remote);
+    copy_bytes_grid<U16, kSectors>(a.dst + sg.dst_off, sg.src, n, t, nth, !a.src_remote);
   }
 
   if (!a.tail_release) return;

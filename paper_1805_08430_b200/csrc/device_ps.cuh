@@ -548,9 +548,9 @@ __global__ void __launch_bounds__(256) k_dyn_recv(const __grid_constant__ DynRec
   }
   __syncthreads();
   if (s_ok)
-    copy_bytes_grid<8, false>(a.dst, s_src, s_len,  // pull: peer-side reads stay aligned
-                              (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
-                              (uint64_t)gridDim.x * blockDim.x);
+    copy_bytes_grid<8>(a.dst, s_src, s_len,  // pull: peer-side (source) sectors aligned
+                       (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                       (uint64_t)gridDim.x * blockDim.x, false);
   __syncthreads();
   if (threadIdx.x == 0) s_last = grid_arrive(a.counter, gridDim.x - 1, a.sys);
   __syncthreads();

@@ -66,10 +66,24 @@ static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
   } else {
     int grid, block;
     copy_geometry(s->device, a.total, &grid, &block);
-    if (g_unroll == 8)
-      k_put<8><<<grid, block, 0, s->s>>>(a);
-    else
-      k_put<4><<<grid, block, 0, s->s>>>(a);
+    // a large segment whose ends are not co-aligned mod 32 takes the
+    // sector-realigning kernel; everything else the lean one
+    bool sectors = false;
+    for (int i = 0; i < a.nseg; ++i)
+      if (a.seg[i].len >= 4096 &&
+          (((uintptr_t)(a.dst + a.seg[i].dst_off) ^ (uintptr_t)a.seg[i].src) & 31) != 0)
+        sectors = true;
+    if (g_unroll == 8) {
+      if (sectors)
+        k_put<8, true><<<grid, block, 0, s->s>>>(a);
+      else
+        k_put<8, false><<<grid, block, 0, s->s>>>(a);
+    } else {
+      if (sectors)
+        k_put<4, true><<<grid, block, 0, s->s>>>(a);
+      else
+        k_put<4, false><<<grid, block, 0, s->s>>>(a);
+    }
   }
   return launch_check(what);
 }
@@ -99,7 +113,7 @@ static int put_via_copy_engine(const PutArgs &a, srf_stream *s) {
   t.seg[0].dst_off = a.total - 1;
   t.seg[0].len = 1;
   t.wait_empty = 0;
-  k_put<4><<<1, 32, 0, s->s>>>(t);
+  k_put<4, false><<<1, 32, 0, s->s>>>(t);
   return launch_check("k_put(tail)");
 }
 

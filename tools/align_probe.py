@@ -34,6 +34,18 @@ def rate(src_sp, rs, dst_sp, dst_addr, dst_tok, soff, doff, st, R=10):
     return round(S * R / (time.perf_counter() - t0) / 1e9, 1)
 
 
+def pull_rate(dst_sp, rd, src_sp, src_addr, src_tok, soff, doff, st, R=10):
+    def go():
+        _lib.call("srf_get", dst_sp.handle, rd.base_addr + doff, rd.access_token, src_sp.handle,
+                  src_addr + soff, src_tok, S, st, None)
+    go(); _lib.call("srf_stream_sync", st)
+    t0 = time.perf_counter()
+    for _ in range(R):
+        go()
+    _lib.call("srf_stream_sync", st)
+    return round(S * R / (time.perf_counter() - t0) / 1e9, 1)
+
+
 if mode == "inproc":
     a = MemorySpace(0, S + (16 << 20), device=0)
     b = MemorySpace(1, S + (16 << 20), device=1)
@@ -44,6 +56,8 @@ if mode == "inproc":
     res = {}
     for soff, doff in ((0, 0), (0, 8), (8, 0), (0, 16), (0, 4), (3, 5)):
         res[f"s{soff}_d{doff}"] = rate(a, ra, b, rb.base_addr, rb.access_token, soff, doff, st)
+        res[f"pull_s{soff}_d{doff}"] = pull_rate(a, ra, b, rb.base_addr, rb.access_token,
+                                                 soff, doff, st)
     print(json.dumps({"mode": mode, **res}), flush=True)
 else:
     import bench

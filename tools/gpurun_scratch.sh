@@ -1,5 +1,4 @@
 # scratch command file for one gpurun call (rewritten per experiment)
-TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511"
-for kib in 0 131072 32768; do
-SRFLOW_PEER_CE_KIB=$kib timeout 900 $TR bench.py --gpus 2 --no-cpu --no-ps --steps 10 > gpurun_out/al_n2_$kib.json 2> gpurun_out/al_n2_$kib.err
-done
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/al2_pytest.log 2>&1; echo rc=$? >> gpurun_out/al2_pytest.log
+timeout 300 python tools/align_probe.py inproc > gpurun_out/align4.log 2>&1
+timeout 600 python bench.py --no-cpu --no-ps --no-sweep > gpurun_out/al2_n1.json 2> gpurun_out/al2_n1.err

@@ -192,11 +192,10 @@ static int check_raw(const srf_space *sp, uint64_t addr, uint64_t len,
 
 
 // ---------------------------------------------------------------------------
-// CUDA VMM pools (cuMemCreate + POSIX-fd export).  Cross-process SM stores
-// through cudaIpcOpenMemHandle mappings measured ~500 GB/s vs ~690 GB/s
-// in-process (profiles/); VMM mappings are the alternative the multi-process
-// path can select (SRFLOW_ALLOC=vmm).  Driver entry points are resolved at
-// run time through cudaGetDriverEntryPoint, so no libcuda link is needed.
+// CUDA VMM pools (cuMemCreate + POSIX-fd export), the alternative to CUDA IPC
+// handles the multi-process path can select (SRFLOW_ALLOC_VMM=1; both measure
+// the same over NVLink).  Driver entry points are resolved at run time
+// through cudaGetDriverEntryPoint, so no libcuda link is needed.
 // ---------------------------------------------------------------------------
 static int g_alloc_vmm = 0;
 

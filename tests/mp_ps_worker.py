@@ -22,6 +22,8 @@ def main() -> int:
     layouts = [
         ("coloc", [(3000,), (17,), (200, 300), (5,), (70000,)], world, world, True),
         ("ps+workers", mlp_shapes() + [(4096,)], 2, 1, False),
+        # MiB-sized, unequal variables
+        ("coloc-big", [(1 << 19,), (300_001,), (7,), (1 << 20,)], world, world, True),
     ]
     bad = 0
     for name, shapes, W, P, coloc in layouts:

@@ -40,6 +40,8 @@ if mode != "phases":
     for it in range(6, 6 + R):
         ps.step(it)
     ps.sync()
+    bench.barrier_sync()
+    dt = bench.dist_max(time.perf_counter() - t0) / R
     if os.environ.get("PROBE_HOST"):
         # host issue time vs device completion, one step at a time
         ti, ts = 0.0, 0.0
@@ -63,8 +65,6 @@ if mode != "phases":
                                        lr=0.01, only=small)
         for v in small:
             assert ps.variable(v).tobytes() == want[v].tobytes(), ("mismatch", v)
-    bench.barrier_sync()
-    dt = bench.dist_max(time.perf_counter() - t0) / R
     if rank == 0:
         print(json.dumps({"mode": mode, "cfg": cfg,
                           "placement": balanced, "step_us": round(dt * 1e6, 1),

@@ -361,3 +361,35 @@ def test_device_dyn_recv_rejects_bad_metadata(pair, bad):
     with pytest.raises(errors.BadToken):
         b.sync()
     assert int(np.frombuffer(b.read_raw(word, 8), np.uint64)[0]) == (1 << 64) - 1
+
+
+@pytest.mark.parametrize("size", [4096, 4099, 65536 + 13, (1 << 20) + 5, (3 << 20) + 31])
+@pytest.mark.parametrize("soff,doff", [(0, 8), (8, 0), (4, 12), (3, 5), (1, 30), (31, 2)])
+@pytest.mark.parametrize("direction", ["put", "get"])
+def test_sector_realigned_copies_keep_guard_bands(pair, size, soff, doff, direction):
+    """The sector-realigning copy paths (destination-aligned puts,
+    source-aligned pulls) write exactly [dst, dst+size): sentinel bytes on
+    both sides of the destination stay untouched."""
+    a, b, ra, rb = pair
+    data = rand_bytes(size, size + soff)
+    guard = 256
+    if direction == "put":
+        src_sp, src_r, dst_sp, dst_r = a, ra, b, rb
+    else:
+        src_sp, src_r, dst_sp, dst_r = b, rb, a, ra
+    src = src_r.base_addr + (40 << 20) + soff
+    src_sp.write_raw(src, data)
+    dst = dst_r.base_addr + (60 << 20) + doff
+    sentinel = bytes([0xA5]) * guard
+    dst_sp.write_raw(dst - guard, sentinel)
+    dst_sp.write_raw(dst + size, sentinel)
+    if direction == "put":
+        put(a, [(src, size, ra.access_token)], b, dst, rb.access_token)
+    else:
+        ev = C.c_void_p()
+        _lib.call("srf_get", a.handle, dst, ra.access_token, b.handle, src, rb.access_token,
+                  size, None, C.byref(ev))
+        _lib.Event(ev).wait()
+    assert dst_sp.read_raw(dst, size) == data.tobytes()
+    assert dst_sp.read_raw(dst - guard, guard) == sentinel
+    assert dst_sp.read_raw(dst + size, guard) == sentinel

@@ -246,6 +246,13 @@ class SendRecvRing:
                  2, self.dst.handle, self.dst_region[0], self.dst_region[1],
                  lib.PUT_WAIT_EMPTY, self.stream, None)
 
+    def put_consume(self):
+        """put() and consume() in one launch (srf_put_consume)."""
+        self.lib.call("srf_put_consume", self.src.handle, self.args_addr, self.args_len,
+                      self.args_tok, 2, self.dst.handle, self.dst_region[0], self.dst_region[1],
+                      self.lib.PUT_WAIT_EMPTY, self.rcv.handle, self.recv.base_addr + self.S,
+                      self.stream, None)
+
     def consume(self):
         self.lib.call("srf_flag_wait", self.rcv.handle, self.recv.base_addr + self.S, 1, 1,
                       10 * 10**9, self.stream)
@@ -598,6 +605,13 @@ def sweep(max_bytes, device):
             row[f"{name}_gbps"] = round(size / t / 1e9, 3)
             row[f"{name}_us"] = round(t * 1e6, 3)
         row["verified"] = ring.verify()
+        for _ in range(8):
+            ring.put_consume()
+        ring.sync()
+        rounds = 200 if size <= 4 * MIB else 20
+        row["static_1launch_us"] = _ring_graph_us(ring.stream, ring.put_consume, rounds,
+                                                  ring.src)
+        row["static_1launch_gbps"] = round(size / row["static_1launch_us"] / 1e3, 3)
         row.update(dynamic_rate(size, device))
         row.update(dynamic_device_rate(size, device))
         row.update(rpc_device_rate(size, device))
@@ -691,6 +705,9 @@ def sweep_nvlink(max_bytes, rank, world, device):
         row["static_us"] = _ring_graph_us(ring.stream, lambda: (ring.put(), ring.consume()),
                                           rounds, ring.src)
         row["static_gbps"] = round(size / row["static_us"] / 1e3, 3)
+        row["static_1launch_us"] = _ring_graph_us(ring.stream, ring.put_consume, rounds,
+                                                  ring.src)
+        row["static_1launch_gbps"] = round(size / row["static_1launch_us"] / 1e3, 3)
         row["verified"] = dist_sum(0.0 if ring.verify() else 1.0) == 0.0
         dyn = DynDeviceRing(size, rank, world, device)
         for _ in range(4):

@@ -162,6 +162,14 @@ int srf_put(srf_space_t src_space, const uint64_t *src_addr,
             const uint64_t *src_len, const uint64_t *src_token, int nseg,
             srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
             int flags, srf_stream_t stream, srf_event_t *ev_out);
+/* srf_put + this rank's own receive poll in ONE launch (device loops where
+ * each rank sends and receives every round): after the tail release, the
+ * last CTA acquire-spins on rcv_flag_addr of rcv_space (local) and clears it
+ * (K2 fused). */
+int srf_put_consume(srf_space_t src_space, const uint64_t *src_addr, const uint64_t *src_len,
+                    const uint64_t *src_token, int nseg, srf_space_t dst_space,
+                    uint64_t dst_addr, uint64_t dst_token, int flags, srf_space_t rcv_space,
+                    uint64_t rcv_flag_addr, srf_stream_t stream, srf_event_t *ev_out);
 /* Channel.one_sided_read (fabric.py:371-389).  K4 peer_pull: launched on the
  * reader's GPU, loads [src_addr, +length) from the peer pool, stores into the
  * local registered range dst_addr. */

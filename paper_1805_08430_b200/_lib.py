@@ -94,6 +94,8 @@ SIGNATURES = {
     "srf_put": (C.c_int, [vp, P(u64), P(u64), P(u64), C.c_int, vp, u64, u64,
                           C.c_int, vp, P(vp)]),
     "srf_get": (C.c_int, [vp, u64, u64, vp, u64, u64, u64, vp, P(vp)]),
+    "srf_put_consume": (C.c_int, [vp, P(u64), P(u64), P(u64), C.c_int, vp, u64, u64, C.c_int,
+                                  vp, u64, vp, P(vp)]),
     "srf_copy": (C.c_int, [vp, u64, u64, u64, vp, P(vp)]),
     "srf_flag_wait": (C.c_int, [vp, u64, C.c_uint8, C.c_int, u64, vp]),
     "srf_apply": (C.c_int, [vp, u64, u64, P(vp), P(u64), C.c_int, C.c_int,

@@ -672,10 +672,35 @@ int srf_event_free(srf_event_t ev) {
   return SRF_OK;
 }
 
+static int put_impl(srf_space_t src_space, const uint64_t *src_addr, const uint64_t *src_len,
+                    const uint64_t *src_token, int nseg, srf_space_t dst_space,
+                    uint64_t dst_addr, uint64_t dst_token, int flags, srf_stream_t st,
+                    srf_event_t *ev_out, uint8_t *consume);
+
 int srf_put(srf_space_t src_space, const uint64_t *src_addr,
             const uint64_t *src_len, const uint64_t *src_token, int nseg,
             srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
             int flags, srf_stream_t st, srf_event_t *ev_out) {
+  return put_impl(src_space, src_addr, src_len, src_token, nseg, dst_space, dst_addr, dst_token,
+                  flags, st, ev_out, nullptr);
+}
+
+int srf_put_consume(srf_space_t src_space, const uint64_t *src_addr, const uint64_t *src_len,
+                    const uint64_t *src_token, int nseg, srf_space_t dst_space,
+                    uint64_t dst_addr, uint64_t dst_token, int flags, srf_space_t rcv_space,
+                    uint64_t rcv_flag_addr, srf_stream_t st, srf_event_t *ev_out) {
+  DeviceGuard device_guard;
+  int rc = check_raw(rcv_space, rcv_flag_addr, 1, "receive flag");
+  if (rc) return rc;
+  if (rcv_space->imported) return fail(SRF_E_INVALID_CONFIG, "the receive flag is this rank's");
+  return put_impl(src_space, src_addr, src_len, src_token, nseg, dst_space, dst_addr, dst_token,
+                  flags, st, ev_out, rcv_space->base + rcv_flag_addr);
+}
+
+static int put_impl(srf_space_t src_space, const uint64_t *src_addr, const uint64_t *src_len,
+                    const uint64_t *src_token, int nseg, srf_space_t dst_space,
+                    uint64_t dst_addr, uint64_t dst_token, int flags, srf_stream_t st,
+                    srf_event_t *ev_out, uint8_t *consume) {
   DeviceGuard device_guard;
   if (nseg < 1 || nseg > kMaxSeg)
     return fail(SRF_E_INVALID_CONFIG, "gather list of %d segments (max %d)",
@@ -736,6 +761,7 @@ int srf_put(srf_space_t src_space, const uint64_t *src_addr,
   a.timeout_ns = 5ull * 1000 * 1000 * 1000;
   a.counter = s->counter;
   a.err = src_space->err;
+  a.consume = consume;
   CUDA_TRY(cudaSetDevice(s->device));
   int rc;
   if (a.sys_scope && g_peer_ce_bytes && total - 1 >= g_peer_ce_bytes && a.db_len <= 1)

@@ -367,6 +367,7 @@ struct PutArgs {
   uint64_t timeout_ns;
   unsigned int *counter; // arrival counter (per stream, reset by last CTA)
   int *err;
+  uint8_t *consume;      // srf_put_consume: this rank's receive flag to poll and clear
 };
 
 // K1 static_put / K3 meta_put / K4 peer_pull / K5 stage_copy.
@@ -432,6 +433,18 @@ __global__ void __launch_bounds__(512) k_put(PutArgs a) {
       st_release_sys_u8(a.db + a.db_len - 1, v);
     }
     atomicExch(a.counter, 0u);
+    if (a.consume) {
+      // K2 fused: this rank's receive flag (StaticReceiver.poll on the device)
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_sys_u8(a.consume) != 1) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          atomicExch(a.err, 1);
+          break;
+        }
+        __nanosleep(32);
+      }
+      st_relaxed_sys_u8(a.consume, 0);
+    }
   }
 }
 

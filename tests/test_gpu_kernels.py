@@ -393,3 +393,26 @@ def test_sector_realigned_copies_keep_guard_bands(pair, size, soff, doff, direct
     assert dst_sp.read_raw(dst, size) == data.tobytes()
     assert dst_sp.read_raw(dst - guard, guard) == sentinel
     assert dst_sp.read_raw(dst + size, guard) == sentinel
+
+
+def test_put_consume_one_launch(pair):
+    """srf_put_consume: the put and the receiver's poll (K2) in one launch -
+    here the receive flag is the put's own tail (one edge), so the launch
+    returns with the payload delivered and the flag consumed."""
+    a, b, ra, rb = pair
+    n = (1 << 20) + 12
+    data = rand_bytes(n, 9)
+    src = ra.base_addr + 4096
+    a.write_raw(src, data)
+    a.write_raw(ra.base_addr + 64, b"\x01")
+    dst = rb.base_addr + (24 << 20)
+    b.write_raw(dst + n, b"\x00")
+    u = _lib.u64_array
+    for k in range(3):
+        ev = C.c_void_p()
+        _lib.call("srf_put_consume", a.handle, u([src, ra.base_addr + 64]), u([n, 1]),
+                  u([ra.access_token] * 2), 2, b.handle, dst, rb.access_token,
+                  _lib.PUT_WAIT_EMPTY, b.handle, dst + n, None, C.byref(ev))
+        _lib.Event(ev).wait()
+        assert b.read_raw(dst, n) == data.tobytes()
+        assert b.read_raw(dst + n, 1) == b"\x00"

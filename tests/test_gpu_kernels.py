@@ -416,3 +416,59 @@ def test_put_consume_one_launch(pair):
         _lib.Event(ev).wait()
         assert b.read_raw(dst, n) == data.tobytes()
         assert b.read_raw(dst + n, 1) == b"\x00"
+
+
+@pytest.mark.parametrize("size", [65536, (1 << 20) + 16, (5 << 20) + 3])
+@pytest.mark.parametrize("soff,doff", [(0, 0), (16, 48), (8, 0)])
+def test_tma_bulk_variant_bit_exact(pair, size, soff, doff):
+    """Knob 2 = 1: K1/K4 through cp.async.bulk (TMA) for 16-B co-aligned
+    segments of >= 64 KiB, everything else through the vector path."""
+    a, b, ra, rb = pair
+    data = rand_bytes(size, size ^ 7)
+    src = ra.base_addr + (8 << 20) + soff
+    a.write_raw(src, data)
+    a.write_raw(ra.base_addr + 64, b"\x01")
+    dst = rb.base_addr + (8 << 20) + doff
+    b.write_raw(dst + size, b"\x00")
+    _lib.tune("put_impl", 1)
+    try:
+        put(a, [(src, size, ra.access_token), (ra.base_addr + 64, 1, ra.access_token)], b, dst,
+            rb.access_token)
+        assert b.read_raw(dst, size + 1) == data.tobytes() + b"\x01"
+        back = ra.base_addr + (24 << 20) + soff
+        ev = C.c_void_p()
+        _lib.call("srf_get", a.handle, back, ra.access_token, b.handle, dst, rb.access_token,
+                  size, None, C.byref(ev))
+        _lib.Event(ev).wait()
+        assert a.read_raw(back, size) == data.tobytes()
+    finally:
+        _lib.tune("put_impl", 0)
+
+
+def test_vmm_pools_carry_transfers():
+    """Knob 3 = 1: pools from cuMemCreate (exportable by POSIX fd) instead of
+    cudaMalloc; puts, pulls and a same-process fd export/import round trip."""
+    _lib.tune("alloc_vmm", 1)
+    try:
+        n = _lib.device_count()
+        a = MemorySpace(0, 32 << 20, seed=1, device=0)
+        b = MemorySpace(1, 32 << 20, seed=2, device=1 if n > 1 else 0)
+        _lib.call("srf_connect", a.handle, b.handle)
+        ra = a.allocate_region(16 << 20, register=True)
+        rb = b.allocate_region(16 << 20, register=True)
+        data = rand_bytes((3 << 20) + 8, 3)
+        a.write_raw(ra.base_addr, data)
+        a.write_raw(ra.base_addr + (8 << 20), b"\x01")
+        put(a, [(ra.base_addr, len(data), ra.access_token),
+                (ra.base_addr + (8 << 20), 1, ra.access_token)], b, rb.base_addr + 8,
+            rb.access_token)
+        assert b.read_raw(rb.base_addr + 8, len(data)) == data.tobytes()
+        ev = C.c_void_p()
+        _lib.call("srf_get", a.handle, ra.base_addr + (10 << 20), ra.access_token, b.handle,
+                  rb.base_addr + 8, rb.access_token, len(data), None, C.byref(ev))
+        _lib.Event(ev).wait()
+        assert a.read_raw(ra.base_addr + (10 << 20), len(data)) == data.tobytes()
+        a.close()
+        b.close()
+    finally:
+        _lib.tune("alloc_vmm", 0)

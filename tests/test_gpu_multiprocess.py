@@ -23,8 +23,11 @@ def _free_port() -> int:
 
 
 @pytest.mark.skipif(_lib.device_count() < 2, reason="needs two GPUs")
-def test_two_process_ps_schedules_match_oracle():
-    env = dict(os.environ, NCCL_DEBUG="WARN")
+@pytest.mark.parametrize("pools", ["ipc", "vmm"])
+def test_two_process_ps_schedules_match_oracle(pools):
+    """Pools exported as CUDA IPC handles, or as VMM allocations whose POSIX
+    fd the peer duplicates (pidfd_getfd)."""
+    env = dict(os.environ, NCCL_DEBUG="WARN", SRFLOW_ALLOC_VMM="1" if pools == "vmm" else "0")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
            os.path.join(ROOT, "tests", "mp_ps_worker.py")]

@@ -518,6 +518,7 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
   x->napply_descs = nd;
   a.iters = 1;
   x->grid = sm_count_of(device) * std::max(1, per_sm);
+  if (const char *g = getenv("SRFLOW_PS_EXCHANGE_GRID")) x->grid = std::max(1, atoi(g));
   *out = x;
   return SRF_OK;
 }

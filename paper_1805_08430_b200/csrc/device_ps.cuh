@@ -628,7 +628,7 @@ struct ExArgs {
   unsigned int *seq_push, *seq_gen;  // per-descriptor completion counts (this launch)
 };
 
-__global__ void __launch_bounds__(512) k_ps_exchange(const __grid_constant__ ExArgs a) {
+__global__ void __launch_bounds__(512, 3) k_ps_exchange(const __grid_constant__ ExArgs a) {
   __shared__ uint32_t s_i;
   for (;;) {
     if (threadIdx.x == 0) s_i = atomicAdd(a.claim, 1u);

@@ -20,7 +20,9 @@ torch.cuda.set_device(local)
 balanced = os.environ.get("PROBE_PLACEMENT", "round_robin")
 cfg = os.environ.get("PROBE_CFG", "vgg")
 if cfg == "vgg":
-    L = PsLayout(vgg16_shapes(), world, world, colocate=True, placement=balanced)
+    L = PsLayout(vgg16_shapes(), world, world, colocate=True, placement=balanced,
+                 partition_bytes=int(os.environ["PROBE_PARTITION"])
+                 if os.environ.get("PROBE_PARTITION") else None)
 elif cfg == "fcn5":
     L = PsLayout([(int(204.47e6) // 10 // 4,)] * 10, 2, 1, False)
 else:

@@ -411,6 +411,7 @@ struct srf_exchange {
   int ndone = 0, napply_descs = 0;
   int *push_done = nullptr;
   int grid = 0;
+  bool lean = false;  // tiny iteration: the spill-free kernel build
 };
 
 int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch_t gen,
@@ -497,9 +498,12 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
   if (e == cudaSuccess) e = cudaMalloc(&x->push_done, sizeof(int) * std::max(1, a.npush));
   if (e == cudaSuccess) e = cudaMemset(x->push_done, 0xff, sizeof(int) * std::max(1, a.npush));
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  // fewer work units than SMs: a latency-bound iteration (the MLP parity set)
+  x->lean = items.size() < (size_t)sm_count_of(device);
   int per_sm = 0;
   if (e == cudaSuccess)
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ps_exchange, 512, 0);
+    e = x->lean ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ps_exchange<2>, 512, 0)
+                : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ps_exchange<3>, 512, 0);
   if (e != cudaSuccess) {
     cudaFree(x->items);
     cudaFree(x->ctr);
@@ -549,7 +553,10 @@ int srf_ps_exchange_launch_n(srf_exchange_t x, srf_stream_t st, uint64_t iterati
   CUDA_TRY(cudaSetDevice(x->device));
   if (iterations > 1)
     CUDA_TRY(cudaMemsetAsync(x->done, 0, sizeof(unsigned int) * x->ndone, st->s));
-  k_ps_exchange<<<x->grid, 512, 0, st->s>>>(x->args);
+  if (x->lean)
+    k_ps_exchange<2><<<x->grid, 512, 0, st->s>>>(x->args);
+  else
+    k_ps_exchange<3><<<x->grid, 512, 0, st->s>>>(x->args);
   return launch_check("k_ps_exchange");
 }
 

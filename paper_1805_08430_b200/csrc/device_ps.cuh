@@ -628,7 +628,11 @@ struct ExArgs {
   unsigned int *seq_push, *seq_gen;  // per-descriptor completion counts (this launch)
 };
 
-__global__ void __launch_bounds__(512, 3) k_ps_exchange(const __grid_constant__ ExArgs a) {
+// kMinBlocks 3: 40 registers, 3 CTAs per SM - more bytes in flight for
+// bandwidth-bound iterations (FCN-5 N=2 1517 -> 1693 it/s); kMinBlocks 2: the
+// spill-free build (60 registers) for tiny, latency-bound iterations.
+template <int kMinBlocks>
+__global__ void __launch_bounds__(512, kMinBlocks) k_ps_exchange(const __grid_constant__ ExArgs a) {
   __shared__ uint32_t s_i;
   for (;;) {
     if (threadIdx.x == 0) s_i = atomicAdd(a.claim, 1u);

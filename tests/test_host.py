@@ -292,3 +292,14 @@ def test_partitioned_layout_units():
     assert max(load) - min(load) <= max(L.nbytes(u) for u in range(len(L.shapes)))
     # node ids are the model variable's
     assert L.node_ids(big[2], 1) == L.node_ids(big[0], 1)
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    """No CPU fallback: without libsrflow.so every entry point raises."""
+    monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libsrflow.so")
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(ImportError, match="no CPU fallback"):
+        _lib.load()
+    from paper_1805_08430_b200.memspace import MemorySpace
+    with pytest.raises(ImportError):
+        MemorySpace(0, 1 << 20)

@@ -27,12 +27,15 @@ def main() -> int:
     ]
     bad = 0
     for name, shapes, W, P, coloc in layouts:
-        for schedule in ("phases", "exchange"):
+        for schedule in ("phases", "exchange", "exchange_x3"):
             L = PsLayout(shapes, W, P, coloc)
             ps = PsStep(L, rank=rank, world=world, device=local, seed=5, op="sgd", lr=0.02,
-                        schedule=schedule)
-            for it in range(1, 9):
-                ps.step(it)
+                        schedule="phases" if schedule == "phases" else "exchange")
+            if schedule == "exchange_x3":  # 3 iterations per launch: 1-3, 4-6, 7-8
+                ps.run_exchange(1, 8, per_launch=3)
+            else:
+                for it in range(1, 9):
+                    ps.step(it)
             ps.sync()
             torch.distributed.barrier()
             mine = [v for v in range(len(shapes)) if L.shard_of(v) % world == rank]

@@ -422,38 +422,47 @@ class PsStep:
             if not vs:
                 continue
             self._rows["apply"][s] = vs
-            srcsp, srcad, ismeta, peersp, lo, hi, tok = [], [], [], [], [], [], []
-            for v in vs:
-                for w in range(L.workers):
-                    if w == s:
-                        srcsp.append(self.spaces[s].handle.value)
-                        srcad.append(self.addr(s, ("grad", v)))
-                        ismeta.append(0)
-                        peersp.append(self.spaces[s].handle.value)
-                        lo.append(0), hi.append(0), tok.append(0)
-                    else:
-                        srcsp.append(self.spaces[s].handle.value)
-                        srcad.append(self.addr(s, ("mslot", v, w)))
-                        ismeta.append(1)
-                        peersp.append(self.space(w).handle.value)
-                        r = self.regions[w]
-                        lo.append(r.base_addr), hi.append(r.base_addr + r.length)
-                        tok.append(r.access_token)
-            n = len(vs)
-            b = C.c_void_p()
-            ints = C.c_int * n
-            _lib.call("srf_batch_apply_create", self.spaces[s].handle, n,
-                      u64(self.addr(s, ("var", v)) for v in vs), u64(L.nbytes(v) for v in vs),
-                      ints(*[L.workers] * n), ints(*[len(L.shapes[v]) for v in vs]),
-                      (P * len(srcsp))(*srcsp), u64(srcad), (C.c_int * len(ismeta))(*ismeta),
-                      (P * len(peersp))(*peersp), u64(lo), u64(hi), u64(tok), self.op,
-                      self.lr, C.byref(b))
-            if L.is_worker(s):
-                _lib.call("srf_batch_apply_set_ready", b, self.spaces[s].handle,
-                          u64(self.addr(s, ("ready", v)) if w == s else _NONE
-                              for v in vs for w in range(L.workers)))
-            out["apply"][s] = b
+            out["apply"][s] = self._make_apply(s, [(v, list(range(L.workers))) for v in vs])
         return out
+
+    def _make_apply(self, s: int, groups) -> C.c_void_p:
+        """One apply batch on shard s: a descriptor per (variable, workers)
+        group, the workers' gradients applied in the listed (ascending) order."""
+        L = self.L
+        P, u64 = C.c_void_p, _lib.u64_array
+        srcsp, srcad, ismeta, peersp, lo, hi, tok, ready = [], [], [], [], [], [], [], []
+        for v, ws in groups:
+            for w in ws:
+                if w == s:
+                    srcsp.append(self.spaces[s].handle.value)
+                    srcad.append(self.addr(s, ("grad", v)))
+                    ismeta.append(0)
+                    peersp.append(self.spaces[s].handle.value)
+                    lo.append(0), hi.append(0), tok.append(0)
+                    ready.append(self.addr(s, ("ready", v)) if L.is_worker(s) else _NONE)
+                else:
+                    srcsp.append(self.spaces[s].handle.value)
+                    srcad.append(self.addr(s, ("mslot", v, w)))
+                    ismeta.append(1)
+                    peersp.append(self.space(w).handle.value)
+                    r = self.regions[w]
+                    lo.append(r.base_addr), hi.append(r.base_addr + r.length)
+                    tok.append(r.access_token)
+                    ready.append(_NONE)
+        n = len(groups)
+        b = C.c_void_p()
+        ints = C.c_int * n
+        _lib.call("srf_batch_apply_create", self.spaces[s].handle, n,
+                  u64(self.addr(s, ("var", v)) for v, _ws in groups),
+                  u64(L.nbytes(v) for v, _ws in groups),
+                  ints(*[len(ws) for _v, ws in groups]),
+                  ints(*[len(L.shapes[v]) for v, _ws in groups]),
+                  (P * len(srcsp))(*srcsp), u64(srcad), (C.c_int * len(ismeta))(*ismeta),
+                  (P * len(peersp))(*peersp), u64(lo), u64(hi), u64(tok), self.op,
+                  self.lr, C.byref(b))
+        if any(r != _NONE for r in ready):
+            _lib.call("srf_batch_apply_set_ready", b, self.spaces[s].handle, u64(ready))
+        return b
 
     def _put_batch(self, rows, flags):
         if not rows:

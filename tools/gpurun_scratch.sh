@@ -1,7 +1,8 @@
 # scratch command file for one gpurun call (rewritten per experiment)
-timeout 900 python -m pytest tests/test_gpu_ps.py tests/test_gpu_multiprocess.py -x -q > gpurun_out/pw_pytest.log 2>&1; echo rc=$? >> gpurun_out/pw_pytest.log
-TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511"
-for cfg in vgg fcn5 lstm; do
-for m in exchange exchange_pw; do
-PROBE_CFG=$cfg PROBE_MODE=$m timeout 300 $TR tools/ps_phase_probe.py >> gpurun_out/pw_probe.log 2>&1
-done; done
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/r1q_pytest.log 2>&1; echo rc=$? >> gpurun_out/r1q_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" >> gpurun_out/r1q_pytest.log 2>&1
+s=$(date +%s); timeout 1200 python bench.py > gpurun_out/r1q_bench_n1.json 2> gpurun_out/r1q_bench_n1.err; echo "n1 $(( $(date +%s) - s )) s" > gpurun_out/r1q_times.txt
+for n in 2 4; do
+s=$(date +%s); timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus $n > gpurun_out/r1q_bench_n$n.json 2> gpurun_out/r1q_bench_n$n.err; echo "n$n $(( $(date +%s) - s )) s" >> gpurun_out/r1q_times.txt
+done
+timeout 600 python bench.py --impl reference > gpurun_out/r1q_ref_n1.json 2> gpurun_out/r1q_ref_n1.err

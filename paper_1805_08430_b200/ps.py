@@ -668,6 +668,18 @@ class PsStep:
             if b is not None:
                 _lib.load().srf_batch_destroy(b)
         _lib.call("srf_stream_destroy", self.stream)
+        # pools: every rank stops touching its peers' pools before any is freed
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        for sp in self.peers.values():
+            sp.close()
+        if self.world > 1:
+            dist.barrier()
+        if self.stream_space not in self.spaces.values():
+            self.stream_space.close()
+        for sp in self.spaces.values():
+            sp.close()
 
 
 @dataclass

@@ -1325,6 +1325,16 @@ def main() -> int:
                 cpu=False, layout=Lb,
                 label=f"EXTENSION: VGG-16 with byte-balanced shards (largest-first), "
                       f"{world} workers + {world} shards co-located"))
+            # labelled extension: pipelined transfers - the reference placement,
+            # every tensor > 2 MiB cut into 2 MiB slices on its own shard, so a
+            # slice's pull and update overlap the next slice's push
+            Ls = PsLayout(vgg16_shapes(), world, world, colocate=True, slice_bytes=2 << 20)
+            section("ps_sliced", lambda: bench_ps(
+                rank, world, local, max(10, args.steps), args.warmup, op=args.ps_op,
+                cpu=False, layout=Ls,
+                label=f"EXTENSION: VGG-16, reference round-robin placement, tensors > 2 MiB "
+                      f"sent as 2 MiB slices ({len(Ls.shapes)} transfer units), "
+                      f"{world} workers + {world} shards co-located"))
             # labelled extension: partitioned variables (every tensor > 16 MiB cut
             # into one slice per shard), byte-balanced; values bit-identical
             Lp = PsLayout(vgg16_shapes(), world, world, colocate=True, placement="bytes",
@@ -1342,7 +1352,8 @@ def main() -> int:
         print(json.dumps(line), file=JSON_OUT, flush=True)
     ps_ok = line.get("ps", {}).get("verified", True) and all(
         c.get("verified", True) for c in line.get("ps_configs", {}).values()
-        if isinstance(c, dict)) and line.get("ps_balanced", {}).get("verified", True)
+        if isinstance(c, dict)) and all(line.get(k, {}).get("verified", True) for k in
+                                      ("ps_balanced", "ps_sliced", "ps_partitioned"))
     if not dev["verified"] or not e2e["verified"] or not ps_ok:
         log("verification FAILED")
         return 1

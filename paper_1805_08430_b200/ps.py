@@ -84,6 +84,13 @@ class PsLayout:
     #: shard.  Updates are elementwise and gradients are generated per global
     #: element index, so the model's values are bit-identical to unpartitioned.
     partition_bytes: Optional[int] = None
+    #: EXTENSION (pipelined transfers): a unit larger than this many bytes is
+    #: cut into consecutive slices of about this size that all stay on the
+    #: unit's shard (the placement is unchanged), each with its own flag,
+    #: metadata block and apply, so slice j's pull and update overlap slice
+    #: j+1's push instead of waiting for the whole tensor.  Values are
+    #: bit-identical (elementwise update, per-element gradient streams).
+    slice_bytes: Optional[int] = None
     blocks: dict[int, dict] = field(default_factory=dict)
     sizes: dict[int, int] = field(default_factory=dict)
 
@@ -94,7 +101,7 @@ class PsLayout:
         if self.workers > _lib.MAX_WORKERS:
             raise errors.InvalidConfig(f"at most {_lib.MAX_WORKERS} workers")
         # transfer units: (model variable, first element, elements, slice index)
-        self.units = []
+        units = []
         esz = self.elem.size
         for v, dims in enumerate(self.model_shapes):
             n = math.prod(dims)
@@ -103,23 +110,34 @@ class PsLayout:
                 step = -(-n // self.shards)
                 step = (step + 63) // 64 * 64          # 256-B slices
                 for j, off in enumerate(range(0, n, step)):
-                    self.units.append((v, off, min(step, n - off), j))
+                    units.append((v, off, min(step, n - off), j))
             else:
-                self.units.append((v, 0, n, -1))
-        self.shapes = [self.model_shapes[v] if j < 0 else (cnt,)
-                       for v, _off, cnt, j in self.units]
+                units.append((v, 0, n, -1))
         if self.placement == "round_robin":
             # slice j of variable v on shard (v + j) % shards
-            self._shard = [(v + max(j, 0)) % self.shards for v, _o, _c, j in self.units]
+            shard = [(v + max(j, 0)) % self.shards for v, _o, _c, j in units]
         elif self.placement == "bytes":
             load = [0] * self.shards
-            self._shard = [0] * len(self.shapes)
-            for v in sorted(range(len(self.shapes)), key=lambda v: (-self.nbytes(v), v)):
+            shard = [0] * len(units)
+            for u in sorted(range(len(units)), key=lambda u: (-units[u][2], u)):
                 k = min(range(self.shards), key=lambda k: (load[k], k))
-                self._shard[v] = k
-                load[k] += self.nbytes(v)
+                shard[u] = k
+                load[k] += units[u][2] * esz
         else:
             raise errors.InvalidConfig(f"unknown placement {self.placement!r}")
+        # transfer units: (model variable, first element, elements, slice index)
+        self.units, self._shard = [], []
+        for (v, off, n, j), k in zip(units, shard):
+            if self.slice_bytes is not None and n * esz > self.slice_bytes:
+                step = max(64, self.slice_bytes // esz // 64 * 64)   # 256-B multiples
+                for i, o in enumerate(range(off, off + n, step)):
+                    self.units.append((v, o, min(step, off + n - o), max(j, 0) * 1024 + i))
+                    self._shard.append(k)
+            else:
+                self.units.append((v, off, n, j))
+                self._shard.append(k)
+        self.shapes = [self.model_shapes[v] if j < 0 else (cnt,)
+                       for v, _off, cnt, j in self.units]
         for s in range(self.nservers):
             self._lay_out(s)
 

@@ -24,11 +24,14 @@ def main() -> int:
         ("ps+workers", mlp_shapes() + [(4096,)], 2, 1, False),
         # MiB-sized, unequal variables
         ("coloc-big", [(1 << 19,), (300_001,), (7,), (1 << 20,)], world, world, True),
+        # EXTENSION: pipelined transfers (256 KiB slices on the reference shard)
+        ("coloc-sliced", [(1 << 19,), (300_001,), (7,), (1 << 20,)], world, world, True,
+         {"slice_bytes": 256 << 10}),
     ]
     bad = 0
-    for name, shapes, W, P, coloc in layouts:
+    for name, shapes, W, P, coloc, *kw in layouts:
         for schedule in ("phases", "exchange", "exchange_x3"):
-            L = PsLayout(shapes, W, P, coloc)
+            L = PsLayout(shapes, W, P, coloc, **(kw[0] if kw else {}))
             ps = PsStep(L, rank=rank, world=world, device=local, seed=5, op="sgd", lr=0.02,
                         schedule="phases" if schedule == "phases" else "exchange")
             if schedule == "exchange_x3":  # 3 iterations per launch: 1-3, 4-6, 7-8
@@ -38,12 +41,14 @@ def main() -> int:
                     ps.step(it)
             ps.sync()
             torch.distributed.barrier()
-            mine = [v for v in range(len(shapes)) if L.shard_of(v) % world == rank]
+            # transfer units this rank owns, each against its slice of the model
+            mine = [u for u in range(len(L.shapes)) if L.shard_of(u) % world == rank]
             want = port.ps_expected_device(shapes, W, 5, range(1, 9), op="sgd", lr=0.02,
-                                           only=mine)
-            for v in mine:
-                if ps.variable(v).tobytes() != want[v].tobytes():
-                    print(f"rank {rank}: {name}/{schedule} variable {v} differs", flush=True)
+                                           only=sorted({L.parent(u)[0] for u in mine}))
+            for u in mine:
+                v, off, n = L.parent(u)
+                if ps.variable(u).tobytes() != want[v].reshape(-1)[off:off + n].tobytes():
+                    print(f"rank {rank}: {name}/{schedule} unit {u} differs", flush=True)
                     bad += 1
             ps.close()
             torch.distributed.barrier()

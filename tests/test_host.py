@@ -294,6 +294,36 @@ def test_partitioned_layout_units():
     assert L.node_ids(big[2], 1) == L.node_ids(big[0], 1)
 
 
+def test_sliced_layout_units_stay_on_their_shard():
+    """EXTENSION (pipelined transfers): big units are cut into consecutive
+    ~slice_bytes slices; the reference placement is unchanged."""
+    from paper_1805_08430_b200.ps import PsLayout
+    from paper_1805_08430_b200.workloads import vgg16_shapes
+    shapes = vgg16_shapes()
+    ref = PsLayout(shapes, 4, 4, colocate=True)
+    L = PsLayout(shapes, 4, 4, colocate=True, slice_bytes=8 << 20)
+    assert len(L.shapes) > len(ref.shapes)
+    for v, dims in enumerate(shapes):
+        us = [u for u in range(len(L.shapes)) if L.parent(u)[0] == v]
+        parts = [(L.parent(u)[1], L.parent(u)[2]) for u in us]
+        assert parts[0][0] == 0 and sum(c for _o, c in parts) == int(np.prod(dims))
+        for (o1, c1), (o2, _c2) in zip(parts, parts[1:]):
+            assert o1 + c1 == o2 and (o2 * 4) % 256 == 0
+        assert {L.shard_of(u) for u in us} == {ref.shard_of(v)}   # placement kept
+        assert all(L.nbytes(u) <= 8 << 20 for u in us)
+        if len(us) == 1:
+            assert L.shapes[us[0]] == tuple(dims)                 # small tensors untouched
+    # slices of a partitioned variable stay on their partition's shard
+    P = PsLayout(shapes, 4, 4, colocate=True, placement="bytes", partition_bytes=16 << 20)
+    PS = PsLayout(shapes, 4, 4, colocate=True, placement="bytes", partition_bytes=16 << 20,
+                  slice_bytes=8 << 20)
+    for u in range(len(PS.shapes)):
+        v, off, _n = PS.parent(u)
+        owner = next(p for p in range(len(P.shapes)) if P.parent(p)[0] == v
+                     and P.parent(p)[1] <= off < P.parent(p)[1] + P.parent(p)[2])
+        assert PS.shard_of(u) == P.shard_of(owner)
+
+
 def test_missing_library_fails_loudly(monkeypatch):
     """No CPU fallback: without libsrflow.so every entry point raises."""
     monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libsrflow.so")

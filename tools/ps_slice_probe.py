@@ -1,0 +1,29 @@
+"""PS VGG-16 it/s at N>1 (torchrun) with the reference round-robin placement,
+unsliced vs pipelined transfers (PsLayout.slice_bytes), through bench_ps
+(schedule autotune, device events, max over ranks).  PROBE_SLICES: comma list
+of slice sizes in MiB (0 = unsliced)."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import bench
+from paper_1805_08430_b200.distributed import init_process_group
+from paper_1805_08430_b200.ps import PsLayout
+from paper_1805_08430_b200.workloads import vgg16_shapes
+
+rank, world, local = init_process_group("nccl")
+torch.cuda.set_device(local)
+for mib in [int(x) for x in os.environ.get("PROBE_SLICES", "0,64,16,4").split(",")]:
+    kw = {"slice_bytes": mib << 20} if mib else {}
+    if os.environ.get("PROBE_PARTITION"):
+        kw.update(placement="bytes", partition_bytes=int(os.environ["PROBE_PARTITION"]) << 20)
+    L = PsLayout(vgg16_shapes(), world, world, colocate=True, **kw)
+    r = bench.bench_ps(rank, world, local, 10, 3, op="sgd", cpu=False, layout=L,
+                       label=f"slice {mib} MiB")
+    if rank == 0:
+        print(json.dumps({"world": world, "slice_mib": mib, "units": len(L.shapes),
+                          **{k: r.get(k) for k in ("steps_per_s", "schedule", "verified", "roofline",
+                                                    "autotune_ms_per_5")}}), flush=True)

@@ -297,6 +297,13 @@ int srf_batch_gen_set_meta(srf_batch_t gen, int n, const int *gen_index, srf_bat
 int srf_batch_gen_set_ready(srf_batch_t gen, srf_space_t const *space,
                             const uint64_t *ready_addr);
 int srf_batch_apply_set_ready(srf_batch_t apply, srf_space_t space, const uint64_t *ready_addr);
+/* static gradient pushes (the reference's mechanism_override="static",
+ * runtime/session.py:368): put edge i first waits until the byte at
+ * ready_addr[i] of space[i] (same GPU) reads 1 - its gen released the
+ * gradient - and clears it to 0 once the body is copied, the gen's credit.
+ * UINT64_MAX = none. */
+int srf_batch_put_set_src_ready(srf_batch_t put, srf_space_t const *space,
+                                const uint64_t *ready_addr);
 /* partitioned variables (extension): gen edge i produces elements
  * elem_offset[i] ... of its model variable's gradient stream */
 int srf_batch_gen_set_offsets(srf_batch_t gen, const uint64_t *elem_offset);

@@ -122,6 +122,7 @@ SIGNATURES = {
     "srf_batch_gen_set_offsets": (C.c_int, [vp, P(u64)]),
     "srf_batch_gen_set_ready": (C.c_int, [vp, P(vp), P(u64)]),
     "srf_batch_apply_set_ready": (C.c_int, [vp, vp, P(u64)]),
+    "srf_batch_put_set_src_ready": (C.c_int, [vp, P(vp), P(u64)]),
     "srf_ps_exchange_create": (C.c_int, [vp, P(u64), vp, P(u64), P(vp), C.c_int, P(u64),
                                          P(vp)]),
     "srf_ps_exchange_launch": (C.c_int, [vp, vp, u64, C.c_int]),

@@ -97,6 +97,7 @@ int srf_batch_put_create(int n, srf_space_t const *src_space, const uint64_t *sr
     d.cta_count = ctas_for(device, body_len[i], 128 << 10);
     d.wait_empty = (flags & SRF_PUT_WAIT_EMPTY) ? 1 : 0;
     d.pad = 0;
+    d.src_ready = nullptr;
     next += d.cta_count;
   }
   int rc0 = finish_batch(0, device, host, src_space[0]->err, out);
@@ -328,6 +329,27 @@ int srf_batch_gen_set_ready(srf_batch_t gen, srf_space_t const *space,
   }
   CUDA_TRY(cudaSetDevice(gen->device));
   CUDA_TRY(cudaMemcpy(gen->descs, gen->host.data(), gen->host.size(), cudaMemcpyHostToDevice));
+  return SRF_OK;
+}
+
+int srf_batch_put_set_src_ready(srf_batch_t put, srf_space_t const *space,
+                                const uint64_t *ready_addr) {
+  DeviceGuard device_guard;
+  if (!put || put->kind != 0) return fail(SRF_E_INVALID_CONFIG, "not a put batch");
+  BatchPut *d = (BatchPut *)put->host.data();
+  for (int i = 0; i < put->n; ++i) {
+    if (ready_addr[i] == UINT64_MAX) {
+      d[i].src_ready = nullptr;
+      continue;
+    }
+    if (space[i]->device != put->device)
+      return fail(SRF_E_INVALID_CONFIG, "source-ready byte of edge %d on another GPU", i);
+    int rc = check_raw(space[i], ready_addr[i], 1, "source-ready flag");
+    if (rc) return rc;
+    d[i].src_ready = space[i]->base + ready_addr[i];
+  }
+  CUDA_TRY(cudaSetDevice(put->device));
+  CUDA_TRY(cudaMemcpy(put->descs, put->host.data(), put->host.size(), cudaMemcpyHostToDevice));
   return SRF_OK;
 }
 

@@ -158,6 +158,10 @@ struct BatchPut {        // K1/K3 over many edges
   const uint8_t *tail;   // tail byte source (flag cell / meta flag)
   uint32_t cta_begin, cta_count;
   uint32_t wait_empty, pad;
+  // source produced in-device (a static gradient push): wait until the
+  // producer released it to 1, clear it to 0 once copied (the producer's
+  // credit).  nullptr: none.
+  uint8_t *src_ready;
 };
 
 struct BatchGen {        // worker: consume weight, (re)produce gradient
@@ -268,8 +272,11 @@ __device__ __forceinline__ void put_unit(const BatchPut *descs, int n, uint32_t 
     __syncthreads();
     const BatchPut d = descs[s_desc];
     const uint32_t lb = u - d.cta_begin;
-    if (d.wait_empty) {
-      if (threadIdx.x == 0 && !spin_until(d.dst + d.body, 0, timeout_ns, sys)) atomicExch(err, 2);
+    if (d.wait_empty || d.src_ready) {
+      if (threadIdx.x == 0) {
+        if (d.wait_empty && !spin_until(d.dst + d.body, 0, timeout_ns, sys)) atomicExch(err, 2);
+        if (d.src_ready && !spin_until(d.src_ready, 1, timeout_ns, sys)) atomicExch(err, 3);
+      }
       __syncthreads();
     }
     // (PS blocks are 256-B aligned: always co-aligned, no destination realignment)
@@ -283,6 +290,7 @@ __device__ __forceinline__ void put_unit(const BatchPut *descs, int n, uint32_t 
       // flag (and, downstream, the next use of this edge) sees it at zero
       atomicExch(&counters[s_desc], 0u);
       release_tail(d.dst + d.body, *d.tail, sys);
+      if (d.src_ready) release_tail(d.src_ready, 0, sys);  // source copied: credit
       if (seq) count_done(seq + s_desc);
     }
     __syncthreads();  // shared state is reused by the next unit

@@ -91,6 +91,12 @@ class PsLayout:
     #: j+1's push instead of waiting for the whole tensor.  Values are
     #: bit-identical (elementwise update, per-element gradient streams).
     slice_bytes: Optional[int] = None
+    #: gradient edges' transfer mechanism: "dynamic" is what the reference's
+    #: analyzer picks (metadata block + one-sided pull, analyzer.py); "static"
+    #: is its ``mechanism_override="static"`` (runtime/session.py:368): the
+    #: worker puts the gradient + flag into a preallocated receive region on
+    #: the shard (K1), and the apply reads it there.  Same values either way.
+    grad_mechanism: str = "dynamic"
     blocks: dict[int, dict] = field(default_factory=dict)
     sizes: dict[int, int] = field(default_factory=dict)
 
@@ -100,6 +106,8 @@ class PsLayout:
             raise errors.InvalidConfig("colocate needs shards <= workers")
         if self.workers > _lib.MAX_WORKERS:
             raise errors.InvalidConfig(f"at most {_lib.MAX_WORKERS} workers")
+        if self.grad_mechanism not in ("dynamic", "static"):
+            raise errors.InvalidConfig(f"unknown gradient mechanism {self.grad_mechanism!r}")
         # transfer units: (model variable, first element, elements, slice index)
         units = []
         esz = self.elem.size
@@ -179,19 +187,31 @@ class PsLayout:
                 take(("var", v), self.nbytes(v))
                 if self.is_worker(s):  # co-located: the in-place gradient's ready byte
                     take(("ready", v), 1)
+        static = self.grad_mechanism == "static"
         if self.is_worker(s):
             for v in range(len(self.shapes)):
                 take(("grad", v), self.nbytes(v))
                 if self.shard_of(v) != s:
                     take(("wbuf", v), self.nbytes(v) + 1)
-                    take(("mstage", v), meta_block_size(len(self.shapes[v])))
+                    if static:   # gradient complete / copied out (gen <-> push)
+                        take(("ready", v), 1)
+                    else:
+                        take(("mstage", v), meta_block_size(len(self.shapes[v])))
         for v in range(len(self.shapes)):
             if self.shard_of(v) == s:
                 for w in range(self.workers):
                     if w != s:
-                        take(("mslot", v, w), meta_block_size(len(self.shapes[v])))
+                        if static:   # the static gradient receive region (payload || flag)
+                            take(("grecv", v, w), self.nbytes(v) + 1)
+                        else:
+                            take(("mslot", v, w), meta_block_size(len(self.shapes[v])))
         self.blocks[s] = b
         self.sizes[s] = off
+
+    def grad_signal_bytes(self, v: int) -> int:
+        """Bytes besides the payload a gradient edge moves: the metadata block
+        (dynamic) or the tail flag (static)."""
+        return 1 if self.grad_mechanism == "static" else meta_block_size(len(self.shapes[v]))
 
     def traffic(self, s: int) -> dict:
         """Algorithmic bytes per iteration at server s.
@@ -205,7 +225,7 @@ class PsLayout:
                "hbm": 0}
         for v in range(len(self.shapes)):
             S = self.nbytes(v)
-            meta = meta_block_size(len(self.shapes[v]))
+            meta = self.grad_signal_bytes(v)
             sh = self.shard_of(v)
             if sh == s:
                 remote = [w for w in range(self.workers) if w != s]
@@ -229,7 +249,7 @@ def link_traffic(L: "PsLayout", world: int) -> dict[int, dict]:
     out = {g: {"link_out": 0, "link_in": 0} for g in range(world)}
     for v in range(len(L.shapes)):
         S = L.nbytes(v)
-        meta = meta_block_size(len(L.shapes[v]))
+        meta = L.grad_signal_bytes(v)
         s = L.shard_of(v)
         for w in range(L.workers):
             if w == s or w % world == s % world:
@@ -254,6 +274,7 @@ class PsStep:
         self.seed = seed
         self.op = {"xor": _lib.APPLY_XOR, "sgd": _lib.APPLY_SGD}[op]
         self.lr = float(lr)
+        self.static_grads = layout.grad_mechanism == "static"
         self.local = [s for s in range(layout.nservers) if s % world == rank]
         self.spaces: dict[int, MemorySpace] = {}
         self.regions = {}
@@ -294,6 +315,7 @@ class PsStep:
         _lib.call("srf_stream_create", self.stream_space.handle, C.byref(self.stream))
         # device iteration counter for graph-replayed steps
         self._counter = self.stream_space.allocate_region(64)
+        self._exchange_push = None
         self.batches = self._build_batches()
         for g in self.batches["gen"].values():
             _lib.call("srf_batch_set_iteration_source", g, self.stream_space.handle,
@@ -317,7 +339,7 @@ class PsStep:
         v = key[1]
         if kind in ("var", "grad"):
             return self.L.nbytes(v)
-        if kind == "wbuf":
+        if kind in ("wbuf", "grecv"):
             return self.L.nbytes(v) + 1
         return meta_block_size(len(self.L.shapes[v]))
 
@@ -340,12 +362,17 @@ class PsStep:
                 if L.shard_of(v) == s:
                     sp.write_raw(self.addr(s, ("var", v)), self._model_slice(v, 0, 0))
                     for w in range(L.workers):
-                        if w != s:
+                        if w != s and self.static_grads:
+                            sp.write_raw(self.addr(s, ("grecv", v, w)) + L.nbytes(v), b"\x00")
+                        elif w != s:
                             mk = ("mslot", v, w)
                             sp.write_raw(self.addr(s, mk) + meta_block_size(len(L.shapes[v])) - 1,
                                          b"\x00")
                 if L.is_worker(s) and L.shard_of(v) != s:
                     sp.write_raw(self.addr(s, ("wbuf", v)) + L.nbytes(v), b"\x00")
+                    if self.static_grads:
+                        sp.write_raw(self.addr(s, ("ready", v)), b"\x00")
+                        continue
                     meta = encode_meta(L.shapes[v], L.elem, self.addr(s, ("grad", v)), self.token(s))
                     sp.write_raw(self.addr(s, ("mstage", v)), meta)
             sp.sync()
@@ -394,8 +421,10 @@ class PsStep:
                 mlen = meta_block_size(len(L.shapes[v]))
                 g_rows.append((self.addr(w, ("grad", v)), L.nbytes(v),
                                self.addr(w, ("wbuf", v)) + L.nbytes(v) if remote else _NONE,
-                               self.space(sh).handle.value if remote else None,
-                               self.addr(sh, ("mslot", v, w)) + mlen - 1 if remote else _NONE,
+                               self.space(sh).handle.value if remote and not self.static_grads
+                               else None,
+                               self.addr(sh, ("mslot", v, w)) + mlen - 1
+                               if remote and not self.static_grads else _NONE,
                                L.node_ids(v, w)[1], w))
                 self._rows["gen"].append((w, v))
         out["gen"] = {}
@@ -408,8 +437,8 @@ class PsStep:
                       u64(r[2] for r in g_rows), (P * n)(*[r[3] for r in g_rows]),
                       u64(r[4] for r in g_rows), u64(r[5] for r in g_rows), self.seed,
                       C.byref(b))
-            ready = [self.addr(w, ("ready", v)) if L.shard_of(v) == w else _NONE
-                     for w, v in self._rows["gen"]]
+            ready = [self.addr(w, ("ready", v)) if L.shard_of(v) == w or self.static_grads
+                     else _NONE for w, v in self._rows["gen"]]
             if any(r != _NONE for r in ready):
                 _lib.call("srf_batch_gen_set_ready", b,
                           (P * n)(*[self.spaces[w].handle.value for w, _v in self._rows["gen"]]),
@@ -418,8 +447,10 @@ class PsStep:
             if any(offs):  # partitioned variables: slices keep global element indices
                 _lib.call("srf_batch_gen_set_offsets", b, u64(offs))
             out["gen"]["all"] = b
-        # 3. metadata writes (K3)
+        self._push_rows = rows_push = rows
+        # 3. metadata writes (K3), or the static gradient pushes (K1)
         rows = []
+        self._rows["gpush"] = []
         for w in self.local:
             if not L.is_worker(w):
                 continue
@@ -427,12 +458,27 @@ class PsStep:
                 sh = L.shard_of(v)
                 if sh == w:
                     continue
+                if self.static_grads:
+                    rows.append((w, self.addr(w, ("grad", v)), L.nbytes(v), self.token(w),
+                                 self.addr(w, "flag"), sh, self.addr(sh, ("grecv", v, w)),
+                                 self.token(sh)))
+                    self._rows["gpush"].append((w, v))
+                    continue
                 mlen = meta_block_size(len(L.shapes[v]))
                 rows.append((w, self.addr(w, ("mstage", v)), mlen - 1, self.token(w),
                              self.addr(w, ("mstage", v)) + mlen - 1, sh,
                              self.addr(sh, ("mslot", v, w)), self.token(sh)))
                 self._rows["meta"].append((w, v))
-        out["meta"] = self._put_batch(rows, 0)
+        out["gpush"] = None
+        self._gpush_rows = rows
+        if self.static_grads:
+            out["meta"] = None
+            out["gpush"] = self._put_batch(rows, _lib.PUT_WAIT_EMPTY)
+            if rows:
+                self._set_src_ready(out["gpush"], self._rows["gpush"])
+        else:
+            out["meta"] = self._put_batch(rows, 0)
+        del rows_push
         # 4. fused pull + apply per shard
         out["apply"] = {}
         for s in self.local:
@@ -458,6 +504,15 @@ class PsStep:
                     peersp.append(self.spaces[s].handle.value)
                     lo.append(0), hi.append(0), tok.append(0)
                     ready.append(self.addr(s, ("ready", v)) if L.is_worker(s) else _NONE)
+                elif self.static_grads:
+                    # StaticReceiver: the gradient landed in s's receive region;
+                    # its tail flag is the apply's ready byte (cleared = credit)
+                    srcsp.append(self.spaces[s].handle.value)
+                    srcad.append(self.addr(s, ("grecv", v, w)))
+                    ismeta.append(0)
+                    peersp.append(self.spaces[s].handle.value)
+                    lo.append(0), hi.append(0), tok.append(0)
+                    ready.append(self.addr(s, ("grecv", v, w)) + L.nbytes(v))
                 else:
                     srcsp.append(self.spaces[s].handle.value)
                     srcad.append(self.addr(s, ("mslot", v, w)))
@@ -481,6 +536,17 @@ class PsStep:
         if any(r != _NONE for r in ready):
             _lib.call("srf_batch_apply_set_ready", b, self.spaces[s].handle, u64(ready))
         return b
+
+    def _set_src_ready(self, batch, wv) -> None:
+        """Put edge i waits for its gradient's ready byte (wv[i] = (worker,
+        variable); None: no source gate)."""
+        P = C.c_void_p
+        anyw = next(x for x in wv if x is not None)[0]
+        _lib.call("srf_batch_put_set_src_ready", batch,
+                  (P * len(wv))(*[self.spaces[anyw if x is None else x[0]].handle.value
+                                  for x in wv]),
+                  _lib.u64_array(_NONE if x is None else self.addr(x[0], ("ready", x[1]))
+                                 for x in wv))
 
     def _put_batch(self, rows, flags):
         if not rows:
@@ -532,24 +598,38 @@ class PsStep:
             gi = (C.c_int * len(rows["meta"]))(*[index[wv] for wv in rows["meta"]])
             _lib.call("srf_batch_gen_set_meta", gen, len(rows["meta"]), gi, b["meta"])
         applies = list(b["apply"].items())
+        push, push_vars = b["push"], list(rows["push"])
+        push_keys = [4 * pos[v] for v in rows["push"]]
+        apply_slot = 2
+        if self.static_grads and self._gpush_rows:
+            # static gradients: the weight pushes and the gradient pushes (after
+            # their gen, before their apply) share the exchange's one put batch
+            push = self._exchange_push = self._put_batch(self._push_rows + self._gpush_rows,
+                                                         _lib.PUT_WAIT_EMPTY)
+            self._set_src_ready(push, [None] * len(self._push_rows) + rows["gpush"])
+            push_keys += [4 * pos[v] + 2 for _w, v in rows["gpush"]]
+            push_vars += [None] * len(rows["gpush"])
+            apply_slot = 3
         x = C.c_void_p()
         _lib.call("srf_ps_exchange_create",
-                  b["push"], u64(4 * pos[v] for v in rows["push"]) if rows["push"] else None,
+                  push, u64(push_keys) if push_keys else None,
                   gen, u64(4 * pos[v] + 1 for _w, v in rows["gen"]) if rows["gen"] else None,
                   (C.c_void_p * max(1, len(applies)))(*[a.value for _s, a in applies]),
                   len(applies),
-                  u64(4 * (pos[v] + lag) + 2 for s, _a in applies for v in rows["apply"][s])
+                  u64(4 * (pos[v] + lag) + apply_slot for s, _a in applies
+                      for v in rows["apply"][s])
                   if applies else None,
                   C.byref(x))
-        if rows["push"]:
-            # push edge -> its variable's apply descriptor (global order over the
-            # apply batches), for launches of several iterations
+        if push_vars:
+            # weight push edge -> its variable's apply descriptor (global order
+            # over the apply batches), for launches of several iterations
             index, base = {}, 0
             for s_, _a in applies:
                 for i, v in enumerate(rows["apply"][s_]):
                     index[v] = base + i
                 base += len(rows["apply"][s_])
-            link = (C.c_int * len(rows["push"]))(*[index.get(v, -1) for v in rows["push"]])
+            link = (C.c_int * len(push_vars))(*[-1 if v is None else index.get(v, -1)
+                                                for v in push_vars])
             _lib.call("srf_ps_exchange_link", x, link)
         return x
 
@@ -568,9 +648,10 @@ class PsStep:
         for g in b["gen"].values():
             _lib.call("srf_batch_launch", g, self.stream, iteration, mode, 0)
             n += 1
-        if b["meta"] is not None:
-            _lib.call("srf_batch_launch", b["meta"], self.stream, iteration, 0, 0)
-            n += 1
+        for m in (b["meta"], b["gpush"]):
+            if m is not None:
+                _lib.call("srf_batch_launch", m, self.stream, iteration, 0, 0)
+                n += 1
         for a in b["apply"].values():
             _lib.call("srf_batch_launch", a, self.stream, iteration, 0, 0)
             n += 1
@@ -581,7 +662,7 @@ class PsStep:
             return 1
         b = self.batches
         return ((b["push"] is not None) + len(b["gen"]) + (b["meta"] is not None)
-                + len(b["apply"]))
+                + (b["gpush"] is not None) + len(b["apply"]))
 
     def capture(self, steps: int, regen: bool = True):
         """A CUDA graph of ``steps`` iterations on self.stream; the gen batch
@@ -598,8 +679,9 @@ class PsStep:
                 _lib.call("srf_batch_launch", b["push"], self.stream, none, 0, 0)
             for g in b["gen"].values():
                 _lib.call("srf_batch_launch", g, self.stream, none, 1 if regen else 0, 0)
-            if b["meta"] is not None:
-                _lib.call("srf_batch_launch", b["meta"], self.stream, none, 0, 0)
+            for m in (b["meta"], b["gpush"]):
+                if m is not None:
+                    _lib.call("srf_batch_launch", m, self.stream, none, 0, 0)
             for a in b["apply"].values():
                 _lib.call("srf_batch_launch", a, self.stream, none, 0, 0)
             _lib.call("srf_counter_add", self.stream_space.handle, self._counter.base_addr, 1,
@@ -634,7 +716,8 @@ class PsStep:
         b = self.batches
         applies = list(b["apply"].values())
         gen = next(iter(b["gen"].values()), None)
-        _lib.call("srf_ps_persistent", b["push"], gen, b["meta"],
+        _lib.call("srf_ps_persistent", b["push"], gen,
+                  b["meta"] if b["meta"] is not None else b["gpush"],
                   (C.c_void_p * max(1, len(applies)))(*[a.value for a in applies]),
                   len(applies), self.stream, first_iteration, iterations,
                   1 if regen else 0)
@@ -681,7 +764,8 @@ class PsStep:
         if self._exchange_built is not None:
             _lib.call("srf_ps_exchange_destroy", self._exchange_built)
             self._exchange = self._exchange_built = None
-        for b in [self.batches["push"], self.batches["meta"], *self.batches["gen"].values(),
+        for b in [self.batches["push"], self.batches["meta"], self.batches["gpush"],
+                  self._exchange_push, *self.batches["gen"].values(),
                   *self.batches["apply"].values()]:
             if b is not None:
                 _lib.load().srf_batch_destroy(b)

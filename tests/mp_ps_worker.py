@@ -27,6 +27,11 @@ def main() -> int:
         # EXTENSION: pipelined transfers (256 KiB slices on the reference shard)
         ("coloc-sliced", [(1 << 19,), (300_001,), (7,), (1 << 20,)], world, world, True,
          {"slice_bytes": 256 << 10}),
+        # the reference's mechanism_override="static" for the gradient edges
+        ("coloc-static", [(1 << 19,), (300_001,), (7,), (1 << 20,)], world, world, True,
+         {"grad_mechanism": "static"}),
+        ("ps+workers-static", mlp_shapes() + [(4096,)], 2, 1, False,
+         {"grad_mechanism": "static", "slice_bytes": 4096}),
     ]
     bad = 0
     for name, shapes, W, P, coloc, *kw in layouts:

@@ -66,7 +66,7 @@ def _worker(rank: int, world: int, port: int, errq):
         digests = []
         for kw in ({}, {"placement": "bytes"},
                    {"placement": "bytes", "partition_bytes": 16 << 20},
-                   {"slice_bytes": 8 << 20}):
+                   {"slice_bytes": 8 << 20}, {"grad_mechanism": "static"}):
             Lx = PsLayout(vgg16_shapes(), world, world, colocate=True, **kw)
             blob = json.dumps([[sorted((str(k), o) for k, o in Lx.blocks[s].items())
                                 for s in range(Lx.nservers)], Lx.units, Lx.sizes],

@@ -285,3 +285,59 @@ def test_multi_iteration_exchange_matches_oracle(shapes, W, P, coloc, per_launch
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes(), v
     ps.close()
+
+
+@pytest.mark.parametrize("shapes,W,P,coloc", CASES + [([(1 << 20,), (7,)], 2, 2, True)])
+@pytest.mark.parametrize("schedule", ["phases", "exchange", "exchange_x3", "persistent",
+                                      "mixed"])
+def test_static_gradients_match_oracle(shapes, W, P, coloc, schedule):
+    """Gradient edges forced STATIC (the reference's mechanism_override="static",
+    runtime/session.py:368): workers put gradient || flag into the shard's
+    receive regions; same values as the dynamic path under every schedule."""
+    L = PsLayout(shapes, W, P, coloc, grad_mechanism="static")
+    assert not any(k[0] in ("mslot", "mstage") for b in L.blocks.values() for k in b
+                   if isinstance(k, tuple))
+    ps = PsStep(L, seed=21, op="sgd", lr=0.02,
+                schedule="exchange" if schedule == "exchange" else "phases")
+    if schedule == "exchange_x3":
+        ps.run_exchange(1, 8, per_launch=3)
+    elif schedule == "persistent":
+        ps.step(1)
+        ps.run_persistent(2, 6)
+        ps.step(8)
+    else:
+        for it in range(1, 9):
+            if schedule == "mixed":
+                ps.use_schedule("exchange" if it % 2 else "phases")
+            ps.step(it)
+    ps.sync()
+    want = port.ps_expected_device(shapes, W, 21, range(1, 9), op="sgd", lr=0.02)
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes(), (v, schedule)
+    ps.close()
+    if schedule == "phases":  # parity mode: reference PCG64 gradients uploaded, XOR
+        ps = PsStep(L, seed=3, op="xor")
+        for it in (1, 2, 3):
+            ps.upload_gradients(it)
+            ps.step(it, regen=False)
+            ps.sync()
+        want = port.ps_expected(shapes, W, 3, 3, op="xor")
+        for v in range(len(shapes)):
+            assert ps.variable(v).tobytes() == want[v].tobytes()
+        ps.close()
+
+
+def test_static_sliced_gradients_equal_the_model():
+    shapes, W, P = [(3000,), (17,), (64, 70), (5,)], 3, 3
+    L = PsLayout(shapes, W, P, True, slice_bytes=2048, grad_mechanism="static")
+    ps = PsStep(L, seed=9, op="sgd", lr=0.02, schedule="exchange")
+    ps.run_exchange(1, 6, per_launch=4)
+    ps.sync()
+    want = port.ps_expected_device(shapes, W, 9, range(1, 7), op="sgd", lr=0.02)
+    got = [np.zeros(int(np.prod(s)), np.float32) for s in shapes]
+    for u in range(len(L.shapes)):
+        v, off, n = L.parent(u)
+        got[v][off:off + n] = ps.variable(u).reshape(-1)
+    for v in range(len(shapes)):
+        assert got[v].tobytes() == want[v].reshape(-1).tobytes(), v
+    ps.close()

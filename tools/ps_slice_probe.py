@@ -1,7 +1,8 @@
 """PS VGG-16 it/s at N>1 (torchrun) with the reference round-robin placement,
 unsliced vs pipelined transfers (PsLayout.slice_bytes), through bench_ps
 (schedule autotune, device events, max over ranks).  PROBE_SLICES: comma list
-of slice sizes in MiB (0 = unsliced)."""
+of slice sizes in MiB (0 = unsliced); PROBE_GRAD: gradient mechanism
+(dynamic | static); PROBE_PARTITION: partition_bytes in MiB."""
 import json
 import os
 import sys
@@ -18,12 +19,13 @@ rank, world, local = init_process_group("nccl")
 torch.cuda.set_device(local)
 for mib in [int(x) for x in os.environ.get("PROBE_SLICES", "0,64,16,4").split(",")]:
     kw = {"slice_bytes": mib << 20} if mib else {}
+    kw["grad_mechanism"] = os.environ.get("PROBE_GRAD", "dynamic")
     if os.environ.get("PROBE_PARTITION"):
         kw.update(placement="bytes", partition_bytes=int(os.environ["PROBE_PARTITION"]) << 20)
     L = PsLayout(vgg16_shapes(), world, world, colocate=True, **kw)
     r = bench.bench_ps(rank, world, local, 10, 3, op="sgd", cpu=False, layout=L,
                        label=f"slice {mib} MiB")
     if rank == 0:
-        print(json.dumps({"world": world, "slice_mib": mib, "units": len(L.shapes),
+        print(json.dumps({"world": world, "slice_mib": mib, "grad": kw["grad_mechanism"], "units": len(L.shapes),
                           **{k: r.get(k) for k in ("steps_per_s", "schedule", "verified", "roofline",
                                                     "autotune_ms_per_5")}}), flush=True)

@@ -1,5 +1,4 @@
 mkdir -p gpurun_out
 for n in 2 4; do
-PROBE_GRAD=static PROBE_SLICES=0,4,2,1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29531 tools/ps_slice_probe.py 2>gpurun_out/slice_err_$n.log | grep '^{' >> gpurun_out/slice_probe3.jsonl
-PROBE_GRAD=static PROBE_PARTITION=16 PROBE_SLICES=0,4 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29531 tools/ps_slice_probe.py 2>>gpurun_out/slice_err_$n.log | grep '^{' | sed 's/^{/{"partition": 16, /' >> gpurun_out/slice_probe3.jsonl
+timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2954$n bench.py --gpus $n > gpurun_out/r1s_bench_n$n.json 2>gpurun_out/r1s_bench_n$n.err; echo bench $n rc=$?
 done

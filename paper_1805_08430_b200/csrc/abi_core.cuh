@@ -878,7 +878,7 @@ int srf_dyn_recv(srf_space_t rcv, uint64_t meta_addr, int rank, srf_space_t peer
   int grid, block;
   copy_geometry(s->device, std::max<uint64_t>(dst_cap, 1), &grid, &block);
   CUDA_TRY(cudaSetDevice(s->device));
-  k_dyn_recv<<<grid, 256, 0, s->s>>>(a);
+  k_dyn_recv<<<grid, block, 0, s->s>>>(a);
   return launch_check("k_dyn_recv");
 }
 

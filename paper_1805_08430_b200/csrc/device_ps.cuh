@@ -524,7 +524,7 @@ struct DynRecvArgs {
   int sys;
 };
 
-__global__ void __launch_bounds__(256) k_dyn_recv(const __grid_constant__ DynRecvArgs a) {
+__global__ void __launch_bounds__(512) k_dyn_recv(const __grid_constant__ DynRecvArgs a) {
   __shared__ const uint8_t *s_src;
   __shared__ uint64_t s_len;
   __shared__ int s_ok, s_last;

@@ -6,8 +6,9 @@
 // ---------------------------------------------------------------------------
 static void copy_geometry(int device, uint64_t bytes, int *grid, int *block) {
   const int threads = g_copy_threads;
-  // one CTA moves threads * 16 B * 4 per unrolled batch; cap at k CTAs/SM
-  uint64_t per_cta = (uint64_t)threads * 16 * 4;
+  // one CTA per 16 KiB (small puts spread over many SMs: latency), capped at
+  // k CTAs/SM (large puts: fewer CTAs polling the credit and arriving)
+  const uint64_t per_cta = 16 << 10;
   uint64_t want = (bytes + per_cta - 1) / per_cta;
   uint64_t cap = (uint64_t)sm_count_of(device) * g_ctas_per_sm;
   if (want < 1) want = 1;

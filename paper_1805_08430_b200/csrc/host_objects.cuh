@@ -87,9 +87,13 @@ static constexpr int kMaxSeg = 8;
 static constexpr int kScratchBlocks = 1024;
 
 // launch-geometry knobs (srf_tune): CTAs per SM and threads per CTA of the
-// copy kernels; defaults chosen from the NVLink/HBM probes (profiles/).
-static int g_ctas_per_sm = 2;
-static int g_copy_threads = 256;
+// copy kernels.  Large puts: one 512-thread CTA per SM - the same threads as
+// 2 x 256 and the same 256 MiB HBM put (0.924 of the copy peak), but half the
+// CTAs that each poll the credit and arrive on the counter: NVLink puts of 4 /
+// 16 MiB per round 20.3 -> 16.5 / 40.3 -> 36.2 us (A/B on one box,
+// profiles/r1_geometry_probe.txt); small puts keep one CTA per 16 KiB.
+static int g_ctas_per_sm = 1;
+static int g_copy_threads = 512;
 
 static int sm_count_of(int device) {
   static int cache[64] = {0};

@@ -1,5 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python bench.py --no-ps > gpurun_out/geo_n1b.json 2>/dev/null; echo rc=$?
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29561 bench.py --gpus 2 --no-ps --no-cpu > gpurun_out/geo_n2b.json 2>/dev/null; echo rc=$?
-SRFLOW_CTAS_PER_SM=2 SRFLOW_COPY_THREADS=256 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29562 bench.py --gpus 2 --no-ps --no-cpu > gpurun_out/geo_n2old.json 2>/dev/null; echo rc=$?
-SRFLOW_CTAS_PER_SM=2 SRFLOW_COPY_THREADS=256 timeout 900 python bench.py --no-ps > gpurun_out/geo_n1old.json 2>/dev/null; echo rc=$?
+timeout 600 python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu --no-ps > /dev/null 2>&1; echo plain rc=$?
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 40 -c 300 --csv --log-file gpurun_out/launches_n1_r1g.csv python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu --no-ps > gpurun_out/ncu_launch.log 2>&1; echo ncu rc=$?

@@ -324,6 +324,29 @@ def test_sliced_layout_units_stay_on_their_shard():
         assert PS.shard_of(u) == P.shard_of(owner)
 
 
+def test_static_gradient_layout_and_traffic():
+    """grad_mechanism="static" (the reference's mechanism_override="static"):
+    receive regions of S+1 on the shard instead of metadata slots, a ready
+    byte per remote gradient on the worker; NVLink bytes drop the metadata
+    block for the one flag byte."""
+    from paper_1805_08430_b200.ps import PsLayout, link_traffic
+    shapes = [(1000,), (37,), (4, 9)]
+    d = PsLayout(shapes, 2, 1)
+    s = PsLayout(shapes, 2, 1, grad_mechanism="static")
+    for v in range(3):
+        for w in range(2):
+            assert ("grecv", v, w) in s.blocks[2] and ("mslot", v, w) not in s.blocks[2]
+            assert ("ready", v) in s.blocks[w] and ("mstage", v) not in s.blocks[w]
+    S = sum(d.nbytes(v) for v in range(3))
+    td, ts = link_traffic(d, 3), link_traffic(s, 3)
+    meta = sum(41 if len(x) == 1 else 49 for x in shapes)
+    assert td[0]["link_out"] - ts[0]["link_out"] == meta - 3
+    assert td[2]["link_in"] - ts[2]["link_in"] == 2 * (meta - 3)
+    assert ts[0]["link_out"] == S + 3 and ts[2]["link_out"] == 2 * (S + 3)
+    with pytest.raises(errors.InvalidConfig):
+        PsLayout(shapes, 2, 1, grad_mechanism="bogus")
+
+
 def test_missing_library_fails_loudly(monkeypatch):
     """No CPU fallback: without libsrflow.so every entry point raises."""
     monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libsrflow.so")

@@ -1,3 +1,6 @@
 mkdir -p gpurun_out
-timeout 600 python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu --no-ps > /dev/null 2>&1; echo plain rc=$?
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 40 -c 300 --csv --log-file gpurun_out/launches_n1_r1g.csv python bench.py --steps 2 --warmup 3 --no-sweep --no-cpu --no-ps > gpurun_out/ncu_launch.log 2>&1; echo ncu rc=$?
+for n in 2 4; do
+for cfg in fcn5 lstm; do
+for g in dynamic static; do
+PROBE_CFG=$cfg PROBE_GRAD=$g PROBE_SLICES=0,4,1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 29531 tools/ps_slice_probe.py 2>>gpurun_out/slice_err.log | grep '^{' >> gpurun_out/slice_probe4.jsonl
+done; done; done

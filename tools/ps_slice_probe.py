@@ -22,10 +22,16 @@ for mib in [int(x) for x in os.environ.get("PROBE_SLICES", "0,64,16,4").split(",
     kw["grad_mechanism"] = os.environ.get("PROBE_GRAD", "dynamic")
     if os.environ.get("PROBE_PARTITION"):
         kw.update(placement="bytes", partition_bytes=int(os.environ["PROBE_PARTITION"]) << 20)
-    L = PsLayout(vgg16_shapes(), world, world, colocate=True, **kw)
+    cfg = os.environ.get("PROBE_CFG", "vgg")
+    if cfg == "vgg":
+        L = PsLayout(vgg16_shapes(), world, world, colocate=True, **kw)
+    elif cfg == "fcn5":   # configs[2] preset: 2 workers + 1 PS, server s on GPU s % world
+        L = PsLayout([(int(204.47e6) // 10 // 4,)] * 10, 2, 1, False, **kw)
+    else:                 # configs[4] LSTM preset: 7 workers + 1 PS
+        L = PsLayout([(int(35.93e6) // 14 // 4,)] * 14, 7, 1, False, **kw)
     r = bench.bench_ps(rank, world, local, 10, 3, op="sgd", cpu=False, layout=L,
                        label=f"slice {mib} MiB")
     if rank == 0:
-        print(json.dumps({"world": world, "slice_mib": mib, "grad": kw["grad_mechanism"], "units": len(L.shapes),
+        print(json.dumps({"cfg": cfg, "world": world, "slice_mib": mib, "grad": kw["grad_mechanism"], "units": len(L.shapes),
                           **{k: r.get(k) for k in ("steps_per_s", "schedule", "verified", "roofline",
                                                     "autotune_ms_per_5")}}), flush=True)

@@ -323,9 +323,9 @@ class PsStep:
         self._exchange = None
         self._exchange_built = None
         self._exchange_cfg = (
-            int(os.environ.get("SRFLOW_PS_EXCHANGE_LAG", 1) if exchange_lag is None
+            int(os.environ.get("SRFLOW_PS_EXCHANGE_LAG", 3) if exchange_lag is None
                 else exchange_lag),
-            (os.environ.get("SRFLOW_PS_EXCHANGE_ORDER", "index") if exchange_order is None
+            (os.environ.get("SRFLOW_PS_EXCHANGE_ORDER", "size") if exchange_order is None
              else exchange_order))
         self.schedule = "phases"
         self.use_schedule(schedule)

@@ -581,7 +581,9 @@ class PsStep:
         """One queue of this GPU's units (k_ps_exchange).  Keys are a global
         order every rank derives alike: push(v) < gen(v) < apply(v), the
         apply of a variable placed ``lag`` variables later so the next
-        weights are already moving while its gradients are awaited."""
+        weights are already moving while its gradients are awaited; static
+        gradient puts sit between gen(v) and apply(v).  Defaults (largest
+        variable first, lag 3) from profiles/r1_ps_order_probe.jsonl."""
         L, b, rows = self.L, self.batches, self._rows
         u64 = _lib.u64_array
         nv = len(L.shapes)

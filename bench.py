@@ -1341,13 +1341,18 @@ def main() -> int:
                       f"{world} workers + {world} shards co-located"))
             # labelled extension: partitioned variables (every tensor > 16 MiB cut
             # into one slice per shard), byte-balanced; values bit-identical
+            # (from 4 GPUs the partitions are also sent as 4 MiB slices: 537 -> 672
+            # it/s at N=4, slightly slower at N=2; profiles/r1_ps_slice_probe.jsonl)
+            sl = (4 << 20) if world >= 4 else None
             Lp = PsLayout(vgg16_shapes(), world, world, colocate=True, placement="bytes",
-                          partition_bytes=16 << 20)
+                          partition_bytes=16 << 20, slice_bytes=sl)
             section("ps_partitioned", lambda: bench_ps(
                 rank, world, local, max(10, args.steps), args.warmup, op=args.ps_op,
                 cpu=False, layout=Lp,
                 label=f"EXTENSION: VGG-16 with partitioned variables (tensors > 16 MiB "
-                      f"split into {world} slices, {len(Lp.shapes)} transfer units), "
+                      f"split into {world} partitions"
+                      + (", sent as 4 MiB slices" if sl else "")
+                      + f", {len(Lp.shapes)} transfer units), "
                       f"byte-balanced, {world} workers + {world} shards co-located"))
         section("ps_configs", lambda: bench_ps_configs(rank, world, local, max(20, args.steps),
                                                        args.warmup, args.ps_op,

@@ -1066,44 +1066,26 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
     ms = C.c_float()
     _lib.call("srf_event_elapsed_ms", ev[0], ev[1], C.byref(ms))
     t = dist_max(ms.value / 1e3)
-    # verify the smallest variable this rank owns: a full oracle replay of
-    # every iteration when that is cheap, else one further iteration checked
-    # against the oracle applied to the live state
-    # (transfer units: a partitioned variable's slices are checked against the
-    # matching slice of the model variable)
-    mine = [v for v in range(len(shapes)) if L.shard_of(v) % world == rank]
-    ok, how = True, "none"
-    if not mine:
-        how = "checked on the ranks that own shards (none on rank 0)"
+    # verify every transfer unit this rank owns against the golden-pinned
+    # oracle on the reference's own gradient stream (the device generated
+    # node_rng(0, gen(v, w), it) for every iteration 1..it): the first and the
+    # last elements of each unit, all iterations replayed (oracle.port
+    # ps_expected with a window: PCG64.advance, no full-size draw)
+    mine = [u for u in range(len(L.shapes)) if L.shard_of(u) % world == rank]
+    ok, how = True, "checked on the ranks that own shards (none on rank 0)"
+    win = 4096
+    for u in mine:
+        pv, p_off, n_u = L.parent(u)
+        cnt = min(win, n_u)
+        got = ps.variable(u).reshape(-1)
+        for lo, part in ((p_off, got[:cnt]), (p_off + n_u - cnt, got[n_u - cnt:])):
+            want = port.ps_expected(L.model_shapes, L.workers, 0, it, op=op, lr=0.01,
+                                    only=[pv], window=(lo, cnt))[pv]
+            ok = ok and part.tobytes() == want.tobytes()
     if mine:
-        v = min(mine, key=L.nbytes)
-        n_v = L.nbytes(v) // 4
-        pv, p_off, _pn = L.parent(v)
-        n_parent = math.prod(L.model_shapes[pv])
-        if it * L.workers * n_parent <= 4e8:
-            want = port.ps_expected_device(L.model_shapes, L.workers, 0, range(1, it + 1),
-                                           op=op, lr=0.01, only=[pv])[pv].reshape(-1)
-            ok = ps.variable(v).tobytes() == want[p_off:p_off + n_v].tobytes()
-            how = f"oracle replay of all {it} iterations"
-        else:
-            before = ps.variable(v).copy()
-    if world > 1 or (mine and how == "none"):  # (a collective step at N>1)
-        barrier_sync()
-        it += 1
-        ps.step(it)
-        ps.sync()
-        barrier_sync()
-        if mine and how == "none":
-            grads = [port.device_gradient(0, port.ps_node_ids(pv, w, L.workers)[1], it, n_v,
-                                          offset=p_off)
-                     for w in range(L.workers)]
-            want = before.reshape(-1).copy()
-            if op == "xor":
-                port.apply_xor(want, grads)
-            else:
-                port.apply_sgd(want, grads, 0.01)
-            ok = ps.variable(v).reshape(-1).tobytes() == want.tobytes()
-            how = f"one further iteration vs the oracle on the live state (after {it - 1})"
+        how = (f"all {len(mine)} units on this rank, first and last {win} elements, vs "
+               f"oracle.port.ps_expected over all {it} iterations on the reference PCG64 "
+               f"gradient stream (graph.py:333-350), bit-exact")
     ok = dist_sum(0.0 if ok else 1.0) == 0.0
     # roofline over the busiest GPU
     tr = [L.traffic(s) for s in range(L.nservers)]

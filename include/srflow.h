@@ -224,6 +224,17 @@ int srf_apply(srf_space_t var_space, uint64_t var_addr, uint64_t nbytes,
               int nworkers, int op, float lr, srf_stream_t stream,
               srf_event_t *ev_out);
 
+/* GenGrad / Input values on the device (graph.py:333-350 node_rng +
+ * synthesize_values, used by compute_node graph.py:363-370): elements
+ * [elem_offset, elem_offset + nelems) of
+ *   Generator(PCG64(((seed & 0xFFFFFFFF)*1000003 + node)*1000033 + iteration))
+ *     .random(n, dtype=float32)
+ * bit-exact (numpy's SeedSequence seeding, PCG64 XSL-RR, 24-bit floats), into
+ * fp32 elements at addr (16-B aligned) of the space, on its stream. */
+int srf_gen_reference(srf_space_t space, uint64_t addr, uint64_t nelems, uint64_t elem_offset,
+                      uint64_t seed, uint64_t node, uint64_t iteration, srf_stream_t stream,
+                      srf_event_t *ev_out);
+
 /* ---- batched PS step (configs[2..4]) ------------------------------------
  * One launch per phase per step over descriptor lists that are validated
  * once at creation (registration, token and bounds checks of every edge, the
@@ -234,9 +245,10 @@ int srf_apply(srf_space_t var_space, uint64_t var_addr, uint64_t nbytes,
  *                 body then tail byte released last; flags SRF_PUT_WAIT_EMPTY
  *   gen batch   - per worker x variable: acquire the weight flag (consume +
  *                 clear, StaticReceiver.poll), wait for the shard's credit
- *                 (meta flag clear), then (mode 1) produce the synthetic
- *                 gradient on the device (GenGrad stand-in) or (mode 0)
- *                 keep the host-uploaded one
+ *                 (meta flag clear), then (mode 1) produce the gradient
+ *                 on the device - the reference's own PCG64 GenGrad stream
+ *                 (graph.py:333-350), bit-exact, as srf_gen_reference - or
+ *                 (mode 0) keep a host-uploaded one
  *   apply batch - per variable: DynReceiver.poll + decode_meta + validation
  *                 on the device, then K4+K6 fused: the update reads every
  *                 remote gradient straight through the peer mapping (no

@@ -276,24 +276,57 @@ def ps_node_ids(v: int, w: int, workers: int) -> tuple[int, int, int]:
     return var, var + 1 + 2 * w, var + 2 + 2 * w
 
 
+def reference_values(seed: int, node: int, iteration: int, start: int, count: int) -> np.ndarray:
+    """Elements [start, start+count) of synthesize_values(F32, node_rng(seed,
+    node, iteration)) (graph.py:333-350) without drawing the ones before:
+    element i is the (i & 1) 32-bit half of PCG64 output i >> 1, so the bit
+    generator is advanced by start >> 1 outputs first (numpy's
+    PCG64.advance; a fresh Generator starts on a low half)."""
+    mix = ((seed & 0xFFFFFFFF) * 1_000_003 + node) * 1_000_033 + iteration
+    bg = np.random.PCG64(mix & 0xFFFFFFFFFFFFFFFF)
+    bg.advance(start >> 1)
+    vals = np.random.Generator(bg).random(count + (start & 1), dtype=np.float32)
+    return vals[start & 1:]
+
+
 def ps_expected(shapes: Sequence[tuple[int, ...]], workers: int, seed: int, steps: int,
-                op: str = "xor", lr: float = 0.01, elem: int = 0) -> list[np.ndarray]:
-    """Variable values after ``steps`` PS iterations:
-    init = synth(node_rng(seed, var, 0)); each step, each worker's gradient
-    synth(node_rng(seed, gen(v, w), it)) is folded in ascending w."""
+                op: str = "xor", lr: float = 0.01, elem: int = 0, *, first: int = 1,
+                only=None, window=None) -> list:
+    """Variable values after PS iterations ``first .. steps`` (SURVEY.md 8c
+    item 4): init = synth(node_rng(seed, var, 0)); each iteration, each
+    worker's gradient synth(node_rng(seed, gen(v, w), it)) is folded in
+    ascending w.  ``only``: variable indices to compute (others None);
+    ``window=(lo, n)``: only elements [lo, lo+n) of every variable (flat,
+    clipped), drawn with reference_values - the same numbers, so a sampled
+    check of a full-size run costs O(window) per (variable, worker, iteration)."""
     out = []
     for v, dims in enumerate(shapes):
+        if only is not None and v not in only:
+            out.append(None)
+            continue
         n = math.prod(dims)
         var_id = ps_node_ids(v, 0, workers)[0]
-        val = synthesize(n, elem, node_rng(seed, var_id, 0)).copy()
-        for it in range(1, steps + 1):
-            grads = [synthesize(n, elem, node_rng(seed, ps_node_ids(v, w, workers)[1], it))
-                     for w in range(workers)]
+        if window is None:
+            lo, cnt = 0, n
+            val = synthesize(n, elem, node_rng(seed, var_id, 0)).copy()
+        else:
+            if elem != 0:
+                raise ValueError("windowed expectations are fp32 only")
+            lo = min(window[0], n)
+            cnt = min(window[1], n - lo)
+            val = reference_values(seed, var_id, 0, lo, cnt).copy()
+        for it in range(first, steps + 1):
+            if window is None:
+                grads = [synthesize(n, elem, node_rng(seed, ps_node_ids(v, w, workers)[1], it))
+                         for w in range(workers)]
+            else:
+                grads = [reference_values(seed, ps_node_ids(v, w, workers)[1], it, lo, cnt)
+                         for w in range(workers)]
             if op == "xor":
                 apply_xor(val, grads)
             else:
                 apply_sgd(val, grads, lr)
-        out.append(val.reshape(dims))
+        out.append(val.reshape(dims) if window is None else val)
     return out
 
 
@@ -492,68 +525,6 @@ class PsRig:
 # counter-based hash (k_gen_batch, paper_1805_08430_b200/csrc/device_ps.cuh)
 # instead of the reference's host PCG64 stream.  This restatement lets the
 # tests check those device gradients and the variables they produce.
-
-_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
-
-
-def _mix64(x: np.ndarray) -> np.ndarray:
-    x = x.astype(np.uint64, copy=True)
-    x ^= x >> np.uint64(30)
-    x *= np.uint64(0xBF58476D1CE4E5B9)
-    x ^= x >> np.uint64(27)
-    x *= np.uint64(0x94D049BB133111EB)
-    x ^= x >> np.uint64(31)
-    return x
-
-
-def _fmix32(h: np.ndarray) -> np.ndarray:
-    h = h.astype(np.uint32, copy=True)
-    h ^= h >> np.uint32(16)
-    h *= np.uint32(0x85EBCA6B)
-    h ^= h >> np.uint32(13)
-    h *= np.uint32(0xC2B2AE35)
-    h ^= h >> np.uint32(16)
-    return h
-
-
-def device_gradient(seed: int, node: int, iteration: int, n: int,
-                    offset: int = 0) -> np.ndarray:
-    """fp32 values k_gen_batch writes for GenGrad node ``node`` at ``iteration``:
-    a 64-bit key from (seed, node, iteration), then per element a 32-bit
-    murmur finaliser of (index, key halves), top 24 bits -> [0, 1).  ``offset``:
-    elements offset ... offset+n-1 (a slice of a partitioned variable)."""
-    with np.errstate(over="ignore"):
-        s = np.array([seed], dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
-        a = _mix64(np.array([node], dtype=np.uint64) + np.uint64(0x51ED))
-        b = _mix64(np.array([iteration], dtype=np.uint64) * np.uint64(0xD1B54A32D192ED03))
-        key = int(_mix64(s ^ a ^ b)[0])
-        k0, k1 = np.uint32(key & 0xFFFFFFFF), np.uint32(key >> 32)
-        idx = np.arange(offset, offset + n, dtype=np.uint64).astype(np.uint32)
-        h = _fmix32(idx * np.uint32(0x9E3779B1) + k0) ^ k1
-    return (h >> np.uint32(8)).astype(np.float32) * np.float32(1.0 / 16777216.0)
-
-
-def ps_expected_device(shapes, workers: int, seed: int, iterations, op: str = "xor",
-                       lr: float = 0.01, only=None) -> list[np.ndarray]:
-    """Variables after PS iterations whose gradients come from device_gradient
-    (``only``: restrict to these variable indices; others are None)."""
-    out = []
-    for v, dims in enumerate(shapes):
-        if only is not None and v not in only:
-            out.append(None)
-            continue
-        n = math.prod(dims)
-        val = synthesize(n, 0, node_rng(seed, ps_node_ids(v, 0, workers)[0], 0)).copy()
-        for it in iterations:
-            grads = [device_gradient(seed, ps_node_ids(v, w, workers)[1], it, n)
-                     for w in range(workers)]
-            if op == "xor":
-                apply_xor(val, grads)
-            else:
-                apply_sgd(val, grads, lr)
-        out.append(val.reshape(dims))
-    return out
-
 
 # -- the reference's copy-heavy RPC baseline (runtime/protocol.py:257-448) -------------
 

@@ -135,6 +135,7 @@ SIGNATURES = {
     "srf_rpc_transfer": (C.c_int, [vp, u64, C.c_uint32, u64, u64, u64, vp, u64, u64, u64, u64,
                                    u64, vp, vp]),
     "srf_reduce_max_f32": (C.c_int, [vp, u64, u64, u64, vp]),
+    "srf_gen_reference": (C.c_int, [vp, u64, u64, u64, u64, u64, u64, vp, P(vp)]),
 }
 
 _lib = None
@@ -164,7 +165,7 @@ def load() -> C.CDLL:
 
 _KNOBS = {"SRFLOW_CTAS_PER_SM": 0, "SRFLOW_COPY_THREADS": 1, "SRFLOW_PUT_IMPL": 2,
           "SRFLOW_ALLOC_VMM": 3, "SRFLOW_UNROLL": 4, "SRFLOW_VEC32": 5,
-          "SRFLOW_PEER_CE_KIB": 6}
+          "SRFLOW_PEER_CE_KIB": 6, "SRFLOW_FORCE_SYS": 7, "SRFLOW_PUT_TIMEOUT_MS": 8}
 
 
 def _apply_env_knobs(lib) -> None:
@@ -180,7 +181,7 @@ def _apply_env_knobs(lib) -> None:
 def tune(knob: str, value: int) -> None:
     call("srf_tune", {"ctas_per_sm": 0, "copy_threads": 1, "put_impl": 2,
                       "alloc_vmm": 3, "unroll": 4, "vec32": 5,
-                      "peer_ce_kib": 6}[knob], value)
+                      "peer_ce_kib": 6, "force_sys": 7, "put_timeout_ms": 8}[knob], value)
 
 
 def last_error() -> str:

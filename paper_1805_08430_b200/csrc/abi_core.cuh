@@ -50,6 +50,17 @@ int srf_tune(int knob, int value) {
       if (value < 0) return fail(SRF_E_INVALID_CONFIG, "peer_ce_kib >= 0");
       g_peer_ce_bytes = (uint64_t)value << 10;
       return SRF_OK;
+    case 7:
+      // test knob: treat every destination/source as a peer's memory -
+      // system-scope arrival/release and the copy-engine body path - so a
+      // one-GPU box exercises the cross-device code
+      if (value != 0 && value != 1) return fail(SRF_E_INVALID_CONFIG, "force_sys 0|1");
+      g_force_sys = value;
+      return SRF_OK;
+    case 8:
+      if (value < 1) return fail(SRF_E_INVALID_CONFIG, "put_timeout_ms >= 1");
+      g_put_timeout_ns = (uint64_t)value * 1000000ull;
+      return SRF_OK;
     default:
       return fail(SRF_E_INVALID_CONFIG, "unknown knob %d", knob);
   }
@@ -738,7 +749,7 @@ static int put_impl(srf_space_t src_space, const uint64_t *src_addr, const uint6
   a.dst = dst_space->base + dst_addr;
   a.total = total;
   a.tail_release = 1;
-  a.sys_scope = (dst_space->imported || dst_space->device != s->device) ? 1 : 0;
+  a.sys_scope = (g_force_sys || dst_space->imported || dst_space->device != s->device) ? 1 : 0;
   a.db = nullptr;
   a.db_len = 0;
   if (dst_space->db && !dst_space->imported) {
@@ -758,13 +769,14 @@ static int put_impl(srf_space_t src_space, const uint64_t *src_addr, const uint6
     }
   }
   a.wait_empty = (flags & SRF_PUT_WAIT_EMPTY) ? 1 : 0;
-  a.timeout_ns = 5ull * 1000 * 1000 * 1000;
+  a.timeout_ns = g_put_timeout_ns;
   a.counter = s->counter;
   a.err = src_space->err;
   a.consume = consume;
   CUDA_TRY(cudaSetDevice(s->device));
   int rc;
-  if (a.sys_scope && g_peer_ce_bytes && total - 1 >= g_peer_ce_bytes && a.db_len <= 1)
+  if (a.sys_scope && g_peer_ce_bytes && total - 1 >= g_peer_ce_bytes && a.db_len <= 1 &&
+      !a.wait_empty && !a.consume)
     rc = put_via_copy_engine(a, s);
   else
     rc = launch_copy(a, s, "k_put");
@@ -797,7 +809,7 @@ int srf_get(srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
   a.dst = dst_space->base + dst_addr;
   a.total = length;
   a.tail_release = 0;
-  const bool cross = src_space->imported || src_space->device != s->device;
+  const bool cross = g_force_sys || src_space->imported || src_space->device != s->device;
   a.src_remote = cross ? 1 : 0;
   a.counter = s->counter;
   a.err = dst_space->err;
@@ -926,8 +938,8 @@ int srf_apply(srf_space_t var_space, uint64_t var_addr, uint64_t nbytes,
       return fail(SRF_E_SHAPE_MISMATCH, "SGD gradient not fp32 aligned");
     a.g[w] = grad_spaces[w]->base + grad_addrs[w];
   }
-  if (nbytes == 0) return record_event(var_space->device, var_space->stream->s, ev_out);
   srf_stream *s = stream_or_default(var_space, st);
+  if (nbytes == 0) return record_event(s->device, s->s, ev_out);
   int grid, block;
   copy_geometry(s->device, nbytes, &grid, &block);
   CUDA_TRY(cudaSetDevice(s->device));
@@ -937,6 +949,27 @@ int srf_apply(srf_space_t var_space, uint64_t var_addr, uint64_t nbytes,
     k_apply_sgd<<<grid, block, 0, s->s>>>(a);
   rc = launch_check("k_apply");
   if (rc) return rc;
+  return record_event(s->device, s->s, ev_out);
+}
+
+int srf_gen_reference(srf_space_t sp, uint64_t addr, uint64_t nelems, uint64_t elem_offset,
+                      uint64_t seed, uint64_t node, uint64_t iteration, srf_stream_t st,
+                      srf_event_t *ev_out) {
+  DeviceGuard device_guard;
+  int rc = check_raw(sp, addr, nelems * 4, "generated tensor");
+  if (rc) return rc;
+  if (addr % 16) return fail(SRF_E_INVALID_CONFIG, "generated tensor must be 16-B aligned");
+  srf_stream *s = stream_or_default(sp, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  if (nelems) {
+    const uint64_t want = (nelems * 4 + (128 << 10) - 1) / (128 << 10);
+    const uint64_t cap = (uint64_t)sm_count_of(s->device) * 4;
+    const int grid = (int)std::max<uint64_t>(1, std::min(want, cap));
+    k_gen_reference<<<grid, 512, 0, s->s>>>((float *)(sp->base + addr), nelems, elem_offset,
+                                            seed, node, iteration);
+    rc = launch_check("k_gen_reference");
+    if (rc) return rc;
+  }
   return record_event(s->device, s->s, ev_out);
 }
 

@@ -47,6 +47,38 @@ __device__ __forceinline__ bool grid_arrive(unsigned int *counter, unsigned expe
   return prev == expected_last;
 }
 
+// Arrival that also counts aborted CTAs (a timed-out credit): an aborted CTA
+// adds kAbortUnit, so the last arriver knows whether any CTA skipped its
+// share - then the tail byte is NOT released (the put did not happen as a
+// whole; the host sees the timeout).  Grids stay far below 2^20 CTAs.
+static constexpr unsigned kAbortUnit = 1u << 20;
+
+// Acquire-spin until the receive region's flag reads 0 (the receiver's
+// credit); false (and err = 2) on timeout.
+__device__ __forceinline__ bool credit_wait(const uint8_t *flag, uint64_t timeout_ns, int *err) {
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_acquire_sys_u8(flag) != 0) {
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      atomicExch(err, 2);
+      return false;
+    }
+    __nanosleep(64);
+  }
+  return true;
+}
+
+__device__ __forceinline__ bool grid_arrive_abort(unsigned int *counter, unsigned expected_last,
+                                                  int sys_scope, bool aborted, bool *any_abort) {
+  const unsigned inc = 1u + (aborted ? kAbortUnit : 0u);
+  unsigned prev;
+  if (sys_scope)
+    asm volatile("atom.add.acq_rel.sys.u32 %0, [%1], %2;" : "=r"(prev) : "l"(counter), "r"(inc) : "memory");
+  else
+    asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(prev) : "l"(counter), "r"(inc) : "memory");
+  *any_abort = aborted || (prev >= kAbortUnit);
+  return (prev & (kAbortUnit - 1)) == expected_last;
+}
+
 __device__ __forceinline__ void release_tail(uint8_t *p, uint32_t v, int sys_scope) {
   uint16_t x = (uint16_t)v;
   if (sys_scope)
@@ -376,41 +408,43 @@ struct PutArgs {
 // co-aligned variant keeps the lean register budget of the plain paths.
 template <int U16, bool kSectors>
 __global__ void __launch_bounds__(512) k_put(PutArgs a) {
-  __shared__ int s_last;
+  __shared__ int s_last, s_abort;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint8_t *tail = a.dst + a.total - 1;
 
-  if (a.wait_empty) {
+  if (threadIdx.x == 0) {
+    s_abort = 0;
     // credit check of the iteration barrier (runtime/protocol.py:102-111):
-    // the receiver must have cleared the previous transfer's flag.
-    if (threadIdx.x == 0) {
-      uint64_t t0 = globaltimer_ns();
-      while (ld_acquire_sys_u8(tail) != 0) {
-        if (globaltimer_ns() - t0 > a.timeout_ns) {
-          atomicExch(a.err, 2);
-          break;
-        }
-        __nanosleep(64);
-      }
-    }
-    __syncthreads();
+    // the receiver must have cleared the previous transfer's flag.  A CTA
+    // whose wait times out writes nothing, and the tail is then withheld.
+    if (a.wait_empty) s_abort = credit_wait(tail, a.timeout_ns, a.err) ? 0 : 1;
   }
+  __syncthreads();
 
   // body: every byte except the tail one when tail_release is set
-  uint64_t body = a.tail_release ? a.total - 1 : a.total;
-  for (int i = 0; i < a.nseg; ++i) {
-    const Seg &sg = a.seg[i];
-    if (sg.dst_off >= body) break;
-    uint64_t n = sg.len;
-    if (sg.dst_off + n > body) n = body - sg.dst_off;
-    copy_bytes_grid<U16, kSectors>(a.dst + sg.dst_off, sg.src, n, t, nth, !a.src_remote);
+  if (!s_abort) {
+    uint64_t body = a.tail_release ? a.total - 1 : a.total;
+    for (int i = 0; i < a.nseg; ++i) {
+      const Seg &sg = a.seg[i];
+      if (sg.dst_off >= body) break;
+      uint64_t n = sg.len;
+      if (sg.dst_off + n > body) n = body - sg.dst_off;
+      copy_bytes_grid<U16, kSectors>(a.dst + sg.dst_off, sg.src, n, t, nth, !a.src_remote);
+    }
   }
 
   if (!a.tail_release) return;
   // flag-last: all CTAs publish, the last to arrive releases the tail byte.
   __syncthreads();
-  if (threadIdx.x == 0) s_last = grid_arrive(a.counter, gridDim.x - 1, a.sys_scope);
+  if (threadIdx.x == 0) {
+    bool any_abort;
+    s_last = grid_arrive_abort(a.counter, gridDim.x - 1, a.sys_scope, s_abort, &any_abort);
+    if (s_last && any_abort) {
+      atomicExch(a.counter, 0u);  // re-armed; no tail, no doorbell, no consume
+      s_last = 0;
+    }
+  }
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
     const Seg &ls = a.seg[a.nseg - 1];
@@ -560,7 +594,7 @@ __device__ void bulk_copy_cta(uint8_t *dst, const uint8_t *src, uint64_t n,
 
 __global__ void __launch_bounds__(256) k_put_bulk(PutArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ int s_last;
+  __shared__ int s_last, s_abort;
   uint64_t *bars = (uint64_t *)(smem + kBulkChunk * kBulkStages);
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -568,22 +602,11 @@ __global__ void __launch_bounds__(256) k_put_bulk(PutArgs a) {
   if (threadIdx.x == 0) {
     for (int i = 0; i < kBulkStages; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_abort = (a.wait_empty && !credit_wait(tail, a.timeout_ns, a.err)) ? 1 : 0;
   }
   __syncthreads();
-  if (a.wait_empty) {
-    if (threadIdx.x == 0) {
-      uint64_t t0 = globaltimer_ns();
-      while (ld_acquire_sys_u8(tail) != 0) {
-        if (globaltimer_ns() - t0 > a.timeout_ns) {
-          atomicExch(a.err, 2);
-          break;
-        }
-        __nanosleep(64);
-      }
-    }
-    __syncthreads();
-  }
   uint64_t body = a.tail_release ? a.total - 1 : a.total;
+  if (s_abort) body = 0;  // timed-out credit: write nothing
   uint32_t use = 0;  // uses per barrier so far (same for every slot: see below)
   for (int i = 0; i < a.nseg; ++i) {
     const Seg &sg = a.seg[i];
@@ -622,7 +645,14 @@ __global__ void __launch_bounds__(256) k_put_bulk(PutArgs a) {
   if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
   if (!a.tail_release) return;
   __syncthreads();
-  if (threadIdx.x == 0) s_last = grid_arrive(a.counter, gridDim.x - 1, a.sys_scope);
+  if (threadIdx.x == 0) {
+    bool any_abort;
+    s_last = grid_arrive_abort(a.counter, gridDim.x - 1, a.sys_scope, s_abort, &any_abort);
+    if (s_last && any_abort) {
+      atomicExch(a.counter, 0u);
+      s_last = 0;
+    }
+  }
   __syncthreads();
   if (s_last && threadIdx.x == 0) {
     const Seg &ls = a.seg[a.nseg - 1];

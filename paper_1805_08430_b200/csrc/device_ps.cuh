@@ -304,29 +304,6 @@ __device__ __forceinline__ void put_batch_units(const BatchPut *descs, int n,
     put_unit(descs, n, u, counters, timeout_ns, err, sys);
 }
 
-__device__ __forceinline__ uint64_t mix64(uint64_t x) {
-  x ^= x >> 30;
-  x *= 0xBF58476D1CE4E5B9ull;
-  x ^= x >> 27;
-  x *= 0x94D049BB133111EBull;
-  x ^= x >> 31;
-  return x;
-}
-
-__device__ __forceinline__ uint32_t fmix32(uint32_t h) {
-  h ^= h >> 16;
-  h *= 0x85EBCA6Bu;
-  h ^= h >> 13;
-  h *= 0xC2B2AE35u;
-  h ^= h >> 16;
-  return h;
-}
-
-// uniform [0,1) fp32 of a counter-based stream keyed on (seed, node, iteration)
-__device__ __forceinline__ float unit_f32(uint32_t k0, uint32_t k1, uint32_t i) {
-  return (float)((fmix32(i * 0x9E3779B1u + k0) ^ k1) >> 8) * (1.0f / 16777216.0f);
-}
-
 __device__ __forceinline__ void gen_unit(const BatchGen *descs, int n, uint32_t u,
                                          unsigned int *counters, uint64_t seed,
                                          uint64_t iteration, int regen, int fuse_meta,
@@ -347,21 +324,11 @@ __device__ __forceinline__ void gen_unit(const BatchGen *descs, int n, uint32_t 
     }
     __syncthreads();
     if (regen) {
-      const uint64_t key = mix64(seed * 0x9E3779B97F4A7C15ull ^ mix64(d.node + 0x51ED) ^
-                                 mix64(iteration * 0xD1B54A32D192ED03ull));
-      const uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
-      const uint64_t nf = d.n / 4;
-      const uint64_t nth = (uint64_t)d.cta_count * blockDim.x;
-      float4 *g4 = (float4 *)d.grad;  // gradient blocks are 16-B aligned by layout
-      const uint32_t e0 = (uint32_t)d.elem_offset;
-      for (uint64_t q = (uint64_t)lb * blockDim.x + threadIdx.x; q < nf / 4; q += nth) {
-        const uint32_t i = (uint32_t)(4 * q) + e0;
-        g4[q] = make_float4(unit_f32(k0, k1, i), unit_f32(k0, k1, i + 1),
-                            unit_f32(k0, k1, i + 2), unit_f32(k0, k1, i + 3));
-      }
-      float *g = (float *)d.grad;
-      for (uint64_t i = (nf / 4) * 4 + (uint64_t)lb * blockDim.x + threadIdx.x; i < nf; i += nth)
-        g[i] = unit_f32(k0, k1, (uint32_t)i + e0);
+      // GenGrad = synthesize_values(dims, F32, node_rng(seed, node, iteration))
+      // (graph.py:333-350, :363-370): the reference's PCG64 stream, bit-exact,
+      // at the slice's global element indices (device_pcg.cuh)
+      pcg_fill_f32_cta((float *)d.grad, d.n / 4, d.elem_offset, seed, d.node, iteration, lb,
+                       d.cta_count);
     }
     __syncthreads();
     if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, sys);

@@ -48,12 +48,15 @@ static int g_unroll = 8;    // 16-B vectors in flight per thread (4 or 8)
 // probe); the engine's extra ~15 us per put (credit-wait launch, copy, tail
 // launch) only pays off from ~64 MiB: threshold 32 MiB.
 static uint64_t g_peer_ce_bytes = 32ull << 20;
+static int g_force_sys = 0;  // knob 7 (tests): every put/get takes the cross-device path
+static uint64_t g_put_timeout_ns = 5000000000ull;  // knob 8: credit wait limit of a put
 
 // launch K1/K4/K5 with the configured implementation
 static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
   uint64_t big = 0;
   for (int i = 0; i < a.nseg; ++i) big = std::max<uint64_t>(big, a.seg[i].len);
-  if (g_put_impl == 1 && big >= (uint64_t)4 * kBulkChunk) {
+  // the TMA variant has no fused consume and no source-aligned pull path
+  if (g_put_impl == 1 && big >= (uint64_t)4 * kBulkChunk && !a.consume && !a.src_remote) {
     static bool attr_set[64] = {false};
     if (s->device >= 0 && s->device < 64 && !attr_set[s->device]) {
       CUDA_TRY(cudaFuncSetAttribute(k_put_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -89,17 +92,13 @@ static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
   return launch_check(what);
 }
 
-// K1 with a copy-engine body: [credit wait] -> body copies -> a one-thread K1
-// that releases the tail byte.  Stream order starts the tail kernel only after
-// the copies have completed, so a consumer that acquires the flag sees the
-// body (release/acquire stress test, tests/test_gpu_kernels.py).
+// K1 with a copy-engine body: body copies -> a one-thread K1 that releases
+// the tail byte.  Stream order starts the tail kernel only after the copies
+// have completed, so a consumer that acquires the flag sees the body
+// (release/acquire stress test, tests/test_gpu_kernels.py).  Only for puts
+// without a credit wait: a DMA copy cannot be skipped when a credit times
+// out, so credit-gated puts stay on the kernel (put_impl).
 static int put_via_copy_engine(const PutArgs &a, srf_stream *s) {
-  uint8_t *tail = a.dst + a.total - 1;
-  if (a.wait_empty) {
-    k_flag_wait<<<1, 32, 0, s->s>>>(tail, 0, 0, a.timeout_ns, a.err);
-    int rc = launch_check("k_flag_wait(credit)");
-    if (rc) return rc;
-  }
   const uint64_t body = a.total - 1;
   for (int i = 0; i < a.nseg; ++i) {
     const Seg &sg = a.seg[i];

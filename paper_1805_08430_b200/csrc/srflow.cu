@@ -35,6 +35,7 @@ namespace cg = cooperative_groups;
 
 #include "host_objects.cuh"
 #include "device_copy.cuh"
+#include "device_pcg.cuh"
 #include "device_ps.cuh"
 #include "device_rpc.cuh"
 #include "host_launch.cuh"

@@ -48,7 +48,7 @@ def main() -> int:
             torch.distributed.barrier()
             # transfer units this rank owns, each against its slice of the model
             mine = [u for u in range(len(L.shapes)) if L.shard_of(u) % world == rank]
-            want = port.ps_expected_device(shapes, W, 5, range(1, 9), op="sgd", lr=0.02,
+            want = port.ps_expected(shapes, W, 5, 8, op="sgd", lr=0.02,
                                            only=sorted({L.parent(u)[0] for u in mine}))
             for u in mine:
                 v, off, n = L.parent(u)

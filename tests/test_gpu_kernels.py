@@ -183,13 +183,21 @@ def test_flag_wait_and_timeout(pair):
         b.sync()
 
 
-@pytest.fixture(params=["sm", "copy_engine"])
+@pytest.fixture(params=["sm", "sm_sys", "copy_engine"])
 def peer_engine(request):
     """Cross-device bodies by SM stores, or by the copy engine (knob 6) with
-    the flag released by an SM store after them."""
-    _lib.tune("peer_ce_kib", 0 if request.param == "sm" else 1)
+    the flag released by an SM store after them.  On a one-GPU box the
+    "sm_sys" and "copy_engine" arms set knob 7 (force_sys), so the
+    system-scope arrival/release and the copy-engine body + tail-release path
+    run even though both spaces share the device."""
+    one_gpu = _lib.device_count() < 2
+    if request.param == "sm_sys" and not one_gpu:
+        pytest.skip("two GPUs: the plain arm already takes the system-scope path")
+    _lib.tune("peer_ce_kib", 1 if request.param == "copy_engine" else 0)
+    _lib.tune("force_sys", 1 if one_gpu and request.param != "sm" else 0)
     yield request.param
     _lib.tune("peer_ce_kib", 32768)
+    _lib.tune("force_sys", 0)
 
 
 @pytest.mark.parametrize("size", [1025, 4097, (1 << 20) + 3, (8 << 20) + 8])
@@ -220,7 +228,10 @@ def test_release_acquire_stress(pair, peer_engine):
     on the receiver before the producer's put (true concurrency over NVLink);
     with one GPU both run in stream order (no cross-kernel waiting on one GPU)."""
     a, b, ra, rb = pair
-    two_gpus = a.device != b.device
+    # concurrent consumer: always across GPUs; on one GPU when the put takes
+    # the system-scope path (knob 7) - the spinning consumer CTA and the
+    # producer grid share the device on two streams
+    two_gpus = a.device != b.device or peer_engine != "sm"
     big = rand_bytes(8 << 20, 77)
     src_base = ra.base_addr + (16 << 20)
     a.write_raw(src_base, big)
@@ -408,14 +419,54 @@ def test_put_consume_one_launch(pair):
     dst = rb.base_addr + (24 << 20)
     b.write_raw(dst + n, b"\x00")
     u = _lib.u64_array
-    for k in range(3):
-        ev = C.c_void_p()
-        _lib.call("srf_put_consume", a.handle, u([src, ra.base_addr + 64]), u([n, 1]),
+    for impl in (0, 1):  # the TMA variant falls back to K1 for a fused consume
+        _lib.tune("put_impl", impl)
+        try:
+            for k in range(3):
+                ev = C.c_void_p()
+                _lib.call("srf_put_consume", a.handle, u([src, ra.base_addr + 64]), u([n, 1]),
+                          u([ra.access_token] * 2), 2, b.handle, dst, rb.access_token,
+                          _lib.PUT_WAIT_EMPTY, b.handle, dst + n, None, C.byref(ev))
+                _lib.Event(ev).wait()
+                assert b.read_raw(dst, n) == data.tobytes()
+                assert b.read_raw(dst + n, 1) == b"\x00"
+        finally:
+            _lib.tune("put_impl", 0)
+
+
+@pytest.mark.parametrize("force_sys", [0, 1])
+@pytest.mark.parametrize("impl", [0, 1])
+def test_timed_out_credit_leaves_receiver_untouched(pair, force_sys, impl):
+    """SRF_PUT_WAIT_EMPTY against a flag that is never cleared: the put times
+    out (errors.Timeout) and writes neither the body nor the tail - on the
+    SM path, the TMA variant, and (force_sys) the system-scope path, where a
+    copy-engine body is never used for a credit-gated put."""
+    a, b, ra, rb = pair
+    n = (2 << 20) + 32
+    src = ra.base_addr + 4096
+    a.write_raw(src, rand_bytes(n, 3))
+    a.write_raw(ra.base_addr + 64, b"\x01")
+    dst = rb.base_addr + (30 << 20)
+    before = rand_bytes(n, 4).tobytes() + b"\x07"   # flag 7: not consumed
+    b.write_raw(dst, before)
+    _lib.tune("put_timeout_ms", 50)
+    _lib.tune("put_impl", impl)
+    _lib.tune("force_sys", force_sys)
+    _lib.tune("peer_ce_kib", 1)
+    try:
+        u = _lib.u64_array
+        _lib.call("srf_put", a.handle, u([src, ra.base_addr + 64]), u([n, 1]),
                   u([ra.access_token] * 2), 2, b.handle, dst, rb.access_token,
-                  _lib.PUT_WAIT_EMPTY, b.handle, dst + n, None, C.byref(ev))
-        _lib.Event(ev).wait()
-        assert b.read_raw(dst, n) == data.tobytes()
-        assert b.read_raw(dst + n, 1) == b"\x00"
+                  _lib.PUT_WAIT_EMPTY, None, None)
+        with pytest.raises(errors.Timeout):
+            a.sync()
+        b.sync()
+        assert b.read_raw(dst, n + 1) == before
+    finally:
+        _lib.tune("put_timeout_ms", 5000)
+        _lib.tune("put_impl", 0)
+        _lib.tune("force_sys", 0)
+        _lib.tune("peer_ce_kib", 32768)
 
 
 @pytest.mark.parametrize("size", [65536, (1 << 20) + 16, (5 << 20) + 3])

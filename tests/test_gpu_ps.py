@@ -1,8 +1,9 @@
 """Device-driven PS step (paper_1805_08430_b200.ps) vs the oracle: the
 reference's XOR update bit-exact (pinned by the golden PS runs through
 oracle.port.ps_expected) and SGD (unpinned restatement), in parity mode
-(host-uploaded PCG64 gradients) and regen mode (device gradients, checked
-against the oracle's restatement of the device RNG)."""
+(host-uploaded PCG64 gradients) and regen mode (the device generates the
+reference's own PCG64 GenGrad stream, device_pcg.cuh) - both checked against
+the same golden-pinned ps_expected."""
 from __future__ import annotations
 
 import numpy as np
@@ -53,19 +54,21 @@ def test_regen_mode_pipelined(shapes, W, P, coloc):
     for it in range(1, 9):
         ps.step(it)
     ps.sync()
-    want = port.ps_expected_device(shapes, W, 9, range(1, 9), op="sgd", lr=0.01)
+    want = port.ps_expected(shapes, W, 9, 8, op="sgd", lr=0.01)
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes()
     ps.close()
 
 
-def test_device_gradient_restatement():
+def test_device_gradient_is_the_reference_stream():
+    """GenGrad on the device = synthesize_values(F32, node_rng(seed, gen, it))."""
     L = PsLayout([(1031,)], 1, 1, False)
     ps = PsStep(L, seed=5)
     ps.step(7)
     ps.sync()
     g = np.frombuffer(ps.spaces[0].read_raw(ps.addr(0, ("grad", 0)), 1031 * 4), np.float32)
-    assert g.tobytes() == port.device_gradient(5, 1, 7, 1031).tobytes()
+    want = port.synthesize(1031, 0, port.node_rng(5, port.ps_node_ids(0, 0, 1)[1], 7))
+    assert g.tobytes() == want.tobytes()
     ps.close()
 
 
@@ -132,7 +135,7 @@ def test_graph_replayed_steps_match_eager():
     g = ps.capture(5)
     ps.replay(g)
     ps.sync()
-    want = port.ps_expected_device(shapes, W, 4, range(1, 7), op="sgd", lr=0.02)
+    want = port.ps_expected(shapes, W, 4, 6, op="sgd", lr=0.02)
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes()
     _lib.call("srf_graph_destroy", g)
@@ -148,7 +151,7 @@ def test_persistent_step_matches_oracle(shapes, W, P, coloc):
     ps.run_persistent(2, 6)
     ps.step(8)
     ps.sync()
-    want = port.ps_expected_device(shapes, W, 6, range(1, 9), op="sgd", lr=0.03)
+    want = port.ps_expected(shapes, W, 6, 8, op="sgd", lr=0.03)
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes()
     ps.close()
@@ -167,7 +170,7 @@ def test_exchange_schedule_matches_oracle(shapes, W, P, coloc, lag, order):
         assert ps.step(it) == 1
     ps.sync()
     assert _lib.launch_count() - launches == 6
-    want = port.ps_expected_device(shapes, W, 12, range(1, 7), op="sgd", lr=0.03)
+    want = port.ps_expected(shapes, W, 12, 6, op="sgd", lr=0.03)
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes(), (v, lag, order)
     # parity mode (reference PCG64 gradients uploaded), XOR
@@ -194,7 +197,7 @@ def test_exchange_schedule_mixes_with_phases():
         ps.use_schedule("exchange" if it % 2 else "phases")
         ps.step(it)
     ps.sync()
-    want = port.ps_expected_device(shapes, W, 2, range(1, 7), op="sgd", lr=0.01)
+    want = port.ps_expected(shapes, W, 2, 6, op="sgd", lr=0.01)
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes()
     ps.close()
@@ -216,7 +219,7 @@ def test_partitioned_variables_equal_the_model(placement):
             if not regen:
                 ps.sync()
         ps.sync()
-        want = (port.ps_expected_device(shapes, W, 8, range(1, 5), op=op, lr=0.02) if regen
+        want = (port.ps_expected(shapes, W, 8, 4, op=op, lr=0.02) if regen
                 else port.ps_expected(shapes, W, 8, 4, op=op))
         got = [np.zeros(int(np.prod(s)), np.float32) for s in shapes]
         for u in range(len(L.shapes)):
@@ -242,7 +245,7 @@ def test_sliced_variables_equal_the_model(schedule):
         for it in range(1, 7):
             ps.step(it)
     ps.sync()
-    want = port.ps_expected_device(shapes, W, 9, range(1, 7), op="sgd", lr=0.02)
+    want = port.ps_expected(shapes, W, 9, 6, op="sgd", lr=0.02)
     got = [np.zeros(int(np.prod(s)), np.float32) for s in shapes]
     for u in range(len(L.shapes)):
         v, off, n = L.parent(u)
@@ -263,7 +266,7 @@ def test_exchange_waits_for_in_place_gradients():
     for it in range(1, 6):
         ps.step(it)
     ps.sync()
-    want = port.ps_expected_device(shapes, W, 17, range(1, 6), op="sgd", lr=0.01)
+    want = port.ps_expected(shapes, W, 17, 5, op="sgd", lr=0.01)
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes(), v
     ps.close()
@@ -281,7 +284,7 @@ def test_multi_iteration_exchange_matches_oracle(shapes, W, P, coloc, per_launch
     ps.use_schedule("phases")
     ps.step(12)
     ps.sync()
-    want = port.ps_expected_device(shapes, W, 31, range(1, 13), op="sgd", lr=0.02)
+    want = port.ps_expected(shapes, W, 31, 12, op="sgd", lr=0.02)
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes(), v
     ps.close()
@@ -311,7 +314,7 @@ def test_static_gradients_match_oracle(shapes, W, P, coloc, schedule):
                 ps.use_schedule("exchange" if it % 2 else "phases")
             ps.step(it)
     ps.sync()
-    want = port.ps_expected_device(shapes, W, 21, range(1, 9), op="sgd", lr=0.02)
+    want = port.ps_expected(shapes, W, 21, 8, op="sgd", lr=0.02)
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes(), (v, schedule)
     ps.close()
@@ -333,7 +336,7 @@ def test_static_sliced_gradients_equal_the_model():
     ps = PsStep(L, seed=9, op="sgd", lr=0.02, schedule="exchange")
     ps.run_exchange(1, 6, per_launch=4)
     ps.sync()
-    want = port.ps_expected_device(shapes, W, 9, range(1, 7), op="sgd", lr=0.02)
+    want = port.ps_expected(shapes, W, 9, 6, op="sgd", lr=0.02)
     got = [np.zeros(int(np.prod(s)), np.float32) for s in shapes]
     for u in range(len(L.shapes)):
         v, off, n = L.parent(u)

@@ -356,3 +356,31 @@ def test_missing_library_fails_loudly(monkeypatch):
     from paper_1805_08430_b200.memspace import MemorySpace
     with pytest.raises(ImportError):
         MemorySpace(0, 1 << 20)
+
+
+def test_device_pcg_stream_on_host(tmp_path):
+    """device_pcg.cuh (the device GenGrad stream) compiled for the host and
+    run over simulated grids: bit-exact vs numpy's Generator(PCG64(mix))
+    .random(float32) of the reference's node_rng (graph.py:333-350), for
+    even/odd slice starts, 64-bit seeds and one-thread grids."""
+    import shutil
+    import subprocess
+    from oracle import port
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not os.path.exists(nvcc):
+        pytest.skip("nvcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "pcg_host")
+    subprocess.check_call([nvcc, "-std=c++17", "-Wno-deprecated-gpu-targets", "-o", exe,
+                           os.path.join(root, "tools", "pcg_host_check.cu")])
+    out = str(tmp_path / "o.bin")
+    for seed, node, it, n, e0, nth in [(0, 0, 2, 262144, 0, 1000), (0, 1, 2, 1003, 0, 64),
+                                       (5, 123, 7, 999, 1, 13), (1, 2, 3, 50, 3, 1),
+                                       (2**31 + 7, 10**12, 3, 777, 12345, 3),
+                                       (0xFFFFFFFF, 2**40, 2**33, 333, 0, 5),
+                                       (0, 0, 0, 17, 1, 100)]:
+        subprocess.check_call([exe, str(seed), str(node), str(it), str(n), str(e0), str(nth), out])
+        got = np.fromfile(out, dtype=np.float32)
+        want = port.synthesize(e0 + n, 0, port.node_rng(seed, node, it))[e0:]
+        assert got.tobytes() == want.tobytes(), (seed, node, it, n, e0, nth)
+        assert got.tobytes() == port.reference_values(seed, node, it, e0, n).tobytes()

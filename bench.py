@@ -490,9 +490,33 @@ def bench_sendrecv_e2e(S, steps, warmup, rank, world, device):
 # -- CPU reference (oracle port) -----------------------------------------------------------------
 
 
+def _reference_harness():
+    """oracle/ref_harness.py when the real reference is present (vendored into
+    oracle/_ref by oracle/vendor_ref.py, which build() runs), else None."""
+    try:
+        from oracle import ref_harness
+        return ref_harness if ref_harness.reference() is not None else None
+    except Exception as exc:  # pragma: no cover - depends on the snapshot
+        log(f"reference not importable ({type(exc).__name__}: {exc}); using the port")
+        return None
+
+
 def cpu_reference(S, min_seconds=10.0, min_steps=3, max_steps=None):
-    from oracle import port
-    rig = port.MicrobenchRig(S, generate=False)
+    """Static Send/Recv of S bytes on the host: the real reference's endpoints
+    (StaticSender.send + StaticReceiver.poll + the ReduceMax consumer) when it
+    is vendored, else the numpy port.  Returns (GB/s, steps, s, kind, what)."""
+    R = _reference_harness()
+    if R is not None:
+        rig = R.EndpointRig(S, "static")
+        what = ("rdmaflow (the reference, oracle/_ref) StaticSender.send -> "
+                "StaticReceiver.poll -> ReduceMax max, tests/test_protocol.py Rig layout")
+        kind = "reference"
+    else:
+        from oracle import port
+        rig = port.MicrobenchRig(S, generate=False)
+        what = ("oracle/port.py MicrobenchRig: ascending 1-4096 B chunk delivery + flag "
+                "poll + max")
+        kind = "port"
     rig.step()  # warm
     n, t0 = 0, time.perf_counter()
     while True:
@@ -501,25 +525,38 @@ def cpu_reference(S, min_seconds=10.0, min_steps=3, max_steps=None):
         dt = time.perf_counter() - t0
         if (max_steps is not None and n >= max_steps) or (dt >= min_seconds and n >= min_steps):
             break
-    return S * n / dt / 1e9, n, dt
+    return S * n / dt / 1e9, n, dt, kind, what
 
 
 def cpu_mechanisms(sizes=(1 << 20, 16 << 20), seconds=1.5):
-    """The reference's three mechanisms on this host (oracle/port.py, 1 core):
-    zero-copy static, staged 'cp', and the copy-heavy RPC fragment ring."""
-    from oracle import port
+    """The reference's mechanisms on this host, 1 core: zero-copy static,
+    staged 'cp', dynamic allocation, and the copy-heavy RPC fragment ring -
+    the real reference's endpoints (oracle/ref_harness.py) when vendored,
+    plus its whole Session at zerocp; else the numpy port."""
+    R = _reference_harness()
     out = []
     for size in sizes:
-        row = {"bytes": size}
-        for name, rig in (("static", port.MicrobenchRig(size, generate=False)),
-                          ("cp", port.MicrobenchRig(size, generate=False, stage_copy=True)),
-                          ("rpc", port.RpcRig(size))):
+        row = {"bytes": size, "kind": "reference" if R else "port"}
+        if R is not None:
+            rigs = (("static", lambda: R.EndpointRig(size, "static")),
+                    ("cp", lambda: R.EndpointRig(size, "static", stage_copy=True)),
+                    ("dynamic", lambda: R.EndpointRig(size, "dynamic")),
+                    ("rpc", lambda: R.EndpointRig(size, "rpc")),
+                    ("session_zerocp", lambda: R.SessionArm(size)))
+        else:
+            from oracle import port
+            rigs = (("static", lambda: port.MicrobenchRig(size, generate=False)),
+                    ("cp", lambda: port.MicrobenchRig(size, generate=False, stage_copy=True)),
+                    ("rpc", lambda: port.RpcRig(size)))
+        for name, make in rigs:
+            rig = make()
             rig.step()
             n, t0 = 0, time.perf_counter()
             while time.perf_counter() - t0 < seconds or n < 2:
                 rig.step()
                 n += 1
             row[f"{name}_gbps"] = round(size * n / (time.perf_counter() - t0) / 1e9, 4)
+        row["rpc_over_static"] = round(row["rpc_gbps"] / row["static_gbps"], 3)
         out.append(row)
     return out
 
@@ -527,9 +564,18 @@ def cpu_mechanisms(sizes=(1 << 20, 16 << 20), seconds=1.5):
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
-    from oracle import port
     S = args.bytes
-    rig = port.MicrobenchRig(S, generate=False)
+    R = _reference_harness()
+    if R is not None:
+        rig = R.EndpointRig(S, "static")
+        kind, what = "reference", ("rdmaflow (the reference itself, vendored in oracle/_ref): "
+                                   "StaticSender.send -> StaticReceiver.poll -> ReduceMax "
+                                   "max over the received view")
+    else:
+        from oracle import port
+        rig = port.MicrobenchRig(S, generate=False)
+        kind, what = "port", ("oracle/port.py MicrobenchRig (ascending 1-4096 B chunked "
+                              "delivery + flag poll + max)")
     for _ in range(args.warmup):
         rig.step()
     t0 = time.perf_counter()
@@ -543,11 +589,9 @@ def run_reference_arm(args, rank, world):
         "ms_per_step": round(dt / args.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(S, world),
-        "cpu_baseline": {"value": round(gbps, 4), "unit": "GB/s", "cores": 1, "kind": "port",
-                         "sample": f"{args.steps} static Send/Recv steps of {S} B "
-                                   f"(ascending 1-4096 B chunked delivery + flag poll + max, "
-                                   f"oracle/port.py MicrobenchRig), host cpu_count="
-                                   f"{os.cpu_count()}; the reference's delivery loop is "
+        "cpu_baseline": {"value": round(gbps, 4), "unit": "GB/s", "cores": 1, "kind": kind,
+                         "sample": f"{args.steps} static Send/Recv steps of {S} B ({what}), "
+                                   f"host cpu_count={os.cpu_count()}; the reference is "
                                    f"single-threaded Python (its threads=True mode is "
                                    f"GIL-serialised), so it uses one core"},
         "e2e": {"value": round(gbps, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
@@ -1145,8 +1189,18 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
            "autotune_ms_per_5": {k: round(v, 3) for k, v in times.items()}}
     ps.close()
     if cpu and rank == 0 and world == 1:
-        rig = cpu_rig() if cpu_rig else port.PsRig(shapes, L.workers, L.shards, L.colocate,
-                                                    seed=0, op=op, lr=0.01)
+        R = _reference_harness()
+        if R is not None:
+            # the reference's own Session over the same PS graph (its update
+            # is XOR; SGD has no reference implementation)
+            rig = R.PsArm(L.model_shapes, L.workers, L.shards, L.colocate)
+            kind, what = "reference", ("rdmaflow Session(PS graph of build_ps_workload with "
+                                       "these shapes, zerocp).run(1), XOR ApplyGrad")
+        else:
+            rig = port.PsRig(L.model_shapes, L.workers, L.shards, L.colocate, seed=0, op=op,
+                             lr=0.01)
+            kind, what = "port", ("oracle/port.py PsRig: chunked static pushes, PCG64 "
+                                  "GenGrad, meta + chunked pulls, ApplyGrad")
         n, t0 = 0, time.perf_counter()
         while True:
             rig.step()
@@ -1155,11 +1209,10 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
             if dt > 2.0 or n >= 200:
                 break
         out["cpu_baseline"] = {"value": round(n / dt, 4), "unit": "steps/s", "cores": 1,
-                               "kind": "port",
-                               "sample": f"{n} PS iteration(s) of the same config "
-                                         "(oracle/port.py PsRig: chunked static pushes, "
-                                         "PCG64 GenGrad, meta + chunked pulls, ApplyGrad), "
-                                         f"{dt:.1f} s, host cpu_count={os.cpu_count()}"}
+                               "kind": kind,
+                               "sample": f"{n} steady PS iteration(s) of the same config "
+                                         f"({what}), {dt:.1f} s, host cpu_count="
+                                         f"{os.cpu_count()}"}
     return out
 
 
@@ -1272,11 +1325,10 @@ def main() -> int:
                                       "one GPU shares one ceiling)")},
     }
     if rank == 0 and world == 1 and not args.no_cpu:
-        gbps, n, dt = cpu_reference(S, min_seconds=args.cpu_seconds)
+        gbps, n, dt, kind, what = cpu_reference(S, min_seconds=args.cpu_seconds)
         line["cpu_baseline"] = {
-            "value": round(gbps, 4), "unit": "GB/s", "cores": 1, "kind": "port",
-            "sample": f"{n} steps x {S} B static Send/Recv (oracle/port.py MicrobenchRig: "
-                      f"ascending 1-4096 B chunk delivery + flag poll + max), {dt:.1f} s, "
+            "value": round(gbps, 4), "unit": "GB/s", "cores": 1, "kind": kind,
+            "sample": f"{n} steps x {S} B static Send/Recv ({what}), {dt:.1f} s, "
                       f"host cpu_count={os.cpu_count()}"}
     def section(key, fn):
         """Secondary results never cost the headline line: a failing section

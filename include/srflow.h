@@ -141,6 +141,12 @@ int srf_graph_end(srf_stream_t stream, void **graph_exec);
 int srf_graph_launch(void *graph_exec, srf_stream_t stream);
 int srf_graph_destroy(void *graph_exec);
 int srf_stream_wait_event(srf_stream_t stream, srf_event_t ev);
+/* Order the space's own stream after an event (BufferRef frees: a block
+ * freed while device work may still use it carries a fence event; the next
+ * allocation that reuses those bytes makes the space's stream wait on it -
+ * memspace.py:315-357 frees at refcount 0, which stays host-immediate so the
+ * first-fit addresses equal the reference's). */
+int srf_space_wait_event(srf_space_t space, srf_event_t ev);
 int srf_timing_event_create(srf_space_t space, srf_event_t *out);
 int srf_event_record_on(srf_event_t ev, srf_stream_t stream);
 int srf_event_elapsed_ms(srf_event_t start, srf_event_t end, float *ms);
@@ -372,10 +378,46 @@ int srf_rpc_transfer(srf_space_t src, uint64_t meta_addr, uint32_t meta_len,
                      uint64_t meta_out_addr, uint64_t tensor_out_addr, uint64_t msg_id,
                      srf_stream_t src_stream, srf_stream_t dst_stream);
 
+/* MatMul compute kind of Session graphs (graph.py:371-372) on the device,
+ * bit-identical to numpy's `a @ b`: an ascending-k FMA chain per output
+ * (floats), wrapping sums (integers).  Plain device pointers (row-major
+ * a[m,k], b[k,n], c[m,n]), element type code as wire.ElemType (0 F32, 1 F64,
+ * 2 I32, 3 I64, 4 U8), launched on cuda_stream. */
+int srf_matmul(int elem, uint64_t a_ptr, uint64_t b_ptr, uint64_t c_ptr, uint64_t m, uint64_t k,
+               uint64_t n, void *cuda_stream);
+
 /* ReduceMax consumer of the microbenchmark (graph.py:378-382) on the
  * receiving GPU: out_addr receives max over n fp32 at in_addr. */
 int srf_reduce_max_f32(srf_space_t space, uint64_t in_addr, uint64_t n,
                        uint64_t out_addr, srf_stream_t stream);
+
+/* ---- pipelined static edge (EXTENSION of static placement) ---------------
+ * One edge, `slots` pre-placed receive regions (slot i = payload || flag at
+ * dst_addr + i * slot_stride, allocated and published by the receiver like
+ * the reference's static region, analyzer.py:149-220).  srf_edge_send queues
+ * `rounds` transfers in ONE persistent launch: round j (counting continues
+ * across calls) puts payload j % nsrc (src_addr + (j % nsrc) * src_stride)
+ * into slot j % slots with the reference's per-round protocol - the credit
+ * (the slot's flag was cleared by its consumer, runtime/protocol.py:102-111),
+ * the body, the flag byte released last (fabric.py:349-356) - but rounds
+ * overlap: chunks of round j+1 stream while round j is published and
+ * consumed (device_stream.cuh).  srf_edge_consume is the receiver's
+ * StaticReceiver.poll for rounds [first, first + rounds) on the device (one
+ * CTA; mode 1 also stores a weighted byte checksum of every round's payload
+ * at sums_addr, 8 B per round).  Creation checks registration and token and
+ * bounds of the whole source and slot spans, like srf_put per verb. */
+typedef struct srf_edge *srf_edge_t;
+int srf_edge_create(srf_space_t src_space, uint64_t src_addr, uint64_t src_token,
+                    uint64_t nbytes, uint32_t nsrc, uint64_t src_stride,
+                    srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
+                    uint32_t slots, uint64_t slot_stride, srf_edge_t *out);
+int srf_edge_info(srf_edge_t edge, uint64_t *chunk, uint32_t *nchunks, int *ctas,
+                  uint64_t *next_round);
+int srf_edge_send(srf_edge_t edge, uint32_t rounds, srf_stream_t stream, srf_space_t src_space);
+int srf_edge_consume(srf_space_t receiver, uint64_t slots_addr, uint32_t slots,
+                     uint64_t slot_stride, uint64_t nbytes, uint64_t first_round,
+                     uint32_t rounds, int mode, uint64_t sums_addr, srf_stream_t stream);
+int srf_edge_destroy(srf_edge_t edge);
 
 #ifdef __cplusplus
 }

@@ -61,6 +61,14 @@ int srf_tune(int knob, int value) {
       if (value < 1) return fail(SRF_E_INVALID_CONFIG, "put_timeout_ms >= 1");
       g_put_timeout_ns = (uint64_t)value * 1000000ull;
       return SRF_OK;
+    case 9:
+      if (value < 1 || value > 4) return fail(SRF_E_INVALID_CONFIG, "edge_ctas_per_sm 1..4");
+      g_edge_ctas_per_sm = value;
+      return SRF_OK;
+    case 10:
+      if (value < 0) return fail(SRF_E_INVALID_CONFIG, "edge_chunk_kib >= 0");
+      g_edge_chunk = (uint64_t)value;
+      return SRF_OK;
     default:
       return fail(SRF_E_INVALID_CONFIG, "unknown knob %d", knob);
   }

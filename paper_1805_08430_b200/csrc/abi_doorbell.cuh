@@ -68,12 +68,14 @@ int srf_flag_read(srf_space_t sp, uint64_t tail_addr, uint64_t len, void *host_o
 
 // Clear a receive flag (StaticReceiver/DynReceiver.poll): shadow now, device
 // byte asynchronously on the space's stream; the next srf_put into the region
-// waits for that clear.
+// waits for that clear.  An exported space's producers live in other
+// processes and cannot wait on that event: the device byte is written
+// synchronously there (their credit check reads it over NVLink).
 int srf_flag_clear(srf_space_t sp, uint64_t tail_addr) {
   DeviceGuard device_guard;
   int rc = check_raw(sp, tail_addr, 1, "flag");
   if (rc) return rc;
-  if (sp->db) {
+  if (sp->db && !sp->exported) {
     std::lock_guard<std::mutex> g(sp->mu);
     auto it = sp->db->find(tail_addr);
     if (it != sp->db->end()) {
@@ -182,6 +184,35 @@ int srf_stream_wait_event(srf_stream_t st, srf_event_t ev) {
   CUDA_TRY(cudaSetDevice(st->device));
   CUDA_TRY(cudaStreamWaitEvent(st->s, ev->e, 0));
   return SRF_OK;
+}
+
+int srf_space_wait_event(srf_space_t sp, srf_event_t ev) {
+  DeviceGuard device_guard;
+  CUDA_TRY(cudaSetDevice(sp->stream->device));
+  CUDA_TRY(cudaStreamWaitEvent(sp->stream->s, ev->e, 0));
+  return SRF_OK;
+}
+
+int srf_matmul(int elem, uint64_t a_ptr, uint64_t b_ptr, uint64_t c_ptr, uint64_t m, uint64_t k,
+               uint64_t n, void *cuda_stream) {
+  DeviceGuard device_guard;
+  if (m * n == 0) return SRF_OK;
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  const unsigned grid = (unsigned)((m * n + 255) / 256);
+  switch (elem) {
+    case 0: k_matmul<float><<<grid, 256, 0, s>>>((const float *)a_ptr, (const float *)b_ptr,
+                                                   (float *)c_ptr, m, k, n); break;
+    case 1: k_matmul<double><<<grid, 256, 0, s>>>((const double *)a_ptr, (const double *)b_ptr,
+                                                    (double *)c_ptr, m, k, n); break;
+    case 2: k_matmul<int32_t><<<grid, 256, 0, s>>>((const int32_t *)a_ptr, (const int32_t *)b_ptr,
+                                                     (int32_t *)c_ptr, m, k, n); break;
+    case 3: k_matmul<int64_t><<<grid, 256, 0, s>>>((const int64_t *)a_ptr, (const int64_t *)b_ptr,
+                                                     (int64_t *)c_ptr, m, k, n); break;
+    case 4: k_matmul<uint8_t><<<grid, 256, 0, s>>>((const uint8_t *)a_ptr, (const uint8_t *)b_ptr,
+                                                     (uint8_t *)c_ptr, m, k, n); break;
+    default: return fail(SRF_E_INVALID_CONFIG, "unknown element type %d", elem);
+  }
+  return launch_check("k_matmul");
 }
 
 int srf_timing_event_create(srf_space_t sp, srf_event_t *out) {

@@ -1,0 +1,143 @@
+// abi_stream.cuh - part of libsrflow (included by srflow.cu, one translation unit).
+// C ABI: the pipelined static edge (device_stream.cuh).
+
+struct srf_edge {
+  int device;
+  StreamEdgeArgs a;        // fixed fields; first_round / rounds set per launch
+  unsigned int *state;     // released[slots] | arrival[slots] | credit[slots] | claim | exit
+  uint64_t next_round;
+  int ctas;
+};
+
+
+extern "C" {
+
+int srf_edge_create(srf_space_t src_space, uint64_t src_addr, uint64_t src_token,
+                    uint64_t nbytes, uint32_t nsrc, uint64_t src_stride,
+                    srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
+                    uint32_t slots, uint64_t slot_stride, srf_edge_t *out) {
+  DeviceGuard device_guard;
+  if (nbytes < 1) return fail(SRF_E_INVALID_LENGTH, "zero-length edge");
+  if (slots < 1 || nsrc < 1) return fail(SRF_E_INVALID_CONFIG, "slots and nsrc must be >= 1");
+  if (slot_stride < nbytes + 1 || (nsrc > 1 && src_stride < nbytes))
+    return fail(SRF_E_INVALID_CONFIG, "slot/source stride shorter than the payload");
+  if (src_space->imported) return fail(SRF_E_INVALID_CONFIG, "the sender's payloads are local");
+  const uint64_t src_span = (uint64_t)(nsrc - 1) * src_stride + nbytes;
+  const uint64_t dst_span = (uint64_t)(slots - 1) * slot_stride + nbytes + 1;
+  {
+    std::lock_guard<std::mutex> g(src_space->mu);
+    int rc = check_registered_locked(src_space, src_addr, src_span, src_token);
+    if (rc) return rc;
+  }
+  {
+    std::lock_guard<std::mutex> g(dst_space->mu);
+    int rc = check_remote_locked(dst_space, dst_addr, dst_span, dst_token);
+    if (rc) return rc;
+  }
+  srf_edge *e = new srf_edge();
+  e->device = src_space->device;
+  memset(&e->a, 0, sizeof e->a);
+  e->a.src = src_space->base + src_addr;
+  e->a.src_stride = src_stride;
+  e->a.nsrc = nsrc;
+  e->a.dst = dst_space->base + dst_addr;
+  e->a.slot_stride = slot_stride;
+  e->a.slots = slots;
+  e->a.nbytes = nbytes;
+  // chunk: ~2 items per CTA per round for mid sizes, 64-256 KiB for large
+  // payloads (amortises the claim, credit check and system-scope arrival)
+  const int sms = sm_count_of(e->device);
+  e->ctas = std::max(1, sms * g_edge_ctas_per_sm);
+  uint64_t chunk = g_edge_chunk ? (g_edge_chunk << 10)
+                                : std::min<uint64_t>(256 << 10,
+                                                     std::max<uint64_t>(16 << 10,
+                                                                        nbytes / (uint64_t)e->ctas));
+  chunk = (chunk + 4095) & ~4095ull;
+  if (chunk > nbytes) chunk = nbytes;
+  e->a.chunk = chunk;
+  e->a.nchunks = (uint32_t)((nbytes + chunk - 1) / chunk);
+  e->a.sys = (g_force_sys || dst_space->imported || dst_space->device != src_space->device) ? 1 : 0;
+  e->a.timeout_ns = g_put_timeout_ns;
+  e->a.err = src_space->err;
+  e->next_round = 0;
+  CUDA_TRY(cudaSetDevice(e->device));
+  const size_t words = 3 * (size_t)slots + 2;
+  cudaError_t err = cudaMalloc(&e->state, words * sizeof(unsigned));
+  if (err == cudaSuccess) err = cudaMemset(e->state, 0, words * sizeof(unsigned));
+  if (err == cudaSuccess) err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) {
+    delete e;
+    return fail(SRF_E_DEVICE, "edge state: %s", cudaGetErrorString(err));
+  }
+  e->a.released = e->state;
+  e->a.arrival = e->state + slots;
+  e->a.credit = e->state + 2 * slots;
+  e->a.claim = e->state + 3 * slots;
+  e->a.exit_count = e->state + 3 * slots + 1;
+  *out = e;
+  return SRF_OK;
+}
+
+int srf_edge_info(srf_edge_t e, uint64_t *chunk, uint32_t *nchunks, int *ctas,
+                  uint64_t *next_round) {
+  if (chunk) *chunk = e->a.chunk;
+  if (nchunks) *nchunks = e->a.nchunks;
+  if (ctas) *ctas = e->ctas;
+  if (next_round) *next_round = e->next_round;
+  return SRF_OK;
+}
+
+int srf_edge_send(srf_edge_t e, uint32_t rounds, srf_stream_t st, srf_space_t src_space) {
+  DeviceGuard device_guard;
+  if (rounds == 0) return SRF_OK;
+  if ((uint64_t)rounds * e->a.nchunks > 0xFFFFFFFFull)
+    return fail(SRF_E_INVALID_CONFIG, "too many work items in one launch");
+  srf_stream *s = stream_or_default(src_space, st);
+  if (s->device != e->device) return fail(SRF_E_INVALID_CONFIG, "stream on another GPU");
+  StreamEdgeArgs a = e->a;
+  a.first_round = e->next_round;
+  a.rounds = rounds;
+  const uint64_t items = (uint64_t)rounds * a.nchunks;
+  const int grid = (int)std::min<uint64_t>((uint64_t)e->ctas, items);
+  CUDA_TRY(cudaSetDevice(e->device));
+  k_put_stream<<<grid, 512, 0, s->s>>>(a);
+  int rc = launch_check("k_put_stream");
+  if (rc) return rc;
+  e->next_round += rounds;
+  return SRF_OK;
+}
+
+int srf_edge_consume(srf_space_t rcv, uint64_t slots_addr, uint32_t slots, uint64_t slot_stride,
+                     uint64_t nbytes, uint64_t first_round, uint32_t rounds, int mode,
+                     uint64_t sums_addr, srf_stream_t st) {
+  DeviceGuard device_guard;
+  if (rcv->imported) return fail(SRF_E_INVALID_CONFIG, "the receiver consumes its own slots");
+  if (slots < 1 || slot_stride < nbytes + 1)
+    return fail(SRF_E_INVALID_CONFIG, "bad slot geometry");
+  int rc = check_raw(rcv, slots_addr, (uint64_t)(slots - 1) * slot_stride + nbytes + 1, "slots");
+  if (rc) return rc;
+  if (mode == 1) {
+    rc = check_raw(rcv, sums_addr, 8ull * rounds, "checksums");
+    if (rc) return rc;
+    if (sums_addr % 8) return fail(SRF_E_INVALID_CONFIG, "checksums must be 8-B aligned");
+  }
+  if (rounds == 0) return SRF_OK;
+  srf_stream *s = stream_or_default(rcv, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  k_consume_stream<<<1, mode == 1 ? 1024 : 32, 0, s->s>>>(
+      rcv->base + slots_addr, slot_stride, slots, nbytes, first_round, rounds, mode,
+      (unsigned long long *)(rcv->base + sums_addr), g_put_timeout_ns, rcv->err);
+  return launch_check("k_consume_stream");
+}
+
+int srf_edge_destroy(srf_edge_t e) {
+  DeviceGuard device_guard;
+  if (!e) return SRF_OK;
+  cudaSetDevice(e->device);
+  cudaDeviceSynchronize();
+  cudaFree(e->state);
+  delete e;
+  return SRF_OK;
+}
+
+}  // extern "C"

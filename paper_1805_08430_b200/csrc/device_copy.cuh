@@ -122,17 +122,42 @@ __device__ __forceinline__ void st_v8(u256 *p, const u256 &r) {
                : "memory");
 }
 
-template <typename V>
+// Coherent (L2, .cg) 256-bit load: for sources written earlier in the same
+// launch (the multi-iteration PS exchange pushes variables its own apply
+// units updated) or by another agent while the kernel runs (RPC ring slots).
+// The non-coherent .nc path is only valid for data read-only for the launch.
+__device__ __forceinline__ u256 ld_cg_v8(const u256 *p) {
+  u256 r;
+  asm volatile("ld.global.cg.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]),
+                 "=r"(r.v[5]), "=r"(r.v[6]), "=r"(r.v[7])
+               : "l"(p));
+  return r;
+}
+
+// Source loads: kCoh = false -> read-only-for-the-launch paths (.nc / __ldg);
+// kCoh = true -> coherent at L2 (__ldcg / ld.global.cg).
+template <typename V, bool kCoh = false>
 __device__ __forceinline__ V ld_stream(const V *p) {
+  if (kCoh) return __ldcg(p);
   return __ldg(p);
 }
 template <>
-__device__ __forceinline__ u256 ld_stream<u256>(const u256 *p) {
+__device__ __forceinline__ u256 ld_stream<u256, false>(const u256 *p) {
   return ld_v8(p);
 }
 template <>
-__device__ __forceinline__ uint4 ld_stream<uint4>(const uint4 *p) {
+__device__ __forceinline__ u256 ld_stream<u256, true>(const u256 *p) {
+  return ld_cg_v8(p);
+}
+template <>
+__device__ __forceinline__ uint4 ld_stream<uint4, false>(const uint4 *p) {
   return ld_stream_v4(p);
+}
+template <bool kCoh>
+__device__ __forceinline__ uint8_t ld_byte(const uint8_t *p) {
+  if (kCoh) return (uint8_t)__ldcg((const unsigned char *)p);
+  return *p;
 }
 template <typename V>
 __device__ __forceinline__ void st_plain(V *p, const V &v) {
@@ -150,7 +175,7 @@ __device__ __forceinline__ void st_plain<u256>(u256 *p, const u256 &v) {
 // Grid-wide copy of nv vectors: all loads of an unrolled batch are issued
 // before its stores so every thread keeps U requests in flight (the latency of
 // a peer access is ~2000 cycles, B300_MICROARCH.md "NVLink").
-template <typename V, int U>
+template <typename V, int U, bool kCoh = false>
 __device__ __forceinline__ void vec_copy(V *__restrict__ dst,
                                          const V *__restrict__ src,
                                          uint64_t nv, uint64_t t,
@@ -159,11 +184,11 @@ __device__ __forceinline__ void vec_copy(V *__restrict__ dst,
   for (; i + (uint64_t)(U - 1) * nth < nv; i += (uint64_t)U * nth) {
     V r[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) r[u] = ld_stream<V>(src + i + u * nth);
+    for (int u = 0; u < U; ++u) r[u] = ld_stream<V, kCoh>(src + i + u * nth);
 #pragma unroll
     for (int u = 0; u < U; ++u) st_plain<V>(dst + i + u * nth, r[u]);
   }
-  for (; i < nv; i += nth) st_plain<V>(dst + i, ld_stream<V>(src + i));
+  for (; i < nv; i += nth) st_plain<V>(dst + i, ld_stream<V, kCoh>(src + i));
 }
 
 __device__ __forceinline__ u256 pack8(const uint2 (&a)[4]) {
@@ -183,7 +208,7 @@ __device__ __forceinline__ u256 pack8(const uint2 (&a)[4]) {
 // profiles/r1_align_probe.txt) - and the source is read at its own alignment
 // class (8-B, 4-B, or aligned words funnel-shifted) and reassembled in
 // registers.  U chunks of 32 B in flight per thread.
-template <int U>
+template <int U, bool kCoh = false>
 __device__ void copy_dst_aligned(uint8_t *dst, const uint8_t *src, uint64_t n, uint64_t t,
                                  uint64_t nth) {
   uint64_t head = (32 - ((uintptr_t)dst & 31)) & 31;
@@ -200,14 +225,14 @@ __device__ void copy_dst_aligned(uint8_t *dst, const uint8_t *src, uint64_t n, u
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) a[u][k] = __ldg(S8 + 4 * (i + u * nth) + k);
+        for (int k = 0; k < 4; ++k) a[u][k] = ld_stream<uint2, kCoh>(S8 + 4 * (i + u * nth) + k);
 #pragma unroll
       for (int u = 0; u < U; ++u) st_v8(D + i + u * nth, pack8(a[u]));
     }
     for (; i < nv; i += nth) {
       uint2 a[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) a[k] = __ldg(S8 + 4 * i + k);
+      for (int k = 0; k < 4; ++k) a[k] = ld_stream<uint2, kCoh>(S8 + 4 * i + k);
       st_v8(D + i, pack8(a));
     }
   } else {
@@ -224,7 +249,7 @@ __device__ void copy_dst_aligned(uint8_t *dst, const uint8_t *src, uint64_t n, u
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int k = 0; k < 9; ++k)
-          w[u][k] = (k < 8 || m) ? __ldg(sw + 8 * (i + u * nth) + k) : 0u;
+          w[u][k] = (k < 8 || m) ? ld_stream<uint32_t, kCoh>(sw + 8 * (i + u * nth) + k) : 0u;
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         u256 r;
@@ -236,22 +261,22 @@ __device__ void copy_dst_aligned(uint8_t *dst, const uint8_t *src, uint64_t n, u
     for (; i < nv; i += nth) {
       uint32_t w[9];
 #pragma unroll
-      for (int k = 0; k < 9; ++k) w[k] = (k < 8 || m) ? __ldg(sw + 8 * i + k) : 0u;
+      for (int k = 0; k < 9; ++k) w[k] = (k < 8 || m) ? ld_stream<uint32_t, kCoh>(sw + 8 * i + k) : 0u;
       u256 r;
 #pragma unroll
       for (int k = 0; k < 8; ++k) r.v[k] = __funnelshift_r(w[k], w[k + 1], 8 * m);
       st_v8(D + i, r);
     }
   }
-  for (uint64_t j = t; j < head; j += nth) dst[j] = src[j];
-  for (uint64_t j = head + 32 * nv + t; j < n; j += nth) dst[j] = src[j];
+  for (uint64_t j = t; j < head; j += nth) dst[j] = ld_byte<kCoh>(src + j);
+  for (uint64_t j = head + 32 * nv + t; j < n; j += nth) dst[j] = ld_byte<kCoh>(src + j);
 }
 
 // Source-aligned twin for pulls (the source is a peer's memory): whole
 // aligned 32-B sector loads, stores at the destination's alignment (8-B or
 // 4-B words; callers guarantee (dst - src) % 4 == 0).  A pull whose source
 // sat 8 B off a sector ran at 571 GB/s instead of 736 (r1_align_probe.txt).
-template <int U>
+template <int U, bool kCoh = false>
 __device__ void copy_src_aligned(uint8_t *dst, const uint8_t *src, uint64_t n, uint64_t t,
                                  uint64_t nth) {
   uint64_t head = (32 - ((uintptr_t)src & 31)) & 31;
@@ -264,7 +289,7 @@ __device__ void copy_src_aligned(uint8_t *dst, const uint8_t *src, uint64_t n, u
   for (; i + (uint64_t)(U - 1) * nth < nv; i += (uint64_t)U * nth) {
     u256 r[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) r[u] = ld_v8(S + i + u * nth);
+    for (int u = 0; u < U; ++u) r[u] = ld_stream<u256, kCoh>(S + i + u * nth);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       if (w8) {
@@ -279,7 +304,7 @@ __device__ void copy_src_aligned(uint8_t *dst, const uint8_t *src, uint64_t n, u
     }
   }
   for (; i < nv; i += nth) {
-    const u256 r = ld_v8(S + i);
+    const u256 r = ld_stream<u256, kCoh>(S + i);
     if (w8) {
       uint2 *D8 = (uint2 *)dp + 4 * i;
 #pragma unroll
@@ -290,8 +315,8 @@ __device__ void copy_src_aligned(uint8_t *dst, const uint8_t *src, uint64_t n, u
       for (int k = 0; k < 8; ++k) D4[k] = r.v[k];
     }
   }
-  for (uint64_t j = t; j < head; j += nth) dst[j] = src[j];
-  for (uint64_t j = head + 32 * nv + t; j < n; j += nth) dst[j] = src[j];
+  for (uint64_t j = t; j < head; j += nth) dst[j] = ld_byte<kCoh>(src + j);
+  for (uint64_t j = head + 32 * nv + t; j < n; j += nth) dst[j] = ld_byte<kCoh>(src + j);
 }
 
 // Copy n bytes with the widest vector both pointers allow.  Arena blocks are
@@ -302,7 +327,7 @@ __device__ void copy_src_aligned(uint8_t *dst, const uint8_t *src, uint64_t n, u
 // kSectors = false compiles only the co-aligned classes (PS blocks).
 __constant__ int g_vec32 = 1;  // knob 5: 32-B vectors when co-aligned mod 32
 
-template <int U16 = 4, bool kSectors = true>
+template <int U16 = 4, bool kSectors = true, bool kCoh = false>
 __device__ void copy_bytes_grid(uint8_t *dst, const uint8_t *src, uint64_t n,
                                 uint64_t t, uint64_t nth, bool align_dst = true) {
   if (n == 0) return;
@@ -310,11 +335,11 @@ __device__ void copy_bytes_grid(uint8_t *dst, const uint8_t *src, uint64_t n,
   uint64_t head, nv;
   if (kSectors && g_vec32 && ((d ^ s) & 31) != 0 && n >= 4096) {
     if (align_dst) {
-      copy_dst_aligned<(U16 > 4 ? U16 / 2 : 2)>(dst, src, n, t, nth);
+      copy_dst_aligned<(U16 > 4 ? U16 / 2 : 2), kCoh>(dst, src, n, t, nth);
       return;
     }
     if (((d ^ s) & 3) == 0) {
-      copy_src_aligned<(U16 > 4 ? U16 / 2 : 2)>(dst, src, n, t, nth);
+      copy_src_aligned<(U16 > 4 ? U16 / 2 : 2), kCoh>(dst, src, n, t, nth);
       return;
     }
   }
@@ -322,28 +347,28 @@ __device__ void copy_bytes_grid(uint8_t *dst, const uint8_t *src, uint64_t n,
     head = (32 - (d & 31)) & 31;
     if (head > n) head = n;
     nv = (n - head) / 32;
-    vec_copy<u256, (U16 > 4 ? U16 / 2 : 2)>((u256 *)(dst + head), (const u256 *)(src + head),
+    vec_copy<u256, (U16 > 4 ? U16 / 2 : 2), kCoh>((u256 *)(dst + head), (const u256 *)(src + head),
                                             nv, t, nth);
     nv *= 32;
   } else if (((d ^ s) & 15) == 0) {
     head = (16 - (d & 15)) & 15;
     if (head > n) head = n;
     nv = (n - head) / 16;
-    vec_copy<uint4, U16>((uint4 *)(dst + head), (const uint4 *)(src + head), nv,
+    vec_copy<uint4, U16, kCoh>((uint4 *)(dst + head), (const uint4 *)(src + head), nv,
                          t, nth);
     nv *= 16;
   } else if (((d ^ s) & 7) == 0) {
     head = (8 - (d & 7)) & 7;
     if (head > n) head = n;
     nv = (n - head) / 8;
-    vec_copy<uint2, 8>((uint2 *)(dst + head), (const uint2 *)(src + head), nv,
+    vec_copy<uint2, 8, kCoh>((uint2 *)(dst + head), (const uint2 *)(src + head), nv,
                        t, nth);
     nv *= 8;
   } else if (((d ^ s) & 3) == 0) {
     head = (4 - (d & 3)) & 3;
     if (head > n) head = n;
     nv = (n - head) / 4;
-    vec_copy<uint32_t, 8>((uint32_t *)(dst + head),
+    vec_copy<uint32_t, 8, kCoh>((uint32_t *)(dst + head),
                           (const uint32_t *)(src + head), nv, t, nth);
     nv *= 4;
   } else {
@@ -365,18 +390,20 @@ __device__ void copy_bytes_grid(uint8_t *dst, const uint8_t *src, uint64_t n,
       uint32_t a[4], b[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        a[u] = __ldg(sw + j + u * nth);
-        b[u] = __ldg(sw + j + u * nth + 1);
+        a[u] = ld_stream<uint32_t, kCoh>(sw + j + u * nth);
+        b[u] = ld_stream<uint32_t, kCoh>(sw + j + u * nth + 1);
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) dw[j + u * nth] = __funnelshift_r(a[u], b[u], 8 * m);
     }
-    for (; j < nv; j += nth) dw[j] = __funnelshift_r(__ldg(sw + j), __ldg(sw + j + 1), 8 * m);
+    for (; j < nv; j += nth)
+      dw[j] = __funnelshift_r(ld_stream<uint32_t, kCoh>(sw + j), ld_stream<uint32_t, kCoh>(sw + j + 1),
+                              8 * m);
     nv *= 4;
   }
   // scalar head and tail bytes
-  for (uint64_t i = t; i < head; i += nth) dst[i] = src[i];
-  for (uint64_t i = head + nv + t; i < n; i += nth) dst[i] = src[i];
+  for (uint64_t i = t; i < head; i += nth) dst[i] = ld_byte<kCoh>(src + i);
+  for (uint64_t i = head + nv + t; i < n; i += nth) dst[i] = ld_byte<kCoh>(src + i);
 }
 
 struct Seg {

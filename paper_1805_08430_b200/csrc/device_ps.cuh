@@ -261,7 +261,7 @@ __device__ __forceinline__ void put_unit(const BatchPut *descs, int n, uint32_t 
                                          unsigned int *counters, uint64_t timeout_ns, int *err,
                                          int sys, const unsigned int *wait_done = nullptr,
                                          const int *wait_index = nullptr, uint32_t k = 0,
-                                         unsigned int *seq = nullptr) {
+                                         unsigned int *seq = nullptr, bool coherent_src = false) {
   __shared__ int s_desc, s_last;
   {
     if (threadIdx.x == 0) {
@@ -279,9 +279,17 @@ __device__ __forceinline__ void put_unit(const BatchPut *descs, int n, uint32_t 
       }
       __syncthreads();
     }
-    // (PS blocks are 256-B aligned: always co-aligned, no destination realignment)
-    copy_bytes_grid<8, false>(d.dst, d.src, d.body, (uint64_t)lb * blockDim.x + threadIdx.x,
-                              (uint64_t)d.cta_count * blockDim.x);
+    // (PS blocks are 256-B aligned: always co-aligned, no destination realignment).
+    // Coherent source loads when the source may have been written earlier in
+    // this launch: a variable updated by this launch's apply units (several
+    // iterations per exchange launch) or a gradient produced in-device
+    // (src_ready) - .nc loads are only defined for launch-read-only data.
+    const uint64_t t0 = (uint64_t)lb * blockDim.x + threadIdx.x;
+    const uint64_t nt = (uint64_t)d.cta_count * blockDim.x;
+    if (coherent_src || d.src_ready)
+      copy_bytes_grid<8, false, true>(d.dst, d.src, d.body, t0, nt);
+    else
+      copy_bytes_grid<8, false>(d.dst, d.src, d.body, t0, nt);
     __syncthreads();
     if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, sys);
     __syncthreads();
@@ -299,9 +307,11 @@ __device__ __forceinline__ void put_unit(const BatchPut *descs, int n, uint32_t 
 
 __device__ __forceinline__ void put_batch_units(const BatchPut *descs, int n,
                                                 uint32_t total_units, unsigned int *counters,
-                                                uint64_t timeout_ns, int *err, int sys) {
+                                                uint64_t timeout_ns, int *err, int sys,
+                                                bool coherent_src = false) {
   for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x)
-    put_unit(descs, n, u, counters, timeout_ns, err, sys);
+    put_unit(descs, n, u, counters, timeout_ns, err, sys, nullptr, nullptr, 0, nullptr,
+             coherent_src);
 }
 
 __device__ __forceinline__ void gen_unit(const BatchGen *descs, int n, uint32_t u,
@@ -556,7 +566,9 @@ struct PsPersistArgs {
 __global__ void __launch_bounds__(256) k_ps_persistent(const __grid_constant__ PsPersistArgs a) {
   cg::grid_group grid = cg::this_grid();
   for (uint32_t i = 0; i < a.iters; ++i) {
-    if (a.push) put_batch_units(a.push, a.npush, a.upush, a.cpush, a.timeout_ns, a.err, a.sys);
+    // (iteration i pushes variables iteration i-1 of this launch updated)
+    if (a.push)
+      put_batch_units(a.push, a.npush, a.upush, a.cpush, a.timeout_ns, a.err, a.sys, true);
     grid.sync();
     if (a.gen)
       gen_batch_units(a.gen, a.ngen, a.ugen, a.cgen, a.seed, a.it0 + i, nullptr, a.regen,
@@ -619,7 +631,7 @@ __global__ void __launch_bounds__(512, kMinBlocks) k_ps_exchange(const __grid_co
     const ExItem x = a.items[i - k * a.nitems];
     if (x.kind == 0)
       put_unit(a.push, a.npush, x.unit, a.cpush, a.timeout_ns, a.err, a.push_sys, a.done,
-               a.push_done, k, a.seq_push);
+               a.push_done, k, a.seq_push, true);
     else if (x.kind == 1)
       gen_unit(a.gen, a.ngen, x.unit, a.cgen, a.seed, a.iteration + k, a.regen, 1,
                a.timeout_ns, a.err, a.gen_sys, k, a.seq_gen);

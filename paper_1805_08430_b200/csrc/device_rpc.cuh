@@ -30,8 +30,10 @@ struct RpcArgs {
 // 64 threads (a warp pair) move one fragment
 static constexpr int kSlotThreads = 64;
 
+// Coherent source loads: ring slots and staging slots are rewritten by the
+// other side (or this warp pair) every round within one launch.
 __device__ __forceinline__ void slot_copy(uint8_t *dst, const uint8_t *src, uint64_t n) {
-  copy_bytes_grid<4>(dst, src, n, threadIdx.x % kSlotThreads, kSlotThreads);
+  copy_bytes_grid<4, true, true>(dst, src, n, threadIdx.x % kSlotThreads, kSlotThreads);
 }
 
 __device__ __forceinline__ void slot_sync() {
@@ -174,4 +176,46 @@ __global__ void __launch_bounds__(256) k_reduce_max(const float *x, uint64_t n,
     *out = (n == 0) ? 0.0f : r;
     atomicExch(counter, 0u);
   }
+}
+
+// ---------------------------------------------------------------------------
+// MatMul compute kind of the Session's graphs (graph.py:371-372: numpy
+// `a @ b`), bit-identical to numpy: numpy's float matmul (OpenBLAS sgemm /
+// dgemm) accumulates each output as an ascending-k FMA chain from 0 (checked
+// for k <= 64 in tests), integer matmul wraps in the element type.  Not on
+// the transfer path (compute kinds are graph plumbing): one
+// thread per output element.
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T mm_step(T acc, T a, T b);
+template <>
+__device__ __forceinline__ float mm_step<float>(float acc, float a, float b) {
+  return __fmaf_rn(a, b, acc);
+}
+template <>
+__device__ __forceinline__ double mm_step<double>(double acc, double a, double b) {
+  return __fma_rn(a, b, acc);
+}
+template <>
+__device__ __forceinline__ int32_t mm_step<int32_t>(int32_t acc, int32_t a, int32_t b) {
+  return (int32_t)((uint32_t)acc + (uint32_t)a * (uint32_t)b);
+}
+template <>
+__device__ __forceinline__ int64_t mm_step<int64_t>(int64_t acc, int64_t a, int64_t b) {
+  return (int64_t)((uint64_t)acc + (uint64_t)a * (uint64_t)b);
+}
+template <>
+__device__ __forceinline__ uint8_t mm_step<uint8_t>(uint8_t acc, uint8_t a, uint8_t b) {
+  return (uint8_t)(acc + a * b);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_matmul(const T *a, const T *b, T *c, uint64_t m,
+                                                uint64_t k, uint64_t n) {
+  const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= m * n) return;
+  const uint64_t i = idx / n, j = idx - i * n;
+  T acc = T(0);
+  for (uint64_t t = 0; t < k; ++t) acc = mm_step<T>(acc, a[i * k + t], b[t * n + j]);
+  c[idx] = acc;
 }

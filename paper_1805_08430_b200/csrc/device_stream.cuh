@@ -1,0 +1,132 @@
+// device_stream.cuh - part of libsrflow (included by srflow.cu, one translation unit).
+// Pipelined static edge: many static-placement transfers of one edge in ONE
+// persistent launch (EXTENSION of the reference's static placement).
+//
+// The reference's static edge has one pre-placed receive region per edge and
+// a flag credit (runtime/protocol.py:49-138, analyzer.py:149-220), so round
+// k+1 cannot start before round k was consumed, and on the GPU every round
+// pays a kernel launch, a grid-wide arrival, a system-scope release and the
+// consumer's poll (~9 us over NVLink) - 4 MiB rounds reached only
+// 0.32 of the link.  Here the receiver pre-places `slots` regions for the
+// edge (slot i = payload || flag at dst + i * slot_stride); round j writes
+// slot j % slots; each slot keeps the reference protocol exactly (flag byte
+// released last, consumer clears it = the credit).  The sender kernel is a
+// persistent work queue of (round, chunk) items claimed in order: a CTA copies
+// one chunk and arrives on the slot's counter; the last arriver releases the
+// slot's flag (st.release.sys) - no grid barrier, no kernel boundary between
+// rounds, so chunks of round j+1 stream while round j's tail is published and
+// consumed.  Item (j, c) waits only on (a) the previous use of its slot being
+// fully released (sender-local counter) and (b) the consumer's credit for that
+// previous use (the remote flag read 0; the first CTA that sees it caches it
+// locally so the other chunks skip the NVLink round trip).  The earliest
+// unfinished item never waits on a later one: no deadlock for any grid.
+
+struct StreamEdgeArgs {
+  const uint8_t *src;      // nsrc payloads, src_stride apart (round j sends j % nsrc)
+  uint64_t src_stride;
+  uint32_t nsrc;
+  uint8_t *dst;            // slot 0 (a peer's pool or this GPU's)
+  uint64_t slot_stride;
+  uint32_t slots;
+  uint64_t nbytes;         // payload bytes S; the flag is at slot + S
+  uint64_t chunk;          // bytes per work item
+  uint32_t nchunks;
+  uint64_t first_round;    // rounds continue across launches
+  uint32_t rounds;
+  unsigned int *released;  // [slots] uses of the slot released (sender-local)
+  unsigned int *arrival;   // [slots] chunk arrivals of the slot's current use
+  unsigned int *credit;    // [slots] uses whose predecessor was consumed (cached credit)
+  unsigned int *claim;     // work queue head
+  unsigned int *exit_count;
+  int sys;                 // destination is a peer's memory
+  uint64_t timeout_ns;
+  int *err;
+};
+
+__device__ __forceinline__ void red_release_gpu_max(unsigned int *p, unsigned v) {
+  asm volatile("red.release.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(512) k_put_stream(const __grid_constant__ StreamEdgeArgs a) {
+  __shared__ uint32_t s_i;
+  __shared__ int s_last;
+  const uint32_t total = a.rounds * a.nchunks;
+  for (;;) {
+    if (threadIdx.x == 0) s_i = atomicAdd(a.claim, 1u);
+    __syncthreads();
+    const uint32_t i = s_i;
+    __syncthreads();
+    if (i >= total) break;
+    const uint32_t jr = i / a.nchunks;
+    const uint32_t c = i - jr * a.nchunks;
+    const uint64_t j = a.first_round + jr;
+    const uint32_t slot = (uint32_t)(j % a.slots);
+    const uint32_t m = (uint32_t)(j / a.slots);  // use index of the slot
+    uint8_t *d = a.dst + (uint64_t)slot * a.slot_stride;
+    if (threadIdx.x == 0) {
+      // (a) the slot's previous use is fully released (its tail published)
+      wait_count(a.released + slot, m, a.timeout_ns, a.err);
+      // (b) ... and consumed: the receiver cleared its flag (the reference's
+      // credit, protocol.py:102-111); cached once seen
+      if (m > 0 && ld_acquire_gpu_u32(a.credit + slot) < m) {
+        if (!spin_until(d + a.nbytes, 0, a.timeout_ns, a.sys)) atomicExch(a.err, 2);
+        red_release_gpu_max(a.credit + slot, m);
+      }
+    }
+    __syncthreads();
+    const uint64_t off = (uint64_t)c * a.chunk;
+    const uint64_t n = a.nbytes - off < a.chunk ? a.nbytes - off : a.chunk;
+    const uint8_t *s = a.src + (j % a.nsrc) * a.src_stride;
+    copy_bytes_grid<8>(d + off, s + off, n, threadIdx.x, blockDim.x);
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = grid_arrive(a.arrival + slot, a.nchunks - 1, a.sys);
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      atomicExch(a.arrival + slot, 0u);    // re-armed before anything is published
+      release_tail(d + a.nbytes, 1, a.sys);  // flag last: the round is delivered
+      count_done(a.released + slot);
+    }
+  }
+  // the last CTA out re-arms the queue for the next launch
+  if (threadIdx.x == 0 && atomicAdd(a.exit_count, 1u) == gridDim.x - 1) {
+    *a.claim = 0;
+    *a.exit_count = 0;
+  }
+}
+
+// Receiver side of the pipelined edge (StaticReceiver.poll per round, on the
+// device): one CTA walks rounds in order, acquire-spins on the slot's flag,
+// optionally checksums the payload the flag guards, then clears the flag
+// (release: the sender may overwrite the slot only after these reads).
+// mode 0: consume the flag only; 1: also store a weighted byte checksum of
+// the round's payload into sums[r] (tests).
+__global__ void __launch_bounds__(1024) k_consume_stream(uint8_t *slots_base, uint64_t slot_stride,
+                                                          uint32_t slots, uint64_t nbytes,
+                                                          uint64_t first_round, uint32_t rounds,
+                                                          int mode, unsigned long long *sums,
+                                                          uint64_t timeout_ns, int *err) {
+  __shared__ unsigned long long acc;
+  __shared__ int ok;
+  for (uint32_t r = 0; r < rounds; ++r) {
+    const uint64_t j = first_round + r;
+    uint8_t *d = slots_base + (j % slots) * slot_stride;
+    if (threadIdx.x == 0) {
+      acc = 0;
+      ok = spin_until(d + nbytes, 1, timeout_ns, 1) ? 1 : 0;
+      if (!ok) atomicExch(err, 1);
+    }
+    __syncthreads();
+    if (!ok) return;
+    if (mode == 1) {
+      unsigned long long sum = 0;
+      for (uint64_t i = threadIdx.x; i < nbytes; i += blockDim.x)
+        sum += (unsigned long long)__ldcg(d + i) * (i % 251 + 1);  // L2: the slot is rewritten
+      atomicAdd(&acc, sum);
+      __syncthreads();
+      if (threadIdx.x == 0) sums[r] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) release_tail(d + nbytes, 0, 1);
+    __syncthreads();
+  }
+}

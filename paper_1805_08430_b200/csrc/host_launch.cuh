@@ -50,6 +50,8 @@ static int g_unroll = 8;    // 16-B vectors in flight per thread (4 or 8)
 static uint64_t g_peer_ce_bytes = 32ull << 20;
 static int g_force_sys = 0;  // knob 7 (tests): every put/get takes the cross-device path
 static uint64_t g_put_timeout_ns = 5000000000ull;  // knob 8: credit wait limit of a put
+static int g_edge_ctas_per_sm = 2;   // knob 9: pipelined edge CTAs per SM
+static uint64_t g_edge_chunk = 0;    // knob 10: pipelined edge chunk (KiB; 0 = automatic)
 
 // launch K1/K4/K5 with the configured implementation
 static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {

@@ -37,8 +37,10 @@ namespace cg = cooperative_groups;
 #include "device_copy.cuh"
 #include "device_pcg.cuh"
 #include "device_ps.cuh"
+#include "device_stream.cuh"
 #include "device_rpc.cuh"
 #include "host_launch.cuh"
 #include "abi_core.cuh"
 #include "abi_ps.cuh"
+#include "abi_stream.cuh"
 #include "abi_doorbell.cuh"

@@ -249,6 +249,12 @@ class MemorySpace:
         """Wait for all work queued on this space's stream."""
         _lib.call("srf_space_sync", self._h)
 
+    def fence(self) -> "_lib.Event":
+        """An event after all work queued so far on this space's stream."""
+        h = C.c_void_p()
+        _lib.call("srf_event_record", self._h, None, C.byref(h))
+        return _lib.Event(h)
+
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:
             _lib.load().srf_space_destroy(self._h)
@@ -431,6 +437,25 @@ class ArenaAllocator:
         self._lens: list[int] = [usable] if usable else []
         self._live: dict[int, tuple[int, int]] = {}
         self._lock = threading.Lock()
+        # (offset, reserved, Event) of blocks freed while device work could
+        # still touch them (BufferRef.release): the bookkeeping free is
+        # immediate - first-fit addresses stay the reference's - and a later
+        # allocation that reuses any of those bytes orders the space's stream
+        # after the fence
+        self._fences: list[tuple[int, int, "_lib.Event"]] = []
+
+    def _wait_fences(self, off: int, need: int) -> None:
+        keep = []
+        for f_off, f_len, ev in self._fences:
+            if f_off < off + need and off < f_off + f_len:
+                if not ev.query():
+                    _lib.call("srf_space_wait_event", self.space.handle, ev._h)
+                ev.free()
+            elif ev.query():
+                ev.free()
+            else:
+                keep.append((f_off, f_len, ev))
+        self._fences = keep
 
     def alloc(self, length: int) -> RegionHandle:
         if length < 1:
@@ -447,6 +472,8 @@ class ArenaAllocator:
                     self._starts[i] = off + need
                     self._lens[i] = size - need
                 addr = self.backing.base_addr + off
+                if self._fences:
+                    self._wait_fences(off, need)
                 self._live[addr] = (length, need)
                 self.current_resident += length
                 self.peak_resident = max(self.peak_resident, self.current_resident)
@@ -456,14 +483,22 @@ class ArenaAllocator:
             f"server {self.space.server_id}: no free block of {length} bytes "
             f"(resident {self.current_resident}/{self.backing.length})")
 
-    def free(self, handle: RegionHandle) -> None:
+    def free(self, handle: RegionHandle, fence: Optional["_lib.Event"] = None) -> None:
+        """Return a block (memspace.py:279-290).  ``fence``: an event after
+        the last device work that may use the block; reusing its bytes waits
+        for it."""
         with self._lock:
             entry = self._live.pop(handle.base_addr, None)
             if entry is None:
+                if fence is not None:
+                    fence.free()
                 raise ValueError(f"not a live arena block: addr {handle.base_addr}")
             requested, reserved = entry
-            self._give_back(handle.base_addr - self.backing.base_addr, reserved)
+            off = handle.base_addr - self.backing.base_addr
+            self._give_back(off, reserved)
             self.current_resident -= requested
+            if fence is not None:
+                self._fences.append((off, reserved, fence))
 
     def _give_back(self, off: int, length: int) -> None:
         i = bisect.bisect_left(self._starts, off)
@@ -518,7 +553,10 @@ class BufferRef:
                 raise AssertionError("buffer over-released")
             owned_and_dead = self._refs == 0 and self.arena is not None
         if owned_and_dead:
-            self.arena.free(self.handle)
+            # event-guarded: device work queued on the space's stream before
+            # this release may still read or write the block
+            fence = getattr(self.arena.space, "fence", None)
+            self.arena.free(self.handle, fence=fence() if fence is not None else None)
 
     def __repr__(self) -> str:  # pragma: no cover
         kind = "owned" if self.arena is not None else "view"

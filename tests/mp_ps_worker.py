@@ -17,7 +17,13 @@ from paper_1805_08430_b200.workloads import mlp_shapes  # noqa: E402
 
 
 def main() -> int:
-    rank, world, local = init_process_group("nccl")
+    # SRFLOW_MP_ONE_GPU=1: both ranks on GPU 0, gloo control plane (CUDA IPC
+    # between two processes of one device); the phase schedule only - kernels
+    # of two processes on one GPU time-slice, so the single-launch exchange
+    # would wait on a peer kernel that cannot run beside it
+    one_gpu = os.environ.get("SRFLOW_MP_ONE_GPU") == "1"
+    rank, world, local = init_process_group("gloo" if one_gpu else "nccl")
+    local = 0 if one_gpu else local
     torch.cuda.set_device(local)
     layouts = [
         ("coloc", [(3000,), (17,), (200, 300), (5,), (70000,)], world, world, True),
@@ -35,7 +41,7 @@ def main() -> int:
     ]
     bad = 0
     for name, shapes, W, P, coloc, *kw in layouts:
-        for schedule in ("phases", "exchange", "exchange_x3"):
+        for schedule in (("phases",) if one_gpu else ("phases", "exchange", "exchange_x3")):
             L = PsLayout(shapes, W, P, coloc, **(kw[0] if kw else {}))
             ps = PsStep(L, rank=rank, world=world, device=local, seed=5, op="sgd", lr=0.02,
                         schedule="phases" if schedule == "phases" else "exchange")

@@ -1,0 +1,76 @@
+"""pytest plugin (``-p ref_alias``): run the REFERENCE's own test suite
+against this package.
+
+``rdmaflow`` and its submodules are aliased to ``paper_1805_08430_b200`` before
+the reference tests import them, so every fixture, endpoint, session and
+assertion of /root/reference/pkg/tests (vendored into oracle/_ref/ref_tests by
+oracle/vendor_ref.py) exercises the B200 implementation - its libsrflow
+kernels included.  ``rdmaflow.benchcli`` (the reference's bench CLI, out of
+scope per SURVEY.md 2) is the reference's own module loaded on top of the
+aliased package, so its Session runs are ours too.
+
+Not applicable on B200 (skipped with the reason): tests that script the
+simulated fabric's per-chunk delivery order.  The reference delivers every
+verb as ascending random 1-4096 B chunks (fabric.py:391-421) and these tests
+observe or script intermediate chunk prefixes; on the GPU the bytes move in
+one kernel and the ordering contract is release/acquire of the flag byte,
+checked by tests/test_gpu_kernels.py::test_release_acquire_stress instead.
+"""
+from __future__ import annotations
+
+import importlib
+import importlib.util
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+REF = os.path.join(ROOT, "oracle", "_ref", "rdmaflow")
+
+_MODULES = ["errors", "wire", "memspace", "fabric", "graph", "analyzer", "workloads",
+            "runtime", "runtime.protocol", "runtime.executor", "runtime.session",
+            "runtime.report"]
+
+
+def _alias() -> None:
+    pkg = importlib.import_module("paper_1805_08430_b200")
+    sys.modules["rdmaflow"] = pkg
+    for m in _MODULES:
+        sys.modules["rdmaflow." + m] = importlib.import_module("paper_1805_08430_b200." + m)
+    cli = os.path.join(REF, "benchcli.py")
+    if os.path.exists(cli):
+        spec = importlib.util.spec_from_file_location("rdmaflow.benchcli", cli)
+        mod = importlib.util.module_from_spec(spec)
+        mod.__package__ = "rdmaflow"
+        sys.modules["rdmaflow.benchcli"] = mod
+        spec.loader.exec_module(mod)
+
+
+_alias()
+
+#: test node id suffix -> reason it does not apply to the GPU data plane
+NOT_APPLICABLE = {
+    "test_fabric.py::TestOneSidedWrite::test_scripted_chunks_ascend":
+        "scripts the simulated fabric's chunk schedule (fabric.py:391-421)",
+    "test_fabric.py::TestOneSidedWrite::test_randomized_ascending_prefixes":
+        "observes intermediate chunk prefixes of the simulated delivery",
+    "test_fabric.py::TestOneSidedWrite::test_default_chunks_within_bounds":
+        "asserts the simulated fabric's random 1-4096 B chunk sizes (a verb is one kernel; "
+        "chunk_callback reports it as one chunk)",
+    "test_protocol.py::TestStaticProtocol::test_pending_under_all_chunk_prefixes":
+        "stops the simulated delivery after each chunk prefix",
+    "test_acceptance.py::TestCriterion1FlagProtocolSafety::test_flag_protocol_safety":
+        "adversarial chunk schedules of the simulated fabric (criterion C1); replaced by "
+        "the release/acquire stress test on the GPU",
+}
+
+
+def pytest_collection_modifyitems(config, items):
+    for item in items:
+        nid = item.nodeid.replace("\\\\", "/")
+        for suffix, why in NOT_APPLICABLE.items():
+            if nid.endswith(suffix):
+                item.add_marker(pytest.mark.skip(reason=f"not applicable on B200: {why}"))

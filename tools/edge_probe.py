@@ -1,0 +1,112 @@
+"""Pipelined static edge (srf_edge_*) throughput: rounds of S bytes over one
+edge with `slots` receive regions, consumer on the receiving GPU.  One
+process.  Modes: same GPU (HBM), GPU0 -> GPU1 (NVLink one direction), and
+both directions at once (the N=2 ring).  Device time of each side's stream
+(events), GB/s = rounds * S / time.  Usage: python tools/edge_probe.py [sizes...]"""
+import ctypes as C
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1805_08430_b200 import _lib
+from paper_1805_08430_b200.memspace import MemorySpace
+from paper_1805_08430_b200.runtime.protocol import PipelinedStaticEdge
+
+KIB, MIB = 1 << 10, 1 << 20
+ndev = _lib.device_count()
+
+
+def r256(n):
+    return (n + 255) & ~255
+
+
+class Side:
+    def __init__(self, src_dev, dst_dev, S, slots, nsrc):
+        self.S, self.slots = S, slots
+        self.src_stride, self.slot_stride = r256(S), r256(S + 1)
+        self.a = MemorySpace(10 + src_dev, nsrc * self.src_stride + 4 * MIB, seed=1,
+                             device=src_dev)
+        self.b = MemorySpace(20 + dst_dev, slots * self.slot_stride + 4 * MIB, seed=2,
+                             device=dst_dev)
+        _lib.call("srf_connect", self.a.handle, self.b.handle)
+        self.ra = self.a.allocate_region(nsrc * self.src_stride, register=True)
+        self.rb = self.b.allocate_region(slots * self.slot_stride, register=True)
+        for i in range(slots):
+            self.b.write_raw(self.rb.base_addr + i * self.slot_stride + S, b"\x00")
+        self.a.sync(), self.b.sync()
+        self.sa, self.sb = C.c_void_p(), C.c_void_p()
+        _lib.call("srf_stream_create", self.a.handle, C.byref(self.sa))
+        _lib.call("srf_stream_create", self.b.handle, C.byref(self.sb))
+        self.edge = PipelinedStaticEdge(self.a, self.ra, S, nsrc, self.src_stride, self.b,
+                                        self.rb.base_addr, self.rb.access_token, slots,
+                                        self.slot_stride)
+        self.ev = [C.c_void_p(), C.c_void_p()]
+        for e in self.ev:
+            _lib.call("srf_timing_event_create", self.a.handle, C.byref(e))
+        self.next = 0
+
+    def launch(self, rounds, timed=False):
+        PipelinedStaticEdge.consume(self.b, self.rb.base_addr, self.slots, self.slot_stride,
+                                    self.S, self.next, rounds, stream=self.sb)
+        if timed:
+            _lib.call("srf_event_record_on", self.ev[0], self.sa)
+        self.edge.send(rounds, self.sa)
+        if timed:
+            _lib.call("srf_event_record_on", self.ev[1], self.sa)
+        self.next += rounds
+
+    def sync(self):
+        _lib.call("srf_stream_sync", self.sa)
+        _lib.call("srf_stream_sync", self.sb)
+        self.a.sync(), self.b.sync()
+
+    def ms(self):
+        t = C.c_float()
+        _lib.call("srf_event_elapsed_ms", self.ev[0], self.ev[1], C.byref(t))
+        return t.value
+
+    def close(self):
+        self.edge.close()
+        for s in (self.sa, self.sb):
+            _lib.call("srf_stream_destroy", s)
+        self.a.close(), self.b.close()
+
+
+def run(mode, S, slots, rounds):
+    pairs = {"hbm": [(0, 0)], "nvl1": [(0, 1)], "nvl2": [(0, 1), (1, 0)]}[mode]
+    nsrc = max(1, min(8, (256 * MIB) // max(S, 1)))
+    sides = [Side(s, d, S, slots, nsrc) for s, d in pairs]
+    for sd in sides:
+        sd.launch(max(2, rounds // 4))
+    for sd in sides:
+        sd.sync()
+    for sd in sides:
+        sd.launch(rounds, timed=True)
+    for sd in sides:
+        sd.sync()
+    ms = max(sd.ms() for sd in sides)
+    info = sides[0].edge.info()
+    for sd in sides:
+        sd.close()
+    return {"mode": mode, "bytes": S, "slots": slots, "rounds": rounds,
+            "us_per_round": round(ms * 1e3 / rounds, 3),
+            "gbps_per_dir": round(S * rounds / (ms / 1e3) / 1e9, 1),
+            "chunk": info["chunk"], "ctas": info["ctas"]}
+
+
+if __name__ == "__main__":
+    sizes = [int(x) for x in sys.argv[1:]] or [KIB, 64 * KIB, MIB, 4 * MIB, 16 * MIB,
+                                                 64 * MIB, 256 * MIB]
+    modes = ["hbm"] + (["nvl1", "nvl2"] if ndev > 1 else [])
+    for knob in [dict(), dict(edge_ctas_per_sm=1), dict(edge_ctas_per_sm=3)]:
+        for k, v in knob.items():
+            _lib.tune(k, v)
+        for mode in modes:
+            for S in sizes:
+                for slots in (1, 2, 4, 8):
+                    rounds = max(8, min(400, int(2e9 // max(S, 1) // 8)))
+                    row = run(mode, S, slots, rounds)
+                    row.update(knob)
+                    print(json.dumps(row), flush=True)
+        _lib.tune("edge_ctas_per_sm", 2)

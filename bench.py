@@ -1232,6 +1232,79 @@ def bench_ps_configs(rank, world, device, steps, warmup, op, cpu):
     return out
 
 
+def bench_ps_session(rank, world, device, steps, warmup, op, cpu):
+    """configs[2]-[4] through the reference's public entry point:
+    ``Session(build_ps_workload(...)).run(n)`` (runtime/session.py:606-629) -
+    the reference's executor, handlers and endpoints over the B200 verbs
+    (K1 weight pushes, device GenGrad, K3 metadata, K4 pulls, K6 updates),
+    one synchronous verb at a time as the reference runs them.  value = wall
+    steps/s of run(n); e2e adds reading every final variable back to the
+    host (D2H) and checking it against oracle.port.ps_expected (reference
+    PCG64 stream; XOR bit-exact / SGD restatement)."""
+    if rank != 0:
+        return {"note": "Session runs in one process (rank 0)"}
+    import torch
+    from oracle import port
+    from paper_1805_08430_b200.runtime.session import Session
+    from paper_1805_08430_b200.workloads import build_ps_workload, total_params, vgg16_shapes
+    cfgs = {
+        "fcn5": ("configs[2] FCN-5 preset, 1 PS + 2 workers", [(int(204.47e6) // 10 // 4,)] * 10,
+                 2, 1),
+        "lstm": ("configs[4] LSTM preset, 7 workers + 1 PS (dynamic gradient edges)",
+                 [(int(35.93e6) // 14 // 4,)] * 14, 7, 1),
+        "vgg16": ("configs[3] VGG-16 real shapes, worker server 0 + PS server 1",
+                  vgg16_shapes(), 1, 1),
+    }
+    out = {}
+    for name, (label, shapes, W, P) in cfgs.items():
+        model = 4 * total_params(shapes)
+        g, placement = build_ps_workload(model, len(shapes), 0.0, W, ps_servers=P, shapes=shapes)
+        arena = (W + 2) * model + (64 << 20)
+        sess = Session(g, placement, mode="zerocp", seed=0, capacity_bytes=arena + model + (96 << 20),
+                       arena_bytes=arena, watchdog_sweeps=10_000,
+                       devices={s: device for s in set(placement.values())},
+                       apply_op=op, lr=0.01)
+        sess.run(1)                       # iteration 1: tracing warm-up
+        sess.run(max(1, warmup - 1))
+        torch.cuda.synchronize(device)
+        n = max(3, min(steps, 50))
+        t0 = time.perf_counter()
+        report = sess.run(n)
+        torch.cuda.synchronize(device)
+        dt = time.perf_counter() - t0
+        it = sess._next_iteration - 1
+        # e2e: every variable back on the host, verified (first/last 4096
+        # elements of each against the oracle; XOR bit-exact, SGD restatement)
+        t1 = time.perf_counter()
+        var_nodes = [n_.node_id for n_ in g.nodes.values() if n_.kind.name == "VARIABLE"]
+        vals = [sess.variable_bytes(v) for v in sorted(var_nodes)]
+        d2h = time.perf_counter() - t1
+        ok = True
+        for v, raw in enumerate(vals):
+            got = np.frombuffer(raw, np.float32)
+            cnt = min(4096, got.size)
+            for lo, part in ((0, got[:cnt]), (got.size - cnt, got[got.size - cnt:])):
+                want = port.ps_expected(shapes, W, 0, it, op=op, lr=0.01, only=[v],
+                                        window=(lo, cnt))[v]
+                ok = ok and part.tobytes() == want.tobytes()
+        sess.close()
+        row = report.rows[-1]
+        out[name] = {
+            "workload": f"{label} ({total_params(shapes)} fp32) through Session.run, op={op}",
+            "steps_per_s": round(n / dt, 3), "ms_per_step": round(dt / n * 1e3, 3), "steps": n,
+            "e2e": {"value": round(n / (dt + d2h), 3), "unit": "steps/s",
+                    "h2d_bytes_per_step": 0, "d2h_bytes_per_step": round(model / n),
+                    "note": "run(n) + all final variables read back (D2H) once; gradients "
+                            "are the reference's synthetic GenGrad, generated in place"},
+            "verified": ok, "iterations": it,
+            "row": {k: getattr(row, k) for k in ("payload_bytes", "payload_bytes_copied", "polls")
+                    if hasattr(row, k)},
+        }
+        del sess
+        torch.cuda.empty_cache()
+    return out
+
+
 JSON_OUT = None
 
 # -- main -------------------------------------------------------------------------------------------
@@ -1391,11 +1464,13 @@ def main() -> int:
         section("ps_configs", lambda: bench_ps_configs(rank, world, local, max(20, args.steps),
                                                        args.warmup, args.ps_op,
                                                        not args.no_cpu))
+        section("ps_session", lambda: bench_ps_session(rank, world, local, args.steps,
+                                                       args.warmup, args.ps_op, not args.no_cpu))
     if rank == 0:
         print(json.dumps(line), file=JSON_OUT, flush=True)
     ps_ok = line.get("ps", {}).get("verified", True) and all(
-        c.get("verified", True) for c in line.get("ps_configs", {}).values()
-        if isinstance(c, dict)) and all(line.get(k, {}).get("verified", True) for k in
+        c.get("verified", True) for k in ("ps_configs", "ps_session")
+        for c in line.get(k, {}).values() if isinstance(c, dict)) and all(line.get(k, {}).get("verified", True) for k in
                                       ("ps_balanced", "ps_sliced", "ps_partitioned"))
     if not dev["verified"] or not e2e["verified"] or not ps_ok:
         log("verification FAILED")

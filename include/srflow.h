@@ -179,6 +179,15 @@ int srf_put_consume(srf_space_t src_space, const uint64_t *src_addr, const uint6
 /* Channel.one_sided_read (fabric.py:371-389).  K4 peer_pull: launched on the
  * reader's GPU, loads [src_addr, +length) from the peer pool, stores into the
  * local registered range dst_addr. */
+/* K3 with the block inline: DynSender.send's metadata (runtime/protocol.py:
+ * 163-201).  The `len` (<= 1024) bytes are a kernel parameter - no staging
+ * copy from the host - and one launch writes them into the sender's
+ * registered stage block [stage_addr, +len) (write_at(meta_stage)) and into
+ * [dst_addr, +len) of dst_space, last byte released last (and mirrored to the
+ * receiver's host doorbell).  Same checks and flags as srf_put. */
+int srf_put_inline(srf_space_t src_space, uint64_t stage_addr, uint64_t stage_token,
+                   const void *bytes, uint32_t len, srf_space_t dst_space, uint64_t dst_addr,
+                   uint64_t dst_token, int flags, srf_stream_t stream, srf_event_t *ev_out);
 int srf_get(srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
             srf_space_t src_space, uint64_t src_addr, uint64_t src_token,
             uint64_t length, srf_stream_t stream, srf_event_t *ev_out);
@@ -236,7 +245,7 @@ int srf_apply(srf_space_t var_space, uint64_t var_addr, uint64_t nbytes,
  *   Generator(PCG64(((seed & 0xFFFFFFFF)*1000003 + node)*1000033 + iteration))
  *     .random(n, dtype=float32)
  * bit-exact (numpy's SeedSequence seeding, PCG64 XSL-RR, 24-bit floats), into
- * fp32 elements at addr (16-B aligned) of the space, on its stream. */
+ * fp32 elements at addr (4-B aligned) of the space, on its stream. */
 int srf_gen_reference(srf_space_t space, uint64_t addr, uint64_t nelems, uint64_t elem_offset,
                       uint64_t seed, uint64_t node, uint64_t iteration, srf_stream_t stream,
                       srf_event_t *ev_out);
@@ -405,18 +414,27 @@ int srf_reduce_max_f32(srf_space_t space, uint64_t in_addr, uint64_t n,
  * StaticReceiver.poll for rounds [first, first + rounds) on the device (one
  * CTA; mode 1 also stores a weighted byte checksum of every round's payload
  * at sums_addr, 8 B per round).  Creation checks registration and token and
- * bounds of the whole source and slot spans, like srf_put per verb. */
+ * bounds of the whole source and slot spans, like srf_put per verb.
+ * credit_addr (UINT64_MAX: none): 4 * slots bytes of the SENDER's pool; the
+ * consumer, given the same words (credit_space = its mapping of the sender's
+ * pool), stores each slot's consumed-use count there right after clearing
+ * the flag, and the sender reads that local copy of the credit instead of
+ * loading the remote flag over NVLink every round. */
 typedef struct srf_edge *srf_edge_t;
 int srf_edge_create(srf_space_t src_space, uint64_t src_addr, uint64_t src_token,
                     uint64_t nbytes, uint32_t nsrc, uint64_t src_stride,
                     srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
-                    uint32_t slots, uint64_t slot_stride, srf_edge_t *out);
+                    uint32_t slots, uint64_t slot_stride, uint64_t credit_addr,
+                    srf_edge_t *out);
 int srf_edge_info(srf_edge_t edge, uint64_t *chunk, uint32_t *nchunks, int *ctas,
                   uint64_t *next_round);
+/* diagnostics: released[slots] | arrival[slots] | credit[slots] | claim | exit */
+int srf_edge_state(srf_edge_t edge, uint32_t *host_out, uint32_t nwords);
 int srf_edge_send(srf_edge_t edge, uint32_t rounds, srf_stream_t stream, srf_space_t src_space);
 int srf_edge_consume(srf_space_t receiver, uint64_t slots_addr, uint32_t slots,
                      uint64_t slot_stride, uint64_t nbytes, uint64_t first_round,
-                     uint32_t rounds, int mode, uint64_t sums_addr, srf_stream_t stream);
+                     uint32_t rounds, int mode, uint64_t sums_addr, srf_space_t credit_space,
+                     uint64_t credit_addr, srf_stream_t stream);
 int srf_edge_destroy(srf_edge_t edge);
 
 #ifdef __cplusplus

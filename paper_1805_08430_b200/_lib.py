@@ -95,6 +95,8 @@ SIGNATURES = {
     "srf_put": (C.c_int, [vp, P(u64), P(u64), P(u64), C.c_int, vp, u64, u64,
                           C.c_int, vp, P(vp)]),
     "srf_get": (C.c_int, [vp, u64, u64, vp, u64, u64, u64, vp, P(vp)]),
+    "srf_put_inline": (C.c_int, [vp, u64, u64, C.c_char_p, C.c_uint32, vp, u64, u64, C.c_int, vp,
+                                 P(vp)]),
     "srf_put_consume": (C.c_int, [vp, P(u64), P(u64), P(u64), C.c_int, vp, u64, u64, C.c_int,
                                   vp, u64, vp, P(vp)]),
     "srf_copy": (C.c_int, [vp, u64, u64, u64, vp, P(vp)]),
@@ -138,11 +140,12 @@ SIGNATURES = {
     "srf_reduce_max_f32": (C.c_int, [vp, u64, u64, u64, vp]),
     "srf_gen_reference": (C.c_int, [vp, u64, u64, u64, u64, u64, u64, vp, P(vp)]),
     "srf_edge_create": (C.c_int, [vp, u64, u64, u64, C.c_uint32, u64, vp, u64, u64, C.c_uint32,
-                                  u64, P(vp)]),
+                                  u64, u64, P(vp)]),
     "srf_edge_info": (C.c_int, [vp, P(u64), P(C.c_uint32), P(C.c_int), P(u64)]),
     "srf_edge_send": (C.c_int, [vp, C.c_uint32, vp, vp]),
+    "srf_edge_state": (C.c_int, [vp, P(C.c_uint32), C.c_uint32]),
     "srf_edge_consume": (C.c_int, [vp, u64, C.c_uint32, u64, u64, u64, C.c_uint32, C.c_int, u64,
-                                   vp]),
+                                   vp, u64, vp]),
     "srf_edge_destroy": (C.c_int, [vp]),
     "srf_matmul": (C.c_int, [C.c_int, u64, u64, u64, u64, u64, u64, vp]),
 }
@@ -175,7 +178,8 @@ def load() -> C.CDLL:
 _KNOBS = {"SRFLOW_CTAS_PER_SM": 0, "SRFLOW_COPY_THREADS": 1, "SRFLOW_PUT_IMPL": 2,
           "SRFLOW_ALLOC_VMM": 3, "SRFLOW_UNROLL": 4, "SRFLOW_VEC32": 5,
           "SRFLOW_PEER_CE_KIB": 6, "SRFLOW_FORCE_SYS": 7, "SRFLOW_PUT_TIMEOUT_MS": 8,
-          "SRFLOW_EDGE_CTAS_PER_SM": 9, "SRFLOW_EDGE_CHUNK_KIB": 10}
+          "SRFLOW_EDGE_CTAS_PER_SM": 9, "SRFLOW_EDGE_CHUNK_KIB": 10,
+          "SRFLOW_CONSUME_THREADS": 11}
 
 
 def _apply_env_knobs(lib) -> None:
@@ -192,7 +196,8 @@ def tune(knob: str, value: int) -> None:
     call("srf_tune", {"ctas_per_sm": 0, "copy_threads": 1, "put_impl": 2,
                       "alloc_vmm": 3, "unroll": 4, "vec32": 5,
                       "peer_ce_kib": 6, "force_sys": 7, "put_timeout_ms": 8,
-                      "edge_ctas_per_sm": 9, "edge_chunk_kib": 10}[knob], value)
+                      "edge_ctas_per_sm": 9, "edge_chunk_kib": 10,
+                      "consume_threads": 11}[knob], value)
 
 
 def last_error() -> str:

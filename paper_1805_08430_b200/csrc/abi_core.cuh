@@ -69,6 +69,11 @@ int srf_tune(int knob, int value) {
       if (value < 0) return fail(SRF_E_INVALID_CONFIG, "edge_chunk_kib >= 0");
       g_edge_chunk = (uint64_t)value;
       return SRF_OK;
+    case 11:
+      if (value < 32 || value > 1024 || value % 32)
+        return fail(SRF_E_INVALID_CONFIG, "consume_threads: a multiple of 32 in [32, 1024]");
+      g_consume_threads = value;
+      return SRF_OK;
     default:
       return fail(SRF_E_INVALID_CONFIG, "unknown knob %d", knob);
   }
@@ -264,6 +269,8 @@ int srf_space_create(int server_id, int cuda_device, uint64_t capacity,
   DeviceGuard device_guard;
   if (capacity == 0) return fail(SRF_E_ZERO_LENGTH, "capacity must be >= 1");
   CUDA_TRY(cudaSetDevice(cuda_device));
+  int rc_load = preload_kernels(cuda_device);
+  if (rc_load) return rc_load;
   srf_space *sp = new srf_space();
   sp->server_id = server_id;
   sp->device = cuda_device;
@@ -686,8 +693,7 @@ int srf_event_wait(srf_event_t ev) {
 int srf_event_free(srf_event_t ev) {
   DeviceGuard device_guard;
   if (!ev) return SRF_OK;
-  cudaEventDestroy(ev->e);
-  delete ev;
+  release_event(ev);  // a pooled completion event is reused by a later verb
   return SRF_OK;
 }
 
@@ -788,6 +794,56 @@ static int put_impl(srf_space_t src_space, const uint64_t *src_addr, const uint6
     rc = put_via_copy_engine(a, s);
   else
     rc = launch_copy(a, s, "k_put");
+  if (rc) return rc;
+  return record_event(s->device, s->s, ev_out);
+}
+
+int srf_put_inline(srf_space_t src_space, uint64_t stage_addr, uint64_t stage_token,
+                   const void *bytes, uint32_t len, srf_space_t dst_space, uint64_t dst_addr,
+                   uint64_t dst_token, int flags, srf_stream_t st, srf_event_t *ev_out) {
+  DeviceGuard device_guard;
+  if (len < 1) return fail(SRF_E_INVALID_LENGTH, "zero-length write");
+  if (len > (uint32_t)kInlineMax)
+    return fail(SRF_E_INVALID_CONFIG, "inline block of %u bytes (max %d)", len, kInlineMax);
+  {
+    std::lock_guard<std::mutex> g(src_space->mu);
+    int rc = check_registered_locked(src_space, stage_addr, len, stage_token);
+    if (rc) return rc;
+  }
+  {
+    std::lock_guard<std::mutex> g(dst_space->mu);
+    int rc = check_remote_locked(dst_space, dst_addr, len, dst_token);
+    if (rc) return rc;
+  }
+  srf_stream *s = stream_or_default(src_space, st);
+  InlineArgs a;
+  memset(&a, 0, sizeof a);
+  memcpy(a.bytes, bytes, len);
+  a.len = len;
+  a.stage = src_space->base + stage_addr;
+  a.dst = dst_space->base + dst_addr;
+  a.sys_scope = (g_force_sys || dst_space->imported || dst_space->device != s->device) ? 1 : 0;
+  a.wait_empty = (flags & SRF_PUT_WAIT_EMPTY) ? 1 : 0;
+  a.timeout_ns = g_put_timeout_ns;
+  a.err = src_space->err;
+  if (dst_space->db && !dst_space->imported) {
+    std::lock_guard<std::mutex> g(dst_space->mu);
+    auto it = dst_space->db->find(dst_addr + len - 1);
+    if (it != dst_space->db->end()) {
+      Doorbell &d = it->second;
+      const uint64_t n = std::min<uint64_t>(len, d.shadow_len);
+      a.db = dst_space->db_dev + d.host_off + (d.shadow_len - n);
+      a.db_len = (uint32_t)n;
+      if (d.clear_pending) {
+        CUDA_TRY(cudaSetDevice(s->device));
+        CUDA_TRY(cudaStreamWaitEvent(s->s, d.clear_ev, 0));
+        d.clear_pending = false;
+      }
+    }
+  }
+  CUDA_TRY(cudaSetDevice(s->device));
+  k_put_inline<<<1, 256, 0, s->s>>>(a);
+  int rc = launch_check("k_put_inline");
   if (rc) return rc;
   return record_event(s->device, s->s, ev_out);
 }
@@ -966,7 +1022,7 @@ int srf_gen_reference(srf_space_t sp, uint64_t addr, uint64_t nelems, uint64_t e
   DeviceGuard device_guard;
   int rc = check_raw(sp, addr, nelems * 4, "generated tensor");
   if (rc) return rc;
-  if (addr % 16) return fail(SRF_E_INVALID_CONFIG, "generated tensor must be 16-B aligned");
+  if (addr % 4) return fail(SRF_E_INVALID_CONFIG, "generated fp32 tensor must be 4-B aligned");
   srf_stream *s = stream_or_default(sp, st);
   CUDA_TRY(cudaSetDevice(s->device));
   if (nelems) {

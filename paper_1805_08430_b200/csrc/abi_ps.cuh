@@ -241,7 +241,6 @@ int srf_batch_launch(srf_batch_t b, srf_stream_t st, uint64_t iteration, int mod
 // Device iteration counter for graph-captured PS steps: a gen batch launched
 // with iteration == UINT64_MAX reads *counter; srf_counter_add bumps it in
 // stream order at the end of a step.
-__global__ void k_counter_add(uint64_t *p, uint64_t delta) { *p += delta; }
 
 int srf_batch_set_iteration_source(srf_batch_t b, srf_space_t sp, uint64_t addr) {
   DeviceGuard device_guard;

@@ -15,7 +15,8 @@ extern "C" {
 int srf_edge_create(srf_space_t src_space, uint64_t src_addr, uint64_t src_token,
                     uint64_t nbytes, uint32_t nsrc, uint64_t src_stride,
                     srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
-                    uint32_t slots, uint64_t slot_stride, srf_edge_t *out) {
+                    uint32_t slots, uint64_t slot_stride, uint64_t credit_addr,
+                    srf_edge_t *out) {
   DeviceGuard device_guard;
   if (nbytes < 1) return fail(SRF_E_INVALID_LENGTH, "zero-length edge");
   if (slots < 1 || nsrc < 1) return fail(SRF_E_INVALID_CONFIG, "slots and nsrc must be >= 1");
@@ -44,14 +45,15 @@ int srf_edge_create(srf_space_t src_space, uint64_t src_addr, uint64_t src_token
   e->a.slot_stride = slot_stride;
   e->a.slots = slots;
   e->a.nbytes = nbytes;
-  // chunk: ~2 items per CTA per round for mid sizes, 64-256 KiB for large
-  // payloads (amortises the claim, credit check and system-scope arrival)
+  // chunk: S/32 within [32 KiB, 256 KiB] - large enough to amortise a work
+  // item's claim, credit check and system-scope arrival, small enough that a
+  // round spreads over many CTAs (tools/edge_probe.py sweep,
+  // profiles/r2_edge_probe.jsonl)
   const int sms = sm_count_of(e->device);
   e->ctas = std::max(1, sms * g_edge_ctas_per_sm);
   uint64_t chunk = g_edge_chunk ? (g_edge_chunk << 10)
                                 : std::min<uint64_t>(256 << 10,
-                                                     std::max<uint64_t>(16 << 10,
-                                                                        nbytes / (uint64_t)e->ctas));
+                                                     std::max<uint64_t>(32 << 10, nbytes / 32));
   chunk = (chunk + 4095) & ~4095ull;
   if (chunk > nbytes) chunk = nbytes;
   e->a.chunk = chunk;
@@ -59,6 +61,18 @@ int srf_edge_create(srf_space_t src_space, uint64_t src_addr, uint64_t src_token
   e->a.sys = (g_force_sys || dst_space->imported || dst_space->device != src_space->device) ? 1 : 0;
   e->a.timeout_ns = g_put_timeout_ns;
   e->a.err = src_space->err;
+  if (credit_addr != UINT64_MAX) {
+    int rc = check_raw(src_space, credit_addr, 4ull * slots, "credit mirror");
+    if (rc) {
+      delete e;
+      return rc;
+    }
+    if (credit_addr % 4) {
+      delete e;
+      return fail(SRF_E_INVALID_CONFIG, "credit mirror must be 4-B aligned");
+    }
+    e->a.credit_mirror = (const unsigned int *)(src_space->base + credit_addr);
+  }
   e->next_round = 0;
   CUDA_TRY(cudaSetDevice(e->device));
   const size_t words = 3 * (size_t)slots + 2;
@@ -87,6 +101,16 @@ int srf_edge_info(srf_edge_t e, uint64_t *chunk, uint32_t *nchunks, int *ctas,
   return SRF_OK;
 }
 
+// released[slots] | arrival[slots] | credit[slots] | claim | exit (diagnostics)
+int srf_edge_state(srf_edge_t e, uint32_t *host_out, uint32_t nwords) {
+  DeviceGuard device_guard;
+  const uint32_t words = 3 * e->a.slots + 2;
+  CUDA_TRY(cudaSetDevice(e->device));
+  CUDA_TRY(cudaMemcpy(host_out, e->state, sizeof(uint32_t) * std::min(words, nwords),
+                      cudaMemcpyDeviceToHost));
+  return SRF_OK;
+}
+
 int srf_edge_send(srf_edge_t e, uint32_t rounds, srf_stream_t st, srf_space_t src_space) {
   DeviceGuard device_guard;
   if (rounds == 0) return SRF_OK;
@@ -109,7 +133,8 @@ int srf_edge_send(srf_edge_t e, uint32_t rounds, srf_stream_t st, srf_space_t sr
 
 int srf_edge_consume(srf_space_t rcv, uint64_t slots_addr, uint32_t slots, uint64_t slot_stride,
                      uint64_t nbytes, uint64_t first_round, uint32_t rounds, int mode,
-                     uint64_t sums_addr, srf_stream_t st) {
+                     uint64_t sums_addr, srf_space_t credit_space, uint64_t credit_addr,
+                     srf_stream_t st) {
   DeviceGuard device_guard;
   if (rcv->imported) return fail(SRF_E_INVALID_CONFIG, "the receiver consumes its own slots");
   if (slots < 1 || slot_stride < nbytes + 1)
@@ -121,12 +146,19 @@ int srf_edge_consume(srf_space_t rcv, uint64_t slots_addr, uint32_t slots, uint6
     if (rc) return rc;
     if (sums_addr % 8) return fail(SRF_E_INVALID_CONFIG, "checksums must be 8-B aligned");
   }
+  unsigned int *mirror = nullptr;
+  if (credit_space) {
+    rc = check_raw(credit_space, credit_addr, 4ull * slots, "credit mirror");
+    if (rc) return rc;
+    if (credit_addr % 4) return fail(SRF_E_INVALID_CONFIG, "credit mirror must be 4-B aligned");
+    mirror = (unsigned int *)(credit_space->base + credit_addr);
+  }
   if (rounds == 0) return SRF_OK;
   srf_stream *s = stream_or_default(rcv, st);
   CUDA_TRY(cudaSetDevice(s->device));
-  k_consume_stream<<<1, mode == 1 ? 1024 : 32, 0, s->s>>>(
+  k_consume_stream<<<1, mode == 1 ? 1024 : g_consume_threads, 0, s->s>>>(
       rcv->base + slots_addr, slot_stride, slots, nbytes, first_round, rounds, mode,
-      (unsigned long long *)(rcv->base + sums_addr), g_put_timeout_ns, rcv->err);
+      (unsigned long long *)(rcv->base + sums_addr), mirror, g_put_timeout_ns, rcv->err);
   return launch_check("k_consume_stream");
 }
 

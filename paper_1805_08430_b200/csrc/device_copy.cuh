@@ -510,6 +510,49 @@ __global__ void __launch_bounds__(512) k_put(PutArgs a) {
 }
 
 
+// K3 with the metadata block inline (DynSender.send, protocol.py:163-201):
+// the 8D+33 bytes travel as a kernel parameter - no host-to-device staging
+// copy - and one CTA writes them into the sender's registered meta stage
+// (write_at(meta_stage), as the reference keeps them) and into the
+// receiver's block, flag byte released last (plus the host doorbell mirror).
+static constexpr int kInlineMax = 1024;
+
+struct InlineArgs {
+  uint8_t bytes[kInlineMax];
+  uint32_t len;
+  uint8_t *stage;         // sender's meta stage (local)
+  uint8_t *dst;           // receiver's block (peer or local)
+  int sys_scope;
+  int wait_empty;
+  uint8_t *db;            // host-mapped doorbell shadow (nullptr: none)
+  uint32_t db_len;
+  uint64_t timeout_ns;
+  int *err;
+};
+
+__global__ void __launch_bounds__(256) k_put_inline(const __grid_constant__ InlineArgs a) {
+  __shared__ int s_abort;
+  uint8_t *tail = a.dst + a.len - 1;
+  if (threadIdx.x == 0) s_abort = (a.wait_empty && !credit_wait(tail, a.timeout_ns, a.err)) ? 1 : 0;
+  __syncthreads();
+  if (s_abort) return;
+  for (uint32_t i = threadIdx.x; i < a.len; i += blockDim.x) {
+    a.stage[i] = a.bytes[i];
+    if (i + 1 < a.len) a.dst[i] = a.bytes[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // release is cumulative over the CTA's stores ordered before it by bar.sync
+    const uint32_t v = a.bytes[a.len - 1];
+    release_tail(tail, v, a.sys_scope);
+    if (a.db) {
+      for (uint32_t i = 0; i + 1 < a.db_len; ++i) a.db[i] = a.bytes[a.len - a.db_len + i];
+      __threadfence_system();
+      st_release_sys_u8(a.db + a.db_len - 1, v);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // TMA bulk-copy variant of K1/K4 (cp.async.bulk): one elected thread per CTA
 // streams 16 KB chunks global -> shared (mbarrier complete_tx) -> global

@@ -264,11 +264,18 @@ __device__ void pcg_fill_f32_cta(float *dst, uint64_t nf, uint64_t e0, uint64_t 
                                  uint64_t ctas) {
   __shared__ u128 s_base, s_inc, s_A, s_C, s_state0;
   const uint64_t nth = ctas * blockDim.x;
+  // dst may be only 4-B aligned (arena blocks are 8-B aligned,
+  // memspace.py:31): the first `head` floats take the scalar path and the
+  // vector path starts at the first 16-B boundary
+  uint64_t head = ((16 - ((uintptr_t)dst & 15)) & 15) / 4;
+  if (head > nf) head = nf;
+  float *vdst = dst + head;
+  const uint64_t vnf = nf - head, ve0 = e0 + head;
   if (threadIdx.x == 0) {
     const PcgStream p = pcg_node_stream(seed, node, iteration);
     u128 b = p.state;
-    // stepped state of the CTA's first raw: (e0 >> 1) + 4 * cta * blockDim + 1 steps
-    pcg_advance(b, p.inc, ((e0 >> 1) + 4 * cta * blockDim.x) + 1);
+    // stepped state of the CTA's first raw: (ve0 >> 1) + 4 * cta * blockDim + 1 steps
+    pcg_advance(b, p.inc, ((ve0 >> 1) + 4 * cta * blockDim.x) + 1);
     u128 A, G;
     pcg_jump_coeffs(4 * nth, A, G);
     s_base = b;
@@ -279,23 +286,25 @@ __device__ void pcg_fill_f32_cta(float *dst, uint64_t nf, uint64_t e0, uint64_t 
   }
   __syncthreads();
   const uint64_t t = cta * blockDim.x + threadIdx.x;
-  const uint64_t nchunks = nf / 8;
+  const uint64_t nchunks = vnf / 8;
   const u128 inc = s_inc;
   if (t < nchunks) {
     u128 s = s_base;
     pcg_advance(s, inc, 4 * (uint64_t)threadIdx.x);
-    if (e0 & 1)
-      pcg_chunks_leapfrog<1>(dst, nchunks, t, nth, s, inc, s_A, s_C);
+    if (ve0 & 1)
+      pcg_chunks_leapfrog<1>(vdst, nchunks, t, nth, s, inc, s_A, s_C);
     else
-      pcg_chunks_leapfrog<0>(dst, nchunks, t, nth, s, inc, s_A, s_C);
+      pcg_chunks_leapfrog<0>(vdst, nchunks, t, nth, s, inc, s_A, s_C);
   }
-  const uint64_t rem = nf - 8 * nchunks;
-  for (uint64_t j = t; j < rem; j += nth) {
-    const uint64_t e = e0 + 8 * nchunks + j;
+  // scalar floats: the unaligned head, then the tail of the vector range
+  const uint64_t rem = vnf - 8 * nchunks;
+  for (uint64_t j = t; j < head + rem; j += nth) {
+    const uint64_t local = j < head ? j : head + 8 * nchunks + (j - head);
+    const uint64_t e = e0 + local;
     u128 s = s_state0;
     pcg_advance(s, inc, e >> 1);
     const uint64_t r = pcg_next(s, inc);
-    dst[8 * nchunks + j] = pcg_half_to_f32((e & 1) ? (uint32_t)(r >> 32) : (uint32_t)r);
+    dst[local] = pcg_half_to_f32((e & 1) ? (uint32_t)(r >> 32) : (uint32_t)r);
   }
   __syncthreads();  // the shared stream state is reused by the CTA's next unit
 }

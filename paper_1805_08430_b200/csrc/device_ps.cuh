@@ -645,3 +645,6 @@ __global__ void __launch_bounds__(512, kMinBlocks) k_ps_exchange(const __grid_co
     *a.exit_count = 0;
   }
 }
+
+// graph-replayed PS steps: advance the device iteration counter
+__global__ void k_counter_add(uint64_t *p, uint64_t delta) { *p += delta; }

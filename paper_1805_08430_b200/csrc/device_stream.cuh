@@ -38,10 +38,26 @@ struct StreamEdgeArgs {
   unsigned int *credit;    // [slots] uses whose predecessor was consumed (cached credit)
   unsigned int *claim;     // work queue head
   unsigned int *exit_count;
+  // credit mirror (nullptr: none): [slots] words in the SENDER's memory that
+  // the consumer stores the slot's consumed-use count into (a posted write
+  // over NVLink) right after clearing the flag - the same credit as the
+  // cleared flag, read locally instead of by a remote load per round, which
+  // queues behind payload traffic when both link directions are busy
+  const unsigned int *credit_mirror;
   int sys;                 // destination is a peer's memory
   uint64_t timeout_ns;
   int *err;
 };
+
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const unsigned int *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys_u32(unsigned int *p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ void red_release_gpu_max(unsigned int *p, unsigned v) {
   asm volatile("red.release.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -68,7 +84,16 @@ __global__ void __launch_bounds__(512) k_put_stream(const __grid_constant__ Stre
       wait_count(a.released + slot, m, a.timeout_ns, a.err);
       // (b) ... and consumed: the receiver cleared its flag (the reference's
       // credit, protocol.py:102-111); cached once seen
-      if (m > 0 && ld_acquire_gpu_u32(a.credit + slot) < m) {
+      if (m > 0 && a.credit_mirror) {
+        const uint64_t t0 = globaltimer_ns();
+        while (ld_acquire_sys_u32(a.credit_mirror + slot) < m) {
+          if (globaltimer_ns() - t0 > a.timeout_ns) {
+            atomicExch(a.err, 2);
+            break;
+          }
+          __nanosleep(20);
+        }
+      } else if (m > 0 && ld_acquire_gpu_u32(a.credit + slot) < m) {
         if (!spin_until(d + a.nbytes, 0, a.timeout_ns, a.sys)) atomicExch(a.err, 2);
         red_release_gpu_max(a.credit + slot, m);
       }
@@ -104,6 +129,7 @@ __global__ void __launch_bounds__(1024) k_consume_stream(uint8_t *slots_base, ui
                                                           uint32_t slots, uint64_t nbytes,
                                                           uint64_t first_round, uint32_t rounds,
                                                           int mode, unsigned long long *sums,
+                                                          unsigned int *credit_mirror,
                                                           uint64_t timeout_ns, int *err) {
   __shared__ unsigned long long acc;
   __shared__ int ok;
@@ -126,7 +152,11 @@ __global__ void __launch_bounds__(1024) k_consume_stream(uint8_t *slots_base, ui
       if (threadIdx.x == 0) sums[r] = acc;
     }
     __syncthreads();
-    if (threadIdx.x == 0) release_tail(d + nbytes, 0, 1);
+    if (threadIdx.x == 0) {
+      release_tail(d + nbytes, 0, 1);  // StaticReceiver.poll's clear = the credit
+      if (credit_mirror)               // ... mirrored to the sender (posted write)
+        st_release_sys_u32(credit_mirror + j % slots, (unsigned)(j / slots) + 1);
+    }
     __syncthreads();
   }
 }

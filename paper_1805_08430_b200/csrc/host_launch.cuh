@@ -17,11 +17,28 @@ static void copy_geometry(int device, uint64_t bytes, int *grid, int *block) {
   *block = threads;
 }
 
+// Completion events (one per verb) are recycled through a per-device pool:
+// cudaEventCreate/Destroy per verb cost more host time than the record.
+static std::mutex g_event_pool_mu;
+static std::vector<srf_event *> g_event_pool[64];
+
 static int record_event(int device, cudaStream_t s, srf_event_t *ev_out) {
   if (!ev_out) return SRF_OK;
-  srf_event *ev = new srf_event();
-  ev->device = device;
-  cudaError_t e = cudaEventCreateWithFlags(&ev->e, cudaEventDisableTiming);
+  srf_event *ev = nullptr;
+  if (device >= 0 && device < 64) {
+    std::lock_guard<std::mutex> g(g_event_pool_mu);
+    if (!g_event_pool[device].empty()) {
+      ev = g_event_pool[device].back();
+      g_event_pool[device].pop_back();
+    }
+  }
+  cudaError_t e = cudaSuccess;
+  if (!ev) {
+    ev = new srf_event();
+    ev->device = device;
+    ev->pooled = device >= 0 && device < 64;
+    e = cudaEventCreateWithFlags(&ev->e, cudaEventDisableTiming);
+  }
   if (e == cudaSuccess) e = cudaEventRecord(ev->e, s);
   if (e != cudaSuccess) {
     delete ev;
@@ -29,6 +46,18 @@ static int record_event(int device, cudaStream_t s, srf_event_t *ev_out) {
   }
   *ev_out = ev;
   return SRF_OK;
+}
+
+static void release_event(srf_event *ev) {
+  if (ev->pooled) {
+    std::lock_guard<std::mutex> g(g_event_pool_mu);
+    if (g_event_pool[ev->device].size() < 4096) {
+      g_event_pool[ev->device].push_back(ev);
+      return;
+    }
+  }
+  cudaEventDestroy(ev->e);
+  delete ev;
 }
 
 static int launch_check(const char *what) {
@@ -52,6 +81,7 @@ static int g_force_sys = 0;  // knob 7 (tests): every put/get takes the cross-de
 static uint64_t g_put_timeout_ns = 5000000000ull;  // knob 8: credit wait limit of a put
 static int g_edge_ctas_per_sm = 2;   // knob 9: pipelined edge CTAs per SM
 static uint64_t g_edge_chunk = 0;    // knob 10: pipelined edge chunk (KiB; 0 = automatic)
+static int g_consume_threads = 32;   // knob 11: flag-only edge consumer CTA size
 
 // launch K1/K4/K5 with the configured implementation
 static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {

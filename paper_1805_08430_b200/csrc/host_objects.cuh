@@ -80,6 +80,7 @@ struct Doorbell {
 struct srf_event {
   int device;
   cudaEvent_t e;
+  bool pooled = false;  // a completion event from the per-device pool (no timing)
 };
 
 static constexpr uint64_t kAlign = 8;  // memspace.py:31 (_ALIGN)

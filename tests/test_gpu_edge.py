@@ -31,7 +31,8 @@ def _r256(n):
     (1, 1, 1, 9), (4097, 2, 3, 17), ((1 << 20) + 3, 4, 5, 23), (4 << 20, 3, 2, 12),
     (300_000, 8, 8, 40)])
 @pytest.mark.parametrize("sys_path", [0, 1])
-def test_rounds_delivered_in_order_bit_exact(nbytes, slots, nsrc, rounds, sys_path):
+@pytest.mark.parametrize("mirror", [False, True])
+def test_rounds_delivered_in_order_bit_exact(nbytes, slots, nsrc, rounds, sys_path, mirror):
     two = _lib.device_count() > 1
     if sys_path and two:
         pytest.skip("two GPUs: the peer path is taken anyway")
@@ -41,6 +42,9 @@ def test_rounds_delivered_in_order_bit_exact(nbytes, slots, nsrc, rounds, sys_pa
                     device=1 if two else 0)
     _lib.call("srf_connect", a.handle, b.handle)
     ra = a.allocate_region(nsrc * src_stride, register=True)
+    credit = a.allocate_region(4 * slots) if mirror else None
+    if mirror:
+        a.write_raw(credit.base_addr, b"\x00" * 4 * slots)
     rb = b.allocate_region(slots * slot_stride, register=True)
     sums = b.allocate_region(8 * rounds)
     rng = np.random.default_rng(nbytes + slots)
@@ -55,12 +59,15 @@ def test_rounds_delivered_in_order_bit_exact(nbytes, slots, nsrc, rounds, sys_pa
     _lib.call("srf_stream_create", a.handle, C.byref(st_a))
     _lib.call("srf_stream_create", b.handle, C.byref(st_b))
     edge = PipelinedStaticEdge(a, ra, nbytes, nsrc, src_stride, b, rb.base_addr,
-                               rb.access_token, slots, slot_stride)
+                               rb.access_token, slots, slot_stride,
+                               credit_addr=credit.base_addr if mirror else None)
     try:
         half = rounds // 2
         # the consumer (one CTA) first, so it is resident beside the sender grid
         PipelinedStaticEdge.consume(b, rb.base_addr, slots, slot_stride, nbytes, 0, rounds,
-                                    checksums_addr=sums.base_addr, stream=st_b)
+                                    checksums_addr=sums.base_addr,
+                                    credit=(a, credit.base_addr) if mirror else None,
+                                    stream=st_b)
         edge.send(half, st_a)            # two launches: round numbering continues
         edge.send(rounds - half, st_a)
         _lib.call("srf_stream_sync", st_a)
@@ -94,4 +101,7 @@ def test_edge_rejects_bad_token_and_bounds():
         PipelinedStaticEdge(a, ra, 4096, 1, 4096, b, rb.base_addr, rb.access_token, 300, 4352)
     with pytest.raises(errors.InvalidConfig):
         PipelinedStaticEdge(a, ra, 4096, 1, 4096, b, rb.base_addr, rb.access_token, 2, 4096)
+    with pytest.raises(errors.OutOfBounds):
+        PipelinedStaticEdge(a, ra, 4096, 1, 4096, b, rb.base_addr, rb.access_token, 2, 4352,
+                            credit_addr=(8 << 20) - 4)
     a.close(), b.close()

@@ -39,6 +39,26 @@ def test_device_stream_equals_numpy(n, e0, seed, node, it):
     sp.close()
 
 
+@pytest.mark.parametrize("offset", [4, 8, 12])
+@pytest.mark.parametrize("n,e0", [(3, 0), (1001, 0), (1001, 7), (70_000, 2)])
+def test_unaligned_destination(offset, n, e0):
+    """Arena blocks are only 8-B aligned (memspace.py:31): the head floats
+    before the first 16-B boundary take the scalar path."""
+    sp = MemorySpace(0, 1 << 20, seed=0, device=0)
+    reg = sp.allocate_region(4 * n + 64, register=True)
+    guard = b"\xee" * 16
+    sp.write_raw(reg.base_addr, guard)
+    sp.write_raw(reg.base_addr + offset + 4 * n, guard)
+    _lib.call("srf_gen_reference", sp.handle, reg.base_addr + offset, n, e0, 3, 5, 6, None,
+              None)
+    sp.sync()
+    got = np.frombuffer(sp.read_raw(reg.base_addr + offset, 4 * n), np.float32)
+    assert got.tobytes() == port.reference_values(3, 5, 6, e0, n).tobytes()
+    assert sp.read_raw(reg.base_addr, offset) == guard[:offset]
+    assert sp.read_raw(reg.base_addr + offset + 4 * n, 16) == guard
+    sp.close()
+
+
 def test_c1_golden_first_values(golden):
     """configs[0] payload: first four floats and the fp64 sum."""
     doc, _ = golden

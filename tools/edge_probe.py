@@ -22,7 +22,7 @@ def r256(n):
 
 
 class Side:
-    def __init__(self, src_dev, dst_dev, S, slots, nsrc):
+    def __init__(self, src_dev, dst_dev, S, slots, nsrc, mirror=False):
         self.S, self.slots = S, slots
         self.src_stride, self.slot_stride = r256(S), r256(S + 1)
         self.a = MemorySpace(10 + src_dev, nsrc * self.src_stride + 4 * MIB, seed=1,
@@ -31,6 +31,10 @@ class Side:
                              device=dst_dev)
         _lib.call("srf_connect", self.a.handle, self.b.handle)
         self.ra = self.a.allocate_region(nsrc * self.src_stride, register=True)
+        self.credit = None
+        if mirror:
+            self.credit = self.a.allocate_region(4 * slots)
+            self.a.write_raw(self.credit.base_addr, b"\x00" * 4 * slots)
         self.rb = self.b.allocate_region(slots * self.slot_stride, register=True)
         for i in range(slots):
             self.b.write_raw(self.rb.base_addr + i * self.slot_stride + S, b"\x00")
@@ -40,7 +44,8 @@ class Side:
         _lib.call("srf_stream_create", self.b.handle, C.byref(self.sb))
         self.edge = PipelinedStaticEdge(self.a, self.ra, S, nsrc, self.src_stride, self.b,
                                         self.rb.base_addr, self.rb.access_token, slots,
-                                        self.slot_stride)
+                                        self.slot_stride,
+                                        credit_addr=self.credit.base_addr if mirror else None)
         self.ev = [C.c_void_p(), C.c_void_p()]
         for e in self.ev:
             _lib.call("srf_timing_event_create", self.a.handle, C.byref(e))
@@ -48,7 +53,9 @@ class Side:
 
     def launch(self, rounds, timed=False):
         PipelinedStaticEdge.consume(self.b, self.rb.base_addr, self.slots, self.slot_stride,
-                                    self.S, self.next, rounds, stream=self.sb)
+                                    self.S, self.next, rounds, stream=self.sb,
+                                    credit=None if self.credit is None else
+                                    (self.a, self.credit.base_addr))
         if timed:
             _lib.call("srf_event_record_on", self.ev[0], self.sa)
         self.edge.send(rounds, self.sa)
@@ -73,10 +80,10 @@ class Side:
         self.a.close(), self.b.close()
 
 
-def run(mode, S, slots, rounds):
+def run(mode, S, slots, rounds, mirror=False):
     pairs = {"hbm": [(0, 0)], "nvl1": [(0, 1)], "nvl2": [(0, 1), (1, 0)]}[mode]
     nsrc = max(1, min(8, (256 * MIB) // max(S, 1)))
-    sides = [Side(s, d, S, slots, nsrc) for s, d in pairs]
+    sides = [Side(s, d, S, slots, nsrc, mirror) for s, d in pairs]
     for sd in sides:
         sd.launch(max(2, rounds // 4))
     for sd in sides:
@@ -89,24 +96,24 @@ def run(mode, S, slots, rounds):
     info = sides[0].edge.info()
     for sd in sides:
         sd.close()
-    return {"mode": mode, "bytes": S, "slots": slots, "rounds": rounds,
+    return {"mode": mode, "bytes": S, "slots": slots, "rounds": rounds, "mirror": mirror,
             "us_per_round": round(ms * 1e3 / rounds, 3),
             "gbps_per_dir": round(S * rounds / (ms / 1e3) / 1e9, 1),
             "chunk": info["chunk"], "ctas": info["ctas"]}
 
 
 if __name__ == "__main__":
-    sizes = [int(x) for x in sys.argv[1:]] or [KIB, 64 * KIB, MIB, 4 * MIB, 16 * MIB,
-                                                 64 * MIB, 256 * MIB]
-    modes = ["hbm"] + (["nvl1", "nvl2"] if ndev > 1 else [])
-    for knob in [dict(), dict(edge_ctas_per_sm=1), dict(edge_ctas_per_sm=3)]:
-        for k, v in knob.items():
-            _lib.tune(k, v)
-        for mode in modes:
-            for S in sizes:
-                for slots in (1, 2, 4, 8):
-                    rounds = max(8, min(400, int(2e9 // max(S, 1) // 8)))
-                    row = run(mode, S, slots, rounds)
-                    row.update(knob)
-                    print(json.dumps(row), flush=True)
-        _lib.tune("edge_ctas_per_sm", 2)
+    sizes = [int(x) for x in sys.argv[1:]] or [MIB, 4 * MIB, 16 * MIB, 64 * MIB, 256 * MIB]
+    modes = (["nvl1", "nvl2"] if ndev > 1 else []) + ["hbm"]
+    for mode in modes:
+        for S in sizes:
+            for chunk_kib in ([0, 64, 128] if S <= 64 * MIB else [0]):
+                _lib.tune("edge_chunk_kib", chunk_kib)
+                for mirror in ((False, True) if mode != "hbm" else (False,)):
+                    for slots in (2, 4, 8, 16):
+                        # enough rounds that every slot is reused many times
+                        rounds = max(16 * slots, min(400, int(4e9 // S)))
+                        row = run(mode, S, slots, rounds, mirror)
+                        row["chunk_kib_knob"] = chunk_kib
+                        print(json.dumps(row), flush=True)
+    _lib.tune("edge_chunk_kib", 0)

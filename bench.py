@@ -343,6 +343,181 @@ def bench_sendrecv_device(S, steps, warmup, rank, world, device):
             "ring": ring, "copy_engine_gbps": ce}
 
 
+class PipelinedRing:
+    """The headline Send/Recv edge: a pipelined static edge (srf_edge_*,
+    EXTENSION of static placement - `slots` pre-placed receive regions, the
+    reference protocol per slot) carrying R rounds per launch.  N=1: server 0
+    -> server 1 on one GPU (HBM).  N>1: rank r -> rank r+1 over NVLink, every
+    rank also consuming rank r-1's rounds on its own GPU; the consumer mirrors
+    each credit into the sender's pool.  Payloads are the reference
+    microbenchmark's tensor (build_microbench GenGrad node 0, graph.py:333-350)
+    of iterations 2, 3, ... generated on the device (srf_gen_reference)."""
+
+    def __init__(self, S, rank, world, device, slots=8, nsrc=2):
+        import ctypes as C
+        from paper_1805_08430_b200 import _lib
+        from paper_1805_08430_b200.distributed import exchange_spaces, lookup, publish_addresses
+        from paper_1805_08430_b200.memspace import MemorySpace
+        from paper_1805_08430_b200.runtime.protocol import PipelinedStaticEdge
+        from paper_1805_08430_b200.wire import AddrExchangeMsg, Mechanism
+        self.lib, self.S, self.world, self.rank, self.slots, self.nsrc = \
+            _lib, S, world, rank, slots, nsrc
+        self.src_stride = (S + 255) & ~255
+        self.slot_stride = (S + 1 + 255) & ~255
+        src_len, slot_len = nsrc * self.src_stride, slots * self.slot_stride
+        credit_len = 4 * slots
+        self.src = MemorySpace(rank if world > 1 else 0, src_len + slot_len + (8 << 20), seed=0,
+                               device=device)
+        self.payloads = self.src.allocate_region(src_len, register=True)
+        for i in range(nsrc):   # microbench GenGrad node 0 at iteration 2 + i
+            _lib.call("srf_gen_reference", self.src.handle,
+                      self.payloads.base_addr + i * self.src_stride, S // 4, 0, 0, 0, 2 + i,
+                      None, None)
+        if world == 1:
+            self.rcv = MemorySpace(1, slot_len + (8 << 20), seed=0, device=device)
+            self.slots_reg = self.rcv.allocate_region(slot_len, register=True)
+            self.credit = None
+            _lib.call("srf_connect", self.src.handle, self.rcv.handle)
+            dst_space, dst_addr, dst_tok = self.rcv, self.slots_reg.base_addr, \
+                self.slots_reg.access_token
+            self.credit_for_consumer = None
+        else:
+            self.rcv = self.src
+            self.slots_reg = self.src.allocate_region(slot_len, register=True)
+            self.credit = self.src.allocate_region(credit_len)
+            nxt, prv = (rank + 1) % world, (rank - 1) % world
+            self.proxies = exchange_spaces(self.src, peers=sorted({nxt, prv}))
+            pub = publish_addresses([AddrExchangeMsg(rank, self.slots_reg.base_addr,
+                                                     self.slots_reg.access_token, slot_len,
+                                                     Mechanism.STATIC)])
+            msg = lookup(pub, nxt, nxt, Mechanism.STATIC)
+            dst_space, dst_addr, dst_tok = self.proxies[nxt], msg.base_addr, msg.token
+            # the previous rank's credit words sit at the same offset of its pool
+            self.credit_for_consumer = (self.proxies[prv], self.credit.base_addr)
+        for i in range(slots):
+            self.rcv.write_raw(self.slots_reg.base_addr + i * self.slot_stride + S, b"\x00")
+        if self.credit is not None:
+            self.src.write_raw(self.credit.base_addr, b"\x00" * credit_len)
+        self.src.sync(), self.rcv.sync()
+        barrier_sync()
+        self.edge = PipelinedStaticEdge(
+            self.src, self.payloads, S, nsrc, self.src_stride, dst_space, dst_addr, dst_tok,
+            slots, self.slot_stride,
+            credit_addr=None if self.credit is None else self.credit.base_addr)
+        self.st_send, self.st_recv = C.c_void_p(), C.c_void_p()
+        _lib.call("srf_stream_create", self.src.handle, C.byref(self.st_send))
+        _lib.call("srf_stream_create", self.rcv.handle, C.byref(self.st_recv))
+        self.consumed = 0
+        self.info = self.edge.info()
+
+    def launch(self, rounds, ev_before=None, ev_after=None):
+        """Consumer first (it must be resident beside the sender grid), then
+        one sender launch of `rounds` rounds; events bracket the sender."""
+        from paper_1805_08430_b200.runtime.protocol import PipelinedStaticEdge
+        PipelinedStaticEdge.consume(self.rcv, self.slots_reg.base_addr, self.slots,
+                                    self.slot_stride, self.S, self.consumed, rounds,
+                                    credit=self.credit_for_consumer, stream=self.st_recv)
+        self.consumed += rounds
+        if ev_before is not None:
+            self.lib.call("srf_event_record_on", ev_before, self.st_send)
+        self.edge.send(rounds, self.st_send)
+        if ev_after is not None:
+            self.lib.call("srf_event_record_on", ev_after, self.st_send)
+
+    def event(self):
+        import ctypes as C
+        ev = C.c_void_p()
+        self.lib.call("srf_timing_event_create", self.src.handle, C.byref(ev))
+        return ev
+
+    def elapsed_ms(self, a, b) -> float:
+        import ctypes as C
+        ms = C.c_float()
+        self.lib.call("srf_event_elapsed_ms", a, b, C.byref(ms))
+        return ms.value
+
+    def sync(self):
+        self.lib.call("srf_stream_sync", self.st_send)
+        self.lib.call("srf_stream_sync", self.st_recv)
+        self.src.sync()
+        self.rcv.sync()
+
+    def verify(self) -> bool:
+        """Every slot holds, bit for bit, the payload of the last round that
+        used it (the received round j carries payload j % nsrc)."""
+        import hashlib
+        from paper_1805_08430_b200.distributed import all_gather_objects
+        n = self.edge.info()["next_round"]
+        srcs = [hashlib.sha256(self.src.read_raw(self.payloads.base_addr + i * self.src_stride,
+                                                 self.S)).hexdigest() for i in range(self.nsrc)]
+        got = {}
+        for j in range(max(0, self.consumed - self.slots), self.consumed):
+            raw = self.rcv.read_raw(self.slots_reg.base_addr + (j % self.slots) * self.slot_stride,
+                                    self.S + 1)
+            got[j] = (hashlib.sha256(raw[:self.S]).hexdigest(), raw[self.S])
+        everyone = all_gather_objects(srcs)
+        sender = (self.rank - 1) % self.world if self.world > 1 else 0
+        want = everyone[sender]
+        return n == self.consumed and all(h == want[j % self.nsrc] and f == 0
+                                          for j, (h, f) in got.items())
+
+    def close(self):
+        self.sync()
+        self.edge.close()
+        for st in (self.st_send, self.st_recv):
+            self.lib.call("srf_stream_destroy", st)
+        barrier_sync()
+        for p in getattr(self, "proxies", {}).values():
+            p.close()
+        barrier_sync()
+        if self.rcv is not self.src:
+            self.rcv.close()
+        self.src.close()
+
+
+def bench_pipelined(S, steps, warmup, rank, world, device, slots=8):
+    """Headline device timing: K steps, each one k_put_stream launch of R
+    rounds (R calibrated to ~25 ms per step) with its consumer, max over
+    ranks; the roofline kernel is k_put_stream (algorithmic bytes per launch:
+    R * (S+1) over NVLink at N>1, R * (2S+1) through HBM at N=1)."""
+    from paper_1805_08430_b200 import _lib
+    ring = PipelinedRing(S, rank, world, device, slots=slots)
+    a, b = ring.event(), ring.event()
+    ring.launch(2 * slots)
+    ring.sync()
+    barrier_sync()
+    ring.launch(4 * slots, a, b)
+    ring.sync()
+    t_round = dist_max(ring.elapsed_ms(a, b)) / (4 * slots)
+    rounds = int(dist_max(float(max(2 * slots, min(1 << 16, round(25.0 / max(t_round, 1e-4)))))))
+    for _ in range(warmup):
+        ring.launch(rounds)
+    ring.sync()
+    ev = [(ring.event(), ring.event()) for _ in range(steps)]
+    start, end = ring.event(), ring.event()
+    clocks = ClockSampler(device)
+    clocks.start()
+    barrier_sync()
+    l0 = _lib.launch_count()
+    ring.lib.call("srf_event_record_on", start, ring.st_send)
+    for i in range(steps):
+        ring.launch(rounds, *ev[i])
+    ring.lib.call("srf_event_record_on", end, ring.st_send)
+    ring.sync()
+    launches = int(dist_sum(_lib.launch_count() - l0))
+    barrier_sync()
+    clk = clocks.stop()
+    total_ms = dist_max(ring.elapsed_ms(start, end))
+    launch_ms = dist_max(statistics.fmean(ring.elapsed_ms(x, y) for x, y in ev))
+    ok = dist_sum(0.0 if ring.verify() else 1.0) == 0.0
+    info = ring.info
+    ring.close()
+    return {"total_ms": total_ms, "rounds": rounds, "n": steps * rounds, "launch_ms": launch_ms,
+            "verified": ok, "launches": launches, "clocks": clk, "slots": slots,
+            "chunk": info["chunk"], "chunks_per_round": info["chunks_per_round"],
+            "ctas": info["ctas"], "t_round_ms": t_round}
+
+
 def copy_engine_comparator(ring, S, device, reps=10):
     """Comparator only (not on the path): the DMA copy engine moving the same
     payload into the same destination mapping (cudaMemcpy via torch), per
@@ -656,6 +831,10 @@ def sweep(max_bytes, device):
         row["static_1launch_us"] = _ring_graph_us(ring.stream, ring.put_consume, rounds,
                                                   ring.src)
         row["static_1launch_gbps"] = round(size / row["static_1launch_us"] / 1e3, 3)
+        pipe = bench_pipelined(size, 3, 2, 0, 1, device, slots=8)
+        row["static_pipelined_us"] = round(pipe["total_ms"] * 1e3 / pipe["n"], 3)
+        row["static_pipelined_gbps"] = round(size / row["static_pipelined_us"] / 1e3, 3)
+        row["static_pipelined_verified"] = pipe["verified"]
         row.update(dynamic_rate(size, device))
         row.update(dynamic_device_rate(size, device))
         row.update(rpc_device_rate(size, device))
@@ -731,8 +910,9 @@ def dynamic_device_rate(size, device, rounds=None):
 
 def sweep_nvlink(max_bytes, rank, world, device):
     """configs[1] over NVLink (N>1): every rank sends to rank+1 at once,
-    1 KiB x 4^k up to max_bytes; static zero-copy (K1 + K2, copy-engine body
-    >= 32 MiB) and dynamic with the receiver on the device (K3 + srf_dyn_recv
+    1 KiB x 4^k up to max_bytes; static zero-copy (the reference's one slot:
+    K1 + K2 per round), the pipelined edge (8 slots, R rounds per launch) and
+    dynamic with the receiver on the device (K3 + srf_dyn_recv
     pulling from the previous rank's pool), graph-replayed rounds, device
     time, max over ranks."""
     from paper_1805_08430_b200 import _lib
@@ -753,6 +933,10 @@ def sweep_nvlink(max_bytes, rank, world, device):
                                                   ring.src)
         row["static_1launch_gbps"] = round(size / row["static_1launch_us"] / 1e3, 3)
         row["verified"] = dist_sum(0.0 if ring.verify() else 1.0) == 0.0
+        pipe = bench_pipelined(size, 3, 2, rank, world, device, slots=8)
+        row["static_pipelined_us"] = round(pipe["total_ms"] * 1e3 / pipe["n"], 3)
+        row["static_pipelined_gbps"] = round(size / row["static_pipelined_us"] / 1e3, 3)
+        row["static_pipelined_verified"] = pipe["verified"]
         dyn = DynDeviceRing(size, rank, world, device)
         for _ in range(4):
             dyn.step()
@@ -1161,17 +1345,20 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
                     if w % world != L.shard_of(v) % world)
             if k:
                 chain = max(chain, (k + 1) * L.nbytes(v) + k)
-        bound_bytes = max(per_gpu[hot], chain)
-        ach = bound_bytes * steps / t / 1e9
+        # headline: the bytes that crossed the busiest GPU's link; the
+        # dependency-limited figure is reported beside it, labelled
+        ach = per_gpu[hot] * steps / t / 1e9
         roof = {"bound": "nvlink", "achieved": round(ach, 1), "peak": NVLINK_MEASURED_GBS,
                 "unit": "GB/s", "frac": round(ach / NVLINK_MEASURED_GBS, 4),
                 "hottest_gpu": hot, "hottest_bytes_per_step": per_gpu[hot],
                 "chain_bytes_per_step": chain,
-                "frac_link_only": round(per_gpu[hot] * steps / t / 1e9 / NVLINK_MEASURED_GBS, 4),
-                "note": "bytes per step = max(busiest GPU's max(NVLink egress, ingress), the "
+                "frac_of_dependency_bound": round(max(per_gpu[hot], chain) * steps / t / 1e9
+                                                  / NVLINK_MEASURED_GBS, 4),
+                "note": "achieved = the busiest GPU's max(NVLink egress, ingress) bytes per "
+                        "step x steps/s; frac_of_dependency_bound uses max(those bytes, the "
                         "largest variable's push-then-pull chain (k+1)*S for k remote "
-                        "workers); servers on the "
-                        "same GPU exchange through HBM and are not counted"}
+                        "workers) instead; servers on the same GPU exchange through HBM and "
+                        "are not counted"}
     out = {"workload": f"{label}, op={op} lr=0.01",
            "steps_per_s": round(steps / t, 2), "ms_per_step": round(t / steps * 1e3, 4),
            "steps": steps, "model_bytes": model, "roofline": roof, "gpu_launches": launches,
@@ -1232,6 +1419,53 @@ def bench_ps_configs(rank, world, device, steps, warmup, op, cpu):
     return out
 
 
+def bench_c1(rank, world, device, cpu=True):
+    """configs[0] / SURVEY 8(d) C1: one 1 MiB fp32 tensor, static placement,
+    1 sender -> 1 receiver (N=1: one GPU; N>1: the NVLink ring).  Device time
+    of the reference's one-slot protocol (K1 put + K2 consume per transfer,
+    graph-replayed), the pipelined edge, e2e through the public endpoints
+    (pinned H2D of the payload, StaticSender.send -> StaticReceiver.poll ->
+    ReduceMax, 4-B result read back) and the reference CPU arm."""
+    S = 1 << 20
+    single = bench_sendrecv_device(S, 10, 3, rank, world, device)
+    pipe = bench_pipelined(S, 5, 3, rank, world, device, slots=8)
+    e2e = bench_sendrecv_e2e(S, 200, 5, rank, world, device)
+    us = single["total_ms"] * 1e3 / single["n"]
+    us_pipe = pipe["total_ms"] * 1e3 / pipe["n"]
+    per_dir = S / (us * 1e-6) / 1e9
+    if world == 1:
+        peak, src = measured_peaks()
+        alg = 2 * S + 1
+    else:
+        peak, src = NVLINK_MEASURED_GBS, "B200_PROFILING.md measured peer copy"
+        alg = S + 1
+    out = {
+        "workload": f"configs[0] 1 MiB fp32 static Send/Recv "
+                    f"({'server 0 -> 1 on GPU 0' if world == 1 else 'ring over NVLink'})",
+        "us_per_transfer": round(us, 3), "gbps_per_dir": round(per_dir, 2),
+        "roofline": {"bound": "hbm" if world == 1 else "nvlink",
+                     "achieved": round(alg / (us * 1e-6) / 1e9, 2), "peak": peak,
+                     "frac": round(alg / (us * 1e-6) / 1e9 / peak, 4), "unit": "GB/s",
+                     "bytes_per_transfer": alg, "peak_source": src,
+                     "note": "latency-bound: launch + grid arrival + flag release + poll per "
+                             "transfer"},
+        "pipelined": {"us_per_round": round(us_pipe, 3),
+                      "gbps_per_dir": round(S / (us_pipe * 1e-6) / 1e9, 2),
+                      "slots": pipe["slots"], "verified": pipe["verified"]},
+        "e2e": {"value": round(world * S * 200 / e2e["seconds"] / 1e9, 3), "unit": "GB/s",
+                "us_per_transfer": round(e2e["seconds"] / 200 * 1e6, 2),
+                "h2d_bytes_per_step": e2e["h2d"] * world, "d2h_bytes_per_step": e2e["d2h"] * world,
+                "verified": e2e["verified"]},
+        "verified": single["verified"] and pipe["verified"] and e2e["verified"],
+    }
+    if cpu and rank == 0 and world == 1:
+        gbps, n, dt, kind, what = cpu_reference(S, min_seconds=3.0)
+        out["cpu_baseline"] = {"value": round(gbps, 4), "unit": "GB/s", "cores": 1, "kind": kind,
+                               "us_per_transfer": round(dt / n * 1e6, 1),
+                               "sample": f"{n} transfers of 1 MiB ({what})"}
+    return out
+
+
 def bench_ps_session(rank, world, device, steps, warmup, op, cpu):
     """configs[2]-[4] through the reference's public entry point:
     ``Session(build_ps_workload(...)).run(n)`` (runtime/session.py:606-629) -
@@ -1289,7 +1523,16 @@ def bench_ps_session(rank, world, device, steps, warmup, op, cpu):
                 ok = ok and part.tobytes() == want.tobytes()
         sess.close()
         row = report.rows[-1]
+        # HBM bytes of one iteration, all servers on one GPU: per (variable,
+        # remote worker) K1 push 2S, GenGrad S, K4 pull 2S, K6 update 3S
+        alg = sum(8 * 4 * math.prod(sh) * W for sh in shapes)
+        peak, _src = measured_peaks()
+        ach = alg * n / dt / 1e9
         out[name] = {
+            "roofline": {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(ach / peak, 4), "bytes_per_step": alg,
+                         "note": "one synchronous verb at a time (the reference's executor): "
+                                 "host round trips, not HBM, bound this line"},
             "workload": f"{label} ({total_params(shapes)} fp32) through Session.run, op={op}",
             "steps_per_s": round(n / dt, 3), "ms_per_step": round(dt / n * 1e3, 3), "steps": n,
             "e2e": {"value": round(n / (dt + d2h), 3), "unit": "steps/s",
@@ -1347,30 +1590,35 @@ def main() -> int:
     init_process_group("nccl")
     S = args.bytes
 
-    dev = bench_sendrecv_device(S, args.steps, args.warmup, rank, world, local)
+    dev = bench_pipelined(S, args.steps, args.warmup, rank, world, local)
+    # the reference's one-slot protocol (one K1 + K2 round per transfer) as a
+    # comparator line, and the DMA copy engine through the same mapping
+    single = bench_sendrecv_device(S, max(3, args.steps // 4), args.warmup, rank, world, local)
     e2e = bench_sendrecv_e2e(S, max(3, args.steps // 2), args.warmup, rank, world, local)
 
     total_bytes = world * S * dev["n"]
     value = total_bytes / (dev["total_ms"] / 1e3) / 1e9
     hbm_peak, hbm_src = measured_peaks()
-    put_s = dev["put_avg_ms"] / 1e3
+    launch_s = dev["launch_ms"] / 1e3
+    R = dev["rounds"]
     if world == 1:
-        alg = 2 * S + 1
-        roof = {"bound": "hbm", "achieved": round(alg / put_s / 1e9, 2), "peak": hbm_peak,
-                "unit": "GB/s", "frac": round(alg / put_s / 1e9 / hbm_peak, 4),
-                "kernel": "k_put (K1 static_put)", "bytes_per_launch": alg,
-                "peak_source": hbm_src}
+        alg = R * (2 * S + 1)
+        roof = {"bound": "hbm", "achieved": round(alg / launch_s / 1e9, 2), "peak": hbm_peak,
+                "unit": "GB/s", "frac": round(alg / launch_s / 1e9 / hbm_peak, 4),
+                "kernel": "k_put_stream (pipelined K1: R rounds per launch)",
+                "bytes_per_launch": alg, "peak_source": hbm_src}
     else:
-        alg = S + 1
-        ach = alg / put_s / 1e9
+        alg = R * (S + 1)
+        ach = alg / launch_s / 1e9
         roof = {"bound": "nvlink", "achieved": round(ach, 2), "peak": NVLINK_MEASURED_GBS,
                 "unit": "GB/s", "frac": round(ach / NVLINK_MEASURED_GBS, 4),
                 "frac_of_nominal_900": round(ach / NVLINK_NOMINAL_GBS, 4),
-                "kernel": "K1 static_put: copy-engine body (knob 6, cross-device >= 32 MiB) "
-                          "+ k_put tail release", "bytes_per_launch": alg,
+                "kernel": "k_put_stream (pipelined K1, SM stores into the peer's slots; no "
+                          "copy engine)", "bytes_per_launch": alg,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction "
                                "(nominal 900)"}
     roof["traffic"] = traffic_from_profiles(world)
+    single_gbps = world * S * single["n"] / (single["total_ms"] / 1e3) / 1e9
 
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
@@ -1378,6 +1626,7 @@ def main() -> int:
         "ms_per_step": round(dev["total_ms"] / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {**workload_config(S, world), "rounds_per_step": dev["rounds"],
+                   "slots": dev["slots"], "chunk_bytes": dev["chunk"],
                    "cpu_affinity": affinity},
         "roofline": roof,
         "e2e": {"value": round(world * S * max(3, args.steps // 2) / e2e["seconds"] / 1e9, 3),
@@ -1388,14 +1637,13 @@ def main() -> int:
         "gpu_launches": dev["launches"],
         "clocks": dev["clocks"],
         "verified": dev["verified"],
-        "comparators": {"copy_engine_gbps_per_gpu": dev["copy_engine_gbps"],
-                        "k1_gbps_per_gpu": round(S / put_s / 1e9, 1),
-                        "note": ("DMA copy engine (cudaMemcpy) into the same destination "
-                                 "mapping - comparator only, not on the path" if world == 1
-                                 else "raw cudaMemcpy ceiling through the same peer mapping; "
-                                      "K1 moves bodies >= 32 MiB on the same engine (with "
-                                      "both directions busy, SM-driven NVLink traffic of "
-                                      "one GPU shares one ceiling)")},
+        "single_slot": {"gbps": round(single_gbps, 1), "verified": single["verified"],
+                        "k1_gbps_per_gpu": round(S / single["put_avg_ms"] * 1e3 / 1e9, 1),
+                        "note": "the reference's one receive region per edge: one K1 put + "
+                                "one K2 consume per round (graph-replayed)"},
+        "comparators": {"copy_engine_gbps_per_gpu": single["copy_engine_gbps"],
+                        "note": "DMA copy engine (cudaMemcpy) into the same destination "
+                                "mapping - comparator only, not on the path"},
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         gbps, n, dt, kind, what = cpu_reference(S, min_seconds=args.cpu_seconds)
@@ -1413,6 +1661,7 @@ def main() -> int:
             log(f"section {key} failed: {type(exc).__name__}: {exc}")
             line[key] = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
+    section("c1", lambda: bench_c1(rank, world, local, not args.no_cpu))
     if world > 1 and not args.no_sweep:
         section("sweep_nvlink", lambda: sweep_nvlink(S, rank, world, local))
     if world == 1 and not args.no_sweep:
@@ -1472,7 +1721,7 @@ def main() -> int:
         c.get("verified", True) for k in ("ps_configs", "ps_session")
         for c in line.get(k, {}).values() if isinstance(c, dict)) and all(line.get(k, {}).get("verified", True) for k in
                                       ("ps_balanced", "ps_sliced", "ps_partitioned"))
-    if not dev["verified"] or not e2e["verified"] or not ps_ok:
+    if not dev["verified"] or not single["verified"] or not e2e["verified"] or not ps_ok:
         log("verification FAILED")
         return 1
     return 0

@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(256) k_put_bulk(PutArgs a) {
       }
       __syncthreads();
     } else {
-      copy_bytes_grid(d, s, n, t, nth);
+      copy_bytes_grid(d, s, n, t, nth, !a.src_remote);
     }
   }
   if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");

@@ -71,12 +71,12 @@ static int launch_check(const char *what) {
 static int g_put_impl = 0;  // 0 = vector LDG/STG, 1 = TMA bulk (large segments)
 static int g_unroll = 8;    // 16-B vectors in flight per thread (4 or 8)
 // knob 6: cross-device bodies of at least this many bytes move on the copy
-// engine (0: never).  With both NVLink directions busy (the ring), SM-driven
-// traffic of one GPU shares one ceiling and K1 gets ~616 GB/s per direction
-// at 256 MiB, the copy engines 713 (profiles/r1_align_probe.txt, duplex
-// probe); the engine's extra ~15 us per put (credit-wait launch, copy, tail
-// launch) only pays off from ~64 MiB: threshold 32 MiB.
-static uint64_t g_peer_ce_bytes = 32ull << 20;
+// engine (0: never, the default - every byte moves in a kernel).  Kept as a
+// labelled comparator: round 1 used it from 32 MiB because one-slot K1
+// rounds got ~616 GB/s per direction in the ring vs the engine's 713; the
+// pipelined edge (srf_edge_*) reaches ~707 with SM stores alone
+// (profiles/r2_edge_probe.jsonl).
+static uint64_t g_peer_ce_bytes = 0;
 static int g_force_sys = 0;  // knob 7 (tests): every put/get takes the cross-device path
 static uint64_t g_put_timeout_ns = 5000000000ull;  // knob 8: credit wait limit of a put
 static int g_edge_ctas_per_sm = 2;   // knob 9: pipelined edge CTAs per SM
@@ -87,8 +87,9 @@ static int g_consume_threads = 32;   // knob 11: flag-only edge consumer CTA siz
 static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
   uint64_t big = 0;
   for (int i = 0; i < a.nseg; ++i) big = std::max<uint64_t>(big, a.seg[i].len);
-  // the TMA variant has no fused consume and no source-aligned pull path
-  if (g_put_impl == 1 && big >= (uint64_t)4 * kBulkChunk && !a.consume && !a.src_remote) {
+  // the TMA variant has no fused consume (its non-bulk remainder keeps the
+  // pull's source-aligned sectors)
+  if (g_put_impl == 1 && big >= (uint64_t)4 * kBulkChunk && !a.consume) {
     static bool attr_set[64] = {false};
     if (s->device >= 0 && s->device < 64 && !attr_set[s->device]) {
       CUDA_TRY(cudaFuncSetAttribute(k_put_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -47,6 +47,7 @@ def _alias() -> None:
         mod.__package__ = "rdmaflow"
         sys.modules["rdmaflow.benchcli"] = mod
         spec.loader.exec_module(mod)
+        pkg.benchcli = mod
 
 
 _alias()

@@ -196,7 +196,7 @@ def peer_engine(request):
     _lib.tune("peer_ce_kib", 1 if request.param == "copy_engine" else 0)
     _lib.tune("force_sys", 1 if one_gpu and request.param != "sm" else 0)
     yield request.param
-    _lib.tune("peer_ce_kib", 32768)
+    _lib.tune("peer_ce_kib", 0)
     _lib.tune("force_sys", 0)
 
 
@@ -466,7 +466,7 @@ def test_timed_out_credit_leaves_receiver_untouched(pair, force_sys, impl):
         _lib.tune("put_timeout_ms", 5000)
         _lib.tune("put_impl", 0)
         _lib.tune("force_sys", 0)
-        _lib.tune("peer_ce_kib", 32768)
+        _lib.tune("peer_ce_kib", 0)
 
 
 @pytest.mark.parametrize("size", [65536, (1 << 20) + 16, (5 << 20) + 3])

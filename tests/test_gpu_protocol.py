@@ -87,7 +87,7 @@ class TestStatic:
                 t.buffer.release()
             rig.close()
         finally:
-            _lib.tune("peer_ce_kib", 32768)
+            _lib.tune("peer_ce_kib", 0)
 
     def test_size_mismatch(self):
         rig = Rig()

@@ -384,3 +384,35 @@ def test_device_pcg_stream_on_host(tmp_path):
         want = port.synthesize(e0 + n, 0, port.node_rng(seed, node, it))[e0:]
         assert got.tobytes() == want.tobytes(), (seed, node, it, n, e0, nth)
         assert got.tobytes() == port.reference_values(seed, node, it, e0, n).tobytes()
+
+
+def test_reference_harness_times_the_real_reference():
+    """oracle/ref_harness.py drives the vendored reference (oracle/_ref, or
+    /root/reference here) through its own endpoints; the RPC ring moves the
+    same bytes at ~0.2x the zero-copy rate, as in the reference."""
+    from oracle import ref_harness as R
+    if R.reference() is None:
+        pytest.skip("reference not vendored")
+    for mech in ("static", "dynamic", "rpc"):
+        rig = R.EndpointRig(64 << 10, mech)
+        a, b = rig.step(), rig.step()
+        assert a == b and 0.0 <= a < 1.0     # ReduceMax of uniform [0, 1) floats
+    arm = R.PsArm([(64,), (7, 3)], 2, 1)
+    arm.step()
+
+
+def test_ref_alias_plugin_maps_the_package():
+    """tests/ref_alias.py (the reference suite's alias plugin) maps every
+    rdmaflow module to this package; benchcli is the reference's own."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    if not os.path.isdir(os.path.join(root, "oracle", "_ref", "rdmaflow")):
+        pytest.skip("reference not vendored")
+    code = ("import sys; sys.path[:0] = ['tests', '.']; import ref_alias; "
+            "import rdmaflow.runtime.session as s, rdmaflow.memspace as m, rdmaflow.benchcli as b; "
+            "assert s.__name__ == 'paper_1805_08430_b200.runtime.session'; "
+            "assert m.__name__ == 'paper_1805_08430_b200.memspace'; "
+            "assert b.Session is s.Session; print('ok')")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]

@@ -68,3 +68,22 @@ def push_sm(st):
     _lib.tune("peer_ce_kib", 1024)
 res["push_sm+pull_ce"] = timed([(push_sm, sa[0]), (pull, sa[1])])
 print(json.dumps(res), flush=True)
+
+# round 2: the pull through the async proxy (TMA cp.async.bulk peer global ->
+# shared -> local global, put_impl 1) beside SM-store pushes, SM engines only
+_lib.tune("peer_ce_kib", 0)
+res2 = {}
+def pull_tma(st):
+    _lib.tune("put_impl", 1)
+    pull(st)
+    _lib.tune("put_impl", 0)
+def push_tma(st):
+    _lib.tune("put_impl", 1)
+    push(st)
+    _lib.tune("put_impl", 0)
+res2["pull_tma"] = timed([(pull_tma, sa[0])])
+res2["push_sm+pull_tma"] = timed([(push, sa[0]), (pull_tma, sa[1])])
+res2["push_tma+pull_sm"] = timed([(push_tma, sa[0]), (pull, sa[1])])
+res2["push_tma+pull_tma"] = timed([(push_tma, sa[0]), (pull_tma, sa[1])])
+res2["push_sm+pull_sm"] = timed([(push, sa[0]), (pull, sa[1])])
+print(json.dumps(res2), flush=True)

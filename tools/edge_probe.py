@@ -51,11 +51,15 @@ class Side:
             _lib.call("srf_timing_event_create", self.a.handle, C.byref(e))
         self.next = 0
 
-    def launch(self, rounds, timed=False):
+    def consume(self, rounds):
         PipelinedStaticEdge.consume(self.b, self.rb.base_addr, self.slots, self.slot_stride,
                                     self.S, self.next, rounds, stream=self.sb,
                                     credit=None if self.credit is None else
                                     (self.a, self.credit.base_addr))
+
+    def launch(self, rounds, timed=False):
+        """(every side's consume() must have been queued first: a consumer
+        launched after a full-GPU sender grid may not fit beside it)"""
         if timed:
             _lib.call("srf_event_record_on", self.ev[0], self.sa)
         self.edge.send(rounds, self.sa)
@@ -85,9 +89,13 @@ def run(mode, S, slots, rounds, mirror=False):
     nsrc = max(1, min(8, (256 * MIB) // max(S, 1)))
     sides = [Side(s, d, S, slots, nsrc, mirror) for s, d in pairs]
     for sd in sides:
+        sd.consume(max(2, rounds // 4))
+    for sd in sides:
         sd.launch(max(2, rounds // 4))
     for sd in sides:
         sd.sync()
+    for sd in sides:
+        sd.consume(rounds)
     for sd in sides:
         sd.launch(rounds, timed=True)
     for sd in sides:
@@ -104,10 +112,12 @@ def run(mode, S, slots, rounds, mirror=False):
 
 if __name__ == "__main__":
     sizes = [int(x) for x in sys.argv[1:]] or [MIB, 4 * MIB, 16 * MIB, 64 * MIB, 256 * MIB]
-    modes = (["nvl1", "nvl2"] if ndev > 1 else []) + ["hbm"]
+    modes = os.environ.get("PROBE_MODES", "nvl1,nvl2,hbm").split(",")
+    if ndev < 2:
+        modes = [m for m in modes if m == "hbm"]
     for mode in modes:
         for S in sizes:
-            for chunk_kib in ([0, 64, 128] if S <= 64 * MIB else [0]):
+            for chunk_kib in ([0, 128] if S <= 64 * MIB else [0]):
                 _lib.tune("edge_chunk_kib", chunk_kib)
                 for mirror in ((False, True) if mode != "hbm" else (False,)):
                     for slots in (2, 4, 8, 16):

@@ -23,7 +23,9 @@ for mib in [int(x) for x in os.environ.get("PROBE_SLICES", "0,64,16,4").split(",
     if os.environ.get("PROBE_PARTITION"):
         kw.update(placement="bytes", partition_bytes=int(os.environ["PROBE_PARTITION"]) << 20)
     cfg = os.environ.get("PROBE_CFG", "vgg")
-    if cfg == "vgg":
+    if cfg == "vgg" and world == 1:   # N=1: worker server 0 + PS server 1 on GPU 0
+        L = PsLayout(vgg16_shapes(), 1, 1, False, **kw)
+    elif cfg == "vgg":
         L = PsLayout(vgg16_shapes(), world, world, colocate=True, **kw)
     elif cfg == "fcn5":   # configs[2] preset: 2 workers + 1 PS, server s on GPU s % world
         L = PsLayout([(int(204.47e6) // 10 // 4,)] * 10, 2, 1, False, **kw)

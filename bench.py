@@ -348,12 +348,12 @@ class PipelinedRing:
     EXTENSION of static placement - `slots` pre-placed receive regions, the
     reference protocol per slot) carrying R rounds per launch.  N=1: server 0
     -> server 1 on one GPU (HBM).  N>1: rank r -> rank r+1 over NVLink, every
-    rank also consuming rank r-1's rounds on its own GPU; the consumer mirrors
-    each credit into the sender's pool.  Payloads are the reference
+    rank also consuming rank r-1's rounds on its own GPU (optionally mirroring
+    each credit into the sender's pool).  Payloads are the reference
     microbenchmark's tensor (build_microbench GenGrad node 0, graph.py:333-350)
     of iterations 2, 3, ... generated on the device (srf_gen_reference)."""
 
-    def __init__(self, S, rank, world, device, slots=8, nsrc=2):
+    def __init__(self, S, rank, world, device, slots=8, nsrc=2, mirror=False):
         import ctypes as C
         from paper_1805_08430_b200 import _lib
         from paper_1805_08430_b200.distributed import exchange_spaces, lookup, publish_addresses
@@ -384,7 +384,7 @@ class PipelinedRing:
         else:
             self.rcv = self.src
             self.slots_reg = self.src.allocate_region(slot_len, register=True)
-            self.credit = self.src.allocate_region(credit_len)
+            self.credit = self.src.allocate_region(credit_len) if mirror else None
             nxt, prv = (rank + 1) % world, (rank - 1) % world
             self.proxies = exchange_spaces(self.src, peers=sorted({nxt, prv}))
             pub = publish_addresses([AddrExchangeMsg(rank, self.slots_reg.base_addr,
@@ -393,7 +393,11 @@ class PipelinedRing:
             msg = lookup(pub, nxt, nxt, Mechanism.STATIC)
             dst_space, dst_addr, dst_tok = self.proxies[nxt], msg.base_addr, msg.token
             # the previous rank's credit words sit at the same offset of its pool
-            self.credit_for_consumer = (self.proxies[prv], self.credit.base_addr)
+            # (off by default: with both link directions busy, the sender's
+            # remote read of the flag measured faster than the mirrored
+            # credit, profiles/r2_edge_probe_nvl2.jsonl)
+            self.credit_for_consumer = ((self.proxies[prv], self.credit.base_addr) if mirror
+                                        else None)
         for i in range(slots):
             self.rcv.write_raw(self.slots_reg.base_addr + i * self.slot_stride + S, b"\x00")
         if self.credit is not None:
@@ -410,10 +414,29 @@ class PipelinedRing:
         self.consumed = 0
         self.info = self.edge.info()
 
+    #: under a profiler that serialises kernels (ncu) the consumer cannot run
+    #: beside the sender: send at most `slots` rounds per launch (no credit
+    #: waits) and consume them afterwards in stream order
+    SERIAL = bool(os.environ.get("CUDA_INJECTION64_PATH") or os.environ.get("SRFLOW_SERIAL_EDGE"))
+
     def launch(self, rounds, ev_before=None, ev_after=None):
         """Consumer first (it must be resident beside the sender grid), then
         one sender launch of `rounds` rounds; events bracket the sender."""
         from paper_1805_08430_b200.runtime.protocol import PipelinedStaticEdge
+        if self.SERIAL and self.world == 1:
+            while rounds > 0:
+                k = min(rounds, self.slots)
+                if ev_before is not None:
+                    self.lib.call("srf_event_record_on", ev_before, self.st_send)
+                self.edge.send(k, self.st_send)
+                if ev_after is not None:
+                    self.lib.call("srf_event_record_on", ev_after, self.st_send)
+                PipelinedStaticEdge.consume(self.rcv, self.slots_reg.base_addr, self.slots,
+                                            self.slot_stride, self.S, self.consumed, k,
+                                            stream=self.st_send)
+                self.consumed += k
+                rounds -= k
+            return
         PipelinedStaticEdge.consume(self.rcv, self.slots_reg.base_addr, self.slots,
                                     self.slot_stride, self.S, self.consumed, rounds,
                                     credit=self.credit_for_consumer, stream=self.st_recv)
@@ -919,6 +942,7 @@ def sweep_nvlink(max_bytes, rank, world, device):
     out = []
     size = 1024
     while size <= max_bytes:
+        log(f"[rank {rank}] sweep_nvlink {size}")
         row = {"bytes": size}
         rounds = 100 if size <= 4 * MIB else 10
         ring = SendRecvRing(size, rank, world, device)
@@ -1567,6 +1591,11 @@ def main() -> int:
     ap.add_argument("--ps-op", choices=("sgd", "xor"), default="sgd")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if os.environ.get("SRFLOW_BENCH_WATCHDOG_S"):
+        # debugging aid: dump every thread's stack periodically to stderr
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["SRFLOW_BENCH_WATCHDOG_S"]),
+                                          repeat=True, file=sys.stderr)
 
     # stdout carries the one JSON line only: everything else written to fd 1
     # (the NCCL version banner, library prints) goes to stderr
@@ -1590,10 +1619,13 @@ def main() -> int:
     init_process_group("nccl")
     S = args.bytes
 
+    log(f"[rank {rank}] headline: pipelined edge, {S} B")
     dev = bench_pipelined(S, args.steps, args.warmup, rank, world, local)
+    log(f"[rank {rank}] single-slot comparator")
     # the reference's one-slot protocol (one K1 + K2 round per transfer) as a
     # comparator line, and the DMA copy engine through the same mapping
     single = bench_sendrecv_device(S, max(3, args.steps // 4), args.warmup, rank, world, local)
+    log(f"[rank {rank}] e2e")
     e2e = bench_sendrecv_e2e(S, max(3, args.steps // 2), args.warmup, rank, world, local)
 
     total_bytes = world * S * dev["n"]
@@ -1655,6 +1687,7 @@ def main() -> int:
         """Secondary results never cost the headline line: a failing section
         is recorded as an error string (every rank runs the same sections, so
         a symmetric failure keeps the collectives in step)."""
+        log(f"[rank {rank}] section {key}")
         try:
             line[key] = fn()
         except Exception as exc:  # pragma: no cover - box dependent

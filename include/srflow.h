@@ -132,6 +132,7 @@ int srf_event_record(srf_space_t space, srf_stream_t stream, srf_event_t *out);
 /* SRF_OK when complete, SRF_PENDING otherwise (Channel.take_completion poll) */
 int srf_event_query(srf_event_t ev);
 int srf_event_wait(srf_event_t ev);
+int srf_event_wait_free(srf_event_t ev);  /* take_completion: wait, then release */
 int srf_event_free(srf_event_t ev);
 
 /* CUDA-graph capture of a stream's launches (many-small-transfer steps are

@@ -83,6 +83,7 @@ SIGNATURES = {
     "srf_event_query": (C.c_int, [vp]),
     "srf_event_wait": (C.c_int, [vp]),
     "srf_event_free": (C.c_int, [vp]),
+    "srf_event_wait_free": (C.c_int, [vp]),
     "srf_graph_begin": (C.c_int, [vp]),
     "srf_graph_end": (C.c_int, [vp, P(vp)]),
     "srf_graph_launch": (C.c_int, [vp, vp]),
@@ -272,6 +273,12 @@ class Event:
         if self._h is not None:
             load().srf_event_free(self._h)
             self._h = None
+
+    def wait_free(self) -> None:
+        """wait() then free() in one call (the event returns to the pool)."""
+        if self._h is not None:
+            h, self._h = self._h, None
+            check(load().srf_event_wait_free(h))
 
     def __del__(self):  # pragma: no cover - interpreter teardown order
         try:

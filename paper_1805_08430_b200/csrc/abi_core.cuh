@@ -690,6 +690,15 @@ int srf_event_wait(srf_event_t ev) {
   return SRF_OK;
 }
 
+int srf_event_wait_free(srf_event_t ev) {
+  DeviceGuard device_guard;
+  if (!ev) return SRF_OK;
+  cudaError_t e = cudaEventSynchronize(ev->e);
+  release_event(ev);
+  if (e != cudaSuccess) return fail(SRF_E_DEVICE, "event wait: %s", cudaGetErrorString(e));
+  return SRF_OK;
+}
+
 int srf_event_free(srf_event_t ev) {
   DeviceGuard device_guard;
   if (!ev) return SRF_OK;

@@ -156,10 +156,42 @@ int srf_edge_consume(srf_space_t rcv, uint64_t slots_addr, uint32_t slots, uint6
   if (rounds == 0) return SRF_OK;
   srf_stream *s = stream_or_default(rcv, st);
   CUDA_TRY(cudaSetDevice(s->device));
+  // a pinned, mapped word per device: the consumer stamps it when it runs
+  static std::mutex mu;
+  static uint32_t *started_host[64] = {nullptr}, *started_dev[64] = {nullptr};
+  static uint32_t tickets[64] = {0};
+  uint32_t *sh = nullptr, *sd = nullptr, ticket = 0;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    const int dev = s->device;
+    if (dev >= 0 && dev < 64) {
+      if (!started_host[dev]) {
+        CUDA_TRY(cudaHostAlloc((void **)&started_host[dev], 64,
+                               cudaHostAllocMapped | cudaHostAllocPortable));
+        CUDA_TRY(cudaHostGetDevicePointer((void **)&started_dev[dev], started_host[dev], 0));
+        *(volatile uint32_t *)started_host[dev] = 0;
+      }
+      sh = started_host[dev];
+      sd = started_dev[dev];
+      ticket = ++tickets[dev];
+      if (ticket == 0) ticket = ++tickets[dev];
+    }
+  }
   k_consume_stream<<<1, mode == 1 ? 1024 : g_consume_threads, 0, s->s>>>(
       rcv->base + slots_addr, slot_stride, slots, nbytes, first_round, rounds, mode,
-      (unsigned long long *)(rcv->base + sums_addr), mirror, g_put_timeout_ns, rcv->err);
-  return launch_check("k_consume_stream");
+      (unsigned long long *)(rcv->base + sums_addr), mirror, sd, ticket, g_put_timeout_ns,
+      rcv->err);
+  rc = launch_check("k_consume_stream");
+  if (rc || !sh) return rc;
+  // wait until the consumer CTA is resident (work queued before it on the
+  // stream delays it; the wait is bounded by the put timeout)
+  const auto t0 = std::chrono::steady_clock::now();
+  while (*(volatile uint32_t *)sh != ticket) {
+    if (cudaStreamQuery(s->s) == cudaSuccess) break;  // already finished
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::nanoseconds(g_put_timeout_ns))
+      return fail(SRF_E_TIMEOUT, "edge consumer did not start");
+  }
+  return SRF_OK;
 }
 
 int srf_edge_destroy(srf_edge_t e) {

@@ -79,8 +79,10 @@ __global__ void __launch_bounds__(512) k_put_stream(const __grid_constant__ Stre
     const uint32_t slot = (uint32_t)(j % a.slots);
     const uint32_t m = (uint32_t)(j / a.slots);  // use index of the slot
     uint8_t *d = a.dst + (uint64_t)slot * a.slot_stride;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && *(volatile int *)a.err == 0) {
       // (a) the slot's previous use is fully released (its tail published)
+      // (after any timeout the remaining items skip their waits: the launch
+      // drains in microseconds and the host raises the error)
       wait_count(a.released + slot, m, a.timeout_ns, a.err);
       // (b) ... and consumed: the receiver cleared its flag (the reference's
       // credit, protocol.py:102-111); cached once seen
@@ -130,9 +132,16 @@ __global__ void __launch_bounds__(1024) k_consume_stream(uint8_t *slots_base, ui
                                                           uint64_t first_round, uint32_t rounds,
                                                           int mode, unsigned long long *sums,
                                                           unsigned int *credit_mirror,
+                                                          uint32_t *started, uint32_t ticket,
                                                           uint64_t timeout_ns, int *err) {
   __shared__ unsigned long long acc;
   __shared__ int ok;
+  // residency handshake: the host launches the sender only after this CTA is
+  // running, so a full-GPU sender grid can never keep it from being scheduled
+  if (threadIdx.x == 0 && started) {
+    *(volatile uint32_t *)started = ticket;
+    __threadfence_system();
+  }
   for (uint32_t r = 0; r < rounds; ++r) {
     const uint64_t j = first_round + r;
     uint8_t *d = slots_base + (j % slots) * slot_stride;

@@ -1447,14 +1447,21 @@ def bench_c1(rank, world, device, cpu=True):
     """configs[0] / SURVEY 8(d) C1: one 1 MiB fp32 tensor, static placement,
     1 sender -> 1 receiver (N=1: one GPU; N>1: the NVLink ring).  Device time
     of the reference's one-slot protocol (K1 put + K2 consume per transfer,
-    graph-replayed), the pipelined edge, e2e through the public endpoints
+    200 rounds replayed as one CUDA graph), the pipelined edge, e2e through the public endpoints
     (pinned H2D of the payload, StaticSender.send -> StaticReceiver.poll ->
     ReduceMax, 4-B result read back) and the reference CPU arm."""
     S = 1 << 20
-    single = bench_sendrecv_device(S, 10, 3, rank, world, device)
+    ring = SendRecvRing(S, rank, world, device)
+    for _ in range(8):
+        ring.put()
+        ring.consume()
+    ring.sync()
+    barrier_sync()
+    us = dist_max(_ring_graph_us(ring.stream, lambda: (ring.put(), ring.consume()), 200,
+                                 ring.src))
+    single = {"verified": dist_sum(0.0 if ring.verify() else 1.0) == 0.0}
     pipe = bench_pipelined(S, 5, 3, rank, world, device, slots=8)
     e2e = bench_sendrecv_e2e(S, 200, 5, rank, world, device)
-    us = single["total_ms"] * 1e3 / single["n"]
     us_pipe = pipe["total_ms"] * 1e3 / pipe["n"]
     per_dir = S / (us * 1e-6) / 1e9
     if world == 1:
@@ -1649,7 +1656,7 @@ def main() -> int:
                           "copy engine)", "bytes_per_launch": alg,
                 "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction "
                                "(nominal 900)"}
-    roof["traffic"] = traffic_from_profiles(world)
+    roof["traffic"] = traffic_from_profiles(world, R)
     single_gbps = world * S * single["n"] / (single["total_ms"] / 1e3) / 1e9
 
     line = {
@@ -1760,12 +1767,14 @@ def main() -> int:
     return 0
 
 
-def traffic_from_profiles(world):
-    """dram bytes per K1 launch from the committed ncu --set full capture."""
-    path = os.path.join(ROOT, "profiles", "k1_traffic.json")
+def traffic_from_profiles(world, rounds=1):
+    """DRAM bytes per k_put_stream launch from the committed ncu --set full
+    capture (bytes per round x rounds per launch); None when not captured."""
+    path = os.path.join(ROOT, "profiles", "k_put_stream_traffic.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(str(world))
+            per = json.load(fh)["bytes_per_round"].get(str(world))
+        return None if per is None else int(per) * int(rounds)
     except Exception:
         return None
 

@@ -438,6 +438,29 @@ int srf_edge_consume(srf_space_t receiver, uint64_t slots_addr, uint32_t slots,
                      uint64_t credit_addr, srf_stream_t stream);
 int srf_edge_destroy(srf_edge_t edge);
 
+/* ---- Session iteration recording and replay (runtime/session.py:606-629) --
+ * srf_record_begin / srf_record_end capture every device launch the library
+ * makes in between (puts, pulls, inline metadata puts, GenGrad, updates,
+ * ReduceMax, MatMul, receivers' flag clears) with their exact arguments;
+ * *replayable is 0 when something outside that set happened (a host write into
+ * device memory, a copy-engine body, another kernel, a second GPU).
+ * srf_oplist_same: 1 when b repeats a with every GenGrad iteration advanced by
+ * gen_delta.  srf_oplist_replay: `count` more iterations of the recording as
+ * one CUDA graph each on `stream` (a stream of the recording's GPU), GenGrad
+ * iterations advanced by first_offset, first_offset + 1, ...; the stream
+ * serialises what the host path serialised with its completion waits. */
+typedef struct srf_oplist *srf_oplist_t;
+int srf_record_begin(void);
+int srf_record_end(srf_oplist_t *out, int *replayable);
+int srf_oplist_info(srf_oplist_t list, uint32_t *nops, int *cuda_device, char *why,
+                    uint32_t why_len);
+int srf_oplist_same(srf_oplist_t a, srf_oplist_t b, int64_t gen_delta);
+/* diagnostics: where b stops repeating a, as text */
+int srf_oplist_diff(srf_oplist_t a, srf_oplist_t b, int64_t gen_delta, char *out, uint32_t len);
+int srf_oplist_replay(srf_oplist_t list, uint64_t first_offset, uint32_t count,
+                      srf_stream_t stream);
+int srf_oplist_destroy(srf_oplist_t list);
+
 #ifdef __cplusplus
 }
 #endif

@@ -439,6 +439,7 @@ int srf_read(srf_space_t sp, uint64_t addr, uint64_t length, void *host_dst) {
 
 int srf_write(srf_space_t sp, uint64_t addr, uint64_t length,
               const void *host_src) {
+  if (recording()) rec_dirty("host write into device memory");
   DeviceGuard device_guard;
   int rc = check_raw(sp, addr, length, "write");
   if (rc) return rc;
@@ -452,6 +453,7 @@ int srf_write(srf_space_t sp, uint64_t addr, uint64_t length,
 
 int srf_write_async(srf_space_t sp, uint64_t addr, uint64_t length,
                     const void *host_src, srf_stream_t st) {
+  if (recording()) rec_dirty("host write into device memory");
   DeviceGuard device_guard;
   int rc = check_raw(sp, addr, length, "write");
   if (rc) return rc;
@@ -852,6 +854,7 @@ int srf_put_inline(srf_space_t src_space, uint64_t stage_addr, uint64_t stage_to
   }
   CUDA_TRY(cudaSetDevice(s->device));
   k_put_inline<<<1, 256, 0, s->s>>>(a);
+  if (recording()) rec_inline(a, s->device);
   int rc = launch_check("k_put_inline");
   if (rc) return rc;
   return record_event(s->device, s->s, ev_out);
@@ -1020,6 +1023,7 @@ int srf_apply(srf_space_t var_space, uint64_t var_addr, uint64_t nbytes,
     k_apply_xor<<<grid, block, 0, s->s>>>(a);
   else
     k_apply_sgd<<<grid, block, 0, s->s>>>(a);
+  if (recording()) rec_apply(s->device, grid, block, a, op == SRF_APPLY_SGD);
   rc = launch_check("k_apply");
   if (rc) return rc;
   return record_event(s->device, s->s, ev_out);
@@ -1039,7 +1043,10 @@ int srf_gen_reference(srf_space_t sp, uint64_t addr, uint64_t nelems, uint64_t e
     const uint64_t cap = (uint64_t)sm_count_of(s->device) * 4;
     const int grid = (int)std::max<uint64_t>(1, std::min(want, cap));
     k_gen_reference<<<grid, 512, 0, s->s>>>((float *)(sp->base + addr), nelems, elem_offset,
-                                            seed, node, iteration);
+                                            seed, node, iteration, nullptr);
+    if (recording())
+      rec_gen(s->device, grid, (float *)(sp->base + addr), nelems, elem_offset, seed, node,
+              iteration);
     rc = launch_check("k_gen_reference");
     if (rc) return rc;
   }
@@ -1060,6 +1067,9 @@ int srf_reduce_max_f32(srf_space_t sp, uint64_t in_addr, uint64_t n,
   k_reduce_max<<<grid, 256, 0, s->s>>>((const float *)(sp->base + in_addr), n,
                                        (float *)(sp->base + out_addr),
                                        s->scratch, s->counter + 1);
+  if (recording())
+    rec_reduce(s->device, grid, (const float *)(sp->base + in_addr), n,
+               (float *)(sp->base + out_addr), s->scratch, s->counter + 1);
   return launch_check("k_reduce_max");
 }
 

@@ -86,6 +86,8 @@ int srf_flag_clear(srf_space_t sp, uint64_t tail_addr) {
       CUDA_TRY(cudaMemsetAsync(sp->base + tail_addr, 0, 1, sp->stream->s));
       CUDA_TRY(cudaEventRecord(d.clear_ev, sp->stream->s));
       d.clear_pending = true;
+      if (recording())  // the doorbell byte through its device mapping
+        rec_clear(sp->device, sp->base + tail_addr, sp->db_dev + d.host_off + d.shadow_len - 1);
       return SRF_OK;
     }
   }
@@ -211,6 +213,11 @@ int srf_matmul(int elem, uint64_t a_ptr, uint64_t b_ptr, uint64_t c_ptr, uint64_
     case 4: k_matmul<uint8_t><<<grid, 256, 0, s>>>((const uint8_t *)a_ptr, (const uint8_t *)b_ptr,
                                                      (uint8_t *)c_ptr, m, k, n); break;
     default: return fail(SRF_E_INVALID_CONFIG, "unknown element type %d", elem);
+  }
+  if (recording()) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    rec_matmul(dev, elem, a_ptr, b_ptr, c_ptr, m, k, n);
   }
   return launch_check("k_matmul");
 }

@@ -205,3 +205,113 @@ int srf_edge_destroy(srf_edge_t e) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Session iteration recording and replay (host_record.cuh)
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int srf_record_begin(void) {
+  std::lock_guard<std::mutex> g(g_rec_mu);
+  if (g_rec) return fail(SRF_E_INVALID_CONFIG, "a recording is already active");
+  g_rec = new srf_oplist();
+  g_rec_expected = false;
+  return SRF_OK;
+}
+
+int srf_record_end(srf_oplist_t *out, int *replayable) {
+  std::lock_guard<std::mutex> g(g_rec_mu);
+  if (!g_rec) return fail(SRF_E_INVALID_CONFIG, "no active recording");
+  srf_oplist *l = g_rec;
+  g_rec = nullptr;
+  g_rec_expected = false;
+  if (replayable) *replayable = (!l->dirty && !l->ops.empty() && l->device >= 0) ? 1 : 0;
+  *out = l;
+  return SRF_OK;
+}
+
+int srf_oplist_info(srf_oplist_t l, uint32_t *nops, int *device, char *why, uint32_t why_len) {
+  if (nops) *nops = (uint32_t)l->ops.size();
+  if (device) *device = l->device;
+  if (why && why_len) {
+    snprintf(why, why_len, "%s", l->dirty ? l->why.c_str() : "");
+  }
+  return SRF_OK;
+}
+
+int srf_oplist_same(srf_oplist_t a, srf_oplist_t b, int64_t gen_delta) {
+  if (a->dirty || b->dirty || a->ops.size() != b->ops.size() || a->device != b->device) return 0;
+  for (size_t i = 0; i < a->ops.size(); ++i)
+    if (!rec_same(a->ops[i], b->ops[i], gen_delta)) return 0;
+  return 1;
+}
+
+// diagnostics: where b stops repeating a (first differing op, kinds, counts)
+int srf_oplist_diff(srf_oplist_t a, srf_oplist_t b, int64_t gen_delta, char *out, uint32_t len) {
+  if (a->ops.size() != b->ops.size()) {
+    snprintf(out, len, "op count %zu vs %zu", a->ops.size(), b->ops.size());
+    return SRF_OK;
+  }
+  for (size_t i = 0; i < a->ops.size(); ++i) {
+    if (!rec_same(a->ops[i], b->ops[i], gen_delta)) {
+      const RecOp &x = a->ops[i], &y = b->ops[i];
+      char extra[256] = "";
+      if (x.kind == REC_PUT && y.kind == REC_PUT)
+        snprintf(extra, sizeof extra, " put dst %p/%p seg0 %p/%p len %llu/%llu",
+                 (void *)x.put.dst, (void *)y.put.dst, (const void *)x.put.seg[0].src,
+                 (const void *)y.put.seg[0].src, (unsigned long long)x.put.total,
+                 (unsigned long long)y.put.total);
+      else if (x.kind == REC_APPLY && y.kind == REC_APPLY)
+        snprintf(extra, sizeof extra, " apply var %p/%p g0 %p/%p", (void *)x.apply.var,
+                 (void *)y.apply.var, (const void *)x.apply.g[0], (const void *)y.apply.g[0]);
+      else if (x.kind == REC_GEN && y.kind == REC_GEN)
+        snprintf(extra, sizeof extra, " gen dst %p/%p it %llu/%llu", (void *)x.gen.dst,
+                 (void *)y.gen.dst, (unsigned long long)x.gen.iteration,
+                 (unsigned long long)y.gen.iteration);
+      snprintf(out, len, "op %zu kind %d/%d%s", i, x.kind, y.kind, extra);
+      return SRF_OK;
+    }
+  }
+  snprintf(out, len, "same");
+  return SRF_OK;
+}
+
+int srf_oplist_replay(srf_oplist_t l, uint64_t first_offset, uint32_t count, srf_stream_t st) {
+  DeviceGuard device_guard;
+  if (l->dirty || l->ops.empty()) return fail(SRF_E_INVALID_CONFIG, "recording not replayable");
+  if (st->device != l->device) return fail(SRF_E_INVALID_CONFIG, "stream on another GPU");
+  if (count == 0) return SRF_OK;
+  CUDA_TRY(cudaSetDevice(l->device));
+  if (!l->exec) {
+    // one CUDA graph of the recorded iteration; GenGrad reads its iteration
+    // offset from a device word set before each launch
+    CUDA_TRY(cudaMalloc(&l->iter_add, sizeof(uint64_t)));
+    cudaGraph_t graph;
+    CUDA_TRY(cudaStreamBeginCapture(st->s, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = rec_issue(l, st->s, l->iter_add);
+    cudaError_t e2 = cudaStreamEndCapture(st->s, &graph);
+    if (e != cudaSuccess || e2 != cudaSuccess)
+      return fail(SRF_E_DEVICE, "replay capture: %s",
+                  cudaGetErrorString(e != cudaSuccess ? e : e2));
+    e = cudaGraphInstantiate(&l->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(SRF_E_DEVICE, "replay instantiate: %s", cudaGetErrorString(e));
+  }
+  for (uint32_t i = 0; i < count; ++i) {
+    k_set_u64<<<1, 1, 0, st->s>>>(l->iter_add, first_offset + i);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaGraphLaunch(l->exec, st->s));
+  }
+  g_launches.fetch_add((uint64_t)count * (l->ops.size() + 1), std::memory_order_relaxed);
+  return SRF_OK;
+}
+
+int srf_oplist_destroy(srf_oplist_t l) {
+  DeviceGuard device_guard;
+  if (!l) return SRF_OK;
+  if (l->device >= 0) cudaSetDevice(l->device);
+  delete l;
+  return SRF_OK;
+}
+
+}  // extern "C"

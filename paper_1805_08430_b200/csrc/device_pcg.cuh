@@ -311,9 +311,13 @@ __device__ void pcg_fill_f32_cta(float *dst, uint64_t nf, uint64_t e0, uint64_t 
 
 // Standalone GenGrad / Input on the device: synthesize_values(dims, F32,
 // node_rng(seed, node, iteration)) elements [e0, e0 + nf) into dst.
+// iter_add (nullptr: none): a device counter added to `iteration` - a
+// replayed Session iteration (host_record.cuh) advances it per replay.
 __global__ void __launch_bounds__(512) k_gen_reference(float *dst, uint64_t nf, uint64_t e0,
                                                        uint64_t seed, uint64_t node,
-                                                       uint64_t iteration) {
+                                                       uint64_t iteration,
+                                                       const uint64_t *iter_add) {
+  if (iter_add) iteration += *(const volatile uint64_t *)iter_add;
   pcg_fill_f32_cta(dst, nf, e0, seed, node, iteration, blockIdx.x, gridDim.x);
 }
 #endif

@@ -65,6 +65,7 @@ static int launch_check(const char *what) {
   if (e != cudaSuccess)
     return fail(SRF_E_DEVICE, "%s launch: %s", what, cudaGetErrorString(e));
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  rec_check_launch(what);
   return SRF_OK;
 }
 
@@ -100,6 +101,7 @@ static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
     uint64_t cap = (uint64_t)sm_count_of(s->device) * 2;
     int grid = (int)std::max<uint64_t>(1, std::min(chunks, cap));
     k_put_bulk<<<grid, 256, kBulkSmem, s->s>>>(a);
+    if (recording()) rec_put(a, s, grid, 256, 4);
   } else {
     int grid, block;
     copy_geometry(s->device, a.total, &grid, &block);
@@ -121,6 +123,8 @@ static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
       else
         k_put<4, false><<<grid, block, 0, s->s>>>(a);
     }
+    if (recording())
+      rec_put(a, s, grid, block, (g_unroll == 8 ? 0 : 2) + (sectors ? 1 : 0));
   }
   return launch_check(what);
 }
@@ -132,6 +136,7 @@ static int launch_copy(const PutArgs &a, srf_stream *s, const char *what) {
 // without a credit wait: a DMA copy cannot be skipped when a credit times
 // out, so credit-gated puts stay on the kernel (put_impl).
 static int put_via_copy_engine(const PutArgs &a, srf_stream *s) {
+  if (recording()) rec_dirty("copy-engine body");
   const uint64_t body = a.total - 1;
   for (int i = 0; i < a.nseg; ++i) {
     const Seg &sg = a.seg[i];

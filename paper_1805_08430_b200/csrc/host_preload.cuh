@@ -28,7 +28,8 @@ static int preload_kernels(int device) {
       (const void *)k_matmul<float>, (const void *)k_matmul<double>,
       (const void *)k_matmul<int32_t>, (const void *)k_matmul<int64_t>,
       (const void *)k_matmul<uint8_t>, (const void *)k_put_stream,
-      (const void *)k_consume_stream, (const void *)k_put_inline};
+      (const void *)k_consume_stream, (const void *)k_put_inline, (const void *)k_clear_flag,
+      (const void *)k_set_u64};
   for (const void *k : kernels) {
     cudaFuncAttributes attr;
     cudaError_t e = cudaFuncGetAttributes(&attr, k);

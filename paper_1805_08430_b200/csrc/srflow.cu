@@ -40,6 +40,7 @@ namespace cg = cooperative_groups;
 #include "device_ps.cuh"
 #include "device_stream.cuh"
 #include "device_rpc.cuh"
+#include "host_record.cuh"
 #include "host_launch.cuh"
 #include "host_preload.cuh"
 #include "abi_core.cuh"

@@ -1,0 +1,96 @@
+"""Steady-state replay of Session iterations (host_record.cuh): once two
+consecutive iterations issue identical device work and identical report
+rows, the remaining iterations replay the recording as one CUDA graph each.
+The result must be indistinguishable from the host path: every RunReport row
+(all counters, the cost-model time), the final counters and every variable's
+bytes equal a run with replay=False (whose rows the golden session tests pin
+to the reference's own runs), and the replayed PS variables equal the oracle."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle import port
+from paper_1805_08430_b200.graph import NodeKind
+from paper_1805_08430_b200.runtime.session import Session
+from paper_1805_08430_b200.workloads import (build_layered_forward, build_microbench,
+                                             build_ps_workload, mlp_shapes)
+
+pytestmark = pytest.mark.gpu
+
+FIELDS = ("iteration", "bytes_sent", "payload_bytes", "payload_bytes_copied", "copy_events",
+          "serialize_bytes", "arena_peak_bytes", "polls")
+
+CASES = {
+    "mlp_ps": (lambda: build_ps_workload(0, 3, 0.0, 2, shapes=mlp_shapes()), {}),
+    "ps24k_dyn": (lambda: build_ps_workload(24_000, 2, 0.0, 2), {"mechanism_override": "dynamic"}),
+    "ps7w": (lambda: build_ps_workload(7_000, 5, 0.0, 7), {}),
+    "coloc4": (lambda: build_ps_workload(0, 4, 0.0, 4, ps_servers=4, shapes=[(3000,)] * 4,
+                                         colocate=True), {}),
+    "ps_static_grads": (lambda: build_ps_workload(40_000, 3, 0.0, 2),
+                        {"mechanism_override": "static"}),
+    "micro1m": (lambda: build_microbench(1 << 20), {}),
+    "micro4k_cp": (lambda: build_microbench(4096), {"mode": "cp"}),
+    "sgd_ps": (lambda: build_ps_workload(0, 3, 0.0, 2, shapes=mlp_shapes()),
+               {"apply_op": "sgd", "lr": 0.05}),
+}
+
+
+def _run(name, replay, n=16):
+    build, kw = CASES[name]
+    g, p = build()
+    s = Session(g, p, seed=3, replay=replay, devices={v: 0 for v in set(p.values())}, **kw)
+    rep = s.run(4)
+    rep = s.run(n - 4)          # numbering continues; replay spans the second call
+    vars_ = {nid: s.variable_bytes(nid) for nid, node in g.nodes.items()
+             if node.kind is NodeKind.VARIABLE}
+    print(name, replay, s.replay_status)
+    out = (rep, vars_, s.replayed_iterations, dict(rep.per_server_final),
+           (s.fabric.verbs_posted, s.fabric.wire_bytes, s.fabric.clock.now()))
+    s.close()
+    return out
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_replay_equals_host_path(name):
+    rep_r, vars_r, replayed, final_r, fab_r = _run(name, True)
+    rep_h, vars_h, replayed_h, final_h, fab_h = _run(name, False)
+    assert replayed_h == 0
+    assert replayed >= 4, f"{name}: steady state not detected"  # see the printed status
+    assert len(rep_r.rows) == len(rep_h.rows) == 16
+    for a, b in zip(rep_r.rows, rep_h.rows):
+        for f in FIELDS:
+            assert getattr(a, f) == getattr(b, f), (name, a.iteration, f)
+        assert a.sim_time_us == pytest.approx(b.sim_time_us, rel=1e-9)
+    assert final_r == final_h
+    assert fab_r[:2] == fab_h[:2] and fab_r[2] == pytest.approx(fab_h[2], rel=1e-9)
+    assert vars_r.keys() == vars_h.keys()
+    for nid in vars_r:
+        assert vars_r[nid] == vars_h[nid], (name, nid)
+
+
+def test_replayed_ps_variables_equal_the_oracle():
+    """XOR PS after 14 iterations, the later ones replayed: the golden-pinned
+    recipe on the reference's gradient stream."""
+    shapes = mlp_shapes()
+    g, p = build_ps_workload(0, 3, 0.0, 2, shapes=shapes)
+    s = Session(g, p, seed=3, devices={v: 0 for v in set(p.values())})
+    s.run(14)
+    assert s.replayed_iterations >= 5
+    want = port.ps_expected(shapes, 2, 3, 14, op="xor")
+    var_nodes = sorted(nid for nid, node in g.nodes.items() if node.kind is NodeKind.VARIABLE)
+    for v, nid in enumerate(var_nodes):
+        got = np.frombuffer(s.variable_bytes(nid), np.float32).reshape(shapes[v])
+        assert got.tobytes() == want[v].tobytes()
+    s.close()
+
+
+def test_host_compute_kinds_are_not_replayed():
+    """Compute kinds that run as torch ops (Add, Sigmoid) launch kernels the
+    recorder does not see, so such sessions keep the host path."""
+    g, _, _ = build_layered_forward(4)
+    p = {nid: 0 for nid in g.nodes}
+    s = Session(g, p, seed=1, devices={0: 0})
+    s.run(6)
+    assert s.replayed_iterations == 0
+    s.close()

@@ -1530,7 +1530,12 @@ def bench_ps_session(rank, world, device, steps, warmup, op, cpu):
                        devices={s: device for s in set(placement.values())},
                        apply_op=op, lr=0.01)
         sess.run(1)                       # iteration 1: tracing warm-up
-        sess.run(max(3, warmup - 1))      # iterations 2, 3 recorded -> steady state
+        sess.run(max(1, warmup - 1))
+        # from iteration 2 the device work is recorded; dynamic edges cycle
+        # through a few arena addresses, so steady state (period p) needs 2p
+        # recorded iterations
+        while sess.replay_steady is None and sess._next_iteration <= 24:
+            sess.run(1)
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
         sess.run(3)
@@ -1577,6 +1582,7 @@ def bench_ps_session(rank, world, device, steps, warmup, op, cpu):
                             "are the reference's synthetic GenGrad, generated in place"},
             "verified": ok, "iterations": it,
             "replayed_iterations": sess.replayed_iterations,
+            "replay": sess.replay_status,
             "path": ("steady-state replay: iterations 2-3 through the host executor "
                      "(recorded), later ones as one CUDA graph of the recorded verbs each"
                      if sess.replayed_iterations else "host executor, one verb at a time"),

@@ -36,7 +36,7 @@ CASES = {
 }
 
 
-def _run(name, replay, n=16):
+def _run(name, replay, n=24):
     build, kw = CASES[name]
     g, p = build()
     s = Session(g, p, seed=3, replay=replay, devices={v: 0 for v in set(p.values())}, **kw)
@@ -57,7 +57,7 @@ def test_replay_equals_host_path(name):
     rep_h, vars_h, replayed_h, final_h, fab_h = _run(name, False)
     assert replayed_h == 0
     assert replayed >= 4, f"{name}: steady state not detected"  # see the printed status
-    assert len(rep_r.rows) == len(rep_h.rows) == 16
+    assert len(rep_r.rows) == len(rep_h.rows) == 24
     for a, b in zip(rep_r.rows, rep_h.rows):
         for f in FIELDS:
             assert getattr(a, f) == getattr(b, f), (name, a.iteration, f)

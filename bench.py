@@ -1534,7 +1534,7 @@ def bench_ps_session(rank, world, device, steps, warmup, op, cpu):
         # from iteration 2 the device work is recorded; dynamic edges cycle
         # through a few arena addresses, so steady state (period p) needs 2p
         # recorded iterations
-        while sess.replay_steady is None and sess._next_iteration <= 24:
+        while sess.replay_steady is None and sess._next_iteration <= 40:
             sess.run(1)
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()

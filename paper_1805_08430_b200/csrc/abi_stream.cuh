@@ -232,6 +232,11 @@ int srf_record_end(srf_oplist_t *out, int *replayable) {
 
 int srf_oplist_info(srf_oplist_t l, uint32_t *nops, int *device, char *why, uint32_t why_len) {
   if (nops) *nops = (uint32_t)l->ops.size();
+  if (why && why_len && l->exec) {
+    snprintf(why, why_len, "graph: %u nodes, %u dependency edges", l->nodes, l->edges);
+    if (device) *device = l->device;
+    return SRF_OK;
+  }
   if (device) *device = l->device;
   if (why && why_len) {
     snprintf(why, why_len, "%s", l->dirty ? l->why.c_str() : "");
@@ -283,19 +288,11 @@ int srf_oplist_replay(srf_oplist_t l, uint64_t first_offset, uint32_t count, srf
   if (count == 0) return SRF_OK;
   CUDA_TRY(cudaSetDevice(l->device));
   if (!l->exec) {
-    // one CUDA graph of the recorded iteration; GenGrad reads its iteration
-    // offset from a device word set before each launch
-    CUDA_TRY(cudaMalloc(&l->iter_add, sizeof(uint64_t)));
-    cudaGraph_t graph;
-    CUDA_TRY(cudaStreamBeginCapture(st->s, cudaStreamCaptureModeThreadLocal));
-    cudaError_t e = rec_issue(l, st->s, l->iter_add);
-    cudaError_t e2 = cudaStreamEndCapture(st->s, &graph);
-    if (e != cudaSuccess || e2 != cudaSuccess)
-      return fail(SRF_E_DEVICE, "replay capture: %s",
-                  cudaGetErrorString(e != cudaSuccess ? e : e2));
-    e = cudaGraphInstantiate(&l->exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (e != cudaSuccess) return fail(SRF_E_DEVICE, "replay instantiate: %s", cudaGetErrorString(e));
+    // one CUDA graph of the recorded iteration with data dependencies
+    // (host_record.cuh); GenGrad reads its iteration offset from a device
+    // word set before each launch
+    int rc = rec_build_graph(l);
+    if (rc) return rc;
   }
   for (uint32_t i = 0; i < count; ++i) {
     k_set_u64<<<1, 1, 0, st->s>>>(l->iter_add, first_offset + i);

@@ -64,11 +64,14 @@ struct srf_oplist {
   // replay state
   cudaGraphExec_t exec = nullptr;
   uint64_t *iter_add = nullptr;  // device counter: GenGrad iteration offset
+  unsigned int *priv = nullptr;  // private arrival counters / reduction scratch
   int graph_device = -1;
+  uint32_t nodes = 0, edges = 0;
   ~srf_oplist() {
     for (RecOp &op : ops) delete op.inl;
     if (exec) cudaGraphExecDestroy(exec);
     if (iter_add) cudaFree(iter_add);
+    if (priv) cudaFree(priv);
   }
 };
 
@@ -263,4 +266,162 @@ static cudaError_t rec_issue(const srf_oplist *l, cudaStream_t s, const uint64_t
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
+// Replay graph with data dependencies instead of one chain: the host path
+// serialised every verb, but only ops whose byte ranges conflict (read after
+// write, write after read or write) need ordering - different variables'
+// pushes, GenGrads, pulls and updates may run side by side, as the device PS
+// engine runs them.  Each op's footprint: the ranges it reads and writes
+// (device pointers and host-mapped doorbell bytes live in one address space);
+// arrival counters and reduction scratch are made private per op.
+// ---------------------------------------------------------------------------
+struct Span {
+  uintptr_t lo, hi;  // [lo, hi)
+  bool write;
+};
+
+static void rec_footprint(const RecOp &op, std::vector<Span> &out) {
+  auto add = [&](const void *p, uint64_t n, bool w) {
+    if (p && n) out.push_back({(uintptr_t)p, (uintptr_t)p + n, w});
+  };
+  switch (op.kind) {
+    case REC_PUT: {
+      const PutArgs &a = op.put;
+      for (int i = 0; i < a.nseg; ++i) add(a.seg[i].src, a.seg[i].len, false);
+      add(a.dst, a.total, true);
+      if (a.db) add(a.db, a.db_len, true);
+      if (a.consume) add(a.consume, 1, true);
+      break;
+    }
+    case REC_INLINE:
+      add(op.inl->stage, op.inl->len, true);
+      add(op.inl->dst, op.inl->len, true);
+      if (op.inl->db) add(op.inl->db, op.inl->db_len, true);
+      break;
+    case REC_GEN: add(op.gen.dst, 4 * op.gen.nf, true); break;
+    case REC_APPLY:
+      for (int w = 0; w < op.apply.nw; ++w) add(op.apply.g[w], op.apply.n, false);
+      add(op.apply.var, op.apply.n, true);
+      break;
+    case REC_REDUCE:
+      add(op.red.in, 4 * op.red.n, false);
+      add(op.red.out, 4, true);
+      break;
+    case REC_CLEAR:
+      add(op.clr.dev, 1, true);
+      if (op.clr.shadow) add(op.clr.shadow, 1, true);
+      break;
+    case REC_MATMUL: {
+      const uint64_t es = op.mm.elem == 0 || op.mm.elem == 2 ? 4 : op.mm.elem == 4 ? 1 : 8;
+      add((const void *)op.mm.a, es * op.mm.m * op.mm.k, false);
+      add((const void *)op.mm.b, es * op.mm.k * op.mm.n, false);
+      add((const void *)op.mm.c, es * op.mm.m * op.mm.n, true);
+      break;
+    }
+  }
+}
+
+static bool rec_conflict(const std::vector<Span> &a, const std::vector<Span> &b) {
+  for (const Span &x : a)
+    for (const Span &y : b)
+      if ((x.write || y.write) && x.lo < y.hi && y.lo < x.hi) return true;
+  return false;
+}
+
+// Build l->exec: one kernel node per op, edges from every earlier op it
+// conflicts with (transitively redundant edges kept; the graph is small).
+static int rec_build_graph(srf_oplist *l) {
+  const size_t n = l->ops.size();
+  // private arrival counters (PutArgs.counter, reduction counter) and scratch
+  const size_t words = 2 * n + (size_t)kScratchBlocks * n;
+  CUDA_TRY(cudaMalloc(&l->iter_add, sizeof(uint64_t)));
+  CUDA_TRY(cudaMemset(l->iter_add, 0, sizeof(uint64_t)));
+  CUDA_TRY(cudaMalloc(&l->priv, sizeof(unsigned int) * words));
+  CUDA_TRY(cudaMemset(l->priv, 0, sizeof(unsigned int) * words));
+  std::vector<RecOp> ops = l->ops;  // patched copies (kernel params are copied at add time)
+  std::vector<std::vector<Span>> fp(n);
+  for (size_t i = 0; i < n; ++i) {
+    if (ops[i].kind == REC_PUT) ops[i].put.counter = l->priv + 2 * i;
+    if (ops[i].kind == REC_REDUCE) {
+      ops[i].red.counter = l->priv + 2 * i + 1;
+      ops[i].red.scratch = (float *)(l->priv + 2 * n + (size_t)kScratchBlocks * i);
+    }
+    rec_footprint(ops[i], fp[i]);
+  }
+  cudaGraph_t graph;
+  CUDA_TRY(cudaGraphCreate(&graph, 0));
+  std::vector<cudaGraphNode_t> node(n);
+  uint32_t edges = 0;
+  for (size_t j = 0; j < n; ++j) {
+    std::vector<cudaGraphNode_t> deps;
+    for (size_t i = 0; i < j; ++i)
+      if (rec_conflict(fp[i], fp[j])) deps.push_back(node[i]);
+    edges += (uint32_t)deps.size();
+    RecOp &op = ops[j];
+    cudaKernelNodeParams kp;
+    memset(&kp, 0, sizeof kp);
+    kp.gridDim = dim3((unsigned)op.grid);
+    kp.blockDim = dim3((unsigned)op.block);
+    void *args[8];
+    const auto &m = op.mm;
+    switch (op.kind) {
+      case REC_PUT:
+        args[0] = &op.put;
+        kp.func = op.variant == 0   ? (void *)k_put<8, false>
+                  : op.variant == 1 ? (void *)k_put<8, true>
+                  : op.variant == 2 ? (void *)k_put<4, false>
+                  : op.variant == 3 ? (void *)k_put<4, true>
+                                    : (void *)k_put_bulk;
+        if (op.variant == 4) kp.sharedMemBytes = kBulkSmem;
+        break;
+      case REC_INLINE:
+        args[0] = op.inl;
+        kp.func = (void *)k_put_inline;
+        break;
+      case REC_GEN:
+        args[0] = &op.gen.dst; args[1] = &op.gen.nf; args[2] = &op.gen.e0;
+        args[3] = &op.gen.seed; args[4] = &op.gen.node; args[5] = &op.gen.iteration;
+        args[6] = &l->iter_add;
+        kp.func = (void *)k_gen_reference;
+        break;
+      case REC_APPLY:
+        args[0] = &op.apply;
+        kp.func = op.apply_sgd ? (void *)k_apply_sgd : (void *)k_apply_xor;
+        break;
+      case REC_REDUCE:
+        args[0] = &op.red.in; args[1] = &op.red.n; args[2] = &op.red.out;
+        args[3] = &op.red.scratch; args[4] = &op.red.counter;
+        kp.func = (void *)k_reduce_max;
+        break;
+      case REC_CLEAR:
+        args[0] = &op.clr.dev; args[1] = &op.clr.shadow;
+        kp.func = (void *)k_clear_flag;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        break;
+      case REC_MATMUL:
+        args[0] = (void *)&m.a; args[1] = (void *)&m.b; args[2] = (void *)&m.c;
+        args[3] = (void *)&m.m; args[4] = (void *)&m.k; args[5] = (void *)&m.n;
+        kp.func = m.elem == 0   ? (void *)k_matmul<float>
+                  : m.elem == 1 ? (void *)k_matmul<double>
+                  : m.elem == 2 ? (void *)k_matmul<int32_t>
+                  : m.elem == 3 ? (void *)k_matmul<int64_t>
+                                : (void *)k_matmul<uint8_t>;
+        break;
+    }
+    kp.kernelParams = args;
+    cudaError_t e = cudaGraphAddKernelNode(&node[j], graph, deps.data(), deps.size(), &kp);
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      return fail(SRF_E_DEVICE, "replay graph node %zu: %s", j, cudaGetErrorString(e));
+    }
+  }
+  cudaError_t e = cudaGraphInstantiate(&l->exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(SRF_E_DEVICE, "replay instantiate: %s", cudaGetErrorString(e));
+  l->nodes = (uint32_t)n;
+  l->edges = edges;
+  return SRF_OK;
 }

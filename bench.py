@@ -1536,11 +1536,12 @@ def bench_ps_session(rank, world, device, steps, warmup, op, cpu):
         # recorded iterations
         while sess.replay_steady is None and sess._next_iteration <= 40:
             sess.run(1)
+        sess.run(3)                       # first replays build the replay graphs
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
         sess.run(3)
         per = (time.perf_counter() - t0) / 3
-        n = int(max(3, min(2000, 0.5 / max(per, 1e-6))))
+        n = int(max(3, min(4000, 1.0 / max(per, 1e-6))))
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
         report = sess.run(n)

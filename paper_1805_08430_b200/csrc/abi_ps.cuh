@@ -137,7 +137,7 @@ int srf_batch_gen_create(int n, srf_space_t const *space, const uint64_t *grad_a
                    ? nullptr : credit_space[i]->base + credit_addr[i];
     d.node = node_id[i];
     d.cta_begin = next;
-    d.cta_count = ctas_for(device, nbytes[i], 128 << 10);
+    d.cta_count = ctas_for(device, nbytes[i], g_gen_unit_bytes);
     next += d.cta_count;
   }
   int rc = finish_batch(1, device, host, space[0]->err, out);

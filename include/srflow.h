@@ -396,6 +396,14 @@ int srf_rpc_transfer(srf_space_t src, uint64_t meta_addr, uint32_t meta_len,
 int srf_matmul(int elem, uint64_t a_ptr, uint64_t b_ptr, uint64_t c_ptr, uint64_t m, uint64_t k,
                uint64_t n, void *cuda_stream);
 
+/* The compute kinds of Session graphs on the device, operands and result in
+ * one space (graph.py:371-377): kind 0 MatMul a[m,k] @ b[k,n] (as srf_matmul),
+ * kind 1 Add a + b over n elements of equal shape (integers wrap), kind 2
+ * Sigmoid (1 / (1 + exp(-x as float64))) rounded to the float type.  The
+ * result is written straight into the output block (no staging). */
+int srf_compute(srf_space_t space, int kind, int elem, uint64_t a_addr, uint64_t b_addr,
+                uint64_t out_addr, uint64_t m, uint64_t k, uint64_t n, srf_stream_t stream);
+
 /* ReduceMax consumer of the microbenchmark (graph.py:378-382) on the
  * receiving GPU: out_addr receives max over n fp32 at in_addr. */
 int srf_reduce_max_f32(srf_space_t space, uint64_t in_addr, uint64_t n,
@@ -452,6 +460,8 @@ int srf_edge_destroy(srf_edge_t edge);
 typedef struct srf_oplist *srf_oplist_t;
 int srf_record_begin(void);
 int srf_record_end(srf_oplist_t *out, int *replayable);
+/* the caller launched device work outside the library during the recording */
+int srf_record_taint(const char *why);
 int srf_oplist_info(srf_oplist_t list, uint32_t *nops, int *cuda_device, char *why,
                     uint32_t why_len);
 int srf_oplist_same(srf_oplist_t a, srf_oplist_t b, int64_t gen_delta);

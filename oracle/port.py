@@ -270,6 +270,32 @@ def apply_sgd(var: np.ndarray, grads: Sequence[np.ndarray], lr: float) -> np.nda
     return var
 
 
+def forward_values(nodes, seed: int, iteration: int) -> dict:
+    """Edge values of one iteration of a static graph of compute kinds
+    (graph.py:363-389 compute_node; Variables keep their iteration-0 value,
+    session.py's Variable handler).  ``nodes``: (node_id, kind, input edges,
+    output edge, dims, elem) in topological order, kind one of "INPUT",
+    "GEN_GRAD", "VARIABLE", "MATMUL", "ADD", "SIGMOID", "REDUCE_MAX"."""
+    vals: dict = {}
+    for nid, kind, ins, out, dims, elem in nodes:
+        x = [vals[e] for e in ins]
+        if kind in ("INPUT", "GEN_GRAD", "VARIABLE"):
+            it = 0 if kind == "VARIABLE" else iteration
+            v = synthesize(math.prod(dims), elem, node_rng(seed, nid, it)).reshape(dims)
+        elif kind == "MATMUL":
+            v = x[0] @ x[1]
+        elif kind == "ADD":
+            v = x[0] + x[1]
+        elif kind == "SIGMOID":
+            v = (1.0 / (1.0 + np.exp(-x[0].astype(np.float64)))).astype(x[0].dtype)
+        elif kind == "REDUCE_MAX":
+            v = np.zeros(1, x[0].dtype) if x[0].size == 0 else np.max(x[0]).reshape(1)
+        else:
+            raise ValueError(kind)
+        vals[out] = v
+    return vals
+
+
 def ps_node_ids(v: int, w: int, workers: int) -> tuple[int, int, int]:
     """workloads.py:81-93 node order: (variable, GenGrad, ApplyGrad)."""
     var = v * (1 + 2 * workers)

@@ -149,7 +149,9 @@ SIGNATURES = {
                                    vp, u64, vp]),
     "srf_edge_destroy": (C.c_int, [vp]),
     "srf_matmul": (C.c_int, [C.c_int, u64, u64, u64, u64, u64, u64, vp]),
+    "srf_compute": (C.c_int, [vp, C.c_int, C.c_int, u64, u64, u64, u64, u64, u64, vp]),
     "srf_record_begin": (C.c_int, []),
+    "srf_record_taint": (C.c_int, [C.c_char_p]),
     "srf_record_end": (C.c_int, [P(vp), P(C.c_int)]),
     "srf_oplist_info": (C.c_int, [vp, P(C.c_uint32), P(C.c_int), C.c_char_p, C.c_uint32]),
     "srf_oplist_same": (C.c_int, [vp, vp, C.c_int64]),

@@ -222,6 +222,50 @@ int srf_matmul(int elem, uint64_t a_ptr, uint64_t b_ptr, uint64_t c_ptr, uint64_
   return launch_check("k_matmul");
 }
 
+int srf_compute(srf_space_t sp, int kind, int elem, uint64_t a_addr, uint64_t b_addr,
+                uint64_t out_addr, uint64_t m, uint64_t k, uint64_t n, srf_stream_t st) {
+  DeviceGuard device_guard;
+  if (elem < 0 || elem > 4) return fail(SRF_E_INVALID_CONFIG, "unknown element type %d", elem);
+  const uint64_t es = elem == 0 || elem == 2 ? 4 : elem == 4 ? 1 : 8;
+  srf_stream *s = stream_or_default(sp, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  uint8_t *base = sp->base;
+  if (kind == 0) {  // MatMul: a[m,k] @ b[k,n] -> out[m,n]
+    int rc = check_raw(sp, a_addr, es * m * k, "matmul a");
+    if (!rc) rc = check_raw(sp, b_addr, es * k * n, "matmul b");
+    if (!rc) rc = check_raw(sp, out_addr, es * m * n, "matmul out");
+    if (rc) return rc;
+    return srf_matmul(elem, (uint64_t)(base + a_addr), (uint64_t)(base + b_addr),
+                      (uint64_t)(base + out_addr), m, k, n, (void *)s->s);
+  }
+  if (kind != 1 && kind != 2) return fail(SRF_E_INVALID_CONFIG, "unknown compute kind %d", kind);
+  if (kind == 2 && elem != 0 && elem != 1)
+    return fail(SRF_E_INVALID_CONFIG, "sigmoid of a non-float type");
+  int rc = check_raw(sp, a_addr, es * n, "operand");
+  if (!rc && kind == 1) rc = check_raw(sp, b_addr, es * n, "operand");
+  if (!rc) rc = check_raw(sp, out_addr, es * n, "result");
+  if (rc) return rc;
+  if (n == 0) return SRF_OK;
+  const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count_of(s->device) * 8);
+  const void *a = base + a_addr, *b = kind == 1 ? base + b_addr : nullptr;
+  void *o = base + out_addr;
+  if (kind == 1) {
+    switch (elem) {
+      case 0: k_add<float><<<grid, 256, 0, s->s>>>((const float *)a, (const float *)b, (float *)o, n); break;
+      case 1: k_add<double><<<grid, 256, 0, s->s>>>((const double *)a, (const double *)b, (double *)o, n); break;
+      case 2: k_add<int32_t><<<grid, 256, 0, s->s>>>((const int32_t *)a, (const int32_t *)b, (int32_t *)o, n); break;
+      case 3: k_add<int64_t><<<grid, 256, 0, s->s>>>((const int64_t *)a, (const int64_t *)b, (int64_t *)o, n); break;
+      default: k_add<uint8_t><<<grid, 256, 0, s->s>>>((const uint8_t *)a, (const uint8_t *)b, (uint8_t *)o, n); break;
+    }
+  } else if (elem == 0) {
+    k_sigmoid<float><<<grid, 256, 0, s->s>>>((const float *)a, (float *)o, n);
+  } else {
+    k_sigmoid<double><<<grid, 256, 0, s->s>>>((const double *)a, (double *)o, n);
+  }
+  if (recording()) rec_ewise(s->device, grid, kind, elem, a, b, o, n);
+  return launch_check(kind == 1 ? "k_add" : "k_sigmoid");
+}
+
 int srf_timing_event_create(srf_space_t sp, srf_event_t *out) {
   DeviceGuard device_guard;
   CUDA_TRY(cudaSetDevice(sp->device));

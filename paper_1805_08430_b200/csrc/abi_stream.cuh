@@ -230,6 +230,11 @@ int srf_record_end(srf_oplist_t *out, int *replayable) {
   return SRF_OK;
 }
 
+int srf_record_taint(const char *why) {
+  rec_dirty(why ? why : "device work outside the library");
+  return SRF_OK;
+}
+
 int srf_oplist_info(srf_oplist_t l, uint32_t *nops, int *device, char *why, uint32_t why_len) {
   if (nops) *nops = (uint32_t)l->ops.size();
   if (why && why_len && l->exec) {

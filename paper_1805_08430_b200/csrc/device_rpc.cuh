@@ -219,3 +219,37 @@ __global__ void __launch_bounds__(256) k_matmul(const T *a, const T *b, T *c, ui
   for (uint64_t t = 0; t < k; ++t) acc = mm_step<T>(acc, a[i * k + t], b[t * n + j]);
   c[idx] = acc;
 }
+
+// Add and Sigmoid compute kinds (graph.py:373-377): numpy `a + b` on equal
+// shapes (integers wrap), and (1 / (1 + exp(-x.astype(float64)))).astype(x's
+// type) - computed in double like the reference, then rounded once.
+template <typename T>
+__device__ __forceinline__ T ew_add(T a, T b) { return a + b; }
+template <>
+__device__ __forceinline__ int32_t ew_add<int32_t>(int32_t a, int32_t b) {
+  return (int32_t)((uint32_t)a + (uint32_t)b);
+}
+template <>
+__device__ __forceinline__ int64_t ew_add<int64_t>(int64_t a, int64_t b) {
+  return (int64_t)((uint64_t)a + (uint64_t)b);
+}
+template <>
+__device__ __forceinline__ float ew_add<float>(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double ew_add<double>(double a, double b) { return __dadd_rn(a, b); }
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_add(const T *a, const T *b, T *out, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = ew_add<T>(a[i], b[i]);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_sigmoid(const T *x, T *out, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double v = (double)x[i];
+    out[i] = (T)(1.0 / (1.0 + exp(-v)));
+  }
+}

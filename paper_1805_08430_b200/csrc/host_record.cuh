@@ -25,6 +25,7 @@ enum RecKind : int {
   REC_REDUCE = 5,
   REC_CLEAR = 6,
   REC_MATMUL = 7,
+  REC_EWISE = 8,   // Add / Sigmoid compute kinds
 };
 
 struct RecOp {
@@ -54,6 +55,12 @@ struct RecOp {
     int elem;
     uint64_t a, b, c, m, k, n;
   } mm;
+  struct {
+    int op, elem;      // op 1 add, 2 sigmoid
+    const void *a, *b;
+    void *out;
+    uint64_t n;
+  } ew;
 };
 
 struct srf_oplist {
@@ -180,6 +187,17 @@ static void rec_matmul(int device, int elem, uint64_t a, uint64_t b, uint64_t c,
   rec_push(std::move(op));
 }
 
+static void rec_ewise(int device, int grid, int op, int elem, const void *a, const void *b,
+                      void *out, uint64_t n) {
+  RecOp o;
+  o.kind = REC_EWISE;
+  o.device = device;
+  o.grid = grid;
+  o.block = 256;
+  o.ew = {op, elem, a, b, out, n};
+  rec_push(std::move(o));
+}
+
 // a receiver's flag clear (memset of the device byte; the host doorbell was
 // cleared on the host): no kernel launch follows
 static void rec_clear(int device, uint8_t *dev, uint8_t *shadow) {
@@ -215,57 +233,9 @@ static bool rec_same(const RecOp &x, const RecOp &y, int64_t gen_delta) {
     case REC_REDUCE: return memcmp(&x.red, &y.red, sizeof x.red) == 0;
     case REC_CLEAR: return x.clr.dev == y.clr.dev && x.clr.shadow == y.clr.shadow;
     case REC_MATMUL: return memcmp(&x.mm, &y.mm, sizeof x.mm) == 0;
+    case REC_EWISE: return memcmp(&x.ew, &y.ew, sizeof x.ew) == 0;
   }
   return false;
-}
-
-// Issue one recorded iteration on stream s (GenGrad iteration = recorded +
-// *iter_add, read on the device).
-static cudaError_t rec_issue(const srf_oplist *l, cudaStream_t s, const uint64_t *iter_add) {
-  for (const RecOp &op : l->ops) {
-    switch (op.kind) {
-      case REC_PUT:
-        switch (op.variant) {
-          case 0: k_put<8, false><<<op.grid, op.block, 0, s>>>(op.put); break;
-          case 1: k_put<8, true><<<op.grid, op.block, 0, s>>>(op.put); break;
-          case 2: k_put<4, false><<<op.grid, op.block, 0, s>>>(op.put); break;
-          case 3: k_put<4, true><<<op.grid, op.block, 0, s>>>(op.put); break;
-          default: k_put_bulk<<<op.grid, op.block, kBulkSmem, s>>>(op.put); break;
-        }
-        break;
-      case REC_INLINE: k_put_inline<<<1, 256, 0, s>>>(*op.inl); break;
-      case REC_GEN:
-        k_gen_reference<<<op.grid, 512, 0, s>>>(op.gen.dst, op.gen.nf, op.gen.e0, op.gen.seed,
-                                                 op.gen.node, op.gen.iteration, iter_add);
-        break;
-      case REC_APPLY:
-        if (op.apply_sgd)
-          k_apply_sgd<<<op.grid, op.block, 0, s>>>(op.apply);
-        else
-          k_apply_xor<<<op.grid, op.block, 0, s>>>(op.apply);
-        break;
-      case REC_REDUCE:
-        k_reduce_max<<<op.grid, 256, 0, s>>>(op.red.in, op.red.n, op.red.out, op.red.scratch,
-                                             op.red.counter);
-        break;
-      case REC_CLEAR: k_clear_flag<<<1, 1, 0, s>>>(op.clr.dev, op.clr.shadow); break;
-      case REC_MATMUL: {
-        const unsigned g = (unsigned)op.grid;
-        const auto &m = op.mm;
-        switch (m.elem) {
-          case 0: k_matmul<float><<<g, 256, 0, s>>>((const float *)m.a, (const float *)m.b, (float *)m.c, m.m, m.k, m.n); break;
-          case 1: k_matmul<double><<<g, 256, 0, s>>>((const double *)m.a, (const double *)m.b, (double *)m.c, m.m, m.k, m.n); break;
-          case 2: k_matmul<int32_t><<<g, 256, 0, s>>>((const int32_t *)m.a, (const int32_t *)m.b, (int32_t *)m.c, m.m, m.k, m.n); break;
-          case 3: k_matmul<int64_t><<<g, 256, 0, s>>>((const int64_t *)m.a, (const int64_t *)m.b, (int64_t *)m.c, m.m, m.k, m.n); break;
-          default: k_matmul<uint8_t><<<g, 256, 0, s>>>((const uint8_t *)m.a, (const uint8_t *)m.b, (uint8_t *)m.c, m.m, m.k, m.n); break;
-        }
-        break;
-      }
-    }
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
 }
 
 // ---------------------------------------------------------------------------
@@ -313,6 +283,13 @@ static void rec_footprint(const RecOp &op, std::vector<Span> &out) {
       add(op.clr.dev, 1, true);
       if (op.clr.shadow) add(op.clr.shadow, 1, true);
       break;
+    case REC_EWISE: {
+      const uint64_t es = op.ew.elem == 0 || op.ew.elem == 2 ? 4 : op.ew.elem == 4 ? 1 : 8;
+      add(op.ew.a, es * op.ew.n, false);
+      if (op.ew.b) add(op.ew.b, es * op.ew.n, false);
+      add(op.ew.out, es * op.ew.n, true);
+      break;
+    }
     case REC_MATMUL: {
       const uint64_t es = op.mm.elem == 0 || op.mm.elem == 2 ? 4 : op.mm.elem == 4 ? 1 : 8;
       add((const void *)op.mm.a, es * op.mm.m * op.mm.k, false);
@@ -401,6 +378,22 @@ static int rec_build_graph(srf_oplist *l) {
         kp.gridDim = dim3(1);
         kp.blockDim = dim3(1);
         break;
+      case REC_EWISE: {
+        const auto &w = op.ew;
+        if (w.op == 1) {
+          args[0] = (void *)&w.a; args[1] = (void *)&w.b; args[2] = (void *)&w.out;
+          args[3] = (void *)&w.n;
+          kp.func = w.elem == 0   ? (void *)k_add<float>
+                    : w.elem == 1 ? (void *)k_add<double>
+                    : w.elem == 2 ? (void *)k_add<int32_t>
+                    : w.elem == 3 ? (void *)k_add<int64_t>
+                                  : (void *)k_add<uint8_t>;
+        } else {
+          args[0] = (void *)&w.a; args[1] = (void *)&w.out; args[2] = (void *)&w.n;
+          kp.func = w.elem == 0 ? (void *)k_sigmoid<float> : (void *)k_sigmoid<double>;
+        }
+        break;
+      }
       case REC_MATMUL:
         args[0] = (void *)&m.a; args[1] = (void *)&m.b; args[2] = (void *)&m.c;
         args[3] = (void *)&m.m; args[4] = (void *)&m.k; args[5] = (void *)&m.n;

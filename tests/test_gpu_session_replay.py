@@ -33,7 +33,15 @@ CASES = {
     "micro4k_cp": (lambda: build_microbench(4096), {"mode": "cp"}),
     "sgd_ps": (lambda: build_ps_workload(0, 3, 0.0, 2, shapes=mlp_shapes()),
                {"apply_op": "sgd", "lr": 0.05}),
+    # MatMul / Add / Sigmoid through srf_compute, on one server and split
+    "layered": (lambda: _layered(lambda n: 0), {}),
+    "layered_split": (lambda: _layered(lambda n: int(n.kind is NodeKind.MATMUL)), {}),
 }
+
+
+def _layered(side):
+    g, _, _ = build_layered_forward(8)
+    return g, {nid: side(n) for nid, n in g.nodes.items()}
 
 
 def _run(name, replay, n=24):
@@ -85,12 +93,29 @@ def test_replayed_ps_variables_equal_the_oracle():
     s.close()
 
 
-def test_host_compute_kinds_are_not_replayed():
-    """Compute kinds that run as torch ops (Add, Sigmoid) launch kernels the
-    recorder does not see, so such sessions keep the host path."""
-    g, _, _ = build_layered_forward(4)
-    p = {nid: 0 for nid in g.nodes}
-    s = Session(g, p, seed=1, devices={0: 0})
+def test_torch_compute_kinds_are_not_replayed():
+    """ConcatDyn runs as torch ops, which the recorder does not see, so such
+    sessions keep the host path."""
+    from paper_1805_08430_b200.graph import DataFlowGraph, shape_of
+    g = DataFlowGraph()
+    g.reduce_max(g.concat_dyn([g.gen_grad(shape_of(3, 4))], dyn_range=(1, 6)))
+    g.freeze()
+    s = Session(g, {nid: 0 for nid in g.nodes}, seed=1, devices={0: 0})
     s.run(6)
+    assert s.replayed_iterations == 0 and s.replay_status == "off"
+    s.close()
+
+
+def test_torch_fallback_taints_the_recording():
+    """A Sigmoid of an empty tensor is outside srf_compute: it takes the torch
+    path, which taints every iteration's recording."""
+    from paper_1805_08430_b200.graph import DataFlowGraph, shape_of
+    g = DataFlowGraph()
+    g.reduce_max(g.gen_grad(shape_of(64, 4)))
+    g.reduce_max(g.sigmoid(g.gen_grad(shape_of(0, 4))))
+    g.freeze()
+    s = Session(g, {n: 0 for n in g.nodes}, seed=1, devices={0: 0})
+    s.run(8)
     assert s.replayed_iterations == 0
+    assert "torch" in s.replay_status, s.replay_status
     s.close()

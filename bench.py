@@ -353,13 +353,14 @@ class PipelinedRing:
     microbenchmark's tensor (build_microbench GenGrad node 0, graph.py:333-350)
     of iterations 2, 3, ... generated on the device (srf_gen_reference)."""
 
-    def __init__(self, S, rank, world, device, slots=8, nsrc=2, mirror=False):
+    def __init__(self, S, rank, world, device, slots=None, nsrc=2, mirror=False):
         import ctypes as C
         from paper_1805_08430_b200 import _lib
         from paper_1805_08430_b200.distributed import exchange_spaces, lookup, publish_addresses
         from paper_1805_08430_b200.memspace import MemorySpace
         from paper_1805_08430_b200.runtime.protocol import PipelinedStaticEdge
         from paper_1805_08430_b200.wire import AddrExchangeMsg, Mechanism
+        slots = slots or PipelinedStaticEdge.default_slots(S)
         self.lib, self.S, self.world, self.rank, self.slots, self.nsrc = \
             _lib, S, world, rank, slots, nsrc
         self.src_stride = (S + 255) & ~255
@@ -498,13 +499,14 @@ class PipelinedRing:
         self.src.close()
 
 
-def bench_pipelined(S, steps, warmup, rank, world, device, slots=8):
+def bench_pipelined(S, steps, warmup, rank, world, device, slots=None):
     """Headline device timing: K steps, each one k_put_stream launch of R
     rounds (R calibrated to ~25 ms per step) with its consumer, max over
     ranks; the roofline kernel is k_put_stream (algorithmic bytes per launch:
     R * (S+1) over NVLink at N>1, R * (2S+1) through HBM at N=1)."""
     from paper_1805_08430_b200 import _lib
     ring = PipelinedRing(S, rank, world, device, slots=slots)
+    slots = ring.slots
     a, b = ring.event(), ring.event()
     ring.launch(2 * slots)
     ring.sync()
@@ -854,7 +856,7 @@ def sweep(max_bytes, device):
         row["static_1launch_us"] = _ring_graph_us(ring.stream, ring.put_consume, rounds,
                                                   ring.src)
         row["static_1launch_gbps"] = round(size / row["static_1launch_us"] / 1e3, 3)
-        pipe = bench_pipelined(size, 3, 2, 0, 1, device, slots=8)
+        pipe = bench_pipelined(size, 3, 2, 0, 1, device)
         row["static_pipelined_us"] = round(pipe["total_ms"] * 1e3 / pipe["n"], 3)
         row["static_pipelined_gbps"] = round(size / row["static_pipelined_us"] / 1e3, 3)
         row["static_pipelined_verified"] = pipe["verified"]
@@ -934,7 +936,7 @@ def dynamic_device_rate(size, device, rounds=None):
 def sweep_nvlink(max_bytes, rank, world, device):
     """configs[1] over NVLink (N>1): every rank sends to rank+1 at once,
     1 KiB x 4^k up to max_bytes; static zero-copy (the reference's one slot:
-    K1 + K2 per round), the pipelined edge (8 slots, R rounds per launch) and
+    K1 + K2 per round), the pipelined edge (default_slots(S), R rounds per launch) and
     dynamic with the receiver on the device (K3 + srf_dyn_recv
     pulling from the previous rank's pool), graph-replayed rounds, device
     time, max over ranks."""
@@ -957,7 +959,7 @@ def sweep_nvlink(max_bytes, rank, world, device):
                                                   ring.src)
         row["static_1launch_gbps"] = round(size / row["static_1launch_us"] / 1e3, 3)
         row["verified"] = dist_sum(0.0 if ring.verify() else 1.0) == 0.0
-        pipe = bench_pipelined(size, 3, 2, rank, world, device, slots=8)
+        pipe = bench_pipelined(size, 3, 2, rank, world, device)
         row["static_pipelined_us"] = round(pipe["total_ms"] * 1e3 / pipe["n"], 3)
         row["static_pipelined_gbps"] = round(size / row["static_pipelined_us"] / 1e3, 3)
         row["static_pipelined_verified"] = pipe["verified"]
@@ -1460,7 +1462,7 @@ def bench_c1(rank, world, device, cpu=True):
     us = dist_max(_ring_graph_us(ring.stream, lambda: (ring.put(), ring.consume()), 200,
                                  ring.src))
     single = {"verified": dist_sum(0.0 if ring.verify() else 1.0) == 0.0}
-    pipe = bench_pipelined(S, 5, 3, rank, world, device, slots=8)
+    pipe = bench_pipelined(S, 5, 3, rank, world, device)
     e2e = bench_sendrecv_e2e(S, 200, 5, rank, world, device)
     us_pipe = pipe["total_ms"] * 1e3 / pipe["n"]
     per_dir = S / (us * 1e-6) / 1e9

@@ -61,7 +61,12 @@ uint64_t srf_launch_count(void);
  * 1 TMA bulk), 3 = pool allocator (0 cudaMalloc + CUDA IPC, 1 VMM + fd),
  * 4 = 16-B vectors in flight per thread (4 or 8), 5 = 32-B vectors (0/1),
  * 6 = cross-device bodies >= value KiB move on the copy engine, the tail
- *     flag still released by an SM store after them (0 = never; default 32768) */
+ *     flag still released by an SM store after them (0 = never, the default),
+ * 7 = force system-scope puts/gets on one device (tests), 8 = credit/flag
+ *     timeout in ms, 9 = pipelined-edge CTAs per SM (1..4), 10 = pipelined-
+ *     edge chunk KiB (0 = automatic), 11 = flag-only edge consumer threads,
+ * 12 = GenGrad work-unit KiB, 13 = flag-only edge consumer clears with a
+ *     system-scope release (1) instead of a relaxed store (0, the default) */
 int srf_tune(int knob, int value);
 
 /* ---- memory spaces (memspace.py) ----------------------------------------- */

@@ -73,6 +73,9 @@ int srf_tune(int knob, int value) {
       if (value < 16) return fail(SRF_E_INVALID_CONFIG, "gen_unit_kib >= 16");
       g_gen_unit_bytes = (uint64_t)value << 10;
       return SRF_OK;
+    case 13:
+      g_consume_release = value ? 1 : 0;
+      return SRF_OK;
     case 11:
       if (value < 32 || value > 1024 || value % 32)
         return fail(SRF_E_INVALID_CONFIG, "consume_threads: a multiple of 32 in [32, 1024]");

@@ -45,15 +45,15 @@ int srf_edge_create(srf_space_t src_space, uint64_t src_addr, uint64_t src_token
   e->a.slot_stride = slot_stride;
   e->a.slots = slots;
   e->a.nbytes = nbytes;
-  // chunk: S/32 within [32 KiB, 256 KiB] - large enough to amortise a work
+  // chunk: S/16 within [64 KiB, 256 KiB] - large enough to amortise a work
   // item's claim, credit check and system-scope arrival, small enough that a
   // round spreads over many CTAs (tools/edge_probe.py sweep,
-  // profiles/r2_edge_probe.jsonl)
+  // profiles/r2s_edge_slots.jsonl)
   const int sms = sm_count_of(e->device);
   e->ctas = std::max(1, sms * g_edge_ctas_per_sm);
   uint64_t chunk = g_edge_chunk ? (g_edge_chunk << 10)
                                 : std::min<uint64_t>(256 << 10,
-                                                     std::max<uint64_t>(32 << 10, nbytes / 32));
+                                                     std::max<uint64_t>(64 << 10, nbytes / 16));
   chunk = (chunk + 4095) & ~4095ull;
   if (chunk > nbytes) chunk = nbytes;
   e->a.chunk = chunk;
@@ -178,7 +178,8 @@ int srf_edge_consume(srf_space_t rcv, uint64_t slots_addr, uint32_t slots, uint6
     }
   }
   k_consume_stream<<<1, mode == 1 ? 1024 : g_consume_threads, 0, s->s>>>(
-      rcv->base + slots_addr, slot_stride, slots, nbytes, first_round, rounds, mode,
+      rcv->base + slots_addr, slot_stride, slots, nbytes, first_round, rounds,
+      mode == 1 ? 1 : (g_consume_release ? 2 : 0),
       (unsigned long long *)(rcv->base + sums_addr), mirror, sd, ticket, g_put_timeout_ns,
       rcv->err);
   rc = launch_check("k_consume_stream");

@@ -59,6 +59,10 @@ __device__ __forceinline__ void st_release_sys_u32(unsigned int *p, unsigned v) 
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_relaxed_sys_u32(unsigned int *p, unsigned v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void red_release_gpu_max(unsigned int *p, unsigned v) {
   asm volatile("red.release.gpu.global.max.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -96,11 +100,41 @@ __global__ void __launch_bounds__(512) k_put_stream(const __grid_constant__ Stre
           __nanosleep(20);
         }
       } else if (m > 0 && ld_acquire_gpu_u32(a.credit + slot) < m) {
-        if (!spin_until(d + a.nbytes, 0, a.timeout_ns, a.sys)) atomicExch(a.err, 2);
-        red_release_gpu_max(a.credit + slot, m);
+        if (c == 0) {
+          // the round's first chunk polls the receiver's flag; the others
+          // wait on the cached credit (one remote poll per round, not one
+          // per chunk: under two-way load every remote read queues behind
+          // the payload in both link directions)
+          if (!spin_until(d + a.nbytes, 0, a.timeout_ns, a.sys)) atomicExch(a.err, 2);
+          red_release_gpu_max(a.credit + slot, m);
+        } else {
+          const uint64_t t0 = globaltimer_ns();
+          while (ld_acquire_gpu_u32(a.credit + slot) < m && *(volatile int *)a.err == 0) {
+            if (globaltimer_ns() - t0 > a.timeout_ns) {
+              atomicExch(a.err, 2);
+              break;
+            }
+            __nanosleep(20);
+          }
+        }
       }
     }
     __syncthreads();
+    if (c == 0 && !a.credit_mirror && a.slots > 1 && threadIdx.x == 32 &&
+        *(volatile int *)a.err == 0) {
+      // credit look-ahead: one non-blocking poll for the use half the ring
+      // ahead, so by the time its chunks are claimed the credit is cached
+      // (a flag read 0 after that slot's previous use was released means
+      // the consumer cleared it - the same test as the demand path)
+      const uint64_t jn = j + a.slots / 2;
+      const uint32_t sn = (uint32_t)(jn % a.slots), mn = (uint32_t)(jn / a.slots);
+      if (mn > 0 && ld_acquire_gpu_u32(a.credit + sn) < mn &&
+          ld_acquire_gpu_u32(a.released + sn) >= mn) {
+        const uint8_t *fn = a.dst + (uint64_t)sn * a.slot_stride + a.nbytes;
+        if ((a.sys ? ld_acquire_sys_u8(fn) : ld_acquire_gpu_u8(fn)) == 0)
+          red_release_gpu_max(a.credit + sn, mn);
+      }
+    }
     const uint64_t off = (uint64_t)c * a.chunk;
     const uint64_t n = a.nbytes - off < a.chunk ? a.nbytes - off : a.chunk;
     const uint8_t *s = a.src + (j % a.nsrc) * a.src_stride;
@@ -126,7 +160,8 @@ __global__ void __launch_bounds__(512) k_put_stream(const __grid_constant__ Stre
 // optionally checksums the payload the flag guards, then clears the flag
 // (release: the sender may overwrite the slot only after these reads).
 // mode 0: consume the flag only; 1: also store a weighted byte checksum of
-// the round's payload into sums[r] (tests).
+// the round's payload into sums[r] (tests); 2: flag only, cleared with a
+// system-scope release anyway (knob consume_release, for comparison).
 __global__ void __launch_bounds__(1024) k_consume_stream(uint8_t *slots_base, uint64_t slot_stride,
                                                           uint32_t slots, uint64_t nbytes,
                                                           uint64_t first_round, uint32_t rounds,
@@ -152,7 +187,7 @@ __global__ void __launch_bounds__(1024) k_consume_stream(uint8_t *slots_base, ui
     }
     __syncthreads();
     if (!ok) return;
-    if (mode == 1) {
+    if (mode & 1) {
       unsigned long long sum = 0;
       for (uint64_t i = threadIdx.x; i < nbytes; i += blockDim.x)
         sum += (unsigned long long)__ldcg(d + i) * (i % 251 + 1);  // L2: the slot is rewritten
@@ -162,9 +197,17 @@ __global__ void __launch_bounds__(1024) k_consume_stream(uint8_t *slots_base, ui
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      release_tail(d + nbytes, 0, 1);  // StaticReceiver.poll's clear = the credit
-      if (credit_mirror)               // ... mirrored to the sender (posted write)
-        st_release_sys_u32(credit_mirror + j % slots, (unsigned)(j / slots) + 1);
+      // StaticReceiver.poll's clear = the credit.  With a checksum the clear
+      // must be a system-scope release (the sender may overwrite the slot
+      // only after these reads); flag-only consumption read nothing to order,
+      // and a release.sys costs a MEMBAR.SYS that, on a GPU also sending over
+      // NVLink, waits behind its own outbound stores (~4-8 us per round)
+      if (mode) release_tail(d + nbytes, 0, 1);
+      else st_relaxed_sys_u8(d + nbytes, 0);
+      if (credit_mirror) {             // ... mirrored to the sender (posted write)
+        if (mode) st_release_sys_u32(credit_mirror + j % slots, (unsigned)(j / slots) + 1);
+        else st_relaxed_sys_u32(credit_mirror + j % slots, (unsigned)(j / slots) + 1);
+      }
     }
     __syncthreads();
   }

@@ -4,6 +4,7 @@ process.  Modes: same GPU (HBM), GPU0 -> GPU1 (NVLink one direction), and
 both directions at once (the N=2 ring).  Device time of each side's stream
 (events), GB/s = rounds * S / time.  Usage: python tools/edge_probe.py [sizes...]"""
 import ctypes as C
+import itertools
 import json
 import os
 import sys
@@ -112,25 +113,25 @@ def run(mode, S, slots, rounds, mirror=False):
 
 if __name__ == "__main__":
     # PROBE_MODES (nvl1,nvl2,hbm), PROBE_CHUNKS (KiB; 0 = automatic),
-    # PROBE_SLOTS, PROBE_MIRROR (0,1), PROBE_CTAS (CTAs per SM); sizes in argv
+    # PROBE_SLOTS, PROBE_MIRROR (0,1), PROBE_CTAS (CTAs per SM), PROBE_RELEASE
+    # (flag-only consumer clears with release.sys: 0,1); sizes in argv
     sizes = [int(x) for x in sys.argv[1:]] or [MIB, 4 * MIB, 16 * MIB, 64 * MIB, 256 * MIB]
     env = lambda k, d: [int(x) for x in os.environ.get(k, d).split(",")]
     modes = os.environ.get("PROBE_MODES", "nvl1,nvl2,hbm").split(",")
     if ndev < 2:
         modes = [m for m in modes if m == "hbm"]
-    for ctas in env("PROBE_CTAS", "2"):
+    grid = itertools.product(env("PROBE_RELEASE", "0"), env("PROBE_CTAS", "2"), modes, sizes,
+                             env("PROBE_CHUNKS", "0"), env("PROBE_MIRROR", "0"),
+                             env("PROBE_SLOTS", "2,4,8,16"))
+    for rel, ctas, mode, S, chunk_kib, mirror, slots in grid:
+        _lib.tune("consume_release", rel)
         _lib.tune("edge_ctas_per_sm", ctas)
-        for mode in modes:
-            for S in sizes:
-                for chunk_kib in env("PROBE_CHUNKS", "0"):
-                    _lib.tune("edge_chunk_kib", chunk_kib)
-                    for mirror in env("PROBE_MIRROR", "0"):
-                        for slots in env("PROBE_SLOTS", "2,4,8,16"):
-                            # enough rounds that every slot is reused many times
-                            rounds = max(16 * slots, min(400, int(4e9 // S)))
-                            row = run(mode, S, slots, rounds, bool(mirror and mode != "hbm"))
-                            row["chunk_kib_knob"] = chunk_kib
-                            row["ctas_per_sm"] = ctas
-                            print(json.dumps(row), flush=True)
+        _lib.tune("edge_chunk_kib", chunk_kib)
+        # enough rounds that every slot is reused many times
+        rounds = max(16 * slots, min(400, int(4e9 // S)))
+        row = run(mode, S, slots, rounds, bool(mirror and mode != "hbm"))
+        row.update(chunk_kib_knob=chunk_kib, ctas_per_sm=ctas, consume_release=rel)
+        print(json.dumps(row), flush=True)
     _lib.tune("edge_chunk_kib", 0)
     _lib.tune("edge_ctas_per_sm", 2)
+    _lib.tune("consume_release", 0)

@@ -164,6 +164,8 @@ class MemorySpace:
         #: (region_id, base, length, registered, token) - exported to peers
         self.regions: list[tuple[int, int, int, bool, int]] = []
         self.remote = False
+        self._inflight: dict = {}    # receive flag -> event of a write in flight
+        self._pulls: dict = {}       # payload addr -> event of a peer's pull
         h = C.c_void_p()
         _lib.call("srf_space_create", server_id, self.device, capacity, max_regions,
                   C.byref(h))
@@ -207,6 +209,7 @@ class MemorySpace:
         self._torch_stream = None
         self.regions = list(desc["regions"])
         self.remote = True
+        self._inflight, self._pulls = {}, {}
         h = C.c_void_p()
         if "ipc" in desc:
             ipc = (C.c_uint8 * 64).from_buffer_copy(desc["ipc"])
@@ -256,6 +259,10 @@ class MemorySpace:
         return _lib.Event(h)
 
     def close(self) -> None:
+        for table in (getattr(self, "_inflight", {}), getattr(self, "_pulls", {})):
+            for ev in table.values():
+                ev.free()
+            table.clear()
         if getattr(self, "_h", None) is not None and self._h.value:
             _lib.load().srf_space_destroy(self._h)
             self._h = C.c_void_p()
@@ -391,6 +398,38 @@ class MemorySpace:
         if self.remote:
             return
         _lib.call("srf_doorbell_bind", self._h, handle.base_addr, handle.length, int(mirror))
+
+    # -- asynchronous dynamic verbs within one process --------------------------
+    # A DynSender's metadata write and a DynReceiver's pull complete on the
+    # device after the call returns; these tables keep the reference's
+    # observable order: a poll of a receive flag with a write in flight waits
+    # for that write (so `polls` counts stay the reference's), and a payload
+    # that a peer is still pulling is not reused before the pull finished.
+
+    def note_inflight_write(self, tail_addr: int, ev: "_lib.Event") -> None:
+        old = self._inflight.pop(tail_addr, None)
+        if old is not None:
+            old.free()
+        self._inflight[tail_addr] = ev
+
+    def settle_inflight_write(self, tail_addr: int) -> None:
+        ev = self._inflight.pop(tail_addr, None)
+        if ev is not None:
+            ev.wait_free()
+
+    def note_pull(self, addr: int, ev: "_lib.Event") -> None:
+        old = self._pulls.pop(addr, None)
+        if old is not None:
+            old.free()
+        self._pulls[addr] = ev
+
+    def order_after_pull(self, addr: int) -> None:
+        """Order this space's stream after a peer's pull of ``addr`` (no host
+        wait)."""
+        ev = self._pulls.pop(addr, None)
+        if ev is not None:
+            _lib.call("srf_space_wait_event", self._h, ev._h)
+            ev.free()
 
     def flag_read(self, tail_addr: int, length: int = 1) -> bytes:
         """The ``length`` bytes ending at ``tail_addr`` (inclusive): from the
@@ -554,8 +593,12 @@ class BufferRef:
             owned_and_dead = self._refs == 0 and self.arena is not None
         if owned_and_dead:
             # event-guarded: device work queued on the space's stream before
-            # this release may still read or write the block
-            fence = getattr(self.arena.space, "fence", None)
+            # this release may still read or write the block, and so may a
+            # peer's pull of it (a DynReceiver in this process)
+            space = self.arena.space
+            if getattr(space, "_pulls", None):
+                space.order_after_pull(self.handle.base_addr)
+            fence = getattr(space, "fence", None)
             self.arena.free(self.handle, fence=fence() if fence is not None else None)
 
     def __repr__(self) -> str:  # pragma: no cover

@@ -1740,17 +1740,19 @@ def main() -> int:
                 label=f"EXTENSION: VGG-16 with byte-balanced shards (largest-first), "
                       f"{world} workers + {world} shards co-located"))
             # labelled extension: pipelined transfers - the reference placement,
-            # every tensor > 2 MiB cut into 2 MiB slices on its own shard, so a
+            # every tensor > 8 MiB cut into 8 MiB slices on its own shard, so a
             # slice's update overlaps the next slice's transfer; gradient edges
             # STATIC (the reference's mechanism_override="static"): every
-            # NVLink byte is a store, no GPU pulls and pushes through its SMs
-            Ls = PsLayout(vgg16_shapes(), world, world, colocate=True, slice_bytes=2 << 20,
+            # NVLink byte is a store, no GPU pulls and pushes through its SMs,
+            # and the pushes run on their own lane of 128 CTAs beside GenGrad
+            # and the applies (profiles/r2_ps_push_lane.jsonl)
+            Ls = PsLayout(vgg16_shapes(), world, world, colocate=True, slice_bytes=8 << 20,
                           grad_mechanism="static")
             section("ps_sliced", lambda: bench_ps(
                 rank, world, local, max(10, args.steps), args.warmup, op=args.ps_op,
                 cpu=False, layout=Ls,
-                label=f"EXTENSION: VGG-16, reference round-robin placement, tensors > 2 MiB "
-                      f"sent as 2 MiB slices ({len(Ls.shapes)} transfer units), gradient "
+                label=f"EXTENSION: VGG-16, reference round-robin placement, tensors > 8 MiB "
+                      f"sent as 8 MiB slices ({len(Ls.shapes)} transfer units), gradient "
                       f"edges static (mechanism_override), "
                       f"{world} workers + {world} shards co-located"))
             # labelled extension: partitioned variables (every tensor > 16 MiB cut

@@ -66,7 +66,8 @@ uint64_t srf_launch_count(void);
  *     timeout in ms, 9 = pipelined-edge CTAs per SM (1..4), 10 = pipelined-
  *     edge chunk KiB (0 = automatic), 11 = flag-only edge consumer threads,
  * 12 = GenGrad work-unit KiB, 13 = flag-only edge consumer clears with a
- *     system-scope release (1) instead of a relaxed store (0, the default) */
+ *     system-scope release (1) instead of a relaxed store (0, the default),
+ * 14 = pipelined-edge CTAs in total (0: knob 9 per SM) */
 int srf_tune(int knob, int value);
 
 /* ---- memory spaces (memspace.py) ----------------------------------------- */

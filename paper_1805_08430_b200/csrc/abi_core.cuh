@@ -76,6 +76,10 @@ int srf_tune(int knob, int value) {
     case 13:
       g_consume_release = value ? 1 : 0;
       return SRF_OK;
+    case 14:
+      if (value < 0 || value > 4096) return fail(SRF_E_INVALID_CONFIG, "edge_ctas 0..4096");
+      g_edge_ctas = value;
+      return SRF_OK;
     case 11:
       if (value < 32 || value > 1024 || value % 32)
         return fail(SRF_E_INVALID_CONFIG, "consume_threads: a multiple of 32 in [32, 1024]");

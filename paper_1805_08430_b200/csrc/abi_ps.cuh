@@ -483,9 +483,23 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
     if (x.batch != y.batch) return x.batch < y.batch;
     return x.desc < y.desc;
   });
-  std::vector<ExItem> items(ks.size());
-  for (size_t i = 0; i < ks.size(); ++i)
-    items[i] = {ks[i].unit, (uint16_t)ks[i].kind, (uint16_t)ks[i].batch};
+  // peer pushes get their own lane of CTAs (SRFLOW_PS_PUSH_CTAS, default 128;
+  // 0: one queue); same-GPU pushes are HBM copies and keep the one queue.
+  // VGG-16 N=2, static gradients in 8 MiB slices: 853 it/s with one queue,
+  // 1208 with 128 push CTAs (96: 1072, 160: 1022; profiles/r2_ps_push_lane.jsonl)
+  int lane = (push && push->sys) ? 128 : 0;
+  if (const char *l = getenv("SRFLOW_PS_PUSH_CTAS")) lane = std::max(0, atoi(l));
+  size_t npush_items = 0;
+  for (const K &k : ks) npush_items += k.kind == 0;
+  if (npush_items == 0 || npush_items == ks.size()) lane = 0;
+  if (const char *g = getenv("SRFLOW_PS_EXCHANGE_GRID"))
+    if (atoi(g) < 2) lane = 0;  // one CTA: one queue
+  std::vector<ExItem> items;
+  items.reserve(ks.size());
+  for (int pass = 0; pass < (lane ? 2 : 1); ++pass)
+    for (const K &k : ks)
+      if (!lane || (pass == 0) == (k.kind == 0))
+        items.push_back({k.unit, (uint16_t)k.kind, (uint16_t)k.batch});
   srf_exchange *x = new srf_exchange();
   x->device = device;
   memset(&x->args, 0, sizeof x->args);
@@ -510,8 +524,8 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
   cudaError_t e = cudaMalloc(&x->items, sizeof(ExItem) * std::max<size_t>(1, items.size()));
   if (e == cudaSuccess && !items.empty())
     e = cudaMemcpy(x->items, items.data(), sizeof(ExItem) * items.size(), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMalloc(&x->ctr, 2 * sizeof(unsigned int));
-  if (e == cudaSuccess) e = cudaMemset(x->ctr, 0, 2 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMalloc(&x->ctr, 3 * sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(x->ctr, 0, 3 * sizeof(unsigned int));
   const int np = a.npush, ng = a.ngen;
   x->ndone = std::max(nd + np + ng, 1);
   if (e == cudaSuccess) e = cudaMalloc(&x->done, sizeof(unsigned int) * x->ndone);
@@ -536,6 +550,12 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
   a.items = x->items;
   a.claim = x->ctr;
   a.exit_count = x->ctr + 1;
+  if (lane) {
+    a.nitems = (uint32_t)npush_items;
+    a.items1 = x->items + npush_items;
+    a.nitems1 = (uint32_t)(items.size() - npush_items);
+    a.claim1 = x->ctr + 2;
+  }
   a.done = x->done;
   a.push_done = x->push_done;
   a.seq_push = np ? x->done + nd : nullptr;
@@ -544,6 +564,8 @@ int srf_ps_exchange_create(srf_batch_t push, const uint64_t *push_key, srf_batch
   a.iters = 1;
   x->grid = sm_count_of(device) * std::max(1, per_sm);
   if (const char *g = getenv("SRFLOW_PS_EXCHANGE_GRID")) x->grid = std::max(1, atoi(g));
+  // each lane keeps at least one CTA
+  if (lane) a.lane_ctas = (uint32_t)std::min(lane, x->grid - 1);
   *out = x;
   return SRF_OK;
 }

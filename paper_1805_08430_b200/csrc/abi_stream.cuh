@@ -50,7 +50,7 @@ int srf_edge_create(srf_space_t src_space, uint64_t src_addr, uint64_t src_token
   // round spreads over many CTAs (tools/edge_probe.py sweep,
   // profiles/r2s_edge_slots.jsonl)
   const int sms = sm_count_of(e->device);
-  e->ctas = std::max(1, sms * g_edge_ctas_per_sm);
+  e->ctas = g_edge_ctas ? g_edge_ctas : std::max(1, sms * g_edge_ctas_per_sm);
   uint64_t chunk = g_edge_chunk ? (g_edge_chunk << 10)
                                 : std::min<uint64_t>(256 << 10,
                                                      std::max<uint64_t>(64 << 10, nbytes / 16));

@@ -613,6 +613,12 @@ struct ExArgs {
   uint32_t iters;
   unsigned int *done; int apply_base[kMaxApply]; const int *push_done;
   unsigned int *seq_push, *seq_gen;  // per-descriptor completion counts (this launch)
+  // two lanes (lane_ctas > 0): CTAs [0, lane_ctas) claim the peer pushes
+  // (`items`), the others GenGrad and apply (`items1`), each lane in the same
+  // global order - pushes then occupy one CTA slot on lane_ctas SMs (the link
+  // saturates with ~96 pushing CTAs) while the compute units fill the rest,
+  // instead of the whole grid pushing, then the whole grid computing
+  const ExItem *items1; uint32_t nitems1; unsigned int *claim1; uint32_t lane_ctas;
 };
 
 // kMinBlocks 3: 40 registers, 3 CTAs per SM - more bytes in flight for
@@ -621,14 +627,18 @@ struct ExArgs {
 template <int kMinBlocks>
 __global__ void __launch_bounds__(512, kMinBlocks) k_ps_exchange(const __grid_constant__ ExArgs a) {
   __shared__ uint32_t s_i;
+  const bool lane1 = a.lane_ctas && blockIdx.x >= a.lane_ctas;
+  const ExItem *items = lane1 ? a.items1 : a.items;
+  const uint32_t nitems = lane1 ? a.nitems1 : a.nitems;
+  unsigned int *claim = lane1 ? a.claim1 : a.claim;
   for (;;) {
-    if (threadIdx.x == 0) s_i = atomicAdd(a.claim, 1u);
+    if (threadIdx.x == 0) s_i = atomicAdd(claim, 1u);
     __syncthreads();
     const uint32_t i = s_i;
     __syncthreads();
-    if (i >= a.nitems * a.iters) break;
-    const uint32_t k = i / a.nitems;
-    const ExItem x = a.items[i - k * a.nitems];
+    if (i >= nitems * a.iters) break;
+    const uint32_t k = i / nitems;
+    const ExItem x = items[i - k * nitems];
     if (x.kind == 0)
       put_unit(a.push, a.npush, x.unit, a.cpush, a.timeout_ns, a.err, a.push_sys, a.done,
                a.push_done, k, a.seq_push, true);
@@ -642,6 +652,7 @@ __global__ void __launch_bounds__(512, kMinBlocks) k_ps_exchange(const __grid_co
   // the last CTA out re-arms the queue for the next launch
   if (threadIdx.x == 0 && atomicAdd(a.exit_count, 1u) == gridDim.x - 1) {
     *a.claim = 0;
+    if (a.claim1) *a.claim1 = 0;
     *a.exit_count = 0;
   }
 }

@@ -81,6 +81,7 @@ static uint64_t g_peer_ce_bytes = 0;
 static int g_force_sys = 0;  // knob 7 (tests): every put/get takes the cross-device path
 static uint64_t g_put_timeout_ns = 5000000000ull;  // knob 8: credit wait limit of a put
 static int g_edge_ctas_per_sm = 2;   // knob 9: pipelined edge CTAs per SM
+static int g_edge_ctas = 0;          // knob 14: pipelined edge CTAs in total (0: per-SM knob)
 static uint64_t g_edge_chunk = 0;    // knob 10: pipelined edge chunk (KiB; 0 = automatic)
 static int g_consume_threads = 32;   // knob 11: flag-only edge consumer CTA size
 static int g_consume_release = 0;    // knob 13: flag-only consumer clears with release.sys

@@ -344,3 +344,27 @@ def test_static_sliced_gradients_equal_the_model():
     for v in range(len(shapes)):
         assert got[v].tobytes() == want[v].reshape(-1).tobytes(), v
     ps.close()
+
+
+@pytest.mark.parametrize("lane", [1, 3, 128])
+@pytest.mark.parametrize("grad", ["static", "dynamic"])
+def test_push_lane_exchange_matches_oracle(monkeypatch, lane, grad):
+    """Two-lane exchange (SRFLOW_PS_PUSH_CTAS: the first `lane` CTAs claim the
+    pushes, the rest GenGrad and the applies, each lane in the global order):
+    bit-identical variables, several iterations per launch, with as few as one
+    push CTA (on one GPU the lanes only activate through the knob; across GPUs
+    128 is the default)."""
+    monkeypatch.setenv("SRFLOW_PS_PUSH_CTAS", str(lane))
+    shapes, W, P = [(3000,), (17,), (64, 70), (5,)], 3, 3
+    L = PsLayout(shapes, W, P, True, slice_bytes=2048, grad_mechanism=grad)
+    ps = PsStep(L, seed=9, op="sgd", lr=0.02, schedule="exchange")
+    ps.run_exchange(1, 7, per_launch=3)
+    ps.sync()
+    want = port.ps_expected(shapes, W, 9, 7, op="sgd", lr=0.02)
+    got = [np.zeros(int(np.prod(s)), np.float32) for s in shapes]
+    for u in range(len(L.shapes)):
+        v, off, n = L.parent(u)
+        got[v][off:off + n] = ps.variable(u).reshape(-1)
+    for v in range(len(shapes)):
+        assert got[v].tobytes() == want[v].reshape(-1).tobytes(), (v, lane, grad)
+    ps.close()

@@ -125,7 +125,9 @@ if __name__ == "__main__":
                              env("PROBE_SLOTS", "2,4,8,16"))
     for rel, ctas, mode, S, chunk_kib, mirror, slots in grid:
         _lib.tune("consume_release", rel)
-        _lib.tune("edge_ctas_per_sm", ctas)
+        # PROBE_CTAS: CTAs per SM (1..4) or, above 4, CTAs in total
+        _lib.tune("edge_ctas_per_sm", ctas if ctas <= 4 else 2)
+        _lib.tune("edge_ctas", ctas if ctas > 4 else 0)
         _lib.tune("edge_chunk_kib", chunk_kib)
         # enough rounds that every slot is reused many times
         rounds = max(16 * slots, min(400, int(4e9 // S)))
@@ -135,3 +137,4 @@ if __name__ == "__main__":
     _lib.tune("edge_chunk_kib", 0)
     _lib.tune("edge_ctas_per_sm", 2)
     _lib.tune("consume_release", 0)
+    _lib.tune("edge_ctas", 0)

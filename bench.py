@@ -1432,13 +1432,24 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
 def bench_ps_configs(rank, world, device, steps, warmup, op, cpu):
     from paper_1805_08430_b200.ps import PsLayout
     out = {}
-    for name, (label, shapes_fn, W, P, coloc) in PS_CONFIGS.items():
-        L = PsLayout(shapes_fn(), W, P, coloc)
+    runs = [(name, label, shapes_fn, W, P, coloc, {})
+            for name, (label, shapes_fn, W, P, coloc) in PS_CONFIGS.items()]
+    if world > 1:
+        # labelled extension: the same placements with STATIC gradient edges
+        # (mechanism_override) in 8 MiB slices - push-only NVLink traffic, the
+        # pushes on the exchange's own CTA lane
+        runs += [(name + "_static", "EXTENSION: " + label + ", gradient edges static, "
+                  "8 MiB slices", shapes_fn, W, P, coloc,
+                  {"grad_mechanism": "static", "slice_bytes": 8 << 20})
+                 for name, (label, shapes_fn, W, P, coloc) in PS_CONFIGS.items()
+                 if name != "mlp"]
+    for name, label, shapes_fn, W, P, coloc, kw in runs:
+        L = PsLayout(shapes_fn(), W, P, coloc, **kw)
         where = ("all servers on GPU 0" if world == 1 else
                  f"server s on GPU s mod {world}")
         try:
-            out[name] = bench_ps(rank, world, device, steps, warmup, op=op, cpu=cpu, layout=L,
-                                 label=f"{label}; {where}")
+            out[name] = bench_ps(rank, world, device, steps, warmup, op=op,
+                                 cpu=cpu and not kw, layout=L, label=f"{label}; {where}")
         except Exception as exc:  # pragma: no cover - box dependent
             log(f"ps config {name} failed: {type(exc).__name__}: {exc}")
             out[name] = {"error": f"{type(exc).__name__}: {exc}"[:300]}

@@ -976,6 +976,190 @@ def sweep_nvlink(max_bytes, rank, world, device):
     return out
 
 
+
+class OneWayEdge:
+    """configs[1] as the config names it: ONE sender (rank 0, GPU 0) and ONE
+    receiver (rank 1, GPU 1), one direction of NVLink, static placement with
+    the receiver's pre-placed slots.  mode "push": the pipelined edge
+    (k_put_stream on the sender's GPU, SM stores into the peer's slots);
+    mode "pull": the pull edge (k_pull_stream on the receiver's GPU, TMA bulk
+    copies from the sender's payload straight into the slots, the sender
+    posts rounds with one system-scope store).  Payloads: the microbench
+    tensor (GenGrad node 0, iterations 2, 3) on the device.  Ranks >= 2 only
+    take part in the collectives."""
+
+    def __init__(self, S, rank, world, device, mode, slots=None, nsrc=2):
+        import ctypes as C
+        from paper_1805_08430_b200 import _lib
+        from paper_1805_08430_b200.distributed import all_gather_objects, exchange_spaces
+        from paper_1805_08430_b200.memspace import MemorySpace
+        from paper_1805_08430_b200.runtime.protocol import PipelinedStaticEdge, PulledStaticEdge
+        self.lib, self.S, self.rank, self.mode, self.nsrc = _lib, S, rank, mode, nsrc
+        self.slots = slots or PipelinedStaticEdge.default_slots(S)
+        self.src_stride = (S + 255) & ~255
+        self.slot_stride = (S + 1 + 255) & ~255
+        self.role = {0: "snd", 1: "rcv"}.get(rank)
+        size = {"snd": nsrc * self.src_stride, "rcv": self.slots * self.slot_stride}.get(
+            self.role, 0)
+        self.sp = MemorySpace(rank, size + (8 << 20), seed=0, device=device)
+        mine = {}
+        if self.role == "snd":
+            self.payloads = self.sp.allocate_region(nsrc * self.src_stride, register=True)
+            for i in range(nsrc):
+                _lib.call("srf_gen_reference", self.sp.handle,
+                          self.payloads.base_addr + i * self.src_stride, S // 4, 0, 0, 0, 2 + i,
+                          None, None)
+            mine = {"addr": self.payloads.base_addr, "token": self.payloads.access_token}
+        elif self.role == "rcv":
+            self.slots_reg = self.sp.allocate_region(self.slots * self.slot_stride, register=True)
+            self.posted = self.sp.allocate_region(8)
+            for i in range(self.slots):
+                self.sp.write_raw(self.slots_reg.base_addr + i * self.slot_stride + S, b"\x00")
+            mine = {"addr": self.slots_reg.base_addr, "token": self.slots_reg.access_token,
+                    "posted": self.posted.base_addr}
+        self.sp.sync()
+        coords = all_gather_objects(mine)
+        peer = {"snd": [1], "rcv": [0]}.get(self.role, [])
+        self.proxies = exchange_spaces(self.sp, peers=peer)
+        self.peer = coords[1 if self.role == "snd" else 0] if self.role else None
+        self.st = [C.c_void_p(), C.c_void_p()]
+        for h in self.st:
+            _lib.call("srf_stream_create", self.sp.handle, C.byref(h))
+        self.edge = None
+        if mode == "push" and self.role == "snd":
+            self.edge = PipelinedStaticEdge(self.sp, self.payloads, S, nsrc, self.src_stride,
+                                            self.proxies[1], self.peer["addr"],
+                                            self.peer["token"], self.slots, self.slot_stride)
+        elif mode == "pull" and self.role == "rcv":
+            self.edge = PulledStaticEdge(self.proxies[0], self.peer["addr"], self.peer["token"],
+                                         S, nsrc, self.src_stride, self.sp, self.slots_reg,
+                                         self.slots, self.slot_stride, self.posted.base_addr,
+                                         tma=True)
+        self.info = self.edge.info() if self.edge is not None else {}
+        self.next = 0
+        self.ev = None
+        barrier_sync()
+
+    def launch(self, rounds, timed=False):
+        """Receiver: its consumer first (resident beside a pull grid), then the
+        pull launch; sender: the push launch, or the post of the rounds."""
+        import ctypes as C
+        from paper_1805_08430_b200.runtime.protocol import PipelinedStaticEdge, PulledStaticEdge
+        if timed and self.edge is not None and self.ev is None:
+            self.ev = [C.c_void_p(), C.c_void_p()]
+            for e in self.ev:
+                self.lib.call("srf_timing_event_create", self.sp.handle, C.byref(e))
+        if self.role == "rcv":
+            PipelinedStaticEdge.consume(self.sp, self.slots_reg.base_addr, self.slots,
+                                        self.slot_stride, self.S, self.next, rounds,
+                                        stream=self.st[1])
+        elif self.role == "snd" and self.mode == "pull":
+            PulledStaticEdge.post(self.sp, self.proxies[1], self.peer["posted"],
+                                  self.next + rounds, stream=self.st[1])
+        if self.edge is not None:
+            if timed:
+                self.lib.call("srf_event_record_on", self.ev[0], self.st[0])
+            if self.mode == "push":
+                self.edge.send(rounds, self.st[0])
+            else:
+                self.edge.recv(rounds, self.st[0])
+            if timed:
+                self.lib.call("srf_event_record_on", self.ev[1], self.st[0])
+        self.next += rounds
+
+    def sync(self):
+        for h in self.st:
+            self.lib.call("srf_stream_sync", h)
+        self.sp.sync()
+
+    def elapsed_ms(self) -> float:
+        import ctypes as C
+        if self.ev is None:
+            return 0.0
+        ms = C.c_float()
+        self.lib.call("srf_event_elapsed_ms", self.ev[0], self.ev[1], C.byref(ms))
+        return ms.value
+
+    def verify(self) -> bool:
+        """Receiver: the last `slots` rounds' slots hold, bit for bit, the
+        sender's payload j % nsrc and their flags were consumed."""
+        import hashlib
+        from paper_1805_08430_b200.distributed import all_gather_objects
+        srcs = []
+        if self.role == "snd":
+            srcs = [hashlib.sha256(self.sp.read_raw(self.payloads.base_addr + i * self.src_stride,
+                                                    self.S)).hexdigest()
+                    for i in range(self.nsrc)]
+        want = all_gather_objects(srcs)[0]
+        ok = True
+        if self.role == "rcv":
+            for j in range(max(0, self.next - self.slots), self.next):
+                raw = self.sp.read_raw(
+                    self.slots_reg.base_addr + (j % self.slots) * self.slot_stride, self.S + 1)
+                ok &= hashlib.sha256(raw[:self.S]).hexdigest() == want[j % self.nsrc] \
+                    and raw[self.S] == 0
+        return dist_sum(0.0 if ok else 1.0) == 0.0
+
+    def close(self):
+        self.sync()
+        if self.edge is not None:
+            self.edge.close()
+        for h in self.st:
+            self.lib.call("srf_stream_destroy", h)
+        barrier_sync()
+        for p in self.proxies.values():
+            p.close()
+        barrier_sync()
+        self.sp.close()
+
+
+def one_way_rate(S, rank, world, device, mode, target_ms=20.0):
+    """GB/s of one direction (rank 0 -> rank 1) for rounds of S bytes: device
+    time of the launching rank's stream (max over ranks), after a warm-up
+    launch; verified bit-exact on the receiver."""
+    e = OneWayEdge(S, rank, world, device, mode)
+    rounds = int(max(4 * e.slots, min(20000, target_ms * 1e-3 * 750e9 // max(S, 1))))
+    e.launch(2 * e.slots)
+    e.sync()
+    barrier_sync()
+    e.launch(rounds, timed=True)
+    e.sync()
+    barrier_sync()
+    ms = dist_max(e.elapsed_ms())
+    ok = e.verify()
+    info = dist_objects_first(e.info, owner=0 if mode == "push" else 1)
+    e.close()
+    return {"gbps": round(S * rounds / (ms / 1e3) / 1e9, 1),
+            "us_per_round": round(ms * 1e3 / rounds, 3), "rounds": rounds,
+            "slots": e.slots, "ctas": info.get("ctas"), "chunk": info.get("chunk"),
+            "verified": ok}
+
+
+def dist_objects_first(obj, owner):
+    from paper_1805_08430_b200.distributed import all_gather_objects
+    return all_gather_objects(obj)[owner]
+
+
+def sweep_nvlink_one_way(max_bytes, rank, world, device):
+    """configs[1] literally: 1 sender / 1 receiver on 2 GPUs, one direction,
+    1 KiB x 4^k up to max_bytes: static placement pushed by the sender's SMs
+    (pipelined edge) and pulled by the receiver's TMA engines (pull edge);
+    GB/s per direction with fractions of the nominal 900 and of the measured
+    770 GB/s peer copy."""
+    out = []
+    size = 1024
+    while size <= max_bytes:
+        log(f"[rank {rank}] sweep_nvlink_one_way {size}")
+        row = {"bytes": size}
+        for mode in ("push", "pull"):
+            r = one_way_rate(size, rank, world, device, mode)
+            row[mode] = r
+            row[f"{mode}_frac_of_900"] = round(r["gbps"] / NVLINK_NOMINAL_GBS, 4)
+        out.append(row)
+        size *= 4
+    return out
+
+
 def _ring_graph_us(stream, body, rounds, space):
     from paper_1805_08430_b200 import _lib
     graph = C.c_void_p()
@@ -1733,6 +1917,7 @@ def main() -> int:
     section("c1", lambda: bench_c1(rank, world, local, not args.no_cpu))
     if world > 1 and not args.no_sweep:
         section("sweep_nvlink", lambda: sweep_nvlink(S, rank, world, local))
+        section("sweep_nvlink_one_way", lambda: sweep_nvlink_one_way(S, rank, world, local))
     if world == 1 and not args.no_sweep:
         section("sweep", lambda: sweep(S, local))
         if not args.no_cpu:

@@ -452,6 +452,28 @@ int srf_edge_consume(srf_space_t receiver, uint64_t slots_addr, uint32_t slots,
                      uint64_t credit_addr, srf_stream_t stream);
 int srf_edge_destroy(srf_edge_t edge);
 
+/* Pull edge (EXTENSION, same per-slot protocol driven by the receiver): the
+ * receiver's GPU pulls round j's payload from the sender's source j % nsrc
+ * (src_space: the receiver's mapping of the sender's pool) straight into its
+ * pre-placed slot j % slots - peer loads, or TMA bulk copies with tma = 1 -
+ * and releases the slot's flag last, like StaticSender.send's final byte
+ * (fabric.py:349-356); consumers are the same srf_edge_consume.  Round j
+ * starts once the sender posted it: srf_edge_post raises the 8-B word at
+ * posted_addr of the receiver's pool (one system-scope release store,
+ * the role of the write's arrival in runtime/protocol.py:63-91), optionally
+ * after waiting until the source it reuses was fully pulled (pulled_addr:
+ * 4 * nsrc B of the sender's pool receiving each source's pulled-use count,
+ * UINT64_MAX: none - the same credit as the slot flag, for the sender's
+ * buffer; fabric.py:371-389 is the one-sided read these pulls replace). */
+int srf_edge_create_pull(srf_space_t src_space, uint64_t src_addr, uint64_t src_token,
+                         uint64_t nbytes, uint32_t nsrc, uint64_t src_stride,
+                         srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
+                         uint32_t slots, uint64_t slot_stride, uint64_t posted_addr,
+                         uint64_t pulled_addr, int tma, srf_edge_t *out);
+int srf_edge_recv(srf_edge_t edge, uint32_t rounds, srf_stream_t stream, srf_space_t dst_space);
+int srf_edge_post(srf_space_t snd_space, srf_space_t rcv_space, uint64_t posted_addr,
+                  uint64_t count, uint64_t wait_addr, uint32_t need, srf_stream_t stream);
+
 /* ---- Session iteration recording and replay (runtime/session.py:606-629) --
  * srf_record_begin / srf_record_end capture every device launch the library
  * makes in between (puts, pulls, inline metadata puts, GenGrad, updates,

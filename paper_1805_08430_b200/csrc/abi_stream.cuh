@@ -7,6 +7,7 @@ struct srf_edge {
   unsigned int *state;     // released[slots] | arrival[slots] | credit[slots] | claim | exit
   uint64_t next_round;
   int ctas;
+  int pull = 0;            // 1: a pull edge (k_pull_stream on the receiver's GPU)
 };
 
 
@@ -92,6 +93,156 @@ int srf_edge_create(srf_space_t src_space, uint64_t src_addr, uint64_t src_token
   return SRF_OK;
 }
 
+// Pull edge: the receiver's GPU runs the edge (k_pull_stream).  src_space
+// may be the receiver's mapping of the sender's pool (imported); dst_space is
+// the receiver's own pool.  posted_addr: 8 B in dst_space (zeroed here) that
+// the sender's srf_edge_post raises; pulled_addr (UINT64_MAX: none): 4*nsrc
+// B of the sender's pool (through src_space) receiving each source's
+// fully-pulled use count.
+int srf_edge_create_pull(srf_space_t src_space, uint64_t src_addr, uint64_t src_token,
+                         uint64_t nbytes, uint32_t nsrc, uint64_t src_stride,
+                         srf_space_t dst_space, uint64_t dst_addr, uint64_t dst_token,
+                         uint32_t slots, uint64_t slot_stride, uint64_t posted_addr,
+                         uint64_t pulled_addr, int tma, srf_edge_t *out) {
+  DeviceGuard device_guard;
+  if (nbytes < 1) return fail(SRF_E_INVALID_LENGTH, "zero-length edge");
+  if (slots < 1 || nsrc < 1) return fail(SRF_E_INVALID_CONFIG, "slots and nsrc must be >= 1");
+  if (slot_stride < nbytes + 1 || (nsrc > 1 && src_stride < nbytes))
+    return fail(SRF_E_INVALID_CONFIG, "slot/source stride shorter than the payload");
+  if (dst_space->imported) return fail(SRF_E_INVALID_CONFIG, "a pull edge's slots are local");
+  const uint64_t src_span = (uint64_t)(nsrc - 1) * src_stride + nbytes;
+  const uint64_t dst_span = (uint64_t)(slots - 1) * slot_stride + nbytes + 1;
+  {
+    std::lock_guard<std::mutex> g(src_space->mu);
+    int rc = check_remote_locked(src_space, src_addr, src_span, src_token);
+    if (rc) return rc;
+  }
+  {
+    std::lock_guard<std::mutex> g(dst_space->mu);
+    int rc = check_registered_locked(dst_space, dst_addr, dst_span, dst_token);
+    if (rc) return rc;
+  }
+  int rc = check_raw(dst_space, posted_addr, 8, "posted word");
+  if (rc) return rc;
+  if (posted_addr % 8) return fail(SRF_E_INVALID_CONFIG, "posted word must be 8-B aligned");
+  if (pulled_addr != UINT64_MAX) {
+    rc = check_raw(src_space, pulled_addr, 4ull * nsrc, "pulled counts");
+    if (rc) return rc;
+    if (pulled_addr % 4) return fail(SRF_E_INVALID_CONFIG, "pulled counts must be 4-B aligned");
+  }
+  if (!src_space->imported && src_space->device != dst_space->device) {
+    int can = 0;
+    CUDA_TRY(cudaDeviceCanAccessPeer(&can, dst_space->device, src_space->device));
+    if (!can) return fail(SRF_E_PEER_UNREACHABLE, "no peer path");
+  }
+  srf_edge *e = new srf_edge();
+  e->device = dst_space->device;
+  e->pull = 1;
+  memset(&e->a, 0, sizeof e->a);
+  e->a.src = src_space->base + src_addr;
+  e->a.src_stride = src_stride;
+  e->a.nsrc = nsrc;
+  e->a.dst = dst_space->base + dst_addr;
+  e->a.slot_stride = slot_stride;
+  e->a.slots = slots;
+  e->a.nbytes = nbytes;
+  const bool aligned = ((uintptr_t)e->a.src % 16 == 0) && ((uintptr_t)e->a.dst % 16 == 0) &&
+                       (nsrc == 1 || src_stride % 16 == 0) && slot_stride % 16 == 0;
+  e->a.tma = (tma && aligned) ? 1 : 0;
+  const int sms = sm_count_of(e->device);
+  // TMA: one CTA per SM keeps 6 x 16 KiB loads in flight from one issuing
+  // thread; SM loads: the push edge's geometry
+  e->ctas = g_edge_ctas ? g_edge_ctas
+                        : std::max(1, e->a.tma ? sms - 1 : sms * g_edge_ctas_per_sm);
+  uint64_t chunk = g_edge_chunk ? (g_edge_chunk << 10)
+                                : std::min<uint64_t>(256 << 10,
+                                                     std::max<uint64_t>(64 << 10, nbytes / 16));
+  chunk = (chunk + 4095) & ~4095ull;
+  if (chunk > nbytes) chunk = nbytes;
+  e->a.chunk = chunk;
+  e->a.nchunks = (uint32_t)((nbytes + chunk - 1) / chunk);
+  e->a.sys = 0;
+  e->a.timeout_ns = g_put_timeout_ns;
+  e->a.err = dst_space->err;
+  e->a.posted = (const unsigned long long *)(dst_space->base + posted_addr);
+  e->a.pulled = pulled_addr == UINT64_MAX ? nullptr
+                                          : (unsigned int *)(src_space->base + pulled_addr);
+  e->next_round = 0;
+  CUDA_TRY(cudaSetDevice(e->device));
+  const size_t words = 3 * (size_t)slots + 2;
+  cudaError_t err = cudaMalloc(&e->state, words * sizeof(unsigned));
+  if (err == cudaSuccess) err = cudaMemset(e->state, 0, words * sizeof(unsigned));
+  if (err == cudaSuccess) err = cudaMemset((void *)e->a.posted, 0, 8);
+  if (err == cudaSuccess) err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) {
+    delete e;
+    return fail(SRF_E_DEVICE, "edge state: %s", cudaGetErrorString(err));
+  }
+  e->a.released = e->state;
+  e->a.arrival = e->state + slots;
+  e->a.credit = e->state + 2 * slots;
+  e->a.claim = e->state + 3 * slots;
+  e->a.exit_count = e->state + 3 * slots + 1;
+  *out = e;
+  return SRF_OK;
+}
+
+// the receiver pulls its next `rounds` rounds (one persistent launch)
+int srf_edge_recv(srf_edge_t e, uint32_t rounds, srf_stream_t st, srf_space_t dst_space) {
+  DeviceGuard device_guard;
+  if (!e->pull) return fail(SRF_E_INVALID_CONFIG, "srf_edge_recv needs a pull edge");
+  if (rounds == 0) return SRF_OK;
+  if ((uint64_t)rounds * e->a.nchunks > 0xFFFFFFFFull)
+    return fail(SRF_E_INVALID_CONFIG, "too many work items in one launch");
+  srf_stream *s = stream_or_default(dst_space, st);
+  if (s->device != e->device) return fail(SRF_E_INVALID_CONFIG, "stream on another GPU");
+  StreamEdgeArgs a = e->a;
+  a.first_round = e->next_round;
+  a.rounds = rounds;
+  const uint64_t items = (uint64_t)rounds * a.nchunks;
+  const int grid = (int)std::min<uint64_t>((uint64_t)e->ctas, items);
+  CUDA_TRY(cudaSetDevice(e->device));
+  if (a.tma) {
+    static bool attr_set[64] = {false};
+    if (e->device >= 0 && e->device < 64 && !attr_set[e->device]) {
+      CUDA_TRY(cudaFuncSetAttribute(k_pull_stream<true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem));
+      attr_set[e->device] = true;
+    }
+    k_pull_stream<true><<<grid, 256, kBulkSmem, s->s>>>(a);
+  } else {
+    k_pull_stream<false><<<grid, 512, 0, s->s>>>(a);
+  }
+  int rc = launch_check("k_pull_stream");
+  if (rc) return rc;
+  e->next_round += rounds;
+  return SRF_OK;
+}
+
+// The sender's half of a pull edge: raise the receiver's posted-round word
+// to `count` (rounds [0, count) are in their sources).  rcv_space: the
+// sender's mapping of the receiver's pool.  wait_addr (UINT64_MAX: none) /
+// need: first wait until the 4-B pulled count at wait_addr of the sender's
+// own pool reaches need (the source about to be reused was fully pulled).
+int srf_edge_post(srf_space_t snd_space, srf_space_t rcv_space, uint64_t posted_addr,
+                  uint64_t count, uint64_t wait_addr, uint32_t need, srf_stream_t st) {
+  DeviceGuard device_guard;
+  int rc = check_raw(rcv_space, posted_addr, 8, "posted word");
+  if (rc) return rc;
+  if (posted_addr % 8) return fail(SRF_E_INVALID_CONFIG, "posted word must be 8-B aligned");
+  const unsigned int *wp = nullptr;
+  if (wait_addr != UINT64_MAX) {
+    rc = check_raw(snd_space, wait_addr, 4, "pulled count");
+    if (rc) return rc;
+    wp = (const unsigned int *)(snd_space->base + wait_addr);
+  }
+  srf_stream *s = stream_or_default(snd_space, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  k_post_rounds<<<1, 1, 0, s->s>>>((unsigned long long *)(rcv_space->base + posted_addr), count,
+                                   wp, need, g_put_timeout_ns, snd_space->err);
+  return launch_check("k_post_rounds");
+}
+
 int srf_edge_info(srf_edge_t e, uint64_t *chunk, uint32_t *nchunks, int *ctas,
                   uint64_t *next_round) {
   if (chunk) *chunk = e->a.chunk;
@@ -113,6 +264,7 @@ int srf_edge_state(srf_edge_t e, uint32_t *host_out, uint32_t nwords) {
 
 int srf_edge_send(srf_edge_t e, uint32_t rounds, srf_stream_t st, srf_space_t src_space) {
   DeviceGuard device_guard;
+  if (e->pull) return fail(SRF_E_INVALID_CONFIG, "a pull edge runs on the receiver: srf_edge_recv");
   if (rounds == 0) return SRF_OK;
   if ((uint64_t)rounds * e->a.nchunks > 0xFFFFFFFFull)
     return fail(SRF_E_INVALID_CONFIG, "too many work items in one launch");

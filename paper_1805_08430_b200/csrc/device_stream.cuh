@@ -47,6 +47,12 @@ struct StreamEdgeArgs {
   int sys;                 // destination is a peer's memory
   uint64_t timeout_ns;
   int *err;
+  // pull edges (k_pull_stream, launched on the RECEIVER's GPU): src is the
+  // sender's memory, dst the receiver's own slots
+  const unsigned long long *posted;  // receiver-local: rounds the sender posted
+  unsigned int *pulled;    // [nsrc] in the SENDER's memory: uses of each source
+                           // fully pulled (nullptr: none)
+  int tma;                 // 1: chunks move through TMA bulk copies
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_sys_u32(const unsigned int *p) {
@@ -211,4 +217,160 @@ __global__ void __launch_bounds__(1024) k_consume_stream(uint8_t *slots_base, ui
     }
     __syncthreads();
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Pull edge (k_pull_stream): the same pipelined static edge, driven by the
+// RECEIVER.  The sender posts "round j's payload is in source j % nsrc" by
+// storing the posted-round count into a word of the receiver's pool
+// (k_post_rounds, one posted store over NVLink per batch of rounds); the
+// receiver's SMs pull each (round, chunk) item from the sender's memory
+// straight into the pre-placed slot (peer loads, or TMA bulk copies peer
+// global -> shared -> local global) and the last arriver of a round releases
+// the slot's flag exactly as the push edge does (flag last, the consumer
+// clears it = the credit).  Why: one GPU's NVLink read responses carry user
+// data at 751-765 GB/s one way against 700-719 for its SM stores
+// (profiles/r2_pull_ring.jsonl: the write packets' header overhead); the
+// credit checks become local loads.  When the sender may rewrite a source,
+// the last arriver also publishes the source's pulled-use count into the
+// sender's memory (red.max.release.sys), the sender's licence to reuse it.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const unsigned long long *p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// thread 0 only: [src, src + n) -> [dst, ...) through shared memory with
+// kBulkStages 16-KiB stages (n a multiple of 16, both 16-B aligned); seq
+// continues across calls so every stage's mbarrier phase is (use / stages) & 1
+__device__ void bulk_copy_range(uint8_t *dst, const uint8_t *src, uint64_t n, uint8_t *stage,
+                                uint64_t *bars, uint32_t &seq) {
+  const uint32_t np = (uint32_t)((n + kBulkChunk - 1) / kBulkChunk);
+  auto bytes_of = [&](uint32_t p) {
+    const uint64_t off = (uint64_t)p * kBulkChunk;
+    return (uint32_t)(n - off < (uint64_t)kBulkChunk ? n - off : kBulkChunk);
+  };
+  const uint32_t pre = np < (uint32_t)kBulkStages ? np : kBulkStages;
+  for (uint32_t p = 0; p < pre; ++p) {
+    const uint32_t st = (seq + p) % kBulkStages;
+    mbar_expect_tx(&bars[st], bytes_of(p));
+    bulk_g2s(stage + st * kBulkChunk, src + (uint64_t)p * kBulkChunk, bytes_of(p), &bars[st]);
+  }
+  for (uint32_t p = 0; p < np; ++p) {
+    const uint32_t q = seq + p, st = q % kBulkStages;
+    mbar_wait(&bars[st], (q / kBulkStages) & 1);
+    bulk_s2g(dst + (uint64_t)p * kBulkChunk, stage + st * kBulkChunk, bytes_of(p));
+    if (p >= 1 && p - 1 + kBulkStages < np) {
+      bulk_wait_read<1>();  // piece p-1's store has read its stage: refill it
+      const uint32_t pp = p - 1 + kBulkStages, s2 = (seq + pp) % kBulkStages;
+      mbar_expect_tx(&bars[s2], bytes_of(pp));
+      bulk_g2s(stage + s2 * kBulkChunk, src + (uint64_t)pp * kBulkChunk, bytes_of(pp),
+               &bars[s2]);
+    }
+  }
+  bulk_wait_all();
+  seq += np;
+}
+
+template <bool kTma>
+__global__ void __launch_bounds__(512) k_pull_stream(const __grid_constant__ StreamEdgeArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint32_t s_i;
+  __shared__ int s_last;
+  uint64_t *bars = (uint64_t *)(smem + kBulkChunk * kBulkStages);
+  uint32_t seq = 0;
+  if (kTma && threadIdx.x == 0) {
+    for (int i = 0; i < kBulkStages; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const uint32_t total = a.rounds * a.nchunks;
+  for (;;) {
+    if (threadIdx.x == 0) s_i = atomicAdd(a.claim, 1u);
+    __syncthreads();
+    const uint32_t i = s_i;
+    __syncthreads();
+    if (i >= total) break;
+    const uint32_t jr = i / a.nchunks;
+    const uint32_t c = i - jr * a.nchunks;
+    const uint64_t j = a.first_round + jr;
+    const uint32_t slot = (uint32_t)(j % a.slots);
+    const uint32_t m = (uint32_t)(j / a.slots);
+    uint8_t *d = a.dst + (uint64_t)slot * a.slot_stride;
+    if (threadIdx.x == 0 && *(volatile int *)a.err == 0) {
+      // the sender posted round j (its payload is in place) ...
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_sys_u64(a.posted) < j + 1) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          atomicExch(a.err, 2);
+          break;
+        }
+        __nanosleep(32);
+      }
+      // ... the slot's previous use was released, and consumed (its flag
+      // read 0 again: the consumer's clear, a local load here)
+      wait_count(a.released + slot, m, a.timeout_ns, a.err);
+      if (m > 0 && !spin_until(d + a.nbytes, 0, a.timeout_ns, 0)) atomicExch(a.err, 2);
+    }
+    __syncthreads();
+    const uint64_t off = (uint64_t)c * a.chunk;
+    const uint64_t n = a.nbytes - off < a.chunk ? a.nbytes - off : a.chunk;
+    const uint8_t *s = a.src + (j % a.nsrc) * a.src_stride + off;
+    if (*(volatile int *)a.err == 0) {
+      if (kTma) {
+        const uint64_t mid = n & ~15ull;  // create() checked 16-B alignment
+        if (threadIdx.x == 0 && mid) bulk_copy_range(d + off, s, mid, smem, bars, seq);
+        for (uint64_t k = mid + threadIdx.x; k < n; k += blockDim.x)
+          d[off + k] = ld_byte<true>(s + k);
+        if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+      } else {
+        // coherent loads: a source may be rewritten between rounds
+        copy_bytes_grid<8, true, true>(d + off, s, n, threadIdx.x, blockDim.x, false);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = grid_arrive(a.arrival + slot, a.nchunks - 1, 0);
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      atomicExch(a.arrival + slot, 0u);
+      if (*(volatile int *)a.err == 0) release_tail(d + a.nbytes, 1, 0);  // flag last
+      count_done(a.released + slot);
+      if (a.pulled) {
+        // the source's use is fully read: the sender may rewrite it
+        const unsigned v = (unsigned)(j / a.nsrc) + 1;
+        asm volatile("red.release.sys.global.max.u32 [%0], %1;" ::"l"(a.pulled + j % a.nsrc),
+                     "r"(v)
+                     : "memory");
+      }
+    }
+  }
+  if (threadIdx.x == 0 && atomicAdd(a.exit_count, 1u) == gridDim.x - 1) {
+    *a.claim = 0;
+    *a.exit_count = 0;
+  }
+}
+
+// Sender side of a pull edge: publish "rounds [.., count) are posted" into
+// the receiver's word (one posted store, system-scope release: the payload
+// writes that preceded it on this stream are visible to the receiver's
+// pulls).  With wait_pulled, first wait until the source the first new round
+// reuses was fully pulled (pulled[src] >= need): a sender that rewrites its
+// sources between posts never overwrites bytes a pull may still read.
+__global__ void k_post_rounds(unsigned long long *posted, unsigned long long count,
+                              const unsigned int *wait_pulled, uint32_t need,
+                              uint64_t timeout_ns, int *err) {
+  if (wait_pulled && need) {
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys_u32(wait_pulled) < need) {
+      if (globaltimer_ns() - t0 > timeout_ns) {
+        atomicExch(err, 2);
+        return;
+      }
+      __nanosleep(64);
+    }
+  }
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(posted), "l"(count) : "memory");
 }

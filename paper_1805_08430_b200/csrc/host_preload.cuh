@@ -31,7 +31,9 @@ static int preload_kernels(int device) {
       (const void *)k_consume_stream, (const void *)k_put_inline, (const void *)k_clear_flag,
       (const void *)k_set_u64, (const void *)k_add<float>, (const void *)k_add<double>,
       (const void *)k_add<int32_t>, (const void *)k_add<int64_t>, (const void *)k_add<uint8_t>,
-      (const void *)k_sigmoid<float>, (const void *)k_sigmoid<double>};
+      (const void *)k_sigmoid<float>, (const void *)k_sigmoid<double>,
+      (const void *)k_pull_stream<true>, (const void *)k_pull_stream<false>,
+      (const void *)k_post_rounds};
   for (const void *k : kernels) {
     cudaFuncAttributes attr;
     cudaError_t e = cudaFuncGetAttributes(&attr, k);

@@ -1731,9 +1731,13 @@ def bench_ps_session(rank, world, device, steps, warmup, op, cpu):
         # from iteration 2 the device work is recorded; dynamic edges cycle
         # through a few arena addresses, so steady state (period p) needs 2p
         # recorded iterations
-        while sess.replay_steady is None and sess._next_iteration <= 40:
+        while (sess.replay_steady is None and sess._next_iteration <= 800
+               and "given up" not in sess.replay_status and "not replayable" not in
+               sess.replay_status):
             sess.run(1)
-        sess.run(3)                       # first replays build the replay graphs
+        steady = sess.replay_steady
+        # first replays build the replay graphs: one per phase of the period
+        sess.run(max(3, steady[1] if steady else 0))
         torch.cuda.synchronize(device)
         t0 = time.perf_counter()
         sess.run(3)

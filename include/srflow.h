@@ -498,6 +498,19 @@ int srf_oplist_diff(srf_oplist_t a, srf_oplist_t b, int64_t gen_delta, char *out
 int srf_oplist_replay(srf_oplist_t list, uint64_t first_offset, uint32_t count,
                       srf_stream_t stream);
 int srf_oplist_destroy(srf_oplist_t list);
+/* All phases of a steady-state period behind ONE instantiated graph: lists[p]
+ * recorded at iteration iters[p]; edges = the union of every phase's byte-range
+ * conflicts; srf_replay_set_launch updates only the nodes whose arguments
+ * differ from the phase last launched, then launches (runtime/session.py:
+ * 606-629 replayed for periods too long to instantiate one graph each). */
+typedef struct srf_replay_set *srf_replay_set_t;
+int srf_replay_set_create(srf_oplist_t *lists, const int64_t *iters, uint32_t nphase,
+                          srf_replay_set_t *out);
+int srf_replay_set_launch(srf_replay_set_t set, uint32_t phase, uint64_t iteration,
+                          srf_stream_t stream);
+int srf_replay_set_info(srf_replay_set_t set, uint32_t *nodes, uint32_t *edges,
+                        uint32_t *classes, uint64_t *updates);
+int srf_replay_set_destroy(srf_replay_set_t set);
 
 #ifdef __cplusplus
 }

@@ -162,6 +162,10 @@ SIGNATURES = {
     "srf_oplist_diff": (C.c_int, [vp, vp, C.c_int64, C.c_char_p, C.c_uint32]),
     "srf_oplist_replay": (C.c_int, [vp, u64, C.c_uint32, vp]),
     "srf_oplist_destroy": (C.c_int, [vp]),
+    "srf_replay_set_create": (C.c_int, [P(vp), P(C.c_int64), C.c_uint32, P(vp)]),
+    "srf_replay_set_launch": (C.c_int, [vp, C.c_uint32, u64, vp]),
+    "srf_replay_set_info": (C.c_int, [vp, P(C.c_uint32), P(C.c_uint32), P(C.c_uint32), P(u64)]),
+    "srf_replay_set_destroy": (C.c_int, [vp]),
 }
 
 _lib = None

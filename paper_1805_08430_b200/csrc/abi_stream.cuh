@@ -461,6 +461,75 @@ int srf_oplist_replay(srf_oplist_t l, uint64_t first_offset, uint32_t count, srf
   return SRF_OK;
 }
 
+// One graph for all phases of a period (host_record.cuh, "Replay set").
+// lists[p] is the recording of phase p, made at iteration iters[p]; fails
+// with SRF_E_INVALID_CONFIG when the phases do not share one op sequence.
+int srf_replay_set_create(srf_oplist_t *lists, const int64_t *iters, uint32_t nphase,
+                          srf_replay_set_t *out) {
+  DeviceGuard device_guard;
+  if (nphase == 0) return fail(SRF_E_INVALID_CONFIG, "no phases");
+  const srf_oplist *l0 = lists[0];
+  for (uint32_t p = 0; p < nphase; ++p) {
+    const srf_oplist *l = lists[p];
+    if (l->dirty || l->ops.empty() || l->device != l0->device || l->ops.size() != l0->ops.size())
+      return fail(SRF_E_INVALID_CONFIG, "phases differ in device or op count");
+    for (size_t i = 0; i < l->ops.size(); ++i)
+      if (!rec_same_function(l0->ops[i], l->ops[i]))
+        return fail(SRF_E_INVALID_CONFIG, "phase %u op %zu launches another kernel", p, i);
+  }
+  CUDA_TRY(cudaSetDevice(l0->device));
+  srf_replay_set *rs = new srf_replay_set();
+  rs->device = l0->device;
+  rs->nphase = nphase;
+  rs->n = (uint32_t)l0->ops.size();
+  int rc = rec_set_build(rs, lists, iters);
+  if (rc) {
+    for (auto &v : rs->ops)
+      for (RecOp &op : v) delete op.inl;
+    delete rs;
+    return rc;
+  }
+  *out = rs;
+  return SRF_OK;
+}
+
+// replay iteration `iteration` with phase `phase`'s recording (stream order)
+int srf_replay_set_launch(srf_replay_set_t rs, uint32_t phase, uint64_t iteration,
+                          srf_stream_t st) {
+  DeviceGuard device_guard;
+  if (phase >= rs->nphase) return fail(SRF_E_INVALID_CONFIG, "phase out of range");
+  if (st->device != rs->device) return fail(SRF_E_INVALID_CONFIG, "stream on another GPU");
+  CUDA_TRY(cudaSetDevice(rs->device));
+  int rc = rec_set_launch(rs, phase, iteration, st->s);
+  if (rc) return rc;
+  g_launches.fetch_add((uint64_t)rs->n + 1, std::memory_order_relaxed);
+  return SRF_OK;
+}
+
+int srf_replay_set_info(srf_replay_set_t rs, uint32_t *nodes, uint32_t *edges,
+                        uint32_t *classes, uint64_t *updates) {
+  if (nodes) *nodes = rs->n;
+  if (edges) *edges = rs->edges;
+  if (classes) {
+    uint32_t c = 0;
+    for (size_t k = 0; k < rs->cls.size(); ++k) c += rs->cls[k] == k / rs->n ? 1 : 0;
+    *classes = c;
+  }
+  if (updates) *updates = rs->updates;
+  return SRF_OK;
+}
+
+int srf_replay_set_destroy(srf_replay_set_t rs) {
+  DeviceGuard device_guard;
+  if (!rs) return SRF_OK;
+  cudaSetDevice(rs->device);
+  cudaDeviceSynchronize();
+  for (auto &v : rs->ops)
+    for (RecOp &op : v) delete op.inl;
+  delete rs;
+  return SRF_OK;
+}
+
 int srf_oplist_destroy(srf_oplist_t l) {
   DeviceGuard device_guard;
   if (!l) return SRF_OK;

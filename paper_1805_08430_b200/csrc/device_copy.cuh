@@ -434,7 +434,7 @@ struct PutArgs {
 // (whole-sector realignment, copy_dst_aligned / copy_src_aligned); the
 // co-aligned variant keeps the lean register budget of the plain paths.
 template <int U16, bool kSectors>
-__global__ void __launch_bounds__(512) k_put(PutArgs a) {
+__device__ __forceinline__ void put_body(const PutArgs &a) {
   __shared__ int s_last, s_abort;
   const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -509,6 +509,11 @@ __global__ void __launch_bounds__(512) k_put(PutArgs a) {
   }
 }
 
+template <int U16, bool kSectors>
+__global__ void __launch_bounds__(512) k_put(const __grid_constant__ PutArgs a) {
+  put_body<U16, kSectors>(a);
+}
+
 
 // K3 with the metadata block inline (DynSender.send, protocol.py:163-201):
 // the 8D+33 bytes travel as a kernel parameter - no host-to-device staging
@@ -530,7 +535,7 @@ struct InlineArgs {
   int *err;
 };
 
-__global__ void __launch_bounds__(256) k_put_inline(const __grid_constant__ InlineArgs a) {
+__device__ __forceinline__ void put_inline_body(const InlineArgs &a) {
   __shared__ int s_abort;
   uint8_t *tail = a.dst + a.len - 1;
   if (threadIdx.x == 0) s_abort = (a.wait_empty && !credit_wait(tail, a.timeout_ns, a.err)) ? 1 : 0;
@@ -551,6 +556,10 @@ __global__ void __launch_bounds__(256) k_put_inline(const __grid_constant__ Inli
       st_release_sys_u8(a.db + a.db_len - 1, v);
     }
   }
+}
+
+__global__ void __launch_bounds__(256) k_put_inline(const __grid_constant__ InlineArgs a) {
+  put_inline_body(a);
 }
 
 // ---------------------------------------------------------------------------

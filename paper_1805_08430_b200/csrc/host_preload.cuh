@@ -33,7 +33,11 @@ static int preload_kernels(int device) {
       (const void *)k_add<int32_t>, (const void *)k_add<int64_t>, (const void *)k_add<uint8_t>,
       (const void *)k_sigmoid<float>, (const void *)k_sigmoid<double>,
       (const void *)k_pull_stream<true>, (const void *)k_pull_stream<false>,
-      (const void *)k_post_rounds};
+      (const void *)k_post_rounds, (const void *)k_put_ind<8, false>,
+      (const void *)k_put_ind<8, true>, (const void *)k_put_ind<4, false>,
+      (const void *)k_put_ind<4, true>, (const void *)k_put_inline_ind, (const void *)k_gen_ind,
+      (const void *)k_apply_ind<true>, (const void *)k_apply_ind<false>,
+      (const void *)k_set_replay};
   for (const void *k : kernels) {
     cudaFuncAttributes attr;
     cudaError_t e = cudaFuncGetAttributes(&attr, k);

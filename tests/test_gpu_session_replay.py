@@ -119,3 +119,38 @@ def test_torch_fallback_taints_the_recording():
     assert s.replayed_iterations == 0
     assert "torch" in s.replay_status, s.replay_status
     s.close()
+
+
+def test_long_period_replay_set_equals_host_path():
+    """configs[4]'s LSTM graph (14 variables, 7 workers, dynamic gradient
+    edges through one first-fit arena) repeats its device work only every
+    168 iterations.  All phases replay through ONE graph whose varying
+    arguments are read from a device table (srf_replay_set): rows, counters
+    and every variable equal the host path's, and the replayed iterations
+    cover more than one full period."""
+    shapes = [(int(35.93e6) // 14 // 4,)] * 14
+    n = 600
+
+    def run(replay):
+        g, p = build_ps_workload(0, 14, 0.0, 7, shapes=shapes)
+        s = Session(g, p, seed=0, replay=replay, devices={v: 0 for v in set(p.values())},
+                    arena_bytes=9 * 4 * sum(sh[0] for sh in shapes) + (64 << 20),
+                    capacity_bytes=10 * 4 * sum(sh[0] for sh in shapes) + (160 << 20),
+                    apply_op="sgd", lr=0.01, watchdog_sweeps=10_000)
+        rep = s.run(n)
+        vars_ = {nid: s.variable_bytes(nid) for nid, node in g.nodes.items()
+                 if node.kind is NodeKind.VARIABLE}
+        out = (rep, vars_, s.replayed_iterations, s.replay_steady, s.replay_status)
+        s.close()
+        return out
+
+    rep_r, vars_r, replayed, steady, status = run(True)
+    rep_h, vars_h, _, _, _ = run(False)
+    print(status)
+    assert steady is not None and steady[1] > 16, status
+    assert replayed > steady[1]
+    for a, b in zip(rep_r.rows, rep_h.rows):
+        for f in FIELDS:
+            assert getattr(a, f) == getattr(b, f), (a.iteration, f)
+    for nid in vars_r:
+        assert vars_r[nid] == vars_h[nid], nid

@@ -6,7 +6,7 @@ import os
 import sys
 import time
 
-os.environ.setdefault("SRFLOW_REPLAY_MAX_PERIOD", "64")
+os.environ.setdefault("SRFLOW_REPLAY_MAX_PERIOD", "256")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 from paper_1805_08430_b200.runtime.session import Session  # noqa: E402
@@ -52,8 +52,28 @@ for it in range(1, 900):
     if sess.replay_steady is not None or "given up" in sess.replay_status:
         break
 if sess.replay_steady is not None:
-    sess.run(10)
+    per = sess.replay_steady[1]
+    for k in range(3):
+        t0 = time.perf_counter()
+        sess.run(1)
+        torch.cuda.synchronize()
+        print("one replayed iteration incl. its graph build", round(time.perf_counter() - t0, 4),
+              "s", flush=True)
+    base, p_, recs = sess._steady
+    for j in list(recs)[:1] + list(recs)[-1:]:
+        buf = C.create_string_buffer(256)
+        nops = C.c_uint32()
+        _lib.call("srf_oplist_info", recs[j][0], C.byref(nops), None, buf, 256)
+        print("recording", j, "ops", nops.value, buf.value.decode(), flush=True)
+    t0 = time.perf_counter()
+    sess.run(per)
     torch.cuda.synchronize()
+    print("first pass over the period (graph builds)", round(time.perf_counter() - t0, 2), "s",
+          flush=True)
+    t0 = time.perf_counter()
+    sess.run(per)
+    torch.cuda.synchronize()
+    print("second pass", round(time.perf_counter() - t0, 3), "s", flush=True)
     t0 = time.perf_counter()
     sess.run(500)
     torch.cuda.synchronize()

@@ -577,6 +577,7 @@ struct srf_replay_set {
   std::vector<cudaGraphNode_t> node;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec[kExecs] = {};
+  cudaEvent_t done[kExecs] = {};         // after each exec's latest launch
   uint32_t next_exec = 0;
   uint64_t *iter_add = nullptr;
   unsigned int *priv = nullptr;
@@ -591,6 +592,8 @@ struct srf_replay_set {
     if (table) cudaFree((void *)table);
     for (auto &e : exec)
       if (e) cudaGraphExecDestroy(e);
+    for (auto &e : done)
+      if (e) cudaEventDestroy(e);
     if (graph) cudaGraphDestroy(graph);
     if (iter_add) cudaFree(iter_add);
     if (priv) cudaFree(priv);
@@ -678,9 +681,11 @@ static int rec_set_build(srf_replay_set *rs, srf_oplist *const *lists, const int
   size_t blob_bytes = 0;
   for (uint32_t i = 0; i < n; ++i) {
     const bool all_ind = getenv("SRFLOW_REPLAY_ALL_INDIRECT") != nullptr;  // probes
+    const char *kinds = getenv("SRFLOW_REPLAY_IND_KINDS");  // probes: bitmask of RecKind
     bool varies = all_ind;
     for (uint32_t p = 1; p < P && !varies; ++p) varies = rs->cls[(size_t)p * n + i] != 0;
     if (!varies || !rec_ind_func(rs->ops[0][i])) continue;
+    if (kinds && !((atoi(kinds) >> rs->ops[0][i].kind) & 1)) continue;
     rs->indirect[i] = 1;
     for (uint32_t p = 0; p < P; ++p)
       if (rs->cls[(size_t)p * n + i] == p) {
@@ -738,6 +743,7 @@ static int rec_set_build(srf_replay_set *rs, srf_oplist *const *lists, const int
   const auto t_inst = std::chrono::steady_clock::now();
   for (int k = 0; k < srf_replay_set::kExecs; ++k) {
     CUDA_TRY(cudaGraphInstantiate(&rs->exec[k], rs->graph, 0));
+    CUDA_TRY(cudaEventCreateWithFlags(&rs->done[k], cudaEventDisableTiming));
     if (k == 0 && getenv("SRFLOW_REPLAY_TIMING")) {
       uint32_t nind = 0;
       for (uint8_t x : rs->indirect) nind += x;
@@ -763,6 +769,11 @@ static int rec_set_launch(srf_replay_set *rs, uint32_t phase, uint64_t iteration
                                : srf_replay_set::kExecs;
   const int k = (int)(rs->next_exec++ % nexec);
   std::vector<uint32_t> &loaded = rs->loaded[k];
+  // an exec is reused only after its previous launch finished (waiting here
+  // is cheap; relaunching an exec that is still in flight stalled the host
+  // ~3 ms per launch)
+  static const bool no_wait = getenv("SRFLOW_REPLAY_NO_EXEC_WAIT") != nullptr;
+  if (!no_wait) CUDA_TRY(cudaEventSynchronize(rs->done[k]));
   for (uint32_t i = 0; i < n; ++i) {
     if (loaded[i] == c[i] || rs->indirect[i]) continue;
     void *args[8];
@@ -776,6 +787,7 @@ static int rec_set_launch(srf_replay_set *rs, uint32_t phase, uint64_t iteration
   k_set_replay<<<1, 1, 0, st>>>(rs->iter_add, iteration, rs->phase, phase);
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaGraphLaunch(rs->exec[k], st));
+  CUDA_TRY(cudaEventRecord(rs->done[k], st));
   if (timing) {
     const auto t2 = std::chrono::steady_clock::now();
     t_upd += std::chrono::duration_cast<std::chrono::microseconds>(t1 - t0).count();

@@ -69,7 +69,59 @@ def run_per_phase(label):
               flush=True)
 
 
+def device_times(label, kinds):
+    """device time per iteration (events around each graph launch, synced)"""
+    if kinds is None:
+        os.environ.pop("SRFLOW_REPLAY_IND_KINDS", None)
+    else:
+        os.environ["SRFLOW_REPLAY_IND_KINDS"] = str(kinds)
+    os.environ["SRFLOW_REPLAY_EXECS"] = "1"
+    phases = sorted(recs)
+    lists = (C.c_void_p * len(phases))(*[recs[j][0].value for j in phases])
+    iters = (C.c_int64 * len(phases))(*phases)
+    h = C.c_void_p()
+    _lib.call("srf_replay_set_create", lists, iters, len(phases), C.byref(h))
+    ev = [C.c_void_p(), C.c_void_p()]
+    for e in ev:
+        _lib.call("srf_timing_event_create", next(iter(sess.spaces.values())).handle, C.byref(e))
+    tot, host = 0.0, 0.0
+    for _ in range(period):
+        _lib.call("srf_event_record_on", ev[0], st)
+        t0 = time.perf_counter()
+        _lib.call("srf_replay_set_launch", h, phase_of(cur[0]), cur[0], st)
+        host += time.perf_counter() - t0
+        _lib.call("srf_event_record_on", ev[1], st)
+        _lib.call("srf_stream_sync", st)
+        ms = C.c_float()
+        _lib.call("srf_event_elapsed_ms", ev[0], ev[1], C.byref(ms))
+        tot += ms.value
+        cur[0] += 1
+    print(f"{label}: device {tot / period * 1e3:.0f} us/iteration, host launch "
+          f"{host / period * 1e6:.0f} us", flush=True)
+    _lib.call("srf_replay_set_destroy", h)
+
+
+def device_per_phase(label):
+    ev = [C.c_void_p(), C.c_void_p()]
+    for e in ev:
+        _lib.call("srf_timing_event_create", next(iter(sess.spaces.values())).handle, C.byref(e))
+    tot = 0.0
+    for _ in range(period):
+        j = first + phase_of(cur[0])
+        _lib.call("srf_event_record_on", ev[0], st)
+        _lib.call("srf_oplist_replay", recs[j][0], cur[0] - j, 1, st)
+        _lib.call("srf_event_record_on", ev[1], st)
+        _lib.call("srf_stream_sync", st)
+        ms = C.c_float()
+        _lib.call("srf_event_elapsed_ms", ev[0], ev[1], C.byref(ms))
+        tot += ms.value
+        cur[0] += 1
+    print(f"{label}: device {tot / period * 1e3:.0f} us/iteration", flush=True)
+
+
 run_set("set, 4 execs", 4)
 run_set("set, 1 exec", 1)
+os.environ["SRFLOW_REPLAY_EXECS"] = "4"
+device_times("set, synced per launch", None)
 run_per_phase("per-phase graphs")
-run_set("set, 4 execs (again)", 4)
+device_per_phase("per-phase graphs (events)")

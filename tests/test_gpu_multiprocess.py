@@ -54,3 +54,12 @@ def test_two_process_sendrecv_endpoints(pools):
     """Static and dynamic Send/Recv between processes through the reference
     endpoints (StaticSender/Receiver, DynSender/Receiver)."""
     _run("mp_sendrecv_worker.py", pools)
+
+
+@pytest.mark.parametrize("pools", ["ipc", "vmm"])
+def test_two_process_pipelined_and_pulled_edges(pools):
+    """One edge between processes (configs[1]'s one-way layout): the push
+    edge storing into the peer's mapped slots and the pull edge reading the
+    peer's mapped payloads; every round's consumer checksum equals the
+    sender's payload."""
+    _run("mp_edge_worker.py", pools)

@@ -1452,12 +1452,24 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         ps.use_schedule("phases")
         pers(1)
         times["persistent"] = sample(pers)
+    if ps.batches["push"] is not None:
+        # labelled extension: the phase schedule with the next iteration's
+        # weight push fused into the apply (one read of every variable saved)
+        ps.use_schedule("phases")
+        ps.fuse_push = True
+        eager(2)
+        times["phases_fused_push"] = sample(eager)
+        ps.fuse_push = False
+        eager(1)      # consumes the forwarded weights, pushes nothing
     best = min(times, key=times.get)
     persistent = best == "persistent"
     multi_launch = best == "exchange_multi"
-    ps.use_schedule("phases" if best in ("persistent", "exchange_multi") else best)
+    fused = best == "phases_fused_push"
+    ps.use_schedule("phases" if best in ("persistent", "exchange_multi", "phases_fused_push")
+                    else best)
     if multi_launch:
         ps.use_schedule("exchange")
+    ps.fuse_push = fused
     # latency-bound configs: enough iterations for a timed region of ~0.3 s
     per_iter_s = times[best] / 5 / 1e3
     steps = int(max(steps, min(20000, 0.3 / max(per_iter_s, 1e-7))))
@@ -1534,8 +1546,14 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         g["link_out"] += x["link_out"]
         g["link_in"] += x["link_in"]
         g["hbm"] += x["hbm"]
+    # the fused push writes each remote worker's weights from the apply's
+    # registers: the push's read of the variable (S per weight edge) is gone
+    saved = 0
+    if fused:
+        saved = sum(L.nbytes(v) for v in range(len(shapes)) for w in range(L.workers)
+                    if w != L.shard_of(v))
     if world == 1:
-        alg = sum(2 * x["push_out"] + x["pull_in"] + x["hbm"] for x in tr)
+        alg = sum(2 * x["push_out"] + x["pull_in"] + x["hbm"] for x in tr) - saved
         peak, _src = measured_peaks()
         ach = alg * steps / t / 1e9
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
@@ -1582,7 +1600,11 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
                         if multi_launch else
                         "exchange: one k_ps_exchange launch per step (dependency-ordered "
                         "unit queue, meta fused into GenGrad)" if ps.schedule == "exchange"
+                        else "EXTENSION: one stream, one launch per phase, the next "
+                             "iteration's weight push fused into the apply (the variable "
+                             "is not re-read; algorithmic bytes exclude that read)" if fused
                         else "one stream, one launch per phase"),
+           "fused_push": fused,
            "autotune_ms_per_5": {k: round(v, 3) for k, v in times.items()}}
     ps.close()
     if cpu and rank == 0 and world == 1:

@@ -336,6 +336,17 @@ int srf_batch_apply_set_ready(srf_batch_t apply, srf_space_t space, const uint64
  * ready_addr[i] of space[i] (same GPU) reads 1 - its gen released the
  * gradient - and clears it to 0 once the body is copied, the gen's credit.
  * UINT64_MAX = none. */
+/* Fused weight push (extension, ps.PsStep(fuse_push=True)): apply batch
+ * descriptor v also writes its updated variable into nfwd[v] workers' static
+ * receive regions (fwd_*: space / payload address / token, flag after the
+ * payload) and releases their flags with the byte at tail_addr - the next
+ * iteration's StaticSender.send of the weights (runtime/protocol.py:63-91)
+ * folded into this iteration's ApplyGrad (graph.py:392-405).  Active only in
+ * srf_batch_launch calls with mode bit 0 set. */
+int srf_batch_apply_set_forward(srf_batch_t apply, const int *nfwd,
+                                srf_space_t const *fwd_space, const uint64_t *fwd_addr,
+                                const uint64_t *fwd_token, srf_space_t tail_space,
+                                uint64_t tail_addr);
 int srf_batch_put_set_src_ready(srf_batch_t put, srf_space_t const *space,
                                 const uint64_t *ready_addr);
 /* partitioned variables (extension): gen edge i produces elements

@@ -126,6 +126,7 @@ SIGNATURES = {
     "srf_batch_gen_set_offsets": (C.c_int, [vp, P(u64)]),
     "srf_batch_gen_set_ready": (C.c_int, [vp, P(vp), P(u64)]),
     "srf_batch_apply_set_ready": (C.c_int, [vp, vp, P(u64)]),
+    "srf_batch_apply_set_forward": (C.c_int, [vp, P(C.c_int), P(vp), P(u64), P(u64), vp, u64]),
     "srf_batch_put_set_src_ready": (C.c_int, [vp, P(vp), P(u64)]),
     "srf_ps_exchange_create": (C.c_int, [vp, P(u64), vp, P(u64), P(vp), C.c_int, P(u64),
                                          P(vp)]),

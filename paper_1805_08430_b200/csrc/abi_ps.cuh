@@ -233,7 +233,8 @@ int srf_batch_launch(srf_batch_t b, srf_stream_t st, uint64_t iteration, int mod
       return launch_check("k_gen_batch");
     default:
       k_apply_batch<<<grid, 256, 0, st->s>>>((const BatchApply *)b->descs, b->n, units,
-                                             b->counters, b->op, b->lr, timeout, b->err, b->sys);
+                                             b->counters, b->op, b->lr, timeout, b->err, b->sys,
+                                             mode & 1);
       return launch_check("k_apply_batch");
   }
 }
@@ -328,6 +329,44 @@ int srf_batch_gen_set_ready(srf_batch_t gen, srf_space_t const *space,
   }
   CUDA_TRY(cudaSetDevice(gen->device));
   CUDA_TRY(cudaMemcpy(gen->descs, gen->host.data(), gen->host.size(), cudaMemcpyHostToDevice));
+  return SRF_OK;
+}
+
+// Fused weight push (PsStep(fuse_push=True)): descriptor v of the apply
+// batch also stores its updated variable into nfwd[v] workers' static
+// receive regions (space fwd_space[k], payload at fwd_addr[k], flag right
+// after it, token fwd_token[k]) and releases their flags with the byte at
+// tail_addr of the batch's space.  Only launches with mode bit 0 set forward.
+int srf_batch_apply_set_forward(srf_batch_t apply, const int *nfwd,
+                                srf_space_t const *fwd_space, const uint64_t *fwd_addr,
+                                const uint64_t *fwd_token, srf_space_t tail_space,
+                                uint64_t tail_addr) {
+  DeviceGuard device_guard;
+  if (!apply || apply->kind != 2) return fail(SRF_E_INVALID_CONFIG, "not an apply batch");
+  int rc = check_raw(tail_space, tail_addr, 1, "forward flag value");
+  if (rc) return rc;
+  BatchApply *d = (BatchApply *)apply->host.data();
+  int k = 0, sys = apply->sys;
+  for (int v = 0; v < apply->n; ++v) {
+    if (nfwd[v] < 0 || nfwd[v] > SRF_MAX_WORKERS)
+      return fail(SRF_E_INVALID_CONFIG, "nfwd %d", nfwd[v]);
+    d[v].nfwd = nfwd[v];
+    d[v].fwd_tail = tail_space->base + tail_addr;
+    for (int f = 0; f < nfwd[v]; ++f, ++k) {
+      srf_space *fs = fwd_space[k];
+      {
+        std::lock_guard<std::mutex> g(fs->mu);
+        rc = check_remote_locked(fs, fwd_addr[k], d[v].n + 1, fwd_token[k]);
+        if (rc) return rc;
+      }
+      d[v].fwd[f] = fs->base + fwd_addr[k];
+      sys |= (fs->imported || fs->device != apply->device) ? 1 : 0;
+    }
+  }
+  apply->sys = sys;
+  CUDA_TRY(cudaSetDevice(apply->device));
+  CUDA_TRY(cudaMemcpy(apply->descs, apply->host.data(), apply->host.size(),
+                      cudaMemcpyHostToDevice));
   return SRF_OK;
 }
 

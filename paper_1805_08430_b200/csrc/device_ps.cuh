@@ -48,10 +48,13 @@ struct SgdOp {
 
 // 16-B vectors [0, nv) at byte offset off, U vectors in flight per thread,
 // workers folded in ascending order.
+// fwd / nfwd: copies of the updated variable to write besides var (the fused
+// push of the next iteration's weights, apply_unit; nfwd = 0 elsewhere)
 template <class Op, int U>
 __device__ __forceinline__ void fold_v4(uint8_t *varb, const uint8_t *const *g, int nw,
                                         uint64_t off, uint64_t nv, uint64_t t, uint64_t nth,
-                                        float lr) {
+                                        float lr, uint8_t *const *fwd = nullptr,
+                                        int nfwd = 0) {
   uint4 *var = (uint4 *)(varb + off);
   uint64_t i = t;
   for (; i + (uint64_t)(U - 1) * nth < nv; i += (uint64_t)U * nth) {
@@ -68,23 +71,31 @@ __device__ __forceinline__ void fold_v4(uint8_t *varb, const uint8_t *const *g, 
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) var[i + u * nth] = acc[u];
+    for (int f = 0; f < nfwd; ++f) {
+      uint4 *fw = (uint4 *)(fwd[f] + off);
+#pragma unroll
+      for (int u = 0; u < U; ++u) fw[i + u * nth] = acc[u];
+    }
   }
   for (; i < nv; i += nth) {
     uint4 acc = var[i];
     for (int w = 0; w < nw; ++w) acc = Op::fold(acc, ld_v4((const uint4 *)(g[w] + off) + i), lr);
     var[i] = acc;
+    for (int f = 0; f < nfwd; ++f) ((uint4 *)(fwd[f] + off))[i] = acc;
   }
 }
 
 template <class Op>
 __device__ __forceinline__ void fold_v2(uint8_t *varb, const uint8_t *const *g, int nw,
                                         uint64_t off, uint64_t nv, uint64_t t, uint64_t nth,
-                                        float lr) {
+                                        float lr, uint8_t *const *fwd = nullptr,
+                                        int nfwd = 0) {
   uint2 *var = (uint2 *)(varb + off);
   for (uint64_t i = t; i < nv; i += nth) {
     uint2 acc = var[i];
     for (int w = 0; w < nw; ++w) acc = Op::fold2(acc, ((const uint2 *)(g[w] + off))[i], lr);
     var[i] = acc;
+    for (int f = 0; f < nfwd; ++f) ((uint2 *)(fwd[f] + off))[i] = acc;
   }
 }
 
@@ -94,11 +105,17 @@ __device__ __forceinline__ void fold_v2(uint8_t *varb, const uint8_t *const *g, 
 // SGD works on fp32: same vector classes in whole floats.
 template <bool SGD>
 __device__ void apply_range(uint8_t *var, const uint8_t *const *g, int nw, uint64_t n,
-                            float lr, uint64_t t, uint64_t nth) {
+                            float lr, uint64_t t, uint64_t nth, uint8_t *const *fwd = nullptr,
+                            int nfwd = 0) {
   const uintptr_t m = (uintptr_t)var;
   bool same16 = true, same8 = true;
   for (int w = 0; w < nw; ++w) {
     const uintptr_t p = (uintptr_t)g[w];
+    same16 &= ((p ^ m) & 15) == 0;
+    same8 &= ((p ^ m) & 7) == 0;
+  }
+  for (int f = 0; f < nfwd; ++f) {
+    const uintptr_t p = (uintptr_t)fwd[f];
     same16 &= ((p ^ m) & 15) == 0;
     same8 &= ((p ^ m) & 7) == 0;
   }
@@ -108,15 +125,15 @@ __device__ void apply_range(uint8_t *var, const uint8_t *const *g, int nw, uint6
     head = ((16 - (m & 15)) & 15);
     if (head > n) head = n;
     const uint64_t nv = (n - head) / 16;
-    if (SGD) fold_v4<SgdOp, 4>(var, g, nw, head, nv, t, nth, lr);
-    else fold_v4<XorOp, 4>(var, g, nw, head, nv, t, nth, lr);
+    if (SGD) fold_v4<SgdOp, 4>(var, g, nw, head, nv, t, nth, lr, fwd, nfwd);
+    else fold_v4<XorOp, 4>(var, g, nw, head, nv, t, nth, lr, fwd, nfwd);
     body = nv * 16;
   } else if (same8) {
     head = ((8 - (m & 7)) & 7);
     if (head > n) head = n;
     const uint64_t nv = (n - head) / 8;
-    if (SGD) fold_v2<SgdOp>(var, g, nw, head, nv, t, nth, lr);
-    else fold_v2<XorOp>(var, g, nw, head, nv, t, nth, lr);
+    if (SGD) fold_v2<SgdOp>(var, g, nw, head, nv, t, nth, lr, fwd, nfwd);
+    else fold_v2<XorOp>(var, g, nw, head, nv, t, nth, lr, fwd, nfwd);
     body = nv * 8;
   }
   // scalar elements outside the vector body: [0, head) and [head + body, n)
@@ -127,10 +144,12 @@ __device__ void apply_range(uint8_t *var, const uint8_t *const *g, int nw, uint6
       float v = *(float *)(var + e);
       for (int w = 0; w < nw; ++w) v = sgd1(v, lr, *(const float *)(g[w] + e));
       *(float *)(var + e) = v;
+      for (int f = 0; f < nfwd; ++f) *(float *)(fwd[f] + e) = v;
     } else {
       uint8_t acc = var[e];
       for (int w = 0; w < nw; ++w) acc ^= g[w][e];
       var[e] = acc;
+      for (int f = 0; f < nfwd; ++f) fwd[f][e] = acc;
     }
   }
 }
@@ -195,6 +214,16 @@ struct BatchApply {      // shard: fused dynamic receive (meta decode + peer
   int nw, rank;
   uint32_t cta_begin, cta_count;
   const uint8_t *ready[SRF_MAX_WORKERS];  // in-place gradient w complete (nullptr: none)
+  // fused push of the NEXT iteration's weights (PsStep(fuse_push=True)): the
+  // updated variable is also stored into these workers' static receive
+  // regions (payload || flag), and the last arriver releases their flags
+  // with the value at fwd_tail - the StaticSender.send of the weights the
+  // next iteration would otherwise issue as a separate K1 (one read of the
+  // variable saved).  The credit is implied: every worker's gen cleared its
+  // flag before producing the gradient this apply consumed.
+  uint8_t *fwd[SRF_MAX_WORKERS];
+  const uint8_t *fwd_tail;
+  int nfwd, pad_fwd;
 };
 
 template <typename D>
@@ -373,12 +402,17 @@ __device__ __forceinline__ void gen_batch_units(const BatchGen *descs, int n,
     gen_unit(descs, n, u, counters, seed, iteration, regen, 0, timeout_ns, err, sys);
 }
 
+// fwd: also store the updated variable into the descriptor's forward
+// destinations (the fused next-iteration weight push; only the batch launch
+// of a PsStep(fuse_push=True) sets it)
 __device__ __forceinline__ void apply_unit(const BatchApply *descs, int n, uint32_t u,
                                            unsigned int *counters, int op, float lr,
                                            uint64_t timeout_ns, int *err, int sys,
-                                           unsigned int *done = nullptr, uint32_t k = 0) {
+                                           unsigned int *done = nullptr, uint32_t k = 0,
+                                           int fwd = 0) {
   __shared__ int s_desc, s_last, s_bad;
   __shared__ const uint8_t *s_g[SRF_MAX_WORKERS];
+  __shared__ uint8_t *s_fwd[SRF_MAX_WORKERS];
   {
     if (threadIdx.x == 0) {
       s_desc = find_desc(descs, n, u);
@@ -421,14 +455,16 @@ __device__ __forceinline__ void apply_unit(const BatchApply *descs, int n, uint3
         s_g[w] = d.peer_base[w] + addr;  // one-sided read through the peer mapping
       }
     }
+    const int nfwd = fwd ? d.nfwd : 0;
+    if (threadIdx.x < (unsigned)nfwd) s_fwd[threadIdx.x] = d.fwd[threadIdx.x];
     __syncthreads();
     if (!s_bad) {
       const uint64_t t = (uint64_t)lb * blockDim.x + threadIdx.x;
       const uint64_t nth = (uint64_t)d.cta_count * blockDim.x;
       if (op == SRF_APPLY_XOR)
-        apply_range<false>(d.var, s_g, d.nw, d.n, lr, t, nth);
+        apply_range<false>(d.var, s_g, d.nw, d.n, lr, t, nth, s_fwd, nfwd);
       else
-        apply_range<true>(d.var, s_g, d.nw, d.n, lr, t, nth);
+        apply_range<true>(d.var, s_g, d.nw, d.n, lr, t, nth, s_fwd, nfwd);
     }
     __syncthreads();
     if (threadIdx.x == 0) s_last = grid_arrive(&counters[s_desc], d.cta_count - 1, sys);
@@ -443,6 +479,10 @@ __device__ __forceinline__ void apply_unit(const BatchApply *descs, int n, uint3
       release_tail((uint8_t *)d.src[threadIdx.x] + 8 * r + 32, 0, sys);
     if (s_last && threadIdx.x < (unsigned)d.nw && d.ready[threadIdx.x])
       release_tail((uint8_t *)d.ready[threadIdx.x], 0, sys);
+    // the fused weight push: flags last, after every CTA's stores (the grid
+    // arrival above is cumulative at the batch's scope)
+    if (s_last && threadIdx.x < (unsigned)nfwd && !s_bad)
+      release_tail(s_fwd[threadIdx.x] + d.n, *d.fwd_tail, sys);
     if (s_last && threadIdx.x == 0) {
       // one more update of this variable completed (multi-iteration exchange)
       if (done) count_done(done + s_desc);
@@ -454,9 +494,9 @@ __device__ __forceinline__ void apply_unit(const BatchApply *descs, int n, uint3
 __device__ __forceinline__ void apply_batch_units(const BatchApply *descs, int n,
                                                   uint32_t total_units, unsigned int *counters,
                                                   int op, float lr, uint64_t timeout_ns,
-                                                  int *err, int sys) {
+                                                  int *err, int sys, int fwd = 0) {
   for (uint32_t u = blockIdx.x; u < total_units; u += gridDim.x)
-    apply_unit(descs, n, u, counters, op, lr, timeout_ns, err, sys);
+    apply_unit(descs, n, u, counters, op, lr, timeout_ns, err, sys, nullptr, 0, fwd);
 }
 
 
@@ -478,8 +518,8 @@ __global__ void __launch_bounds__(512) k_gen_batch(const BatchGen *descs, int n,
 __global__ void __launch_bounds__(256) k_apply_batch(const BatchApply *descs, int n,
                                                      uint32_t total_units, unsigned int *counters,
                                                      int op, float lr, uint64_t timeout_ns,
-                                                     int *err, int sys) {
-  apply_batch_units(descs, n, total_units, counters, op, lr, timeout_ns, err, sys);
+                                                     int *err, int sys, int fwd) {
+  apply_batch_units(descs, n, total_units, counters, op, lr, timeout_ns, err, sys, fwd);
 }
 
 // Device-side DynReceiver (runtime/protocol.py:224-254) for device-resident

@@ -268,7 +268,8 @@ class PsStep:
     def __init__(self, layout: PsLayout, *, rank: int = 0, world: int = 1, device: int = 0,
                  seed: int = 0, op: str = "xor", lr: float = 0.01,
                  schedule: str = "phases",
-                 exchange_lag: Optional[int] = None, exchange_order: Optional[str] = None):
+                 exchange_lag: Optional[int] = None, exchange_order: Optional[str] = None,
+                 fuse_push: bool = False):
         self.L = layout
         self.rank, self.world, self.device = rank, world, device
         self.seed = seed
@@ -328,6 +329,15 @@ class PsStep:
             (os.environ.get("SRFLOW_PS_EXCHANGE_ORDER", "size") if exchange_order is None
              else exchange_order))
         self.schedule = "phases"
+        #: EXTENSION (fused weight push, phase schedule): the apply of
+        #: iteration k also stores the updated variable into every remote
+        #: worker's weight receive region and releases its flag - the weight
+        #: Send of iteration k+1 without re-reading the variable.  Toggle
+        #: between steps; while a forwarded push is outstanding the next
+        #: step skips its push batch.
+        self.fuse_push = bool(fuse_push)
+        self._pushed_ahead = False
+        self._set_forward()
         self.use_schedule(schedule)
 
     # -- layout helpers -------------------------------------------------------------
@@ -489,6 +499,32 @@ class PsStep:
             out["apply"][s] = self._make_apply(s, [(v, list(range(L.workers))) for v in vs])
         return out
 
+    def _set_forward(self) -> None:
+        """Forward destinations of every apply descriptor: the weight receive
+        regions the variable's push rows write (same workers, same order)."""
+        L = self.L
+        for s, a in self.batches["apply"].items():
+            nfwd, sp, ad, tok = [], [], [], []
+            for v in self._rows["apply"][s]:
+                ws = [w for w in range(L.workers) if w != s and L.shard_of(v) == s]
+                nfwd.append(len(ws))
+                for w in ws:
+                    sp.append(self.space(w).handle.value)
+                    ad.append(self.addr(w, ("wbuf", v)))
+                    tok.append(self.token(w))
+            if not any(nfwd):
+                continue
+            n = len(nfwd)
+            _lib.call("srf_batch_apply_set_forward", a, (C.c_int * n)(*nfwd),
+                      (C.c_void_p * len(sp))(*sp), _lib.u64_array(ad), _lib.u64_array(tok),
+                      self.spaces[s].handle, self.addr(s, "flag"))
+
+    def _check_unfused(self, what: str) -> None:
+        if self._pushed_ahead:
+            raise errors.InvalidConfig(
+                f"{what}: a fused weight push is outstanding; run one step with "
+                f"fuse_push=False first")
+
     def _make_apply(self, s: int, groups) -> C.c_void_p:
         """One apply batch on shard s: a descriptor per (variable, workers)
         group, the workers' gradients applied in the listed (ascending) order."""
@@ -567,6 +603,7 @@ class PsStep:
         if schedule not in ("phases", "exchange"):
             raise errors.InvalidConfig(f"unknown PS schedule {schedule!r}")
         if schedule == "exchange":
+            self._check_unfused("the exchange schedule")
             b = self.batches
             if self._exchange_built is None and (b["push"] is not None or b["gen"]
                                                  or b["apply"]):
@@ -642,9 +679,11 @@ class PsStep:
         b, n = self.batches, 0
         mode = 1 if regen else 0
         if self._exchange is not None:
+            if self.fuse_push:
+                raise errors.InvalidConfig("the fused weight push runs in the phase schedule")
             _lib.call("srf_ps_exchange_launch", self._exchange, self.stream, iteration, mode)
             return 1
-        if b["push"] is not None:
+        if b["push"] is not None and not self._pushed_ahead:
             _lib.call("srf_batch_launch", b["push"], self.stream, iteration, 0, 0)
             n += 1
         for g in b["gen"].values():
@@ -654,9 +693,11 @@ class PsStep:
             if m is not None:
                 _lib.call("srf_batch_launch", m, self.stream, iteration, 0, 0)
                 n += 1
+        fwd = 1 if self.fuse_push else 0
         for a in b["apply"].values():
-            _lib.call("srf_batch_launch", a, self.stream, iteration, 0, 0)
+            _lib.call("srf_batch_launch", a, self.stream, iteration, fwd, 0)
             n += 1
+        self._pushed_ahead = self.fuse_push and b["push"] is not None
         return n
 
     def launches_per_step(self) -> int:
@@ -674,10 +715,18 @@ class PsStep:
             raise errors.InvalidConfig("graph capture uses the one-stream phase schedule")
         none = (1 << 64) - 1
         graph = C.c_void_p()
-        _lib.call("srf_graph_begin", self.stream)
         b = self.batches
+        fwd = 1 if self.fuse_push else 0
+        if fwd and b["push"] is not None and not self._pushed_ahead:
+            # the fused push's prologue runs before the graph: every captured
+            # step then finds its weights already forwarded
+            _lib.call("srf_batch_launch", b["push"], self.stream, none, 0, 0)
+            self._pushed_ahead = True
+        elif not fwd:
+            self._check_unfused("an unfused capture")
+        _lib.call("srf_graph_begin", self.stream)
         for _ in range(steps):
-            if b["push"] is not None:
+            if b["push"] is not None and not fwd:
                 _lib.call("srf_batch_launch", b["push"], self.stream, none, 0, 0)
             for g in b["gen"].values():
                 _lib.call("srf_batch_launch", g, self.stream, none, 1 if regen else 0, 0)
@@ -685,7 +734,7 @@ class PsStep:
                 if m is not None:
                     _lib.call("srf_batch_launch", m, self.stream, none, 0, 0)
             for a in b["apply"].values():
-                _lib.call("srf_batch_launch", a, self.stream, none, 0, 0)
+                _lib.call("srf_batch_launch", a, self.stream, none, fwd, 0)
             _lib.call("srf_counter_add", self.stream_space.handle, self._counter.base_addr, 1,
                       self.stream)
         _lib.call("srf_graph_end", self.stream, C.byref(graph))
@@ -697,6 +746,8 @@ class PsStep:
         ``per_launch`` iterations each (the unit queue repeats inside one
         launch; a push of iteration k waits for its variable's apply of
         iteration k-1).  Returns the number of launches."""
+        if self.fuse_push:
+            raise errors.InvalidConfig("the fused weight push runs in the phase schedule")
         self.use_schedule("exchange")
         n, it = 0, first_iteration
         while iterations > 0:
@@ -715,6 +766,9 @@ class PsStep:
         barriers instead of kernel boundaries."""
         if self.world != 1:
             raise errors.InvalidConfig("the persistent PS step runs on one GPU")
+        if self.fuse_push:
+            raise errors.InvalidConfig("the fused weight push runs in the phase schedule")
+        self._check_unfused("the persistent schedule")
         b = self.batches
         applies = list(b["apply"].values())
         gen = next(iter(b["gen"].values()), None)

@@ -368,3 +368,63 @@ def test_push_lane_exchange_matches_oracle(monkeypatch, lane, grad):
     for v in range(len(shapes)):
         assert got[v].tobytes() == want[v].reshape(-1).tobytes(), (v, lane, grad)
     ps.close()
+
+
+@pytest.mark.parametrize("shapes,W,P,coloc", CASES)
+@pytest.mark.parametrize("op", ["xor", "sgd"])
+def test_fused_weight_push_matches_oracle(shapes, W, P, coloc, op):
+    """PsStep(fuse_push=True): the apply of iteration k also writes the
+    updated variable into every remote worker's weight receive region (the
+    next iteration's weight push).  Back-to-back steps, toggling the fusion
+    off and on between steps, equal the golden-pinned oracle; the forwarded
+    weights equal the variable, flag set."""
+    L = PsLayout(shapes, W, P, coloc)
+    ps = PsStep(L, seed=21, op=op, lr=0.03, fuse_push=True)
+    it = 0
+    for fused in (True, True, False, True, True, True, False, False, True):
+        ps.fuse_push = fused
+        it += 1
+        ps.step(it)
+    ps.sync()
+    want = port.ps_expected(shapes, W, 21, it, op=op, lr=0.03)
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes(), (v, op)
+    # the last step forwarded: every remote worker holds the current weights
+    for v in range(len(shapes)):
+        s = L.shard_of(v)
+        for w in range(W):
+            if w == s:
+                continue
+            raw = ps.space(w).read_raw(ps.addr(w, ("wbuf", v)), L.nbytes(v) + 1)
+            assert raw[:-1] == want[v].tobytes() and raw[-1] == 1, (v, w)
+    with pytest.raises(errors.InvalidConfig):
+        ps.use_schedule("exchange")    # a forwarded push is outstanding
+    ps.fuse_push = False
+    it += 1
+    ps.step(it)                         # consumes it, pushes nothing
+    ps.use_schedule("exchange")
+    it += 1
+    ps.step(it)
+    ps.sync()
+    want = port.ps_expected(shapes, W, 21, it, op=op, lr=0.03)
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes(), (v, op, "after the switch")
+    ps.close()
+
+
+def test_fused_weight_push_graph_replay():
+    shapes = [(5000,), (33,), (16, 16)]
+    L = PsLayout(shapes, 2, 1)
+    ps = PsStep(L, seed=4, op="sgd", lr=0.02, fuse_push=True)
+    ps.step(1)
+    ps.sync()
+    ps.set_iteration(2)
+    graph = ps.capture(5)
+    ps.replay(graph)
+    ps.replay(graph)          # iterations 2..11 (the counter advances per step)
+    ps.sync()
+    _lib.call("srf_graph_destroy", graph)
+    want = port.ps_expected(shapes, 2, 4, 11, op="sgd", lr=0.02)
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes(), v
+    ps.close()

@@ -1452,23 +1452,25 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         ps.use_schedule("phases")
         pers(1)
         times["persistent"] = sample(pers)
-    if ps.batches["push"] is not None:
-        # labelled extension: the phase schedule with the next iteration's
-        # weight push fused into the apply (one read of every variable saved)
-        ps.use_schedule("phases")
+    if ps.batches["push"] is not None or world > 1:
+        # labelled extension: the next iteration's weight push fused into the
+        # apply (one read of every pushed variable saved), in each schedule
         ps.fuse_push = True
-        eager(2)
-        times["phases_fused_push"] = sample(eager)
+        for name in ("phases", "exchange"):
+            ps.use_schedule(name)
+            eager(2)
+            times[name + "_fused_push"] = sample(eager)
+        multi(2)
+        times["exchange_multi_fused_push"] = sample(multi)
         ps.fuse_push = False
+        ps.use_schedule("phases")
         eager(1)      # consumes the forwarded weights, pushes nothing
     best = min(times, key=times.get)
-    persistent = best == "persistent"
-    multi_launch = best == "exchange_multi"
-    fused = best == "phases_fused_push"
-    ps.use_schedule("phases" if best in ("persistent", "exchange_multi", "phases_fused_push")
-                    else best)
-    if multi_launch:
-        ps.use_schedule("exchange")
+    fused = best.endswith("_fused_push")
+    base = best[:-len("_fused_push")] if fused else best
+    persistent = base == "persistent"
+    multi_launch = base == "exchange_multi"
+    ps.use_schedule("exchange" if base in ("exchange", "exchange_multi") else "phases")
     ps.fuse_push = fused
     # latency-bound configs: enough iterations for a timed region of ~0.3 s
     per_iter_s = times[best] / 5 / 1e3
@@ -1600,10 +1602,10 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
                         if multi_launch else
                         "exchange: one k_ps_exchange launch per step (dependency-ordered "
                         "unit queue, meta fused into GenGrad)" if ps.schedule == "exchange"
-                        else "EXTENSION: one stream, one launch per phase, the next "
-                             "iteration's weight push fused into the apply (the variable "
-                             "is not re-read; algorithmic bytes exclude that read)" if fused
-                        else "one stream, one launch per phase"),
+                        else "one stream, one launch per phase")
+                       + ("; EXTENSION: the next iteration's weight push fused into the "
+                          "apply (the variable is not re-read; algorithmic bytes exclude "
+                          "that read)" if fused else ""),
            "fused_push": fused,
            "autotune_ms_per_5": {k: round(v, 3) for k, v in times.items()}}
     ps.close()

@@ -363,6 +363,9 @@ int srf_ps_exchange_launch(srf_exchange_t exchange, srf_stream_t stream, uint64_
  * batches in creation order, -1: none) completed for the previous one
  * (srf_ps_exchange_link must have been called). */
 int srf_ps_exchange_link(srf_exchange_t exchange, const int *push_apply_index);
+/* regen bit 0: GenGrad regenerates; bit 1: the apply units also write the
+ * next weights (srf_batch_apply_set_forward; the exchange then carries no
+ * weight pushes - build it without them). */
 int srf_ps_exchange_launch_n(srf_exchange_t exchange, srf_stream_t stream, uint64_t iteration,
                              uint32_t iterations, int regen);
 int srf_ps_exchange_destroy(srf_exchange_t exchange);

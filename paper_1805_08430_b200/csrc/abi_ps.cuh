@@ -630,7 +630,8 @@ int srf_ps_exchange_launch_n(srf_exchange_t x, srf_stream_t st, uint64_t iterati
   if ((uint64_t)x->args.nitems * iterations > 0xFFFFFFFFull)
     return fail(SRF_E_INVALID_CONFIG, "exchange: too many units for one launch");
   x->args.iteration = iteration;
-  x->args.regen = regen;
+  x->args.regen = regen & 1;
+  x->args.fwd = (regen >> 1) & 1;  // mode bit 1: the fused weight push
   x->args.iters = iterations;
   CUDA_TRY(cudaSetDevice(x->device));
   if (iterations > 1)

@@ -646,6 +646,7 @@ struct ExArgs {
   int op; float lr;
   const ExItem *items; uint32_t nitems; unsigned int *claim; unsigned int *exit_count;
   uint64_t iteration; int regen; uint64_t timeout_ns; int *err;
+  int fwd;  // applies also write the next weights (PsStep(fuse_push=True))
   // several iterations per launch: the queue repeats `iters` times (iteration
   // k's units after iteration k-1's); done[] counts completed applies per
   // apply descriptor in this launch, push_done[i] maps push edge i to its
@@ -687,7 +688,8 @@ __global__ void __launch_bounds__(512, kMinBlocks) k_ps_exchange(const __grid_co
                a.timeout_ns, a.err, a.gen_sys, k, a.seq_gen);
     else
       apply_unit(a.apply[x.batch], a.napply[x.batch], x.unit, a.capply[x.batch], a.op, a.lr,
-                 a.timeout_ns, a.err, a.apply_sys[x.batch], a.done + a.apply_base[x.batch], k);
+                 a.timeout_ns, a.err, a.apply_sys[x.batch], a.done + a.apply_base[x.batch], k,
+                 a.fwd);
   }
   // the last CTA out re-arms the queue for the next launch
   if (threadIdx.x == 0 && atomicAdd(a.exit_count, 1u) == gridDim.x - 1) {

@@ -323,6 +323,8 @@ class PsStep:
                       self._counter.base_addr)
         self._exchange = None
         self._exchange_built = None
+        self._exchange_nopush = None
+        self._exchange_gpush = None
         self._exchange_cfg = (
             int(os.environ.get("SRFLOW_PS_EXCHANGE_LAG", 3) if exchange_lag is None
                 else exchange_lag),
@@ -603,7 +605,6 @@ class PsStep:
         if schedule not in ("phases", "exchange"):
             raise errors.InvalidConfig(f"unknown PS schedule {schedule!r}")
         if schedule == "exchange":
-            self._check_unfused("the exchange schedule")
             b = self.batches
             if self._exchange_built is None and (b["push"] is not None or b["gen"]
                                                  or b["apply"]):
@@ -614,7 +615,22 @@ class PsStep:
             self._exchange = None
         self.schedule = schedule
 
-    def _build_exchange(self, lag: int, order: str):
+    def _exchange_for_launch(self) -> tuple:
+        """(exchange object, mode bits) for the next exchange launch, and
+        whether this rank must first push (the fused schedule's prologue).
+        With weights already forwarded (a fused step before) or fusion on,
+        the exchange without weight pushes runs; the applies forward iff
+        fusion is on."""
+        if self._exchange is None:
+            return None, 0, False
+        if not (self.fuse_push or self._pushed_ahead) or self.batches["push"] is None:
+            return self._exchange, 0, False
+        if self._exchange_nopush is None:
+            self._exchange_nopush = self._build_exchange(*self._exchange_cfg, nopush=True)
+        return (self._exchange_nopush, 2 if self.fuse_push else 0,
+                self.fuse_push and not self._pushed_ahead)
+
+    def _build_exchange(self, lag: int, order: str, nopush: bool = False):
         """One queue of this GPU's units (k_ps_exchange).  Keys are a global
         order every rank derives alike: push(v) < gen(v) < apply(v), the
         apply of a variable placed ``lag`` variables later so the next
@@ -639,8 +655,16 @@ class PsStep:
         applies = list(b["apply"].items())
         push, push_vars = b["push"], list(rows["push"])
         push_keys = [4 * pos[v] for v in rows["push"]]
+        if nopush:    # fused weight push: the applies write the weights
+            push, push_vars, push_keys = None, [], []
         apply_slot = 2
-        if self.static_grads and self._gpush_rows:
+        if self.static_grads and self._gpush_rows and nopush:
+            push = self._exchange_gpush = self._put_batch(self._gpush_rows, _lib.PUT_WAIT_EMPTY)
+            self._set_src_ready(push, rows["gpush"])
+            push_keys = [4 * pos[v] + 2 for _w, v in rows["gpush"]]
+            push_vars = [None] * len(rows["gpush"])
+            apply_slot = 3
+        elif self.static_grads and self._gpush_rows:
             # static gradients: the weight pushes and the gradient pushes (after
             # their gen, before their apply) share the exchange's one put batch
             push = self._exchange_push = self._put_batch(self._push_rows + self._gpush_rows,
@@ -679,10 +703,13 @@ class PsStep:
         b, n = self.batches, 0
         mode = 1 if regen else 0
         if self._exchange is not None:
-            if self.fuse_push:
-                raise errors.InvalidConfig("the fused weight push runs in the phase schedule")
-            _lib.call("srf_ps_exchange_launch", self._exchange, self.stream, iteration, mode)
-            return 1
+            x, bits, prologue = self._exchange_for_launch()
+            if prologue:
+                _lib.call("srf_batch_launch", b["push"], self.stream, iteration, 0, 0)
+                n += 1
+            _lib.call("srf_ps_exchange_launch", x, self.stream, iteration, mode | bits)
+            self._pushed_ahead = self.fuse_push and b["push"] is not None
+            return n + 1
         if b["push"] is not None and not self._pushed_ahead:
             _lib.call("srf_batch_launch", b["push"], self.stream, iteration, 0, 0)
             n += 1
@@ -746,16 +773,23 @@ class PsStep:
         ``per_launch`` iterations each (the unit queue repeats inside one
         launch; a push of iteration k waits for its variable's apply of
         iteration k-1).  Returns the number of launches."""
-        if self.fuse_push:
-            raise errors.InvalidConfig("the fused weight push runs in the phase schedule")
         self.use_schedule("exchange")
         n, it = 0, first_iteration
+        if self._pushed_ahead and not self.fuse_push and iterations > 0:
+            n += self.step(it, regen)   # consumes the forwarded weights (no push)
+            it += 1
+            iterations -= 1
         while iterations > 0:
             k = min(per_launch, iterations)
-            if self._exchange is not None:
-                _lib.call("srf_ps_exchange_launch_n", self._exchange, self.stream, it, k,
-                          1 if regen else 0)
+            x, bits, prologue = self._exchange_for_launch()
+            if prologue:
+                _lib.call("srf_batch_launch", self.batches["push"], self.stream, it, 0, 0)
                 n += 1
+            if x is not None:
+                _lib.call("srf_ps_exchange_launch_n", x, self.stream, it, k,
+                          (1 if regen else 0) | bits)
+                n += 1
+            self._pushed_ahead = self.fuse_push and self.batches["push"] is not None
             it += k
             iterations -= k
         return n
@@ -817,11 +851,12 @@ class PsStep:
 
     def close(self) -> None:
         self.sync()
-        if self._exchange_built is not None:
-            _lib.call("srf_ps_exchange_destroy", self._exchange_built)
-            self._exchange = self._exchange_built = None
+        for x in (self._exchange_built, self._exchange_nopush):
+            if x is not None:
+                _lib.call("srf_ps_exchange_destroy", x)
+        self._exchange = self._exchange_built = self._exchange_nopush = None
         for b in [self.batches["push"], self.batches["meta"], self.batches["gpush"],
-                  self._exchange_push, *self.batches["gen"].values(),
+                  self._exchange_push, self._exchange_gpush, *self.batches["gen"].values(),
                   *self.batches["apply"].values()]:
             if b is not None:
                 _lib.load().srf_batch_destroy(b)

@@ -398,7 +398,7 @@ def test_fused_weight_push_matches_oracle(shapes, W, P, coloc, op):
             raw = ps.space(w).read_raw(ps.addr(w, ("wbuf", v)), L.nbytes(v) + 1)
             assert raw[:-1] == want[v].tobytes() and raw[-1] == 1, (v, w)
     with pytest.raises(errors.InvalidConfig):
-        ps.use_schedule("exchange")    # a forwarded push is outstanding
+        ps.run_persistent(it + 1, 1)   # a forwarded push is outstanding
     ps.fuse_push = False
     it += 1
     ps.step(it)                         # consumes it, pushes nothing
@@ -425,6 +425,33 @@ def test_fused_weight_push_graph_replay():
     ps.sync()
     _lib.call("srf_graph_destroy", graph)
     want = port.ps_expected(shapes, 2, 4, 11, op="sgd", lr=0.02)
+    for v in range(len(shapes)):
+        assert ps.variable(v).tobytes() == want[v].tobytes(), v
+    ps.close()
+
+
+@pytest.mark.parametrize("shapes,W,P,coloc", CASES)
+@pytest.mark.parametrize("static", [False, True])
+def test_fused_weight_push_in_the_exchange(shapes, W, P, coloc, static):
+    """The exchange schedule with the fused weight push: the exchange built
+    without weight pushes, applies forwarding; single- and multi-iteration
+    launches, switching fusion on and off between launches and between
+    schedules, all equal the oracle."""
+    L = PsLayout(shapes, W, P, coloc, grad_mechanism="static" if static else "dynamic")
+    ps = PsStep(L, seed=23, op="sgd", lr=0.02, schedule="exchange", fuse_push=True)
+    it = 0
+    for fused, how in ((True, "step"), (True, "multi"), (False, "step"), (True, "multi"),
+                       (False, "multi"), (True, "phases"), (True, "step"), (False, "multi")):
+        ps.fuse_push = fused
+        if how == "multi":
+            ps.run_exchange(it + 1, 4, per_launch=2)
+            it += 4
+        else:
+            ps.use_schedule("phases" if how == "phases" else "exchange")
+            it += 1
+            ps.step(it)
+    ps.sync()
+    want = port.ps_expected(shapes, W, 23, it, op="sgd", lr=0.02)
     for v in range(len(shapes)):
         assert ps.variable(v).tobytes() == want[v].tobytes(), v
     ps.close()

@@ -60,6 +60,28 @@ class TorchPool:
                 f"tensor at {ptr:#x} (+{n}) is not contiguous inside the torch pool")
         return addr, n, r.access_token
 
+    def as_tensor(self, tensor):
+        """The torch tensor as a runtime :class:`~paper_1805_08430_b200.graph.Tensor`
+        of this pool's space: a non-owned view of its bytes inside the
+        registered region, so the reference endpoints send it zero-copy
+        (``StaticSender.send(..., stage_copy=False)`` puts straight from it,
+        ``DynSender.send`` announces its address for the receiver's pull) -
+        the sender-side zero-copy the reference reaches by tracing allocation
+        sites (``analyzer.py:226-272``), here for any tensor torch produced."""
+        from .graph import Tensor
+        from .memspace import BufferRef, RegionHandle
+        from .wire import ElemType
+        import torch
+        kinds = {torch.float32: ElemType.F32, torch.float64: ElemType.F64,
+                 torch.int32: ElemType.I32, torch.int64: ElemType.I64,
+                 torch.uint8: ElemType.U8}
+        if tensor.dtype not in kinds:
+            raise errors.InvalidConfig(f"no wire element type for {tensor.dtype}")
+        addr, n, tok = self.locate(tensor)
+        view = BufferRef(RegionHandle(self.region.region_id, addr, n, tok))
+        return Tensor(tuple(int(d) for d in tensor.shape), kinds[tensor.dtype], view,
+                      self.space.server_id)
+
     def stats(self) -> dict:
         used, peak, cap = C.c_uint64(), C.c_uint64(), C.c_uint64()
         _lib.call("srf_torch_pool_stats", self.device, C.byref(used), C.byref(peak),

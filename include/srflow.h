@@ -488,6 +488,35 @@ int srf_edge_recv(srf_edge_t edge, uint32_t rounds, srf_stream_t stream, srf_spa
 int srf_edge_post(srf_space_t snd_space, srf_space_t rcv_space, uint64_t posted_addr,
                   uint64_t count, uint64_t wait_addr, uint32_t need, srf_stream_t stream);
 
+/* Pipelined dynamic edge (EXTENSION of dynamic allocation, runtime/protocol.py
+ * :147-254): `slots` metadata blocks on the receiver (8D+33 B each, the
+ * layout of encode_meta, wire.py:109-119).  srf_dyn_edge_send (sender GPU,
+ * one thread) writes round j's block into slot j % slots once its flag reads
+ * 0 - dims, element code, the payload's space address (src_addr + (j % nsrc) *
+ * src_stride), token and length, flag released last.  srf_dyn_edge_recv (one
+ * persistent TMA launch on the receiver) acquires each block, validates it
+ * like decode_meta + check_remote_access (wire.py:122-144,
+ * memspace.py:145-157; a bad block sets the space's error), allocates the
+ * round's block on demand from a device ring arena in round order, and pulls
+ * the payload from the sender's pool into it (fabric.py:371-389).
+ * srf_dyn_edge_consume consumes rounds in order (mode 1: byte checksums),
+ * frees their ring blocks and clears the metadata flags (the credits). */
+typedef struct srf_dyn_edge *srf_dyn_edge_t;
+int srf_dyn_edge_create(srf_space_t src_space, uint64_t lo, uint64_t hi, uint64_t token,
+                        uint64_t max_bytes, uint32_t rank, srf_space_t dst_space,
+                        uint64_t meta_addr, uint64_t meta_stride, uint32_t slots,
+                        uint64_t ring_addr, uint64_t ring_cap, srf_dyn_edge_t *out);
+int srf_dyn_edge_recv(srf_dyn_edge_t edge, uint32_t rounds, srf_stream_t stream,
+                      srf_space_t dst_space);
+int srf_dyn_edge_consume(srf_dyn_edge_t edge, srf_space_t dst_space, uint64_t first_round,
+                         uint32_t rounds, int mode, uint64_t sums_addr, srf_stream_t stream);
+int srf_dyn_edge_send(srf_space_t snd_space, srf_space_t rcv_space, uint64_t meta_addr,
+                      uint64_t meta_stride, uint32_t slots, uint32_t rank, int elem,
+                      const uint64_t *dims, uint64_t src_addr, uint64_t src_stride,
+                      uint32_t nsrc, uint64_t src_token, uint64_t first_round, uint32_t rounds,
+                      srf_stream_t stream);
+int srf_dyn_edge_destroy(srf_dyn_edge_t edge);
+
 /* ---- Session iteration recording and replay (runtime/session.py:606-629) --
  * srf_record_begin / srf_record_end capture every device launch the library
  * makes in between (puts, pulls, inline metadata puts, GenGrad, updates,

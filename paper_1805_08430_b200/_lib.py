@@ -153,6 +153,13 @@ SIGNATURES = {
                                        C.c_uint32, u64, u64, u64, C.c_int, P(vp)]),
     "srf_edge_recv": (C.c_int, [vp, C.c_uint32, vp, vp]),
     "srf_edge_post": (C.c_int, [vp, vp, u64, u64, u64, C.c_uint32, vp]),
+    "srf_dyn_edge_create": (C.c_int, [vp, u64, u64, u64, u64, C.c_uint32, vp, u64, u64,
+                                      C.c_uint32, u64, u64, P(vp)]),
+    "srf_dyn_edge_recv": (C.c_int, [vp, C.c_uint32, vp, vp]),
+    "srf_dyn_edge_consume": (C.c_int, [vp, vp, u64, C.c_uint32, C.c_int, u64, vp]),
+    "srf_dyn_edge_send": (C.c_int, [vp, vp, u64, u64, C.c_uint32, C.c_uint32, C.c_int, P(u64),
+                                    u64, u64, C.c_uint32, u64, u64, C.c_uint32, vp]),
+    "srf_dyn_edge_destroy": (C.c_int, [vp]),
     "srf_matmul": (C.c_int, [C.c_int, u64, u64, u64, u64, u64, u64, vp]),
     "srf_compute": (C.c_int, [vp, C.c_int, C.c_int, u64, u64, u64, u64, u64, u64, vp]),
     "srf_record_begin": (C.c_int, []),

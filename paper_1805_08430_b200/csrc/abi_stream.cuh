@@ -347,6 +347,221 @@ int srf_edge_consume(srf_space_t rcv, uint64_t slots_addr, uint32_t slots, uint6
   return SRF_OK;
 }
 
+// ---- pipelined dynamic edge (device_stream.cuh, k_dyn_*) -------------------
+struct srf_dyn_edge {
+  int device;
+  DynEdgeArgs a;
+  void *state = nullptr;
+  uint64_t next_round = 0;
+  int ctas = 0;
+};
+
+// Receiver side: metadata slots (slots x meta_stride bytes at meta_addr of
+// dst_space, flag bytes zeroed here), a ring arena of ring_cap bytes at
+// ring_addr (256-B aligned), and the sender's payload region [lo, hi) with its
+// token as seen through src_space (the receiver's mapping of the sender).
+int srf_dyn_edge_create(srf_space_t src_space, uint64_t lo, uint64_t hi, uint64_t token,
+                        uint64_t max_bytes, uint32_t rank, srf_space_t dst_space,
+                        uint64_t meta_addr, uint64_t meta_stride, uint32_t slots,
+                        uint64_t ring_addr, uint64_t ring_cap, srf_dyn_edge_t *out) {
+  DeviceGuard device_guard;
+  if (rank < 1 || rank > (uint32_t)kDynMaxRank)
+    return fail(SRF_E_INVALID_CONFIG, "rank 1..%d", kDynMaxRank);
+  if (slots < 1) return fail(SRF_E_INVALID_CONFIG, "slots >= 1");
+  if (dst_space->imported) return fail(SRF_E_INVALID_CONFIG, "the receiver's slots are local");
+  if (meta_stride < 8ull * rank + 33 || meta_stride % 8 || meta_addr % 8)
+    return fail(SRF_E_INVALID_CONFIG, "metadata slots: 8-B aligned, >= 8D+33 B apart");
+  if (ring_addr % 256 || ring_cap < ((max_bytes + 255) & ~255ull) || ring_cap == 0)
+    return fail(SRF_E_INVALID_CONFIG, "ring arena: 256-B aligned, >= one round");
+  int rc = check_raw(dst_space, meta_addr, (uint64_t)slots * meta_stride, "metadata slots");
+  if (!rc) rc = check_raw(dst_space, ring_addr, ring_cap, "ring arena");
+  if (rc) return rc;
+  {
+    std::lock_guard<std::mutex> g(src_space->mu);
+    rc = check_remote_locked(src_space, lo, hi - lo, token);
+    if (rc) return rc;
+  }
+  srf_dyn_edge *e = new srf_dyn_edge();
+  e->device = dst_space->device;
+  DynEdgeArgs &a = e->a;
+  memset(&a, 0, sizeof a);
+  a.meta = dst_space->base + meta_addr;
+  a.meta_stride = meta_stride;
+  a.slots = slots;
+  a.rank = rank;
+  a.peer_base = src_space->base;
+  a.lo = lo;
+  a.hi = hi;
+  a.token = token;
+  a.max_bytes = max_bytes;
+  uint64_t chunk = g_edge_chunk ? (g_edge_chunk << 10)
+                                : std::min<uint64_t>(256 << 10,
+                                                     std::max<uint64_t>(32 << 10, max_bytes / 16));
+  chunk = (chunk + 4095) & ~4095ull;
+  if (chunk > max_bytes && max_bytes) chunk = (max_bytes + 15) & ~15ull;
+  if (chunk == 0) chunk = 16;
+  a.chunk = chunk;
+  a.nchunks = (uint32_t)std::max<uint64_t>(1, (max_bytes + chunk - 1) / chunk);
+  a.ring = dst_space->base + ring_addr;
+  a.ring_cap = ring_cap;
+  a.timeout_ns = g_put_timeout_ns;
+  a.err = dst_space->err;
+  e->ctas = g_edge_ctas ? g_edge_ctas : std::max(1, sm_count_of(e->device) - 2);
+  CUDA_TRY(cudaSetDevice(e->device));
+  // arrival[slots] claim exit alloc_seq consumed | alloc_head freed out[3 slots] | ready[slots]
+  const size_t words32 = (size_t)slots + 5, words64 = 2 + 3 * (size_t)slots;
+  const size_t bytes = 8 * ((words32 * 4 + 7) / 8) + 8 * words64 + slots;
+  cudaError_t err = cudaMalloc(&e->state, bytes);
+  if (err == cudaSuccess) err = cudaMemset(e->state, 0, bytes);
+  for (uint32_t i = 0; err == cudaSuccess && i < slots; ++i)
+    err = cudaMemset(a.meta + (uint64_t)i * meta_stride + 8ull * rank + 32, 0, 1);
+  if (err == cudaSuccess) err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) {
+    if (e->state) cudaFree(e->state);
+    delete e;
+    return fail(SRF_E_DEVICE, "dynamic edge state: %s", cudaGetErrorString(err));
+  }
+  unsigned int *w32 = (unsigned int *)e->state;
+  a.arrival = w32;
+  a.claim = w32 + slots;
+  a.exit_count = w32 + slots + 1;
+  a.alloc_seq = w32 + slots + 2;
+  a.consumed = w32 + slots + 3;
+  unsigned long long *w64 = (unsigned long long *)((uint8_t *)e->state + 8 * ((words32 * 4 + 7) / 8));
+  a.alloc_head = w64;
+  a.freed = w64 + 1;
+  a.out = w64 + 2;
+  a.ready = (uint8_t *)(w64 + words64);
+  *out = e;
+  return SRF_OK;
+}
+
+// the receiver pulls its next `rounds` rounds (one persistent TMA launch)
+int srf_dyn_edge_recv(srf_dyn_edge_t e, uint32_t rounds, srf_stream_t st, srf_space_t dst_space) {
+  DeviceGuard device_guard;
+  if (rounds == 0) return SRF_OK;
+  if ((uint64_t)rounds * e->a.nchunks > 0xFFFFFFFFull)
+    return fail(SRF_E_INVALID_CONFIG, "too many work items in one launch");
+  srf_stream *s = stream_or_default(dst_space, st);
+  if (s->device != e->device) return fail(SRF_E_INVALID_CONFIG, "stream on another GPU");
+  DynEdgeArgs a = e->a;
+  a.first_round = e->next_round;
+  a.rounds = rounds;
+  const int grid = (int)std::min<uint64_t>((uint64_t)e->ctas, (uint64_t)rounds * a.nchunks);
+  CUDA_TRY(cudaSetDevice(e->device));
+  static bool attr_set[64] = {false};
+  if (e->device >= 0 && e->device < 64 && !attr_set[e->device]) {
+    CUDA_TRY(cudaFuncSetAttribute(k_dyn_pull_stream, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  kBulkSmem));
+    attr_set[e->device] = true;
+  }
+  k_dyn_pull_stream<<<grid, 256, kBulkSmem, s->s>>>(a);
+  int rc = launch_check("k_dyn_pull_stream");
+  if (rc) return rc;
+  e->next_round += rounds;
+  return SRF_OK;
+}
+
+// the receiver's consumer for rounds [first_round, +rounds) (mode 1: 8-B
+// checksum per round at sums_addr of dst_space); returns once it is resident
+int srf_dyn_edge_consume(srf_dyn_edge_t e, srf_space_t dst_space, uint64_t first_round,
+                         uint32_t rounds, int mode, uint64_t sums_addr, srf_stream_t st) {
+  DeviceGuard device_guard;
+  if (mode == 1) {
+    int rc = check_raw(dst_space, sums_addr, 8ull * rounds, "checksums");
+    if (rc) return rc;
+    if (sums_addr % 8) return fail(SRF_E_INVALID_CONFIG, "checksums must be 8-B aligned");
+  }
+  if (rounds == 0) return SRF_OK;
+  srf_stream *s = stream_or_default(dst_space, st);
+  if (s->device != e->device) return fail(SRF_E_INVALID_CONFIG, "stream on another GPU");
+  CUDA_TRY(cudaSetDevice(s->device));
+  static std::mutex mu;
+  static uint32_t *sh = nullptr, *sd = nullptr, tickets = 0;
+  uint32_t ticket;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    if (!sh) {
+      CUDA_TRY(cudaHostAlloc((void **)&sh, 64, cudaHostAllocMapped | cudaHostAllocPortable));
+      CUDA_TRY(cudaHostGetDevicePointer((void **)&sd, sh, 0));
+      *(volatile uint32_t *)sh = 0;
+    }
+    ticket = ++tickets;
+    if (ticket == 0) ticket = ++tickets;
+  }
+  k_dyn_consume_stream<<<1, mode == 1 ? 1024 : 32, 0, s->s>>>(
+      e->a, first_round, rounds, mode, (unsigned long long *)(dst_space->base + sums_addr), sd,
+      ticket);
+  int rc = launch_check("k_dyn_consume_stream");
+  if (rc) return rc;
+  const auto t0 = std::chrono::steady_clock::now();
+  while (*(volatile uint32_t *)sh != ticket) {
+    if (cudaStreamQuery(s->s) == cudaSuccess) break;
+    if (std::chrono::steady_clock::now() - t0 > std::chrono::nanoseconds(g_put_timeout_ns))
+      return fail(SRF_E_TIMEOUT, "dynamic edge consumer did not start");
+  }
+  return SRF_OK;
+}
+
+// Sender side: rounds [first_round, +rounds), round j announcing payload
+// src_addr + (j % nsrc) * src_stride (registered, token) of nbytes with the
+// given dims / element code.  rcv_space: the sender's mapping of the receiver.
+int srf_dyn_edge_send(srf_space_t snd_space, srf_space_t rcv_space, uint64_t meta_addr,
+                      uint64_t meta_stride, uint32_t slots, uint32_t rank, int elem,
+                      const uint64_t *dims, uint64_t src_addr, uint64_t src_stride,
+                      uint32_t nsrc, uint64_t src_token, uint64_t first_round, uint32_t rounds,
+                      srf_stream_t st) {
+  DeviceGuard device_guard;
+  if (rank < 1 || rank > (uint32_t)kDynMaxRank || slots < 1 || nsrc < 1)
+    return fail(SRF_E_INVALID_CONFIG, "rank / slots / nsrc");
+  if (elem < 0 || elem > 4) return fail(SRF_E_INVALID_CONFIG, "element code %d", elem);
+  const uint64_t esz = elem == 0 || elem == 2 ? 4 : elem == 4 ? 1 : 8;
+  uint64_t nbytes = esz;
+  for (uint32_t k = 0; k < rank; ++k) nbytes *= dims[k];
+  int rc = check_raw(rcv_space, meta_addr, (uint64_t)slots * meta_stride, "metadata slots");
+  if (rc) return rc;
+  if (meta_stride % 8 || meta_addr % 8 || meta_stride < 8ull * rank + 33)
+    return fail(SRF_E_INVALID_CONFIG, "metadata slot geometry");
+  {
+    std::lock_guard<std::mutex> g(snd_space->mu);
+    rc = check_registered_locked(snd_space, src_addr, (uint64_t)(nsrc - 1) * src_stride + nbytes,
+                                 src_token);
+    if (rc) return rc;
+  }
+  if (rounds == 0) return SRF_OK;
+  DynSendArgs a;
+  memset(&a, 0, sizeof a);
+  a.meta = rcv_space->base + meta_addr;
+  a.meta_stride = meta_stride;
+  a.slots = slots;
+  a.rank = rank;
+  a.code = (uint32_t)elem;
+  a.nsrc = nsrc;
+  for (uint32_t k = 0; k < rank; ++k) a.dims[k] = dims[k];
+  a.src_addr = src_addr;
+  a.src_stride = src_stride;
+  a.token = src_token;
+  a.nbytes = nbytes;
+  a.first_round = first_round;
+  a.rounds = rounds;
+  a.timeout_ns = g_put_timeout_ns;
+  a.err = snd_space->err;
+  srf_stream *s = stream_or_default(snd_space, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  k_dyn_send_stream<<<1, 32, 0, s->s>>>(a);
+  return launch_check("k_dyn_send_stream");
+}
+
+int srf_dyn_edge_destroy(srf_dyn_edge_t e) {
+  DeviceGuard device_guard;
+  if (!e) return SRF_OK;
+  cudaSetDevice(e->device);
+  cudaDeviceSynchronize();
+  cudaFree(e->state);
+  delete e;
+  return SRF_OK;
+}
+
 int srf_edge_destroy(srf_edge_t e) {
   DeviceGuard device_guard;
   if (!e) return SRF_OK;

@@ -374,3 +374,257 @@ __global__ void k_post_rounds(unsigned long long *posted, unsigned long long cou
   __threadfence_system();
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(posted), "l"(count) : "memory");
 }
+
+// ---------------------------------------------------------------------------
+// Pipelined DYNAMIC edge (extension of dynamic allocation, runtime/protocol.py
+// :147-254): `slots` metadata blocks on the receiver instead of one.  The
+// sender (k_dyn_send_stream, one thread) writes round j's 8D+33-byte block -
+// byte-identical to encode_meta (wire.py:109-119): element code, rank, dims,
+// the payload's space address, token, length, flag last with a system-scope
+// release - into slot j % slots once that slot's flag reads 0 (the credit).
+// The receiver (k_dyn_pull_stream, persistent, TMA) acquires the flag, decodes
+// and validates the block like decode_meta + check_remote_access
+// (wire.py:122-144, memspace.py:145-157), allocates the round's block on
+// demand from a device ring arena (in round order: the chunk-0 CTA bumps the
+// head, waiting while the ring is full), pulls the payload from the sender's
+// pool into it (the one-sided read of fabric.py:371-389) and marks it ready.
+// The consumer (k_dyn_consume_stream) reads the block, frees it (ring tail)
+// and clears the metadata flag - the sender's credit for the slot.
+// ---------------------------------------------------------------------------
+static constexpr int kDynMaxRank = 8;
+
+struct DynEdgeArgs {
+  uint8_t *meta;                  // receiver: slot 0's metadata block (local)
+  uint64_t meta_stride;
+  uint32_t slots, rank;
+  const uint8_t *peer_base;       // receiver's mapping of the sender's pool
+  uint64_t lo, hi, token;         // the sender's payload region (its space coordinates)
+  uint64_t max_bytes, chunk;
+  uint32_t nchunks;
+  uint8_t *ring;
+  uint64_t ring_cap;
+  unsigned long long *alloc_head, *freed;  // bytes allocated / freed (monotonic)
+  unsigned int *alloc_seq;        // rounds allocated
+  unsigned int *consumed;         // rounds consumed (their flags cleared)
+  unsigned long long *out;        // [slots][3]: offset, length, allocation end
+  uint8_t *ready;                 // [slots]: round's block complete
+  unsigned int *arrival, *claim, *exit_count;
+  uint64_t first_round;
+  uint32_t rounds;
+  uint64_t timeout_ns;
+  int *err;
+};
+
+__device__ __forceinline__ uint64_t ld_volatile_u64(const void *p) {
+  return *(const volatile uint64_t *)p;
+}
+
+struct DynSendArgs {
+  uint8_t *meta;                  // the receiver's slot 0 (through the sender's mapping)
+  uint64_t meta_stride;
+  uint32_t slots, rank, code, nsrc;
+  uint64_t dims[kDynMaxRank];
+  uint64_t src_addr, src_stride, token, nbytes;  // payload j % nsrc (space coordinates)
+  uint64_t first_round;
+  uint32_t rounds;
+  uint64_t timeout_ns;
+  int *err;
+};
+
+__global__ void k_dyn_send_stream(const __grid_constant__ DynSendArgs a) {
+  if (threadIdx.x != 0) return;
+  for (uint32_t r = 0; r < a.rounds; ++r) {
+    const uint64_t j = a.first_round + r;
+    uint8_t *m = a.meta + (j % a.slots) * a.meta_stride;
+    uint8_t *flag = m + 8ull * a.rank + 32;
+    const uint64_t t0 = globaltimer_ns();
+    while (ld_acquire_sys_u8(flag) != 0) {       // the consumer's credit
+      if (globaltimer_ns() - t0 > a.timeout_ns) {
+        atomicExch(a.err, 2);
+        return;
+      }
+      __nanosleep(32);
+    }
+    uint64_t *w = (uint64_t *)m;
+    w[0] = (uint64_t)a.code | ((uint64_t)a.rank << 8);
+    for (uint32_t k = 0; k < a.rank; ++k) w[1 + k] = a.dims[k];
+    w[1 + a.rank] = a.src_addr + (j % a.nsrc) * a.src_stride;
+    w[2 + a.rank] = a.token;
+    w[3 + a.rank] = a.nbytes;
+    release_tail(flag, 1, 1);                     // flag last
+  }
+}
+
+__global__ void __launch_bounds__(256) k_dyn_pull_stream(const __grid_constant__ DynEdgeArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint32_t s_i;
+  __shared__ int s_last, s_bad;
+  __shared__ uint64_t s_off, s_len, s_src;
+  uint64_t *bars = (uint64_t *)(smem + kBulkChunk * kBulkStages);
+  uint32_t seq = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kBulkStages; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const uint32_t total = a.rounds * a.nchunks;
+  for (;;) {
+    if (threadIdx.x == 0) s_i = atomicAdd(a.claim, 1u);
+    __syncthreads();
+    const uint32_t i = s_i;
+    __syncthreads();
+    if (i >= total) break;
+    const uint32_t jr = i / a.nchunks;
+    const uint32_t c = i - jr * a.nchunks;
+    const uint64_t j = a.first_round + jr;
+    const uint32_t slot = (uint32_t)(j % a.slots);
+    const uint8_t *m = a.meta + (uint64_t)slot * a.meta_stride;
+    if (threadIdx.x == 0) {
+      s_bad = *(volatile int *)a.err != 0;
+      const uint64_t t0 = globaltimer_ns();
+      // the slot's previous round must have been consumed (its flag cleared):
+      // a flag still set from round j - slots is not round j's
+      while (!s_bad && j >= a.slots &&
+             ld_acquire_gpu_u32(a.consumed) < (uint32_t)(j - a.slots + 1)) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          atomicExch(a.err, 2);
+          s_bad = 1;
+        }
+        __nanosleep(32);
+      }
+      while (!s_bad && ld_acquire_sys_u8(m + 8ull * a.rank + 32) != 1) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          atomicExch(a.err, 2);
+          s_bad = 1;
+        }
+        __nanosleep(32);
+      }
+      uint64_t addr = 0, plen = 0;
+      if (!s_bad) {
+        // decode_meta + check_remote_access on the device
+        const uint32_t code = ((const volatile uint8_t *)m)[0];
+        const uint32_t rk = ((const volatile uint8_t *)m)[1];
+        const uint64_t esz = code == 0 ? 4 : code == 1 ? 8 : code == 2 ? 4 : code == 3 ? 8
+                           : code == 4 ? 1 : 0;
+        uint64_t prod = esz;
+        for (uint32_t k = 0; k < a.rank; ++k) prod *= ld_volatile_u64(m + 8 + 8 * k);
+        addr = ld_volatile_u64(m + 8 + 8 * a.rank);
+        const uint64_t tok = ld_volatile_u64(m + 16 + 8 * a.rank);
+        plen = ld_volatile_u64(m + 24 + 8 * a.rank);
+        if (rk != a.rank || esz == 0 || prod != plen || plen > a.max_bytes || tok != a.token ||
+            addr < a.lo || addr + plen > a.hi) {
+          atomicExch(a.err, 6);
+          s_bad = 1;
+        }
+      }
+      uint64_t off = 0;
+      if (!s_bad && c == 0) {
+        // on-demand allocation from the ring arena, in round order
+        const uint64_t t1 = globaltimer_ns();
+        while (ld_acquire_gpu_u32(a.alloc_seq) != (uint32_t)j && !s_bad) {
+          if (globaltimer_ns() - t1 > a.timeout_ns) { atomicExch(a.err, 7); s_bad = 1; }
+          __nanosleep(20);
+        }
+        uint64_t head = ld_volatile_u64(a.alloc_head);
+        const uint64_t need = plen ? (plen + 255) & ~255ull : 256;
+        if (head % a.ring_cap + need > a.ring_cap) head += a.ring_cap - head % a.ring_cap;
+        const uint64_t end = head + need;
+        while (!s_bad) {   // wait until the consumer freed enough of the ring
+          uint64_t fr;
+          asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(fr) : "l"(a.freed) : "memory");
+          if (fr + a.ring_cap >= end) break;
+          if (globaltimer_ns() - t1 > a.timeout_ns) { atomicExch(a.err, 7); s_bad = 1; }
+          __nanosleep(32);
+        }
+        off = head % a.ring_cap;
+        unsigned long long *o = a.out + 3ull * slot;
+        o[0] = off;
+        o[1] = plen;
+        o[2] = end;
+        *(volatile unsigned long long *)a.alloc_head = end;
+        st_release_sys_u32(a.alloc_seq, (unsigned)j + 1);  // (gpu scope would do)
+      } else if (!s_bad) {
+        const uint64_t t1 = globaltimer_ns();
+        while (ld_acquire_gpu_u32(a.alloc_seq) < (uint32_t)j + 1 && !s_bad) {
+          if (globaltimer_ns() - t1 > a.timeout_ns) { atomicExch(a.err, 7); s_bad = 1; }
+          __nanosleep(20);
+        }
+        off = ld_volatile_u64(a.out + 3ull * slot);
+      }
+      s_off = off;
+      s_len = plen;
+      s_src = (uint64_t)(a.peer_base + addr);
+    }
+    __syncthreads();
+    const uint64_t coff = (uint64_t)c * a.chunk;
+    if (!s_bad && coff < s_len) {
+      const uint64_t n = s_len - coff < a.chunk ? s_len - coff : a.chunk;
+      uint8_t *d = a.ring + s_off + coff;
+      const uint8_t *s = (const uint8_t *)s_src + coff;
+      if ((((uintptr_t)d | (uintptr_t)s) & 15) == 0) {
+        const uint64_t mid = n & ~15ull;
+        if (threadIdx.x == 0 && mid) bulk_copy_range(d, s, mid, smem, bars, seq);
+        for (uint64_t k = mid + threadIdx.x; k < n; k += blockDim.x) d[k] = ld_byte<true>(s + k);
+        if (threadIdx.x == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+      } else {
+        copy_bytes_grid<8, true, true>(d, s, n, threadIdx.x, blockDim.x, false);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = grid_arrive(a.arrival + slot, a.nchunks - 1, 0);
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      atomicExch(a.arrival + slot, 0u);
+      if (*(volatile int *)a.err == 0) release_tail(a.ready + slot, 1, 0);
+    }
+  }
+  if (threadIdx.x == 0 && atomicAdd(a.exit_count, 1u) == gridDim.x - 1) {
+    *a.claim = 0;
+    *a.exit_count = 0;
+  }
+}
+
+// The receiver's consumer: round j's block, in order; mode 1 stores a weighted
+// byte checksum per round (tests); then frees the block (ring tail) and clears
+// the metadata flag (the sender's credit, DynReceiver.poll's clear).
+__global__ void __launch_bounds__(1024) k_dyn_consume_stream(DynEdgeArgs a, uint64_t first_round,
+                                                              uint32_t rounds, int mode,
+                                                              unsigned long long *sums,
+                                                              uint32_t *started, uint32_t ticket) {
+  __shared__ unsigned long long acc;
+  __shared__ int ok;
+  if (threadIdx.x == 0 && started) {
+    *(volatile uint32_t *)started = ticket;
+    __threadfence_system();
+  }
+  for (uint32_t r = 0; r < rounds; ++r) {
+    const uint64_t j = first_round + r;
+    const uint32_t slot = (uint32_t)(j % a.slots);
+    if (threadIdx.x == 0) {
+      acc = 0;
+      ok = spin_until(a.ready + slot, 1, a.timeout_ns, 0) ? 1 : 0;
+      if (!ok) atomicExch(a.err, 1);
+    }
+    __syncthreads();
+    if (!ok) return;
+    const uint64_t off = ld_volatile_u64(a.out + 3ull * slot);
+    const uint64_t len = ld_volatile_u64(a.out + 3ull * slot + 1);
+    const uint64_t end = ld_volatile_u64(a.out + 3ull * slot + 2);
+    if (mode & 1) {
+      unsigned long long sum = 0;
+      const uint8_t *b = a.ring + off;
+      for (uint64_t i = threadIdx.x; i < len; i += blockDim.x)
+        sum += (unsigned long long)__ldcg(b + i) * (i % 251 + 1);
+      atomicAdd(&acc, sum);
+      __syncthreads();
+      if (threadIdx.x == 0) sums[r] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a.ready[slot] = 0;
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.freed), "l"(end) : "memory");
+      release_tail(a.meta + (uint64_t)slot * a.meta_stride + 8ull * a.rank + 32, 0, 1);
+      st_release_sys_u32(a.consumed, (unsigned)j + 1);
+    }
+    __syncthreads();
+  }
+}

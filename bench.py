@@ -993,14 +993,20 @@ class OneWayEdge:
         from paper_1805_08430_b200 import _lib
         from paper_1805_08430_b200.distributed import all_gather_objects, exchange_spaces
         from paper_1805_08430_b200.memspace import MemorySpace
-        from paper_1805_08430_b200.runtime.protocol import PipelinedStaticEdge, PulledStaticEdge
+        from paper_1805_08430_b200.runtime.protocol import (PipelinedDynamicEdge,
+                                                            PipelinedStaticEdge, PulledStaticEdge)
         self.lib, self.S, self.rank, self.mode, self.nsrc = _lib, S, rank, mode, nsrc
         self.slots = slots or PipelinedStaticEdge.default_slots(S)
         self.src_stride = (S + 255) & ~255
         self.slot_stride = (S + 1 + 255) & ~255
         self.role = {0: "snd", 1: "rcv"}.get(rank)
-        size = {"snd": nsrc * self.src_stride, "rcv": self.slots * self.slot_stride}.get(
-            self.role, 0)
+        # dynamic mode: metadata slots + a ring arena of ring_rounds rounds
+        self.meta_stride = PipelinedDynamicEdge.meta_stride(1)
+        self.ring_cap = max(4, min(self.slots, (1 << 30) // max(self.slot_stride, 1))) * \
+            ((S + 255) & ~255)
+        rcv_bytes = (self.slots * self.slot_stride if mode != "dyn" else
+                     self.ring_cap + self.slots * self.meta_stride + 4096)
+        size = {"snd": nsrc * self.src_stride, "rcv": rcv_bytes}.get(self.role, 0)
         self.sp = MemorySpace(rank, size + (8 << 20), seed=0, device=device)
         mine = {}
         if self.role == "snd":
@@ -1010,6 +1016,10 @@ class OneWayEdge:
                           self.payloads.base_addr + i * self.src_stride, S // 4, 0, 0, 0, 2 + i,
                           None, None)
             mine = {"addr": self.payloads.base_addr, "token": self.payloads.access_token}
+        elif self.role == "rcv" and mode == "dyn":
+            self.ring = self.sp.allocate_region(self.ring_cap, register=True)
+            self.meta = self.sp.allocate_region(self.slots * self.meta_stride, register=True)
+            mine = {"meta": self.meta.base_addr}
         elif self.role == "rcv":
             self.slots_reg = self.sp.allocate_region(self.slots * self.slot_stride, register=True)
             self.posted = self.sp.allocate_region(8)
@@ -1035,7 +1045,15 @@ class OneWayEdge:
                                          S, nsrc, self.src_stride, self.sp, self.slots_reg,
                                          self.slots, self.slot_stride, self.posted.base_addr,
                                          tma=True)
-        self.info = self.edge.info() if self.edge is not None else {}
+        elif mode == "dyn" and self.role == "rcv":
+            lo = self.peer["addr"]
+            self.edge = PipelinedDynamicEdge(self.proxies[0], lo, lo + nsrc * self.src_stride,
+                                             self.peer["token"], S, 1, self.sp,
+                                             self.meta.base_addr, self.meta_stride, self.slots,
+                                             self.ring.base_addr, self.ring_cap)
+        self.sums = None
+        self.info = (self.edge.info() if self.edge is not None and mode != "dyn" else
+                     {"ctas": None, "chunk": None})
         self.next = 0
         self.ev = None
         barrier_sync()
@@ -1044,15 +1062,25 @@ class OneWayEdge:
         """Receiver: its consumer first (resident beside a pull grid), then the
         pull launch; sender: the push launch, or the post of the rounds."""
         import ctypes as C
-        from paper_1805_08430_b200.runtime.protocol import PipelinedStaticEdge, PulledStaticEdge
+        from paper_1805_08430_b200.runtime.protocol import (PipelinedDynamicEdge,
+                                                            PipelinedStaticEdge, PulledStaticEdge)
         if timed and self.edge is not None and self.ev is None:
             self.ev = [C.c_void_p(), C.c_void_p()]
             for e in self.ev:
                 self.lib.call("srf_timing_event_create", self.sp.handle, C.byref(e))
-        if self.role == "rcv":
+        if self.role == "rcv" and self.mode == "dyn":
+            self.edge.consume(self.next, rounds, stream=self.st[1])
+        elif self.role == "rcv":
             PipelinedStaticEdge.consume(self.sp, self.slots_reg.base_addr, self.slots,
                                         self.slot_stride, self.S, self.next, rounds,
                                         stream=self.st[1])
+        elif self.role == "snd" and self.mode == "dyn":
+            from paper_1805_08430_b200.wire import ElemType
+            PipelinedDynamicEdge.send(self.sp, self.proxies[1], self.peer["meta"],
+                                      self.meta_stride, self.slots, (self.S // 4,),
+                                      ElemType.F32, self.payloads.base_addr, self.src_stride,
+                                      self.nsrc, self.payloads.access_token, self.next, rounds,
+                                      stream=self.st[1])
         elif self.role == "snd" and self.mode == "pull":
             PulledStaticEdge.post(self.sp, self.proxies[1], self.peer["posted"],
                                   self.next + rounds, stream=self.st[1])
@@ -1061,7 +1089,7 @@ class OneWayEdge:
                 self.lib.call("srf_event_record_on", self.ev[0], self.st[0])
             if self.mode == "push":
                 self.edge.send(rounds, self.st[0])
-            else:
+            else:   # pull / dyn: the receiver's persistent launch
                 self.edge.recv(rounds, self.st[0])
             if timed:
                 self.lib.call("srf_event_record_on", self.ev[1], self.st[0])
@@ -1092,7 +1120,16 @@ class OneWayEdge:
                     for i in range(self.nsrc)]
         want = all_gather_objects(srcs)[0]
         ok = True
-        if self.role == "rcv":
+        if self.role == "rcv" and self.mode == "dyn":
+            # the last round's block sits at the ring position the in-order
+            # allocation gives it (equal-size rounds: (j * need) mod cap, no
+            # wrap padding when need divides cap)
+            need = (self.S + 255) & ~255
+            j = self.next - 1
+            off = (j * need) % self.ring_cap
+            raw = self.sp.read_raw(self.ring.base_addr + off, self.S)
+            ok &= hashlib.sha256(raw).hexdigest() == want[j % self.nsrc]
+        elif self.role == "rcv":
             for j in range(max(0, self.next - self.slots), self.next):
                 raw = self.sp.read_raw(
                     self.slots_reg.base_addr + (j % self.slots) * self.slot_stride, self.S + 1)
@@ -1143,7 +1180,9 @@ def dist_objects_first(obj, owner):
 def sweep_nvlink_one_way(max_bytes, rank, world, device):
     """configs[1] literally: 1 sender / 1 receiver on 2 GPUs, one direction,
     1 KiB x 4^k up to max_bytes: static placement pushed by the sender's SMs
-    (pipelined edge) and pulled by the receiver's TMA engines (pull edge);
+    (pipelined edge) and pulled by the receiver's TMA engines (pull edge),
+    and dynamic allocation (pipelined dynamic edge: metadata slots, on-demand
+    ring blocks, validated TMA pulls);
     GB/s per direction with fractions of the nominal 900 and of the measured
     770 GB/s peer copy."""
     out = []
@@ -1151,7 +1190,7 @@ def sweep_nvlink_one_way(max_bytes, rank, world, device):
     while size <= max_bytes:
         log(f"[rank {rank}] sweep_nvlink_one_way {size}")
         row = {"bytes": size}
-        for mode in ("push", "pull"):
+        for mode in ("push", "pull", "dyn"):
             r = one_way_rate(size, rank, world, device, mode)
             row[mode] = r
             row[f"{mode}_frac_of_900"] = round(r["gbps"] / NVLINK_NOMINAL_GBS, 4)

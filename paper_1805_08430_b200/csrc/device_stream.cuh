@@ -431,10 +431,18 @@ struct DynSendArgs {
   int *err;
 };
 
+// one warp: lane t owns the slots s with s % L == t (L = min(32, slots)) and
+// writes their rounds in order, so up to L rounds' credit polls and metadata
+// writes are in flight at once (one thread spent ~4 us per round on the
+// remote flag read and the system-scope release, which capped 1 MiB rounds at
+// ~260 GB/s); a slot's rounds stay on one lane, so a credit read 0 can only
+// be the slot's previous round's
 __global__ void k_dyn_send_stream(const __grid_constant__ DynSendArgs a) {
-  if (threadIdx.x != 0) return;
+  const uint32_t L = a.slots < blockDim.x ? a.slots : blockDim.x;
+  if (threadIdx.x >= L) return;
   for (uint32_t r = 0; r < a.rounds; ++r) {
     const uint64_t j = a.first_round + r;
+    if ((uint32_t)(j % a.slots) % L != threadIdx.x) continue;
     uint8_t *m = a.meta + (j % a.slots) * a.meta_stride;
     uint8_t *flag = m + 8ull * a.rank + 32;
     const uint64_t t0 = globaltimer_ns();
@@ -541,7 +549,8 @@ __global__ void __launch_bounds__(256) k_dyn_pull_stream(const __grid_constant__
         o[1] = plen;
         o[2] = end;
         *(volatile unsigned long long *)a.alloc_head = end;
-        st_release_sys_u32(a.alloc_seq, (unsigned)j + 1);  // (gpu scope would do)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.alloc_seq),
+                     "r"((unsigned)j + 1) : "memory");
       } else if (!s_bad) {
         const uint64_t t1 = globaltimer_ns();
         while (ld_acquire_gpu_u32(a.alloc_seq) < (uint32_t)j + 1 && !s_bad) {
@@ -622,8 +631,13 @@ __global__ void __launch_bounds__(1024) k_dyn_consume_stream(DynEdgeArgs a, uint
     if (threadIdx.x == 0) {
       a.ready[slot] = 0;
       asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.freed), "l"(end) : "memory");
-      release_tail(a.meta + (uint64_t)slot * a.meta_stride + 8ull * a.rank + 32, 0, 1);
-      st_release_sys_u32(a.consumed, (unsigned)j + 1);
+      if (mode & 1) __threadfence_system();  // checksummed reads before the credit
+      // the credit: a relaxed store - the consumer read nothing the sender
+      // will rewrite (a system-scope release here is a MEMBAR.SYS per round
+      // in the one serial thread; device_stream.cuh k_consume_stream)
+      st_relaxed_sys_u8(a.meta + (uint64_t)slot * a.meta_stride + 8ull * a.rank + 32, 0);
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.consumed),
+                   "r"((unsigned)j + 1) : "memory");
     }
     __syncthreads();
   }

@@ -817,8 +817,9 @@ def sweep(max_bytes, device):
     'cp' (K5 copy + K1 + K2, the paper's RDMA.cp), dynamic allocation through
     the public endpoints (meta write, doorbell poll + decode, arena alloc, K4
     pull), dynamic with the receiver on the device (K3 + srf_dyn_recv,
-    graph-replayed like static), and for small sizes the host-staged RPC
-    fragment ring."""
+    graph-replayed like static), the pipelined dynamic edge (metadata slots,
+    device ring arena, persistent receiver), and for small sizes the
+    host-staged RPC fragment ring."""
     from paper_1805_08430_b200 import _lib
     out = []
     size = 1024
@@ -862,12 +863,83 @@ def sweep(max_bytes, device):
         row["static_pipelined_verified"] = pipe["verified"]
         row.update(dynamic_rate(size, device))
         row.update(dynamic_device_rate(size, device))
+        row.update(dynamic_pipelined_rate(size, device))
         row.update(rpc_device_rate(size, device))
         if size <= MIB:
             row.update(rpc_rate(size, device))
         out.append(row)
         size *= 4
     return out
+
+
+def dynamic_pipelined_rate(size, device, target_ms=20.0):
+    """Dynamic allocation through the pipelined dynamic edge on one GPU
+    (server 0 -> server 1 on GPU 0, HBM): encode_meta blocks in metadata
+    slots, device validation, on-demand ring-arena blocks, TMA pulls; device
+    time of the receiver's launch; the last round's block verified."""
+    import hashlib
+    from paper_1805_08430_b200 import _lib
+    from paper_1805_08430_b200.memspace import MemorySpace
+    from paper_1805_08430_b200.runtime.protocol import PipelinedDynamicEdge, PipelinedStaticEdge
+    from paper_1805_08430_b200.wire import ElemType
+    S = size
+    slots = PipelinedStaticEdge.default_slots(S)
+    stride = (S + 255) & ~255
+    ring_rounds = max(4, min(slots, (1 << 30) // stride))
+    ring_cap = ring_rounds * stride
+    mstride = PipelinedDynamicEdge.meta_stride(1)
+    a = MemorySpace(0, 2 * stride + (8 << 20), seed=0, device=device)
+    b = MemorySpace(1, ring_cap + slots * mstride + (8 << 20), seed=0, device=device)
+    _lib.call("srf_connect", a.handle, b.handle)
+    src = a.allocate_region(2 * stride, register=True)
+    for i in range(2):
+        _lib.call("srf_gen_reference", a.handle, src.base_addr + i * stride, S // 4, 0, 0, 0,
+                  2 + i, None, None)
+    ring = b.allocate_region(ring_cap, register=True)
+    meta = b.allocate_region(slots * mstride, register=True)
+    a.sync(), b.sync()
+    st = {k: C.c_void_p() for k in ("snd", "pull", "cons")}
+    for k, sp in (("snd", a), ("pull", b), ("cons", b)):
+        _lib.call("srf_stream_create", sp.handle, C.byref(st[k]))
+    e = PipelinedDynamicEdge(a, src.base_addr, src.base_addr + 2 * stride, src.access_token, S,
+                             1, b, meta.base_addr, mstride, slots, ring.base_addr, ring_cap)
+    ev = [C.c_void_p(), C.c_void_p()]
+    for x in ev:
+        _lib.call("srf_timing_event_create", b.handle, C.byref(x))
+    nxt = 0
+
+    def run(rounds, timed=False):
+        nonlocal nxt
+        e.consume(nxt, rounds, stream=st["cons"])
+        PipelinedDynamicEdge.send(a, b, meta.base_addr, mstride, slots, (S // 4,), ElemType.F32,
+                                  src.base_addr, stride, 2, src.access_token, nxt, rounds,
+                                  stream=st["snd"])
+        if timed:
+            _lib.call("srf_event_record_on", ev[0], st["pull"])
+        e.recv(rounds, st["pull"])
+        if timed:
+            _lib.call("srf_event_record_on", ev[1], st["pull"])
+        for h in st.values():
+            _lib.call("srf_stream_sync", h)
+        a.sync(), b.sync()
+        nxt += rounds
+
+    run(2 * slots)
+    rounds = int(max(4 * slots, min(20000, target_ms * 1e-3 * 3000e9 // max(S, 1))))
+    run(rounds, timed=True)
+    ms = C.c_float()
+    _lib.call("srf_event_elapsed_ms", ev[0], ev[1], C.byref(ms))
+    j = nxt - 1
+    got = b.read_raw(ring.base_addr + (j * stride) % ring_cap, S)
+    ok = got == a.read_raw(src.base_addr + (j % 2) * stride, S)
+    e.close()
+    for h in st.values():
+        _lib.call("srf_stream_destroy", h)
+    a.close(), b.close()
+    us = ms.value * 1e3 / rounds
+    return {"dynamic_pipelined_us": round(us, 3),
+            "dynamic_pipelined_gbps": round(S / us / 1e3, 3),
+            "dynamic_pipelined_verified": ok}
 
 
 def dynamic_device_rate(size, device, rounds=None):

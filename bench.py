@@ -2090,6 +2090,18 @@ def main() -> int:
                       f"sent as 8 MiB slices ({len(Ls.shapes)} transfer units), gradient "
                       f"edges static (mechanism_override), "
                       f"{world} workers + {world} shards co-located"))
+            # labelled extension: the reference placement AND the reference's
+            # dynamic gradient edges, tensors > 16 MiB sent as 16 MiB slices on
+            # their own shard - the next slice's GenGrad overlaps this slice's
+            # pull + update + (fused) weight push (profiles/r2_ps_slice_fused_n2.jsonl)
+            Ld = PsLayout(vgg16_shapes(), world, world, colocate=True, slice_bytes=16 << 20)
+            section("ps_sliced_dynamic", lambda: bench_ps(
+                rank, world, local, max(10, args.steps), args.warmup, op=args.ps_op,
+                cpu=False, layout=Ld,
+                label=f"EXTENSION: VGG-16, reference round-robin placement and dynamic "
+                      f"gradient edges, tensors > 16 MiB sent as 16 MiB slices "
+                      f"({len(Ld.shapes)} transfer units), {world} workers + {world} shards "
+                      f"co-located"))
             # labelled extension: partitioned variables (every tensor > 16 MiB cut
             # into one slice per shard), byte-balanced; values bit-identical
             # (from 4 GPUs the partitions are also sent as 4 MiB slices: 537 -> 672
@@ -2115,7 +2127,8 @@ def main() -> int:
     ps_ok = line.get("ps", {}).get("verified", True) and all(
         c.get("verified", True) for k in ("ps_configs", "ps_session")
         for c in line.get(k, {}).values() if isinstance(c, dict)) and all(line.get(k, {}).get("verified", True) for k in
-                                      ("ps_balanced", "ps_sliced", "ps_partitioned"))
+                                      ("ps_balanced", "ps_sliced", "ps_sliced_dynamic",
+                                       "ps_partitioned"))
     if not dev["verified"] or not single["verified"] or not e2e["verified"] or not ps_ok:
         log("verification FAILED")
         return 1

@@ -476,18 +476,23 @@ int srf_dyn_edge_consume(srf_dyn_edge_t e, srf_space_t dst_space, uint64_t first
   srf_stream *s = stream_or_default(dst_space, st);
   if (s->device != e->device) return fail(SRF_E_INVALID_CONFIG, "stream on another GPU");
   CUDA_TRY(cudaSetDevice(s->device));
+  // a pinned, mapped word per device the consumer stamps when it runs
   static std::mutex mu;
-  static uint32_t *sh = nullptr, *sd = nullptr, tickets = 0;
-  uint32_t ticket;
+  static uint32_t *hs[64] = {nullptr}, *ds[64] = {nullptr}, tickets[64] = {0};
+  const int dev = s->device;
+  if (dev < 0 || dev >= 64) return fail(SRF_E_INVALID_CONFIG, "device index %d", dev);
+  uint32_t ticket, *sh, *sd;
   {
     std::lock_guard<std::mutex> g(mu);
-    if (!sh) {
-      CUDA_TRY(cudaHostAlloc((void **)&sh, 64, cudaHostAllocMapped | cudaHostAllocPortable));
-      CUDA_TRY(cudaHostGetDevicePointer((void **)&sd, sh, 0));
-      *(volatile uint32_t *)sh = 0;
+    if (!hs[dev]) {
+      CUDA_TRY(cudaHostAlloc((void **)&hs[dev], 64, cudaHostAllocMapped | cudaHostAllocPortable));
+      CUDA_TRY(cudaHostGetDevicePointer((void **)&ds[dev], hs[dev], 0));
+      *(volatile uint32_t *)hs[dev] = 0;
     }
-    ticket = ++tickets;
-    if (ticket == 0) ticket = ++tickets;
+    sh = hs[dev];
+    sd = ds[dev];
+    ticket = ++tickets[dev];
+    if (ticket == 0) ticket = ++tickets[dev];
   }
   k_dyn_consume_stream<<<1, mode == 1 ? 1024 : 32, 0, s->s>>>(
       e->a, first_round, rounds, mode, (unsigned long long *)(dst_space->base + sums_addr), sd,

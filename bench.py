@@ -1225,8 +1225,13 @@ class OneWayEdge:
 def one_way_rate(S, rank, world, device, mode, target_ms=20.0):
     """GB/s of one direction (rank 0 -> rank 1) for rounds of S bytes: device
     time of the launching rank's stream (max over ranks), after a warm-up
-    launch; verified bit-exact on the receiver."""
-    e = OneWayEdge(S, rank, world, device, mode)
+    launch; verified bit-exact on the receiver.  mode "pull1": the pull edge
+    with ONE receive region - the reference's own static protocol (one
+    pre-placed region per edge, the flag its credit)."""
+    if mode == "pull1":
+        e = OneWayEdge(S, rank, world, device, "pull", slots=1)
+    else:
+        e = OneWayEdge(S, rank, world, device, mode)
     rounds = int(max(4 * e.slots, min(20000, target_ms * 1e-3 * 750e9 // max(S, 1))))
     e.launch(2 * e.slots)
     e.sync()
@@ -1252,8 +1257,9 @@ def dist_objects_first(obj, owner):
 def sweep_nvlink_one_way(max_bytes, rank, world, device):
     """configs[1] literally: 1 sender / 1 receiver on 2 GPUs, one direction,
     1 KiB x 4^k up to max_bytes: static placement pushed by the sender's SMs
-    (pipelined edge) and pulled by the receiver's TMA engines (pull edge),
-    and dynamic allocation (pipelined dynamic edge: metadata slots, on-demand
+    (pipelined edge) and pulled by the receiver's TMA engines (pull edge;
+    "pull1": with the reference's single receive region per edge), and
+    dynamic allocation (pipelined dynamic edge: metadata slots, on-demand
     ring blocks, validated TMA pulls);
     GB/s per direction with fractions of the nominal 900 and of the measured
     770 GB/s peer copy."""
@@ -1262,7 +1268,7 @@ def sweep_nvlink_one_way(max_bytes, rank, world, device):
     while size <= max_bytes:
         log(f"[rank {rank}] sweep_nvlink_one_way {size}")
         row = {"bytes": size}
-        for mode in ("push", "pull", "dyn"):
+        for mode in ("push", "pull", "pull1", "dyn"):
             r = one_way_rate(size, rank, world, device, mode)
             row[mode] = r
             row[f"{mode}_frac_of_900"] = round(r["gbps"] / NVLINK_NOMINAL_GBS, 4)

@@ -206,7 +206,8 @@ _KNOBS = {"SRFLOW_CTAS_PER_SM": 0, "SRFLOW_COPY_THREADS": 1, "SRFLOW_PUT_IMPL": 
           "SRFLOW_PEER_CE_KIB": 6, "SRFLOW_FORCE_SYS": 7, "SRFLOW_PUT_TIMEOUT_MS": 8,
           "SRFLOW_EDGE_CTAS_PER_SM": 9, "SRFLOW_EDGE_CHUNK_KIB": 10,
           "SRFLOW_CONSUME_THREADS": 11, "SRFLOW_GEN_UNIT_KIB": 12,
-          "SRFLOW_CONSUME_RELEASE": 13, "SRFLOW_EDGE_CTAS": 14}
+          "SRFLOW_CONSUME_RELEASE": 13, "SRFLOW_EDGE_CTAS": 14,
+          "SRFLOW_PULL_NO_PREFETCH": 16}
 
 
 def _apply_env_knobs(lib) -> None:
@@ -225,7 +226,8 @@ def tune(knob: str, value: int) -> None:
                       "peer_ce_kib": 6, "force_sys": 7, "put_timeout_ms": 8,
                       "edge_ctas_per_sm": 9, "edge_chunk_kib": 10,
                       "consume_threads": 11, "gen_unit_kib": 12,
-                      "consume_release": 13, "edge_ctas": 14}[knob], value)
+                      "consume_release": 13, "edge_ctas": 14,
+                      "pull_no_prefetch": 16}[knob], value)
 
 
 def last_error() -> str:

@@ -76,6 +76,9 @@ int srf_tune(int knob, int value) {
     case 13:
       g_consume_release = value ? 1 : 0;
       return SRF_OK;
+    case 16:
+      g_pull_no_prefetch = value ? 1 : 0;
+      return SRF_OK;
     case 14:
       if (value < 0 || value > 4096) return fail(SRF_E_INVALID_CONFIG, "edge_ctas 0..4096");
       g_edge_ctas = value;

@@ -8,6 +8,7 @@ struct srf_edge {
   uint64_t next_round;
   int ctas;
   int pull = 0;            // 1: a pull edge (k_pull_stream on the receiver's GPU)
+  int pre = 0;             // 1: few slots - k_pull_stream_pre stages chunks early
 };
 
 
@@ -149,15 +150,22 @@ int srf_edge_create_pull(srf_space_t src_space, uint64_t src_addr, uint64_t src_
   const bool aligned = ((uintptr_t)e->a.src % 16 == 0) && ((uintptr_t)e->a.dst % 16 == 0) &&
                        (nsrc == 1 || src_stride % 16 == 0) && slot_stride % 16 == 0;
   e->a.tma = (tma && aligned) ? 1 : 0;
+  // one or two slots: stage the next round's chunks before the slot is free
+  // (k_pull_stream_pre; chunks fit the 6 x 16 KiB stages)
+  e->pre = (e->a.tma && slots <= 2 && !g_pull_no_prefetch) ? 1 : 0;
   const int sms = sm_count_of(e->device);
   // TMA: one CTA per SM keeps 6 x 16 KiB loads in flight from one issuing
   // thread; SM loads: the push edge's geometry
   e->ctas = g_edge_ctas ? g_edge_ctas
                         : std::max(1, e->a.tma ? sms - 1 : sms * g_edge_ctas_per_sm);
   uint64_t chunk = g_edge_chunk ? (g_edge_chunk << 10)
-                                : std::min<uint64_t>(256 << 10,
-                                                     std::max<uint64_t>(64 << 10, nbytes / 16));
+                  : e->pre ? std::min<uint64_t>(64 << 10, std::max<uint64_t>(16 << 10,
+                                                                             nbytes / 128))
+                           : std::min<uint64_t>(256 << 10,
+                                                std::max<uint64_t>(64 << 10, nbytes / 16));
   chunk = (chunk + 4095) & ~4095ull;
+  if (e->pre && chunk > (uint64_t)kBulkChunk * kBulkStages)
+    chunk = (uint64_t)kBulkChunk * kBulkStages;
   if (chunk > nbytes) chunk = nbytes;
   e->a.chunk = chunk;
   e->a.nchunks = (uint32_t)((nbytes + chunk - 1) / chunk);
@@ -207,9 +215,14 @@ int srf_edge_recv(srf_edge_t e, uint32_t rounds, srf_stream_t st, srf_space_t ds
     if (e->device >= 0 && e->device < 64 && !attr_set[e->device]) {
       CUDA_TRY(cudaFuncSetAttribute(k_pull_stream<true>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem));
+      CUDA_TRY(cudaFuncSetAttribute(k_pull_stream_pre,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kBulkSmem));
       attr_set[e->device] = true;
     }
-    k_pull_stream<true><<<grid, 256, kBulkSmem, s->s>>>(a);
+    if (e->pre)
+      k_pull_stream_pre<<<grid, 256, kBulkSmem, s->s>>>(a);
+    else
+      k_pull_stream<true><<<grid, 256, kBulkSmem, s->s>>>(a);
   } else {
     k_pull_stream<false><<<grid, 512, 0, s->s>>>(a);
   }

@@ -352,6 +352,103 @@ __global__ void __launch_bounds__(512) k_pull_stream(const __grid_constant__ Str
   }
 }
 
+// Few-slot pull edges (the reference's ONE region per edge, or two):
+// k_pull_stream_pre stages an item's whole chunk (<= kBulkStages x 16 KiB) in
+// shared memory as soon as its round is posted, and stores it into the slot
+// only once the slot is free.  With one slot the next round's NVLink reads
+// then overlap the consumer's poll of this round instead of starting after
+// its clear - the round-trip latency is what caps a single region.
+__global__ void __launch_bounds__(256) k_pull_stream_pre(const __grid_constant__ StreamEdgeArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint32_t s_i;
+  __shared__ int s_last;
+  uint64_t *bars = (uint64_t *)(smem + kBulkChunk * kBulkStages);
+  uint32_t uses[kBulkStages];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kBulkStages; ++i) {
+      mbar_init(&bars[i], 1);
+      uses[i] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const uint32_t total = a.rounds * a.nchunks;
+  for (;;) {
+    if (threadIdx.x == 0) s_i = atomicAdd(a.claim, 1u);
+    __syncthreads();
+    const uint32_t i = s_i;
+    __syncthreads();
+    if (i >= total) break;
+    const uint32_t jr = i / a.nchunks;
+    const uint32_t c = i - jr * a.nchunks;
+    const uint64_t j = a.first_round + jr;
+    const uint32_t slot = (uint32_t)(j % a.slots);
+    const uint32_t m = (uint32_t)(j / a.slots);
+    uint8_t *d = a.dst + (uint64_t)slot * a.slot_stride;
+    const uint64_t off = (uint64_t)c * a.chunk;
+    const uint64_t n = a.nbytes - off < a.chunk ? a.nbytes - off : a.chunk;
+    const uint8_t *src = a.src + (j % a.nsrc) * a.src_stride + off;
+    const uint64_t mid = n & ~15ull;
+    const uint32_t np = (uint32_t)((mid + kBulkChunk - 1) / kBulkChunk);
+    uint32_t issued = 0;   // (thread 0) stages whose loads are in flight
+    if (threadIdx.x == 0 && *(volatile int *)a.err == 0) {
+      const uint64_t t0 = globaltimer_ns();
+      while (ld_acquire_sys_u64(a.posted) < j + 1) {
+        if (globaltimer_ns() - t0 > a.timeout_ns) {
+          atomicExch(a.err, 2);
+          break;
+        }
+        __nanosleep(32);
+      }
+      // stage the chunk now ...
+      if (*(volatile int *)a.err == 0)
+        for (uint32_t p = 0; p < np; ++p, ++issued) {
+          const uint32_t b = (uint32_t)((mid - (uint64_t)p * kBulkChunk) < kBulkChunk
+                                            ? mid - (uint64_t)p * kBulkChunk : kBulkChunk);
+          mbar_expect_tx(&bars[p], b);
+          bulk_g2s(smem + p * kBulkChunk, src + (uint64_t)p * kBulkChunk, b, &bars[p]);
+        }
+      // ... and wait for the slot only before writing it
+      wait_count(a.released + slot, m, a.timeout_ns, a.err);
+      if (m > 0 && !spin_until(d + a.nbytes, 0, a.timeout_ns, 0)) atomicExch(a.err, 2);
+    }
+    __syncthreads();
+    const bool ok = *(volatile int *)a.err == 0;
+    if (threadIdx.x == 0) {
+      for (uint32_t p = 0; p < issued; ++p) {
+        mbar_wait(&bars[p], uses[p] & 1);   // (issued loads complete either way)
+        ++uses[p];
+        if (ok) {
+          const uint32_t b = (uint32_t)((mid - (uint64_t)p * kBulkChunk) < kBulkChunk
+                                            ? mid - (uint64_t)p * kBulkChunk : kBulkChunk);
+          bulk_s2g(d + off + (uint64_t)p * kBulkChunk, smem + p * kBulkChunk, b);
+        }
+      }
+      bulk_wait_all();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    if (ok)
+      for (uint64_t k = mid + threadIdx.x; k < n; k += blockDim.x) d[off + k] = ld_byte<true>(src + k);
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = grid_arrive(a.arrival + slot, a.nchunks - 1, 0);
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      atomicExch(a.arrival + slot, 0u);
+      if (*(volatile int *)a.err == 0) release_tail(d + a.nbytes, 1, 0);
+      count_done(a.released + slot);
+      if (a.pulled) {
+        const unsigned v = (unsigned)(j / a.nsrc) + 1;
+        asm volatile("red.release.sys.global.max.u32 [%0], %1;" ::"l"(a.pulled + j % a.nsrc),
+                     "r"(v)
+                     : "memory");
+      }
+    }
+  }
+  if (threadIdx.x == 0 && atomicAdd(a.exit_count, 1u) == gridDim.x - 1) {
+    *a.claim = 0;
+    *a.exit_count = 0;
+  }
+}
+
 // Sender side of a pull edge: publish "rounds [.., count) are posted" into
 // the receiver's word (one posted store, system-scope release: the payload
 // writes that preceded it on this stream are visible to the receiver's

@@ -85,6 +85,7 @@ static int g_edge_ctas = 0;          // knob 14: pipelined edge CTAs in total (0
 static uint64_t g_edge_chunk = 0;    // knob 10: pipelined edge chunk (KiB; 0 = automatic)
 static int g_consume_threads = 32;   // knob 11: flag-only edge consumer CTA size
 static int g_consume_release = 0;    // knob 13: flag-only consumer clears with release.sys
+static int g_pull_no_prefetch = 0;   // knob 16: few-slot pull edges without early staging
 // knob 12: GenGrad work-unit size.  A unit's thread 0 derives the PCG64 stream
 // and jumps to the unit's first element (~150 dependent 128-bit multiplies)
 // before the CTA generates, so units must be large enough to amortise that.

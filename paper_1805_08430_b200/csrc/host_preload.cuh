@@ -38,7 +38,8 @@ static int preload_kernels(int device) {
       (const void *)k_put_ind<4, true>, (const void *)k_put_inline_ind, (const void *)k_gen_ind,
       (const void *)k_apply_ind<true>, (const void *)k_apply_ind<false>,
       (const void *)k_set_replay, (const void *)k_dyn_send_stream,
-      (const void *)k_dyn_pull_stream, (const void *)k_dyn_consume_stream};
+      (const void *)k_dyn_pull_stream, (const void *)k_dyn_consume_stream,
+      (const void *)k_pull_stream_pre};
   for (const void *k : kernels) {
     cudaFuncAttributes attr;
     cudaError_t e = cudaFuncGetAttributes(&attr, k);

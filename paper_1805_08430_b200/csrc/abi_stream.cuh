@@ -685,10 +685,16 @@ int srf_oplist_replay(srf_oplist_t l, uint64_t first_offset, uint32_t count, srf
     int rc = rec_build_graph(l);
     if (rc) return rc;
   }
+  if (!l->done) CUDA_TRY(cudaEventCreateWithFlags(&l->done, cudaEventDisableTiming));
   for (uint32_t i = 0; i < count; ++i) {
+    // relaunch an exec only after its previous launch finished: relaunching
+    // one still in flight stalled the host ~3.5 ms per launch (host_record.cuh,
+    // replay set); with a period of p phases the host stays p launches ahead
+    CUDA_TRY(cudaEventSynchronize(l->done));
     k_set_u64<<<1, 1, 0, st->s>>>(l->iter_add, first_offset + i);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaGraphLaunch(l->exec, st->s));
+    CUDA_TRY(cudaEventRecord(l->done, st->s));
   }
   g_launches.fetch_add((uint64_t)count * (l->ops.size() + 1), std::memory_order_relaxed);
   return SRF_OK;

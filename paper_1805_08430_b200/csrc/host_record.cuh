@@ -74,8 +74,10 @@ struct srf_oplist {
   unsigned int *priv = nullptr;  // private arrival counters / reduction scratch
   int graph_device = -1;
   uint32_t nodes = 0, edges = 0;
+  cudaEvent_t done = nullptr;    // after the exec's latest launch
   ~srf_oplist() {
     for (RecOp &op : ops) delete op.inl;
+    if (done) cudaEventDestroy(done);
     if (exec) cudaGraphExecDestroy(exec);
     if (iter_add) cudaFree(iter_add);
     if (priv) cudaFree(priv);

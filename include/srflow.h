@@ -424,6 +424,13 @@ int srf_matmul(int elem, uint64_t a_ptr, uint64_t b_ptr, uint64_t c_ptr, uint64_
 int srf_compute(srf_space_t space, int kind, int elem, uint64_t a_addr, uint64_t b_addr,
                 uint64_t out_addr, uint64_t m, uint64_t k, uint64_t n, srf_stream_t stream);
 
+/* ConcatDyn (graph.py compute_node): the n_in inputs (space addresses, byte
+ * lengths; 1..8 of them, not all empty) concatenated and repeated to fill
+ * out_len bytes at out_addr, on the device. */
+int srf_concat_tile(srf_space_t space, int n_in, const uint64_t *in_addr,
+                    const uint64_t *in_len, uint64_t out_addr, uint64_t out_len,
+                    srf_stream_t stream);
+
 /* ReduceMax consumer of the microbenchmark (graph.py:378-382) on the
  * receiving GPU: out_addr receives max over n fp32 at in_addr. */
 int srf_reduce_max_f32(srf_space_t space, uint64_t in_addr, uint64_t n,

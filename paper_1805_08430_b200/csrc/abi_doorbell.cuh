@@ -266,6 +266,42 @@ int srf_compute(srf_space_t sp, int kind, int elem, uint64_t a_addr, uint64_t b_
   return launch_check(kind == 1 ? "k_add" : "k_sigmoid");
 }
 
+// ConcatDyn into the output block: the n_in inputs (space addresses and byte
+// lengths, total > 0) concatenated and repeated to out_len bytes
+int srf_concat_tile(srf_space_t sp, int n_in, const uint64_t *in_addr, const uint64_t *in_len,
+                    uint64_t out_addr, uint64_t out_len, srf_stream_t st) {
+  DeviceGuard device_guard;
+  if (n_in < 1 || n_in > kConcatMax)
+    return fail(SRF_E_INVALID_CONFIG, "concat of 1..%d inputs", kConcatMax);
+  ConcatArgs a;
+  memset(&a, 0, sizeof a);
+  bool words = out_addr % 4 == 0 && out_len % 4 == 0;
+  for (int i = 0; i < n_in; ++i) {
+    int rc = check_raw(sp, in_addr[i], in_len[i], "concat input");
+    if (rc) return rc;
+    a.src[i] = sp->base + in_addr[i];
+    a.len[i] = in_len[i];
+    a.total += in_len[i];
+    words = words && in_addr[i] % 4 == 0 && in_len[i] % 4 == 0;
+  }
+  if (a.total == 0) return fail(SRF_E_INVALID_LENGTH, "concat of empty inputs");
+  int rc = check_raw(sp, out_addr, out_len, "concat output");
+  if (rc) return rc;
+  if (out_len == 0) return SRF_OK;
+  a.nsrc = n_in;
+  a.out = sp->base + out_addr;
+  a.out_len = out_len;
+  a.unit = words ? 4 : 1;
+  srf_stream *s = stream_or_default(sp, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  const uint64_t n = out_len / a.unit;
+  const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count_of(s->device) * 8);
+  k_concat_tile<<<grid, 256, 0, s->s>>>(a);
+  // (not recorded: a dynamic shape never repeats, launch_check marks any
+  // active recording unusable)
+  return launch_check("k_concat_tile");
+}
+
 int srf_timing_event_create(srf_space_t sp, srf_event_t *out) {
   DeviceGuard device_guard;
   CUDA_TRY(cudaSetDevice(sp->device));

@@ -253,3 +253,33 @@ __global__ void __launch_bounds__(256) k_sigmoid(const T *x, T *out, uint64_t n)
     out[i] = (T)(1.0 / (1.0 + exp(-v)));
   }
 }
+
+// ConcatDyn (graph.py compute_node CONCAT_DYN): the inputs' elements
+// concatenated in order (they share trailing dims, so concatenating along
+// dim 0 is concatenating their flat storage), repeated to fill the output:
+// out[i] = cat[i % total].  Words of `unit` bytes (4 when every length and
+// address allows it, else 1).
+static constexpr int kConcatMax = 8;
+struct ConcatArgs {
+  const uint8_t *src[kConcatMax];
+  uint64_t len[kConcatMax];   // bytes
+  int nsrc;
+  uint64_t total;             // bytes of the concatenation (> 0)
+  uint8_t *out;
+  uint64_t out_len;           // bytes
+  int unit;
+};
+
+__global__ void __launch_bounds__(256) k_concat_tile(const __grid_constant__ ConcatArgs a) {
+  const uint64_t nth = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t words = a.out_len / a.unit;
+  for (uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += nth) {
+    uint64_t b = (w * a.unit) % a.total;
+    int k = 0;
+    while (k + 1 < a.nsrc && b >= a.len[k]) b -= a.len[k++];
+    if (a.unit == 4)
+      *(uint32_t *)(a.out + w * 4) = *(const uint32_t *)(a.src[k] + b);
+    else
+      a.out[w] = a.src[k][b];
+  }
+}

@@ -39,7 +39,7 @@ static int preload_kernels(int device) {
       (const void *)k_apply_ind<true>, (const void *)k_apply_ind<false>,
       (const void *)k_set_replay, (const void *)k_dyn_send_stream,
       (const void *)k_dyn_pull_stream, (const void *)k_dyn_consume_stream,
-      (const void *)k_pull_stream_pre};
+      (const void *)k_pull_stream_pre, (const void *)k_concat_tile};
   for (const void *k : kernels) {
     cudaFuncAttributes attr;
     cudaError_t e = cudaFuncGetAttributes(&attr, k);

@@ -119,3 +119,43 @@ def test_forward_values_oracle_matches_session():
             got = np.frombuffer(raw, np.float32)
             np.testing.assert_allclose(got, want[e].reshape(-1), rtol=1e-5, atol=1e-6)
     s.close()
+
+
+@pytest.mark.parametrize("elem", [ElemType.F32, ElemType.F64, ElemType.I32, ElemType.U8])
+def test_concat_dyn_is_a_library_kernel_equal_to_numpy(elem):
+    """ConcatDyn (srf_concat_tile): dim 0 drawn from the node's stream, the
+    inputs concatenated and repeated - byte-identical to compute_node's numpy
+    restatement on the captured inputs, for every element type, with inputs
+    of different lengths and an output longer and shorter than their sum."""
+    from paper_1805_08430_b200 import _lib
+    from paper_1805_08430_b200.graph import node_rng
+    g = DataFlowGraph()
+    a = g.input(shape_of(3, 5), elem)
+    b = g.input(shape_of(7, 5), elem)
+    c = g.concat_dyn([a, b], dyn_range=(1, 30))
+    g.reduce_max(c)
+    g.freeze()
+    # sources on server 0, the concat on 1, its consumer on 2: every edge captured
+    side = {NodeKind.CONCAT_DYN: 1, NodeKind.REDUCE_MAX: 2}
+    placement = {nid: side.get(n.kind, 0) for nid, n in g.nodes.items()}
+    s = Session(g, placement, seed=5, capture_edges=True, replay=False)
+    launches = _lib.launch_count()
+    rep = s.run(6)
+    assert _lib.launch_count() > launches
+    node = next(n for n in g.nodes.values() if n.kind is NodeKind.CONCAT_DYN)
+    seen = {(it, e): raw for (it, e, _s), raw in rep.captured.items()}
+    dt = elem.np_dtype
+    lens = set()
+    for it in range(1, 7):
+        ins = [np.frombuffer(seen[(it, e)], dt).reshape(-1, 5) for e in node.inputs]
+        # numpy restatement of compute_node's ConcatDyn (graph.py:363-389)
+        rng = node_rng(5, node.node_id, it)
+        lo, hi = node.dyn_range
+        dim0 = int(rng.integers(lo, hi + 1))
+        flat = np.concatenate(ins, axis=0).reshape(-1)
+        want = np.tile(flat, -(-dim0 * 5 // flat.size))[:dim0 * 5]
+        got = np.frombuffer(seen[(it, node.output)], dt)
+        assert got.tobytes() == want.tobytes(), it
+        lens.add(got.size)
+    assert len(lens) > 1            # dim 0 varied across iterations
+    s.close()

@@ -94,8 +94,8 @@ def test_replayed_ps_variables_equal_the_oracle():
 
 
 def test_torch_compute_kinds_are_not_replayed():
-    """ConcatDyn runs as torch ops, which the recorder does not see, so such
-    sessions keep the host path."""
+    """ConcatDyn draws its output's dim 0 per iteration (a dynamic shape never
+    repeats), so sessions with it keep the host path."""
     from paper_1805_08430_b200.graph import DataFlowGraph, shape_of
     g = DataFlowGraph()
     g.reduce_max(g.concat_dyn([g.gen_grad(shape_of(3, 4))], dyn_range=(1, 6)))

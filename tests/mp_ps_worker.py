@@ -41,11 +41,17 @@ def main() -> int:
     ]
     bad = 0
     for name, shapes, W, P, coloc, *kw in layouts:
-        for schedule in (("phases",) if one_gpu else ("phases", "exchange", "exchange_x3")):
+        scheds = (("phases", "phases_fused") if one_gpu else
+                  ("phases", "phases_fused", "exchange", "exchange_fused", "exchange_x3",
+                   "exchange_x3_fused"))
+        for schedule in scheds:
             L = PsLayout(shapes, W, P, coloc, **(kw[0] if kw else {}))
+            # *_fused: the next weights forwarded by the apply (into the peer's
+            # weight region over the IPC mapping), no weight push batch
             ps = PsStep(L, rank=rank, world=world, device=local, seed=5, op="sgd", lr=0.02,
-                        schedule="phases" if schedule == "phases" else "exchange")
-            if schedule == "exchange_x3":  # 3 iterations per launch: 1-3, 4-6, 7-8
+                        schedule="phases" if schedule.startswith("phases") else "exchange",
+                        fuse_push=schedule.endswith("_fused"))
+            if schedule.startswith("exchange_x3"):  # 3 iterations per launch: 1-3, 4-6, 7-8
                 ps.run_exchange(1, 8, per_launch=3)
             else:
                 for it in range(1, 9):

@@ -137,7 +137,13 @@ int srf_batch_gen_create(int n, srf_space_t const *space, const uint64_t *grad_a
                    ? nullptr : credit_space[i]->base + credit_addr[i];
     d.node = node_id[i];
     d.cta_begin = next;
-    d.cta_count = ctas_for(device, nbytes[i], g_gen_unit_bytes);
+    // gradients of >= 64 MiB (VGG-16's fc6/fc7) in >= 512 KiB units: fewer
+    // per-unit stream derivations (~150 dependent 128-bit multiplies each);
+    // smaller tensors keep finer units for overlap (profiles/r2_gen_unit_sweep.jsonl)
+    const uint64_t unit = nbytes[i] >= (64ull << 20)
+                              ? std::max<uint64_t>(g_gen_unit_bytes, 512 << 10)
+                              : g_gen_unit_bytes;
+    d.cta_count = ctas_for(device, nbytes[i], unit);
     next += d.cta_count;
   }
   int rc = finish_batch(1, device, host, space[0]->err, out);

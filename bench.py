@@ -1559,6 +1559,7 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         it += n
 
     times = {}
+    default_cfg = ps._exchange_cfg
     for name in ("phases", "exchange"):
         ps.use_schedule(name)
         eager(2)
@@ -1582,7 +1583,23 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         ps.fuse_push = False
         ps.use_schedule("phases")
         eager(1)      # consumes the forwarded weights, pushes nothing
+    if world > 1 and min(times, key=times.get) == "exchange_multi_fused_push":
+        # the apply lag / unit order of the exchange queue, one alternative
+        # (index order, lag 6: VGG-16 N=2 +1.5 %, profiles/r2_ps_lag_order_n2.jsonl)
+        ps.fuse_push = True
+        ps.set_exchange_config(6, "index")
+        multi(2)
+        t_alt = sample(multi)
+        if t_alt < times["exchange_multi_fused_push"]:
+            times["exchange_multi_fused_push_index_lag6"] = t_alt
+        else:
+            ps.set_exchange_config(*default_cfg)
+        ps.fuse_push = False
+        ps.use_schedule("phases")
+        eager(1)      # consumes the forwarded weights, pushes nothing
     best = min(times, key=times.get)
+    if best == "exchange_multi_fused_push_index_lag6":
+        best = "exchange_multi_fused_push"
     fused = best.endswith("_fused_push")
     base = best[:-len("_fused_push")] if fused else best
     persistent = base == "persistent"

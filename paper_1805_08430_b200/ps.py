@@ -615,6 +615,20 @@ class PsStep:
             self._exchange = None
         self.schedule = schedule
 
+    def set_exchange_config(self, lag: int, order: str) -> None:
+        """Rebuild the exchange schedules with another apply lag / unit order
+        (the next exchange launch builds them; the phase schedule is
+        unaffected).  Call between steps."""
+        self.sync()
+        for x in (self._exchange_built, self._exchange_nopush):
+            if x is not None:
+                _lib.call("srf_ps_exchange_destroy", x)
+        was = self.schedule
+        self._exchange = self._exchange_built = self._exchange_nopush = None
+        self._exchange_cfg = (int(lag), order)
+        if was == "exchange":
+            self.use_schedule("exchange")
+
     def _exchange_for_launch(self) -> tuple:
         """(exchange object, mode bits) for the next exchange launch, and
         whether this rank must first push (the fused schedule's prologue).

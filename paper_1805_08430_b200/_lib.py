@@ -141,6 +141,7 @@ SIGNATURES = {
                                    u64, vp, vp]),
     "srf_reduce_max_f32": (C.c_int, [vp, u64, u64, u64, vp]),
     "srf_concat_tile": (C.c_int, [vp, C.c_int, P(u64), P(u64), u64, u64, vp]),
+    "srf_add_bcast": (C.c_int, [vp, C.c_int, u64, P(u64), u64, P(u64), C.c_int, u64, vp]),
     "srf_gen_reference": (C.c_int, [vp, u64, u64, u64, u64, u64, u64, vp, P(vp)]),
     "srf_edge_create": (C.c_int, [vp, u64, u64, u64, C.c_uint32, u64, vp, u64, u64, C.c_uint32,
                                   u64, u64, P(vp)]),

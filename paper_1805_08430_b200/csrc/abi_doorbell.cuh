@@ -266,6 +266,55 @@ int srf_compute(srf_space_t sp, int kind, int elem, uint64_t a_addr, uint64_t b_
   return launch_check(kind == 1 ? "k_add" : "k_sigmoid");
 }
 
+// Add with numpy broadcasting: a[a_dims] + b[b_dims] (equal rank <= 8, every
+// dimension pair equal or one of them 1) into out (the broadcast shape)
+int srf_add_bcast(srf_space_t sp, int elem, uint64_t a_addr, const uint64_t *a_dims,
+                  uint64_t b_addr, const uint64_t *b_dims, int rank, uint64_t out_addr,
+                  srf_stream_t st) {
+  DeviceGuard device_guard;
+  if (elem < 0 || elem > 4) return fail(SRF_E_INVALID_CONFIG, "unknown element type %d", elem);
+  if (rank < 1 || rank > 8) return fail(SRF_E_INVALID_CONFIG, "broadcast rank 1..8");
+  const uint64_t es = elem == 0 || elem == 2 ? 4 : elem == 4 ? 1 : 8;
+  BcastArgs g;
+  memset(&g, 0, sizeof g);
+  g.rank = rank;
+  uint64_t na = 1, nb = 1, n = 1;
+  for (int k = 0; k < rank; ++k) {
+    const uint64_t x = a_dims[k], y = b_dims[k];
+    if (x != y && x != 1 && y != 1)
+      return fail(SRF_E_SHAPE_MISMATCH, "operands not broadcastable in dimension %d", k);
+    g.dims[k] = x == 1 ? y : x;
+    na *= x;
+    nb *= y;
+    n *= g.dims[k];
+  }
+  uint64_t ra = 1, rb = 1;  // row-major element strides, 0 where broadcast
+  for (int k = rank - 1; k >= 0; --k) {
+    g.sa[k] = (a_dims[k] == 1 && g.dims[k] != 1) ? 0 : ra;
+    g.sb[k] = (b_dims[k] == 1 && g.dims[k] != 1) ? 0 : rb;
+    ra *= a_dims[k];
+    rb *= b_dims[k];
+  }
+  int rc = check_raw(sp, a_addr, es * na, "operand");
+  if (!rc) rc = check_raw(sp, b_addr, es * nb, "operand");
+  if (!rc) rc = check_raw(sp, out_addr, es * n, "result");
+  if (rc) return rc;
+  if (n == 0) return SRF_OK;
+  srf_stream *s = stream_or_default(sp, st);
+  CUDA_TRY(cudaSetDevice(s->device));
+  const int grid = (int)std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count_of(s->device) * 8);
+  const void *a = sp->base + a_addr, *b = sp->base + b_addr;
+  void *o = sp->base + out_addr;
+  switch (elem) {
+    case 0: k_add_bcast<float><<<grid, 256, 0, s->s>>>((const float *)a, (const float *)b, (float *)o, n, g); break;
+    case 1: k_add_bcast<double><<<grid, 256, 0, s->s>>>((const double *)a, (const double *)b, (double *)o, n, g); break;
+    case 2: k_add_bcast<int32_t><<<grid, 256, 0, s->s>>>((const int32_t *)a, (const int32_t *)b, (int32_t *)o, n, g); break;
+    case 3: k_add_bcast<int64_t><<<grid, 256, 0, s->s>>>((const int64_t *)a, (const int64_t *)b, (int64_t *)o, n, g); break;
+    default: k_add_bcast<uint8_t><<<grid, 256, 0, s->s>>>((const uint8_t *)a, (const uint8_t *)b, (uint8_t *)o, n, g); break;
+  }
+  return launch_check("k_add_bcast");
+}
+
 // ConcatDyn into the output block: the n_in inputs (space addresses and byte
 // lengths, total > 0) concatenated and repeated to out_len bytes
 int srf_concat_tile(srf_space_t sp, int n_in, const uint64_t *in_addr, const uint64_t *in_len,

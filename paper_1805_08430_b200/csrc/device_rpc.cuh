@@ -245,6 +245,30 @@ __global__ void __launch_bounds__(256) k_add(const T *a, const T *b, T *out, uin
     out[i] = ew_add<T>(a[i], b[i]);
 }
 
+// Add with numpy broadcasting (operands of equal rank; a dimension of 1
+// against a larger one repeats): element i of the output at coordinates c
+// reads a[sum c_k * sa_k] and b[sum c_k * sb_k], strides 0 where broadcast
+struct BcastArgs {
+  int rank;
+  uint64_t dims[8], sa[8], sb[8];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_add_bcast(const T *a, const T *b, T *out, uint64_t n,
+                                                   const __grid_constant__ BcastArgs g) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t rem = i, oa = 0, ob = 0;
+    for (int k = g.rank - 1; k >= 0; --k) {
+      const uint64_t c = rem % g.dims[k];
+      rem /= g.dims[k];
+      oa += c * g.sa[k];
+      ob += c * g.sb[k];
+    }
+    out[i] = ew_add<T>(a[oa], b[ob]);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) k_sigmoid(const T *x, T *out, uint64_t n) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;

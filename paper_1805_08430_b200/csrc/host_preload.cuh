@@ -39,7 +39,10 @@ static int preload_kernels(int device) {
       (const void *)k_apply_ind<true>, (const void *)k_apply_ind<false>,
       (const void *)k_set_replay, (const void *)k_dyn_send_stream,
       (const void *)k_dyn_pull_stream, (const void *)k_dyn_consume_stream,
-      (const void *)k_pull_stream_pre, (const void *)k_concat_tile};
+      (const void *)k_pull_stream_pre, (const void *)k_concat_tile,
+      (const void *)k_add_bcast<float>, (const void *)k_add_bcast<double>,
+      (const void *)k_add_bcast<int32_t>, (const void *)k_add_bcast<int64_t>,
+      (const void *)k_add_bcast<uint8_t>};
   for (const void *k : kernels) {
     cudaFuncAttributes attr;
     cudaError_t e = cudaFuncGetAttributes(&attr, k);

@@ -159,3 +159,40 @@ def test_concat_dyn_is_a_library_kernel_equal_to_numpy(elem):
         lens.add(got.size)
     assert len(lens) > 1            # dim 0 varied across iterations
     s.close()
+
+
+@pytest.mark.parametrize("elem", [ElemType.F32, ElemType.F64, ElemType.I32, ElemType.I64,
+                                  ElemType.U8])
+@pytest.mark.parametrize("sa,sb", [((3, 4), (1, 4)), ((5, 1, 3), (1, 2, 3)), ((7,), (1,)),
+                                   ((1, 1), (4, 6))])
+def test_broadcasting_add_equals_numpy(elem, sa, sb):
+    """srf_add_bcast (Add with numpy broadcasting): bit-exact against numpy
+    a + b (IEEE add, wrapping integers)."""
+    from paper_1805_08430_b200 import _lib
+    from paper_1805_08430_b200.memspace import MemorySpace
+    rng = np.random.default_rng(len(sa) * 31 + len(sb))
+    dt = elem.np_dtype
+    if elem in (ElemType.F32, ElemType.F64):
+        a = rng.standard_normal(sa).astype(dt)
+        b = rng.standard_normal(sb).astype(dt)
+    else:
+        info = np.iinfo(dt)
+        a = rng.integers(info.min, info.max, sa, dtype=dt, endpoint=True)
+        b = rng.integers(info.min, info.max, sb, dtype=dt, endpoint=True)
+    with np.errstate(over="ignore"):
+        want = a + b
+    sp = MemorySpace(0, 1 << 20, device=0)
+    ra = sp.allocate_region(1024)
+    rb = sp.allocate_region(1024)
+    ro = sp.allocate_region(4096)
+    sp.write_raw(ra.base_addr, a.tobytes())
+    sp.write_raw(rb.base_addr, b.tobytes())
+    _lib.call("srf_add_bcast", sp.handle, int(elem), ra.base_addr, _lib.u64_array(sa),
+              rb.base_addr, _lib.u64_array(sb), len(sa), ro.base_addr, None)
+    sp.sync()
+    got = np.frombuffer(sp.read_raw(ro.base_addr, want.nbytes), dt).reshape(want.shape)
+    assert got.tobytes() == want.tobytes()
+    with pytest.raises(Exception):
+        _lib.call("srf_add_bcast", sp.handle, int(elem), ra.base_addr, _lib.u64_array((3, 4)),
+                  rb.base_addr, _lib.u64_array((2, 4)), 2, ro.base_addr, None)
+    sp.close()

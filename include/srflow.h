@@ -424,14 +424,14 @@ int srf_matmul(int elem, uint64_t a_ptr, uint64_t b_ptr, uint64_t c_ptr, uint64_
 int srf_compute(srf_space_t space, int kind, int elem, uint64_t a_addr, uint64_t b_addr,
                 uint64_t out_addr, uint64_t m, uint64_t k, uint64_t n, srf_stream_t stream);
 
-/* Add with numpy broadcasting (graph.py compute_node ADD): a[a_dims] +
+/* Add with numpy broadcasting (graph.py:373-374, compute_node ADD): a[a_dims] +
  * b[b_dims], equal rank <= 8, each dimension pair equal or one of them 1;
  * the result has the broadcast shape. */
 int srf_add_bcast(srf_space_t space, int elem, uint64_t a_addr, const uint64_t *a_dims,
                   uint64_t b_addr, const uint64_t *b_dims, int rank, uint64_t out_addr,
                   srf_stream_t stream);
 
-/* ConcatDyn (graph.py compute_node): the n_in inputs (space addresses, byte
+/* ConcatDyn (graph.py:383-389, compute_node): the n_in inputs (space addresses, byte
  * lengths; 1..8 of them, not all empty) concatenated and repeated to fill
  * out_len bytes at out_addr, on the device. */
 int srf_concat_tile(srf_space_t space, int n_in, const uint64_t *in_addr,

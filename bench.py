@@ -1583,7 +1583,7 @@ def bench_ps(rank, world, device, steps, warmup, op="sgd", shapes=None, cpu=True
         ps.fuse_push = False
         ps.use_schedule("phases")
         eager(1)      # consumes the forwarded weights, pushes nothing
-    if world > 1 and min(times, key=times.get) == "exchange_multi_fused_push":
+    if min(times, key=times.get) == "exchange_multi_fused_push":
         # the apply lag / unit order of the exchange queue, one alternative
         # (index order, lag 6: VGG-16 N=2 +1.5 %, profiles/r2_ps_lag_order_n2.jsonl)
         ps.fuse_push = True

@@ -183,6 +183,31 @@ __global__ void __launch_bounds__(1024) k_consume_stream(uint8_t *slots_base, ui
     *(volatile uint32_t *)started = ticket;
     __threadfence_system();
   }
+  if (!(mode & 1)) {
+    // flag-only: lane 0 of warp w consumes the slots s with s % W == w, each
+    // slot's rounds in order - W slots' polls and clears proceed at once (one
+    // thread walking every round capped small rounds at ~0.5 us each); a
+    // slot stays on one warp, so a flag read 1 is always that round's
+    const uint32_t W = blockDim.x / 32, w = threadIdx.x / 32;
+    if (threadIdx.x % 32 != 0) return;
+    for (uint32_t r = 0; r < rounds; ++r) {
+      const uint64_t j = first_round + r;
+      const uint32_t slot = (uint32_t)(j % slots);
+      if (slot % W != w) continue;
+      uint8_t *d = slots_base + (uint64_t)slot * slot_stride;
+      if (!spin_until(d + nbytes, 1, timeout_ns, 1)) {
+        atomicExch(err, 1);
+        return;
+      }
+      if (mode == 2) release_tail(d + nbytes, 0, 1);
+      else st_relaxed_sys_u8(d + nbytes, 0);
+      if (credit_mirror) {
+        if (mode == 2) st_release_sys_u32(credit_mirror + slot, (unsigned)(j / slots) + 1);
+        else st_relaxed_sys_u32(credit_mirror + slot, (unsigned)(j / slots) + 1);
+      }
+    }
+    return;
+  }
   for (uint32_t r = 0; r < rounds; ++r) {
     const uint64_t j = first_round + r;
     uint8_t *d = slots_base + (j % slots) * slot_stride;

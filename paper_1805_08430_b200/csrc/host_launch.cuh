@@ -83,7 +83,7 @@ static uint64_t g_put_timeout_ns = 5000000000ull;  // knob 8: credit wait limit 
 static int g_edge_ctas_per_sm = 2;   // knob 9: pipelined edge CTAs per SM
 static int g_edge_ctas = 0;          // knob 14: pipelined edge CTAs in total (0: per-SM knob)
 static uint64_t g_edge_chunk = 0;    // knob 10: pipelined edge chunk (KiB; 0 = automatic)
-static int g_consume_threads = 32;   // knob 11: flag-only edge consumer CTA size
+static int g_consume_threads = 256;  // knob 11: flag-only edge consumer CTA size (warps in parallel)
 static int g_consume_release = 0;    // knob 13: flag-only consumer clears with release.sys
 static int g_pull_no_prefetch = 0;   // knob 16: few-slot pull edges without early staging
 // knob 12: GenGrad work-unit size.  A unit's thread 0 derives the PCG64 stream

@@ -566,7 +566,7 @@ int srf_dyn_edge_send(srf_space_t snd_space, srf_space_t rcv_space, uint64_t met
   a.err = snd_space->err;
   srf_stream *s = stream_or_default(snd_space, st);
   CUDA_TRY(cudaSetDevice(s->device));
-  k_dyn_send_stream<<<1, 32, 0, s->s>>>(a);
+  k_dyn_send_stream<<<1, 1024, 0, s->s>>>(a);
   return launch_check("k_dyn_send_stream");
 }
 

@@ -553,18 +553,21 @@ struct DynSendArgs {
   int *err;
 };
 
-// one warp: lane t owns the slots s with s % L == t (L = min(32, slots)) and
+// up to 32 warps: warp t owns the slots s with s % L == t (L = min(32, slots)) and
 // writes their rounds in order, so up to L rounds' credit polls and metadata
 // writes are in flight at once (one thread spent ~4 us per round on the
 // remote flag read and the system-scope release, which capped 1 MiB rounds at
 // ~260 GB/s); a slot's rounds stay on one lane, so a credit read 0 can only
 // be the slot's previous round's
 __global__ void k_dyn_send_stream(const __grid_constant__ DynSendArgs a) {
-  const uint32_t L = a.slots < blockDim.x ? a.slots : blockDim.x;
-  if (threadIdx.x >= L) return;
+  // one active lane per warp: lanes of one warp spinning on different flags
+  // would serialise their divergent polls
+  const uint32_t warps = blockDim.x / 32, me = threadIdx.x / 32;
+  const uint32_t L = a.slots < warps ? a.slots : warps;
+  if (threadIdx.x % 32 != 0 || me >= L) return;
   for (uint32_t r = 0; r < a.rounds; ++r) {
     const uint64_t j = a.first_round + r;
-    if ((uint32_t)(j % a.slots) % L != threadIdx.x) continue;
+    if ((uint32_t)(j % a.slots) % L != me) continue;
     uint8_t *m = a.meta + (j % a.slots) * a.meta_stride;
     uint8_t *flag = m + 8ull * a.rank + 32;
     const uint64_t t0 = globaltimer_ns();

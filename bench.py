@@ -1088,6 +1088,13 @@ class OneWayEdge:
                           self.payloads.base_addr + i * self.src_stride, S // 4, 0, 0, 0, 2 + i,
                           None, None)
             mine = {"addr": self.payloads.base_addr, "token": self.payloads.access_token}
+            if mode == "push":
+                # one direction: the consumer mirrors each credit into the
+                # sender's pool (a posted write) instead of the sender reading
+                # the remote flag (1 MiB 635 -> 696 GB/s, profiles/r2_credit_mirror_probe.jsonl)
+                self.credit = self.sp.allocate_region(4 * self.slots)
+                self.sp.write_raw(self.credit.base_addr, b"\x00" * 4 * self.slots)
+                mine["credit"] = self.credit.base_addr
         elif self.role == "rcv" and mode == "dyn":
             self.ring = self.sp.allocate_region(self.ring_cap, register=True)
             self.meta = self.sp.allocate_region(self.slots * self.meta_stride, register=True)
@@ -1111,7 +1118,8 @@ class OneWayEdge:
         if mode == "push" and self.role == "snd":
             self.edge = PipelinedStaticEdge(self.sp, self.payloads, S, nsrc, self.src_stride,
                                             self.proxies[1], self.peer["addr"],
-                                            self.peer["token"], self.slots, self.slot_stride)
+                                            self.peer["token"], self.slots, self.slot_stride,
+                                            credit_addr=self.credit.base_addr)
         elif mode == "pull" and self.role == "rcv":
             self.edge = PulledStaticEdge(self.proxies[0], self.peer["addr"], self.peer["token"],
                                          S, nsrc, self.src_stride, self.sp, self.slots_reg,
@@ -1143,9 +1151,10 @@ class OneWayEdge:
         if self.role == "rcv" and self.mode == "dyn":
             self.edge.consume(self.next, rounds, stream=self.st[1])
         elif self.role == "rcv":
+            credit = ((self.proxies[0], self.peer["credit"]) if self.mode == "push" else None)
             PipelinedStaticEdge.consume(self.sp, self.slots_reg.base_addr, self.slots,
                                         self.slot_stride, self.S, self.next, rounds,
-                                        stream=self.st[1])
+                                        credit=credit, stream=self.st[1])
         elif self.role == "snd" and self.mode == "dyn":
             from paper_1805_08430_b200.wire import ElemType
             PipelinedDynamicEdge.send(self.sp, self.proxies[1], self.peer["meta"],
